@@ -1,0 +1,95 @@
+"""The CPU oracle against the reference-generated golden vectors (no GPU)."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from golden_cases import CASE_NAMES, DEALER, G, META, SEED, case
+from oracle import nnmirror as N
+from oracle import rss as R
+
+OPS = {
+    "mul": R.mul, "mul_bcast": R.mul, "matmul": R.matmul_shares, "matmul_bits": R.matmul_shares,
+    "conv": R.conv2d_shares, "conv11s4": R.conv2d_shares, "trunc20": R.truncate, "trunc1": R.truncate,
+    "trunc61": R.truncate, "a2b": R.a2b, "msb": R.msb, "relu": R.relu, "relu_mask": R.relu_with_mask,
+    "drelu": R.drelu, "max_tree": R.max_tree, "exp": R.exp_approx, "reciprocal": R.reciprocal,
+    "softmax": R.softmax, "avgpool2": R.avgpool_shares, "avgpool3": R.avgpool_shares,
+}
+
+
+def test_prf_known_answer():
+    key = G["prf_kat_key"].tobytes()
+    assert np.array_equal(R.prf_words(key, 1, 0, 4), G["prf_kat_words"])
+    # SURVEY.md 8(c) KAT
+    assert [hex(int(v)) for v in G["prf_kat_words"]] == [
+        "0xa0877cdd63d37ce3", "0x829ce0603e0eff9a", "0x19ff076bfae7e67f", "0x62f3c9d7c774a10d"]
+
+
+def test_party_keys_and_streams():
+    ks = R.party_keys(SEED)
+    assert np.array_equal(np.stack([np.frombuffer(k, np.uint8) for k in ks]), G["party_keys_seed3"])
+    assert np.array_equal(np.stack([np.frombuffer(k, np.uint8) for k in R.party_keys(0)]), G["party_keys_seed0"])
+    for purpose, index, count in META["prf_rows"]:
+        assert np.array_equal(R.prf_words(ks[1], purpose, index, count), G[f"prf_k1_{purpose}_{index}_{count}"])
+
+
+def test_prf_prefix_and_range():
+    k = R.party_keys(0)[0]
+    assert np.array_equal(R.prf_words(k, 2, 7, 5), R.prf_words(k, 2, 7, 11)[:5])
+    with pytest.raises(ValueError):
+        R.prf_words(k, 1 << 16, 0, 1)
+    with pytest.raises(ValueError):
+        R.prf_words(k, 1, 1 << 48, 1)
+
+
+def test_bilinear_engine():
+    assert np.array_equal(R.ring_matmul(G["mm_a"], G["mm_b"]), G["mm_out"])
+    assert np.array_equal(R.wrap_matmul(G["mm_a"], G["mm_b"]), G["mm_out"])
+    assert np.array_equal(R.ring_conv2d(G["cv_x"], G["cv_k"], (2, 2), (1, 1)), G["cv_out"])
+    assert np.array_equal(R.wrap_conv2d(G["cv_x"], G["cv_k"], (2, 2), (1, 1)), G["cv_out"])
+    assert np.array_equal(R.ring_sumpool(G["cv_x"], (3, 3), (2, 2)), G["sp_out"])
+
+
+@pytest.mark.parametrize("name", CASE_NAMES)
+def test_protocol_shares_bit_exact(name):
+    ins, outs, kw, _ = case(name)
+    s = R.Session(SEED)
+    rin = np.random.default_rng(DEALER)
+    sh = [R.share(x, rin) for x in ins]
+    got = OPS[name](s, *sh, **kw)
+    got = list(got) if isinstance(got, tuple) else [got]
+    assert len(got) == len(outs)
+    for a, b in zip(got, outs):
+        assert np.array_equal(a, b)
+
+
+def test_lenet_inference_shares():
+    layers, ishape = N.lenet()
+    w = N.init_params(layers, ishape, 20, 31)
+    s = R.Session(SEED)
+    rin = np.random.default_rng(DEALER)
+    P = [R.share(x, rin) for x in w]
+    xs = R.share(R.fx_encode(G["lenet_infer_x"]), rin)
+    assert np.array_equal(N.infer_private(s, layers, P, xs), G["lenet_infer_logits"])
+
+
+def test_lenet_train_step_weights():
+    layers, ishape = N.lenet()
+    s = R.Session(0)
+    P, _ = N.train_private(s, layers, ishape, G["train_lenet_images"], G["train_lenet_labels"], 0.01, 3, 1, seed=5)
+    for i, p in enumerate(P):
+        assert np.array_equal(R.open_trio(p), G[f"train_lenet_w{i}"])
+    fixed = N.train_plain_fixed(layers, ishape, G["train_lenet_images"], G["train_lenet_labels"], 0.01, 3, 1,
+                                seed=5, offsets=R.TruncationRandomness(0))
+    for i, p in enumerate(fixed):
+        assert np.array_equal(p, G[f"train_lenet_w{i}"])
+
+
+@pytest.mark.slow
+def test_alexnet_train_step_digest():
+    layers, ishape = N.alexnet_cifar()
+    fixed = N.train_plain_fixed(layers, ishape, G["train_alexnet_images"], G["train_alexnet_labels"], 0.01, 4, 1,
+                                seed=5, offsets=R.TruncationRandomness(0))
+    d = hashlib.sha256(b"".join(np.ascontiguousarray(x, "<u8").tobytes() for x in fixed)).hexdigest()
+    assert d == META["train_alexnet_digest"]
