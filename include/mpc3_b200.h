@@ -1,0 +1,224 @@
+/*
+ * mpc3_b200.h — C ABI of the B200-native 3-party replicated-secret-sharing
+ * engine over Z_2^64 (CryptGPU, arXiv 2104.10949).
+ *
+ * The reference (`mpc3`, pure Python) has no FFI; its drop-in boundary is the
+ * Python protocol API and the duck-typed nn engine seam.
+ * Every entry point below is the native body of one reference function; the
+ * comment on each cites the reference file:line it replaces
+ * (paths relative to /root/reference/pkg/src/mpc3/).
+ *
+ * Conventions
+ *  - All tensor pointers are DEVICE pointers (cudaMalloc / torch storage) to
+ *    little-endian uint64 ring words, except where stated.  The library never
+ *    retains caller buffers and never allocates on the hot path; the caller
+ *    owns outputs and workspaces.
+ *  - A "trio" tensor of n elements is the three additive (or XOR) share
+ *    components stored as 3 planes: component c at ptr[c * n + e].  Party i's
+ *    replicated share (lo, hi) is (plane i, plane (i+1)%3) (sharing.py:37-49).
+ *  - rk3 points to 3 x 44 uint32 AES-128 round-key words (keys k_0, k_1, k_2
+ *    of the session, as produced by mpc3_aes128_expand).
+ *  - Counters j_* are the per-purpose lockstep stream counters that
+ *    PartyContext.take (sharing.py:225-230) would hand out; the host keeps
+ *    them and checks freshness before launch (sharing.py:190-204).
+ *  - `stream` is a cudaStream_t passed as void*.  Calls are asynchronous on
+ *    it and reentrant.  Return value: MPC3_OK or an error status; statuses
+ *    map 1:1 onto the reference's exception taxonomy (errors.py:4-53).
+ */
+#ifndef MPC3_B200_H
+#define MPC3_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (errors.py:4-53) ---- */
+#define MPC3_OK 0
+#define MPC3_ERR_RANGE 1      /* RangeError      */
+#define MPC3_ERR_SHAPE 2      /* ShapeError      */
+#define MPC3_ERR_EXACTNESS 3  /* ExactnessError  */
+#define MPC3_ERR_CONFIG 4     /* ConfigError     */
+#define MPC3_ERR_FRESHNESS 5  /* FreshnessError  */
+#define MPC3_ERR_TOPOLOGY 6   /* TopologyError   */
+#define MPC3_ERR_INTEGRITY 7  /* IntegrityError  */
+#define MPC3_ERR_CUDA 100     /* CUDA runtime / launch failure */
+#define MPC3_ERR_UNSUPPORTED 101 /* device is not sm_100 */
+
+#define MPC3_ABI_VERSION 1
+
+int mpc3_abi_version(void);
+const char* mpc3_status_name(int status);
+/* Last CUDA error string seen by the library on this thread (diagnostics). */
+const char* mpc3_last_error(void);
+
+/* ---- PRF (prf.py:31-61) ---- */
+
+/* Host function: AES-128 key expansion of one 16-byte key (prf.py:36-38,
+ * the key schedule behind cryptography's AES). */
+int mpc3_aes128_expand(const uint8_t key[16], uint32_t round_keys[44]);
+
+/* words[i] = word (word_off + i) of stream (key, purpose, index); the stream
+ * is PrfKey.words(purpose, index, .) of prf.py:40-49, seekable by word.
+ * rk = one key's 44 round-key words (device). */
+int mpc3_prf_words(const uint32_t* rk, uint32_t purpose, uint64_t index, uint64_t word_off,
+                   uint64_t count, uint64_t* words, void* stream);
+
+/* Arithmetic (xor_mode=0) or XOR (xor_mode=1) zero sharing of n words,
+ * trio output z_i = F(k_i) -/^ F(k_{i-1}) (sharing.py:233-250). */
+int mpc3_rss_zero_share(const uint32_t* rk3, uint32_t purpose, uint64_t index, int xor_mode,
+                        uint64_t n, uint64_t* out_trio, void* stream);
+
+/* ---- local ring ops (ring.py:50-79, protocols.py:57-72, sharing.py:54-67) ---- */
+#define MPC3_EW_ADD 0      /* out = a + b          */
+#define MPC3_EW_SUB 1      /* out = a - b          */
+#define MPC3_EW_NEG 2      /* out = -a             */
+#define MPC3_EW_MULC 3     /* out = a * c          */
+#define MPC3_EW_ADDC 4     /* out = a + c          */
+#define MPC3_EW_XOR 5      /* out = a ^ b          */
+#define MPC3_EW_SHL 6      /* out = a << c         */
+#define MPC3_EW_SHR 7      /* out = a >> c (logical) */
+#define MPC3_EW_SAR 8      /* out = sar(a, c)      */
+#define MPC3_EW_AXPY 9     /* out = a + c * b      */
+/* Elementwise over n words; b may be NULL for unary ops. */
+int mpc3_ring_ew(int op, const uint64_t* a, const uint64_t* b, uint64_t c, uint64_t* out, uint64_t n,
+                 void* stream);
+
+/* Broadcast-add along a trailing axis: out[r, j] = a[r, j] op b[r] (max_tree /
+ * softmax centring, protocols.py:463-466).  op: ADD or SUB.  rows x cols. */
+int mpc3_ring_rowop(int op, const uint64_t* a, const uint64_t* b, uint64_t* out, uint64_t rows,
+                    uint64_t cols, void* stream);
+
+/* Row sums of the last axis: out[r] = sum_j a[r, j] (protocols.py:466). */
+int mpc3_ring_rowsum(const uint64_t* a, uint64_t* out, uint64_t rows, uint64_t cols, void* stream);
+
+/* ---- elementwise protocols on trio tensors ---- */
+
+/* mul (protocols.py:79-94): out = reshare(x*y), 1 ARITH_ZERO counter. */
+int mpc3_rss_mul(const uint32_t* rk3, uint64_t j_arith, const uint64_t* x, const uint64_t* y,
+                 uint64_t* out, uint64_t n, void* stream);
+
+/* truncate (protocols.py:171-216): bits in [1,61]; TRUNC_RHO and TRUNC_R counters. */
+int mpc3_rss_truncate(const uint32_t* rk3, uint64_t j_rho, uint64_t j_r, int bits, const uint64_t* x,
+                      uint64_t* out, uint64_t n, void* stream);
+
+/* mul + truncate fused (protocols.py:79-94 then 171-216; the `truncate(mul())`
+ * pairs of exp_approx / reciprocal / division / softmax, 414-468). */
+int mpc3_rss_mul_truncate(const uint32_t* rk3, uint64_t j_arith, uint64_t j_rho, uint64_t j_r, int bits,
+                          const uint64_t* x, const uint64_t* y, uint64_t* out, uint64_t n, void* stream);
+
+/* Sign circuit (protocols.py:266-348): a2b + 64-bit Kogge-Stone + msb +
+ * bit_inject + relu, fused, all 11 rounds in registers.
+ * mode 0 = a2b (out: XOR trio of x), 1 = msb (XOR trio of the sign bit),
+ * 2 = drelu (arithmetic {0,1} trio), 3 = relu (out = relu, mask = drelu).
+ * Counters: BIN_INPUT j_bin; XOR_ZERO j_xor..j_xor+6; ARITH_ZERO j_arith..+2
+ * (modes 2/3 use 2/3 of them).  n_total/elem_off allow a shard of a larger
+ * tensor (the Kogge-Stone p-half lives at word n_total + e). */
+int mpc3_rss_sign(const uint32_t* rk3, int mode, uint64_t j_bin, uint64_t j_xor, uint64_t j_arith,
+                  const uint64_t* x, uint64_t* out, uint64_t* mask, uint64_t n, uint64_t n_total,
+                  uint64_t elem_off, void* stream);
+
+/* bit_inject of XOR-shared bits (protocols.py:304-331), 2 ARITH counters. */
+int mpc3_rss_bit_inject(const uint32_t* rk3, uint64_t j_arith, const uint64_t* bits, uint64_t* out,
+                        uint64_t n, void* stream);
+
+/* Output view of a bilinear result: the logical ("full") output is a 4-d
+ * C-order tensor of sizes full[4]; PRF word index = its flat index.  Only the
+ * sub-box crop[4] (crop[k] <= full[k], origin 0) is produced.  Element
+ * (i0..i3) reads z at z + sum i_k*z_stride[k] (plane stride z_plane) and
+ * writes out + sum i_k*out_stride[k] (plane stride out_plane). */
+typedef struct {
+  int64_t full[4];
+  int64_t crop[4];
+  int64_t z_stride[4];
+  int64_t out_stride[4];
+  int64_t z_plane;
+  int64_t out_plane;
+} mpc3_view4;
+
+/* Reshare of per-party local products z (z_i in plane i) followed by
+ * truncation (protocols.py:110-117 / 129-136: _reshare then truncate).
+ * bits = 0 skips truncation (bare reshare). */
+int mpc3_rss_reshare_truncate(const uint32_t* rk3, uint64_t j_arith, uint64_t j_rho, uint64_t j_r,
+                              int bits, const uint64_t* z, const mpc3_view4* view, uint64_t* out,
+                              void* stream);
+
+/* avgpool (protocols.py:139-159): window sums, then truncate(log2 area) when
+ * the area is a power of two, else mul_const(mulc) + truncate(t).  x/out are
+ * trio NCHW; bits/mulc chosen by the caller (mulc = 1 for power-of-two). */
+int mpc3_rss_avgpool(const uint32_t* rk3, uint64_t j_rho, uint64_t j_r, int bits, uint64_t mulc,
+                     const uint64_t* x, uint64_t* out, int64_t N, int64_t C, int64_t H, int64_t W,
+                     int kh, int kw, int sh, int sw, void* stream);
+
+/* avgpool backward (nn.py:487-499): scatter-add of g into the windows, then
+ * div_area (truncate / mul_const+truncate) — fused. g: (N,C,OH,OW) trio;
+ * out: (N,C,H,W) trio. */
+int mpc3_rss_avgpool_backward(const uint32_t* rk3, uint64_t j_rho, uint64_t j_r, int bits, uint64_t mulc,
+                              const uint64_t* g, uint64_t* out, int64_t N, int64_t C, int64_t H,
+                              int64_t W, int64_t OH, int64_t OW, int kh, int kw, int sh, int sw,
+                              void* stream);
+
+/* Plain sum-pool of one ring tensor (ring.py:259-268). */
+int mpc3_ring_sumpool(const uint64_t* x, uint64_t* out, int64_t N, int64_t C, int64_t H, int64_t W,
+                      int kh, int kw, int sh, int sw, void* stream);
+
+/* ---- ring GEMM (ring.py:144-256 bilinear_exact; protocols.py:97-136) ----
+ *
+ * Operands are packed into u8 limb planes: packed[g][limb][row][kp] with
+ * limb l = byte l of the 64-bit word, kp = roundup(K, 16) (zero padded).
+ * The tcgen05 kernel computes, per group g, C[g] = A[g] . B[g]^T over Z_2^64
+ * with A (M rows) and B (N rows) both K-contiguous: 36 u8 x u8 limb-pair MMAs
+ * accumulate 8 diagonal int32 sums S_d in TMEM; the epilogue recombines
+ * sum_d S_d << 8d mod 2^64.  Exact for K <= 16512 per split (S_3 < 2^32);
+ * longer K is split and the splits are added with 64-bit atomics. */
+
+/* Operand gather descriptor for packing. */
+#define MPC3_GATHER_DENSE 0   /* v(r,k) = src[off + r*s_r + k0*t0 + k1*t1 + k2*t2], k=(k0,k1,k2) */
+#define MPC3_GATHER_IM2COL 1  /* r=(n,y,x), k=(c,u,v): in[n,c,(y*sh+u-ph)/dh,(x*sw+v-pw)/dw] */
+#define MPC3_GATHER_WGRAD 2   /* r=(c,u,v), k=(n,y,x): in[n,c,y*sh+u-ph,x*sw+v-pw]           */
+typedef struct {
+  int mode;
+  int64_t rows, k;         /* logical operand rows and inner length K */
+  /* DENSE */
+  int64_t off, s_r, t0, t1, t2, K1, K2;
+  /* IM2COL / WGRAD geometry: input (N,C,H,W) with element strides */
+  int64_t n, c, h, w, sN, sC, sH, sW;
+  int64_t kh, kw, sh, sw, ph, pw, dh, dw, oh, ow;
+} mpc3_operand;
+
+/* Cross-term packing for the secure bilinear op (protocols.py:110-115):
+ * for each party i, K' = 2K and
+ *   role 0 (left operand):  row r of party i = [x_i + x_{i+1} | x_i]
+ *   role 1 (right operand): row r of party i = [y_i | y_{i+1}]
+ * so that z_i = x_i y_i + x_{i+1} y_i + x_i y_{i+1} is ONE ring GEMM with
+ * inner length 2K.  role 2 packs a single plain operand (group count 1).
+ * src: trio planes (plane stride src_plane) or one plane for role 2.
+ * out: [3 or 1][8][rows][kp], kp = roundup(K', 16). */
+int mpc3_ring_pack(const uint64_t* src, int64_t src_plane, const mpc3_operand* op, int role,
+                   uint8_t* out, int64_t kp, void* stream);
+
+/* C[g] (+)= A[g] . B[g]^T over Z_2^64 (tcgen05 kind::i8, TMA-fed).
+ * A: [groups][8][M][kp] u8, B: [groups][8][N][kp] u8, C: rows M, cols N,
+ * leading dim ldc, group stride c_group.  splits > 1 requires C zeroed (the
+ * splits add with u64 atomics).  kp % 16 == 0. */
+int mpc3_ring_gemm_packed(const uint8_t* A, const uint8_t* B, uint64_t* C, int groups, int64_t M,
+                          int64_t N, int64_t kp, int64_t ldc, int64_t c_group, int splits, void* stream);
+
+/* Reference GPU path (CUDA cores, 64-bit IMAD): C = A . B mod 2^64 with
+ * arbitrary strides; used as an on-device cross-check and for tiny shapes. */
+int mpc3_ring_gemm_simt(const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t M, int64_t N, int64_t K,
+                        int64_t sam, int64_t sak, int64_t sbk, int64_t sbn, int64_t ldc, void* stream);
+
+/* Convenience: plain ring matmul C (M,N) = A (M,K) . B (K,N), row-major,
+ * exactly `bilinear_exact(a, b, matmul_spec(m,k,n))` (ring.py:183-222) minus
+ * its 2^20 limit.  workspace >= mpc3_ring_matmul_workspace(M,N,K) bytes. */
+size_t mpc3_ring_matmul_workspace(int64_t M, int64_t N, int64_t K);
+int mpc3_ring_matmul_u64(const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t M, int64_t N,
+                         int64_t K, void* workspace, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPC3_B200_H */

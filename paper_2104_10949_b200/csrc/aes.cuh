@@ -1,0 +1,189 @@
+// AES-128 counter-mode keystream, bit-exact with the reference PRF
+// (prf.py:31-55: cryptography's AES-128-CTR whose initial counter block is
+// purpose_LE16 || index_LE48 || 0^64 and whose per-block increment runs over
+// the big-endian 128-bit block).  Block b of stream (key, purpose, index) is
+// AES_k(purpose_LE16 || index_LE48 || BE64(b)); it yields words 2b and 2b+1
+// as the two little-endian halves of the ciphertext.
+//
+// T-table implementation: the four 1 KiB round tables and the S-box live in
+// shared memory on the device (built once per CTA) and in static host arrays
+// for the CPU self-check build (hostcheck.cpp), with one code path for both.
+#pragma once
+#include "common.cuh"
+
+namespace mpc3 {
+
+#if defined(__CUDACC__)
+__constant__ uint8_t c_sbox[256] = {
+#else
+static const uint8_t c_sbox[256] = {
+#endif
+    0x63, 0x7c, 0x77, 0x7b, 0xf2, 0x6b, 0x6f, 0xc5, 0x30, 0x01, 0x67, 0x2b, 0xfe, 0xd7, 0xab, 0x76,
+    0xca, 0x82, 0xc9, 0x7d, 0xfa, 0x59, 0x47, 0xf0, 0xad, 0xd4, 0xa2, 0xaf, 0x9c, 0xa4, 0x72, 0xc0,
+    0xb7, 0xfd, 0x93, 0x26, 0x36, 0x3f, 0xf7, 0xcc, 0x34, 0xa5, 0xe5, 0xf1, 0x71, 0xd8, 0x31, 0x15,
+    0x04, 0xc7, 0x23, 0xc3, 0x18, 0x96, 0x05, 0x9a, 0x07, 0x12, 0x80, 0xe2, 0xeb, 0x27, 0xb2, 0x75,
+    0x09, 0x83, 0x2c, 0x1a, 0x1b, 0x6e, 0x5a, 0xa0, 0x52, 0x3b, 0xd6, 0xb3, 0x29, 0xe3, 0x2f, 0x84,
+    0x53, 0xd1, 0x00, 0xed, 0x20, 0xfc, 0xb1, 0x5b, 0x6a, 0xcb, 0xbe, 0x39, 0x4a, 0x4c, 0x58, 0xcf,
+    0xd0, 0xef, 0xaa, 0xfb, 0x43, 0x4d, 0x33, 0x85, 0x45, 0xf9, 0x02, 0x7f, 0x50, 0x3c, 0x9f, 0xa8,
+    0x51, 0xa3, 0x40, 0x8f, 0x92, 0x9d, 0x38, 0xf5, 0xbc, 0xb6, 0xda, 0x21, 0x10, 0xff, 0xf3, 0xd2,
+    0xcd, 0x0c, 0x13, 0xec, 0x5f, 0x97, 0x44, 0x17, 0xc4, 0xa7, 0x7e, 0x3d, 0x64, 0x5d, 0x19, 0x73,
+    0x60, 0x81, 0x4f, 0xdc, 0x22, 0x2a, 0x90, 0x88, 0x46, 0xee, 0xb8, 0x14, 0xde, 0x5e, 0x0b, 0xdb,
+    0xe0, 0x32, 0x3a, 0x0a, 0x49, 0x06, 0x24, 0x5c, 0xc2, 0xd3, 0xac, 0x62, 0x91, 0x95, 0xe4, 0x79,
+    0xe7, 0xc8, 0x37, 0x6d, 0x8d, 0xd5, 0x4e, 0xa9, 0x6c, 0x56, 0xf4, 0xea, 0x65, 0x7a, 0xae, 0x08,
+    0xba, 0x78, 0x25, 0x2e, 0x1c, 0xa6, 0xb4, 0xc6, 0xe8, 0xdd, 0x74, 0x1f, 0x4b, 0xbd, 0x8b, 0x8a,
+    0x70, 0x3e, 0xb5, 0x66, 0x48, 0x03, 0xf6, 0x0e, 0x61, 0x35, 0x57, 0xb9, 0x86, 0xc1, 0x1d, 0x9e,
+    0xe1, 0xf8, 0x98, 0x11, 0x69, 0xd9, 0x8e, 0x94, 0x9b, 0x1e, 0x87, 0xe9, 0xce, 0x55, 0x28, 0xdf,
+    0x8c, 0xa1, 0x89, 0x0d, 0xbf, 0xe6, 0x42, 0x68, 0x41, 0x99, 0x2d, 0x0f, 0xb0, 0x54, 0xbb, 0x16,
+};
+
+HD uint32_t ror32(uint32_t v, int r) { return (v >> r) | (v << (32 - r)); }
+HD uint32_t bswap32(uint32_t v) {
+  return (v >> 24) | ((v >> 8) & 0xff00u) | ((v << 8) & 0xff0000u) | (v << 24);
+}
+HD uint32_t xtime(uint32_t b) { return ((b << 1) ^ ((b & 0x80) ? 0x1b : 0)) & 0xff; }
+
+// Te0[x] = (2*S[x], S[x], S[x], 3*S[x]) big-endian; Te1..3 are rotations.
+HD uint32_t te0_entry(uint32_t x) {
+  uint32_t s = c_sbox[x];
+  uint32_t s2 = xtime(s);
+  return (s2 << 24) | (s << 16) | (s << 8) | (s2 ^ s);
+}
+
+// Expanded AES-128 key: 44 big-endian round-key words (FIPS-197 5.2).
+HD void aes128_expand(const uint8_t key[16], uint32_t rk[44]) {
+  const uint8_t rcon[10] = {0x01, 0x02, 0x04, 0x08, 0x10, 0x20, 0x40, 0x80, 0x1b, 0x36};
+  for (int i = 0; i < 4; ++i)
+    rk[i] = ((uint32_t)key[4 * i] << 24) | ((uint32_t)key[4 * i + 1] << 16) |
+            ((uint32_t)key[4 * i + 2] << 8) | key[4 * i + 3];
+  for (int i = 4; i < 44; ++i) {
+    uint32_t t = rk[i - 1];
+    if (i % 4 == 0) {
+      t = ((uint32_t)c_sbox[(t >> 16) & 0xff] << 24) | ((uint32_t)c_sbox[(t >> 8) & 0xff] << 16) |
+          ((uint32_t)c_sbox[t & 0xff] << 8) | c_sbox[t >> 24];
+      t ^= (uint32_t)rcon[i / 4 - 1] << 24;
+    }
+    rk[i] = rk[i - 4] ^ t;
+  }
+}
+
+// Columns 0-1 of every counter block of stream (purpose, index).
+struct StreamHead {
+  uint32_t s0, s1;
+};
+HD StreamHead stream_head(uint32_t purpose, uint64_t index) {
+  uint8_t b[8];
+  b[0] = purpose & 0xff;
+  b[1] = (purpose >> 8) & 0xff;
+  for (int i = 0; i < 6; ++i) b[2 + i] = (index >> (8 * i)) & 0xff;
+  StreamHead h;
+  h.s0 = ((uint32_t)b[0] << 24) | ((uint32_t)b[1] << 16) | ((uint32_t)b[2] << 8) | b[3];
+  h.s1 = ((uint32_t)b[4] << 24) | ((uint32_t)b[5] << 16) | ((uint32_t)b[6] << 8) | b[7];
+  return h;
+}
+
+// Table access policy: T is any object exposing t0(i) and sb(i).
+template <class T>
+HD void aes128_block(const T& tab, const uint32_t* rk, uint32_t& s0, uint32_t& s1, uint32_t& s2,
+                     uint32_t& s3) {
+  s0 ^= rk[0];
+  s1 ^= rk[1];
+  s2 ^= rk[2];
+  s3 ^= rk[3];
+#if defined(__CUDA_ARCH__)
+#pragma unroll 1
+#endif
+  for (int r = 1; r < 10; ++r) {
+    const uint32_t* k = rk + 4 * r;
+    uint32_t t0 = tab.t0(s0 >> 24) ^ ror32(tab.t0((s1 >> 16) & 0xff), 8) ^
+                  ror32(tab.t0((s2 >> 8) & 0xff), 16) ^ ror32(tab.t0(s3 & 0xff), 24) ^ k[0];
+    uint32_t t1 = tab.t0(s1 >> 24) ^ ror32(tab.t0((s2 >> 16) & 0xff), 8) ^
+                  ror32(tab.t0((s3 >> 8) & 0xff), 16) ^ ror32(tab.t0(s0 & 0xff), 24) ^ k[1];
+    uint32_t t2 = tab.t0(s2 >> 24) ^ ror32(tab.t0((s3 >> 16) & 0xff), 8) ^
+                  ror32(tab.t0((s0 >> 8) & 0xff), 16) ^ ror32(tab.t0(s1 & 0xff), 24) ^ k[2];
+    uint32_t t3 = tab.t0(s3 >> 24) ^ ror32(tab.t0((s0 >> 16) & 0xff), 8) ^
+                  ror32(tab.t0((s1 >> 8) & 0xff), 16) ^ ror32(tab.t0(s2 & 0xff), 24) ^ k[3];
+    s0 = t0;
+    s1 = t1;
+    s2 = t2;
+    s3 = t3;
+  }
+  const uint32_t* k = rk + 40;
+  uint32_t t0 = (tab.sb(s0 >> 24) << 24) | (tab.sb((s1 >> 16) & 0xff) << 16) |
+                (tab.sb((s2 >> 8) & 0xff) << 8) | tab.sb(s3 & 0xff);
+  uint32_t t1 = (tab.sb(s1 >> 24) << 24) | (tab.sb((s2 >> 16) & 0xff) << 16) |
+                (tab.sb((s3 >> 8) & 0xff) << 8) | tab.sb(s0 & 0xff);
+  uint32_t t2 = (tab.sb(s2 >> 24) << 24) | (tab.sb((s3 >> 16) & 0xff) << 16) |
+                (tab.sb((s0 >> 8) & 0xff) << 8) | tab.sb(s1 & 0xff);
+  uint32_t t3 = (tab.sb(s3 >> 24) << 24) | (tab.sb((s0 >> 16) & 0xff) << 16) |
+                (tab.sb((s1 >> 8) & 0xff) << 8) | tab.sb(s2 & 0xff);
+  s0 = t0 ^ k[0];
+  s1 = t1 ^ k[1];
+  s2 = t2 ^ k[2];
+  s3 = t3 ^ k[3];
+}
+
+// Words 2b and 2b+1 of stream (head, key).
+struct Word2 {
+  uint64_t w0, w1;
+};
+template <class T>
+HD Word2 prf_block(const T& tab, const uint32_t* rk, StreamHead h, uint64_t b) {
+  uint32_t s0 = h.s0, s1 = h.s1, s2 = (uint32_t)(b >> 32), s3 = (uint32_t)b;
+  aes128_block(tab, rk, s0, s1, s2, s3);
+  Word2 w;
+  w.w0 = (uint64_t)bswap32(s0) | ((uint64_t)bswap32(s1) << 32);
+  w.w1 = (uint64_t)bswap32(s2) | ((uint64_t)bswap32(s3) << 32);
+  return w;
+}
+
+// Single word w of the stream.
+template <class T>
+HD uint64_t prf_word(const T& tab, const uint32_t* rk, StreamHead h, uint64_t w) {
+  Word2 p = prf_block(tab, rk, h, w >> 1);
+  return (w & 1) ? p.w1 : p.w0;
+}
+
+#if !defined(__CUDA_ARCH__)
+// Host tables for the CPU self-check build.
+struct HostTables {
+  uint32_t te[256];
+  HostTables() {
+    for (int i = 0; i < 256; ++i) te[i] = te0_entry(i);
+  }
+  inline uint32_t t0(uint32_t i) const { return te[i]; }
+  inline uint32_t sb(uint32_t i) const { return c_sbox[i]; }
+};
+#endif
+
+#if defined(__CUDACC__)
+// Shared-memory tables, built once per CTA.
+struct SmemTables {
+  uint32_t* te;
+  const uint8_t* sbox;
+  DEV uint32_t t0(uint32_t i) const { return te[i]; }
+  DEV uint32_t sb(uint32_t i) const { return sbox[i]; }
+};
+
+// Shared layout for protocol kernels: T-table, S-box and three key schedules.
+struct AesSmem {
+  uint32_t te[256];
+  uint8_t sbox[256];
+  uint32_t rk[3][44];
+};
+
+// rk_dev: 3 x 44 round-key words (k_0, k_1, k_2 of the session).
+__device__ inline SmemTables aes_smem_init(AesSmem& sm, const uint32_t* __restrict__ rk_dev, int nkeys) {
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    sm.te[i] = te0_entry(i);
+    sm.sbox[i] = c_sbox[i];
+  }
+  for (int i = threadIdx.x; i < nkeys * 44; i += blockDim.x) (&sm.rk[0][0])[i] = rk_dev[i];
+  __syncthreads();
+  SmemTables t;
+  t.te = sm.te;
+  t.sbox = sm.sbox;
+  return t;
+}
+#endif
+
+}  // namespace mpc3

@@ -1,0 +1,437 @@
+// Z_2^64 ring GEMM on the 5th-generation tensor cores (tcgen05 kind::i8).
+//
+// Replaces the reference's float-limb engine (ring.py:123-222: 4 x 16-bit
+// limbs as float64, 10 dgemms, recombined with wrapping shifts).  Here each
+// 64-bit operand is split into 8 unsigned byte limbs; the 36 limb pairs (i, j)
+// with i + j < 8 are accumulated exactly in int32 into 8 "diagonal"
+// accumulators S_d = sum_{i+j=d} A_i B_j^T held in TMEM (8 x 64 columns =
+// the whole 512-column TMEM of the SM), and the epilogue forms
+// sum_d S_d << 8d mod 2^64.  S_d for d >= 4 only matters mod 2^32 (the int32
+// accumulator wraps); S_d for d <= 3 is exact while K <= 16512.
+//
+// Tile: 128 rows (M) x 64 columns (N) per CTA, K step 32 bytes.  The B tile
+// of all 8 limbs is laid out as one 512-row K-major operand, so the products
+// A_i x [B_0 .. B_{7-i}] are ONE MMA with N = 64 (8 - i) (split at 256)
+// written at TMEM column 64 i: column block j lands on diagonal i + j.  That
+// is 12 MMAs per K step instead of 36, and B is read from shared memory once
+// per (i, block) instead of once per pair.
+//
+// Warp roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer,
+// warp 2 = TMEM allocator, warps 4-7 = epilogue (TMEM lanes 0-127).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <string.h>
+
+#include <mutex>
+
+#include "launch.cuh"
+#include "items.cuh"
+
+namespace mpc3 {
+
+// ---------------------------------------------------------------------------
+// operand packing: u64 gather -> 8 byte-limb planes [g][limb][row][kp]
+
+__global__ void pack_kernel(const uint64_t* __restrict__ src, int64_t plane, Operand o, int role, int groups,
+                            uint8_t* __restrict__ out, int64_t kp) {
+  int64_t total = (int64_t)groups * o.rows * (kp / 8);
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x)
+    pack_item(src, plane, o, role, out, kp, t);
+}
+
+// ---------------------------------------------------------------------------
+// SIMT reference kernel (64-bit IMAD on CUDA cores)
+
+constexpr int ST = 32;
+__global__ void __launch_bounds__(256) gemm_simt_kernel(const uint64_t* __restrict__ A,
+                                                       const uint64_t* __restrict__ B, uint64_t* __restrict__ C,
+                                                       int64_t M, int64_t N, int64_t K, int64_t sam, int64_t sak,
+                                                       int64_t sbk, int64_t sbn, int64_t ldc) {
+  __shared__ uint64_t sa[16][ST + 1];
+  __shared__ uint64_t sb[16][ST + 1];
+  int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 32 x 8 threads, 4 rows each
+  int64_t m0 = blockIdx.y * (int64_t)ST, n0 = blockIdx.x * (int64_t)ST;
+  uint64_t acc[4] = {0, 0, 0, 0};
+  for (int64_t k0 = 0; k0 < K; k0 += 16) {
+    for (int i = threadIdx.x; i < 16 * ST; i += 256) {
+      int kk = i % 16, mm = i / 16;
+      int64_t m = m0 + mm, k = k0 + kk;
+      sa[kk][mm] = (m < M && k < K) ? A[m * sam + k * sak] : 0;
+      int nn = i % ST, kb = i / ST;
+      int64_t n = n0 + nn, k2 = k0 + kb;
+      sb[kb][nn] = (n < N && k2 < K) ? B[k2 * sbk + n * sbn] : 0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      uint64_t b = sb[kk][tx];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[r] += sa[kk][ty * 4 + r] * b;
+    }
+    __syncthreads();
+  }
+  for (int r = 0; r < 4; ++r) {
+    int64_t m = m0 + ty * 4 + r, n = n0 + tx;
+    if (m < M && n < N) C[m * ldc + n] = acc[r];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// tcgen05 kernel
+
+constexpr int BM = 128;            // rows per CTA (TMEM lanes)
+constexpr int BN = 64;             // output columns per CTA (per limb block)
+constexpr int BK = 32;             // K bytes per stage (one kind::i8 MMA K)
+constexpr int STAGES = 4;
+constexpr int A_STAGE = 8 * BM * BK;  // 32 KiB
+constexpr int B_STAGE = 8 * BN * BK;  // 16 KiB
+constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int MAX_SPLIT_K = 16384;   // exactness: S_3 <= 4 K 255^2 < 2^32
+
+DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+DEV void tma_load_3d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+// K-major, 32-byte-swizzled UMMA shared-memory descriptor (atom 8 rows x 32 B).
+DEV uint64_t umma_desc_sw32(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3fff);      // start address
+  d |= (uint64_t)0 << 16;                       // LBO (unused: one atom along K)
+  d |= (uint64_t)((256 >> 4) & 0x3fff) << 32;  // SBO: 8 rows x 32 B
+  d |= (uint64_t)1 << 46;                       // descriptor version (sm_100)
+  d |= (uint64_t)6 << 61;                       // SWIZZLE_32B
+  return d;
+}
+
+// Instruction descriptor: u8 x u8 -> s32, K-major A and B, M = 128.
+__host__ __device__ constexpr uint32_t idesc_i8(int n) {
+  return (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
+DEV void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+DEV void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__global__ void __launch_bounds__(256, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   uint64_t* __restrict__ C, int64_t M, int64_t N, int64_t kp, int64_t ldc, int64_t c_group,
+                   int splits, int kb_per_split) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t n0 = (int64_t)blockIdx.x * BN, m0 = (int64_t)blockIdx.y * BM;
+  const int g = blockIdx.z / splits, split = blockIdx.z % splits;
+  const int nkb_total = (int)((kp + BK - 1) / BK);
+  const int kb0 = split * kb_per_split;
+  int kb1 = kb0 + kb_per_split;
+  if (kb1 > nkb_total) kb1 = nkb_total;
+  const int nkb = kb1 > kb0 ? kb1 - kb0 : 0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer ----
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    for (int i = 0; i < nkb; ++i) {
+      int s = i % STAGES;
+      uint32_t ph = (i / STAGES) & 1;
+      mbar_wait(&empty[s], ph ^ 1);
+      mbar_expect_tx(&full[s], A_STAGE + B_STAGE);
+      int kc = (kb0 + i) * BK;
+      tma_load_3d(&tmA, &full[s], sA + s * A_STAGE, kc, (int)m0, g * 8);
+      tma_load_3d(&tmB, &full[s], sB + s * B_STAGE, kc, (int)n0, g * 8);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer ----
+    for (int i = 0; i < nkb; ++i) {
+      int s = i % STAGES;
+      uint32_t ph = (i / STAGES) & 1;
+      mbar_wait(&full[s], ph);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      uint32_t a_base = smem_u32(sA + s * A_STAGE);
+      uint32_t b_base = smem_u32(sB + s * B_STAGE);
+#pragma unroll
+      for (int li = 0; li < 8; ++li) {
+        uint64_t da = umma_desc_sw32(a_base + li * (BM * BK));
+        int nblk = 8 - li;  // limb blocks j = 0 .. 7 - li  ->  diagonals li .. 7
+        int first = nblk > 4 ? 4 : nblk;
+        uint32_t acc = (i > 0 || li > 0) ? 1u : 0u;
+        mma_i8(tmem + li * BN, da, umma_desc_sw32(b_base), idesc_i8(first * BN), acc);
+        if (nblk > 4) {
+          mma_i8(tmem + (li + 4) * BN, da, umma_desc_sw32(b_base + 4 * (BN * BK)), idesc_i8((nblk - 4) * BN),
+                 acc);
+        }
+      }
+      mma_commit(&empty[s]);
+    }
+    mma_commit(tmem_full);
+  } else if (warp >= 4) {
+    // ---- epilogue: TMEM -> registers -> recombine -> global ----
+    const int wq = warp - 4;  // TMEM lanes 32 wq .. 32 wq + 31
+    const int64_t row = m0 + wq * 32 + lane;
+    uint64_t* crow = C + (int64_t)g * c_group + row * ldc;
+    if (nkb > 0) {
+      mbar_wait(tmem_full, 0);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+    }
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 8) {
+      uint64_t acc[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = 0;
+      if (nkb > 0) {
+#pragma unroll
+        for (int d = 0; d < 8; ++d) {
+          uint32_t r[8];
+          uint32_t taddr = tmem + ((uint32_t)(wq * 32) << 16) + d * BN + c0;
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+              : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] += (uint64_t)r[e] << (8 * d);
+        }
+      }
+      if (row < M) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          int64_t col = n0 + c0 + e;
+          if (col < N) {
+            if (splits > 1)
+              atomicAdd(reinterpret_cast<unsigned long long*>(crow + col), (unsigned long long)acc[e]);
+            else
+              crow[col] = acc[e];
+          }
+        }
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+  }
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host: tensor maps via the driver entry point (no -lcuda link needed)
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+static int make_map(CUtensorMap* map, const uint8_t* base, int64_t kp, int64_t rows, int64_t planes, int box_rows) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) {
+    set_last_error("cuTensorMapEncodeTiled unavailable");
+    return MPC3_ERR_CUDA;
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)kp, (cuuint64_t)rows, (cuuint64_t)planes};
+  cuuint64_t strides[2] = {(cuuint64_t)kp, (cuuint64_t)(kp * rows)};
+  cuuint32_t box[3] = {(cuuint32_t)BK, (cuuint32_t)box_rows, 8};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)base, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_last_error("cuTensorMapEncodeTiled failed");
+    return MPC3_ERR_CUDA;
+  }
+  return MPC3_OK;
+}
+
+static Operand to_operand(const mpc3_operand* o) {
+  Operand p;
+  p.mode = o->mode;
+  p.rows = o->rows;
+  p.k = o->k;
+  p.off = o->off;
+  p.s_r = o->s_r;
+  p.t0 = o->t0;
+  p.t1 = o->t1;
+  p.t2 = o->t2;
+  p.K1 = o->K1 > 0 ? o->K1 : 1;
+  p.K2 = o->K2 > 0 ? o->K2 : 1;
+  p.n = o->n;
+  p.c = o->c;
+  p.h = o->h;
+  p.w = o->w;
+  p.sN = o->sN;
+  p.sC = o->sC;
+  p.sH = o->sH;
+  p.sW = o->sW;
+  p.kh = o->kh > 0 ? o->kh : 1;
+  p.kw = o->kw > 0 ? o->kw : 1;
+  p.sh = o->sh > 0 ? o->sh : 1;
+  p.sw = o->sw > 0 ? o->sw : 1;
+  p.ph = o->ph;
+  p.pw = o->pw;
+  p.dh = o->dh > 0 ? o->dh : 1;
+  p.dw = o->dw > 0 ? o->dw : 1;
+  p.oh = o->oh > 0 ? o->oh : 1;
+  p.ow = o->ow > 0 ? o->ow : 1;
+  return p;
+}
+
+}  // namespace mpc3
+
+using namespace mpc3;
+
+extern "C" {
+
+int mpc3_ring_pack(const uint64_t* src, int64_t src_plane, const mpc3_operand* op, int role, uint8_t* out,
+                   int64_t kp, void* stream) {
+  if (!op || role < 0 || role > 2) return MPC3_ERR_CONFIG;
+  if (kp % 16) return MPC3_ERR_SHAPE;
+  int64_t kneed = role == 2 ? op->k : 2 * op->k;
+  if (kp < kneed || op->rows < 0 || op->k < 0) return MPC3_ERR_SHAPE;
+  if (op->mode < 0 || op->mode > 2) return MPC3_ERR_CONFIG;
+  Operand o = to_operand(op);
+  int groups = role == 2 ? 1 : 3;
+  int64_t total = (int64_t)groups * o.rows * (kp / 8);
+  if (total == 0) return MPC3_OK;
+  pack_kernel<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(src, src_plane, o, role, groups, out, kp);
+  return check_launch("ring_pack");
+}
+
+int mpc3_ring_gemm_packed(const uint8_t* A, const uint8_t* B, uint64_t* C, int groups, int64_t M, int64_t N,
+                          int64_t kp, int64_t ldc, int64_t c_group, int splits, void* stream) {
+  if (groups < 1 || M < 0 || N < 0 || kp < 0 || splits < 1) return MPC3_ERR_SHAPE;
+  if (kp % 16) return MPC3_ERR_SHAPE;
+  if (M == 0 || N == 0) return MPC3_OK;
+  if (M > (1 << 30) || N > (1 << 30)) return MPC3_ERR_SHAPE;
+  int nkb = (int)((kp + BK - 1) / BK);
+  int kbs = (nkb + splits - 1) / splits;
+  if ((int64_t)kbs * BK > MAX_SPLIT_K) return MPC3_ERR_EXACTNESS;  // caller must split longer K
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) !=
+        cudaSuccess)
+      return check_launch("gemm_tc attr");
+    attr_set = true;
+  }
+  CUtensorMap ta, tb;
+  int st = make_map(&ta, A, kp, M, (int64_t)groups * 8, BM);
+  if (st) return st;
+  st = make_map(&tb, B, kp, N, (int64_t)groups * 8, BN);
+  if (st) return st;
+  dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)(groups * splits));
+  gemm_tc_kernel<<<grid, 256, SMEM_BYTES, as_stream(stream)>>>(ta, tb, C, M, N, kp, ldc, c_group, splits, kbs);
+  return check_launch("ring_gemm_tc");
+}
+
+int mpc3_ring_gemm_simt(const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t M, int64_t N, int64_t K,
+                        int64_t sam, int64_t sak, int64_t sbk, int64_t sbn, int64_t ldc, void* stream) {
+  if (M < 0 || N < 0 || K < 0) return MPC3_ERR_SHAPE;
+  if (M == 0 || N == 0) return MPC3_OK;
+  dim3 grid((unsigned)((N + ST - 1) / ST), (unsigned)((M + ST - 1) / ST));
+  gemm_simt_kernel<<<grid, 256, 0, as_stream(stream)>>>(A, B, C, M, N, K, sam, sak, sbk, sbn, ldc);
+  return check_launch("ring_gemm_simt");
+}
+
+size_t mpc3_ring_matmul_workspace(int64_t M, int64_t N, int64_t K) {
+  int64_t kp = (K + 15) / 16 * 16;
+  return (size_t)(8 * M * kp + 8 * N * kp);
+}
+
+int mpc3_ring_matmul_u64(const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t M, int64_t N, int64_t K,
+                         void* workspace, void* stream) {
+  if (M < 0 || N < 0 || K < 0) return MPC3_ERR_SHAPE;
+  if (M == 0 || N == 0) return MPC3_OK;
+  int64_t kp = (K + 15) / 16 * 16;
+  uint8_t* pa = reinterpret_cast<uint8_t*>(workspace);
+  uint8_t* pb = pa + 8 * M * kp;
+  mpc3_operand oa;
+  memset(&oa, 0, sizeof(oa));
+  oa.mode = MPC3_GATHER_DENSE;
+  oa.rows = M;
+  oa.k = K;
+  oa.s_r = K;
+  oa.t2 = 1;
+  mpc3_operand ob = oa;
+  ob.rows = N;
+  ob.s_r = 1;
+  ob.t2 = N;
+  int st = mpc3_ring_pack(A, 0, &oa, 2, pa, kp, stream);
+  if (st) return st;
+  st = mpc3_ring_pack(B, 0, &ob, 2, pb, kp, stream);
+  if (st) return st;
+  int nkb = (int)((kp + BK - 1) / BK);
+  int splits = (int)((nkb * (int64_t)BK + MAX_SPLIT_K - 1) / MAX_SPLIT_K);
+  if (splits > 1) {
+    if (cudaMemsetAsync(C, 0, (size_t)M * N * 8, as_stream(stream)) != cudaSuccess) return check_launch("memset");
+  }
+  return mpc3_ring_gemm_packed(pa, pb, C, 1, M, N, kp, N, 0, splits, stream);
+}
+
+}  // extern "C"

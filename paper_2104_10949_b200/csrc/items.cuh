@@ -1,0 +1,208 @@
+// Per-work-item bodies of the elementwise protocol kernels.  Each kernel in
+// elementwise.cu is a grid-stride loop over these; hostcheck.cpp runs the same
+// functions in a plain loop on the CPU so the oracle can check the device
+// logic bit-for-bit without a GPU.
+#pragma once
+#include "pack.cuh"
+#include "protocol.cuh"
+
+namespace mpc3 {
+
+HD Trio load_trio(const uint64_t* p, uint64_t plane, uint64_t e) {
+  Trio t;
+  t.c[0] = p[e];
+  t.c[1] = p[plane + e];
+  t.c[2] = p[2 * plane + e];
+  return t;
+}
+HD void store_trio(uint64_t* p, uint64_t plane, uint64_t e, const Trio& t) {
+  p[e] = t.c[0];
+  p[plane + e] = t.c[1];
+  p[2 * plane + e] = t.c[2];
+}
+
+// words [word_off, word_off+count) of one stream; item t = stream block first_blk + t
+template <class T>
+HD void prf_words_item(const T& tab, const uint32_t* rk, StreamHead h, uint64_t word_off, uint64_t count,
+                       uint64_t* out, uint64_t t) {
+  uint64_t blk = (word_off >> 1) + t;
+  Word2 w = prf_block(tab, rk, h, blk);
+  uint64_t w0 = 2 * blk;
+  if (w0 >= word_off && w0 < word_off + count) out[w0 - word_off] = w.w0;
+  if (w0 + 1 >= word_off && w0 + 1 < word_off + count) out[w0 + 1 - word_off] = w.w1;
+}
+
+template <class T>
+HD void zero_share_item(const T& tab, const uint32_t* rk3, StreamHead h, int xor_mode, uint64_t n,
+                        uint64_t* out, uint64_t b) {
+  KeyWords f[2];
+  key_words_pair(tab, rk3, h, b, f[0], f[1]);
+  for (int e = 0; e < 2; ++e) {
+    uint64_t idx = 2 * b + e;
+    if (idx >= n) break;
+    for (int i = 0; i < 3; ++i) {
+      uint64_t a = f[e].k[i], p = f[e].k[(i + 2) % 3];
+      out[i * n + idx] = xor_mode ? (a ^ p) : (a - p);
+    }
+  }
+}
+
+// kind: 0 = mul, 1 = truncate, 2 = mul then truncate
+template <class T>
+HD void arith_item(const T& tab, const uint32_t* rk3, int kind, StreamHead ha, StreamHead hrho, StreamHead hr,
+                   int bits, const uint64_t* x, const uint64_t* y, uint64_t* out, uint64_t n, uint64_t b) {
+  bool two = 2 * b + 1 < n;
+  Trio v[2];
+  v[0] = load_trio(x, n, 2 * b);
+  v[1] = two ? load_trio(x, n, 2 * b + 1) : v[0];
+  if (kind != 1) {
+    Trio w[2];
+    w[0] = load_trio(y, n, 2 * b);
+    w[1] = two ? load_trio(y, n, 2 * b + 1) : w[0];
+    KeyWords f0, f1;
+    key_words_pair(tab, rk3, ha, b, f0, f1);
+    v[0] = trio_mul(v[0], w[0], f0);
+    v[1] = trio_mul(v[1], w[1], f1);
+  }
+  if (kind != 0) {
+    Word2 rho = prf_block(tab, rk3 + 2 * 44, hrho, b);
+    Word2 r = prf_block(tab, rk3 + 1 * 44, hr, b);
+    v[0] = trio_truncate(v[0], rho.w0, r.w0, bits);
+    v[1] = trio_truncate(v[1], rho.w1, r.w1, bits);
+  }
+  store_trio(out, n, 2 * b, v[0]);
+  if (two) store_trio(out, n, 2 * b + 1, v[1]);
+}
+
+template <class T>
+HD void sign_item(const T& tab, const uint32_t* rk3, const SignStreams& st, int mode, const uint64_t* x,
+                  uint64_t* out, uint64_t* mask, uint64_t n, uint64_t n_total, uint64_t elem_off, uint64_t b) {
+  bool two = 2 * b + 1 < n;
+  Trio v[2], o[2], m[2];
+  v[0] = load_trio(x, n, 2 * b);
+  v[1] = two ? load_trio(x, n, 2 * b + 1) : v[0];
+  sign_circuit_pair(tab, rk3, st, n_total, (elem_off >> 1) + b, mode, v, o, m);
+  store_trio(out, n, 2 * b, o[0]);
+  if (two) store_trio(out, n, 2 * b + 1, o[1]);
+  if (mode == MODE_RELU && mask) {
+    store_trio(mask, n, 2 * b, m[0]);
+    if (two) store_trio(mask, n, 2 * b + 1, m[1]);
+  }
+}
+
+template <class T>
+HD void inject_item(const T& tab, const uint32_t* rk3, StreamHead a0, StreamHead a1, const uint64_t* bits,
+                    uint64_t* out, uint64_t n, uint64_t b) {
+  bool two = 2 * b + 1 < n;
+  Trio v[2], o[2];
+  v[0] = load_trio(bits, n, 2 * b);
+  v[1] = two ? load_trio(bits, n, 2 * b + 1) : v[0];
+  inject_pair(tab, rk3, a0, a1, b, v, o);
+  store_trio(out, n, 2 * b, o[0]);
+  if (two) store_trio(out, n, 2 * b + 1, o[1]);
+}
+
+struct View4 {
+  int64_t full[4], crop[4], zs[4], os[4], zp, op;
+};
+
+template <class T>
+HD void reshare_trunc_item(const T& tab, const uint32_t* rk3, StreamHead ha, StreamHead hrho, StreamHead hr,
+                           int bits, const uint64_t* z, const View4& v, uint64_t* out, uint64_t n, uint64_t b) {
+  int64_t zoff[2] = {0, 0}, ooff[2] = {0, 0};
+  bool ok[2];
+  for (int e = 0; e < 2; ++e) {
+    uint64_t f = 2 * b + e;
+    ok[e] = f < n;
+    uint64_t r = f;
+    int64_t i3 = r % v.full[3];
+    r /= v.full[3];
+    int64_t i2 = r % v.full[2];
+    r /= v.full[2];
+    int64_t i1 = r % v.full[1];
+    int64_t i0 = r / v.full[1];
+    ok[e] = ok[e] && i0 < v.crop[0] && i1 < v.crop[1] && i2 < v.crop[2] && i3 < v.crop[3];
+    zoff[e] = i0 * v.zs[0] + i1 * v.zs[1] + i2 * v.zs[2] + i3 * v.zs[3];
+    ooff[e] = i0 * v.os[0] + i1 * v.os[1] + i2 * v.os[2] + i3 * v.os[3];
+  }
+  if (!ok[0] && !ok[1]) return;
+  KeyWords f0, f1;
+  key_words_pair(tab, rk3, ha, b, f0, f1);
+  Word2 rho = {0, 0}, r = {0, 0};
+  if (bits) {
+    rho = prf_block(tab, rk3 + 2 * 44, hrho, b);
+    r = prf_block(tab, rk3 + 1 * 44, hr, b);
+  }
+  for (int e = 0; e < 2; ++e) {
+    if (!ok[e]) continue;
+    Trio t = load_trio(z + zoff[e], v.zp, 0);
+    t = trio_reshare(t, e ? f1 : f0);
+    if (bits) t = trio_truncate(t, e ? rho.w1 : rho.w0, e ? r.w1 : r.w0, bits);
+    store_trio(out + ooff[e], v.op, 0, t);
+  }
+}
+
+struct PoolGeom {
+  int64_t N, C, H, W, OH, OW;
+  int kh, kw, sh, sw;
+};
+
+// fused window sum (x mulc) + truncate; backward = scatter-add then the same
+template <class T>
+HD void pool_item(const T& tab, const uint32_t* rk3, bool backward, StreamHead hrho, StreamHead hr, int bits,
+                  uint64_t mulc, const uint64_t* x, uint64_t* out, const PoolGeom& p, uint64_t b) {
+  uint64_t n = backward ? (uint64_t)p.N * p.C * p.H * p.W : (uint64_t)p.N * p.C * p.OH * p.OW;
+  uint64_t nin = backward ? (uint64_t)p.N * p.C * p.OH * p.OW : (uint64_t)p.N * p.C * p.H * p.W;
+  Trio s[2];
+  for (int e = 0; e < 2; ++e) {
+    uint64_t f = 2 * b + e;
+    s[e].c[0] = s[e].c[1] = s[e].c[2] = 0;
+    if (f >= n) continue;
+    if (!backward) {
+      int64_t ox = f % p.OW, oy = (f / p.OW) % p.OH, nc = f / (p.OW * p.OH);
+      const uint64_t* base = x + nc * p.H * p.W + (oy * p.sh) * p.W + ox * p.sw;
+      for (int u = 0; u < p.kh; ++u)
+        for (int q = 0; q < p.kw; ++q)
+          for (int i = 0; i < 3; ++i) s[e].c[i] += base[i * nin + u * p.W + q];
+    } else {
+      // windows (oy, ox) with oy*sh <= iy < oy*sh + kh, oy < OH (nn.py:487-499)
+      int64_t ix = f % p.W, iy = (f / p.W) % p.H, nc = f / (p.W * p.H);
+      for (int64_t oy = iy / p.sh; oy >= 0 && oy * p.sh + p.kh > iy; --oy) {
+        if (oy >= p.OH) continue;
+        for (int64_t ox = ix / p.sw; ox >= 0 && ox * p.sw + p.kw > ix; --ox) {
+          if (ox >= p.OW) continue;
+          uint64_t gi = nc * p.OH * p.OW + oy * p.OW + ox;
+          for (int i = 0; i < 3; ++i) s[e].c[i] += x[i * nin + gi];
+        }
+      }
+    }
+    for (int i = 0; i < 3; ++i) s[e].c[i] *= mulc;
+  }
+  Word2 rho = prf_block(tab, rk3 + 2 * 44, hrho, b);
+  Word2 r = prf_block(tab, rk3 + 1 * 44, hr, b);
+  for (int e = 0; e < 2; ++e) {
+    uint64_t f = 2 * b + e;
+    if (f >= n) break;
+    store_trio(out, n, f, trio_truncate(s[e], e ? rho.w1 : rho.w0, e ? r.w1 : r.w0, bits));
+  }
+}
+
+// packing item: 8 consecutive kk of one (g, r) -> one u64 per limb plane
+HD void pack_item(const uint64_t* src, int64_t plane, const Operand& o, int role, uint8_t* out, int64_t kp,
+                  int64_t t) {
+  int64_t chunks = kp / 8;
+  int64_t ch = t % chunks;
+  int64_t q = t / chunks;
+  int64_t r = q % o.rows;
+  int g = (int)(q / o.rows);
+  uint64_t v[8];
+  for (int e = 0; e < 8; ++e) v[e] = packed_value(o, src, plane, role, g, r, ch * 8 + e);
+  uint8_t* base = out + ((int64_t)g * 8 * o.rows + r) * kp + ch * 8;
+  for (int l = 0; l < 8; ++l) {
+    uint64_t word = 0;
+    for (int e = 0; e < 8; ++e) word |= ((v[e] >> (8 * l)) & 0xffull) << (8 * e);
+    *reinterpret_cast<uint64_t*>(base + (int64_t)l * o.rows * kp) = word;
+  }
+}
+
+}  // namespace mpc3

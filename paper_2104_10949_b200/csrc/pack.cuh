@@ -1,0 +1,68 @@
+// Operand gathers for the ring GEMM: dense / im2col / weight-gradient views of
+// a ring tensor (ring.py:225-256 _im2col; nn.py:435-484 conv gradients).
+#pragma once
+#include "common.cuh"
+
+namespace mpc3 {
+
+struct Operand {
+  int mode;
+  int64_t rows, k;
+  int64_t off, s_r, t0, t1, t2, K1, K2;
+  int64_t n, c, h, w, sN, sC, sH, sW;
+  int64_t kh, kw, sh, sw, ph, pw, dh, dw, oh, ow;
+};
+
+// Element offset of v(r, k) in one component plane, or -1 for a structural zero.
+HD int64_t gather_offset(const Operand& o, int64_t r, int64_t k) {
+  if (o.mode == MPC3_GATHER_DENSE) {
+    int64_t k2 = k % o.K2;
+    int64_t q = k / o.K2;
+    int64_t k1 = q % o.K1;
+    int64_t k0 = q / o.K1;
+    return o.off + r * o.s_r + k0 * o.t0 + k1 * o.t1 + k2 * o.t2;
+  }
+  if (o.mode == MPC3_GATHER_IM2COL) {
+    // r = (n, y, x) over (N, OH, OW); k = (c, u, v) over (C, kh, kw)
+    int64_t x = r % o.ow, q = r / o.ow;
+    int64_t y = q % o.oh, n = q / o.oh;
+    int64_t v = k % o.kw;
+    q = k / o.kw;
+    int64_t u = q % o.kh, c = q / o.kh;
+    int64_t iy = y * o.sh + u - o.ph, ix = x * o.sw + v - o.pw;  // dilated coordinates
+    if (iy < 0 || ix < 0 || iy > (o.h - 1) * o.dh || ix > (o.w - 1) * o.dw) return -1;
+    if (iy % o.dh || ix % o.dw) return -1;
+    return n * o.sN + c * o.sC + (iy / o.dh) * o.sH + (ix / o.dw) * o.sW;
+  }
+  // WGRAD: r = (c, u, v) over (C, kh, kw); k = (n, y, x) over (N, OH, OW)
+  int64_t v = r % o.kw, q = r / o.kw;
+  int64_t u = q % o.kh, c = q / o.kh;
+  int64_t x = k % o.ow;
+  q = k / o.ow;
+  int64_t y = q % o.oh, n = q / o.oh;
+  int64_t iy = y * o.sh + u - o.ph, ix = x * o.sw + v - o.pw;
+  if (iy < 0 || ix < 0 || iy >= o.h || ix >= o.w) return -1;
+  return n * o.sN + c * o.sC + iy * o.sH + ix * o.sW;
+}
+
+// Value of the packed operand of group g (party, or 0 for a plain operand) at
+// (r, kk) with kk in [0, 2K) for the cross-term roles (protocols.py:110-115).
+HD uint64_t packed_value(const Operand& o, const uint64_t* src, int64_t plane, int role, int g, int64_t r,
+                         int64_t kk) {
+  if (role == 2) {
+    if (kk >= o.k) return 0;
+    int64_t off = gather_offset(o, r, kk);
+    return off < 0 ? 0 : src[off];
+  }
+  if (kk >= 2 * o.k) return 0;
+  bool first = kk < o.k;
+  int64_t k = first ? kk : kk - o.k;
+  int64_t off = gather_offset(o, r, k);
+  if (off < 0) return 0;
+  int gn = (g + 1) % 3;
+  uint64_t self = src[g * plane + off], nxt = src[gn * plane + off];
+  if (role == 0) return first ? self + nxt : self;  // [x_i + x_{i+1} | x_i]
+  return first ? self : nxt;                        // [y_i | y_{i+1}]
+}
+
+}  // namespace mpc3

@@ -1,0 +1,244 @@
+// Per-element trio protocol logic (three co-resident parties, components in
+// registers).  Host+device so the CPU self-check build runs the very same code.
+//
+// Notation: a trio is the three additive (or XOR) components c0,c1,c2 of a
+// replicated sharing; party i holds (c_i, c_{i+1}) (sharing.py:1-12).  A
+// reshare keeps party i's local product z_i as its new `hi`, which makes
+// z_i the new component i+1 (protocols.py:88-94, 223-230).
+#pragma once
+#include "aes.cuh"
+
+namespace mpc3 {
+
+struct Trio {
+  uint64_t c[3];
+};
+
+// Three per-key words of one stream position: W[i] = F(k_i)[w].
+struct KeyWords {
+  uint64_t k[3];
+};
+
+// z_i = x_i*y_i + x_{i+1}*y_i + x_i*y_{i+1} + (F_i - F_{i-1}); c'_{i+1} = z_i
+// (protocols.py:79-94, sharing.py:233-240).
+HD Trio trio_mul(const Trio& x, const Trio& y, const KeyWords& f) {
+  uint64_t z[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    int n = (i + 1) % 3, p = (i + 2) % 3;
+    z[i] = x.c[i] * y.c[i] + x.c[n] * y.c[i] + x.c[i] * y.c[n] + (f.k[i] - f.k[p]);
+  }
+  Trio o;
+  o.c[1] = z[0];
+  o.c[2] = z[1];
+  o.c[0] = z[2];
+  return o;
+}
+
+// XOR-sharing AND gate with zero share F_i ^ F_{i-1} (protocols.py:223-230).
+HD Trio trio_and(const Trio& a, const Trio& b, const KeyWords& f) {
+  uint64_t z[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    int n = (i + 1) % 3, p = (i + 2) % 3;
+    z[i] = (a.c[i] & b.c[i]) ^ (a.c[n] & b.c[i]) ^ (a.c[i] & b.c[n]) ^ f.k[i] ^ f.k[p];
+  }
+  Trio o;
+  o.c[1] = z[0];
+  o.c[2] = z[1];
+  o.c[0] = z[2];
+  return o;
+}
+
+// Reshare of local products z (already z_i per party) (protocols.py:88-94).
+HD Trio trio_reshare(const Trio& z, const KeyWords& f) {
+  Trio o;
+  o.c[1] = z.c[0] + (f.k[0] - f.k[2]);
+  o.c[2] = z.c[1] + (f.k[1] - f.k[0]);
+  o.c[0] = z.c[2] + (f.k[2] - f.k[1]);
+  return o;
+}
+
+// Truncation by `bits` with rho = offset(F(k_2, TRUNC_RHO)), r = F(k_1, TRUNC_R):
+// out = (sar(rho+h), sar(c0-rho+c1+c2+h) - r, r) (protocols.py:171-216).
+HD Trio trio_truncate(const Trio& x, uint64_t rho_raw, uint64_t r, int bits) {
+  uint64_t half = 1ull << (bits - 1);
+  uint64_t rho = trunc_offset(rho_raw);
+  Trio o;
+  o.c[0] = sar(rho + half, bits);
+  uint64_t b = (x.c[0] - rho) + x.c[1] + x.c[2];
+  o.c[1] = sar(b + half, bits) - r;
+  o.c[2] = r;
+  return o;
+}
+
+HD Trio trio_xor(const Trio& a, const Trio& b) {
+  Trio o;
+  for (int i = 0; i < 3; ++i) o.c[i] = a.c[i] ^ b.c[i];
+  return o;
+}
+HD Trio trio_shl(const Trio& a, int d) {
+  Trio o;
+  for (int i = 0; i < 3; ++i) o.c[i] = a.c[i] << d;
+  return o;
+}
+
+// ReLU family modes (how far the sign circuit runs).
+enum SignMode : int {
+  MODE_A2B = 0,    // binary sharing of x (a2b, protocols.py:266-295)
+  MODE_MSB = 1,    // binary sharing of the sign bit (protocols.py:298-301)
+  MODE_DRELU = 2,  // arithmetic {0,1} mask 1 - msb (protocols.py:334-337)
+  MODE_RELU = 3,   // relu = x * mask, plus the mask (protocols.py:340-348)
+};
+
+// Stream heads of one sign-circuit invocation; counters are the lockstep
+// per-purpose counters the host allotted (sharing.py:225-230).
+struct SignStreams {
+  StreamHead bin;     // BIN_INPUT, 1 counter (k_0 only)
+  StreamHead x[7];    // XOR_ZERO, counters j0..j0+6
+  StreamHead a[3];    // ARITH_ZERO, counters ja..ja+2 (inject, inject, mask)
+};
+
+// Key-word provider over a pair of adjacent elements (words 2b, 2b+1 of each
+// stream share one AES block per key).
+template <class T>
+HD void key_words_pair(const T& tab, const uint32_t* rk3, StreamHead h, uint64_t blk, KeyWords& w0,
+                       KeyWords& w1) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    Word2 p = prf_block(tab, rk3 + 44 * i, h, blk);
+    w0.k[i] = p.w0;
+    w1.k[i] = p.w1;
+  }
+}
+
+template <class T>
+HD KeyWords key_words_one(const T& tab, const uint32_t* rk3, StreamHead h, uint64_t w) {
+  KeyWords o;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) o.k[i] = prf_word(tab, rk3 + 44 * i, h, w);
+  return o;
+}
+
+// The fused sign circuit for the element pair (2*blk, 2*blk+1) of a tensor of
+// n_total elements (n_total sets where the Kogge-Stone p-half lives, word
+// n_total + e, protocols.py:247-259).  valid1 = second element exists.
+// Outputs: out[e] (binary or arithmetic per mode) and, for MODE_RELU, mask[e].
+// AES blocks per element pair: BIN 1, XOR 3 + 6*(3 + 3) - 3 (the last
+// level's p-half is dead: p is never read after the loop, protocols.py:259-263),
+// ARITH 3 per mul.
+template <class T>
+HD void sign_circuit_pair(const T& tab, const uint32_t* rk3, const SignStreams& st, uint64_t n_total,
+                          uint64_t blk, int mode, const Trio x[2], Trio out[2], Trio mask[2]) {
+  // a2b input sharing (protocols.py:278-295): w = ((c0+c1)^r, r, 0), x2 = (0,0,c2)
+  Word2 rb = prf_block(tab, rk3 + 0 * 44, st.bin, blk);
+  Trio a[2], b[2], p[2], g[2], pleaf[2];
+  for (int e = 0; e < 2; ++e) {
+    uint64_t r = e ? rb.w1 : rb.w0;
+    a[e].c[0] = (x[e].c[0] + x[e].c[1]) ^ r;
+    a[e].c[1] = r;
+    a[e].c[2] = 0;
+    b[e].c[0] = 0;
+    b[e].c[1] = 0;
+    b[e].c[2] = x[e].c[2];
+    p[e] = trio_xor(a[e], b[e]);
+    pleaf[e] = p[e];
+  }
+  {
+    KeyWords f0, f1;
+    key_words_pair(tab, rk3, st.x[0], blk, f0, f1);
+    g[0] = trio_and(a[0], b[0], f0);
+    g[1] = trio_and(a[1], b[1], f1);
+  }
+  const bool even_n = (n_total & 1) == 0;
+#if defined(__CUDA_ARCH__)
+#pragma unroll 1
+#endif
+  for (int lvl = 1; lvl <= 6; ++lvl) {
+    const int d = 1 << (lvl - 1);
+    KeyWords f0, f1;
+    key_words_pair(tab, rk3, st.x[lvl], blk, f0, f1);
+    Trio gt0 = trio_and(p[0], trio_shl(g[0], d), f0);
+    Trio gt1 = trio_and(p[1], trio_shl(g[1], d), f1);
+    if (lvl < 6) {
+      KeyWords q0, q1;
+      uint64_t w = n_total + 2 * blk;
+      if (even_n) {
+        key_words_pair(tab, rk3, st.x[lvl], w >> 1, q0, q1);
+      } else {
+        q0 = key_words_one(tab, rk3, st.x[lvl], w);
+        q1 = key_words_one(tab, rk3, st.x[lvl], w + 1);
+      }
+      Trio pt0 = trio_and(p[0], trio_shl(p[0], d), q0);
+      Trio pt1 = trio_and(p[1], trio_shl(p[1], d), q1);
+      p[0] = pt0;
+      p[1] = pt1;
+    }
+    g[0] = trio_xor(g[0], gt0);
+    g[1] = trio_xor(g[1], gt1);
+  }
+  Trio s[2];
+  for (int e = 0; e < 2; ++e) s[e] = trio_xor(pleaf[e], trio_shl(g[e], 1));
+  if (mode == MODE_A2B) {
+    out[0] = s[0];
+    out[1] = s[1];
+    return;
+  }
+  Trio bit[2];
+  for (int e = 0; e < 2; ++e)
+    for (int i = 0; i < 3; ++i) bit[e].c[i] = s[e].c[i] >> 63;
+  if (mode == MODE_MSB) {
+    out[0] = bit[0];
+    out[1] = bit[1];
+    return;
+  }
+  // bit_inject (protocols.py:304-331): u = s0 + s1 - 2 mul(s0, s1); v = u + s2 - 2 mul(u, s2)
+  Trio m[2];
+  {
+    KeyWords f0, f1, h0, h1;
+    key_words_pair(tab, rk3, st.a[0], blk, f0, f1);
+    key_words_pair(tab, rk3, st.a[1], blk, h0, h1);
+    for (int e = 0; e < 2; ++e) {
+      Trio t0 = {{bit[e].c[0], 0, 0}}, t1 = {{0, bit[e].c[1], 0}}, t2 = {{0, 0, bit[e].c[2]}};
+      Trio pr = trio_mul(t0, t1, e ? f1 : f0);
+      Trio u;
+      for (int i = 0; i < 3; ++i) u.c[i] = t0.c[i] + t1.c[i] - 2 * pr.c[i];
+      Trio pv = trio_mul(u, t2, e ? h1 : h0);
+      Trio v;
+      for (int i = 0; i < 3; ++i) v.c[i] = u.c[i] + t2.c[i] - 2 * pv.c[i];
+      // drelu = 1 - v: negate, constant into component 0 (protocols.py:57-66, 334-337)
+      for (int i = 0; i < 3; ++i) m[e].c[i] = 0 - v.c[i];
+      m[e].c[0] += 1;
+    }
+  }
+  if (mode == MODE_DRELU) {
+    out[0] = m[0];
+    out[1] = m[1];
+    return;
+  }
+  KeyWords f0, f1;
+  key_words_pair(tab, rk3, st.a[2], blk, f0, f1);
+  out[0] = trio_mul(x[0], m[0], f0);
+  out[1] = trio_mul(x[1], m[1], f1);
+  mask[0] = m[0];
+  mask[1] = m[1];
+}
+
+// bit_inject alone on binary bit shares (protocols.py:304-331).
+template <class T>
+HD void inject_pair(const T& tab, const uint32_t* rk3, StreamHead a0, StreamHead a1, uint64_t blk,
+                    const Trio bit[2], Trio out[2]) {
+  KeyWords f0, f1, h0, h1;
+  key_words_pair(tab, rk3, a0, blk, f0, f1);
+  key_words_pair(tab, rk3, a1, blk, h0, h1);
+  for (int e = 0; e < 2; ++e) {
+    Trio t0 = {{bit[e].c[0], 0, 0}}, t1 = {{0, bit[e].c[1], 0}}, t2 = {{0, 0, bit[e].c[2]}};
+    Trio pr = trio_mul(t0, t1, e ? f1 : f0);
+    Trio u;
+    for (int i = 0; i < 3; ++i) u.c[i] = t0.c[i] + t1.c[i] - 2 * pr.c[i];
+    Trio pv = trio_mul(u, t2, e ? h1 : h0);
+    for (int i = 0; i < 3; ++i) out[e].c[i] = u.c[i] + t2.c[i] - 2 * pv.c[i];
+  }
+}
+
+}  // namespace mpc3
