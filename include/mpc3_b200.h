@@ -21,6 +21,10 @@
  *  - Counters j_* are the per-purpose lockstep stream counters that
  *    PartyContext.take (sharing.py:225-230) would hand out; the host keeps
  *    them and checks freshness before launch (sharing.py:190-204).
+ *  - ctr (nullable) is a DEVICE pointer to uint64[8] indexed by purpose tag;
+ *    the effective counter is j + ctr[purpose].  A CUDA graph captured with a
+ *    ctr buffer advances its PRF counters on every replay by bumping ctr,
+ *    reproducing the sequential counter schedule of the reference.
  *  - `stream` is a cudaStream_t passed as void*.  Calls are asynchronous on
  *    it and reentrant.  Return value: MPC3_OK or an error status; statuses
  *    map 1:1 onto the reference's exception taxonomy (errors.py:4-53).
@@ -68,7 +72,7 @@ int mpc3_prf_words(const uint32_t* rk, uint32_t purpose, uint64_t index, uint64_
 
 /* Arithmetic (xor_mode=0) or XOR (xor_mode=1) zero sharing of n words,
  * trio output z_i = F(k_i) -/^ F(k_{i-1}) (sharing.py:233-250). */
-int mpc3_rss_zero_share(const uint32_t* rk3, uint32_t purpose, uint64_t index, int xor_mode,
+int mpc3_rss_zero_share(const uint32_t* rk3, const uint64_t* ctr, uint32_t purpose, uint64_t index, int xor_mode,
                         uint64_t n, uint64_t* out_trio, void* stream);
 
 /* ---- local ring ops (ring.py:50-79, protocols.py:57-72, sharing.py:54-67) ---- */
@@ -97,16 +101,16 @@ int mpc3_ring_rowsum(const uint64_t* a, uint64_t* out, uint64_t rows, uint64_t c
 /* ---- elementwise protocols on trio tensors ---- */
 
 /* mul (protocols.py:79-94): out = reshare(x*y), 1 ARITH_ZERO counter. */
-int mpc3_rss_mul(const uint32_t* rk3, uint64_t j_arith, const uint64_t* x, const uint64_t* y,
+int mpc3_rss_mul(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, const uint64_t* x, const uint64_t* y,
                  uint64_t* out, uint64_t n, void* stream);
 
 /* truncate (protocols.py:171-216): bits in [1,61]; TRUNC_RHO and TRUNC_R counters. */
-int mpc3_rss_truncate(const uint32_t* rk3, uint64_t j_rho, uint64_t j_r, int bits, const uint64_t* x,
+int mpc3_rss_truncate(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_rho, uint64_t j_r, int bits, const uint64_t* x,
                       uint64_t* out, uint64_t n, void* stream);
 
 /* mul + truncate fused (protocols.py:79-94 then 171-216; the `truncate(mul())`
  * pairs of exp_approx / reciprocal / division / softmax, 414-468). */
-int mpc3_rss_mul_truncate(const uint32_t* rk3, uint64_t j_arith, uint64_t j_rho, uint64_t j_r, int bits,
+int mpc3_rss_mul_truncate(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, uint64_t j_rho, uint64_t j_r, int bits,
                           const uint64_t* x, const uint64_t* y, uint64_t* out, uint64_t n, void* stream);
 
 /* Sign circuit (protocols.py:266-348): a2b + 64-bit Kogge-Stone + msb +
@@ -116,21 +120,23 @@ int mpc3_rss_mul_truncate(const uint32_t* rk3, uint64_t j_arith, uint64_t j_rho,
  * Counters: BIN_INPUT j_bin; XOR_ZERO j_xor..j_xor+6; ARITH_ZERO j_arith..+2
  * (modes 2/3 use 2/3 of them).  n_total/elem_off allow a shard of a larger
  * tensor (the Kogge-Stone p-half lives at word n_total + e). */
-int mpc3_rss_sign(const uint32_t* rk3, int mode, uint64_t j_bin, uint64_t j_xor, uint64_t j_arith,
+int mpc3_rss_sign(const uint32_t* rk3, const uint64_t* ctr, int mode, uint64_t j_bin, uint64_t j_xor, uint64_t j_arith,
                   const uint64_t* x, uint64_t* out, uint64_t* mask, uint64_t n, uint64_t n_total,
                   uint64_t elem_off, void* stream);
 
 /* bit_inject of XOR-shared bits (protocols.py:304-331), 2 ARITH counters. */
-int mpc3_rss_bit_inject(const uint32_t* rk3, uint64_t j_arith, const uint64_t* bits, uint64_t* out,
+int mpc3_rss_bit_inject(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, const uint64_t* bits, uint64_t* out,
                         uint64_t n, void* stream);
 
 /* Output view of a bilinear result: the logical ("full") output is a 4-d
  * C-order tensor of sizes full[4]; PRF word index = its flat index.  Only the
- * sub-box crop[4] (crop[k] <= full[k], origin 0) is produced.  Element
- * (i0..i3) reads z at z + sum i_k*z_stride[k] (plane stride z_plane) and
- * writes out + sum i_k*out_stride[k] (plane stride out_plane). */
+ * sub-box [origin, origin + crop) is produced (the reference's crop /
+ * embed of conv gradients, nn.py:456, 478-482).  Element (i0..i3) reads z at
+ * z + sum i_k*z_stride[k] (plane stride z_plane) and writes
+ * out + sum (i_k - origin_k)*out_stride[k] (plane stride out_plane). */
 typedef struct {
   int64_t full[4];
+  int64_t origin[4];
   int64_t crop[4];
   int64_t z_stride[4];
   int64_t out_stride[4];
@@ -141,21 +147,21 @@ typedef struct {
 /* Reshare of per-party local products z (z_i in plane i) followed by
  * truncation (protocols.py:110-117 / 129-136: _reshare then truncate).
  * bits = 0 skips truncation (bare reshare). */
-int mpc3_rss_reshare_truncate(const uint32_t* rk3, uint64_t j_arith, uint64_t j_rho, uint64_t j_r,
+int mpc3_rss_reshare_truncate(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, uint64_t j_rho, uint64_t j_r,
                               int bits, const uint64_t* z, const mpc3_view4* view, uint64_t* out,
                               void* stream);
 
 /* avgpool (protocols.py:139-159): window sums, then truncate(log2 area) when
  * the area is a power of two, else mul_const(mulc) + truncate(t).  x/out are
  * trio NCHW; bits/mulc chosen by the caller (mulc = 1 for power-of-two). */
-int mpc3_rss_avgpool(const uint32_t* rk3, uint64_t j_rho, uint64_t j_r, int bits, uint64_t mulc,
+int mpc3_rss_avgpool(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_rho, uint64_t j_r, int bits, uint64_t mulc,
                      const uint64_t* x, uint64_t* out, int64_t N, int64_t C, int64_t H, int64_t W,
                      int kh, int kw, int sh, int sw, void* stream);
 
 /* avgpool backward (nn.py:487-499): scatter-add of g into the windows, then
  * div_area (truncate / mul_const+truncate) — fused. g: (N,C,OH,OW) trio;
  * out: (N,C,H,W) trio. */
-int mpc3_rss_avgpool_backward(const uint32_t* rk3, uint64_t j_rho, uint64_t j_r, int bits, uint64_t mulc,
+int mpc3_rss_avgpool_backward(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_rho, uint64_t j_r, int bits, uint64_t mulc,
                               const uint64_t* g, uint64_t* out, int64_t N, int64_t C, int64_t H,
                               int64_t W, int64_t OH, int64_t OW, int kh, int kw, int sh, int sw,
                               void* stream);

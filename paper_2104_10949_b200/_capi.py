@@ -35,6 +35,7 @@ MODE_A2B, MODE_MSB, MODE_DRELU, MODE_RELU = 0, 1, 2, 3
 class View4(C.Structure):
     _fields_ = [
         ("full", C.c_int64 * 4),
+        ("origin", C.c_int64 * 4),
         ("crop", C.c_int64 * 4),
         ("z_stride", C.c_int64 * 4),
         ("out_stride", C.c_int64 * 4),
@@ -51,13 +52,17 @@ class Operand(C.Structure):
     _fields_ = [("mode", C.c_int)] + _fields_
 
 
-def make_view(full, crop=None, z_stride=None, out_stride=None, z_plane=None, out_plane=None) -> View4:
+def make_view(full, crop=None, z_stride=None, out_stride=None, z_plane=None, out_plane=None,
+              origin=None) -> View4:
     full = [int(v) for v in full]
     while len(full) < 4:
         full.insert(0, 1)
     crop = full if crop is None else [int(v) for v in crop]
     while len(crop) < 4:
         crop.insert(0, 1)
+    org = [0, 0, 0, 0] if origin is None else [int(v) for v in origin]
+    while len(org) < 4:
+        org.insert(0, 0)
 
     def cstrides(shape):
         s, acc = [0] * 4, 1
@@ -76,6 +81,7 @@ def make_view(full, crop=None, z_stride=None, out_stride=None, z_plane=None, out
     n_crop = crop[0] * crop[1] * crop[2] * crop[3]
     v = View4()
     v.full[:] = full
+    v.origin[:] = org
     v.crop[:] = crop
     v.z_stride[:] = zs
     v.out_stride[:] = os_
@@ -119,19 +125,19 @@ _SIGS = {
     "mpc3_last_error": (C.c_char_p, []),
     "mpc3_aes128_expand": (C.c_int, [C.c_char_p, _P]),
     "mpc3_prf_words": (C.c_int, [_P, C.c_uint32, _U64, _U64, _U64, _P, _P]),
-    "mpc3_rss_zero_share": (C.c_int, [_P, C.c_uint32, _U64, C.c_int, _U64, _P, _P]),
+    "mpc3_rss_zero_share": (C.c_int, [_P, _P, C.c_uint32, _U64, C.c_int, _U64, _P, _P]),
     "mpc3_ring_ew": (C.c_int, [C.c_int, _P, _P, _U64, _P, _U64, _P]),
     "mpc3_ring_rowop": (C.c_int, [C.c_int, _P, _P, _P, _U64, _U64, _P]),
     "mpc3_ring_rowsum": (C.c_int, [_P, _P, _U64, _U64, _P]),
-    "mpc3_rss_mul": (C.c_int, [_P, _U64, _P, _P, _P, _U64, _P]),
-    "mpc3_rss_truncate": (C.c_int, [_P, _U64, _U64, C.c_int, _P, _P, _U64, _P]),
-    "mpc3_rss_mul_truncate": (C.c_int, [_P, _U64, _U64, _U64, C.c_int, _P, _P, _P, _U64, _P]),
-    "mpc3_rss_sign": (C.c_int, [_P, C.c_int, _U64, _U64, _U64, _P, _P, _P, _U64, _U64, _U64, _P]),
-    "mpc3_rss_bit_inject": (C.c_int, [_P, _U64, _P, _P, _U64, _P]),
-    "mpc3_rss_reshare_truncate": (C.c_int, [_P, _U64, _U64, _U64, C.c_int, _P, C.POINTER(View4), _P, _P]),
-    "mpc3_rss_avgpool": (C.c_int, [_P, _U64, _U64, C.c_int, _U64, _P, _P, _I64, _I64, _I64, _I64,
+    "mpc3_rss_mul": (C.c_int, [_P, _P, _U64, _P, _P, _P, _U64, _P]),
+    "mpc3_rss_truncate": (C.c_int, [_P, _P, _U64, _U64, C.c_int, _P, _P, _U64, _P]),
+    "mpc3_rss_mul_truncate": (C.c_int, [_P, _P, _U64, _U64, _U64, C.c_int, _P, _P, _P, _U64, _P]),
+    "mpc3_rss_sign": (C.c_int, [_P, _P, C.c_int, _U64, _U64, _U64, _P, _P, _P, _U64, _U64, _U64, _P]),
+    "mpc3_rss_bit_inject": (C.c_int, [_P, _P, _U64, _P, _P, _U64, _P]),
+    "mpc3_rss_reshare_truncate": (C.c_int, [_P, _P, _U64, _U64, _U64, C.c_int, _P, C.POINTER(View4), _P, _P]),
+    "mpc3_rss_avgpool": (C.c_int, [_P, _P, _U64, _U64, C.c_int, _U64, _P, _P, _I64, _I64, _I64, _I64,
                                    C.c_int, C.c_int, C.c_int, C.c_int, _P]),
-    "mpc3_rss_avgpool_backward": (C.c_int, [_P, _U64, _U64, C.c_int, _U64, _P, _P, _I64, _I64, _I64, _I64,
+    "mpc3_rss_avgpool_backward": (C.c_int, [_P, _P, _U64, _U64, C.c_int, _U64, _P, _P, _I64, _I64, _I64, _I64,
                                             _I64, _I64, C.c_int, C.c_int, C.c_int, C.c_int, _P]),
     "mpc3_ring_sumpool": (C.c_int, [_P, _P, _I64, _I64, _I64, _I64, C.c_int, C.c_int, C.c_int, C.c_int, _P]),
     "mpc3_ring_pack": (C.c_int, [_P, _I64, C.POINTER(Operand), C.c_int, _P, _I64, _P]),

@@ -18,6 +18,23 @@ void set_last_error(const char* msg) {
 
 constexpr int kThreads = 256;
 
+// Stream counters may be offset by a device-resident per-purpose base
+// (ctr[purpose], nullable) so a captured CUDA graph advances its PRF counters
+// on every replay exactly as the sequential schedule would.
+struct StreamRef {
+  uint32_t purpose;
+  uint64_t j;
+};
+DEV StreamHead resolve(StreamRef r, const uint64_t* __restrict__ ctr) {
+  return stream_head(r.purpose, r.j + (ctr ? ctr[r.purpose] : 0));
+}
+HD StreamRef sref(uint32_t purpose, uint64_t j) {
+  StreamRef r;
+  r.purpose = purpose;
+  r.j = j;
+  return r;
+}
+
 #define GRID_LOOP(var, count) \
   for (uint64_t var = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; var < (count); \
        var += (uint64_t)gridDim.x * blockDim.x)
@@ -35,9 +52,10 @@ __global__ void __launch_bounds__(kThreads) prf_words_kernel(const uint32_t* __r
 }
 
 __global__ void __launch_bounds__(kThreads) zero_share_kernel(const uint32_t* __restrict__ rk3,
-                                                             StreamHead h, int xor_mode, uint64_t n,
-                                                             uint64_t* __restrict__ out) {
+                                                             const uint64_t* __restrict__ ctr, StreamRef rh,
+                                                             int xor_mode, uint64_t n, uint64_t* __restrict__ out) {
   __shared__ AesSmem sm;
+  StreamHead h = resolve(rh, ctr);
   SmemTables tab = aes_smem_init(sm, rk3, 3);
   GRID_LOOP(b, (n + 1) >> 1) zero_share_item(tab, &sm.rk[0][0], h, xor_mode, n, out, b);
 }
@@ -86,53 +104,64 @@ __global__ void ring_rowsum_kernel(const uint64_t* __restrict__ a, uint64_t* __r
 // protocols
 
 __global__ void __launch_bounds__(kThreads) arith_kernel(int kind, const uint32_t* __restrict__ rk3,
-                                                        StreamHead ha, StreamHead hrho, StreamHead hr,
-                                                        int bits, const uint64_t* __restrict__ x,
+                                                        const uint64_t* __restrict__ ctr, StreamRef ra,
+                                                        StreamRef rrho, StreamRef rr, int bits, const uint64_t* __restrict__ x,
                                                         const uint64_t* __restrict__ y,
                                                         uint64_t* __restrict__ out, uint64_t n) {
   __shared__ AesSmem sm;
   SmemTables tab = aes_smem_init(sm, rk3, 3);
+  StreamHead ha = resolve(ra, ctr), hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
   GRID_LOOP(b, (n + 1) >> 1) arith_item(tab, &sm.rk[0][0], kind, ha, hrho, hr, bits, x, y, out, n, b);
 }
 
 struct SignArgs {
-  SignStreams st;
+  uint64_t jbin, jxor, ja;
 };
 
-__global__ void __launch_bounds__(kThreads) sign_kernel(const uint32_t* __restrict__ rk3, SignArgs args,
+__global__ void __launch_bounds__(kThreads) sign_kernel(const uint32_t* __restrict__ rk3,
+                                                       const uint64_t* __restrict__ ctr, SignArgs args,
                                                        int mode, const uint64_t* __restrict__ x,
                                                        uint64_t* __restrict__ out,
                                                        uint64_t* __restrict__ mask, uint64_t n,
                                                        uint64_t n_total, uint64_t elem_off) {
   __shared__ AesSmem sm;
   SmemTables tab = aes_smem_init(sm, rk3, 3);
-  GRID_LOOP(b, (n + 1) >> 1) sign_item(tab, &sm.rk[0][0], args.st, mode, x, out, mask, n, n_total, elem_off, b);
+  SignStreams st;
+  st.bin = resolve(sref(BIN_INPUT, args.jbin), ctr);
+  for (int l = 0; l < 7; ++l) st.x[l] = resolve(sref(XOR_ZERO, args.jxor + l), ctr);
+  for (int l = 0; l < 3; ++l) st.a[l] = resolve(sref(ARITH_ZERO, args.ja + l), ctr);
+  GRID_LOOP(b, (n + 1) >> 1) sign_item(tab, &sm.rk[0][0], st, mode, x, out, mask, n, n_total, elem_off, b);
 }
 
-__global__ void __launch_bounds__(kThreads) inject_kernel(const uint32_t* __restrict__ rk3, StreamHead a0,
-                                                         StreamHead a1, const uint64_t* __restrict__ bits,
+__global__ void __launch_bounds__(kThreads) inject_kernel(const uint32_t* __restrict__ rk3,
+                                                         const uint64_t* __restrict__ ctr, StreamRef r0,
+                                                         StreamRef r1, const uint64_t* __restrict__ bits,
                                                          uint64_t* __restrict__ out, uint64_t n) {
   __shared__ AesSmem sm;
   SmemTables tab = aes_smem_init(sm, rk3, 3);
+  StreamHead a0 = resolve(r0, ctr), a1 = resolve(r1, ctr);
   GRID_LOOP(b, (n + 1) >> 1) inject_item(tab, &sm.rk[0][0], a0, a1, bits, out, n, b);
 }
 
 __global__ void __launch_bounds__(kThreads) reshare_trunc_kernel(const uint32_t* __restrict__ rk3,
-                                                                StreamHead ha, StreamHead hrho,
-                                                                StreamHead hr, int bits,
+                                                                const uint64_t* __restrict__ ctr, StreamRef ra,
+                                                                StreamRef rrho, StreamRef rr, int bits,
                                                                 const uint64_t* __restrict__ z, View4 v,
                                                                 uint64_t* __restrict__ out, uint64_t n) {
   __shared__ AesSmem sm;
   SmemTables tab = aes_smem_init(sm, rk3, 3);
+  StreamHead ha = resolve(ra, ctr), hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
   GRID_LOOP(b, (n + 1) >> 1) reshare_trunc_item(tab, &sm.rk[0][0], ha, hrho, hr, bits, z, v, out, n, b);
 }
 
-__global__ void __launch_bounds__(kThreads) pool_kernel(const uint32_t* __restrict__ rk3, int backward,
-                                                       StreamHead hrho, StreamHead hr, int bits, uint64_t mulc,
+__global__ void __launch_bounds__(kThreads) pool_kernel(const uint32_t* __restrict__ rk3,
+                                                       const uint64_t* __restrict__ ctr, int backward,
+                                                       StreamRef rrho, StreamRef rr, int bits, uint64_t mulc,
                                                        const uint64_t* __restrict__ x,
                                                        uint64_t* __restrict__ out, PoolGeom p, uint64_t n) {
   __shared__ AesSmem sm;
   SmemTables tab = aes_smem_init(sm, rk3, 3);
+  StreamHead hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
   GRID_LOOP(b, (n + 1) >> 1) pool_item(tab, &sm.rk[0][0], backward != 0, hrho, hr, bits, mulc, x, out, p, b);
 }
 
@@ -197,13 +226,13 @@ int mpc3_prf_words(const uint32_t* rk, uint32_t purpose, uint64_t index, uint64_
   return check_launch("prf_words");
 }
 
-int mpc3_rss_zero_share(const uint32_t* rk3, uint32_t purpose, uint64_t index, int xor_mode, uint64_t n,
+int mpc3_rss_zero_share(const uint32_t* rk3, const uint64_t* ctr, uint32_t purpose, uint64_t index, int xor_mode, uint64_t n,
                         uint64_t* out, void* stream) {
   int st = check_stream_args(purpose, index);
   if (st) return st;
   if (n == 0) return MPC3_OK;
   zero_share_kernel<<<grid_for((n + 1) / 2, kThreads), kThreads, 0, as_stream(stream)>>>(
-      rk3, stream_head(purpose, index), xor_mode, n, out);
+      rk3, ctr, sref(purpose, index), xor_mode, n, out);
   return check_launch("zero_share");
 }
 
@@ -229,33 +258,32 @@ int mpc3_ring_rowsum(const uint64_t* a, uint64_t* out, uint64_t rows, uint64_t c
   return check_launch("ring_rowsum");
 }
 
-static int arith_launch(int kind, const uint32_t* rk3, uint64_t ja, uint64_t jrho, uint64_t jr, int bits,
+static int arith_launch(int kind, const uint32_t* rk3, const uint64_t* ctr, uint64_t ja, uint64_t jrho, uint64_t jr, int bits,
                         const uint64_t* x, const uint64_t* y, uint64_t* out, uint64_t n, void* stream) {
   if (kind != 0 && (bits < 1 || bits > 61)) return MPC3_ERR_RANGE;  // protocols.py:185-186
   if (ja >= (1ull << 48) || jrho >= (1ull << 48) || jr >= (1ull << 48)) return MPC3_ERR_RANGE;
   if (n == 0) return MPC3_OK;
   arith_kernel<<<grid_for((n + 1) / 2, kThreads), kThreads, 0, as_stream(stream)>>>(
-      kind, rk3, stream_head(ARITH_ZERO, ja), stream_head(TRUNC_RHO, jrho), stream_head(TRUNC_R, jr), bits,
-      x, y, out, n);
+      kind, rk3, ctr, sref(ARITH_ZERO, ja), sref(TRUNC_RHO, jrho), sref(TRUNC_R, jr), bits, x, y, out, n);
   return check_launch("rss_arith");
 }
 
-int mpc3_rss_mul(const uint32_t* rk3, uint64_t j_arith, const uint64_t* x, const uint64_t* y, uint64_t* out,
+int mpc3_rss_mul(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, const uint64_t* x, const uint64_t* y, uint64_t* out,
                  uint64_t n, void* stream) {
-  return arith_launch(0, rk3, j_arith, 0, 0, 0, x, y, out, n, stream);
+  return arith_launch(0, rk3, ctr, j_arith, 0, 0, 0, x, y, out, n, stream);
 }
 
-int mpc3_rss_truncate(const uint32_t* rk3, uint64_t j_rho, uint64_t j_r, int bits, const uint64_t* x,
+int mpc3_rss_truncate(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_rho, uint64_t j_r, int bits, const uint64_t* x,
                       uint64_t* out, uint64_t n, void* stream) {
-  return arith_launch(1, rk3, 0, j_rho, j_r, bits, x, nullptr, out, n, stream);
+  return arith_launch(1, rk3, ctr, 0, j_rho, j_r, bits, x, nullptr, out, n, stream);
 }
 
-int mpc3_rss_mul_truncate(const uint32_t* rk3, uint64_t j_arith, uint64_t j_rho, uint64_t j_r, int bits,
+int mpc3_rss_mul_truncate(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, uint64_t j_rho, uint64_t j_r, int bits,
                           const uint64_t* x, const uint64_t* y, uint64_t* out, uint64_t n, void* stream) {
-  return arith_launch(2, rk3, j_arith, j_rho, j_r, bits, x, y, out, n, stream);
+  return arith_launch(2, rk3, ctr, j_arith, j_rho, j_r, bits, x, y, out, n, stream);
 }
 
-int mpc3_rss_sign(const uint32_t* rk3, int mode, uint64_t j_bin, uint64_t j_xor, uint64_t j_arith,
+int mpc3_rss_sign(const uint32_t* rk3, const uint64_t* ctr, int mode, uint64_t j_bin, uint64_t j_xor, uint64_t j_arith,
                   const uint64_t* x, uint64_t* out, uint64_t* mask, uint64_t n, uint64_t n_total,
                   uint64_t elem_off, void* stream) {
   if (mode < MODE_A2B || mode > MODE_RELU) return MPC3_ERR_CONFIG;
@@ -265,24 +293,24 @@ int mpc3_rss_sign(const uint32_t* rk3, int mode, uint64_t j_bin, uint64_t j_xor,
     return MPC3_ERR_RANGE;
   if (n == 0) return MPC3_OK;
   SignArgs a;
-  a.st.bin = stream_head(BIN_INPUT, j_bin);
-  for (int l = 0; l < 7; ++l) a.st.x[l] = stream_head(XOR_ZERO, j_xor + l);
-  for (int l = 0; l < 3; ++l) a.st.a[l] = stream_head(ARITH_ZERO, j_arith + l);
+  a.jbin = j_bin;
+  a.jxor = j_xor;
+  a.ja = j_arith;
   sign_kernel<<<grid_for((n + 1) / 2, kThreads, 16), kThreads, 0, as_stream(stream)>>>(
-      rk3, a, mode, x, out, mask, n, n_total, elem_off);
+      rk3, ctr, a, mode, x, out, mask, n, n_total, elem_off);
   return check_launch("rss_sign");
 }
 
-int mpc3_rss_bit_inject(const uint32_t* rk3, uint64_t j_arith, const uint64_t* bits, uint64_t* out,
+int mpc3_rss_bit_inject(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, const uint64_t* bits, uint64_t* out,
                         uint64_t n, void* stream) {
   if (j_arith + 1 >= (1ull << 48)) return MPC3_ERR_RANGE;
   if (n == 0) return MPC3_OK;
   inject_kernel<<<grid_for((n + 1) / 2, kThreads), kThreads, 0, as_stream(stream)>>>(
-      rk3, stream_head(ARITH_ZERO, j_arith), stream_head(ARITH_ZERO, j_arith + 1), bits, out, n);
+      rk3, ctr, sref(ARITH_ZERO, j_arith), sref(ARITH_ZERO, j_arith + 1), bits, out, n);
   return check_launch("rss_bit_inject");
 }
 
-int mpc3_rss_reshare_truncate(const uint32_t* rk3, uint64_t j_arith, uint64_t j_rho, uint64_t j_r, int bits,
+int mpc3_rss_reshare_truncate(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, uint64_t j_rho, uint64_t j_r, int bits,
                               const uint64_t* z, const mpc3_view4* view, uint64_t* out, void* stream) {
   if (bits != 0 && (bits < 1 || bits > 61)) return MPC3_ERR_RANGE;
   if (!view) return MPC3_ERR_CONFIG;
@@ -290,18 +318,18 @@ int mpc3_rss_reshare_truncate(const uint32_t* rk3, uint64_t j_arith, uint64_t j_
   uint64_t n = 1;
   for (int k = 0; k < 4; ++k) {
     v.full[k] = view->full[k];
+    v.org[k] = view->origin[k];
     v.crop[k] = view->crop[k];
     v.zs[k] = view->z_stride[k];
     v.os[k] = view->out_stride[k];
-    if (v.crop[k] > v.full[k] || v.full[k] < 0 || v.crop[k] < 0) return MPC3_ERR_SHAPE;
+    if (v.org[k] < 0 || v.full[k] < 0 || v.crop[k] < 0) return MPC3_ERR_SHAPE;
     n *= (uint64_t)v.full[k];
   }
   v.zp = view->z_plane;
   v.op = view->out_plane;
   if (n == 0) return MPC3_OK;
   reshare_trunc_kernel<<<grid_for((n + 1) / 2, kThreads), kThreads, 0, as_stream(stream)>>>(
-      rk3, stream_head(ARITH_ZERO, j_arith), stream_head(TRUNC_RHO, j_rho), stream_head(TRUNC_R, j_r), bits,
-      z, v, out, n);
+      rk3, ctr, sref(ARITH_ZERO, j_arith), sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, z, v, out, n);
   return check_launch("rss_reshare_truncate");
 }
 
@@ -313,7 +341,7 @@ static PoolGeom pool_geom(int64_t N, int64_t C, int64_t H, int64_t W, int64_t OH
   return p;
 }
 
-int mpc3_rss_avgpool(const uint32_t* rk3, uint64_t j_rho, uint64_t j_r, int bits, uint64_t mulc,
+int mpc3_rss_avgpool(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_rho, uint64_t j_r, int bits, uint64_t mulc,
                      const uint64_t* x, uint64_t* out, int64_t N, int64_t C, int64_t H, int64_t W, int kh,
                      int kw, int sh, int sw, void* stream) {
   if (bits < 1 || bits > 61) return MPC3_ERR_RANGE;
@@ -322,12 +350,12 @@ int mpc3_rss_avgpool(const uint32_t* rk3, uint64_t j_rho, uint64_t j_r, int bits
   uint64_t n = (uint64_t)N * C * OH * OW;
   if (n == 0) return MPC3_OK;
   pool_kernel<<<grid_for((n + 1) / 2, kThreads), kThreads, 0, as_stream(stream)>>>(
-      rk3, 0, stream_head(TRUNC_RHO, j_rho), stream_head(TRUNC_R, j_r), bits, mulc, x, out,
+      rk3, ctr, 0, sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, mulc, x, out,
       pool_geom(N, C, H, W, OH, OW, kh, kw, sh, sw), n);
   return check_launch("rss_avgpool");
 }
 
-int mpc3_rss_avgpool_backward(const uint32_t* rk3, uint64_t j_rho, uint64_t j_r, int bits, uint64_t mulc,
+int mpc3_rss_avgpool_backward(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_rho, uint64_t j_r, int bits, uint64_t mulc,
                               const uint64_t* g, uint64_t* out, int64_t N, int64_t C, int64_t H, int64_t W,
                               int64_t OH, int64_t OW, int kh, int kw, int sh, int sw, void* stream) {
   if (bits < 1 || bits > 61) return MPC3_ERR_RANGE;
@@ -335,7 +363,7 @@ int mpc3_rss_avgpool_backward(const uint32_t* rk3, uint64_t j_rho, uint64_t j_r,
   uint64_t n = (uint64_t)N * C * H * W;
   if (n == 0) return MPC3_OK;
   pool_kernel<<<grid_for((n + 1) / 2, kThreads), kThreads, 0, as_stream(stream)>>>(
-      rk3, 1, stream_head(TRUNC_RHO, j_rho), stream_head(TRUNC_R, j_r), bits, mulc, g, out,
+      rk3, ctr, 1, sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, mulc, g, out,
       pool_geom(N, C, H, W, OH, OW, kh, kw, sh, sw), n);
   return check_launch("rss_avgpool_backward");
 }

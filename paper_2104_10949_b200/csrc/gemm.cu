@@ -321,7 +321,7 @@ static Operand to_operand(const mpc3_operand* o) {
   p.t1 = o->t1;
   p.t2 = o->t2;
   p.K1 = o->K1 > 0 ? o->K1 : 1;
-  p.K2 = o->K2 > 0 ? o->K2 : 1;
+  p.K2 = o->K2 > 0 ? o->K2 : (o->k > 0 ? o->k : 1);  // default: K is one digit of stride t2
   p.n = o->n;
   p.c = o->c;
   p.h = o->h;

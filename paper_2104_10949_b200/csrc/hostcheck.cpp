@@ -73,6 +73,7 @@ void hc_reshare_truncate(const uint8_t* keys48, uint64_t ja, uint64_t jrho, uint
   uint64_t n = 1;
   for (int k = 0; k < 4; ++k) {
     v.full[k] = view->full[k];
+    v.org[k] = view->origin[k];
     v.crop[k] = view->crop[k];
     v.zs[k] = view->z_stride[k];
     v.os[k] = view->out_stride[k];
@@ -103,7 +104,7 @@ void hc_pack(const uint64_t* src, int64_t plane, const mpc3_operand* op, int rol
   Operand o;
   memset(&o, 0, sizeof(o));
   o.mode = op->mode; o.rows = op->rows; o.k = op->k; o.off = op->off; o.s_r = op->s_r;
-  o.t0 = op->t0; o.t1 = op->t1; o.t2 = op->t2; o.K1 = op->K1 > 0 ? op->K1 : 1; o.K2 = op->K2 > 0 ? op->K2 : 1;
+  o.t0 = op->t0; o.t1 = op->t1; o.t2 = op->t2; o.K1 = op->K1 > 0 ? op->K1 : 1; o.K2 = op->K2 > 0 ? op->K2 : (op->k > 0 ? op->k : 1);
   o.n = op->n; o.c = op->c; o.h = op->h; o.w = op->w; o.sN = op->sN; o.sC = op->sC; o.sH = op->sH; o.sW = op->sW;
   o.kh = op->kh > 0 ? op->kh : 1; o.kw = op->kw > 0 ? op->kw : 1; o.sh = op->sh > 0 ? op->sh : 1;
   o.sw = op->sw > 0 ? op->sw : 1; o.ph = op->ph; o.pw = op->pw; o.dh = op->dh > 0 ? op->dh : 1;

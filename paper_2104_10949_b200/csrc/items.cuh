@@ -103,7 +103,7 @@ HD void inject_item(const T& tab, const uint32_t* rk3, StreamHead a0, StreamHead
 }
 
 struct View4 {
-  int64_t full[4], crop[4], zs[4], os[4], zp, op;
+  int64_t full[4], org[4], crop[4], zs[4], os[4], zp, op;
 };
 
 template <class T>
@@ -121,8 +121,13 @@ HD void reshare_trunc_item(const T& tab, const uint32_t* rk3, StreamHead ha, Str
     r /= v.full[2];
     int64_t i1 = r % v.full[1];
     int64_t i0 = r / v.full[1];
-    ok[e] = ok[e] && i0 < v.crop[0] && i1 < v.crop[1] && i2 < v.crop[2] && i3 < v.crop[3];
     zoff[e] = i0 * v.zs[0] + i1 * v.zs[1] + i2 * v.zs[2] + i3 * v.zs[3];
+    i0 -= v.org[0];
+    i1 -= v.org[1];
+    i2 -= v.org[2];
+    i3 -= v.org[3];
+    ok[e] = ok[e] && i0 >= 0 && i1 >= 0 && i2 >= 0 && i3 >= 0 && i0 < v.crop[0] && i1 < v.crop[1] &&
+            i2 < v.crop[2] && i3 < v.crop[3];
     ooff[e] = i0 * v.os[0] + i1 * v.os[1] + i2 * v.os[2] + i3 * v.os[3];
   }
   if (!ok[0] && !ok[1]) return;

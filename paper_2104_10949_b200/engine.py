@@ -1,0 +1,703 @@
+"""The trio engine: all three RSS parties co-resident on one B200.
+
+A shared tensor (`RssTensor`) is ONE device buffer of shape (3, *shape),
+int64 bit-cast of the three additive components c0, c1, c2; party i's
+replicated share (lo, hi) is (c_i, c_{i+1}) (sharing.py:37-49).  Every
+protocol of the reference (protocols.py:57-468) runs as fused CUDA kernels
+over the trio: the local cross terms of all three parties, the PRF zero
+shares (AES-CTR generated inline, bit-exact with prf.py:40-49) and the
+"messages" (register / HBM handoffs) in one launch per protocol call, with
+the reference's lockstep per-purpose counters (sharing.py:225-230) kept on
+the host.  Communication is charged analytically into per-party CommStats
+with the reference's byte and round accounting.
+
+There is no CPU path: every compute call goes through libmpc3b200.so.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _capi as K
+from .errors import ConfigError, FreshnessError, RangeError, ShapeError
+from .prf import (
+    PURPOSE_ARITH_ZERO as ARITH,
+    PURPOSE_BIN_INPUT as BIN,
+    PURPOSE_TRUNC_R as TR_R,
+    PURPOSE_TRUNC_RHO as TR_RHO,
+    PURPOSE_XOR_ZERO as XOR,
+    PURPOSES,
+    PrfKey,
+    derive_key,
+)
+from .ring import DEFAULT_FP, FixedPointConfig, as_ring, check_accumulation, fx_encode
+from .transport import Ledger
+
+U64 = np.uint64
+MAX_SPLIT_K = 16384  # per-split K bound of the int8-limb GEMM (exactness of S_3)
+SMS = 148
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _dev():
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def to_device(a: np.ndarray) -> torch.Tensor:
+    """Host uint64 array -> device int64 tensor (bit-cast)."""
+    a = np.ascontiguousarray(np.asarray(a, dtype=U64))
+    return torch.from_numpy(a.view(np.int64)).to(_dev(), non_blocking=False)
+
+
+def to_host(t: torch.Tensor) -> np.ndarray:
+    return t.detach().contiguous().cpu().numpy().view(U64)
+
+
+def _round_up(v: int, m: int) -> int:
+    return (v + m - 1) // m * m
+
+
+# ---------------------------------------------------------------------------
+# shared tensors
+
+
+class RssTensor:
+    """Three components of a replicated sharing in one (3, *shape) buffer."""
+
+    __slots__ = ("data", "fp")
+
+    def __init__(self, data: torch.Tensor, fp: FixedPointConfig = DEFAULT_FP):
+        if data.dtype != torch.int64 or data.dim() < 1 or data.shape[0] != 3:
+            raise ShapeError("RssTensor data must be int64 of shape (3, ...)")
+        self.data = data
+        self.fp = fp
+
+    @property
+    def shape(self) -> tuple:
+        return tuple(self.data.shape[1:])
+
+    @property
+    def ndim(self) -> int:
+        return self.data.dim() - 1
+
+    @property
+    def numel(self) -> int:
+        return int(np.prod(self.shape, dtype=np.int64)) if self.shape else 1
+
+    def contiguous(self) -> "RssTensor":
+        return self if self.data.is_contiguous() else RssTensor(self.data.contiguous(), self.fp)
+
+    def reshape(self, *shape) -> "RssTensor":
+        if len(shape) == 1 and isinstance(shape[0], (tuple, list)):
+            shape = tuple(shape[0])
+        return RssTensor(self.data.reshape((3,) + tuple(shape)), self.fp)
+
+    def apply(self, f) -> "RssTensor":
+        """Structural (per-component) transform f on the (3, ...) buffer."""
+        return RssTensor(f(self.data), self.fp)
+
+    def __getitem__(self, idx) -> "RssTensor":
+        if not isinstance(idx, tuple):
+            idx = (idx,)
+        return RssTensor(self.data[(slice(None),) + idx], self.fp)
+
+    def comp(self, i: int) -> torch.Tensor:
+        return self.data[i]
+
+    def __repr__(self):
+        return f"RssTensor(shape={self.shape}, device={self.data.device})"
+
+
+def empty(shape, fp=DEFAULT_FP) -> RssTensor:
+    return RssTensor(torch.empty((3,) + tuple(shape), dtype=torch.int64, device=_dev()), fp)
+
+
+def zeros(shape, fp=DEFAULT_FP) -> RssTensor:
+    return RssTensor(torch.zeros((3,) + tuple(shape), dtype=torch.int64, device=_dev()), fp)
+
+
+def _flat(t: RssTensor) -> torch.Tensor:
+    return t.data if t.data.is_contiguous() else t.data.contiguous()
+
+
+# ---------------------------------------------------------------------------
+# session
+
+
+def make_session_id(seed):
+    import hashlib
+    import os
+
+    if seed is None:
+        return os.urandom(16)
+    return hashlib.sha256(f"mpc3-session|{seed}".encode()).digest()[:16]
+
+
+def session_keys(seed, session_id=None) -> list[PrfKey]:
+    """k_0, k_1, k_2 exactly as the reference's seeded setup (session.py:43-59)."""
+    import os
+
+    sid = session_id if session_id is not None else make_session_id(seed)
+    if seed is None:
+        return [PrfKey(os.urandom(16)) for _ in range(3)]
+    return [derive_key(f"seed{seed}".encode(), sid, f"party{i}") for i in range(3)]
+
+
+@dataclass(frozen=True)
+class ExpConfig:
+    """e^x ~ (1 + x/m)^m (protocols.py:387-399)."""
+
+    m: int = 512
+
+    def __post_init__(self):
+        if self.m < 2 or self.m & (self.m - 1):
+            raise ConfigError(f"m={self.m} must be a power of two >= 2")
+
+    @property
+    def squarings(self) -> int:
+        return self.m.bit_length() - 1
+
+
+@dataclass(frozen=True)
+class ReciprocalConfig:
+    """Newton 1/y on [1, Y] from z0 = 1/Y (protocols.py:402-411)."""
+
+    Y: float = 200.0
+    iterations: int = 13
+
+    def __post_init__(self):
+        if self.Y < 1 or self.iterations < 0:
+            raise ConfigError("need Y >= 1 and iterations >= 0")
+
+
+class TrioSession:
+    """Keys, lockstep PRF counters and communication ledger of one 3-party
+    session whose parties are co-resident on the current CUDA device."""
+
+    def __init__(self, seed: int | None = 0, fp: FixedPointConfig = DEFAULT_FP, session_id: bytes | None = None,
+                 keys: list[PrfKey] | None = None):
+        self.fp = fp
+        self.seed = seed
+        self.session_id = session_id if session_id is not None else make_session_id(seed)
+        self.keys = keys if keys is not None else session_keys(seed, self.session_id)
+        rk = np.stack([k.round_keys for k in self.keys])
+        self.rk3 = torch.from_numpy(rk.view(np.int32).copy()).to(_dev())
+        self.seq = {p: 0 for p in PURPOSES}
+        self.ledger = Ledger()
+        self.ctr = None  # optional device per-purpose counter base (CUDA-graph replay)
+        self._pool = {}
+
+    # -- counters (sharing.py:190-204, 225-230) --
+    def take(self, purpose: int, count: int = 1) -> int:
+        j = self.seq[purpose]
+        if j + count > (1 << 48):
+            raise FreshnessError(f"stream counters for purpose {purpose:#06x} exhausted")
+        self.seq[purpose] = j + count
+        return j
+
+    def counters(self) -> dict:
+        return dict(self.seq)
+
+    def rewind(self, seq: dict) -> None:
+        """Counters only move forward; a rewind would reuse PRF streams."""
+        for p, j in seq.items():
+            if j < self.seq[p]:
+                raise FreshnessError(f"counter {j} already used for purpose {p:#06x}")
+        self.seq.update(seq)
+
+    @property
+    def ctr_ptr(self):
+        return None if self.ctr is None else self.ctr.data_ptr()
+
+    @property
+    def rk(self) -> int:
+        return self.rk3.data_ptr()
+
+    # -- host boundary (session.py:62-91, 116-121; sharing.py:113-155) --
+    def share(self, x, rng: np.random.Generator, label: str = "share.input", owner: int = 0) -> RssTensor:
+        """Dealer draws c0, c1 ~ rng (numpy, as sharing.py:113-118), c2 = x - c0 - c1;
+        the three components are uploaded as one trio buffer."""
+        x = as_ring(x)
+        c0 = rng.integers(0, 1 << 64, size=x.shape, dtype=U64)
+        c1 = rng.integers(0, 1 << 64, size=x.shape, dtype=U64)
+        comps = np.stack([c0, c1, x - c0 - c1])
+        n = int(x.size)
+        self.ledger.round(label, [(owner, p, 2 * n) for p in range(3) if p != owner])
+        return RssTensor(to_device(comps), self.fp)
+
+    def from_components(self, comps) -> RssTensor:
+        return RssTensor(to_device(np.asarray(comps, U64)), self.fp)
+
+    def reveal(self, x: RssTensor, label: str = "open") -> np.ndarray:
+        """open_share: every party learns c0 + c1 + c2 (session.py:116-121)."""
+        self.ledger.ring(label, x.numel)
+        return to_host(reconstruct_device(x)).reshape(x.shape)
+
+    # -- local ops (protocols.py:57-72, sharing.py:54-67) --
+    def add(self, a, b):
+        return _ew2(K.EW_ADD, a, b)
+
+    def sub(self, a, b):
+        return _ew2(K.EW_SUB, a, b)
+
+    def neg(self, a):
+        out = empty(a.shape, a.fp)
+        K.call("mpc3_ring_ew", K.EW_NEG, _flat(a).data_ptr(), None, 0, out.data.data_ptr(), 3 * a.numel, _stream())
+        return out
+
+    def mul_const(self, a, c: int):
+        out = empty(a.shape, a.fp)
+        K.call("mpc3_ring_ew", K.EW_MULC, _flat(a).data_ptr(), None, int(c) % (1 << 64), out.data.data_ptr(),
+               3 * a.numel, _stream())
+        return out
+
+    def add_const(self, a, c):
+        """Public constant into component 0 (protocols.py:57-62)."""
+        a = a.contiguous()
+        cv = np.broadcast_to(as_ring(c), a.shape)
+        if cv.ndim == 0 or np.all(cv == cv.flat[0]):
+            out = RssTensor(a.data.clone(), a.fp)
+            K.call("mpc3_ring_ew", K.EW_ADDC, a.data.data_ptr(), None, int(cv.flat[0]) if cv.size else 0,
+                   out.data.data_ptr(), a.numel, _stream())
+            return out
+        out = RssTensor(a.data.clone(), a.fp)
+        cd = to_device(np.ascontiguousarray(cv))
+        K.call("mpc3_ring_ew", K.EW_ADD, a.data.data_ptr(), cd.data_ptr(), 0, out.data.data_ptr(), a.numel, _stream())
+        return out
+
+    def sub_from_const(self, c, a):
+        return self.add_const(self.neg(a), c)
+
+    def const_share(self, value, shape) -> RssTensor:
+        """Components (c, 0, 0) (sharing.py:184-187)."""
+        out = zeros(shape, self.fp)
+        out.data[0] = torch.from_numpy(np.broadcast_to(as_ring(value), shape).astype(U64).view(np.int64)).to(_dev())
+        return out
+
+    # -- multiplication (protocols.py:79-94) --
+    def mul(self, x: RssTensor, y: RssTensor, label: str = "mul.reshare") -> RssTensor:
+        x, y = _broadcast(x, y)
+        out = empty(x.shape, x.fp)
+        j = self.take(ARITH)
+        K.call("mpc3_rss_mul", self.rk, self.ctr_ptr, j, x.data.data_ptr(), y.data.data_ptr(), out.data.data_ptr(),
+               x.numel, _stream())
+        self.ledger.ring(label, x.numel)
+        return out
+
+    def truncate(self, x: RssTensor, bits: int | None = None) -> RssTensor:
+        bits = self.fp.t if bits is None else bits
+        if not 1 <= bits <= 61:
+            raise RangeError(f"truncation by {bits} bits outside [1, 61]")
+        x = x.contiguous()
+        out = empty(x.shape, x.fp)
+        jr, jq = self.take(TR_RHO), self.take(TR_R)
+        K.call("mpc3_rss_truncate", self.rk, self.ctr_ptr, jr, jq, bits, x.data.data_ptr(), out.data.data_ptr(),
+               x.numel, _stream())
+        self._charge_trunc(x.numel)
+        return out
+
+    def mul_truncate(self, x, y, bits=None, label="mul.reshare") -> RssTensor:
+        """truncate(mul(x, y)) in one launch; same counters and accounting."""
+        bits = self.fp.t if bits is None else bits
+        if not 1 <= bits <= 61:
+            raise RangeError(f"truncation by {bits} bits outside [1, 61]")
+        x, y = _broadcast(x, y)
+        out = empty(x.shape, x.fp)
+        ja = self.take(ARITH)
+        jr, jq = self.take(TR_RHO), self.take(TR_R)
+        K.call("mpc3_rss_mul_truncate", self.rk, self.ctr_ptr, ja, jr, jq, bits, x.data.data_ptr(),
+               y.data.data_ptr(), out.data.data_ptr(), x.numel, _stream())
+        self.ledger.ring(label, x.numel)
+        self._charge_trunc(x.numel)
+        return out
+
+    def _charge_trunc(self, n):
+        # P0 -> P1 (c0 - rho), then P1 -> P0 (z1); P2 silent (protocols.py:201-216)
+        self.ledger.round("trunc.mask", [(0, 1, n)])
+        self.ledger.round("trunc.open", [(1, 0, n)])
+
+    # -- binary world (protocols.py:223-353) --
+    def _sign(self, x: RssTensor, mode: int):
+        x = x.contiguous()
+        n = x.numel
+        out = empty(x.shape, x.fp)
+        mask = empty(x.shape, x.fp) if mode == K.MODE_RELU else None
+        jb = self.take(BIN)
+        jx = self.take(XOR, 7)
+        ja = self.take(ARITH, [0, 0, 2, 3][mode]) if mode >= K.MODE_DRELU else self.seq[ARITH]
+        K.call("mpc3_rss_sign", self.rk, self.ctr_ptr, mode, jb, jx, ja, x.data.data_ptr(), out.data.data_ptr(),
+               None if mask is None else mask.data.data_ptr(), n, n, 0, _stream())
+        L = self.ledger
+        L.round("share.a2b", [(0, 2, n)])
+        L.ring("and.ks.g", n)
+        for d in (1, 2, 4, 8, 16, 32):
+            L.ring(f"and.ks.{d}", 2 * n)
+        if mode >= K.MODE_DRELU:
+            L.ring("mul.inject", n)
+            L.ring("mul.inject", n)
+        if mode == K.MODE_RELU:
+            L.ring("mul.mask", n)
+        return out, mask
+
+    def a2b(self, x):
+        return self._sign(x, K.MODE_A2B)[0]
+
+    def msb(self, x):
+        return self._sign(x, K.MODE_MSB)[0]
+
+    def drelu(self, x):
+        return self._sign(x, K.MODE_DRELU)[0]
+
+    def relu_with_mask(self, x):
+        return self._sign(x, K.MODE_RELU)
+
+    def relu(self, x):
+        return self._sign(x, K.MODE_RELU)[0]
+
+    def compare(self, x, y):
+        return self.drelu(self.sub(x, y))
+
+    def bit_inject(self, b: RssTensor) -> RssTensor:
+        b = b.contiguous()
+        out = empty(b.shape, b.fp)
+        ja = self.take(ARITH, 2)
+        K.call("mpc3_rss_bit_inject", self.rk, self.ctr_ptr, ja, b.data.data_ptr(), out.data.data_ptr(), b.numel,
+               _stream())
+        self.ledger.ring("mul.inject", b.numel)
+        self.ledger.ring("mul.inject", b.numel)
+        return out
+
+    # -- bilinear layers (protocols.py:97-136, nn.py:435-484) --
+    def _cross_gemm(self, a_src, a_op, b_src, b_op, M, N, Kd) -> torch.Tensor:
+        """z_i = (x_i + x_{i+1}) y_i + x_i y_{i+1} for the three parties, as one
+        batched ring GEMM with inner length 2K (protocols.py:110-115)."""
+        kp = _round_up(2 * Kd, 16)
+        A = torch.empty(3 * 8 * M * kp, dtype=torch.uint8, device=_dev())
+        B = torch.empty(3 * 8 * N * kp, dtype=torch.uint8, device=_dev())
+        st = _stream()
+        K.call("mpc3_ring_pack", a_src.data_ptr(), a_src.stride(0), C.byref(a_op), 0, A.data_ptr(), kp, st)
+        K.call("mpc3_ring_pack", b_src.data_ptr(), b_src.stride(0), C.byref(b_op), 1, B.data_ptr(), kp, st)
+        splits = gemm_splits(M, N, kp, groups=3)
+        z = (torch.zeros if splits > 1 else torch.empty)(3 * M * N, dtype=torch.int64, device=_dev())
+        K.call("mpc3_ring_gemm_packed", A.data_ptr(), B.data_ptr(), z.data_ptr(), 3, M, N, kp, N, M * N, splits, st)
+        return z
+
+    def _finish(self, z, view, out: RssTensor, bits, label):
+        ja = self.take(ARITH)
+        jr = jq = 0
+        if bits:
+            jr, jq = self.take(TR_RHO), self.take(TR_R)
+        K.call("mpc3_rss_reshare_truncate", self.rk, self.ctr_ptr, ja, jr, jq, bits, z.data_ptr(), C.byref(view),
+               out.data.data_ptr(), _stream())
+        full = int(np.prod(view.full))
+        self.ledger.ring(label, full)
+        if bits:
+            self._charge_trunc(full)
+        return out
+
+    def matmul(self, x: RssTensor, y: RssTensor, bits: int | None = None) -> RssTensor:
+        """matmul_shares (protocols.py:97-117): cross terms, reshare, truncate."""
+        if x.ndim != 2 or y.ndim != 2 or x.shape[1] != y.shape[0]:
+            raise ShapeError(f"matmul shapes {x.shape} x {y.shape}")
+        m, k = x.shape
+        n = y.shape[1]
+        check_accumulation(k)
+        bits = self.fp.t if bits is None else bits
+        if not 1 <= bits <= 61:
+            raise RangeError(f"truncation by {bits} bits outside [1, 61]")
+        xs, ys = x.data.stride(), y.data.stride()
+        a_op = K.dense_operand(m, k, s_r=xs[1], t2=xs[2])
+        b_op = K.dense_operand(n, k, s_r=ys[2], t2=ys[1])
+        z = self._cross_gemm(x.data, a_op, y.data, b_op, m, n, k)
+        out = empty((m, n), x.fp)
+        return self._finish(z, K.make_view((1, 1, m, n)), out, bits, "mul.reshare")
+
+    def conv2d(self, x: RssTensor, k: RssTensor, stride=(1, 1), padding=(0, 0), bits=None) -> RssTensor:
+        """conv2d_shares (protocols.py:120-136), NCHW cross-correlation."""
+        if x.ndim != 4 or k.ndim != 4 or x.shape[1] != k.shape[1]:
+            raise ShapeError(f"kernel {k.shape} incompatible with input {x.shape}")
+        nb, c, h, w = x.shape
+        o, _, kh, kw = k.shape
+        sh, sw = stride
+        ph, pw = padding
+        check_accumulation(c * kh * kw)
+        if h + 2 * ph < kh or w + 2 * pw < kw:
+            raise ShapeError("kernel larger than padded input")
+        bits = self.fp.t if bits is None else bits
+        oh, ow = (h + 2 * ph - kh) // sh + 1, (w + 2 * pw - kw) // sw + 1
+        xs, ks = x.data.stride(), k.data.stride()
+        a_op = K.conv_operand(K.GATHER_IM2COL, nb * oh * ow, c * kh * kw, nb, c, h, w, xs[1:], kh, kw, sh, sw, ph, pw,
+                              oh, ow)
+        b_op = K.dense_operand(o, c * kh * kw, s_r=ks[1], t0=ks[2], t1=ks[3], t2=ks[4], K1=kh, K2=kw)
+        z = self._cross_gemm(x.data, a_op, k.data, b_op, nb * oh * ow, o, c * kh * kw)
+        out = empty((nb, o, oh, ow), x.fp)
+        view = K.make_view((nb, o, oh, ow), z_stride=(oh * ow * o, 1, ow * o, o))
+        return self._finish(z, view, out, bits, "mul.reshare")
+
+    def conv2d_wgrad(self, x: RssTensor, g: RssTensor, kernel, stride, padding, bits) -> RssTensor:
+        """Kernel gradient (nn.py:435-457) as one direct implicit GEMM with
+        K = N*OH*OW; the reference's dilated zeros contribute nothing, and the
+        zero shares / truncation words are indexed over its full (C,O,fh,fw)
+        output so the result is bit-exact."""
+        nb, c, h, w = x.shape
+        nb2, o, oh, ow = g.shape
+        kh, kw = kernel
+        sh, sw = stride
+        ph, pw = padding
+        ghd, gwd = (oh - 1) * sh + 1, (ow - 1) * sw + 1
+        check_accumulation(nb * ghd * gwd)
+        if h + 2 * ph < ghd or w + 2 * pw < gwd:
+            raise ShapeError("kernel larger than padded input")
+        fh, fw = h + 2 * ph - ghd + 1, w + 2 * pw - gwd + 1
+        xs, gs = x.data.stride(), g.data.stride()
+        a_op = K.conv_operand(K.GATHER_WGRAD, c * kh * kw, nb * oh * ow, nb, c, h, w, xs[1:], kh, kw, sh, sw, ph, pw,
+                              oh, ow)
+        b_op = K.dense_operand(o, nb * oh * ow, s_r=gs[2], t0=gs[1], t1=gs[3], t2=gs[4], K1=oh, K2=ow)
+        z = self._cross_gemm(x.data, a_op, g.data, b_op, c * kh * kw, o, nb * oh * ow)
+        out = empty((o, c, kh, kw), x.fp)
+        view = K.make_view((c, o, fh, fw), crop=(c, o, kh, kw), z_stride=(kh * kw * o, 1, kw * o, o),
+                           out_stride=(kh * kw, c * kh * kw, kw, 1), z_plane=c * kh * kw * o)
+        return self._finish(z, view, out, bits, "mul.reshare")
+
+    def conv2d_dgrad(self, g: RssTensor, k: RssTensor, stride, padding, in_shape, bits) -> RssTensor:
+        """Input gradient (nn.py:460-484): correlation of the dilated, padded
+        output gradient with the flipped kernel, then the embed/crop."""
+        nb, o, oh, ow = g.shape
+        o2, c, kh, kw = k.shape
+        sh, sw = stride
+        ph, pw = padding
+        h, w = in_shape[-2:]
+        check_accumulation(o * kh * kw)
+        hf, wf = (oh - 1) * sh + kh, (ow - 1) * sw + kw
+        gs, ks = g.data.stride(), k.data.stride()
+        a_op = K.conv_operand(K.GATHER_IM2COL, nb * hf * wf, o * kh * kw, nb, o, oh, ow, gs[1:], kh, kw, 1, 1,
+                              kh - 1, kw - 1, hf, wf, dh=sh, dw=sw)
+        b_op = K.dense_operand(c, o * kh * kw, s_r=ks[2], off=(kh - 1) * ks[3] + (kw - 1) * ks[4], t0=ks[1],
+                               t1=-ks[3], t2=-ks[4], K1=kh, K2=kw)
+        z = self._cross_gemm(g.data, a_op, k.data, b_op, nb * hf * wf, c, o * kh * kw)
+        out = zeros((nb, c, h, w), g.fp)
+        crop = (nb, c, max(0, min(h, hf - ph)), max(0, min(w, wf - pw)))
+        view = K.make_view((nb, c, hf, wf), crop=crop, origin=(0, 0, ph, pw), z_stride=(hf * wf * c, 1, wf * c, c),
+                           out_stride=(c * h * w, h * w, w, 1), out_plane=nb * c * h * w, z_plane=nb * hf * wf * c)
+        return self._finish(z, view, out, bits, "mul.reshare")
+
+    # -- pooling (protocols.py:139-159, nn.py:487-499) --
+    def _area_params(self, area: int):
+        if area & (area - 1) == 0:
+            return area.bit_length() - 1, 1
+        return self.fp.t, int(fx_encode(1.0 / area, self.fp))
+
+    def avgpool(self, x: RssTensor, window, stride=None) -> RssTensor:
+        kh, kw = window
+        sh, sw = stride or window
+        if x.ndim != 4 or x.shape[2] < kh or x.shape[3] < kw:
+            raise ShapeError("window larger than input")
+        x = x.contiguous()
+        nb, c, h, w = x.shape
+        oh, ow = (h - kh) // sh + 1, (w - kw) // sw + 1
+        bits, mulc = self._area_params(kh * kw)
+        out = empty((nb, c, oh, ow), x.fp)
+        jr, jq = self.take(TR_RHO), self.take(TR_R)
+        K.call("mpc3_rss_avgpool", self.rk, self.ctr_ptr, jr, jq, bits, mulc, x.data.data_ptr(), out.data.data_ptr(),
+               nb, c, h, w, kh, kw, sh, sw, _stream())
+        self._charge_trunc(out.numel)
+        return out
+
+    def avgpool_backward(self, g: RssTensor, window, stride, in_shape) -> RssTensor:
+        kh, kw = window
+        sh, sw = stride
+        g = g.contiguous()
+        nb, c, oh, ow = g.shape
+        h, w = in_shape[-2:]
+        bits, mulc = self._area_params(kh * kw)
+        out = empty((nb, c, h, w), g.fp)
+        jr, jq = self.take(TR_RHO), self.take(TR_R)
+        K.call("mpc3_rss_avgpool_backward", self.rk, self.ctr_ptr, jr, jq, bits, mulc, g.data.data_ptr(),
+               out.data.data_ptr(), nb, c, h, w, oh, ow, kh, kw, sh, sw, _stream())
+        self._charge_trunc(out.numel)
+        return out
+
+    def div_area(self, x: RssTensor, area: int) -> RssTensor:
+        bits, mulc = self._area_params(area)
+        if mulc != 1:
+            return self.mul_truncate_const(x, mulc, bits)
+        return self.truncate(x, bits)
+
+    def mul_truncate_const(self, x, c, bits):
+        return self.truncate(self.mul_const(x, c), bits)
+
+    # -- comparisons and function approximations (protocols.py:356-468) --
+    def max_tree(self, v: RssTensor) -> RssTensor:
+        m = v.shape[-1] if v.ndim else 0
+        if m < 1:
+            raise ShapeError("max_tree needs at least one element")
+        while m > 1:
+            k = m // 2
+            a = v.apply(lambda d: d[..., 0:2 * k:2].contiguous())
+            b = v.apply(lambda d: d[..., 1:2 * k:2].contiguous())
+            mx = self.add(b, self.relu(self.sub(a, b)))
+            if m % 2:
+                mx = RssTensor(torch.cat([mx.data, v.data[..., -1:]], dim=-1), v.fp)
+            v = mx
+            m = v.shape[-1]
+        return v.apply(lambda d: d[..., 0].contiguous())
+
+    def exp_approx(self, x: RssTensor, cfg: ExpConfig = ExpConfig()) -> RssTensor:
+        s = cfg.squarings
+        if self.fp.t + 2 * s > 61:
+            raise ConfigError(f"m={cfg.m} too large for t={self.fp.t}")
+        y = self.add_const(x, fx_encode(float(cfg.m), self.fp))
+        y = self.mul_truncate(y, y, self.fp.t + 2 * s)
+        for _ in range(s - 1):
+            y = self.mul_truncate(y, y)
+        return y
+
+    def reciprocal(self, y: RssTensor, cfg: ReciprocalConfig = ReciprocalConfig()) -> RssTensor:
+        z = self.const_share(fx_encode(1.0 / cfg.Y, self.fp), y.shape)
+        for _ in range(cfg.iterations):
+            z2 = self.mul_truncate(z, z)
+            yz2 = self.mul_truncate(y, z2)
+            z = self.sub(self.mul_const(z, 2), yz2)
+        return z
+
+    def division(self, x, y, cfg: ReciprocalConfig = ReciprocalConfig()):
+        return self.mul_truncate(x, self.reciprocal(y, cfg))
+
+    def softmax(self, z: RssTensor, cfg: ReciprocalConfig = ReciprocalConfig()) -> RssTensor:
+        d = z.shape[-1]
+        if d > cfg.Y:
+            raise ConfigError(f"class count {d} exceeds reciprocal domain Y={cfg.Y}")
+        z = z.contiguous()
+        mx = self.max_tree(z)
+        x = _rowop(K.EW_SUB, z, mx)
+        e = self.exp_approx(x)
+        tot = _rowsum(e)
+        r = self.reciprocal(tot, cfg)
+        return self.mul_truncate(e, RssTensor(r.data.expand(e.data.shape).contiguous(), r.fp))
+
+
+# ---------------------------------------------------------------------------
+# kernel helpers
+
+
+def gemm_splits(M: int, N: int, kp: int, groups: int) -> int:
+    """Split-K count: enough for the exactness bound, and enough CTAs to cover
+    the 148 SMs when the tile grid alone does not (>= 8 K-blocks per split)."""
+    nkb = (kp + 31) // 32
+    need = max(1, math.ceil(nkb * 32 / MAX_SPLIT_K))
+    tiles = math.ceil(M / 128) * math.ceil(N / 64) * groups
+    occ = max(1, min(math.ceil(SMS / tiles), nkb // 8))
+    return max(need, occ)
+
+
+def _ew2(op, a: RssTensor, b: RssTensor) -> RssTensor:
+    a, b = _broadcast(a, b)
+    out = empty(a.shape, a.fp)
+    K.call("mpc3_ring_ew", op, a.data.data_ptr(), b.data.data_ptr(), 0, out.data.data_ptr(), 3 * a.numel, _stream())
+    return out
+
+
+def _broadcast(x: RssTensor, y: RssTensor):
+    if x.shape == y.shape:
+        return x.contiguous(), y.contiguous()
+    try:
+        shape = tuple(np.broadcast_shapes(x.shape, y.shape))
+    except ValueError as e:
+        raise ShapeError(str(e)) from None
+
+    def ex(t):
+        d = t.data.reshape((3,) + (1,) * (len(shape) - t.ndim) + t.shape)
+        return RssTensor(d.expand((3,) + shape).contiguous(), t.fp)
+
+    return ex(x), ex(y)
+
+
+def _rowop(op, a: RssTensor, b: RssTensor) -> RssTensor:
+    """a[..., j] op b[...] for the trio (b has a's shape without the last axis)."""
+    a = a.contiguous()
+    b = b.contiguous()
+    cols = a.shape[-1]
+    rows = 3 * (a.numel // cols)
+    out = empty(a.shape, a.fp)
+    K.call("mpc3_ring_rowop", op, a.data.data_ptr(), b.data.data_ptr(), out.data.data_ptr(), rows, cols, _stream())
+    return out
+
+
+def _rowsum(a: RssTensor) -> RssTensor:
+    a = a.contiguous()
+    cols = a.shape[-1]
+    out = empty(a.shape[:-1] + (1,), a.fp)
+    K.call("mpc3_ring_rowsum", a.data.data_ptr(), out.data.data_ptr(), 3 * (a.numel // cols), cols, _stream())
+    return out
+
+
+def reconstruct_device(x: RssTensor) -> torch.Tensor:
+    x = x.contiguous()
+    n = x.numel
+    out = torch.empty(n, dtype=torch.int64, device=x.data.device)
+    d = x.data.reshape(3, n)
+    K.call("mpc3_ring_ew", K.EW_ADD, d[0].data_ptr(), d[1].data_ptr(), 0, out.data_ptr(), n, _stream())
+    K.call("mpc3_ring_ew", K.EW_ADD, out.data_ptr(), d[2].data_ptr(), 0, out.data_ptr(), n, _stream())
+    return out
+
+
+# ---------------------------------------------------------------------------
+# plain (non-shared) exact ring ops: bilinear_exact's device body
+
+
+def plain_matmul(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    m, k = a.shape
+    n = b.shape[1]
+    if m == 0 or n == 0:
+        return np.zeros((m, n), U64)
+    da, db = to_device(a), to_device(b)
+    ws = torch.empty(K.lib().mpc3_ring_matmul_workspace(m, n, k), dtype=torch.uint8, device=_dev())
+    out = torch.empty(m * n, dtype=torch.int64, device=_dev())
+    K.call("mpc3_ring_matmul_u64", da.data_ptr(), db.data_ptr(), out.data_ptr(), m, n, k, ws.data_ptr(), _stream())
+    return to_host(out).reshape(m, n)
+
+
+def plain_conv2d(x: np.ndarray, k: np.ndarray, stride, padding) -> np.ndarray:
+    nb, c, h, w = x.shape
+    o, _, kh, kw = k.shape
+    sh, sw = stride
+    ph, pw = padding
+    if h + 2 * ph < kh or w + 2 * pw < kw:
+        raise ShapeError("kernel larger than padded input")
+    oh, ow = (h + 2 * ph - kh) // sh + 1, (w + 2 * pw - kw) // sw + 1
+    dx, dk = to_device(x), to_device(k)
+    K_ = c * kh * kw
+    M = nb * oh * ow
+    kp = _round_up(K_, 16)
+    A = torch.empty(8 * M * kp, dtype=torch.uint8, device=_dev())
+    B = torch.empty(8 * o * kp, dtype=torch.uint8, device=_dev())
+    a_op = K.conv_operand(K.GATHER_IM2COL, M, K_, nb, c, h, w, dx.stride(), kh, kw, sh, sw, ph, pw, oh, ow)
+    b_op = K.dense_operand(o, K_, s_r=K_, t2=1)
+    st = _stream()
+    K.call("mpc3_ring_pack", dx.data_ptr(), 0, C.byref(a_op), 2, A.data_ptr(), kp, st)
+    K.call("mpc3_ring_pack", dk.data_ptr(), 0, C.byref(b_op), 2, B.data_ptr(), kp, st)
+    splits = gemm_splits(M, o, kp, 1)
+    z = (torch.zeros if splits > 1 else torch.empty)(M * o, dtype=torch.int64, device=_dev())
+    K.call("mpc3_ring_gemm_packed", A.data_ptr(), B.data_ptr(), z.data_ptr(), 1, M, o, kp, o, M * o, splits, st)
+    return to_host(z).reshape(nb, oh, ow, o).transpose(0, 3, 1, 2).copy()
+
+
+def plain_sumpool(x: np.ndarray, window, stride) -> np.ndarray:
+    kh, kw = window
+    sh, sw = stride
+    nb, c, h, w = x.shape
+    if h < kh or w < kw:
+        raise ShapeError("window larger than input")
+    oh, ow = (h - kh) // sh + 1, (w - kw) // sw + 1
+    dx = to_device(x)
+    out = torch.empty(nb * c * oh * ow, dtype=torch.int64, device=_dev())
+    K.call("mpc3_ring_sumpool", dx.data_ptr(), out.data_ptr(), nb, c, h, w, kh, kw, sh, sw, _stream())
+    return to_host(out).reshape(nb, c, oh, ow)

@@ -1,0 +1,530 @@
+"""Layer graphs and the private forward / backward / SGD schedule on the GPU.
+
+API of the reference's nn.py (nn.py:43-793): LayerSpec builders, ModelGraph
+shape inference, parameter init, the per-party entry points
+(infer_private, forward_private, loss_grad_output, backward, sgd_step,
+share_model, train_private) and TrainConfig / TrainResult.
+
+The schedule runs on `TrioNet`, the B200 engine behind the reference's
+duck-typed engine seam (nn.py:209-253): conv/FC layers are one batched
+tcgen05 ring GEMM over the three parties' cross terms plus one fused
+reshare+truncate kernel; conv gradients are direct implicit GEMMs (no
+materialised dilation / padding / flips, nn.py:435-484); ReLU is one fused
+sign-circuit kernel; pooling forward/backward are one fused kernel each.
+PRF counters are consumed in exactly the reference's order, so opened
+results — and per-party shares — are bit-identical to the reference.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import engine as E
+from .engine import ReciprocalConfig, RssTensor, TrioSession
+from .errors import ConfigError, ProtocolError, ShapeError
+from .ring import DEFAULT_FP, FixedPointConfig, fx_decode, fx_encode
+from .sharing import ArithmeticShare, PartyContext, assemble, split_trio
+
+CONV2D = "Conv2d"
+FULLY_CONNECTED = "FullyConnected"
+AVGPOOL = "AvgPool"
+RELU = "ReLU"
+FLATTEN = "Flatten"
+
+
+def _pair(v) -> tuple:
+    if isinstance(v, (tuple, list)):
+        a, b = v
+        return (int(a), int(b))
+    return (int(v), int(v))
+
+
+@dataclass(frozen=True)
+class LayerSpec:
+    kind: str
+    out_channels: int = 0
+    out_features: int = 0
+    kernel: tuple = ()
+    stride: tuple = (1, 1)
+    padding: tuple = (0, 0)
+    window: tuple = ()
+
+
+def conv2d(out_channels: int, kernel, stride=1, padding=0) -> LayerSpec:
+    return LayerSpec(CONV2D, out_channels=int(out_channels), kernel=_pair(kernel), stride=_pair(stride),
+                     padding=_pair(padding))
+
+
+def fully_connected(out_features: int) -> LayerSpec:
+    return LayerSpec(FULLY_CONNECTED, out_features=int(out_features))
+
+
+def avgpool(window, stride=None) -> LayerSpec:
+    w = _pair(window)
+    return LayerSpec(AVGPOOL, window=w, stride=_pair(stride) if stride is not None else w)
+
+
+def relu() -> LayerSpec:
+    return LayerSpec(RELU)
+
+
+def flatten() -> LayerSpec:
+    return LayerSpec(FLATTEN)
+
+
+@dataclass
+class ModelGraph:
+    """Ordered layers, input shape (C,H,W) and per-layer parameters."""
+
+    layers: tuple
+    input_shape: tuple
+    params: list | None = None
+
+    def __post_init__(self):
+        self.layers = tuple(self.layers)
+        self.input_shape = tuple(int(d) for d in self.input_shape)
+        self._shapes = self._infer_shapes()
+
+    def _infer_shapes(self) -> list:
+        shape = self.input_shape
+        out = []
+        for s in self.layers:
+            if s.kind == CONV2D:
+                if len(shape) != 3:
+                    raise ShapeError(f"Conv2d needs (C,H,W), got {shape}")
+                c, h, w = shape
+                (kh, kw), (sh, sw), (ph, pw) = s.kernel, s.stride, s.padding
+                ho, wo = (h + 2 * ph - kh) // sh + 1, (w + 2 * pw - kw) // sw + 1
+                if h + 2 * ph < kh or w + 2 * pw < kw or ho < 1 or wo < 1:
+                    raise ShapeError(f"Conv2d kernel {s.kernel} does not fit {shape}")
+                shape = (s.out_channels, ho, wo)
+            elif s.kind == AVGPOOL:
+                if len(shape) != 3:
+                    raise ShapeError(f"AvgPool needs (C,H,W), got {shape}")
+                c, h, w = shape
+                ho, wo = (h - s.window[0]) // s.stride[0] + 1, (w - s.window[1]) // s.stride[1] + 1
+                if ho < 1 or wo < 1:
+                    raise ShapeError(f"AvgPool window {s.window} does not fit {shape}")
+                shape = (c, ho, wo)
+            elif s.kind == FULLY_CONNECTED:
+                if len(shape) != 1:
+                    raise ShapeError(f"FullyConnected needs a flat input, got {shape}")
+                shape = (s.out_features,)
+            elif s.kind == FLATTEN:
+                shape = (int(np.prod(shape)),)
+            elif s.kind != RELU:
+                raise ConfigError(f"unknown layer kind {s.kind!r}")
+            out.append(shape)
+        return out
+
+    @property
+    def output_shapes(self) -> list:
+        return list(self._shapes)
+
+    @property
+    def num_classes(self) -> int:
+        last = self._shapes[-1]
+        if len(last) != 1:
+            raise ShapeError(f"model output {last} is not a logit vector")
+        return last[0]
+
+    def param_shapes(self) -> list:
+        shape, out = self.input_shape, []
+        for s, nxt in zip(self.layers, self._shapes):
+            if s.kind == CONV2D:
+                out.append((s.out_channels, shape[0]) + s.kernel)
+            elif s.kind == FULLY_CONNECTED:
+                out.append((s.out_features, shape[0]))
+            shape = nxt
+        return out
+
+    def validate(self, recip: ReciprocalConfig = ReciprocalConfig()) -> None:
+        if self.num_classes > recip.Y:
+            raise ConfigError(f"{self.num_classes} classes exceed the reciprocal domain")
+        if self.params is not None:
+            want = self.param_shapes()
+            if len(self.params) != len(want):
+                raise ShapeError(f"expected {len(want)} parameter tensors, got {len(self.params)}")
+            for p, w in zip(self.params, want):
+                if tuple(p.shape) != w:
+                    raise ShapeError(f"parameter shape {tuple(p.shape)} != {w}")
+
+    def with_params(self, params) -> "ModelGraph":
+        return ModelGraph(self.layers, self.input_shape, params)
+
+
+def init_params_float(model: ModelGraph, seed: int = 0) -> list:
+    """U(-1/sqrt(fan_in), 1/sqrt(fan_in)) per parameter, in order (nn.py:190-198)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for shp in model.param_shapes():
+        bound = 1.0 / np.sqrt(int(np.prod(shp[1:])))
+        out.append(rng.uniform(-bound, bound, shp))
+    return out
+
+
+def init_params(model: ModelGraph, fp: FixedPointConfig = DEFAULT_FP, seed: int = 0) -> list:
+    return [fx_encode(w, fp) for w in init_params_float(model, seed)]
+
+
+# ---------------------------------------------------------------------------
+# the B200 engine behind the seam
+
+
+class TrioNet:
+    """Forward / backward / SGD of a ModelGraph on trio tensors."""
+
+    def __init__(self, sess: TrioSession):
+        self.s = sess
+        self.t = sess.fp.t
+
+    def forward(self, model: ModelGraph, params: list, x: RssTensor, record: bool):
+        """nn.py:405-432."""
+        S, acts, h, pi = self.s, [], x, 0
+        for spec in model.layers:
+            if spec.kind == CONV2D:
+                k = params[pi]
+                pi += 1
+                acts.append((h, k) if record else None)
+                h = S.conv2d(h, k, spec.stride, spec.padding)
+            elif spec.kind == FULLY_CONNECTED:
+                w = params[pi]
+                pi += 1
+                acts.append((h, w) if record else None)
+                h = S.matmul(h, w.apply(lambda d: d.transpose(1, 2)))
+            elif spec.kind == AVGPOOL:
+                acts.append((h.shape,) if record else None)
+                h = S.avgpool(h, spec.window, spec.stride)
+            elif spec.kind == RELU:
+                h, mask = S.relu_with_mask(h)
+                acts.append((mask,) if record else None)
+            elif spec.kind == FLATTEN:
+                shp = h.shape
+                acts.append((shp,) if record else None)
+                h = h.contiguous().reshape(shp[0], -1)
+        return h, acts
+
+    def backward(self, model: ModelGraph, acts, grad_out: RssTensor, batch_bits: int = 0) -> list:
+        """nn.py:502-536."""
+        if acts is None or len(acts) != len(model.layers) or any(a is None for a in acts):
+            raise ProtocolError("missing activation cache; run the forward pass with recording")
+        S, t = self.s, self.t
+        plist = [i for i, s in enumerate(model.layers) if s.kind in (CONV2D, FULLY_CONNECTED)]
+        grads = [None] * len(plist)
+        pi, g = len(plist), grad_out
+        for li in range(len(model.layers) - 1, -1, -1):
+            spec, cached = model.layers[li], acts[li]
+            if spec.kind == FULLY_CONNECTED:
+                x, w = cached
+                pi -= 1
+                grads[pi] = S.matmul(g.apply(lambda d: d.transpose(1, 2)), x, bits=t + batch_bits)
+                if li == plist[0]:
+                    break
+                g = S.matmul(g, w)
+            elif spec.kind == CONV2D:
+                x, k = cached
+                pi -= 1
+                grads[pi] = S.conv2d_wgrad(x, g, spec.kernel, spec.stride, spec.padding, bits=t + batch_bits)
+                if li == plist[0]:
+                    break
+                g = S.conv2d_dgrad(g, k, spec.stride, spec.padding, x.shape, bits=t)
+            elif spec.kind == AVGPOOL:
+                g = S.avgpool_backward(g, spec.window, spec.stride, cached[0])
+            elif spec.kind == RELU:
+                g = S.mul(g, cached[0], "mul.mask")
+            elif spec.kind == FLATTEN:
+                g = g.contiguous().reshape(cached[0])
+        return grads
+
+    def sgd(self, params: list, grads: list, lr: float) -> list:
+        """W <- W - truncate(c * grad), c = enc(lr) (nn.py:539-543)."""
+        c = int(fx_encode(lr, self.s.fp))
+        if c == 0:
+            return list(params)
+        S = self.s
+        return [S.sub(p, S.truncate(S.mul_const(g, c))) for p, g in zip(params, grads)]
+
+    def loss_grad(self, logits: RssTensor, y: RssTensor) -> RssTensor:
+        """softmax(logits) - y (nn.py:561-568)."""
+        if logits.shape[-1] != y.shape[-1]:
+            raise ShapeError(f"logit/label length mismatch {logits.shape} vs {y.shape}")
+        return self.s.sub(self.s.softmax(logits), y)
+
+
+# ---------------------------------------------------------------------------
+# training configuration and helpers (nn.py:625-676)
+
+
+@dataclass(frozen=True)
+class TrainConfig:
+    learning_rate: float
+    batch_size: int
+    iterations: int
+    seed: int = 0
+
+    def __post_init__(self):
+        if not self.learning_rate > 0:
+            raise ConfigError("learning_rate must be positive")
+        if self.batch_size < 1 or self.iterations < 0:
+            raise ConfigError("batch_size must be >= 1 and iterations >= 0")
+
+
+@dataclass
+class TrainResult:
+    weights: list
+    ce_history: list = field(default_factory=list)
+
+
+def batch_indices(iteration: int, batch_size: int, n: int) -> np.ndarray:
+    return (np.arange(batch_size) + iteration * batch_size) % n
+
+
+def cross_entropy(logits: np.ndarray, labels: np.ndarray) -> float:
+    z = logits - logits.max(axis=-1, keepdims=True)
+    logp = z - np.log(np.exp(z).sum(axis=-1, keepdims=True))
+    return float(-logp[np.arange(len(labels)), labels].mean())
+
+
+def moving_average(values, window: int = 20) -> np.ndarray:
+    v = np.asarray(values, dtype=np.float64)
+    half = window // 2
+    return np.array([v[max(0, i - half): i + window - half].mean() for i in range(len(v))])
+
+
+def one_hot(labels: np.ndarray, num_classes: int) -> np.ndarray:
+    labels = np.asarray(labels)
+    out = np.zeros((len(labels), num_classes))
+    out[np.arange(len(labels)), labels] = 1.0
+    return out
+
+
+def mean_relative_error(test, ref) -> float:
+    test, ref = np.asarray(test, np.float64), np.asarray(ref, np.float64)
+    return float((np.abs(test - ref).max(axis=-1) / np.abs(ref).max(axis=-1)).mean())
+
+
+def batch_bits(batch_size: int) -> int:
+    return batch_size.bit_length() - 1 if batch_size & (batch_size - 1) == 0 else 0
+
+
+# ---------------------------------------------------------------------------
+# trio drivers (single thread; what bench.py and the facade call)
+
+
+class TrainState:
+    """Shared weights + the dealer of one private training run (nn.py:679-751)."""
+
+    def __init__(self, sess: TrioSession, model: ModelGraph, cfg: TrainConfig, owner: int = 0, params=None):
+        model.validate()
+        self.sess, self.model, self.cfg, self.owner = sess, model, cfg, owner
+        self.net = TrioNet(sess)
+        self.rng = np.random.default_rng(cfg.seed)
+        plain = init_params(model, sess.fp, cfg.seed) if params is None else params
+        self.params = [sess.share(w, self.rng, owner=owner) for w in plain]
+        self.bbits = batch_bits(cfg.batch_size)
+        self.inv_b = int(fx_encode(1.0 / cfg.batch_size, sess.fp)) if self.bbits == 0 else 0
+
+    def deal_batch(self, xb_enc: np.ndarray, yb_enc: np.ndarray):
+        S = self.sess
+        return S.share(xb_enc, self.rng, owner=self.owner), S.share(yb_enc, self.rng, owner=self.owner)
+
+    def step(self, xs: RssTensor, ys: RssTensor) -> RssTensor:
+        """One private SGD iteration on dealt shares; returns the shared logits."""
+        S, net = self.sess, self.net
+        logits, acts = net.forward(self.model, self.params, xs, record=True)
+        g = net.loss_grad(logits, ys)
+        if self.bbits == 0:
+            g = S.truncate(S.mul_const(g, self.inv_b))
+        grads = net.backward(self.model, acts, g, self.bbits)
+        self.params = net.sgd(self.params, grads, self.cfg.learning_rate)
+        return logits
+
+
+def train_trio(sess: TrioSession, model: ModelGraph, cfg: TrainConfig, images: np.ndarray, labels: np.ndarray,
+               owner: int = 0) -> TrainResult:
+    """train_private with all three parties in one thread (nn.py:679-751)."""
+    st = TrainState(sess, model, cfg, owner)
+    n = len(images)
+    if n < 1:
+        raise ConfigError("empty training set")
+    d = model.num_classes
+    ce = []
+    for it in range(cfg.iterations):
+        idx = batch_indices(it, cfg.batch_size, n)
+        xs, ys = st.deal_batch(fx_encode(images[idx], sess.fp), fx_encode(one_hot(labels[idx], d), sess.fp))
+        logits = st.step(xs, ys)
+        ce.append(cross_entropy(fx_decode(sess.reveal(logits), sess.fp), labels[idx]))
+    weights = [sess.reveal(p) for p in st.params]
+    return TrainResult(weights=weights, ce_history=ce)
+
+
+def infer_trio(sess: TrioSession, model: ModelGraph, params: list, x: RssTensor) -> RssTensor:
+    return TrioNet(sess).forward(model, params, x, record=False)[0]
+
+
+# ---------------------------------------------------------------------------
+# per-party entry points (nn.py:550-609, 679-751)
+
+
+def _params_payload(model):
+    if model.params is None:
+        raise ProtocolError("model has no parameters")
+    return list(model.params)
+
+
+def _assemble_list(ps, key, fp):
+    n = len(ps[0][key])
+    return [assemble({p: ps[p][key][i] for p in range(3)}, fp) for i in range(n)]
+
+
+def infer_private(ctx: PartyContext, model: ModelGraph, x: ArithmeticShare) -> ArithmeticShare:
+    def fn(sess, ps):
+        params = _assemble_list(ps, 0, ctx.fp)
+        return split_trio(infer_trio(sess, model, params, assemble({p: ps[p][1] for p in range(3)}, ctx.fp)))
+
+    return ctx.collective("infer_private", (_params_payload(model), x), fn)[ctx.party]
+
+
+class _Acts:
+    """Per-party activation cache: per-party views of the trio cache."""
+
+    def __init__(self, items):
+        self.items = items
+
+    def __len__(self):
+        return len(self.items)
+
+    def __iter__(self):
+        return iter(self.items)
+
+    def __getitem__(self, i):
+        return self.items[i]
+
+
+def _split_acts(acts):
+    per = [[], [], []]
+    for a in acts:
+        for p in range(3):
+            if a is None:
+                per[p].append(None)
+            else:
+                per[p].append(tuple(split_trio(v)[p] if isinstance(v, RssTensor) else v for v in a))
+    return [_Acts(v) for v in per]
+
+
+def _join_acts(ps, key, fp):
+    n = len(ps[0][key])
+    out = []
+    for i in range(n):
+        a0 = ps[0][key][i]
+        if a0 is None:
+            out.append(None)
+            continue
+        out.append(tuple(assemble({p: ps[p][key][i][j] for p in range(3)}, fp)
+                         if isinstance(a0[j], ArithmeticShare) else a0[j] for j in range(len(a0))))
+    return out
+
+
+def forward_private(ctx: PartyContext, model: ModelGraph, x: ArithmeticShare):
+    def fn(sess, ps):
+        params = _assemble_list(ps, 0, ctx.fp)
+        logits, acts = TrioNet(sess).forward(model, params, assemble({p: ps[p][1] for p in range(3)}, ctx.fp), True)
+        return split_trio(logits), _split_acts(acts)
+
+    logits, acts = ctx.collective("forward_private", (_params_payload(model), x), fn)
+    return logits[ctx.party], acts[ctx.party]
+
+
+def loss_grad_output(ctx: PartyContext, logits: ArithmeticShare, y: ArithmeticShare) -> ArithmeticShare:
+    if logits.shape[-1] != y.shape[-1]:
+        raise ShapeError(f"logit/label length mismatch {logits.shape} vs {y.shape}")
+
+    def fn(sess, ps):
+        lg = assemble({p: ps[p][0] for p in range(3)}, ctx.fp)
+        yy = assemble({p: ps[p][1] for p in range(3)}, ctx.fp)
+        return split_trio(TrioNet(sess).loss_grad(lg, yy))
+
+    return ctx.collective("loss_grad_output", (logits, y), fn)[ctx.party]
+
+
+def backward(ctx: PartyContext, model: ModelGraph, acts, grad_out: ArithmeticShare, batch_bits: int = 0) -> list:
+    if acts is None or len(acts) != len(model.layers) or any(a is None for a in acts):
+        raise ProtocolError("missing activation cache; run the forward pass with recording")
+
+    def fn(sess, ps):
+        cache = _join_acts(ps, 0, ctx.fp)
+        g = assemble({p: ps[p][1] for p in range(3)}, ctx.fp)
+        grads = TrioNet(sess).backward(model, cache, g, batch_bits)
+        return [split_trio(t) for t in grads]
+
+    res = ctx.collective("backward", (list(acts), grad_out), fn)
+    return [r[ctx.party] for r in res]
+
+
+def sgd_step(ctx: PartyContext, params: list, grads: list, lr: float) -> list:
+    def fn(sess, ps):
+        P = _assemble_list(ps, 0, ctx.fp)
+        G = _assemble_list(ps, 1, ctx.fp)
+        return [split_trio(t) for t in TrioNet(sess).sgd(P, G, lr)]
+
+    res = ctx.collective("sgd_step", (list(params), list(grads)), fn)
+    return [r[ctx.party] for r in res]
+
+
+def share_model(ctx: PartyContext, model: ModelGraph, rng=None, owner: int = 0) -> ModelGraph:
+    from .session import distribute_input
+
+    shapes = model.param_shapes()
+    params = [distribute_input(ctx, model.params[i] if ctx.party == owner else None, rng, owner, shape=shapes[i])
+              for i in range(len(shapes))]
+    return model.with_params(params)
+
+
+def train_private(ctx: PartyContext, model: ModelGraph, cfg: TrainConfig, data=None, owner: int = 0) -> TrainResult:
+    """Minibatch SGD on shares; weights opened at the end (nn.py:679-751)."""
+    model.validate()
+    if ctx.party == owner and data is None:
+        raise ProtocolError("owner must supply the training data")
+
+    def fn(sess, ps):
+        images, labels = ps[owner]
+        res = train_trio(sess, model.with_params(None), cfg, np.asarray(images), np.asarray(labels), owner)
+        return res
+
+    res = ctx.collective("train_private", data if ctx.party == owner else None, fn)
+    return TrainResult(weights=res.weights, ce_history=res.ce_history if ctx.party == owner else [])
+
+
+def infer_plain_float(model: ModelGraph, x: np.ndarray) -> np.ndarray:
+    """float64 reference forward pass (nn.py:360-398), evaluated on the GPU."""
+    import torch
+    import torch.nn.functional as F
+
+    h = torch.as_tensor(np.asarray(x, np.float64), device="cuda")
+    pi = 0
+    for s in model.layers:
+        if s.kind == CONV2D:
+            h = F.conv2d(h, torch.as_tensor(np.asarray(model.params[pi], np.float64), device="cuda"),
+                         stride=s.stride, padding=s.padding)
+            pi += 1
+        elif s.kind == FULLY_CONNECTED:
+            h = h @ torch.as_tensor(np.asarray(model.params[pi], np.float64), device="cuda").T
+            pi += 1
+        elif s.kind == AVGPOOL:
+            h = F.avg_pool2d(h, s.window, s.stride)
+        elif s.kind == RELU:
+            h = h * (h >= 0)
+        elif s.kind == FLATTEN:
+            h = h.reshape(h.shape[0], -1)
+    return h.cpu().numpy()
+
+
+__all__ = [
+    "LayerSpec", "ModelGraph", "TrainConfig", "TrainResult", "TrioNet", "TrainState", "avgpool", "backward",
+    "conv2d", "flatten", "forward_private", "fully_connected", "infer_plain_float", "infer_private", "infer_trio",
+    "init_params", "init_params_float", "loss_grad_output", "mean_relative_error", "relu", "sgd_step",
+    "share_model", "train_private", "train_trio", "one_hot", "cross_entropy", "batch_indices", "moving_average",
+]
+_ = E

@@ -1,0 +1,212 @@
+"""Device kernels through the C ABI vs the oracle (needs a B200)."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle import nnmirror as N
+from oracle import rss as R
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2104_10949_b200 import _capi  # noqa: E402
+
+U64 = np.uint64
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, U64).view(np.int64)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy().view(U64)
+
+
+_PINNED = []
+
+
+def p(t):
+    # keep temporaries alive: a freed block could be handed to the next
+    # argument's allocation before the launch reads it
+    _PINNED.append(t)
+    if len(_PINNED) > 64:
+        del _PINNED[:32]
+    return C.c_void_p(t.data_ptr())
+
+
+def rk3(keys):
+    rk = np.zeros((3, 44), np.uint32)
+    for i, k in enumerate(keys):
+        _capi.check(_capi.lib().mpc3_aes128_expand(C.c_char_p(k), rk[i].ctypes.data_as(C.c_void_p)))
+    return torch.from_numpy(rk.view(np.int32)).cuda()
+
+
+S = None
+
+
+def stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def rnd(rng, shape):
+    return rng.integers(0, 1 << 64, size=shape, dtype=U64)
+
+
+def test_library_loads_and_abi():
+    assert _capi.lib().mpc3_abi_version() == 1
+    cap = torch.cuda.get_device_capability()
+    assert cap[0] == 10, cap
+
+
+@pytest.mark.parametrize("purpose,index,off,count", [(1, 0, 0, 4), (2, 5, 3, 17), (5, (1 << 48) - 1, 1, 1),
+                                                     (4, 123456, 0, 100001)])
+def test_prf_words(purpose, index, off, count):
+    keys = R.party_keys(3)
+    rk = rk3(keys)
+    out = torch.zeros(count, dtype=torch.int64, device="cuda")
+    _capi.call("mpc3_prf_words", C.c_void_p(rk.data_ptr() + 44 * 4), purpose, index, off, count, p(out), stream())
+    ref = R.prf_words(keys[1], purpose, index, off + count)[off:]
+    assert np.array_equal(host(out), ref)
+
+
+def test_prf_range_errors():
+    rk = rk3(R.party_keys(0))
+    out = torch.zeros(4, dtype=torch.int64, device="cuda")
+    with pytest.raises(_capi.E.RangeError):
+        _capi.call("mpc3_prf_words", p(rk), 1 << 16, 0, 0, 4, p(out), stream())
+    with pytest.raises(_capi.E.RangeError):
+        _capi.call("mpc3_prf_words", p(rk), 1, 1 << 48, 0, 4, p(out), stream())
+
+
+@pytest.mark.parametrize("n", [1, 2, 7, 1 << 16, (1 << 16) + 3])
+def test_mul_truncate(n):
+    rng = np.random.default_rng(n)
+    x, y = R.share(rnd(rng, n), rng), R.share(rnd(rng, n), rng)
+    s = R.Session(5)
+    rk = rk3(s.keys)
+    out = torch.empty(3 * n, dtype=torch.int64, device="cuda")
+    _capi.call("mpc3_rss_mul", p(rk), None, 0, p(dev(x)), p(dev(y)), p(out), n, stream())
+    assert np.array_equal(host(out).reshape(3, n), R.mul(s, x, y))
+    v = R.share(rng.integers(-(1 << 61), 1 << 61, n, dtype=np.int64).view(U64), rng)
+    for bits in (1, 20, 61):
+        s = R.Session(5)
+        _capi.call("mpc3_rss_truncate", p(rk), None, 0, 0, bits, p(dev(v)), p(out), n, stream())
+        assert np.array_equal(host(out).reshape(3, n), R.truncate(s, v, bits))
+    with pytest.raises(_capi.E.RangeError):
+        _capi.call("mpc3_rss_truncate", p(rk), None, 0, 0, 62, p(dev(v)), p(out), n, stream())
+
+
+@pytest.mark.parametrize("n", [5, 101, 4096, 100003])
+def test_sign_modes(n):
+    rng = np.random.default_rng(n)
+    edges = np.array([0, 1, (1 << 63) - 1, 1 << 63, (1 << 64) - 1], U64)
+    x = np.concatenate([edges, rnd(rng, n)])[:n]
+    xs = R.share(x, rng)
+    keys = R.Session(9).keys
+    rk = rk3(keys)
+    xd = dev(xs)
+    out = torch.empty(3 * n, dtype=torch.int64, device="cuda")
+    mask = torch.empty(3 * n, dtype=torch.int64, device="cuda")
+    for mode, fn in [(0, R.a2b), (1, R.msb), (2, R.drelu)]:
+        _capi.call("mpc3_rss_sign", p(rk), None, mode, 0, 0, 0, p(xd), p(out), p(mask), n, n, 0, stream())
+        assert np.array_equal(host(out).reshape(3, n), fn(R.Session(9), xs)), mode
+    _capi.call("mpc3_rss_sign", p(rk), None, 3, 0, 0, 0, p(xd), p(out), p(mask), n, n, 0, stream())
+    ro, rm = R.relu_with_mask(R.Session(9), xs)
+    assert np.array_equal(host(out).reshape(3, n), ro)
+    assert np.array_equal(host(mask).reshape(3, n), rm)
+
+
+def _gemm_packed(A, B, groups, M, Nn, kp, splits):
+    Cm = torch.zeros(groups * M * Nn, dtype=torch.int64, device="cuda")
+    _capi.call("mpc3_ring_gemm_packed", p(A), p(B), p(Cm), groups, M, Nn, kp, Nn, M * Nn, splits, stream())
+    return host(Cm).reshape(groups, M, Nn)
+
+
+def _pack(src, plane, op, role, kp):
+    groups = 1 if role == 2 else 3
+    out = torch.empty(groups * 8 * op.rows * kp, dtype=torch.uint8, device="cuda")
+    _capi.call("mpc3_ring_pack", p(src), plane, C.byref(op), role, p(out), kp, stream())
+    return out
+
+
+@pytest.mark.parametrize("M,K,Nn", [(1, 1, 1), (9, 33, 7), (128, 64, 64), (130, 100, 70), (300, 257, 129),
+                                    (64, 16384, 40), (200, 4608, 512)])
+def test_ring_matmul_tcgen05_exact(M, K, Nn):
+    rng = np.random.default_rng(M * 7 + K)
+    a = rnd(rng, (M, K))
+    b = rnd(rng, (K, Nn))
+    ref = R.wrap_matmul(a, b) if M * K * Nn <= 50_000_000 else None
+    kp = (K + 15) // 16 * 16
+    A = _pack(dev(a), 0, _capi.dense_operand(M, K, s_r=K, t2=1), 2, kp)
+    B = _pack(dev(b), 0, _capi.dense_operand(Nn, K, s_r=1, t2=Nn), 2, kp)
+    got = _gemm_packed(A, B, 1, M, Nn, kp, 1)[0]
+    simt = torch.empty(M * Nn, dtype=torch.int64, device="cuda")
+    _capi.call("mpc3_ring_gemm_simt", p(dev(a)), p(dev(b)), p(simt), M, Nn, K, K, 1, Nn, 1, Nn, stream())
+    simt = host(simt).reshape(M, Nn)
+    assert np.array_equal(got, simt)
+    if ref is not None:
+        assert np.array_equal(got, ref)
+
+
+def test_ring_matmul_all_ones_worst_case_and_split():
+    # adversarial all-0xFF limbs at the exactness edge, and split-K beyond it
+    for K, splits in [(16384, 1), (16384 * 2 + 48, 3)]:
+        a = np.full((128, K), (1 << 64) - 1, U64)
+        b = np.full((K, 64), (1 << 64) - 1, U64)
+        kp = (K + 15) // 16 * 16
+        A = _pack(dev(a), 0, _capi.dense_operand(128, K, s_r=K, t2=1), 2, kp)
+        B = _pack(dev(b), 0, _capi.dense_operand(64, K, s_r=1, t2=64), 2, kp)
+        got = _gemm_packed(A, B, 1, 128, 64, kp, splits)[0]
+        assert np.all(got == U64(K % (1 << 64)))  # (-1)(-1) K = K
+
+
+def test_ring_matmul_u64_convenience():
+    rng = np.random.default_rng(3)
+    M, K, Nn = 77, 20000, 33
+    a, b = rnd(rng, (M, K)), rnd(rng, (K, Nn))
+    ws = torch.empty(_capi.lib().mpc3_ring_matmul_workspace(M, Nn, K), dtype=torch.uint8, device="cuda")
+    out = torch.empty(M * Nn, dtype=torch.int64, device="cuda")
+    _capi.call("mpc3_ring_matmul_u64", p(dev(a)), p(dev(b)), p(out), M, Nn, K, p(ws), stream())
+    assert np.array_equal(host(out).reshape(M, Nn), R.wrap_matmul(a, b))
+
+
+def test_secure_matmul_cross_terms_reshare_truncate():
+    rng = np.random.default_rng(11)
+    M, K, Nn = 37, 200, 19
+    x = R.share(R.fx_encode(rng.uniform(-4, 4, (M, K))), rng)
+    y = R.share(R.fx_encode(rng.uniform(-4, 4, (K, Nn))), rng)
+    kp = (2 * K + 15) // 16 * 16
+    A = _pack(dev(x), M * K, _capi.dense_operand(M, K, s_r=K, t2=1), 0, kp)
+    B = _pack(dev(y), K * Nn, _capi.dense_operand(Nn, K, s_r=1, t2=Nn), 1, kp)
+    Cm = torch.zeros(3 * M * Nn, dtype=torch.int64, device="cuda")
+    _capi.call("mpc3_ring_gemm_packed", p(A), p(B), p(Cm), 3, M, Nn, kp, Nn, M * Nn, 1, stream())
+    s = R.Session(7)
+    ref = R.matmul_shares(s, x, y)
+    out = torch.empty(3 * M * Nn, dtype=torch.int64, device="cuda")
+    v = _capi.make_view((1, 1, M, Nn))
+    _capi.call("mpc3_rss_reshare_truncate", p(rk3(s.keys)), None, 0, 0, 0, 20, p(Cm), C.byref(v), p(out),
+               stream())
+    assert np.array_equal(host(out).reshape(3, M, Nn), ref)
+
+
+def test_avgpool_kernels():
+    rng = np.random.default_rng(21)
+    shape, win, stride = (2, 3, 9, 8), (3, 3), (2, 2)
+    x = R.share(R.fx_encode(rng.uniform(-4, 4, shape)), rng)
+    s = R.Session(3)
+    ref = R.avgpool_shares(s, x, win, stride)
+    rk = rk3(s.keys)
+    out = torch.empty(ref.size, dtype=torch.int64, device="cuda")
+    _capi.call("mpc3_rss_avgpool", p(rk), None, 0, 0, 20, int(R.fx_encode(1.0 / 9)), p(dev(x)), p(out), *shape, 3, 3, 2, 2,
+               stream())
+    assert np.array_equal(host(out).reshape(ref.shape), ref)
+    g = R.share(R.fx_encode(rng.uniform(-1, 1, ref.shape[1:])), rng)
+    s = R.Session(3)
+    refb = N.avgpool_backward(N.TrioEngine(s), g, win, stride, shape)
+    outb = torch.empty(refb.size, dtype=torch.int64, device="cuda")
+    _capi.call("mpc3_rss_avgpool_backward", p(rk), None, 0, 0, 20, int(R.fx_encode(1.0 / 9)), p(dev(g)), p(outb), *shape,
+               ref.shape[3], ref.shape[4], 3, 3, 2, 2, stream())
+    assert np.array_equal(host(outb).reshape(refb.shape), refb)

@@ -1,0 +1,135 @@
+"""Kernel microbenchmarks on one B200 (CUDA-event timed, warm, L2-flushed).
+
+python tools/microbench.py [--out gpurun_out/microbench.json] [--quick]
+
+Reports: ring GEMM (tcgen05 kind::i8) ring-TOPS and int8-op rate for the
+M=N=K sweep, cuBLASLt int8 (torch._int_mm) as the measured int8 roofline,
+AES-CTR PRF blocks/s, and the fused sign (ReLU) / truncate kernels.
+"""
+
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2104_10949_b200 import _capi  # noqa: E402
+
+L2_FLUSH = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+
+
+def p(t):
+    return C.c_void_p(t.data_ptr())
+
+
+def st():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def timeit(fn, iters=10, warmup=3, flush=True):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(iters):
+        if flush:
+            L2_FLUSH.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        times.append(a.elapsed_time(b) / 1e3)
+    return float(np.median(times)), float(np.min(times))
+
+
+def rk3():
+    rk = np.zeros((3, 44), np.uint32)
+    for i in range(3):
+        _capi.check(_capi.lib().mpc3_aes128_expand(C.c_char_p(bytes([i]) * 16), rk[i].ctypes.data_as(C.c_void_p)))
+    return torch.from_numpy(rk.view(np.int32)).cuda()
+
+
+def gemm_sweep(sizes):
+    out = []
+    for n in sizes:
+        kp = (n + 15) // 16 * 16
+        A = torch.randint(0, 256, (8 * n * kp,), dtype=torch.uint8, device="cuda")
+        B = torch.randint(0, 256, (8 * n * kp,), dtype=torch.uint8, device="cuda")
+        Cm = torch.empty(n * n, dtype=torch.int64, device="cuda")
+
+        def run():
+            _capi.call("mpc3_ring_gemm_packed", p(A), p(B), p(Cm), 1, n, n, kp, n, 0, 1, st())
+
+        med, best = timeit(run, iters=5 if n >= 4096 else 10)
+        ring_macs = n ** 3
+        out.append({"n": n, "ms": med * 1e3, "ring_tops": 2 * ring_macs / med / 1e12,
+                    "int8_tops": 72 * ring_macs / med / 1e12, "best_ms": best * 1e3})
+        print("gemm", out[-1], flush=True)
+        del A, B, Cm
+    return out
+
+
+def int8_peak():
+    n = 8192
+    a = torch.randint(-128, 127, (n, n), dtype=torch.int8, device="cuda")
+    b = torch.randint(-128, 127, (n, n), dtype=torch.int8, device="cuda").t().contiguous().t()
+    try:
+        med, best = timeit(lambda: torch._int_mm(a, b), iters=10, flush=False)
+    except Exception as e:  # noqa: BLE001
+        return {"error": repr(e)}
+    return {"n": n, "ms": med * 1e3, "tops": 2 * n ** 3 / med / 1e12, "best_tops": 2 * n ** 3 / best / 1e12}
+
+
+def aes_rate():
+    rk = rk3()
+    count = 1 << 28  # words -> 2^27 blocks
+    out = torch.empty(count, dtype=torch.int64, device="cuda")
+    med, _ = timeit(lambda: _capi.call("mpc3_prf_words", p(rk), 1, 0, 0, count, p(out), st()), iters=5)
+    return {"blocks": count // 2, "ms": med * 1e3, "gblocks_s": count / 2 / med / 1e9,
+            "gbytes_s": count * 8 / med / 1e9}
+
+
+def protocol_rates():
+    rk = rk3()
+    res = {}
+    n = 1 << 24
+    x = torch.randint(-(1 << 40), 1 << 40, (3 * n,), dtype=torch.int64, device="cuda")
+    y = torch.empty_like(x)
+    m = torch.empty_like(x)
+    med, _ = timeit(lambda: _capi.call("mpc3_rss_sign", p(rk), None, 3, 0, 0, 0, p(x), p(y), p(m), n, n, 0, st()), iters=5)
+    res["relu"] = {"n": n, "ms": med * 1e3, "gelem_s": n / med / 1e9, "aes_gblocks_s": 23 * n / 2 / med / 1e9 * 2 / 2,
+                   "hbm_gbs": 72 * n / med / 1e9}
+    med, _ = timeit(lambda: _capi.call("mpc3_rss_truncate", p(rk), None, 0, 0, 20, p(x), p(y), n, st()), iters=5)
+    res["truncate"] = {"n": n, "ms": med * 1e3, "gelem_s": n / med / 1e9, "hbm_gbs": 48 * n / med / 1e9}
+    med, _ = timeit(lambda: _capi.call("mpc3_rss_mul", p(rk), None, 0, p(x), p(x), p(y), n, st()), iters=5)
+    res["mul"] = {"n": n, "ms": med * 1e3, "gelem_s": n / med / 1e9, "hbm_gbs": 72 * n / med / 1e9}
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default="gpurun_out/microbench.json")
+    ap.add_argument("--quick", action="store_true")
+    args = ap.parse_args()
+    os.makedirs(os.path.dirname(args.out), exist_ok=True)
+    res = {"device": torch.cuda.get_device_name(), "when": time.time()}
+    res["aes"] = aes_rate()
+    print("aes", res["aes"], flush=True)
+    res["protocols"] = protocol_rates()
+    print("protocols", res["protocols"], flush=True)
+    res["int8_cublaslt"] = int8_peak()
+    print("int8", res["int8_cublaslt"], flush=True)
+    res["gemm"] = gemm_sweep([1024, 2048, 4096] if args.quick else [256, 512, 1024, 2048, 4096, 8192])
+    with open(args.out, "w") as f:
+        json.dump(res, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
