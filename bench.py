@@ -1,0 +1,328 @@
+"""Headline benchmark: AlexNet-CIFAR private training step (3-party RSS over
+Z_2^64, batch 128 per GPU), images/s — BASELINE.json configs[1].
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port P bench.py --gpus N ...
+
+One "step" = one private SGD iteration (forward, softmax loss gradient,
+backward, SGD update, all on shares) over one synthetic CIFAR-shaped batch.
+`value`: device-resident dealt batches, CUDA-event timed per step with an L2
+flush (256 MiB write) before each timed step, outside its events; max over
+ranks.  `e2e`: the same step through the public API with host inputs: the
+owner's fx-encoding + dealing on the host, pinned H2D of the shares, the
+step, and the D2H of the opened logits (nn.py:746) inside the timed region.
+Multi-GPU (N>1): each rank trains an independent replica on its own batch
+(replicas; no data-path collective yet — see DESIGN.md), "scaling": "weak".
+
+`--impl reference` times the reference algorithm's CPU implementation (the
+oracle port, oracle/nnmirror.py) on the host cores on rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "private images/sec (ResNet-50 inf, AlexNet train) at 1/2/4/8 B200; ring-GEMM TOPS"
+UNIT = "images/s"
+BATCH = 128
+CPU_SAMPLE_BATCH = 32
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--batch", type=int, default=BATCH)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _config(args, ws):
+    return {"workload": "AlexNet-CIFAR private training step (3-party RSS, Z_2^64, t=20)",
+            "model": "alexnet_cifar", "global_batch": args.batch * ws, "per_gpu_batch": args.batch,
+            "input": "3x32x32", "classes": 10, "parallelism": f"replicas{ws}" if ws > 1 else "single",
+            "l2": "flushed (256 MiB write) before every timed step, outside its events"}
+
+
+def _synthetic(batch, seed):
+    rng = np.random.default_rng(seed)
+    return rng.uniform(0, 1, (batch, 3, 32, 32)), rng.integers(0, 10, batch)
+
+
+# ---------------------------------------------------------------------------
+# CPU: the reference algorithm (oracle port)
+
+
+def cpu_steps(batch, steps, warmup):
+    from oracle import nnmirror as N
+    from oracle import rss as R
+
+    layers, ish = N.alexnet_cifar()
+    imgs, labels = _synthetic(batch, 0)
+    loop = N.TrainLoop(R.Session(0), layers, ish, 0.01, batch)
+    if warmup:
+        wi, wl = _synthetic(4, 1)
+        wloop = N.TrainLoop(R.Session(1), layers, ish, 0.01, 4)
+        for _ in range(warmup):
+            wloop.step(wi, wl)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        loop.step(imgs, labels)
+    dt = time.perf_counter() - t0
+    return batch * steps / dt, dt / steps
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    steps = max(1, args.steps)
+    value, per_step = cpu_steps(CPU_SAMPLE_BATCH, steps, min(args.warmup, 1))
+    cores = os.cpu_count()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": steps, "warmup": args.warmup,
+        "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u64 ring (int)", "data": "synthetic", "config": _config(args, ws), "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"AlexNet-CIFAR private train step at batch {CPU_SAMPLE_BATCH} per step "
+                                   f"(numpy/OpenBLAS float-limb restatement of the reference, 3 party threads "
+                                   f"for bilinear ops; warm-up at batch 4)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region."""
+
+    def __init__(self, index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        sm = [float(r[1]) for r in rows if len(r) > 8 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) > 8 and r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            if len(r) > 8:
+                for i, nm in enumerate(names):
+                    if r[5 + i].strip().lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def run_b200(args, ws, rank, local):
+    import torch
+
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2104_10949_b200 as M
+    from paper_2104_10949_b200 import _capi, engine
+    from paper_2104_10949_b200.nn import TrainState, one_hot
+
+    b = args.batch
+    dev = torch.device("cuda", local)
+    sess = M.TrioSession(seed=rank)
+    model = M.alexnet_cifar()
+    cfg = M.TrainConfig(0.01, b, args.warmup + args.steps, seed=rank)
+    st = TrainState(sess, model, cfg)
+    imgs, labels = _synthetic(b, 100 + rank)
+    xe, ye = M.fx_encode(imgs), M.fx_encode(one_hot(labels, 10))
+
+    # device-resident dealt batches (dealing outside the timed region)
+    batches = [st.deal_batch(xe, ye) for _ in range(args.warmup + args.steps)]
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    counter = {"n": 0}
+    orig_call = _capi.call
+
+    def counting_call(name, *a):
+        if name not in ("mpc3_aes128_expand",):
+            counter["n"] += 1
+        return orig_call(name, *a)
+
+    # roofline instrumentation: CUDA events around every launch of the
+    # dominant kernel (the fused sign / ReLU kernel) on its launch stream
+    sign_events = []
+    instrument = {"on": False}
+
+    def traced_call(name, *a):
+        if instrument["on"] and name == "mpc3_rss_sign":
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            counting_call(name, *a)
+            e1.record()
+            sign_events.append((e0, e1, int(a[9])))
+            return
+        return counting_call(name, *a)
+
+    _capi.call = traced_call
+    engine.K.call = traced_call
+
+    for i in range(args.warmup):
+        st.step(*batches[i])
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    clocks = Clocks(local)
+    counter["n"] = 0
+    instrument["on"] = True
+    step_ms = []
+    for i in range(args.steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        st.step(*batches[args.warmup + i])
+        e1.record()
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    instrument["on"] = False
+    launches = counter["n"]
+    clk = clocks.stop()
+    total_ms = float(sum(step_ms))
+    if ws > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+        torch.distributed.barrier()
+    value = b * args.steps * ws / (total_ms / 1e3)
+
+    # roofline of the dominant kernel: fused sign circuit (HBM 72 B/elem algorithmic)
+    sign_ms = sum(a.elapsed_time(c) for a, c, _ in sign_events)
+    sign_elems = sum(n for _, _, n in sign_events)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    nlaunch = max(1, len(sign_events))
+    achieved = (72.0 * sign_elems / nlaunch) / (sign_ms / nlaunch / 1e3) / 1e9 if sign_ms else None
+    roofline = {"kernel": "mpc3_rss_sign (fused a2b + Kogge-Stone + bit_inject + ReLU, AES-CTR inline)",
+                "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": (achieved / hbm_peak) if achieved else None, "traffic": None,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650 GB/s",
+                "share_of_step": sign_ms / max(total_ms, 1e-9) if ws == 1 else None,
+                "aes_gblocks_s": (23 * sign_elems / 2) / (sign_ms / 1e3) / 1e9 if sign_ms else None,
+                "algorithmic_bytes_per_elem": 72}
+
+    # end-to-end through the public API with host inputs
+    e2e = None
+    if not args.no_e2e:
+        _capi.call = orig_call
+        engine.K.call = orig_call
+        pin_x = torch.empty((3,) + xe.shape, dtype=torch.int64).pin_memory()
+        pin_y = torch.empty((3,) + ye.shape, dtype=torch.int64).pin_memory()
+        out_host = torch.empty((3, b, 10), dtype=torch.int64).pin_memory()
+        rng = np.random.default_rng(7)
+
+        def host_deal(v):
+            c0 = rng.integers(0, 1 << 64, size=v.shape, dtype=np.uint64)
+            c1 = rng.integers(0, 1 << 64, size=v.shape, dtype=np.uint64)
+            return np.stack([c0, c1, v - c0 - c1]).view(np.int64)
+
+        def e2e_step():
+            x_enc = M.fx_encode(imgs)
+            y_enc = M.fx_encode(one_hot(labels, 10))
+            pin_x.numpy()[...] = host_deal(x_enc)
+            pin_y.numpy()[...] = host_deal(y_enc)
+            xs = engine.RssTensor(pin_x.to(dev, non_blocking=True))
+            ys = engine.RssTensor(pin_y.to(dev, non_blocking=True))
+            logits = st.step(xs, ys)
+            out_host.copy_(logits.data, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            return (out_host[0] + out_host[1] + out_host[2]).numpy()
+
+        for _ in range(2):
+            e2e_step()
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        dt = time.perf_counter() - t0
+        if ws > 1:
+            t = torch.tensor([dt], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e = {"value": b * args.steps * ws / dt, "unit": UNIT,
+               "h2d_bytes_per_step": int(pin_x.numel() * 8 + pin_y.numel() * 8),
+               "d2h_bytes_per_step": int(out_host.numel() * 8),
+               "note": "host fx-encode + numpy dealer (sharing.py:113-118) + pinned H2D + step + opened-logits D2H"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        v, _ = cpu_steps(CPU_SAMPLE_BATCH, 1, 0)
+        cpu = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+               "sample": f"one AlexNet-CIFAR private train step at batch {CPU_SAMPLE_BATCH} "
+                         f"(oracle port of the reference, numpy/OpenBLAS, 3 party threads)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64 ring (int)", "data": "synthetic",
+            "config": _config(args, ws), "clocks": clk, "gpu_launches": launches, "roofline": roofline,
+            "e2e": e2e, "cpu_baseline": cpu,
+            "step_ms": [round(v, 3) for v in step_ms],
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = _args()
+    ws, rank, local = _dist()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+    else:
+        run_b200(args, ws, rank, local)
+
+
+if __name__ == "__main__":
+    main()

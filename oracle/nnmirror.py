@@ -392,6 +392,33 @@ def train_private(s: R.Session, layers, input_shape, images, labels, lr, batch, 
     return P, logits_hist
 
 
+class TrainLoop:
+    """train_private split into setup (param dealing) and per-iteration steps,
+    so the CPU baseline times iterations the way bench.py times the GPU."""
+
+    def __init__(self, s: R.Session, layers, input_shape, lr, batch, seed=0):
+        self.s, self.layers, self.lr, self.batch = s, layers, lr, batch
+        outs, _ = shapes(layers, input_shape)
+        self.d = outs[-1][0]
+        self.rng = np.random.default_rng(seed)
+        self.P = [R.share(w, self.rng) for w in init_params(layers, input_shape, s.t, seed)]
+        self.bb = batch_bits(batch)
+        self.inv_b = int(R.fx_encode(1.0 / batch, s.t)) if self.bb == 0 else 0
+        self.eng = TrioEngine(s)
+
+    def step(self, images, labels):
+        s, eng = self.s, self.eng
+        xs = R.share(R.fx_encode(images, s.t), self.rng)
+        ys = R.share(R.fx_encode(one_hot(labels, self.d), s.t), self.rng)
+        logits, acts = forward(eng, self.layers, self.P, xs, True)
+        g = R.softmax(s, logits) - ys
+        if self.bb == 0:
+            g = R.truncate(s, R.mul_const(g, self.inv_b))
+        grads = backward(eng, self.layers, acts, g, self.bb)
+        self.P = sgd(eng, self.P, grads, self.lr)
+        return R.open_trio(logits)
+
+
 def train_plain_fixed(layers, input_shape, images, labels, lr, batch, iterations, seed=0, t=20, offsets=None):
     """nn.py:754-793."""
     outs, _ = shapes(layers, input_shape)

@@ -287,12 +287,23 @@ def mul(s: Session, x, y):
     return reshare(s, z)
 
 
+_POOL = None
+
+
 def _bilinear3(fn, x, y):
     """z_i = f(x_i, y_i) + f(x_{i+1}, y_i) + f(x_i, y_{i+1}) per party
-    (protocols.py:110-115)."""
-    return np.stack(
-        [fn(x[i], y[i]) + fn(x[(i + 1) % 3], y[i]) + fn(x[i], y[(i + 1) % 3]) for i in range(3)]
-    )
+    (protocols.py:110-115).  The three parties run concurrently, as the
+    reference's three party threads do (session.py:141-152)."""
+    global _POOL
+    if _POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+
+        _POOL = ThreadPoolExecutor(3)
+
+    def party(i):
+        return fn(x[i], y[i]) + fn(x[(i + 1) % 3], y[i]) + fn(x[i], y[(i + 1) % 3])
+
+    return np.stack(list(_POOL.map(party, range(3))))
 
 
 def matmul_shares(s: Session, x, y, bits=None):
