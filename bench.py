@@ -201,27 +201,44 @@ def run_b200(args, ws, rank, local):
     _capi.call = traced_call
     engine.K.call = traced_call
 
-    for i in range(args.warmup):
+    for i in range(max(0, args.warmup - 1)):
         st.step(*batches[i])
+    # capture one iteration as a CUDA graph (static input buffers)
+    xs_static = engine.RssTensor(batches[0][0].data.clone())
+    ys_static = engine.RssTensor(batches[0][1].data.clone())
+    counter["n"] = 0
+    graph = st.capture(xs_static, ys_static)
+    launches_per_step = counter["n"]
+    graph.replay()  # last warm-up step, through the graph
     torch.cuda.synchronize()
     if ws > 1:
         torch.distributed.barrier()
     clocks = Clocks(local)
-    counter["n"] = 0
-    instrument["on"] = True
     step_ms = []
     for i in range(args.steps):
         flush.zero_()
+        xb, yb = batches[args.warmup + i]
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        st.step(*batches[args.warmup + i])
+        xs_static.data.copy_(xb.data)
+        ys_static.data.copy_(yb.data)
+        graph.replay()
         e1.record()
         e1.synchronize()
         step_ms.append(e0.elapsed_time(e1))
     torch.cuda.synchronize()
-    instrument["on"] = False
-    launches = counter["n"]
     clk = clocks.stop()
+    launches = launches_per_step * args.steps
+    # eager instrumented pass (outside the timed region): per-launch CUDA
+    # events around the dominant kernel on its launch stream
+    instrument["on"] = True
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    st.step(*batches[-1])
+    e1.record()
+    torch.cuda.synchronize()
+    instrument["on"] = False
+    eager_ms = e0.elapsed_time(e1)
     total_ms = float(sum(step_ms))
     if ws > 1:
         t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
@@ -245,7 +262,8 @@ def run_b200(args, ws, rank, local):
                 "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": (achieved / hbm_peak) if achieved else None, "traffic": None,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650 GB/s",
-                "share_of_step": sign_ms / max(total_ms, 1e-9) if ws == 1 else None,
+                "share_of_step": sign_ms / max(eager_ms, 1e-9),
+                "measured": "per-launch CUDA events in one eager step after the graph-timed region",
                 "aes_gblocks_s": (23 * sign_elems / 2) / (sign_ms / 1e3) / 1e9 if sign_ms else None,
                 "algorithmic_bytes_per_elem": 72}
 
@@ -269,9 +287,9 @@ def run_b200(args, ws, rank, local):
             y_enc = M.fx_encode(one_hot(labels, 10))
             pin_x.numpy()[...] = host_deal(x_enc)
             pin_y.numpy()[...] = host_deal(y_enc)
-            xs = engine.RssTensor(pin_x.to(dev, non_blocking=True))
-            ys = engine.RssTensor(pin_y.to(dev, non_blocking=True))
-            logits = st.step(xs, ys)
+            xs_static.data.copy_(pin_x, non_blocking=True)
+            ys_static.data.copy_(pin_y, non_blocking=True)
+            logits = graph.replay()
             out_host.copy_(logits.data, non_blocking=True)
             torch.cuda.current_stream().synchronize()
             return (out_host[0] + out_host[1] + out_host[2]).numpy()

@@ -151,6 +151,19 @@ int mpc3_rss_reshare_truncate(const uint32_t* rk3, const uint64_t* ctr, uint64_t
                               int bits, const uint64_t* z, const mpc3_view4* view, uint64_t* out,
                               void* stream);
 
+/* Input gradient epilogue (nn.py:460-484): z holds per-party cross terms
+ * cols[(n,y,x), (c,a,b)] = sum_o g[n,o,y,x] k[o,c,a,b] (a GEMM with inner
+ * length O, instead of the reference's correlation of the dilated, padded
+ * gradient with the flipped kernel).  Each element of the reference's full
+ * output (N, C, hf, wf), hf = (OH-1)*sh + kh, is the col2im sum of its
+ * contributions, reshared and truncated with PRF words at its flat index,
+ * and written at (y'-ph, x'-pw) of out (N, C, H, W) when inside (out must be
+ * zero-initialised; uncovered positions stay 0 as in the reference's embed). */
+int mpc3_rss_col2im_reshare_truncate(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, uint64_t j_rho,
+                                     uint64_t j_r, int bits, const uint64_t* z, int64_t N, int64_t C, int64_t OH,
+                                     int64_t OW, int kh, int kw, int sh, int sw, int ph, int pw, int64_t H,
+                                     int64_t W, uint64_t* out, void* stream);
+
 /* avgpool (protocols.py:139-159): window sums, then truncate(log2 area) when
  * the area is a power of two, else mul_const(mulc) + truncate(t).  x/out are
  * trio NCHW; bits/mulc chosen by the caller (mulc = 1 for power-of-two). */

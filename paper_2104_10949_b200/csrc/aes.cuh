@@ -163,31 +163,31 @@ struct HostTables {
 
 #if defined(__CUDACC__)
 // Shared-memory tables, built once per CTA.
+// Bank-conflict-free lookups: the 1 KiB table is stored 32 times, interleaved
+// so that entry e of lane l's copy sits at word 32 e + l, i.e. always in bank
+// l.  A warp's 32 data-dependent lookups then take one shared-memory
+// wavefront instead of ~4 (random indices over 32 banks).  The final round's
+// S-box is byte 2 of Te0 (Te0[x] = (2S, S, S, 3S)), so no second table.
 struct SmemTables {
-  uint32_t* te;
-  const uint8_t* sbox;
-  DEV uint32_t t0(uint32_t i) const { return te[i]; }
-  DEV uint32_t sb(uint32_t i) const { return sbox[i]; }
+  const uint32_t* te;  // &table[lane]
+  DEV uint32_t t0(uint32_t i) const { return te[i * 32]; }
+  DEV uint32_t sb(uint32_t i) const { return (te[i * 32] >> 8) & 0xff; }
 };
 
-// Shared layout for protocol kernels: T-table, S-box and three key schedules.
+// Shared layout for protocol kernels: lane-interleaved T-table and the
+// three key schedules (33.3 KiB).
 struct AesSmem {
-  uint32_t te[256];
-  uint8_t sbox[256];
+  uint32_t te[256 * 32];
   uint32_t rk[3][44];
 };
 
 // rk_dev: 3 x 44 round-key words (k_0, k_1, k_2 of the session).
 __device__ inline SmemTables aes_smem_init(AesSmem& sm, const uint32_t* __restrict__ rk_dev, int nkeys) {
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-    sm.te[i] = te0_entry(i);
-    sm.sbox[i] = c_sbox[i];
-  }
+  for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) sm.te[i] = te0_entry(i >> 5);
   for (int i = threadIdx.x; i < nkeys * 44; i += blockDim.x) (&sm.rk[0][0])[i] = rk_dev[i];
   __syncthreads();
   SmemTables t;
-  t.te = sm.te;
-  t.sbox = sm.sbox;
+  t.te = sm.te + (threadIdx.x & 31);
   return t;
 }
 #endif

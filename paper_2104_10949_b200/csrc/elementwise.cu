@@ -165,6 +165,17 @@ __global__ void __launch_bounds__(kThreads) pool_kernel(const uint32_t* __restri
   GRID_LOOP(b, (n + 1) >> 1) pool_item(tab, &sm.rk[0][0], backward != 0, hrho, hr, bits, mulc, x, out, p, b);
 }
 
+__global__ void __launch_bounds__(kThreads) col2im_kernel(const uint32_t* __restrict__ rk3,
+                                                         const uint64_t* __restrict__ ctr, StreamRef ra,
+                                                         StreamRef rrho, StreamRef rr, int bits,
+                                                         const uint64_t* __restrict__ z, Col2Im g,
+                                                         uint64_t* __restrict__ out, uint64_t n) {
+  __shared__ AesSmem sm;
+  SmemTables tab = aes_smem_init(sm, rk3, 3);
+  StreamHead ha = resolve(ra, ctr), hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
+  GRID_LOOP(b, (n + 1) >> 1) col2im_item(tab, &sm.rk[0][0], ha, hrho, hr, bits, z, g, out, b);
+}
+
 __global__ void sumpool_kernel(const uint64_t* __restrict__ x, uint64_t* __restrict__ out, PoolGeom p) {
   uint64_t n = (uint64_t)p.N * p.C * p.OH * p.OW;
   GRID_LOOP(f, n) {
@@ -366,6 +377,24 @@ int mpc3_rss_avgpool_backward(const uint32_t* rk3, const uint64_t* ctr, uint64_t
       rk3, ctr, 1, sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, mulc, g, out,
       pool_geom(N, C, H, W, OH, OW, kh, kw, sh, sw), n);
   return check_launch("rss_avgpool_backward");
+}
+
+int mpc3_rss_col2im_reshare_truncate(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, uint64_t j_rho,
+                                     uint64_t j_r, int bits, const uint64_t* z, int64_t N, int64_t C, int64_t OH,
+                                     int64_t OW, int kh, int kw, int sh, int sw, int ph, int pw, int64_t H,
+                                     int64_t W, uint64_t* out, void* stream) {
+  if (bits < 1 || bits > 61) return MPC3_ERR_RANGE;
+  if (kh < 1 || kw < 1 || sh < 1 || sw < 1 || ph < 0 || pw < 0) return MPC3_ERR_SHAPE;
+  Col2Im g;
+  g.N = N; g.C = C; g.OH = OH; g.OW = OW; g.H = H; g.W = W;
+  g.kh = kh; g.kw = kw; g.sh = sh; g.sw = sw; g.ph = ph; g.pw = pw;
+  g.hf = (OH - 1) * sh + kh;
+  g.wf = (OW - 1) * sw + kw;
+  uint64_t n = (uint64_t)N * C * g.hf * g.wf;
+  if (n == 0) return MPC3_OK;
+  col2im_kernel<<<grid_for((n + 1) / 2, kThreads), kThreads, 0, as_stream(stream)>>>(
+      rk3, ctr, sref(ARITH_ZERO, j_arith), sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, z, g, out, n);
+  return check_launch("rss_col2im_reshare_truncate");
 }
 
 int mpc3_ring_sumpool(const uint64_t* x, uint64_t* out, int64_t N, int64_t C, int64_t H, int64_t W, int kh,

@@ -100,6 +100,22 @@ void hc_pool(const uint8_t* keys48, int backward, uint64_t jrho, uint64_t jr, in
               p, b);
 }
 
+void hc_col2im(const uint8_t* keys48, uint64_t ja, uint64_t jrho, uint64_t jr, int bits, const uint64_t* z,
+               int64_t N, int64_t C, int64_t OH, int64_t OW, int kh, int kw, int sh, int sw, int ph, int pw,
+               int64_t H, int64_t W, uint64_t* out) {
+  uint32_t rk[132];
+  expand3(keys48, rk);
+  Col2Im g;
+  g.N = N; g.C = C; g.OH = OH; g.OW = OW; g.H = H; g.W = W;
+  g.kh = kh; g.kw = kw; g.sh = sh; g.sw = sw; g.ph = ph; g.pw = pw;
+  g.hf = (OH - 1) * sh + kh;
+  g.wf = (OW - 1) * sw + kw;
+  uint64_t n = (uint64_t)N * C * g.hf * g.wf;
+  for (uint64_t b = 0; b < (n + 1) / 2; ++b)
+    col2im_item(tabs(), rk, stream_head(ARITH_ZERO, ja), stream_head(TRUNC_RHO, jrho), stream_head(TRUNC_R, jr), bits,
+                z, g, out, b);
+}
+
 void hc_pack(const uint64_t* src, int64_t plane, const mpc3_operand* op, int role, uint8_t* out, int64_t kp) {
   Operand o;
   memset(&o, 0, sizeof(o));

@@ -147,6 +147,65 @@ HD void reshare_trunc_item(const T& tab, const uint32_t* rk3, StreamHead ha, Str
   }
 }
 
+// Input gradient as GEMM + col2im (nn.py:460-484).  z holds, per party, the
+// cross terms cols[(n,y,x), (c,a,b)] = sum_o g[n,o,y,x] k[o,c,a,b]; element
+// (n, c, y', x') of the reference's full correlation output (N,C,hf,wf) is the
+// sum of cols over the (a, b) with y' = y*sh + a, x' = x*sw + b (the
+// transposed convolution), then reshared and truncated with PRF words at its
+// flat index, and embedded at (y'-ph, x'-pw) if inside (H, W).
+struct Col2Im {
+  int64_t N, C, OH, OW, hf, wf, H, W;
+  int kh, kw, sh, sw, ph, pw;
+};
+
+template <class T>
+HD void col2im_item(const T& tab, const uint32_t* rk3, StreamHead ha, StreamHead hrho, StreamHead hr, int bits,
+                    const uint64_t* z, const Col2Im& g, uint64_t* out, uint64_t b) {
+  const uint64_t n_full = (uint64_t)g.N * g.C * g.hf * g.wf;
+  const int64_t ncols = (int64_t)g.C * g.kh * g.kw;
+  const int64_t zplane = (int64_t)g.N * g.OH * g.OW * ncols;
+  const int64_t oplane = g.N * g.C * g.H * g.W;
+  Trio s[2];
+  int64_t ooff[2] = {-1, -1};
+  for (int e = 0; e < 2; ++e) {
+    uint64_t f = 2 * b + e;
+    s[e].c[0] = s[e].c[1] = s[e].c[2] = 0;
+    if (f >= n_full) continue;
+    int64_t xq = f % g.wf, yq = (f / g.wf) % g.hf;
+    int64_t c = (f / (g.wf * g.hf)) % g.C, n = f / (g.wf * g.hf * g.C);
+    int64_t yo = yq - g.ph, xo = xq - g.pw;
+    if (yo < 0 || xo < 0 || yo >= g.H || xo >= g.W) continue;
+    ooff[e] = ((n * g.C + c) * g.H + yo) * g.W + xo;
+    for (int a = 0; a < g.kh; ++a) {
+      int64_t ty = yq - a;
+      if (ty < 0) break;
+      if (ty % g.sh) continue;
+      int64_t y = ty / g.sh;
+      if (y >= g.OH) continue;
+      for (int bb = 0; bb < g.kw; ++bb) {
+        int64_t tx = xq - bb;
+        if (tx < 0) break;
+        if (tx % g.sw) continue;
+        int64_t x = tx / g.sw;
+        if (x >= g.OW) continue;
+        int64_t zi = ((n * g.OH + y) * g.OW + x) * ncols + (c * g.kh + a) * g.kw + bb;
+        for (int i = 0; i < 3; ++i) s[e].c[i] += z[i * zplane + zi];
+      }
+    }
+  }
+  if (ooff[0] < 0 && ooff[1] < 0) return;
+  KeyWords f0, f1;
+  key_words_pair(tab, rk3, ha, b, f0, f1);
+  Word2 rho = prf_block(tab, rk3 + 2 * 44, hrho, b);
+  Word2 r = prf_block(tab, rk3 + 1 * 44, hr, b);
+  for (int e = 0; e < 2; ++e) {
+    if (ooff[e] < 0) continue;
+    Trio t = trio_reshare(s[e], e ? f1 : f0);
+    t = trio_truncate(t, e ? rho.w1 : rho.w0, e ? r.w1 : r.w0, bits);
+    store_trio(out + ooff[e], oplane, 0, t);
+  }
+}
+
 struct PoolGeom {
   int64_t N, C, H, W, OH, OW;
   int kh, kw, sh, sw;
@@ -201,7 +260,34 @@ HD void pack_item(const uint64_t* src, int64_t plane, const Operand& o, int role
   int64_t r = q % o.rows;
   int g = (int)(q / o.rows);
   uint64_t v[8];
-  for (int e = 0; e < 8; ++e) v[e] = packed_value(o, src, plane, role, g, r, ch * 8 + e);
+  const int64_t K = o.k, lim = role == 2 ? K : 2 * K;
+  const int gn = (g + 1) % 3;
+  GatherCursor cur;
+  int half = -1;
+  for (int e = 0; e < 8; ++e) {
+    int64_t kk = ch * 8 + e;
+    if (kk >= lim) {
+      v[e] = 0;
+      continue;
+    }
+    int h = (role != 2 && kk >= K) ? 1 : 0;
+    if (h != half) {  // (re)start the cursor at this half's first k
+      cur.init(o, r, h ? kk - K : kk);
+      half = h;
+    }
+    int64_t off = cur.offset(o);
+    uint64_t val = 0;
+    if (off >= 0) {
+      if (role == 2) {
+        val = src[off];
+      } else {
+        uint64_t self = src[g * plane + off], nxt = src[gn * plane + off];
+        val = role == 0 ? (h == 0 ? self + nxt : self) : (h == 0 ? self : nxt);  // protocols.py:110-115
+      }
+    }
+    v[e] = val;
+    cur.next(o);
+  }
   uint8_t* base = out + ((int64_t)g * 8 * o.rows + r) * kp + ch * 8;
   for (int l = 0; l < 8; ++l) {
     uint64_t word = 0;

@@ -45,6 +45,70 @@ HD int64_t gather_offset(const Operand& o, int64_t r, int64_t k) {
   return n * o.sN + c * o.sC + iy * o.sH + ix * o.sW;
 }
 
+// Incremental gather over consecutive k of one row: the divisions happen once
+// per run (init), each next() is a digit increment with carries.
+struct GatherCursor {
+  int64_t base, iy0, ix0;
+  int64_t d0, d1, d2;
+
+  HD void init(const Operand& o, int64_t r, int64_t k) {
+    if (o.mode == MPC3_GATHER_DENSE) {
+      base = o.off + r * o.s_r;
+      d2 = k % o.K2;
+      int64_t q = k / o.K2;
+      d1 = q % o.K1;
+      d0 = q / o.K1;
+      iy0 = ix0 = 0;
+    } else if (o.mode == MPC3_GATHER_IM2COL) {
+      int64_t x = r % o.ow, q = r / o.ow;
+      int64_t y = q % o.oh, n = q / o.oh;
+      base = n * o.sN;
+      iy0 = y * o.sh - o.ph;
+      ix0 = x * o.sw - o.pw;
+      d2 = k % o.kw;
+      q = k / o.kw;
+      d1 = q % o.kh;
+      d0 = q / o.kh;
+    } else {
+      int64_t v = r % o.kw, q = r / o.kw;
+      int64_t u = q % o.kh, c = q / o.kh;
+      base = c * o.sC;
+      iy0 = u - o.ph;
+      ix0 = v - o.pw;
+      d2 = k % o.ow;
+      q = k / o.ow;
+      d1 = q % o.oh;
+      d0 = q / o.oh;
+    }
+  }
+
+  HD int64_t offset(const Operand& o) const {
+    if (o.mode == MPC3_GATHER_DENSE) return base + d0 * o.t0 + d1 * o.t1 + d2 * o.t2;
+    if (o.mode == MPC3_GATHER_IM2COL) {
+      int64_t iy = iy0 + d1, ix = ix0 + d2;  // dilated coordinates
+      if (iy < 0 || ix < 0 || iy > (o.h - 1) * o.dh || ix > (o.w - 1) * o.dw) return -1;
+      if (o.dh == 1 && o.dw == 1) return base + d0 * o.sC + iy * o.sH + ix * o.sW;
+      if (iy % o.dh || ix % o.dw) return -1;
+      return base + d0 * o.sC + (iy / o.dh) * o.sH + (ix / o.dw) * o.sW;
+    }
+    int64_t iy = d1 * o.sh + iy0, ix = d2 * o.sw + ix0;
+    if (iy < 0 || ix < 0 || iy >= o.h || ix >= o.w) return -1;
+    return base + d0 * o.sN + iy * o.sH + ix * o.sW;
+  }
+
+  HD void next(const Operand& o) {
+    int64_t s2 = o.mode == MPC3_GATHER_DENSE ? o.K2 : (o.mode == MPC3_GATHER_IM2COL ? o.kw : o.ow);
+    int64_t s1 = o.mode == MPC3_GATHER_DENSE ? o.K1 : (o.mode == MPC3_GATHER_IM2COL ? o.kh : o.oh);
+    if (++d2 == s2) {
+      d2 = 0;
+      if (++d1 == s1) {
+        d1 = 0;
+        ++d0;
+      }
+    }
+  }
+};
+
 // Value of the packed operand of group g (party, or 0 for a plain operand) at
 // (r, kk) with kk in [0, 2K) for the cross-term roles (protocols.py:110-115).
 HD uint64_t packed_value(const Operand& o, const uint64_t* src, int64_t plane, int role, int g, int64_t r,

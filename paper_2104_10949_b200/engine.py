@@ -245,8 +245,8 @@ class TrioSession:
     def add(self, a, b):
         return _ew2(K.EW_ADD, a, b)
 
-    def sub(self, a, b):
-        return _ew2(K.EW_SUB, a, b)
+    def sub(self, a, b, out: RssTensor | None = None):
+        return _ew2(K.EW_SUB, a, b, out)
 
     def neg(self, a):
         out = empty(a.shape, a.fp)
@@ -279,7 +279,12 @@ class TrioSession:
     def const_share(self, value, shape) -> RssTensor:
         """Components (c, 0, 0) (sharing.py:184-187)."""
         out = zeros(shape, self.fp)
-        out.data[0] = torch.from_numpy(np.broadcast_to(as_ring(value), shape).astype(U64).view(np.int64)).to(_dev())
+        v = as_ring(value)
+        if v.ndim == 0:  # device fill, no host copy (CUDA-graph safe)
+            c = int(v)
+            out.data[0].fill_(c - (1 << 64) if c >= 1 << 63 else c)
+        else:
+            out.data[0] = torch.from_numpy(np.broadcast_to(v, shape).astype(U64).view(np.int64)).to(_dev())
         return out
 
     # -- multiplication (protocols.py:79-94) --
@@ -468,8 +473,37 @@ class TrioSession:
         return self._finish(z, view, out, bits, "mul.reshare")
 
     def conv2d_dgrad(self, g: RssTensor, k: RssTensor, stride, padding, in_shape, bits) -> RssTensor:
-        """Input gradient (nn.py:460-484): correlation of the dilated, padded
-        output gradient with the flipped kernel, then the embed/crop."""
+        """Input gradient (nn.py:460-484) as a transposed convolution: one
+        ring GEMM cols = g^T-rows x k (inner length O) and a fused
+        col2im + reshare + truncate + embed kernel.  Equal mod 2^64 to the
+        reference's correlation of the dilated, padded gradient with the
+        flipped kernel, with the PRF words at the reference's flat indices."""
+        nb, o, oh, ow = g.shape
+        o2, c, kh, kw = k.shape
+        sh, sw = stride
+        ph, pw = padding
+        h, w = in_shape[-2:]
+        check_accumulation(o * kh * kw)
+        k = k.contiguous()
+        gs = g.data.stride()
+        a_op = K.conv_operand(K.GATHER_IM2COL, nb * oh * ow, o, nb, o, oh, ow, gs[1:], 1, 1, 1, 1, 0, 0, oh, ow)
+        ncols = c * kh * kw
+        b_op = K.dense_operand(ncols, o, s_r=1, t2=ncols)
+        z = self._cross_gemm(g.data, a_op, k.data, b_op, nb * oh * ow, ncols, o)
+        out = zeros((nb, c, h, w), g.fp)
+        ja = self.take(ARITH)
+        jr, jq = self.take(TR_RHO), self.take(TR_R)
+        K.call("mpc3_rss_col2im_reshare_truncate", self.rk, self.ctr_ptr, ja, jr, jq, bits, z.data_ptr(), nb, c, oh,
+               ow, kh, kw, sh, sw, ph, pw, h, w, out.data.data_ptr(), _stream())
+        hf, wf = (oh - 1) * sh + kh, (ow - 1) * sw + kw
+        full = nb * c * hf * wf
+        self.ledger.ring("mul.reshare", full)
+        self._charge_trunc(full)
+        return out
+
+    def conv2d_dgrad_im2col(self, g: RssTensor, k: RssTensor, stride, padding, in_shape, bits) -> RssTensor:
+        """Input gradient by explicit im2col of the dilated, padded gradient
+        (the reference's formulation, kept as a cross-check path)."""
         nb, o, oh, ow = g.shape
         o2, c, kh, kw = k.shape
         sh, sw = stride
@@ -598,9 +632,12 @@ def gemm_splits(M: int, N: int, kp: int, groups: int) -> int:
     return max(need, occ)
 
 
-def _ew2(op, a: RssTensor, b: RssTensor) -> RssTensor:
+def _ew2(op, a: RssTensor, b: RssTensor, out: RssTensor | None = None) -> RssTensor:
     a, b = _broadcast(a, b)
-    out = empty(a.shape, a.fp)
+    if out is None:
+        out = empty(a.shape, a.fp)
+    elif not out.data.is_contiguous() or out.shape != a.shape:
+        raise ShapeError("in-place output must be contiguous and of the operand shape")
     K.call("mpc3_ring_ew", op, a.data.data_ptr(), b.data.data_ptr(), 0, out.data.data_ptr(), 3 * a.numel, _stream())
     return out
 

@@ -238,13 +238,16 @@ class TrioNet:
                 g = g.contiguous().reshape(cached[0])
         return grads
 
-    def sgd(self, params: list, grads: list, lr: float) -> list:
-        """W <- W - truncate(c * grad), c = enc(lr) (nn.py:539-543)."""
+    def sgd(self, params: list, grads: list, lr: float, inplace: bool = False) -> list:
+        """W <- W - truncate(c * grad), c = enc(lr) (nn.py:539-543).  inplace
+        writes the new shares into the parameter buffers (static addresses
+        for CUDA-graph replay)."""
         c = int(fx_encode(lr, self.s.fp))
         if c == 0:
             return list(params)
         S = self.s
-        return [S.sub(p, S.truncate(S.mul_const(g, c))) for p, g in zip(params, grads)]
+        return [S.sub(p, S.truncate(S.mul_const(g, c)), out=p if inplace else None)
+                for p, g in zip(params, grads)]
 
     def loss_grad(self, logits: RssTensor, y: RssTensor) -> RssTensor:
         """softmax(logits) - y (nn.py:561-568)."""
@@ -338,8 +341,70 @@ class TrainState:
         if self.bbits == 0:
             g = S.truncate(S.mul_const(g, self.inv_b))
         grads = net.backward(self.model, acts, g, self.bbits)
-        self.params = net.sgd(self.params, grads, self.cfg.learning_rate)
+        self.params = net.sgd(self.params, grads, self.cfg.learning_rate, inplace=True)
         return logits
+
+    def capture(self, xs: RssTensor, ys: RssTensor) -> "GraphStep":
+        """Record one step as a CUDA graph (see GraphStep)."""
+        return GraphStep(self, xs, ys)
+
+
+class GraphStep:
+    """One training iteration captured as a CUDA graph.
+
+    The ~200 launches of a step replay with one cudaGraphLaunch.  PRF stream
+    counters advance exactly as in the sequential schedule: kernels read
+    j = j_capture + ctr[purpose] where `ctr` is a device buffer set to
+    k * (per-step consumption) before replay k, so replay k draws the same
+    words the k-th eager step would (sharing.py:225-230).  Parameters are
+    updated in place; inputs are read from the static buffers xs / ys.
+    """
+
+    def __init__(self, st: TrainState, xs: RssTensor, ys: RssTensor):
+        import torch
+
+        S = st.sess
+        self.st, self.xs, self.ys = st, xs, ys
+        self.seq0 = dict(S.seq)
+        S.ctr = torch.zeros(8, dtype=torch.int64, device=xs.data.device)
+        self.ctr = S.ctr
+        self.graph = torch.cuda.CUDAGraph()
+        ledger_on = S.ledger.enabled
+        S.ledger.enabled = False
+        try:
+            with torch.cuda.graph(self.graph):
+                self.logits = st.step(xs, ys)
+        finally:
+            S.ledger.enabled = ledger_on
+            S.ctr = None  # the graph keeps the buffer's address; eager calls stay absolute
+        self.delta = {p: S.seq[p] - self.seq0[p] for p in S.seq}
+        S.seq = dict(self.seq0)  # nothing consumed until a replay
+        self.replays = 0
+        # ring of pinned counter buffers; an event guards each against reuse
+        self._host = [torch.zeros(8, dtype=torch.int64).pin_memory() for _ in range(4)]
+        self._done = [None] * 4
+
+    def replay(self):
+        """Run one iteration at the session's current counters, then advance
+        them by one step's consumption (eager calls may interleave)."""
+        import torch
+
+        S = self.st.sess
+        slot = self.replays % 4
+        if self._done[slot] is not None:
+            self._done[slot].synchronize()
+        hv = self._host[slot].numpy()
+        for p in self.delta:
+            hv[p] = S.seq[p] - self.seq0[p]
+        self.ctr.copy_(self._host[slot], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._done[slot] = ev
+        self.graph.replay()
+        self.replays += 1
+        for p, d in self.delta.items():
+            S.seq[p] += d
+        return self.logits
 
 
 def train_trio(sess: TrioSession, model: ModelGraph, cfg: TrainConfig, images: np.ndarray, labels: np.ndarray,

@@ -101,3 +101,12 @@ def gemm_packed(A, B, split_k=16384):
     lib().hc_gemm_packed(ptr(A), ptr(B), ptr(Cm), C.c_int(groups), C.c_int64(M), C.c_int64(N), C.c_int64(kp),
                          C.c_int64(N), C.c_int64(M * N), C.c_int64(split_k))
     return Cm
+
+
+def col2im(keys, ja, jrho, jr, bits, z, N, Cc, OH, OW, kh, kw, sh, sw, ph, pw, H, W):
+    z = np.ascontiguousarray(z, np.uint64)
+    out = np.zeros((3, N, Cc, H, W), np.uint64)
+    lib().hc_col2im(keys48(keys), C.c_uint64(ja), C.c_uint64(jrho), C.c_uint64(jr), C.c_int(bits), ptr(z),
+                    C.c_int64(N), C.c_int64(Cc), C.c_int64(OH), C.c_int64(OW), C.c_int(kh), C.c_int(kw), C.c_int(sh),
+                    C.c_int(sw), C.c_int(ph), C.c_int(pw), C.c_int64(H), C.c_int64(W), ptr(out))
+    return out

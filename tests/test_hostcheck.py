@@ -214,3 +214,30 @@ def test_avgpool_forward_backward(win, stride, shape):
     ref = N.avgpool_backward(N.TrioEngine(s), g, win, stride, shape)
     got = H.pool(s.keys, 1, 0, 0, bits, mulc, g, nb, c, h, w, oh, ow, win[0], win[1], stride[0], stride[1])
     assert np.array_equal(got.reshape(ref.shape), ref)
+
+
+@pytest.mark.parametrize("geom", [((2, 3, 10, 10), (4, 3, 3, 3), (2, 2), (1, 1)),
+                                  ((2, 4, 4, 4), (6, 4, 5, 5), (1, 1), (1, 1)),
+                                  ((1, 3, 32, 32), (8, 3, 11, 11), (4, 4), (9, 9)),
+                                  ((2, 2, 9, 7), (3, 2, 5, 2), (1, 2), (2, 0))])
+def test_dgrad_gemm_col2im_matches_reference_schedule(geom):
+    """Input gradient via cols = g-rows x k (inner length O) + col2im equals the
+    reference's correlation of the dilated/padded gradient with the flipped
+    kernel, including reshare + truncate words and the embed."""
+    xs_, ks_, st, pd = geom
+    rng = np.random.default_rng(sum(xs_) + 1)
+    n, c, h, w = xs_
+    o, _, kh, kw = ks_
+    oh, ow = R.conv_out_hw(h, w, kh, kw, st, pd)
+    g = R.share(R.fx_encode(rng.uniform(-1, 1, (n, o, oh, ow))), rng)
+    k = R.share(R.fx_encode(rng.uniform(-0.5, 0.5, ks_)), rng)
+    s = R.Session(4)
+    ref = N.conv_grad_input(N.TrioEngine(s), g, k, N.conv(o, (kh, kw), st, pd), (n, c, h, w), 20)
+    ncols = c * kh * kw
+    kp = (2 * o + 15) // 16 * 16
+    A = H.pack(g, g[0].size, _capi.conv_operand(_capi.GATHER_IM2COL, n * oh * ow, o, n, o, oh, ow,
+                                                (o * oh * ow, oh * ow, ow, 1), 1, 1, 1, 1, 0, 0, oh, ow), 0, kp)
+    B = H.pack(k, k[0].size, _capi.dense_operand(ncols, o, s_r=1, t2=ncols), 1, kp)
+    z = H.gemm_packed(A, B)
+    got = H.col2im(R.Session(4).keys, 0, 0, 0, 20, z, n, c, oh, ow, kh, kw, st[0], st[1], pd[0], pd[1], h, w)
+    assert np.array_equal(got, ref)
