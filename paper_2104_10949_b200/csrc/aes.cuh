@@ -128,6 +128,12 @@ HD void aes128_block(const T& tab, const uint32_t* rk, uint32_t& s0, uint32_t& s
   s3 = t3 ^ k[3];
 }
 
+#if defined(__CUDACC__)
+struct SmemTables;
+HD void aes128_block(const SmemTables& tab, const uint32_t* rk, uint32_t& s0, uint32_t& s1, uint32_t& s2,
+                     uint32_t& s3);
+#endif
+
 // Words 2b and 2b+1 of stream (head, key).
 struct Word2 {
   uint64_t w0, w1;
@@ -176,10 +182,64 @@ struct SmemTables {
 
 // Shared layout for protocol kernels: lane-interleaved T-table and the
 // three key schedules (33.3 KiB).
-struct AesSmem {
+struct __align__(16) AesSmem {
   uint32_t te[256 * 32];
   uint32_t rk[3][44];
 };
+
+// Device rounds on the lane-interleaved table: each lookup is one byte
+// extract (PRMT / SHF), one LEA (idx * 128 B + lane base) and one LDS; the
+// generic template above is the host self-check path.
+HD void aes128_block(const SmemTables& tab, const uint32_t* rk, uint32_t& s0, uint32_t& s1, uint32_t& s2,
+                     uint32_t& s3) {
+#if defined(__CUDA_ARCH__)
+  const uint32_t* T = tab.te;
+#define LK(x) T[(x) << 5]
+#define B3(x) ((x) >> 24)
+#define B2(x) __byte_perm((x), 0, 0x4442)
+#define B1(x) __byte_perm((x), 0, 0x4441)
+#define B0(x) ((x)&0xffu)
+  s0 ^= rk[0];
+  s1 ^= rk[1];
+  s2 ^= rk[2];
+  s3 ^= rk[3];
+#pragma unroll 1
+  for (int r = 1; r < 10; ++r) {
+    const uint4 k = *reinterpret_cast<const uint4*>(rk + 4 * r);
+    uint32_t t0 = LK(B3(s0)) ^ __funnelshift_r(LK(B2(s1)), LK(B2(s1)), 8) ^
+                  __funnelshift_r(LK(B1(s2)), LK(B1(s2)), 16) ^ __funnelshift_r(LK(B0(s3)), LK(B0(s3)), 24) ^ k.x;
+    uint32_t t1 = LK(B3(s1)) ^ __funnelshift_r(LK(B2(s2)), LK(B2(s2)), 8) ^
+                  __funnelshift_r(LK(B1(s3)), LK(B1(s3)), 16) ^ __funnelshift_r(LK(B0(s0)), LK(B0(s0)), 24) ^ k.y;
+    uint32_t t2 = LK(B3(s2)) ^ __funnelshift_r(LK(B2(s3)), LK(B2(s3)), 8) ^
+                  __funnelshift_r(LK(B1(s0)), LK(B1(s0)), 16) ^ __funnelshift_r(LK(B0(s1)), LK(B0(s1)), 24) ^ k.z;
+    uint32_t t3 = LK(B3(s3)) ^ __funnelshift_r(LK(B2(s0)), LK(B2(s0)), 8) ^
+                  __funnelshift_r(LK(B1(s1)), LK(B1(s1)), 16) ^ __funnelshift_r(LK(B0(s2)), LK(B0(s2)), 24) ^ k.w;
+    s0 = t0;
+    s1 = t1;
+    s2 = t2;
+    s3 = t3;
+  }
+  // final round: S[x] is byte 2 of Te0[x] = (2S, S, S, 3S)
+  const uint4 k = *reinterpret_cast<const uint4*>(rk + 40);
+  uint32_t t0 = (LK(B3(s0)) & 0x00ff0000u) << 8 | (LK(B2(s1)) & 0x00ff0000u) | (LK(B1(s2)) & 0x0000ff00u) |
+                (LK(B0(s3)) >> 8 & 0xffu);
+  uint32_t t1 = (LK(B3(s1)) & 0x00ff0000u) << 8 | (LK(B2(s2)) & 0x00ff0000u) | (LK(B1(s3)) & 0x0000ff00u) |
+                (LK(B0(s0)) >> 8 & 0xffu);
+  uint32_t t2 = (LK(B3(s2)) & 0x00ff0000u) << 8 | (LK(B2(s3)) & 0x00ff0000u) | (LK(B1(s0)) & 0x0000ff00u) |
+                (LK(B0(s1)) >> 8 & 0xffu);
+  uint32_t t3 = (LK(B3(s3)) & 0x00ff0000u) << 8 | (LK(B2(s0)) & 0x00ff0000u) | (LK(B1(s1)) & 0x0000ff00u) |
+                (LK(B0(s2)) >> 8 & 0xffu);
+  s0 = t0 ^ k.x;
+  s1 = t1 ^ k.y;
+  s2 = t2 ^ k.z;
+  s3 = t3 ^ k.w;
+#undef LK
+#undef B3
+#undef B2
+#undef B1
+#undef B0
+#endif
+}
 
 // rk_dev: 3 x 44 round-key words (k_0, k_1, k_2 of the session).
 __device__ inline SmemTables aes_smem_init(AesSmem& sm, const uint32_t* __restrict__ rk_dev, int nkeys) {
