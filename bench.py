@@ -49,6 +49,7 @@ def _args():
     ap.add_argument("--batch", type=int, default=BATCH)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-resnet", action="store_true", help="skip the ResNet-50 inference side measurement")
     return ap.parse_args()
 
 
@@ -319,8 +320,17 @@ def run_b200(args, ws, rank, local):
                "sample": f"one AlexNet-CIFAR private train step at batch {CPU_SAMPLE_BATCH} "
                          f"(oracle port of the reference, numpy/OpenBLAS, 3 party threads)"}
 
+    also = {}
+    if not args.no_resnet:
+        try:
+            also["resnet50_b64"] = resnet50_inference(dev, 64, 2, use_graph=False)
+            also["resnet50_b1"] = resnet50_inference(dev, 1, 5, use_graph=True)
+        except Exception as e:  # noqa: BLE001 - reported, not fatal to the headline
+            also["resnet50_error"] = repr(e)[:300]
+
     if rank == 0:
         line = {
+            "also": also,
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64 ring (int)", "data": "synthetic",
@@ -331,6 +341,40 @@ def run_b200(args, ws, rank, local):
         print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
+
+
+def resnet50_inference(dev, batch: int, steps: int, use_graph: bool):
+    """ResNet-50 private inference (configs[3]), device-resident dealt input,
+    CUDA-event timed per batch with an L2 flush before each; images/s."""
+    import torch
+
+    import paper_2104_10949_b200 as M
+    from paper_2104_10949_b200.nn import InferenceGraph, TrioNet
+
+    sess = M.TrioSession(seed=11)
+    model = M.models.resnet50()
+    rng = np.random.default_rng(11)
+    params = [sess.share(w, rng) for w in M.init_params(model, seed=11)]
+    x = sess.share(M.fx_encode(rng.uniform(0, 1, (batch, 3, 224, 224))), rng)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    net = TrioNet(sess)
+    run = (lambda g=InferenceGraph(sess, model, params, x): g.replay()) if use_graph else \
+        (lambda: net.forward(model, params, x, record=False)[0])
+    run()
+    torch.cuda.synchronize()
+    ms = []
+    for _ in range(steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        run()
+        e1.record()
+        e1.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    t = float(np.mean(ms))
+    return {"workload": f"ResNet-50 v1.5 private inference, ImageNet 3x224x224, batch {batch}",
+            "value": batch / (t / 1e3), "unit": "images/s", "ms_per_batch": t, "steps": steps,
+            "cuda_graph": use_graph, "data": "synthetic (random-init folded-BN weights, U(0,1) images)"}
 
 
 def main():

@@ -166,17 +166,19 @@ int mpc3_rss_col2im_reshare_truncate(const uint32_t* rk3, const uint64_t* ctr, u
 
 /* avgpool (protocols.py:139-159): window sums, then truncate(log2 area) when
  * the area is a power of two, else mul_const(mulc) + truncate(t).  x/out are
- * trio NCHW; bits/mulc chosen by the caller (mulc = 1 for power-of-two). */
+ * trio NCHW; bits/mulc chosen by the caller (mulc = 1 for power-of-two).
+ * ph/pw: zero padding with the full window area as divisor (the reference
+ * has no padded pooling; used by ResNet's stem, composed as pad + avgpool). */
 int mpc3_rss_avgpool(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_rho, uint64_t j_r, int bits, uint64_t mulc,
                      const uint64_t* x, uint64_t* out, int64_t N, int64_t C, int64_t H, int64_t W,
-                     int kh, int kw, int sh, int sw, void* stream);
+                     int kh, int kw, int sh, int sw, int ph, int pw, void* stream);
 
 /* avgpool backward (nn.py:487-499): scatter-add of g into the windows, then
  * div_area (truncate / mul_const+truncate) — fused. g: (N,C,OH,OW) trio;
  * out: (N,C,H,W) trio. */
 int mpc3_rss_avgpool_backward(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_rho, uint64_t j_r, int bits, uint64_t mulc,
                               const uint64_t* g, uint64_t* out, int64_t N, int64_t C, int64_t H,
-                              int64_t W, int64_t OH, int64_t OW, int kh, int kw, int sh, int sw,
+                              int64_t W, int64_t OH, int64_t OW, int kh, int kw, int sh, int sw, int ph, int pw,
                               void* stream);
 
 /* Plain sum-pool of one ring tensor (ring.py:259-268). */

@@ -22,6 +22,9 @@ U64 = R.U64
 CONV, FC, POOL, RELU, FLAT = "Conv2d", "FullyConnected", "AvgPool", "ReLU", "Flatten"
 
 
+RES = "Residual"
+
+
 @dataclass(frozen=True)
 class Layer:
     kind: str
@@ -30,6 +33,19 @@ class Layer:
     stride: tuple = (1, 1)
     padding: tuple = (0, 0)
     window: tuple = ()
+    bias: bool = False
+    main: tuple = ()
+    shortcut: tuple = ()
+
+
+def from_spec(spec):
+    """Oracle layer from a product LayerSpec (so composed models are built once)."""
+    kind = spec.kind
+    return Layer(kind, out=spec.out_channels or spec.out_features, kernel=tuple(spec.kernel),
+                 stride=tuple(spec.stride), padding=tuple(spec.padding), window=tuple(spec.window),
+                 bias=bool(getattr(spec, "bias", False)),
+                 main=tuple(from_spec(s) for s in getattr(spec, "main", ())),
+                 shortcut=tuple(from_spec(s) for s in getattr(spec, "shortcut", ())))
 
 
 def _p(v):
@@ -443,3 +459,37 @@ def train_plain_fixed(layers, input_shape, images, labels, lr, batch, iterations
 
 def infer_private(s: R.Session, layers, params_trio, x_trio):
     return forward(TrioEngine(s), layers, params_trio, x_trio, False)[0]
+
+
+def forward_ext(s: R.Session, layers, it, h):
+    """Inference with the ResNet extensions, COMPOSED from reference
+    primitives (no reference model has them): conv2d_shares /
+    matmul_shares then a local add of the shared bias; residual = local add of
+    the two branches; padded average pool = zero-pad each component, then
+    avgpool_shares (protocols.py:139-159)."""
+    for L in layers:
+        if L.kind == CONV:
+            h = R.conv2d_shares(s, h, next(it), L.stride, L.padding)
+            if L.bias:
+                b = next(it)
+                h = h + b[:, None, :, None, None]
+        elif L.kind == FC:
+            w = next(it)
+            h = R.matmul_shares(s, h, np.stack([w[i].T for i in range(3)]))
+            if L.bias:
+                b = next(it)
+                h = h + b[:, None, :]
+        elif L.kind == POOL:
+            ph, pw = L.padding
+            if ph or pw:
+                h = np.pad(h, ((0, 0), (0, 0), (0, 0), (ph, ph), (pw, pw)))
+            h = R.avgpool_shares(s, h, L.window, L.stride)
+        elif L.kind == RELU:
+            h = R.relu(s, h)
+        elif L.kind == FLAT:
+            h = h.reshape(3, h.shape[1], -1)
+        elif L.kind == RES:
+            hm = forward_ext(s, L.main, it, h) if L.main else h
+            hs = forward_ext(s, L.shortcut, it, h) if L.shortcut else h
+            h = hm + hs
+    return h

@@ -118,18 +118,20 @@ struct SignArgs {
   uint64_t jbin, jxor, ja;
 };
 
-__global__ void __launch_bounds__(kThreads) sign_kernel(const uint32_t* __restrict__ rk3,
-                                                       const uint64_t* __restrict__ ctr, SignArgs args,
-                                                       int mode, const uint64_t* __restrict__ x,
-                                                       uint64_t* __restrict__ out,
-                                                       uint64_t* __restrict__ mask, uint64_t n,
-                                                       uint64_t n_total, uint64_t elem_off) {
+__global__ void __launch_bounds__(kThreads, 3) sign_kernel(const uint32_t* __restrict__ rk3,
+                                                          const uint64_t* __restrict__ ctr, SignArgs args,
+                                                          int mode, const uint64_t* __restrict__ x,
+                                                          uint64_t* __restrict__ out,
+                                                          uint64_t* __restrict__ mask, uint64_t n,
+                                                          uint64_t n_total, uint64_t elem_off) {
   __shared__ AesSmem sm;
-  SmemTables tab = aes_smem_init(sm, rk3, 3);
-  SignStreams st;
-  st.bin = resolve(sref(BIN_INPUT, args.jbin), ctr);
-  for (int l = 0; l < 7; ++l) st.x[l] = resolve(sref(XOR_ZERO, args.jxor + l), ctr);
-  for (int l = 0; l < 3; ++l) st.a[l] = resolve(sref(ARITH_ZERO, args.ja + l), ctr);
+  __shared__ SignStreams st;  // uniform stream heads, indexed by level from shared memory
+  if (threadIdx.x == 0) {
+    st.bin = resolve(sref(BIN_INPUT, args.jbin), ctr);
+    for (int l = 0; l < 7; ++l) st.x[l] = resolve(sref(XOR_ZERO, args.jxor + l), ctr);
+    for (int l = 0; l < 3; ++l) st.a[l] = resolve(sref(ARITH_ZERO, args.ja + l), ctr);
+  }
+  SmemTables tab = aes_smem_init(sm, rk3, 3);  // includes the barrier
   GRID_LOOP(b, (n + 1) >> 1) sign_item(tab, &sm.rk[0][0], st, mode, x, out, mask, n, n_total, elem_off, b);
 }
 
@@ -345,37 +347,38 @@ int mpc3_rss_reshare_truncate(const uint32_t* rk3, const uint64_t* ctr, uint64_t
 }
 
 static PoolGeom pool_geom(int64_t N, int64_t C, int64_t H, int64_t W, int64_t OH, int64_t OW, int kh, int kw,
-                          int sh, int sw) {
+                          int sh, int sw, int ph = 0, int pw = 0) {
   PoolGeom p;
   p.N = N; p.C = C; p.H = H; p.W = W; p.OH = OH; p.OW = OW;
-  p.kh = kh; p.kw = kw; p.sh = sh; p.sw = sw;
+  p.kh = kh; p.kw = kw; p.sh = sh; p.sw = sw; p.ph = ph; p.pw = pw;
   return p;
 }
 
 int mpc3_rss_avgpool(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_rho, uint64_t j_r, int bits, uint64_t mulc,
                      const uint64_t* x, uint64_t* out, int64_t N, int64_t C, int64_t H, int64_t W, int kh,
-                     int kw, int sh, int sw, void* stream) {
+                     int kw, int sh, int sw, int ph, int pw, void* stream) {
   if (bits < 1 || bits > 61) return MPC3_ERR_RANGE;
-  if (kh < 1 || kw < 1 || sh < 1 || sw < 1 || H < kh || W < kw) return MPC3_ERR_SHAPE;
-  int64_t OH = (H - kh) / sh + 1, OW = (W - kw) / sw + 1;
+  if (kh < 1 || kw < 1 || sh < 1 || sw < 1 || ph < 0 || pw < 0 || H + 2 * ph < kh || W + 2 * pw < kw)
+    return MPC3_ERR_SHAPE;
+  int64_t OH = (H + 2 * ph - kh) / sh + 1, OW = (W + 2 * pw - kw) / sw + 1;
   uint64_t n = (uint64_t)N * C * OH * OW;
   if (n == 0) return MPC3_OK;
   pool_kernel<<<grid_for((n + 1) / 2, kThreads), kThreads, 0, as_stream(stream)>>>(
       rk3, ctr, 0, sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, mulc, x, out,
-      pool_geom(N, C, H, W, OH, OW, kh, kw, sh, sw), n);
+      pool_geom(N, C, H, W, OH, OW, kh, kw, sh, sw, ph, pw), n);
   return check_launch("rss_avgpool");
 }
 
 int mpc3_rss_avgpool_backward(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_rho, uint64_t j_r, int bits, uint64_t mulc,
                               const uint64_t* g, uint64_t* out, int64_t N, int64_t C, int64_t H, int64_t W,
-                              int64_t OH, int64_t OW, int kh, int kw, int sh, int sw, void* stream) {
+                              int64_t OH, int64_t OW, int kh, int kw, int sh, int sw, int ph, int pw, void* stream) {
   if (bits < 1 || bits > 61) return MPC3_ERR_RANGE;
-  if (kh < 1 || kw < 1 || sh < 1 || sw < 1) return MPC3_ERR_SHAPE;
+  if (kh < 1 || kw < 1 || sh < 1 || sw < 1 || ph < 0 || pw < 0) return MPC3_ERR_SHAPE;
   uint64_t n = (uint64_t)N * C * H * W;
   if (n == 0) return MPC3_OK;
   pool_kernel<<<grid_for((n + 1) / 2, kThreads), kThreads, 0, as_stream(stream)>>>(
       rk3, ctr, 1, sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, mulc, g, out,
-      pool_geom(N, C, H, W, OH, OW, kh, kw, sh, sw), n);
+      pool_geom(N, C, H, W, OH, OW, kh, kw, sh, sw, ph, pw), n);
   return check_launch("rss_avgpool_backward");
 }
 

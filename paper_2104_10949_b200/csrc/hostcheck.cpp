@@ -88,12 +88,12 @@ void hc_reshare_truncate(const uint8_t* keys48, uint64_t ja, uint64_t jrho, uint
 
 void hc_pool(const uint8_t* keys48, int backward, uint64_t jrho, uint64_t jr, int bits, uint64_t mulc,
              const uint64_t* x, uint64_t* out, int64_t N, int64_t C, int64_t H, int64_t W, int64_t OH, int64_t OW,
-             int kh, int kw, int sh, int sw) {
+             int kh, int kw, int sh, int sw, int ph, int pw) {
   uint32_t rk[132];
   expand3(keys48, rk);
   PoolGeom p;
   p.N = N; p.C = C; p.H = H; p.W = W; p.OH = OH; p.OW = OW;
-  p.kh = kh; p.kw = kw; p.sh = sh; p.sw = sw;
+  p.kh = kh; p.kw = kw; p.sh = sh; p.sw = sw; p.ph = ph; p.pw = pw;
   uint64_t n = backward ? (uint64_t)N * C * H * W : (uint64_t)N * C * OH * OW;
   for (uint64_t b = 0; b < (n + 1) / 2; ++b)
     pool_item(tabs(), rk, backward != 0, stream_head(TRUNC_RHO, jrho), stream_head(TRUNC_R, jr), bits, mulc, x, out,

@@ -78,10 +78,14 @@ template <class T>
 HD void sign_item(const T& tab, const uint32_t* rk3, const SignStreams& st, int mode, const uint64_t* x,
                   uint64_t* out, uint64_t* mask, uint64_t n, uint64_t n_total, uint64_t elem_off, uint64_t b) {
   bool two = 2 * b + 1 < n;
-  Trio v[2], o[2], m[2];
-  v[0] = load_trio(x, n, 2 * b);
-  v[1] = two ? load_trio(x, n, 2 * b + 1) : v[0];
-  sign_circuit_pair(tab, rk3, st, n_total, (elem_off >> 1) + b, mode, v, o, m);
+  Trio o[2], m[2];
+  struct Loader {
+    const uint64_t* x;
+    uint64_t n, e0;
+    bool two;
+    HD Trio operator()(int e) const { return load_trio(x, n, (e && two) ? e0 + 1 : e0); }
+  } ld{x, n, 2 * b, two};
+  sign_circuit_pair(tab, rk3, st, n_total, (elem_off >> 1) + b, mode, ld, o, m);
   store_trio(out, n, 2 * b, o[0]);
   if (two) store_trio(out, n, 2 * b + 1, o[1]);
   if (mode == MODE_RELU && mask) {
@@ -209,6 +213,7 @@ HD void col2im_item(const T& tab, const uint32_t* rk3, StreamHead ha, StreamHead
 struct PoolGeom {
   int64_t N, C, H, W, OH, OW;
   int kh, kw, sh, sw;
+  int ph, pw;  // zero padding (count_include_pad): the window area stays kh*kw
 };
 
 // fused window sum (x mulc) + truncate; backward = scatter-add then the same
@@ -224,13 +229,20 @@ HD void pool_item(const T& tab, const uint32_t* rk3, bool backward, StreamHead h
     if (f >= n) continue;
     if (!backward) {
       int64_t ox = f % p.OW, oy = (f / p.OW) % p.OH, nc = f / (p.OW * p.OH);
-      const uint64_t* base = x + nc * p.H * p.W + (oy * p.sh) * p.W + ox * p.sw;
-      for (int u = 0; u < p.kh; ++u)
-        for (int q = 0; q < p.kw; ++q)
-          for (int i = 0; i < 3; ++i) s[e].c[i] += base[i * nin + u * p.W + q];
+      int64_t y0 = oy * p.sh - p.ph, x0 = ox * p.sw - p.pw;
+      const uint64_t* base = x + nc * p.H * p.W;
+      for (int u = 0; u < p.kh; ++u) {
+        int64_t iy = y0 + u;
+        if (iy < 0 || iy >= p.H) continue;
+        for (int q = 0; q < p.kw; ++q) {
+          int64_t ix = x0 + q;
+          if (ix < 0 || ix >= p.W) continue;
+          for (int i = 0; i < 3; ++i) s[e].c[i] += base[i * nin + iy * p.W + ix];
+        }
+      }
     } else {
-      // windows (oy, ox) with oy*sh <= iy < oy*sh + kh, oy < OH (nn.py:487-499)
-      int64_t ix = f % p.W, iy = (f / p.W) % p.H, nc = f / (p.W * p.H);
+      // windows (oy, ox) with oy*sh - ph <= iy < oy*sh - ph + kh, oy < OH (nn.py:487-499)
+      int64_t ix = f % p.W + p.pw, iy = (f / p.W) % p.H + p.ph, nc = f / (p.W * p.H);
       for (int64_t oy = iy / p.sh; oy >= 0 && oy * p.sh + p.kh > iy; --oy) {
         if (oy >= p.OH) continue;
         for (int64_t ox = ix / p.sw; ox >= 0 && ox * p.sw + p.kw > ix; --ox) {

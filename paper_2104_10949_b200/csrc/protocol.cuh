@@ -120,65 +120,121 @@ HD KeyWords key_words_one(const T& tab, const uint32_t* rk3, StreamHead h, uint6
   return o;
 }
 
+// Local products WITHOUT randomness or relabel; the zero-share words are
+// folded in key by key below so only one AES block (2 words) is live at a
+// time (register pressure of the fused sign kernel).
+HD Trio and_local(const Trio& a, const Trio& b) {
+  Trio z;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    int n = (i + 1) % 3;
+    z.c[i] = (a.c[i] & b.c[i]) ^ (a.c[n] & b.c[i]) ^ (a.c[i] & b.c[n]);
+  }
+  return z;
+}
+HD Trio mul_local(const Trio& x, const Trio& y) {
+  Trio z;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    int n = (i + 1) % 3;
+    z.c[i] = x.c[i] * y.c[i] + x.c[n] * y.c[i] + x.c[i] * y.c[n];
+  }
+  return z;
+}
+HD Trio relabel(const Trio& z) {
+  Trio o;
+  o.c[1] = z.c[0];
+  o.c[2] = z.c[1];
+  o.c[0] = z.c[2];
+  return o;
+}
+// F(k_k) enters z_k (as +/^ F_i) and z_{k+1} (as -/^ F_{i-1}) (sharing.py:233-250)
+HD void fold_word(Trio& z, int k, uint64_t w, bool xor_mode) {
+  int k1 = (k + 1) % 3;
+  if (xor_mode) {
+    z.c[k] ^= w;
+    z.c[k1] ^= w;
+  } else {
+    z.c[k] += w;
+    z.c[k1] -= w;
+  }
+}
+template <class T>
+HD void fold_pair(const T& tab, const uint32_t* rk3, StreamHead h, uint64_t blk, Trio z[2], bool xor_mode) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {  // unrolled: k indexes registers
+    Word2 w = prf_block(tab, rk3 + 44 * k, h, blk);
+    fold_word(z[0], k, w.w0, xor_mode);
+    fold_word(z[1], k, w.w1, xor_mode);
+  }
+}
+// the pair's words sit at stream words w, w+1 that may straddle two blocks
+template <class T>
+HD void fold_words(const T& tab, const uint32_t* rk3, StreamHead h, uint64_t w, Trio z[2], bool xor_mode) {
+  if ((w & 1) == 0) {
+    fold_pair(tab, rk3, h, w >> 1, z, xor_mode);
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    fold_word(z[0], k, prf_block(tab, rk3 + 44 * k, h, w >> 1).w1, xor_mode);
+    fold_word(z[1], k, prf_block(tab, rk3 + 44 * k, h, (w + 1) >> 1).w0, xor_mode);
+  }
+}
+
 // The fused sign circuit for the element pair (2*blk, 2*blk+1) of a tensor of
 // n_total elements (n_total sets where the Kogge-Stone p-half lives, word
-// n_total + e, protocols.py:247-259).  valid1 = second element exists.
+// n_total + e, protocols.py:247-259).  x is read through `ld` (local element
+// index e0, e0+1; second element absent => duplicate of the first, results
+// discarded by the caller), twice, so the input shares need not stay live
+// across the 7 AND levels.
 // Outputs: out[e] (binary or arithmetic per mode) and, for MODE_RELU, mask[e].
 // AES blocks per element pair: BIN 1, XOR 3 + 6*(3 + 3) - 3 (the last
 // level's p-half is dead: p is never read after the loop, protocols.py:259-263),
 // ARITH 3 per mul.
-template <class T>
+template <class T, class Ld>
 HD void sign_circuit_pair(const T& tab, const uint32_t* rk3, const SignStreams& st, uint64_t n_total,
-                          uint64_t blk, int mode, const Trio x[2], Trio out[2], Trio mask[2]) {
+                          uint64_t blk, int mode, const Ld& ld, Trio out[2], Trio mask[2]) {
   // a2b input sharing (protocols.py:278-295): w = ((c0+c1)^r, r, 0), x2 = (0,0,c2)
-  Word2 rb = prf_block(tab, rk3 + 0 * 44, st.bin, blk);
-  Trio a[2], b[2], p[2], g[2], pleaf[2];
+  const Word2 rb = prf_block(tab, rk3 + 0 * 44, st.bin, blk);
+  Trio p[2], g[2];
   for (int e = 0; e < 2; ++e) {
+    Trio x = ld(e);
     uint64_t r = e ? rb.w1 : rb.w0;
-    a[e].c[0] = (x[e].c[0] + x[e].c[1]) ^ r;
-    a[e].c[1] = r;
-    a[e].c[2] = 0;
-    b[e].c[0] = 0;
-    b[e].c[1] = 0;
-    b[e].c[2] = x[e].c[2];
-    p[e] = trio_xor(a[e], b[e]);
-    pleaf[e] = p[e];
+    Trio a = {{(x.c[0] + x.c[1]) ^ r, r, 0}};
+    Trio b = {{0, 0, x.c[2]}};
+    p[e] = trio_xor(a, b);
+    g[e] = and_local(a, b);
   }
-  {
-    KeyWords f0, f1;
-    key_words_pair(tab, rk3, st.x[0], blk, f0, f1);
-    g[0] = trio_and(a[0], b[0], f0);
-    g[1] = trio_and(a[1], b[1], f1);
-  }
-  const bool even_n = (n_total & 1) == 0;
+  fold_pair(tab, rk3, st.x[0], blk, g, true);
+  g[0] = relabel(g[0]);
+  g[1] = relabel(g[1]);
 #if defined(__CUDA_ARCH__)
 #pragma unroll 1
 #endif
   for (int lvl = 1; lvl <= 6; ++lvl) {
     const int d = 1 << (lvl - 1);
-    KeyWords f0, f1;
-    key_words_pair(tab, rk3, st.x[lvl], blk, f0, f1);
-    Trio gt0 = trio_and(p[0], trio_shl(g[0], d), f0);
-    Trio gt1 = trio_and(p[1], trio_shl(g[1], d), f1);
+    Trio t[2];
+    t[0] = and_local(p[0], trio_shl(g[0], d));
+    t[1] = and_local(p[1], trio_shl(g[1], d));
+    fold_pair(tab, rk3, st.x[lvl], blk, t, true);
+    g[0] = trio_xor(g[0], relabel(t[0]));
+    g[1] = trio_xor(g[1], relabel(t[1]));
     if (lvl < 6) {
-      KeyWords q0, q1;
-      uint64_t w = n_total + 2 * blk;
-      if (even_n) {
-        key_words_pair(tab, rk3, st.x[lvl], w >> 1, q0, q1);
-      } else {
-        q0 = key_words_one(tab, rk3, st.x[lvl], w);
-        q1 = key_words_one(tab, rk3, st.x[lvl], w + 1);
-      }
-      Trio pt0 = trio_and(p[0], trio_shl(p[0], d), q0);
-      Trio pt1 = trio_and(p[1], trio_shl(p[1], d), q1);
-      p[0] = pt0;
-      p[1] = pt1;
+      t[0] = and_local(p[0], trio_shl(p[0], d));
+      t[1] = and_local(p[1], trio_shl(p[1], d));
+      fold_words(tab, rk3, st.x[lvl], n_total + 2 * blk, t, true);
+      p[0] = relabel(t[0]);
+      p[1] = relabel(t[1]);
     }
-    g[0] = trio_xor(g[0], gt0);
-    g[1] = trio_xor(g[1], gt1);
   }
   Trio s[2];
-  for (int e = 0; e < 2; ++e) s[e] = trio_xor(pleaf[e], trio_shl(g[e], 1));
+  for (int e = 0; e < 2; ++e) {  // sum = p_leaf ^ (g << 1), p_leaf rebuilt from x and r
+    Trio x = ld(e);
+    uint64_t r = e ? rb.w1 : rb.w0;
+    Trio pleaf = {{(x.c[0] + x.c[1]) ^ r, r, x.c[2]}};
+    s[e] = trio_xor(pleaf, trio_shl(g[e], 1));
+  }
   if (mode == MODE_A2B) {
     out[0] = s[0];
     out[1] = s[1];
@@ -193,33 +249,37 @@ HD void sign_circuit_pair(const T& tab, const uint32_t* rk3, const SignStreams& 
     return;
   }
   // bit_inject (protocols.py:304-331): u = s0 + s1 - 2 mul(s0, s1); v = u + s2 - 2 mul(u, s2)
-  Trio m[2];
-  {
-    KeyWords f0, f1, h0, h1;
-    key_words_pair(tab, rk3, st.a[0], blk, f0, f1);
-    key_words_pair(tab, rk3, st.a[1], blk, h0, h1);
-    for (int e = 0; e < 2; ++e) {
-      Trio t0 = {{bit[e].c[0], 0, 0}}, t1 = {{0, bit[e].c[1], 0}}, t2 = {{0, 0, bit[e].c[2]}};
-      Trio pr = trio_mul(t0, t1, e ? f1 : f0);
-      Trio u;
-      for (int i = 0; i < 3; ++i) u.c[i] = t0.c[i] + t1.c[i] - 2 * pr.c[i];
-      Trio pv = trio_mul(u, t2, e ? h1 : h0);
-      Trio v;
-      for (int i = 0; i < 3; ++i) v.c[i] = u.c[i] + t2.c[i] - 2 * pv.c[i];
-      // drelu = 1 - v: negate, constant into component 0 (protocols.py:57-66, 334-337)
-      for (int i = 0; i < 3; ++i) m[e].c[i] = 0 - v.c[i];
-      m[e].c[0] += 1;
-    }
+  Trio u[2], m[2];
+  for (int e = 0; e < 2; ++e) {
+    Trio t0 = {{bit[e].c[0], 0, 0}}, t1 = {{0, bit[e].c[1], 0}};
+    u[e] = mul_local(t0, t1);
+  }
+  fold_pair(tab, rk3, st.a[0], blk, u, false);
+  for (int e = 0; e < 2; ++e) {
+    Trio pr = relabel(u[e]);
+    Trio t0 = {{bit[e].c[0], 0, 0}}, t1 = {{0, bit[e].c[1], 0}};
+    for (int i = 0; i < 3; ++i) u[e].c[i] = t0.c[i] + t1.c[i] - 2 * pr.c[i];
+    Trio t2 = {{0, 0, bit[e].c[2]}};
+    m[e] = mul_local(u[e], t2);
+  }
+  fold_pair(tab, rk3, st.a[1], blk, m, false);
+  for (int e = 0; e < 2; ++e) {
+    Trio pv = relabel(m[e]);
+    // drelu = 1 - v: negate, constant into component 0 (protocols.py:57-66, 334-337)
+    m[e].c[0] = 1 - (u[e].c[0] - 2 * pv.c[0]);
+    m[e].c[1] = 0 - (u[e].c[1] - 2 * pv.c[1]);
+    m[e].c[2] = 0 - (u[e].c[2] + bit[e].c[2] - 2 * pv.c[2]);
   }
   if (mode == MODE_DRELU) {
     out[0] = m[0];
     out[1] = m[1];
     return;
   }
-  KeyWords f0, f1;
-  key_words_pair(tab, rk3, st.a[2], blk, f0, f1);
-  out[0] = trio_mul(x[0], m[0], f0);
-  out[1] = trio_mul(x[1], m[1], f1);
+  Trio z[2];
+  for (int e = 0; e < 2; ++e) z[e] = mul_local(ld(e), m[e]);
+  fold_pair(tab, rk3, st.a[2], blk, z, false);
+  out[0] = relabel(z[0]);
+  out[1] = relabel(z[1]);
   mask[0] = m[0];
   mask[1] = m[1];
 }

@@ -529,25 +529,29 @@ class TrioSession:
             return area.bit_length() - 1, 1
         return self.fp.t, int(fx_encode(1.0 / area, self.fp))
 
-    def avgpool(self, x: RssTensor, window, stride=None) -> RssTensor:
+    def avgpool(self, x: RssTensor, window, stride=None, padding=(0, 0)) -> RssTensor:
+        """avgpool_shares (protocols.py:139-159); padding (zero, divisor kh*kw)
+        extends the reference for ResNet's stem (composed: pad + avgpool)."""
         kh, kw = window
         sh, sw = stride or window
-        if x.ndim != 4 or x.shape[2] < kh or x.shape[3] < kw:
+        ph, pw = padding
+        if x.ndim != 4 or x.shape[2] + 2 * ph < kh or x.shape[3] + 2 * pw < kw:
             raise ShapeError("window larger than input")
         x = x.contiguous()
         nb, c, h, w = x.shape
-        oh, ow = (h - kh) // sh + 1, (w - kw) // sw + 1
+        oh, ow = (h + 2 * ph - kh) // sh + 1, (w + 2 * pw - kw) // sw + 1
         bits, mulc = self._area_params(kh * kw)
         out = empty((nb, c, oh, ow), x.fp)
         jr, jq = self.take(TR_RHO), self.take(TR_R)
         K.call("mpc3_rss_avgpool", self.rk, self.ctr_ptr, jr, jq, bits, mulc, x.data.data_ptr(), out.data.data_ptr(),
-               nb, c, h, w, kh, kw, sh, sw, _stream())
+               nb, c, h, w, kh, kw, sh, sw, ph, pw, _stream())
         self._charge_trunc(out.numel)
         return out
 
-    def avgpool_backward(self, g: RssTensor, window, stride, in_shape) -> RssTensor:
+    def avgpool_backward(self, g: RssTensor, window, stride, in_shape, padding=(0, 0)) -> RssTensor:
         kh, kw = window
         sh, sw = stride
+        ph, pw = padding
         g = g.contiguous()
         nb, c, oh, ow = g.shape
         h, w = in_shape[-2:]
@@ -555,7 +559,7 @@ class TrioSession:
         out = empty((nb, c, h, w), g.fp)
         jr, jq = self.take(TR_RHO), self.take(TR_R)
         K.call("mpc3_rss_avgpool_backward", self.rk, self.ctr_ptr, jr, jq, bits, mulc, g.data.data_ptr(),
-               out.data.data_ptr(), nb, c, h, w, oh, ow, kh, kw, sh, sw, _stream())
+               out.data.data_ptr(), nb, c, h, w, oh, ow, kh, kw, sh, sw, ph, pw, _stream())
         self._charge_trunc(out.numel)
         return out
 

@@ -32,6 +32,10 @@ FULLY_CONNECTED = "FullyConnected"
 AVGPOOL = "AvgPool"
 RELU = "ReLU"
 FLATTEN = "Flatten"
+# inference-only extensions for ResNet (absent from the reference, nn.py:43-47;
+# composed from its primitives: bias = local add after the truncation,
+# residual = local add of two branches, padded avg-pool = zero pad + avg-pool)
+RESIDUAL = "Residual"
 
 
 def _pair(v) -> tuple:
@@ -50,20 +54,28 @@ class LayerSpec:
     stride: tuple = (1, 1)
     padding: tuple = (0, 0)
     window: tuple = ()
+    bias: bool = False
+    main: tuple = ()
+    shortcut: tuple = ()
 
 
-def conv2d(out_channels: int, kernel, stride=1, padding=0) -> LayerSpec:
+def conv2d(out_channels: int, kernel, stride=1, padding=0, bias: bool = False) -> LayerSpec:
     return LayerSpec(CONV2D, out_channels=int(out_channels), kernel=_pair(kernel), stride=_pair(stride),
-                     padding=_pair(padding))
+                     padding=_pair(padding), bias=bool(bias))
 
 
-def fully_connected(out_features: int) -> LayerSpec:
-    return LayerSpec(FULLY_CONNECTED, out_features=int(out_features))
+def fully_connected(out_features: int, bias: bool = False) -> LayerSpec:
+    return LayerSpec(FULLY_CONNECTED, out_features=int(out_features), bias=bool(bias))
 
 
-def avgpool(window, stride=None) -> LayerSpec:
+def avgpool(window, stride=None, padding=0) -> LayerSpec:
     w = _pair(window)
-    return LayerSpec(AVGPOOL, window=w, stride=_pair(stride) if stride is not None else w)
+    return LayerSpec(AVGPOOL, window=w, stride=_pair(stride) if stride is not None else w, padding=_pair(padding))
+
+
+def residual(main, shortcut=()) -> LayerSpec:
+    """out = main(x) + shortcut(x) (identity when shortcut is empty)."""
+    return LayerSpec(RESIDUAL, main=tuple(main), shortcut=tuple(shortcut))
 
 
 def relu() -> LayerSpec:
@@ -88,36 +100,7 @@ class ModelGraph:
         self._shapes = self._infer_shapes()
 
     def _infer_shapes(self) -> list:
-        shape = self.input_shape
-        out = []
-        for s in self.layers:
-            if s.kind == CONV2D:
-                if len(shape) != 3:
-                    raise ShapeError(f"Conv2d needs (C,H,W), got {shape}")
-                c, h, w = shape
-                (kh, kw), (sh, sw), (ph, pw) = s.kernel, s.stride, s.padding
-                ho, wo = (h + 2 * ph - kh) // sh + 1, (w + 2 * pw - kw) // sw + 1
-                if h + 2 * ph < kh or w + 2 * pw < kw or ho < 1 or wo < 1:
-                    raise ShapeError(f"Conv2d kernel {s.kernel} does not fit {shape}")
-                shape = (s.out_channels, ho, wo)
-            elif s.kind == AVGPOOL:
-                if len(shape) != 3:
-                    raise ShapeError(f"AvgPool needs (C,H,W), got {shape}")
-                c, h, w = shape
-                ho, wo = (h - s.window[0]) // s.stride[0] + 1, (w - s.window[1]) // s.stride[1] + 1
-                if ho < 1 or wo < 1:
-                    raise ShapeError(f"AvgPool window {s.window} does not fit {shape}")
-                shape = (c, ho, wo)
-            elif s.kind == FULLY_CONNECTED:
-                if len(shape) != 1:
-                    raise ShapeError(f"FullyConnected needs a flat input, got {shape}")
-                shape = (s.out_features,)
-            elif s.kind == FLATTEN:
-                shape = (int(np.prod(shape)),)
-            elif s.kind != RELU:
-                raise ConfigError(f"unknown layer kind {s.kind!r}")
-            out.append(shape)
-        return out
+        return _infer(self.layers, self.input_shape)
 
     @property
     def output_shapes(self) -> list:
@@ -131,14 +114,7 @@ class ModelGraph:
         return last[0]
 
     def param_shapes(self) -> list:
-        shape, out = self.input_shape, []
-        for s, nxt in zip(self.layers, self._shapes):
-            if s.kind == CONV2D:
-                out.append((s.out_channels, shape[0]) + s.kernel)
-            elif s.kind == FULLY_CONNECTED:
-                out.append((s.out_features, shape[0]))
-            shape = nxt
-        return out
+        return _param_shapes(self.layers, self.input_shape)
 
     def validate(self, recip: ReciprocalConfig = ReciprocalConfig()) -> None:
         if self.num_classes > recip.Y:
@@ -154,13 +130,82 @@ class ModelGraph:
     def with_params(self, params) -> "ModelGraph":
         return ModelGraph(self.layers, self.input_shape, params)
 
+    @property
+    def trainable(self) -> bool:
+        """The reference's layer kinds only (backward is defined for them)."""
+        return all(s.kind != RESIDUAL and not s.bias for s in self.layers)
+
+
+def _infer(layers, shape) -> list:
+    """Per-layer output shapes (nn.py:99-143, extended with Residual / padding)."""
+    shape = tuple(shape)
+    out = []
+    if True:
+        for s in layers:
+            if s.kind == RESIDUAL:
+                m = _infer(s.main, shape)[-1] if s.main else shape
+                sc = _infer(s.shortcut, shape)[-1] if s.shortcut else shape
+                if m != sc:
+                    raise ShapeError(f"residual branches disagree: {m} vs {sc}")
+                shape = m
+            elif s.kind == CONV2D:
+                if len(shape) != 3:
+                    raise ShapeError(f"Conv2d needs (C,H,W), got {shape}")
+                c, h, w = shape
+                (kh, kw), (sh, sw), (ph, pw) = s.kernel, s.stride, s.padding
+                ho, wo = (h + 2 * ph - kh) // sh + 1, (w + 2 * pw - kw) // sw + 1
+                if h + 2 * ph < kh or w + 2 * pw < kw or ho < 1 or wo < 1:
+                    raise ShapeError(f"Conv2d kernel {s.kernel} does not fit {shape}")
+                shape = (s.out_channels, ho, wo)
+            elif s.kind == AVGPOOL:
+                if len(shape) != 3:
+                    raise ShapeError(f"AvgPool needs (C,H,W), got {shape}")
+                c, h, w = shape
+                ph, pw = s.padding
+                ho = (h + 2 * ph - s.window[0]) // s.stride[0] + 1
+                wo = (w + 2 * pw - s.window[1]) // s.stride[1] + 1
+                if ho < 1 or wo < 1:
+                    raise ShapeError(f"AvgPool window {s.window} does not fit {shape}")
+                shape = (c, ho, wo)
+            elif s.kind == FULLY_CONNECTED:
+                if len(shape) != 1:
+                    raise ShapeError(f"FullyConnected needs a flat input, got {shape}")
+                shape = (s.out_features,)
+            elif s.kind == FLATTEN:
+                shape = (int(np.prod(shape)),)
+            elif s.kind != RELU:
+                raise ConfigError(f"unknown layer kind {s.kind!r}")
+            out.append(shape)
+        return out
+
+
+def _param_shapes(layers, shape) -> list:
+    """Parameter shapes in schedule order (nn.py:145-153): conv weight
+    (O,C,kh,kw) / FC weight (out,in), each followed by its (O,) bias when
+    present; residual blocks list main then shortcut parameters."""
+    out = []
+    for s, nxt in zip(layers, _infer(layers, shape)):
+        if s.kind == CONV2D:
+            out.append((s.out_channels, shape[0]) + s.kernel)
+            if s.bias:
+                out.append((s.out_channels,))
+        elif s.kind == FULLY_CONNECTED:
+            out.append((s.out_features, shape[0]))
+            if s.bias:
+                out.append((s.out_features,))
+        elif s.kind == RESIDUAL:
+            out += _param_shapes(s.main, shape) + _param_shapes(s.shortcut, shape)
+        shape = nxt
+    return out
+
 
 def init_params_float(model: ModelGraph, seed: int = 0) -> list:
     """U(-1/sqrt(fan_in), 1/sqrt(fan_in)) per parameter, in order (nn.py:190-198)."""
     rng = np.random.default_rng(seed)
     out = []
     for shp in model.param_shapes():
-        bound = 1.0 / np.sqrt(int(np.prod(shp[1:])))
+        # 1-d parameters are the (folded-BN) biases of the ResNet extension
+        bound = 1.0 / np.sqrt(int(np.prod(shp[1:]))) if len(shp) > 1 else 0.05
         out.append(rng.uniform(-bound, bound, shp))
     return out
 
@@ -181,22 +226,32 @@ class TrioNet:
         self.t = sess.fp.t
 
     def forward(self, model: ModelGraph, params: list, x: RssTensor, record: bool):
-        """nn.py:405-432."""
-        S, acts, h, pi = self.s, [], x, 0
-        for spec in model.layers:
+        """nn.py:405-432 (plus the inference-only bias / residual / padded pool)."""
+        return self._run(model.layers, iter(params), x, record)
+
+    def _bias(self, h: RssTensor, b: RssTensor) -> RssTensor:
+        """Shared bias, local add after the truncation (scale t)."""
+        shape = (3, 1, b.shape[0]) + (1,) * (h.ndim - 2)
+        return self.s.add(h, RssTensor(b.data.reshape(shape).expand(h.data.shape), h.fp))
+
+    def _run(self, layers, it, h: RssTensor, record: bool):
+        S, acts = self.s, []
+        for spec in layers:
             if spec.kind == CONV2D:
-                k = params[pi]
-                pi += 1
+                k = next(it)
                 acts.append((h, k) if record else None)
                 h = S.conv2d(h, k, spec.stride, spec.padding)
+                if spec.bias:
+                    h = self._bias(h, next(it))
             elif spec.kind == FULLY_CONNECTED:
-                w = params[pi]
-                pi += 1
+                w = next(it)
                 acts.append((h, w) if record else None)
                 h = S.matmul(h, w.apply(lambda d: d.transpose(1, 2)))
+                if spec.bias:
+                    h = self._bias(h, next(it))
             elif spec.kind == AVGPOOL:
                 acts.append((h.shape,) if record else None)
-                h = S.avgpool(h, spec.window, spec.stride)
+                h = S.avgpool(h, spec.window, spec.stride, spec.padding)
             elif spec.kind == RELU:
                 h, mask = S.relu_with_mask(h)
                 acts.append((mask,) if record else None)
@@ -204,12 +259,20 @@ class TrioNet:
                 shp = h.shape
                 acts.append((shp,) if record else None)
                 h = h.contiguous().reshape(shp[0], -1)
+            elif spec.kind == RESIDUAL:
+                hm = self._run(spec.main, it, h, False)[0] if spec.main else h
+                hs = self._run(spec.shortcut, it, h, False)[0] if spec.shortcut else h
+                h = S.add(hm, hs)
+                acts.append(("residual",) if record else None)
         return h, acts
 
     def backward(self, model: ModelGraph, acts, grad_out: RssTensor, batch_bits: int = 0) -> list:
         """nn.py:502-536."""
         if acts is None or len(acts) != len(model.layers) or any(a is None for a in acts):
             raise ProtocolError("missing activation cache; run the forward pass with recording")
+        if not model.trainable:
+            raise ConfigError("backward is defined for the reference's layer kinds only "
+                              "(bias / residual layers are an inference extension)")
         S, t = self.s, self.t
         plist = [i for i, s in enumerate(model.layers) if s.kind in (CONV2D, FULLY_CONNECTED)]
         grads = [None] * len(plist)
@@ -402,6 +465,49 @@ class GraphStep:
         self._done[slot] = ev
         self.graph.replay()
         self.replays += 1
+        for p, d in self.delta.items():
+            S.seq[p] += d
+        return self.logits
+
+
+class InferenceGraph:
+    """Private inference of a fixed-shape batch captured as a CUDA graph.
+
+    Same counter mechanism as GraphStep: each replay draws the PRF words the
+    next eager inference would.  `x` is the static input buffer."""
+
+    def __init__(self, sess: TrioSession, model: ModelGraph, params: list, x: RssTensor):
+        import torch
+
+        self.sess, self.x = sess, x
+        self.seq0 = dict(sess.seq)
+        self.ctr = sess.ctr = torch.zeros(8, dtype=torch.int64, device=x.data.device)
+        net = TrioNet(sess)
+        net.forward(model, params, x, record=False)  # warm allocations outside capture
+        self.seq0 = dict(sess.seq)
+        self.graph = torch.cuda.CUDAGraph()
+        on = sess.ledger.enabled
+        sess.ledger.enabled = False
+        try:
+            with torch.cuda.graph(self.graph):
+                self.logits = net.forward(model, params, x, record=False)[0]
+        finally:
+            sess.ledger.enabled = on
+            sess.ctr = None
+        self.delta = {p: sess.seq[p] - self.seq0[p] for p in sess.seq}
+        sess.seq = dict(self.seq0)
+        self._host = torch.zeros(8, dtype=torch.int64).pin_memory()
+
+    def replay(self) -> RssTensor:
+        import torch
+
+        S = self.sess
+        torch.cuda.current_stream().synchronize()  # the pinned counter buffer is reused
+        hv = self._host.numpy()
+        for p in self.delta:
+            hv[p] = S.seq[p] - self.seq0[p]
+        self.ctr.copy_(self._host, non_blocking=True)
+        self.graph.replay()
         for p, d in self.delta.items():
             S.seq[p] += d
         return self.logits

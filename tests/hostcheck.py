@@ -76,13 +76,14 @@ def reshare_truncate(keys, ja, jrho, jr, bits, z, view, out_shape):
     return out
 
 
-def pool(keys, backward, jrho, jr, bits, mulc, x, N, Cc, H, W, OH, OW, kh, kw, sh, sw):
+def pool(keys, backward, jrho, jr, bits, mulc, x, N, Cc, H, W, OH, OW, kh, kw, sh, sw, ph=0, pw=0):
     x = np.ascontiguousarray(x, np.uint64)
     n = N * Cc * (H * W if backward else OH * OW)
     out = np.zeros((3, n), np.uint64)
     lib().hc_pool(keys48(keys), C.c_int(backward), C.c_uint64(jrho), C.c_uint64(jr), C.c_int(bits),
                   C.c_uint64(mulc), ptr(x), ptr(out), C.c_int64(N), C.c_int64(Cc), C.c_int64(H), C.c_int64(W),
-                  C.c_int64(OH), C.c_int64(OW), C.c_int(kh), C.c_int(kw), C.c_int(sh), C.c_int(sw))
+                  C.c_int64(OH), C.c_int64(OW), C.c_int(kh), C.c_int(kw), C.c_int(sh), C.c_int(sw),
+                  C.c_int(ph), C.c_int(pw))
     return out
 
 

@@ -200,7 +200,7 @@ def test_avgpool_kernels():
     ref = R.avgpool_shares(s, x, win, stride)
     rk = rk3(s.keys)
     out = torch.empty(ref.size, dtype=torch.int64, device="cuda")
-    _capi.call("mpc3_rss_avgpool", p(rk), None, 0, 0, 20, int(R.fx_encode(1.0 / 9)), p(dev(x)), p(out), *shape, 3, 3, 2, 2,
+    _capi.call("mpc3_rss_avgpool", p(rk), None, 0, 0, 20, int(R.fx_encode(1.0 / 9)), p(dev(x)), p(out), *shape, 3, 3, 2, 2, 0, 0,
                stream())
     assert np.array_equal(host(out).reshape(ref.shape), ref)
     g = R.share(R.fx_encode(rng.uniform(-1, 1, ref.shape[1:])), rng)
@@ -208,5 +208,5 @@ def test_avgpool_kernels():
     refb = N.avgpool_backward(N.TrioEngine(s), g, win, stride, shape)
     outb = torch.empty(refb.size, dtype=torch.int64, device="cuda")
     _capi.call("mpc3_rss_avgpool_backward", p(rk), None, 0, 0, 20, int(R.fx_encode(1.0 / 9)), p(dev(g)), p(outb), *shape,
-               ref.shape[3], ref.shape[4], 3, 3, 2, 2, stream())
+               ref.shape[3], ref.shape[4], 3, 3, 2, 2, 0, 0, stream())
     assert np.array_equal(host(outb).reshape(refb.shape), refb)

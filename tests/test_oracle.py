@@ -86,6 +86,51 @@ def test_lenet_train_step_weights():
         assert np.array_equal(p, G[f"train_lenet_w{i}"])
 
 
+def test_composed_resnet_oracle_tracks_float():
+    """The composed (bias / residual / padded-pool) oracle decodes to the float
+    network it encodes, within fixed-point error (no GPU)."""
+    torch = pytest.importorskip("torch")
+    import torch.nn.functional as F
+
+    from paper_2104_10949_b200.models import tiny_resnet
+    from paper_2104_10949_b200.nn import init_params_float
+
+    model = tiny_resnet()
+    layers = tuple(N.from_spec(sp) for sp in model.layers)
+    wf = init_params_float(model, seed=3)
+    x = np.random.default_rng(0).uniform(0, 1, (2, 3, 16, 16))
+    rin = np.random.default_rng(2)
+    P = [R.share(R.fx_encode(t), rin) for t in wf]
+    out = R.open_trio(N.forward_ext(R.Session(1), layers, iter(P), R.share(R.fx_encode(x), rin)))
+
+    it = iter([torch.tensor(t) for t in wf])
+
+    def run(ls, h):
+        for L in ls:
+            if L.kind == N.CONV:
+                h = F.conv2d(h, next(it), stride=L.stride, padding=L.padding)
+                if L.bias:
+                    h = h + next(it)[None, :, None, None]
+            elif L.kind == N.FC:
+                h = h @ next(it).T
+                if L.bias:
+                    h = h + next(it)
+            elif L.kind == N.POOL:
+                h = F.avg_pool2d(h, L.window, L.stride, L.padding, count_include_pad=True)
+            elif L.kind == N.RELU:
+                h = torch.relu(h)
+            elif L.kind == N.FLAT:
+                h = h.reshape(h.shape[0], -1)
+            elif L.kind == N.RES:
+                hm = run(L.main, h) if L.main else h
+                hs = run(L.shortcut, h) if L.shortcut else h
+                h = hm + hs
+        return h
+
+    ref = run(layers, torch.tensor(x)).numpy()
+    assert np.max(np.abs(R.fx_decode(out) - ref)) < 1e-3
+
+
 @pytest.mark.slow
 def test_alexnet_train_step_digest():
     layers, ishape = N.alexnet_cifar()
