@@ -98,20 +98,24 @@ int mpc3_ring_rowop(int op, const uint64_t* a, const uint64_t* b, uint64_t* out,
 /* Row sums of the last axis: out[r] = sum_j a[r, j] (protocols.py:466). */
 int mpc3_ring_rowsum(const uint64_t* a, uint64_t* out, uint64_t rows, uint64_t cols, void* stream);
 
-/* ---- elementwise protocols on trio tensors ---- */
+/* ---- elementwise protocols on trio tensors ----
+ * elem_off (even): global stream-word index of the call's element 0, i.e. the
+ * offset of a batch shard inside the reference's flat tensor (0 when the call
+ * covers the whole tensor); PRF words are drawn at elem_off + local index. */
 
 /* mul (protocols.py:79-94): out = reshare(x*y), 1 ARITH_ZERO counter. */
 int mpc3_rss_mul(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, const uint64_t* x, const uint64_t* y,
-                 uint64_t* out, uint64_t n, void* stream);
+                 uint64_t* out, uint64_t n, uint64_t elem_off, void* stream);
 
 /* truncate (protocols.py:171-216): bits in [1,61]; TRUNC_RHO and TRUNC_R counters. */
 int mpc3_rss_truncate(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_rho, uint64_t j_r, int bits, const uint64_t* x,
-                      uint64_t* out, uint64_t n, void* stream);
+                      uint64_t* out, uint64_t n, uint64_t elem_off, void* stream);
 
 /* mul + truncate fused (protocols.py:79-94 then 171-216; the `truncate(mul())`
  * pairs of exp_approx / reciprocal / division / softmax, 414-468). */
 int mpc3_rss_mul_truncate(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, uint64_t j_rho, uint64_t j_r, int bits,
-                          const uint64_t* x, const uint64_t* y, uint64_t* out, uint64_t n, void* stream);
+                          const uint64_t* x, const uint64_t* y, uint64_t* out, uint64_t n, uint64_t elem_off,
+                          void* stream);
 
 /* Sign circuit (protocols.py:266-348): a2b + 64-bit Kogge-Stone + msb +
  * bit_inject + relu, fused, all 11 rounds in registers.
@@ -149,7 +153,7 @@ typedef struct {
  * bits = 0 skips truncation (bare reshare). */
 int mpc3_rss_reshare_truncate(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, uint64_t j_rho, uint64_t j_r,
                               int bits, const uint64_t* z, const mpc3_view4* view, uint64_t* out,
-                              void* stream);
+                              uint64_t elem_off, void* stream);
 
 /* Input gradient epilogue (nn.py:460-484): z holds per-party cross terms
  * cols[(n,y,x), (c,a,b)] = sum_o g[n,o,y,x] k[o,c,a,b] (a GEMM with inner
@@ -162,7 +166,7 @@ int mpc3_rss_reshare_truncate(const uint32_t* rk3, const uint64_t* ctr, uint64_t
 int mpc3_rss_col2im_reshare_truncate(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, uint64_t j_rho,
                                      uint64_t j_r, int bits, const uint64_t* z, int64_t N, int64_t C, int64_t OH,
                                      int64_t OW, int kh, int kw, int sh, int sw, int ph, int pw, int64_t H,
-                                     int64_t W, uint64_t* out, void* stream);
+                                     int64_t W, uint64_t* out, uint64_t elem_off, void* stream);
 
 /* avgpool (protocols.py:139-159): window sums, then truncate(log2 area) when
  * the area is a power of two, else mul_const(mulc) + truncate(t).  x/out are
@@ -171,7 +175,7 @@ int mpc3_rss_col2im_reshare_truncate(const uint32_t* rk3, const uint64_t* ctr, u
  * has no padded pooling; used by ResNet's stem, composed as pad + avgpool). */
 int mpc3_rss_avgpool(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_rho, uint64_t j_r, int bits, uint64_t mulc,
                      const uint64_t* x, uint64_t* out, int64_t N, int64_t C, int64_t H, int64_t W,
-                     int kh, int kw, int sh, int sw, int ph, int pw, void* stream);
+                     int kh, int kw, int sh, int sw, int ph, int pw, uint64_t elem_off, void* stream);
 
 /* avgpool backward (nn.py:487-499): scatter-add of g into the windows, then
  * div_area (truncate / mul_const+truncate) — fused. g: (N,C,OH,OW) trio;
@@ -179,7 +183,7 @@ int mpc3_rss_avgpool(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_rho, u
 int mpc3_rss_avgpool_backward(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_rho, uint64_t j_r, int bits, uint64_t mulc,
                               const uint64_t* g, uint64_t* out, int64_t N, int64_t C, int64_t H,
                               int64_t W, int64_t OH, int64_t OW, int kh, int kw, int sh, int sw, int ph, int pw,
-                              void* stream);
+                              uint64_t elem_off, void* stream);
 
 /* Plain sum-pool of one ring tensor (ring.py:259-268). */
 int mpc3_ring_sumpool(const uint64_t* x, uint64_t* out, int64_t N, int64_t C, int64_t H, int64_t W,

@@ -129,19 +129,21 @@ _SIGS = {
     "mpc3_ring_ew": (C.c_int, [C.c_int, _P, _P, _U64, _P, _U64, _P]),
     "mpc3_ring_rowop": (C.c_int, [C.c_int, _P, _P, _P, _U64, _U64, _P]),
     "mpc3_ring_rowsum": (C.c_int, [_P, _P, _U64, _U64, _P]),
-    "mpc3_rss_mul": (C.c_int, [_P, _P, _U64, _P, _P, _P, _U64, _P]),
-    "mpc3_rss_truncate": (C.c_int, [_P, _P, _U64, _U64, C.c_int, _P, _P, _U64, _P]),
-    "mpc3_rss_mul_truncate": (C.c_int, [_P, _P, _U64, _U64, _U64, C.c_int, _P, _P, _P, _U64, _P]),
+    "mpc3_rss_mul": (C.c_int, [_P, _P, _U64, _P, _P, _P, _U64, _U64, _P]),
+    "mpc3_rss_truncate": (C.c_int, [_P, _P, _U64, _U64, C.c_int, _P, _P, _U64, _U64, _P]),
+    "mpc3_rss_mul_truncate": (C.c_int, [_P, _P, _U64, _U64, _U64, C.c_int, _P, _P, _P, _U64, _U64, _P]),
     "mpc3_rss_sign": (C.c_int, [_P, _P, C.c_int, _U64, _U64, _U64, _P, _P, _P, _U64, _U64, _U64, _P]),
     "mpc3_rss_bit_inject": (C.c_int, [_P, _P, _U64, _P, _P, _U64, _P]),
-    "mpc3_rss_reshare_truncate": (C.c_int, [_P, _P, _U64, _U64, _U64, C.c_int, _P, C.POINTER(View4), _P, _P]),
+    "mpc3_rss_reshare_truncate": (C.c_int, [_P, _P, _U64, _U64, _U64, C.c_int, _P, C.POINTER(View4), _P, _U64,
+                                            _P]),
     "mpc3_rss_avgpool": (C.c_int, [_P, _P, _U64, _U64, C.c_int, _U64, _P, _P, _I64, _I64, _I64, _I64,
-                                   C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P]),
+                                   C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _U64, _P]),
     "mpc3_rss_avgpool_backward": (C.c_int, [_P, _P, _U64, _U64, C.c_int, _U64, _P, _P, _I64, _I64, _I64, _I64,
-                                            _I64, _I64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P]),
+                                            _I64, _I64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _U64,
+                                            _P]),
     "mpc3_rss_col2im_reshare_truncate": (C.c_int, [_P, _P, _U64, _U64, _U64, C.c_int, _P, _I64, _I64, _I64, _I64,
                                                    C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _I64,
-                                                   _I64, _P, _P]),
+                                                   _I64, _P, _U64, _P]),
     "mpc3_ring_sumpool": (C.c_int, [_P, _P, _I64, _I64, _I64, _I64, C.c_int, C.c_int, C.c_int, C.c_int, _P]),
     "mpc3_ring_pack": (C.c_int, [_P, _I64, C.POINTER(Operand), C.c_int, _P, _I64, _P]),
     "mpc3_ring_gemm_packed": (C.c_int, [_P, _P, _P, C.c_int, _I64, _I64, _I64, _I64, _I64, C.c_int, _P]),

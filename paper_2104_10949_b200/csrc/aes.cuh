@@ -241,6 +241,56 @@ HD void aes128_block(const SmemTables& tab, const uint32_t* rk, uint32_t& s0, ui
 #endif
 }
 
+// Three blocks with the same counter under k_0, k_1, k_2, interleaved round by
+// round: every zero share needs all three keys' words at one position
+// (sharing.py:233-250), and the three independent dependency chains triple
+// the instruction-level parallelism of the table rounds.
+DEV void aes128_block3(const SmemTables& tab, const uint32_t* rk3, uint32_t s[3][4]) {
+  const uint32_t* T = tab.te;
+#define LK(x) T[(x) << 5]
+#define B2(x) __byte_perm((x), 0, 0x4442)
+#define B1(x) __byte_perm((x), 0, 0x4441)
+#define ROUND_COL(a, b, c, d, kk) \
+  (LK((a) >> 24) ^ __funnelshift_r(LK(B2(b)), LK(B2(b)), 8) ^ __funnelshift_r(LK(B1(c)), LK(B1(c)), 16) ^ \
+   __funnelshift_r(LK((d)&0xffu), LK((d)&0xffu), 24) ^ (kk))
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) s[i][j] ^= rk3[44 * i + j];
+#pragma unroll 1
+  for (int r = 1; r < 10; ++r) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const uint4 k = *reinterpret_cast<const uint4*>(rk3 + 44 * i + 4 * r);
+      uint32_t t0 = ROUND_COL(s[i][0], s[i][1], s[i][2], s[i][3], k.x);
+      uint32_t t1 = ROUND_COL(s[i][1], s[i][2], s[i][3], s[i][0], k.y);
+      uint32_t t2 = ROUND_COL(s[i][2], s[i][3], s[i][0], s[i][1], k.z);
+      uint32_t t3 = ROUND_COL(s[i][3], s[i][0], s[i][1], s[i][2], k.w);
+      s[i][0] = t0;
+      s[i][1] = t1;
+      s[i][2] = t2;
+      s[i][3] = t3;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const uint4 k = *reinterpret_cast<const uint4*>(rk3 + 44 * i + 40);
+    uint32_t a = s[i][0], b = s[i][1], c = s[i][2], d = s[i][3];
+#define FIN(w, x, y, z) \
+  ((LK((w) >> 24) & 0x00ff0000u) << 8 | (LK(B2(x)) & 0x00ff0000u) | (LK(B1(y)) & 0x0000ff00u) | \
+   (LK((z)&0xffu) >> 8 & 0xffu))
+    s[i][0] = FIN(a, b, c, d) ^ k.x;
+    s[i][1] = FIN(b, c, d, a) ^ k.y;
+    s[i][2] = FIN(c, d, a, b) ^ k.z;
+    s[i][3] = FIN(d, a, b, c) ^ k.w;
+#undef FIN
+  }
+#undef ROUND_COL
+#undef LK
+#undef B2
+#undef B1
+}
+
 // rk_dev: 3 x 44 round-key words (k_0, k_1, k_2 of the session).
 __device__ inline SmemTables aes_smem_init(AesSmem& sm, const uint32_t* __restrict__ rk_dev, int nkeys) {
   for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) sm.te[i] = te0_entry(i >> 5);

@@ -107,11 +107,11 @@ __global__ void __launch_bounds__(kThreads) arith_kernel(int kind, const uint32_
                                                         const uint64_t* __restrict__ ctr, StreamRef ra,
                                                         StreamRef rrho, StreamRef rr, int bits, const uint64_t* __restrict__ x,
                                                         const uint64_t* __restrict__ y,
-                                                        uint64_t* __restrict__ out, uint64_t n) {
+                                                        uint64_t* __restrict__ out, uint64_t n, uint64_t pb0) {
   __shared__ AesSmem sm;
   SmemTables tab = aes_smem_init(sm, rk3, 3);
   StreamHead ha = resolve(ra, ctr), hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
-  GRID_LOOP(b, (n + 1) >> 1) arith_item(tab, &sm.rk[0][0], kind, ha, hrho, hr, bits, x, y, out, n, b);
+  GRID_LOOP(b, (n + 1) >> 1) arith_item(tab, &sm.rk[0][0], kind, ha, hrho, hr, bits, x, y, out, n, b, pb0);
 }
 
 struct SignArgs {
@@ -149,33 +149,35 @@ __global__ void __launch_bounds__(kThreads) reshare_trunc_kernel(const uint32_t*
                                                                 const uint64_t* __restrict__ ctr, StreamRef ra,
                                                                 StreamRef rrho, StreamRef rr, int bits,
                                                                 const uint64_t* __restrict__ z, View4 v,
-                                                                uint64_t* __restrict__ out, uint64_t n) {
+                                                                uint64_t* __restrict__ out, uint64_t n,
+                                                                uint64_t pb0) {
   __shared__ AesSmem sm;
   SmemTables tab = aes_smem_init(sm, rk3, 3);
   StreamHead ha = resolve(ra, ctr), hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
-  GRID_LOOP(b, (n + 1) >> 1) reshare_trunc_item(tab, &sm.rk[0][0], ha, hrho, hr, bits, z, v, out, n, b);
+  GRID_LOOP(b, (n + 1) >> 1) reshare_trunc_item(tab, &sm.rk[0][0], ha, hrho, hr, bits, z, v, out, n, b, pb0);
 }
 
 __global__ void __launch_bounds__(kThreads) pool_kernel(const uint32_t* __restrict__ rk3,
                                                        const uint64_t* __restrict__ ctr, int backward,
                                                        StreamRef rrho, StreamRef rr, int bits, uint64_t mulc,
                                                        const uint64_t* __restrict__ x,
-                                                       uint64_t* __restrict__ out, PoolGeom p, uint64_t n) {
+                                                       uint64_t* __restrict__ out, PoolGeom p, uint64_t n,
+                                                       uint64_t pb0) {
   __shared__ AesSmem sm;
   SmemTables tab = aes_smem_init(sm, rk3, 3);
   StreamHead hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
-  GRID_LOOP(b, (n + 1) >> 1) pool_item(tab, &sm.rk[0][0], backward != 0, hrho, hr, bits, mulc, x, out, p, b);
+  GRID_LOOP(b, (n + 1) >> 1) pool_item(tab, &sm.rk[0][0], backward != 0, hrho, hr, bits, mulc, x, out, p, b, pb0);
 }
 
 __global__ void __launch_bounds__(kThreads) col2im_kernel(const uint32_t* __restrict__ rk3,
                                                          const uint64_t* __restrict__ ctr, StreamRef ra,
                                                          StreamRef rrho, StreamRef rr, int bits,
                                                          const uint64_t* __restrict__ z, Col2Im g,
-                                                         uint64_t* __restrict__ out, uint64_t n) {
+                                                         uint64_t* __restrict__ out, uint64_t n, uint64_t pb0) {
   __shared__ AesSmem sm;
   SmemTables tab = aes_smem_init(sm, rk3, 3);
   StreamHead ha = resolve(ra, ctr), hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
-  GRID_LOOP(b, (n + 1) >> 1) col2im_item(tab, &sm.rk[0][0], ha, hrho, hr, bits, z, g, out, b);
+  GRID_LOOP(b, (n + 1) >> 1) col2im_item(tab, &sm.rk[0][0], ha, hrho, hr, bits, z, g, out, b, pb0);
 }
 
 __global__ void sumpool_kernel(const uint64_t* __restrict__ x, uint64_t* __restrict__ out, PoolGeom p) {
@@ -272,28 +274,32 @@ int mpc3_ring_rowsum(const uint64_t* a, uint64_t* out, uint64_t rows, uint64_t c
 }
 
 static int arith_launch(int kind, const uint32_t* rk3, const uint64_t* ctr, uint64_t ja, uint64_t jrho, uint64_t jr, int bits,
-                        const uint64_t* x, const uint64_t* y, uint64_t* out, uint64_t n, void* stream) {
+                        const uint64_t* x, const uint64_t* y, uint64_t* out, uint64_t n, uint64_t elem_off,
+                        void* stream) {
   if (kind != 0 && (bits < 1 || bits > 61)) return MPC3_ERR_RANGE;  // protocols.py:185-186
   if (ja >= (1ull << 48) || jrho >= (1ull << 48) || jr >= (1ull << 48)) return MPC3_ERR_RANGE;
+  if (elem_off & 1) return MPC3_ERR_CONFIG;
   if (n == 0) return MPC3_OK;
   arith_kernel<<<grid_for((n + 1) / 2, kThreads), kThreads, 0, as_stream(stream)>>>(
-      kind, rk3, ctr, sref(ARITH_ZERO, ja), sref(TRUNC_RHO, jrho), sref(TRUNC_R, jr), bits, x, y, out, n);
+      kind, rk3, ctr, sref(ARITH_ZERO, ja), sref(TRUNC_RHO, jrho), sref(TRUNC_R, jr), bits, x, y, out, n,
+      elem_off >> 1);
   return check_launch("rss_arith");
 }
 
 int mpc3_rss_mul(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, const uint64_t* x, const uint64_t* y, uint64_t* out,
-                 uint64_t n, void* stream) {
-  return arith_launch(0, rk3, ctr, j_arith, 0, 0, 0, x, y, out, n, stream);
+                 uint64_t n, uint64_t elem_off, void* stream) {
+  return arith_launch(0, rk3, ctr, j_arith, 0, 0, 0, x, y, out, n, elem_off, stream);
 }
 
 int mpc3_rss_truncate(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_rho, uint64_t j_r, int bits, const uint64_t* x,
-                      uint64_t* out, uint64_t n, void* stream) {
-  return arith_launch(1, rk3, ctr, 0, j_rho, j_r, bits, x, nullptr, out, n, stream);
+                      uint64_t* out, uint64_t n, uint64_t elem_off, void* stream) {
+  return arith_launch(1, rk3, ctr, 0, j_rho, j_r, bits, x, nullptr, out, n, elem_off, stream);
 }
 
 int mpc3_rss_mul_truncate(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, uint64_t j_rho, uint64_t j_r, int bits,
-                          const uint64_t* x, const uint64_t* y, uint64_t* out, uint64_t n, void* stream) {
-  return arith_launch(2, rk3, ctr, j_arith, j_rho, j_r, bits, x, y, out, n, stream);
+                          const uint64_t* x, const uint64_t* y, uint64_t* out, uint64_t n, uint64_t elem_off,
+                          void* stream) {
+  return arith_launch(2, rk3, ctr, j_arith, j_rho, j_r, bits, x, y, out, n, elem_off, stream);
 }
 
 int mpc3_rss_sign(const uint32_t* rk3, const uint64_t* ctr, int mode, uint64_t j_bin, uint64_t j_xor, uint64_t j_arith,
@@ -324,9 +330,10 @@ int mpc3_rss_bit_inject(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_ari
 }
 
 int mpc3_rss_reshare_truncate(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, uint64_t j_rho, uint64_t j_r, int bits,
-                              const uint64_t* z, const mpc3_view4* view, uint64_t* out, void* stream) {
+                              const uint64_t* z, const mpc3_view4* view, uint64_t* out, uint64_t elem_off,
+                              void* stream) {
   if (bits != 0 && (bits < 1 || bits > 61)) return MPC3_ERR_RANGE;
-  if (!view) return MPC3_ERR_CONFIG;
+  if (!view || (elem_off & 1)) return MPC3_ERR_CONFIG;
   View4 v;
   uint64_t n = 1;
   for (int k = 0; k < 4; ++k) {
@@ -342,7 +349,8 @@ int mpc3_rss_reshare_truncate(const uint32_t* rk3, const uint64_t* ctr, uint64_t
   v.op = view->out_plane;
   if (n == 0) return MPC3_OK;
   reshare_trunc_kernel<<<grid_for((n + 1) / 2, kThreads), kThreads, 0, as_stream(stream)>>>(
-      rk3, ctr, sref(ARITH_ZERO, j_arith), sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, z, v, out, n);
+      rk3, ctr, sref(ARITH_ZERO, j_arith), sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, z, v, out, n,
+      elem_off >> 1);
   return check_launch("rss_reshare_truncate");
 }
 
@@ -356,8 +364,9 @@ static PoolGeom pool_geom(int64_t N, int64_t C, int64_t H, int64_t W, int64_t OH
 
 int mpc3_rss_avgpool(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_rho, uint64_t j_r, int bits, uint64_t mulc,
                      const uint64_t* x, uint64_t* out, int64_t N, int64_t C, int64_t H, int64_t W, int kh,
-                     int kw, int sh, int sw, int ph, int pw, void* stream) {
+                     int kw, int sh, int sw, int ph, int pw, uint64_t elem_off, void* stream) {
   if (bits < 1 || bits > 61) return MPC3_ERR_RANGE;
+  if (elem_off & 1) return MPC3_ERR_CONFIG;
   if (kh < 1 || kw < 1 || sh < 1 || sw < 1 || ph < 0 || pw < 0 || H + 2 * ph < kh || W + 2 * pw < kw)
     return MPC3_ERR_SHAPE;
   int64_t OH = (H + 2 * ph - kh) / sh + 1, OW = (W + 2 * pw - kw) / sw + 1;
@@ -365,28 +374,31 @@ int mpc3_rss_avgpool(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_rho, u
   if (n == 0) return MPC3_OK;
   pool_kernel<<<grid_for((n + 1) / 2, kThreads), kThreads, 0, as_stream(stream)>>>(
       rk3, ctr, 0, sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, mulc, x, out,
-      pool_geom(N, C, H, W, OH, OW, kh, kw, sh, sw, ph, pw), n);
+      pool_geom(N, C, H, W, OH, OW, kh, kw, sh, sw, ph, pw), n, elem_off >> 1);
   return check_launch("rss_avgpool");
 }
 
 int mpc3_rss_avgpool_backward(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_rho, uint64_t j_r, int bits, uint64_t mulc,
                               const uint64_t* g, uint64_t* out, int64_t N, int64_t C, int64_t H, int64_t W,
-                              int64_t OH, int64_t OW, int kh, int kw, int sh, int sw, int ph, int pw, void* stream) {
+                              int64_t OH, int64_t OW, int kh, int kw, int sh, int sw, int ph, int pw,
+                              uint64_t elem_off, void* stream) {
   if (bits < 1 || bits > 61) return MPC3_ERR_RANGE;
+  if (elem_off & 1) return MPC3_ERR_CONFIG;
   if (kh < 1 || kw < 1 || sh < 1 || sw < 1 || ph < 0 || pw < 0) return MPC3_ERR_SHAPE;
   uint64_t n = (uint64_t)N * C * H * W;
   if (n == 0) return MPC3_OK;
   pool_kernel<<<grid_for((n + 1) / 2, kThreads), kThreads, 0, as_stream(stream)>>>(
       rk3, ctr, 1, sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, mulc, g, out,
-      pool_geom(N, C, H, W, OH, OW, kh, kw, sh, sw, ph, pw), n);
+      pool_geom(N, C, H, W, OH, OW, kh, kw, sh, sw, ph, pw), n, elem_off >> 1);
   return check_launch("rss_avgpool_backward");
 }
 
 int mpc3_rss_col2im_reshare_truncate(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, uint64_t j_rho,
                                      uint64_t j_r, int bits, const uint64_t* z, int64_t N, int64_t C, int64_t OH,
                                      int64_t OW, int kh, int kw, int sh, int sw, int ph, int pw, int64_t H,
-                                     int64_t W, uint64_t* out, void* stream) {
+                                     int64_t W, uint64_t* out, uint64_t elem_off, void* stream) {
   if (bits < 1 || bits > 61) return MPC3_ERR_RANGE;
+  if (elem_off & 1) return MPC3_ERR_CONFIG;
   if (kh < 1 || kw < 1 || sh < 1 || sw < 1 || ph < 0 || pw < 0) return MPC3_ERR_SHAPE;
   Col2Im g;
   g.N = N; g.C = C; g.OH = OH; g.OW = OW; g.H = H; g.W = W;
@@ -396,7 +408,8 @@ int mpc3_rss_col2im_reshare_truncate(const uint32_t* rk3, const uint64_t* ctr, u
   uint64_t n = (uint64_t)N * C * g.hf * g.wf;
   if (n == 0) return MPC3_OK;
   col2im_kernel<<<grid_for((n + 1) / 2, kThreads), kThreads, 0, as_stream(stream)>>>(
-      rk3, ctr, sref(ARITH_ZERO, j_arith), sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, z, g, out, n);
+      rk3, ctr, sref(ARITH_ZERO, j_arith), sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, z, g, out, n,
+      elem_off >> 1);
   return check_launch("rss_col2im_reshare_truncate");
 }
 

@@ -50,7 +50,10 @@ HD void zero_share_item(const T& tab, const uint32_t* rk3, StreamHead h, int xor
 // kind: 0 = mul, 1 = truncate, 2 = mul then truncate
 template <class T>
 HD void arith_item(const T& tab, const uint32_t* rk3, int kind, StreamHead ha, StreamHead hrho, StreamHead hr,
-                   int bits, const uint64_t* x, const uint64_t* y, uint64_t* out, uint64_t n, uint64_t b) {
+                   int bits, const uint64_t* x, const uint64_t* y, uint64_t* out, uint64_t n, uint64_t b,
+                   uint64_t pb0 = 0) {
+  // pb0: PRF block of local element 0 (a batch shard starts at an even global word)
+  const uint64_t pb = pb0 + b;
   bool two = 2 * b + 1 < n;
   Trio v[2];
   v[0] = load_trio(x, n, 2 * b);
@@ -60,13 +63,13 @@ HD void arith_item(const T& tab, const uint32_t* rk3, int kind, StreamHead ha, S
     w[0] = load_trio(y, n, 2 * b);
     w[1] = two ? load_trio(y, n, 2 * b + 1) : w[0];
     KeyWords f0, f1;
-    key_words_pair(tab, rk3, ha, b, f0, f1);
+    key_words_pair(tab, rk3, ha, pb, f0, f1);
     v[0] = trio_mul(v[0], w[0], f0);
     v[1] = trio_mul(v[1], w[1], f1);
   }
   if (kind != 0) {
-    Word2 rho = prf_block(tab, rk3 + 2 * 44, hrho, b);
-    Word2 r = prf_block(tab, rk3 + 1 * 44, hr, b);
+    Word2 rho = prf_block(tab, rk3 + 2 * 44, hrho, pb);
+    Word2 r = prf_block(tab, rk3 + 1 * 44, hr, pb);
     v[0] = trio_truncate(v[0], rho.w0, r.w0, bits);
     v[1] = trio_truncate(v[1], rho.w1, r.w1, bits);
   }
@@ -112,7 +115,9 @@ struct View4 {
 
 template <class T>
 HD void reshare_trunc_item(const T& tab, const uint32_t* rk3, StreamHead ha, StreamHead hrho, StreamHead hr,
-                           int bits, const uint64_t* z, const View4& v, uint64_t* out, uint64_t n, uint64_t b) {
+                           int bits, const uint64_t* z, const View4& v, uint64_t* out, uint64_t n, uint64_t b,
+                           uint64_t pb0 = 0) {
+  const uint64_t pb = pb0 + b;
   int64_t zoff[2] = {0, 0}, ooff[2] = {0, 0};
   bool ok[2];
   for (int e = 0; e < 2; ++e) {
@@ -136,11 +141,11 @@ HD void reshare_trunc_item(const T& tab, const uint32_t* rk3, StreamHead ha, Str
   }
   if (!ok[0] && !ok[1]) return;
   KeyWords f0, f1;
-  key_words_pair(tab, rk3, ha, b, f0, f1);
+  key_words_pair(tab, rk3, ha, pb, f0, f1);
   Word2 rho = {0, 0}, r = {0, 0};
   if (bits) {
-    rho = prf_block(tab, rk3 + 2 * 44, hrho, b);
-    r = prf_block(tab, rk3 + 1 * 44, hr, b);
+    rho = prf_block(tab, rk3 + 2 * 44, hrho, pb);
+    r = prf_block(tab, rk3 + 1 * 44, hr, pb);
   }
   for (int e = 0; e < 2; ++e) {
     if (!ok[e]) continue;
@@ -164,7 +169,8 @@ struct Col2Im {
 
 template <class T>
 HD void col2im_item(const T& tab, const uint32_t* rk3, StreamHead ha, StreamHead hrho, StreamHead hr, int bits,
-                    const uint64_t* z, const Col2Im& g, uint64_t* out, uint64_t b) {
+                    const uint64_t* z, const Col2Im& g, uint64_t* out, uint64_t b, uint64_t pb0 = 0) {
+  const uint64_t pb = pb0 + b;
   const uint64_t n_full = (uint64_t)g.N * g.C * g.hf * g.wf;
   const int64_t ncols = (int64_t)g.C * g.kh * g.kw;
   const int64_t zplane = (int64_t)g.N * g.OH * g.OW * ncols;
@@ -199,9 +205,9 @@ HD void col2im_item(const T& tab, const uint32_t* rk3, StreamHead ha, StreamHead
   }
   if (ooff[0] < 0 && ooff[1] < 0) return;
   KeyWords f0, f1;
-  key_words_pair(tab, rk3, ha, b, f0, f1);
-  Word2 rho = prf_block(tab, rk3 + 2 * 44, hrho, b);
-  Word2 r = prf_block(tab, rk3 + 1 * 44, hr, b);
+  key_words_pair(tab, rk3, ha, pb, f0, f1);
+  Word2 rho = prf_block(tab, rk3 + 2 * 44, hrho, pb);
+  Word2 r = prf_block(tab, rk3 + 1 * 44, hr, pb);
   for (int e = 0; e < 2; ++e) {
     if (ooff[e] < 0) continue;
     Trio t = trio_reshare(s[e], e ? f1 : f0);
@@ -219,7 +225,8 @@ struct PoolGeom {
 // fused window sum (x mulc) + truncate; backward = scatter-add then the same
 template <class T>
 HD void pool_item(const T& tab, const uint32_t* rk3, bool backward, StreamHead hrho, StreamHead hr, int bits,
-                  uint64_t mulc, const uint64_t* x, uint64_t* out, const PoolGeom& p, uint64_t b) {
+                  uint64_t mulc, const uint64_t* x, uint64_t* out, const PoolGeom& p, uint64_t b, uint64_t pb0 = 0) {
+  const uint64_t pb = pb0 + b;
   uint64_t n = backward ? (uint64_t)p.N * p.C * p.H * p.W : (uint64_t)p.N * p.C * p.OH * p.OW;
   uint64_t nin = backward ? (uint64_t)p.N * p.C * p.OH * p.OW : (uint64_t)p.N * p.C * p.H * p.W;
   Trio s[2];
@@ -254,8 +261,8 @@ HD void pool_item(const T& tab, const uint32_t* rk3, bool backward, StreamHead h
     }
     for (int i = 0; i < 3; ++i) s[e].c[i] *= mulc;
   }
-  Word2 rho = prf_block(tab, rk3 + 2 * 44, hrho, b);
-  Word2 r = prf_block(tab, rk3 + 1 * 44, hr, b);
+  Word2 rho = prf_block(tab, rk3 + 2 * 44, hrho, pb);
+  Word2 r = prf_block(tab, rk3 + 1 * 44, hr, pb);
   for (int e = 0; e < 2; ++e) {
     uint64_t f = 2 * b + e;
     if (f >= n) break;

@@ -99,16 +99,43 @@ struct SignStreams {
   StreamHead a[3];    // ARITH_ZERO, counters ja..ja+2 (inject, inject, mask)
 };
 
+// Block `blk` of one stream under the three session keys.
+template <class T>
+HD void prf_block3(const T& tab, const uint32_t* rk3, StreamHead h, uint64_t blk, Word2 w[3]) {
+  for (int i = 0; i < 3; ++i) w[i] = prf_block(tab, rk3 + 44 * i, h, blk);
+}
+#if defined(__CUDACC__)
+HD void prf_block3(const SmemTables& tab, const uint32_t* rk3, StreamHead h, uint64_t blk, Word2 w[3]) {
+#if defined(__CUDA_ARCH__)
+  uint32_t s[3][4];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    s[i][0] = h.s0;
+    s[i][1] = h.s1;
+    s[i][2] = (uint32_t)(blk >> 32);
+    s[i][3] = (uint32_t)blk;
+  }
+  aes128_block3(tab, rk3, s);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    w[i].w0 = (uint64_t)bswap32(s[i][0]) | ((uint64_t)bswap32(s[i][1]) << 32);
+    w[i].w1 = (uint64_t)bswap32(s[i][2]) | ((uint64_t)bswap32(s[i][3]) << 32);
+  }
+#endif
+}
+#endif
+
 // Key-word provider over a pair of adjacent elements (words 2b, 2b+1 of each
 // stream share one AES block per key).
 template <class T>
 HD void key_words_pair(const T& tab, const uint32_t* rk3, StreamHead h, uint64_t blk, KeyWords& w0,
                        KeyWords& w1) {
+  Word2 p[3];
+  prf_block3(tab, rk3, h, blk, p);
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    Word2 p = prf_block(tab, rk3 + 44 * i, h, blk);
-    w0.k[i] = p.w0;
-    w1.k[i] = p.w1;
+    w0.k[i] = p[i].w0;
+    w1.k[i] = p[i].w1;
   }
 }
 
@@ -161,11 +188,12 @@ HD void fold_word(Trio& z, int k, uint64_t w, bool xor_mode) {
 }
 template <class T>
 HD void fold_pair(const T& tab, const uint32_t* rk3, StreamHead h, uint64_t blk, Trio z[2], bool xor_mode) {
+  Word2 w[3];
+  prf_block3(tab, rk3, h, blk, w);
 #pragma unroll
   for (int k = 0; k < 3; ++k) {  // unrolled: k indexes registers
-    Word2 w = prf_block(tab, rk3 + 44 * k, h, blk);
-    fold_word(z[0], k, w.w0, xor_mode);
-    fold_word(z[1], k, w.w1, xor_mode);
+    fold_word(z[0], k, w[k].w0, xor_mode);
+    fold_word(z[1], k, w[k].w1, xor_mode);
   }
 }
 // the pair's words sit at stream words w, w+1 that may straddle two blocks
@@ -175,11 +203,13 @@ HD void fold_words(const T& tab, const uint32_t* rk3, StreamHead h, uint64_t w, 
     fold_pair(tab, rk3, h, w >> 1, z, xor_mode);
     return;
   }
+  Word2 a[3];
+  prf_block3(tab, rk3, h, w >> 1, a);
 #pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    fold_word(z[0], k, prf_block(tab, rk3 + 44 * k, h, w >> 1).w1, xor_mode);
-    fold_word(z[1], k, prf_block(tab, rk3 + 44 * k, h, (w + 1) >> 1).w0, xor_mode);
-  }
+  for (int k = 0; k < 3; ++k) fold_word(z[0], k, a[k].w1, xor_mode);
+  prf_block3(tab, rk3, h, (w + 1) >> 1, a);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) fold_word(z[1], k, a[k].w0, xor_mode);
 }
 
 // The fused sign circuit for the element pair (2*blk, 2*blk+1) of a tensor of

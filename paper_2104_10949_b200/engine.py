@@ -193,7 +193,37 @@ class TrioSession:
         self.seq = {p: 0 for p in PURPOSES}
         self.ledger = Ledger()
         self.ctr = None  # optional device per-purpose counter base (CUDA-graph replay)
-        self._pool = {}
+        self.dp = None  # DataParallel: this session computes one batch shard
+        self._replicated = 0
+
+    # -- data parallelism --
+    def shard_offset(self, numel: int) -> tuple[int, int]:
+        """(global word offset of this shard's element 0, global element count)
+        of a batch-major tensor whose local part has `numel` elements.  Every
+        rank holds an equal batch shard, so the shard is one contiguous range
+        of the reference's flat tensor and its PRF words a seekable range."""
+        if self.dp is None or self._replicated:
+            return 0, numel
+        return self.dp.rank * numel, self.dp.world * numel
+
+    def replicated(self):
+        """Context: ops on replicated (non-batch) tensors, e.g. the SGD update."""
+        sess = self
+
+        class _Ctx:
+            def __enter__(self):
+                sess._replicated += 1
+
+            def __exit__(self, *a):
+                sess._replicated -= 1
+
+        return _Ctx()
+
+    def _reduce_cross_terms(self, z: torch.Tensor) -> None:
+        """Weight gradients: sum the shards' raw cross terms (mod 2^64) BEFORE
+        the reshare/truncation, which then run replicated on every rank."""
+        if self.dp is not None and self.dp.world > 1:
+            self.dp.allreduce(z)
 
     # -- counters (sharing.py:190-204, 225-230) --
     def take(self, purpose: int, count: int = 1) -> int:
@@ -293,7 +323,7 @@ class TrioSession:
         out = empty(x.shape, x.fp)
         j = self.take(ARITH)
         K.call("mpc3_rss_mul", self.rk, self.ctr_ptr, j, x.data.data_ptr(), y.data.data_ptr(), out.data.data_ptr(),
-               x.numel, _stream())
+               x.numel, self.shard_offset(x.numel)[0], _stream())
         self.ledger.ring(label, x.numel)
         return out
 
@@ -305,7 +335,7 @@ class TrioSession:
         out = empty(x.shape, x.fp)
         jr, jq = self.take(TR_RHO), self.take(TR_R)
         K.call("mpc3_rss_truncate", self.rk, self.ctr_ptr, jr, jq, bits, x.data.data_ptr(), out.data.data_ptr(),
-               x.numel, _stream())
+               x.numel, self.shard_offset(x.numel)[0], _stream())
         self._charge_trunc(x.numel)
         return out
 
@@ -319,7 +349,7 @@ class TrioSession:
         ja = self.take(ARITH)
         jr, jq = self.take(TR_RHO), self.take(TR_R)
         K.call("mpc3_rss_mul_truncate", self.rk, self.ctr_ptr, ja, jr, jq, bits, x.data.data_ptr(),
-               y.data.data_ptr(), out.data.data_ptr(), x.numel, _stream())
+               y.data.data_ptr(), out.data.data_ptr(), x.numel, self.shard_offset(x.numel)[0], _stream())
         self.ledger.ring(label, x.numel)
         self._charge_trunc(x.numel)
         return out
@@ -338,8 +368,9 @@ class TrioSession:
         jb = self.take(BIN)
         jx = self.take(XOR, 7)
         ja = self.take(ARITH, [0, 0, 2, 3][mode]) if mode >= K.MODE_DRELU else self.seq[ARITH]
+        off, n_total = self.shard_offset(n)
         K.call("mpc3_rss_sign", self.rk, self.ctr_ptr, mode, jb, jx, ja, x.data.data_ptr(), out.data.data_ptr(),
-               None if mask is None else mask.data.data_ptr(), n, n, 0, _stream())
+               None if mask is None else mask.data.data_ptr(), n, n_total, off, _stream())
         L = self.ledger
         L.round("share.a2b", [(0, 2, n)])
         L.ring("and.ks.g", n)
@@ -400,21 +431,24 @@ class TrioSession:
         jr = jq = 0
         if bits:
             jr, jq = self.take(TR_RHO), self.take(TR_R)
-        K.call("mpc3_rss_reshare_truncate", self.rk, self.ctr_ptr, ja, jr, jq, bits, z.data_ptr(), C.byref(view),
-               out.data.data_ptr(), _stream())
         full = int(np.prod(view.full))
+        K.call("mpc3_rss_reshare_truncate", self.rk, self.ctr_ptr, ja, jr, jq, bits, z.data_ptr(), C.byref(view),
+               out.data.data_ptr(), self.shard_offset(full)[0], _stream())
         self.ledger.ring(label, full)
         if bits:
             self._charge_trunc(full)
         return out
 
-    def matmul(self, x: RssTensor, y: RssTensor, bits: int | None = None) -> RssTensor:
-        """matmul_shares (protocols.py:97-117): cross terms, reshare, truncate."""
+    def matmul(self, x: RssTensor, y: RssTensor, bits: int | None = None, wgrad: bool = False) -> RssTensor:
+        """matmul_shares (protocols.py:97-117): cross terms, reshare, truncate.
+        wgrad=True marks a weight gradient g^T x whose inner dimension is the
+        batch: under data parallelism the shards' cross terms are summed
+        before the (replicated) reshare + truncate."""
         if x.ndim != 2 or y.ndim != 2 or x.shape[1] != y.shape[0]:
             raise ShapeError(f"matmul shapes {x.shape} x {y.shape}")
         m, k = x.shape
         n = y.shape[1]
-        check_accumulation(k)
+        check_accumulation(k * (self.dp.world if (wgrad and self.dp) else 1))
         bits = self.fp.t if bits is None else bits
         if not 1 <= bits <= 61:
             raise RangeError(f"truncation by {bits} bits outside [1, 61]")
@@ -423,6 +457,10 @@ class TrioSession:
         b_op = K.dense_operand(n, k, s_r=ys[2], t2=ys[1])
         z = self._cross_gemm(x.data, a_op, y.data, b_op, m, n, k)
         out = empty((m, n), x.fp)
+        if wgrad:
+            self._reduce_cross_terms(z)
+            with self.replicated():
+                return self._finish(z, K.make_view((1, 1, m, n)), out, bits, "mul.reshare")
         return self._finish(z, K.make_view((1, 1, m, n)), out, bits, "mul.reshare")
 
     def conv2d(self, x: RssTensor, k: RssTensor, stride=(1, 1), padding=(0, 0), bits=None) -> RssTensor:
@@ -458,7 +496,7 @@ class TrioSession:
         sh, sw = stride
         ph, pw = padding
         ghd, gwd = (oh - 1) * sh + 1, (ow - 1) * sw + 1
-        check_accumulation(nb * ghd * gwd)
+        check_accumulation(nb * (self.dp.world if self.dp else 1) * ghd * gwd)
         if h + 2 * ph < ghd or w + 2 * pw < gwd:
             raise ShapeError("kernel larger than padded input")
         fh, fw = h + 2 * ph - ghd + 1, w + 2 * pw - gwd + 1
@@ -470,7 +508,9 @@ class TrioSession:
         out = empty((o, c, kh, kw), x.fp)
         view = K.make_view((c, o, fh, fw), crop=(c, o, kh, kw), z_stride=(kh * kw * o, 1, kw * o, o),
                            out_stride=(kh * kw, c * kh * kw, kw, 1), z_plane=c * kh * kw * o)
-        return self._finish(z, view, out, bits, "mul.reshare")
+        self._reduce_cross_terms(z)  # sum over the batch shards before reshare / truncate
+        with self.replicated():
+            return self._finish(z, view, out, bits, "mul.reshare")
 
     def conv2d_dgrad(self, g: RssTensor, k: RssTensor, stride, padding, in_shape, bits) -> RssTensor:
         """Input gradient (nn.py:460-484) as a transposed convolution: one
@@ -493,10 +533,10 @@ class TrioSession:
         out = zeros((nb, c, h, w), g.fp)
         ja = self.take(ARITH)
         jr, jq = self.take(TR_RHO), self.take(TR_R)
-        K.call("mpc3_rss_col2im_reshare_truncate", self.rk, self.ctr_ptr, ja, jr, jq, bits, z.data_ptr(), nb, c, oh,
-               ow, kh, kw, sh, sw, ph, pw, h, w, out.data.data_ptr(), _stream())
         hf, wf = (oh - 1) * sh + kh, (ow - 1) * sw + kw
         full = nb * c * hf * wf
+        K.call("mpc3_rss_col2im_reshare_truncate", self.rk, self.ctr_ptr, ja, jr, jq, bits, z.data_ptr(), nb, c, oh,
+               ow, kh, kw, sh, sw, ph, pw, h, w, out.data.data_ptr(), self.shard_offset(full)[0], _stream())
         self.ledger.ring("mul.reshare", full)
         self._charge_trunc(full)
         return out
@@ -544,7 +584,7 @@ class TrioSession:
         out = empty((nb, c, oh, ow), x.fp)
         jr, jq = self.take(TR_RHO), self.take(TR_R)
         K.call("mpc3_rss_avgpool", self.rk, self.ctr_ptr, jr, jq, bits, mulc, x.data.data_ptr(), out.data.data_ptr(),
-               nb, c, h, w, kh, kw, sh, sw, ph, pw, _stream())
+               nb, c, h, w, kh, kw, sh, sw, ph, pw, self.shard_offset(out.numel)[0], _stream())
         self._charge_trunc(out.numel)
         return out
 
@@ -559,7 +599,8 @@ class TrioSession:
         out = empty((nb, c, h, w), g.fp)
         jr, jq = self.take(TR_RHO), self.take(TR_R)
         K.call("mpc3_rss_avgpool_backward", self.rk, self.ctr_ptr, jr, jq, bits, mulc, g.data.data_ptr(),
-               out.data.data_ptr(), nb, c, h, w, oh, ow, kh, kw, sh, sw, ph, pw, _stream())
+               out.data.data_ptr(), nb, c, h, w, oh, ow, kh, kw, sh, sw, ph, pw, self.shard_offset(out.numel)[0],
+               _stream())
         self._charge_trunc(out.numel)
         return out
 

@@ -282,7 +282,7 @@ class TrioNet:
             if spec.kind == FULLY_CONNECTED:
                 x, w = cached
                 pi -= 1
-                grads[pi] = S.matmul(g.apply(lambda d: d.transpose(1, 2)), x, bits=t + batch_bits)
+                grads[pi] = S.matmul(g.apply(lambda d: d.transpose(1, 2)), x, bits=t + batch_bits, wgrad=True)
                 if li == plist[0]:
                     break
                 g = S.matmul(g, w)
@@ -309,8 +309,9 @@ class TrioNet:
         if c == 0:
             return list(params)
         S = self.s
-        return [S.sub(p, S.truncate(S.mul_const(g, c)), out=p if inplace else None)
-                for p, g in zip(params, grads)]
+        with S.replicated():  # parameters are replicated, not batch-sharded
+            return [S.sub(p, S.truncate(S.mul_const(g, c)), out=p if inplace else None)
+                    for p, g in zip(params, grads)]
 
     def loss_grad(self, logits: RssTensor, y: RssTensor) -> RssTensor:
         """softmax(logits) - y (nn.py:561-568)."""
@@ -468,6 +469,31 @@ class GraphStep:
         for p, d in self.delta.items():
             S.seq[p] += d
         return self.logits
+
+
+class DataParallel:
+    """Batch-sharded private training/inference across GPUs.
+
+    Every rank hosts all three parties for an equal contiguous batch shard.
+    Batch-major tensors are contiguous ranges of the reference's flat tensors,
+    so each kernel draws its PRF words at the shard's global offset
+    (TrioSession.shard_offset) and the shards together reproduce the
+    single-GPU run bit for bit.  The only exchange is the weight gradient:
+    the raw per-party cross terms are summed mod 2^64 across ranks before the
+    (replicated) reshare + truncation.  `allreduce(z)` sums an int64 CUDA
+    tensor in place (NCCL sum wraps like the ring)."""
+
+    def __init__(self, rank: int, world: int, allreduce):
+        self.rank, self.world, self.allreduce = rank, world, allreduce
+
+    @classmethod
+    def nccl(cls, group=None):
+        import torch.distributed as dist
+
+        def allreduce(z):
+            dist.all_reduce(z, op=dist.ReduceOp.SUM, group=group)
+
+        return cls(dist.get_rank(group), dist.get_world_size(group), allreduce)
 
 
 class InferenceGraph:

@@ -1,0 +1,106 @@
+"""Data-parallel training/inference shards reproduce the single-GPU run bit
+for bit.  Two virtual ranks run in two threads on one B200; their weight
+gradient cross terms meet in an in-process all-reduce (the NCCL path differs
+only in the transport of that one sum)."""
+
+import threading
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+import paper_2104_10949_b200 as M  # noqa: E402
+from paper_2104_10949_b200.engine import RssTensor, TrioSession  # noqa: E402
+from paper_2104_10949_b200.nn import DataParallel, TrainState, one_hot  # noqa: E402
+
+
+class ThreadAllReduce:
+    def __init__(self, world):
+        self.world = world
+        self.cv = threading.Condition()
+        self.buf, self.gen, self.done = [], 0, {}
+
+    def __call__(self, z):
+        with self.cv:
+            gen = self.gen
+            self.buf.append(z)
+            if len(self.buf) == self.world:
+                torch.cuda.synchronize()
+                total = self.buf[0].clone()
+                for t in self.buf[1:]:
+                    total += t  # int64 add wraps mod 2^64
+                for t in self.buf:
+                    t.copy_(total)
+                torch.cuda.synchronize()
+                self.buf, self.gen = [], self.gen + 1
+                self.done[gen] = True
+                self.cv.notify_all()
+            else:
+                self.cv.wait_for(lambda: self.done.get(gen), timeout=300)
+
+
+def _shard(t: RssTensor, r, world):
+    b = t.shape[0] // world
+    return RssTensor(t.data[:, r * b:(r + 1) * b].contiguous(), t.fp)
+
+
+def _run_threads(fns):
+    errs = []
+
+    def wrap(f):
+        try:
+            f()
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+
+    ths = [threading.Thread(target=wrap, args=(f,)) for f in fns]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    if errs:
+        raise errs[0]
+
+
+@pytest.mark.parametrize("model_name,batch,world", [("lenet", 8, 2), ("alexnet", 8, 2), ("lenet", 12, 4)])
+def test_dp_train_step_bit_exact(model_name, batch, world):
+    mk = M.lenet if model_name == "lenet" else M.alexnet_cifar
+    cfg = M.TrainConfig(0.05, batch, 2, seed=3)
+    rng = np.random.default_rng(5)
+    shape = (1, 28, 28) if model_name == "lenet" else (3, 32, 32)
+    xs_plain = [M.fx_encode(rng.uniform(0, 1, (batch,) + shape)) for _ in range(2)]
+    ys_plain = [M.fx_encode(one_hot(rng.integers(0, 10, batch), 10)) for _ in range(2)]
+
+    # single-GPU reference run (global batch)
+    s0 = TrioSession(7)
+    st0 = TrainState(s0, mk(), cfg)
+    batches = [st0.deal_batch(x, y) for x, y in zip(xs_plain, ys_plain)]
+    logits0 = [s0.reveal(st0.step(*b)) for b in batches]
+    w0 = [s0.reveal(p) for p in st0.params]
+
+    # `world` virtual ranks, each with its own session and batch shard
+    ar = ThreadAllReduce(world)
+    out = [None] * world
+
+    def rank(r):
+        s = TrioSession(7)
+        s.dp = DataParallel(r, world, ar)
+        st = TrainState(s, mk(), cfg)
+        _ = [st.deal_batch(x, y) for x, y in zip(xs_plain, ys_plain)]  # keep the dealer rng in step
+        lg = []
+        for xb, yb in batches:
+            lg.append(st.step(_shard(xb, r, world), _shard(yb, r, world)))
+        torch.cuda.synchronize()
+        out[r] = ([x.data.clone() for x in lg], [p.data.clone() for p in st.params], dict(s.seq))
+
+    _run_threads([lambda r=r: rank(r) for r in range(world)])
+    for i in range(2):
+        full = torch.cat([out[r][0][i] for r in range(world)], dim=1)
+        got = (full[0] + full[1] + full[2]).cpu().numpy().view(np.uint64)
+        assert np.array_equal(got, logits0[i])
+    for r in range(world):
+        for p, w in zip(out[r][1], w0):
+            assert np.array_equal((p[0] + p[1] + p[2]).cpu().numpy().view(np.uint64), w)
+        assert out[r][2] == s0.seq

@@ -88,15 +88,15 @@ def test_mul_truncate(n):
     s = R.Session(5)
     rk = rk3(s.keys)
     out = torch.empty(3 * n, dtype=torch.int64, device="cuda")
-    _capi.call("mpc3_rss_mul", p(rk), None, 0, p(dev(x)), p(dev(y)), p(out), n, stream())
+    _capi.call("mpc3_rss_mul", p(rk), None, 0, p(dev(x)), p(dev(y)), p(out), n, 0, stream())
     assert np.array_equal(host(out).reshape(3, n), R.mul(s, x, y))
     v = R.share(rng.integers(-(1 << 61), 1 << 61, n, dtype=np.int64).view(U64), rng)
     for bits in (1, 20, 61):
         s = R.Session(5)
-        _capi.call("mpc3_rss_truncate", p(rk), None, 0, 0, bits, p(dev(v)), p(out), n, stream())
+        _capi.call("mpc3_rss_truncate", p(rk), None, 0, 0, bits, p(dev(v)), p(out), n, 0, stream())
         assert np.array_equal(host(out).reshape(3, n), R.truncate(s, v, bits))
     with pytest.raises(_capi.E.RangeError):
-        _capi.call("mpc3_rss_truncate", p(rk), None, 0, 0, 62, p(dev(v)), p(out), n, stream())
+        _capi.call("mpc3_rss_truncate", p(rk), None, 0, 0, 62, p(dev(v)), p(out), n, 0, stream())
 
 
 @pytest.mark.parametrize("n", [5, 101, 4096, 100003])
@@ -187,7 +187,7 @@ def test_secure_matmul_cross_terms_reshare_truncate():
     ref = R.matmul_shares(s, x, y)
     out = torch.empty(3 * M * Nn, dtype=torch.int64, device="cuda")
     v = _capi.make_view((1, 1, M, Nn))
-    _capi.call("mpc3_rss_reshare_truncate", p(rk3(s.keys)), None, 0, 0, 0, 20, p(Cm), C.byref(v), p(out),
+    _capi.call("mpc3_rss_reshare_truncate", p(rk3(s.keys)), None, 0, 0, 0, 20, p(Cm), C.byref(v), p(out), 0,
                stream())
     assert np.array_equal(host(out).reshape(3, M, Nn), ref)
 
@@ -200,7 +200,7 @@ def test_avgpool_kernels():
     ref = R.avgpool_shares(s, x, win, stride)
     rk = rk3(s.keys)
     out = torch.empty(ref.size, dtype=torch.int64, device="cuda")
-    _capi.call("mpc3_rss_avgpool", p(rk), None, 0, 0, 20, int(R.fx_encode(1.0 / 9)), p(dev(x)), p(out), *shape, 3, 3, 2, 2, 0, 0,
+    _capi.call("mpc3_rss_avgpool", p(rk), None, 0, 0, 20, int(R.fx_encode(1.0 / 9)), p(dev(x)), p(out), *shape, 3, 3, 2, 2, 0, 0, 0,
                stream())
     assert np.array_equal(host(out).reshape(ref.shape), ref)
     g = R.share(R.fx_encode(rng.uniform(-1, 1, ref.shape[1:])), rng)
@@ -208,5 +208,5 @@ def test_avgpool_kernels():
     refb = N.avgpool_backward(N.TrioEngine(s), g, win, stride, shape)
     outb = torch.empty(refb.size, dtype=torch.int64, device="cuda")
     _capi.call("mpc3_rss_avgpool_backward", p(rk), None, 0, 0, 20, int(R.fx_encode(1.0 / 9)), p(dev(g)), p(outb), *shape,
-               ref.shape[3], ref.shape[4], 3, 3, 2, 2, 0, 0, stream())
+               ref.shape[3], ref.shape[4], 3, 3, 2, 2, 0, 0, 0, stream())
     assert np.array_equal(host(outb).reshape(refb.shape), refb)

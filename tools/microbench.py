@@ -106,9 +106,9 @@ def protocol_rates():
     med, _ = timeit(lambda: _capi.call("mpc3_rss_sign", p(rk), None, 3, 0, 0, 0, p(x), p(y), p(m), n, n, 0, st()), iters=5)
     res["relu"] = {"n": n, "ms": med * 1e3, "gelem_s": n / med / 1e9, "aes_gblocks_s": 23 * n / 2 / med / 1e9 * 2 / 2,
                    "hbm_gbs": 72 * n / med / 1e9}
-    med, _ = timeit(lambda: _capi.call("mpc3_rss_truncate", p(rk), None, 0, 0, 20, p(x), p(y), n, st()), iters=5)
+    med, _ = timeit(lambda: _capi.call("mpc3_rss_truncate", p(rk), None, 0, 0, 20, p(x), p(y), n, 0, st()), iters=5)
     res["truncate"] = {"n": n, "ms": med * 1e3, "gelem_s": n / med / 1e9, "hbm_gbs": 48 * n / med / 1e9}
-    med, _ = timeit(lambda: _capi.call("mpc3_rss_mul", p(rk), None, 0, p(x), p(x), p(y), n, st()), iters=5)
+    med, _ = timeit(lambda: _capi.call("mpc3_rss_mul", p(rk), None, 0, p(x), p(x), p(y), n, 0, st()), iters=5)
     res["mul"] = {"n": n, "ms": med * 1e3, "gelem_s": n / med / 1e9, "hbm_gbs": 72 * n / med / 1e9}
     return res
 
