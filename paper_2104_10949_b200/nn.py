@@ -487,13 +487,24 @@ class DataParallel:
         self.rank, self.world, self.allreduce = rank, world, allreduce
 
     @classmethod
-    def nccl(cls, group=None):
+    def from_process_group(cls, group=None):
+        """Ranks of an initialised torch.distributed group (NCCL on the GPUs;
+        gloo in the CPU tests of the host-side logic)."""
         import torch.distributed as dist
 
         def allreduce(z):
             dist.all_reduce(z, op=dist.ReduceOp.SUM, group=group)
 
         return cls(dist.get_rank(group), dist.get_world_size(group), allreduce)
+
+    nccl = from_process_group
+
+    def shard_rows(self, global_batch: int) -> slice:
+        """This rank's contiguous batch rows."""
+        if global_batch % self.world:
+            raise ConfigError(f"global batch {global_batch} not divisible by {self.world} ranks")
+        b = global_batch // self.world
+        return slice(self.rank * b, (self.rank + 1) * b)
 
 
 class InferenceGraph:

@@ -21,9 +21,17 @@ class ThreadAllReduce:
         self.world = world
         self.cv = threading.Condition()
         self.buf, self.gen, self.done = [], 0, {}
+        self.failed = False
+
+    def fail(self):
+        with self.cv:
+            self.failed = True
+            self.cv.notify_all()
 
     def __call__(self, z):
         with self.cv:
+            if self.failed:
+                raise RuntimeError("peer rank failed")
             gen = self.gen
             self.buf.append(z)
             if len(self.buf) == self.world:
@@ -38,7 +46,9 @@ class ThreadAllReduce:
                 self.done[gen] = True
                 self.cv.notify_all()
             else:
-                self.cv.wait_for(lambda: self.done.get(gen), timeout=300)
+                self.cv.wait_for(lambda: self.done.get(gen) or self.failed, timeout=120)
+                if not self.done.get(gen):
+                    raise RuntimeError("all-reduce aborted: a peer rank failed or timed out")
 
 
 def _shard(t: RssTensor, r, world):
@@ -46,7 +56,7 @@ def _shard(t: RssTensor, r, world):
     return RssTensor(t.data[:, r * b:(r + 1) * b].contiguous(), t.fp)
 
 
-def _run_threads(fns):
+def _run_threads(fns, ar=None):
     errs = []
 
     def wrap(f):
@@ -54,6 +64,8 @@ def _run_threads(fns):
             f()
         except BaseException as e:  # noqa: BLE001
             errs.append(e)
+            if ar is not None:
+                ar.fail()
 
     ths = [threading.Thread(target=wrap, args=(f,)) for f in fns]
     for t in ths:
@@ -64,7 +76,7 @@ def _run_threads(fns):
         raise errs[0]
 
 
-@pytest.mark.parametrize("model_name,batch,world", [("lenet", 8, 2), ("alexnet", 8, 2), ("lenet", 12, 4)])
+@pytest.mark.parametrize("model_name,batch,world", [("lenet", 8, 2), ("alexnet", 8, 2), ("lenet", 16, 4)])
 def test_dp_train_step_bit_exact(model_name, batch, world):
     mk = M.lenet if model_name == "lenet" else M.alexnet_cifar
     cfg = M.TrainConfig(0.05, batch, 2, seed=3)
@@ -95,7 +107,7 @@ def test_dp_train_step_bit_exact(model_name, batch, world):
         torch.cuda.synchronize()
         out[r] = ([x.data.clone() for x in lg], [p.data.clone() for p in st.params], dict(s.seq))
 
-    _run_threads([lambda r=r: rank(r) for r in range(world)])
+    _run_threads([lambda r=r: rank(r) for r in range(world)], ar)
     for i in range(2):
         full = torch.cat([out[r][0][i] for r in range(world)], dim=1)
         got = (full[0] + full[1] + full[2]).cpu().numpy().view(np.uint64)
