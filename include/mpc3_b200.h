@@ -75,6 +75,22 @@ int mpc3_prf_words(const uint32_t* rk, uint32_t purpose, uint64_t index, uint64_
 int mpc3_rss_zero_share(const uint32_t* rk3, const uint64_t* ctr, uint32_t purpose, uint64_t index, int xor_mode,
                         uint64_t n, uint64_t* out_trio, void* stream);
 
+/* ---- host->device boundary: encoding and dealing (ring.py:104-115,
+ *      sharing.py:113-118, session.py:62-91) ---- */
+
+/* Fixed-point encoding of float64 inputs: round-half-away-from-zero of
+ * x * 2^t, two's complement; *bad (device int, nullable) is set to 1 when
+ * some |x| >= 2^(63-t) or is not finite (the reference's RangeError). */
+int mpc3_fx_encode(const double* x, uint64_t* out, uint64_t n, int t, int* bad, void* stream);
+
+/* Dealer on the device, bit-exact with numpy's PCG64 Generator:
+ * c0 = the next n draws of rng.integers(0, 2^64), c1 = the following n,
+ * c2 = x - c0 - c1, written as trio planes.  (state, inc) is the 128-bit
+ * PCG64 state of the host Generator (bit_generator.state); the caller then
+ * advances the host Generator by 2n (bit_generator.advance). */
+int mpc3_deal_pcg64(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, const uint64_t* x,
+                    uint64_t* out_trio, uint64_t n, void* stream);
+
 /* ---- local ring ops (ring.py:50-79, protocols.py:57-72, sharing.py:54-67) ---- */
 #define MPC3_EW_ADD 0      /* out = a + b          */
 #define MPC3_EW_SUB 1      /* out = a - b          */

@@ -126,6 +126,8 @@ _SIGS = {
     "mpc3_aes128_expand": (C.c_int, [C.c_char_p, _P]),
     "mpc3_prf_words": (C.c_int, [_P, C.c_uint32, _U64, _U64, _U64, _P, _P]),
     "mpc3_rss_zero_share": (C.c_int, [_P, _P, C.c_uint32, _U64, C.c_int, _U64, _P, _P]),
+    "mpc3_fx_encode": (C.c_int, [_P, _P, _U64, C.c_int, _P, _P]),
+    "mpc3_deal_pcg64": (C.c_int, [_U64, _U64, _U64, _U64, _P, _P, _U64, _P]),
     "mpc3_ring_ew": (C.c_int, [C.c_int, _P, _P, _U64, _P, _U64, _P]),
     "mpc3_ring_rowop": (C.c_int, [C.c_int, _P, _P, _P, _U64, _U64, _P]),
     "mpc3_ring_rowsum": (C.c_int, [_P, _P, _U64, _U64, _P]),

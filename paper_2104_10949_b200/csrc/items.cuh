@@ -308,11 +308,9 @@ HD void pack_item(const uint64_t* src, int64_t plane, const Operand& o, int role
     cur.next(o);
   }
   uint8_t* base = out + ((int64_t)g * 8 * o.rows + r) * kp + ch * 8;
-  for (int l = 0; l < 8; ++l) {
-    uint64_t word = 0;
-    for (int e = 0; e < 8; ++e) word |= ((v[e] >> (8 * l)) & 0xffull) << (8 * e);
-    *reinterpret_cast<uint64_t*>(base + (int64_t)l * o.rows * kp) = word;
-  }
+  uint64_t w[8];
+  byte_transpose8(v, w);  // w[l] byte e = byte l of v[e]
+  for (int l = 0; l < 8; ++l) *reinterpret_cast<uint64_t*>(base + (int64_t)l * o.rows * kp) = w[l];
 }
 
 }  // namespace mpc3

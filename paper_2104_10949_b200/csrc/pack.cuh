@@ -109,6 +109,40 @@ struct GatherCursor {
   }
 };
 
+// __byte_perm on the device, its definition on the host (self-check build).
+HD uint32_t perm32(uint32_t a, uint32_t b, uint32_t sel) {
+#if defined(__CUDA_ARCH__)
+  return __byte_perm(a, b, sel);
+#else
+  uint64_t ab = ((uint64_t)b << 32) | a;
+  uint32_t r = 0;
+  for (int i = 0; i < 4; ++i) r |= (uint32_t)((ab >> (8 * ((sel >> (4 * i)) & 7))) & 0xff) << (8 * i);
+  return r;
+#endif
+}
+
+// 4x4 byte transpose of four words: r[l] byte e = byte l of a[e] (8 PRMTs).
+HD void byte_transpose4(const uint32_t a[4], uint32_t r[4]) {
+  uint32_t t0 = perm32(a[0], a[1], 0x5140), t1 = perm32(a[0], a[1], 0x7362);
+  uint32_t t2 = perm32(a[2], a[3], 0x5140), t3 = perm32(a[2], a[3], 0x7362);
+  r[0] = perm32(t0, t2, 0x5410);
+  r[1] = perm32(t0, t2, 0x7632);
+  r[2] = perm32(t1, t3, 0x5410);
+  r[3] = perm32(t1, t3, 0x7632);
+}
+
+// 8x8 byte transpose: w[l] byte e = byte l of v[e] (limb planes of 8 words).
+HD void byte_transpose8(const uint64_t v[8], uint64_t w[8]) {
+  uint32_t a[4], r0[4], r1[4];
+  for (int half = 0; half < 2; ++half) {  // limbs 0-3 from the low words, 4-7 from the high
+    for (int e = 0; e < 4; ++e) a[e] = (uint32_t)(v[e] >> (32 * half));
+    byte_transpose4(a, r0);
+    for (int e = 0; e < 4; ++e) a[e] = (uint32_t)(v[4 + e] >> (32 * half));
+    byte_transpose4(a, r1);
+    for (int l = 0; l < 4; ++l) w[4 * half + l] = (uint64_t)r0[l] | ((uint64_t)r1[l] << 32);
+  }
+}
+
 // Value of the packed operand of group g (party, or 0 for a plain operand) at
 // (r, kk) with kk in [0, 2K) for the cross-term roles (protocols.py:110-115).
 HD uint64_t packed_value(const Operand& o, const uint64_t* src, int64_t plane, int role, int g, int64_t r,

@@ -263,6 +263,35 @@ class TrioSession:
         self.ledger.round(label, [(owner, p, 2 * n) for p in range(3) if p != owner])
         return RssTensor(to_device(comps), self.fp)
 
+    def share_device(self, x: torch.Tensor, rng: np.random.Generator, label: str = "share.input",
+                     owner: int = 0) -> RssTensor:
+        """`share` for an input already on the device (int64 bit-cast ring
+        values): the dealer's PCG64 draws are generated by the GPU, word for
+        word the ones numpy would return, and the host Generator is advanced
+        past them (sharing.py:113-118)."""
+        st = rng.bit_generator.state
+        if st.get("bit_generator") != "PCG64":
+            raise ConfigError("device dealing reproduces numpy's PCG64 Generator only")
+        s, inc = int(st["state"]["state"]), int(st["state"]["inc"])
+        x = x.contiguous()
+        n = x.numel()
+        out = empty(tuple(x.shape), self.fp)
+        m64 = (1 << 64) - 1
+        K.call("mpc3_deal_pcg64", s >> 64, s & m64, inc >> 64, inc & m64, x.data_ptr(), out.data.data_ptr(), n,
+               _stream())
+        rng.bit_generator.advance(2 * n)
+        self.ledger.round(label, [(owner, p, 2 * n) for p in range(3) if p != owner])
+        return out
+
+    def fx_encode_device(self, x: torch.Tensor, bad: torch.Tensor | None = None) -> torch.Tensor:
+        """ring.fx_encode on a float64 device tensor; `bad` (int32 device
+        scalar) becomes 1 on an out-of-range input (checked by the caller)."""
+        x = x.to(torch.float64).contiguous()
+        out = torch.empty(x.shape, dtype=torch.int64, device=x.device)
+        K.call("mpc3_fx_encode", x.data_ptr(), out.data_ptr(), x.numel(), self.fp.t,
+               None if bad is None else bad.data_ptr(), _stream())
+        return out
+
     def from_components(self, comps) -> RssTensor:
         return RssTensor(to_device(np.asarray(comps, U64)), self.fp)
 

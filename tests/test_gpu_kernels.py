@@ -210,3 +210,34 @@ def test_avgpool_kernels():
     _capi.call("mpc3_rss_avgpool_backward", p(rk), None, 0, 0, 20, int(R.fx_encode(1.0 / 9)), p(dev(g)), p(outb), *shape,
                ref.shape[3], ref.shape[4], 3, 3, 2, 2, 0, 0, 0, stream())
     assert np.array_equal(host(outb).reshape(refb.shape), refb)
+
+
+@pytest.mark.parametrize("n", [1, 31, 32, 33, 100003])
+def test_device_dealer_matches_numpy_pcg64(n):
+    from paper_2104_10949_b200.engine import TrioSession
+
+    rng = np.random.default_rng(5 + n)
+    x = rnd(rng, n)
+    s = TrioSession(0)
+    r_host, r_dev = np.random.default_rng(99), np.random.default_rng(99)
+    r_host.integers(0, 10, 7)  # arbitrary prior use of the generator
+    r_dev.integers(0, 10, 7)
+    ref = R.share(x, r_host)
+    got = s.share_device(dev(x), r_dev)
+    assert np.array_equal(got.data.cpu().numpy().view(U64), ref)
+    # the host generator stays in lockstep afterwards
+    assert np.array_equal(r_host.integers(0, 1 << 64, 5, dtype=U64), r_dev.integers(0, 1 << 64, 5, dtype=U64))
+
+
+def test_device_fx_encode_matches_reference():
+    from paper_2104_10949_b200.engine import TrioSession
+
+    rng = np.random.default_rng(1)
+    x = np.concatenate([rng.uniform(-1e6, 1e6, 10000), [0.0, -0.0, 0.5 / (1 << 20), -0.5 / (1 << 20), 3.5, -3.5]])
+    s = TrioSession(0)
+    bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+    got = s.fx_encode_device(torch.from_numpy(x).cuda(), bad)
+    assert np.array_equal(got.cpu().numpy().view(U64), R.fx_encode(x))
+    assert int(bad.item()) == 0
+    s.fx_encode_device(torch.tensor([float(1 << 43)], dtype=torch.float64, device="cuda"), bad)
+    assert int(bad.item()) == 1
