@@ -247,6 +247,19 @@ int mpc3_ring_pack(const uint64_t* src, int64_t src_plane, const mpc3_operand* o
 int mpc3_ring_gemm_packed(const uint8_t* A, const uint8_t* B, uint64_t* C, int groups, int64_t M,
                           int64_t N, int64_t kp, int64_t ldc, int64_t c_group, int splits, void* stream);
 
+/* The secure layer's per-party cross terms as ONE implicit ring GEMM per
+ * party (protocols.py:110-115):
+ *   C[g] = [a_g + a_{g+1} | a_g] . [b_g | b_{g+1}]^T,  g = 0, 1, 2,
+ * gathered straight from the trio tensors through the operand descriptors
+ * (dense / im2col / weight-gradient views, op_a->k == op_b->k = K, inner
+ * length 2K): producer warps split the gathered u64 values into byte limbs in
+ * shared memory, so no packed operand is materialised.  C: 3 groups of
+ * op_a->rows x op_b->rows, leading dim ldc, group stride c_group; splits > 1
+ * needs C zeroed. */
+int mpc3_ring_gemm_cross(const uint64_t* src_a, int64_t plane_a, const mpc3_operand* op_a, const uint64_t* src_b,
+                         int64_t plane_b, const mpc3_operand* op_b, uint64_t* C, int64_t ldc, int64_t c_group,
+                         int splits, void* stream);
+
 /* Reference GPU path (CUDA cores, 64-bit IMAD): C = A . B mod 2^64 with
  * arbitrary strides; used as an on-device cross-check and for tiny shapes. */
 int mpc3_ring_gemm_simt(const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t M, int64_t N, int64_t K,

@@ -271,6 +271,210 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 // ---------------------------------------------------------------------------
+// Implicit ring GEMM: the secure layer's cross terms straight from the trio
+// tensors.  Producer warps gather the u64 operand values (dense / im2col /
+// weight-gradient views, protocols.py:110-115 cross-term concatenation),
+// split them into byte limbs and write the 32-byte-swizzled K-major tiles the
+// UMMA descriptors read; no packed operand ever touches HBM.  MMA issue,
+// TMEM accumulation and the epilogue are those of gemm_tc_kernel.
+
+constexpr int IG_PRODUCERS = 128;  // warps 0-3
+constexpr int IG_THREADS = 288;    // + warp 4 (MMA, TMEM alloc) + warps 5-8 (epilogue)
+
+// byte offset of (row, 4-byte k-group kq) in a K-major SWIZZLE_32B tile
+// (Swizzle<1,4,3>: the 16-byte chunk index XORs with row bit 2)
+DEV uint32_t sw32_off(int row, int kq) {
+  uint32_t off = (uint32_t)row * 32 + (uint32_t)kq * 4;
+  return off ^ ((((uint32_t)row >> 2) & 1u) << 4);
+}
+
+DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// 4 consecutive packed values (k .. k+3 of the 2K-long cross-term row) ->
+// 8 limb words of 4 bytes each, stored into the limb planes of one tile.
+DEV void produce4(const uint64_t* __restrict__ src, int64_t plane, const Operand& o, int role, int g, int64_t r,
+                  int64_t rows, int64_t k, uint8_t* tile, int row_in_tile, int kq, int limb_stride) {
+  uint64_t v[4] = {0, 0, 0, 0};
+  if (r < rows) {
+    const int64_t K = o.k;
+    const int gn = (g + 1) % 3;
+    GatherCursor cur;
+    int half = -1;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int64_t kk = k + j;
+      if (kk >= 2 * K) break;
+      int h = kk >= K ? 1 : 0;
+      if (h != half) {
+        cur.init(o, r, h ? kk - K : kk);
+        half = h;
+      }
+      int64_t off = cur.offset(o);
+      if (off >= 0) {
+        uint64_t self = __ldg(src + g * plane + off), nxt = __ldg(src + gn * plane + off);
+        v[j] = role == 0 ? (h == 0 ? self + nxt : self) : (h == 0 ? self : nxt);
+      }
+      cur.next(o);
+    }
+  }
+  uint32_t lo[4], hi[4], tl[4], th[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    lo[j] = (uint32_t)v[j];
+    hi[j] = (uint32_t)(v[j] >> 32);
+  }
+  byte_transpose4(lo, tl);  // tl[l] = byte l of v[0..3]
+  byte_transpose4(hi, th);
+  uint32_t o_ = sw32_off(row_in_tile, kq);
+#pragma unroll
+  for (int l = 0; l < 4; ++l) {
+    *reinterpret_cast<uint32_t*>(tile + l * limb_stride + o_) = tl[l];
+    *reinterpret_cast<uint32_t*>(tile + (l + 4) * limb_stride + o_) = th[l];
+  }
+}
+
+__global__ void __launch_bounds__(IG_THREADS, 1)
+    gemm_ig_kernel(const uint64_t* __restrict__ srcA, int64_t planeA, Operand oa, const uint64_t* __restrict__ srcB,
+                   int64_t planeB, Operand ob, uint64_t* __restrict__ C, int64_t M, int64_t N, int64_t ldc,
+                   int64_t c_group, int splits, int kb_per_split) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t n0 = (int64_t)blockIdx.x * BN, m0 = (int64_t)blockIdx.y * BM;
+  const int g = blockIdx.z / splits, split = blockIdx.z % splits;
+  const int64_t kp = 2 * oa.k;
+  const int nkb_total = (int)((kp + BK - 1) / BK);
+  const int kb0 = split * kb_per_split;
+  int kb1 = kb0 + kb_per_split;
+  if (kb1 > nkb_total) kb1 = nkb_total;
+  const int nkb = kb1 > kb0 ? kb1 - kb0 : 0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], IG_PRODUCERS);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 4) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {
+    // ---- producers: gather + limb split into the swizzled tiles ----
+    const int t = threadIdx.x;
+    for (int i = 0; i < nkb; ++i) {
+      int s = i % STAGES;
+      uint32_t ph = (i / STAGES) & 1;
+      mbar_wait(&empty[s], ph ^ 1);
+      const int64_t kbase = (int64_t)(kb0 + i) * BK;
+      uint8_t* ta = sA + s * A_STAGE;
+      uint8_t* tb = sB + s * B_STAGE;
+#pragma unroll 1
+      for (int task = t; task < BM * 8; task += IG_PRODUCERS) {  // A: 128 rows x 8 k-quads
+        int row = task >> 3, kq = task & 7;
+        produce4(srcA, planeA, oa, 0, g, m0 + row, M, kbase + 4 * kq, ta, row, kq, BM * BK);
+      }
+#pragma unroll 1
+      for (int task = t; task < BN * 8; task += IG_PRODUCERS) {  // B: 64 rows x 8 k-quads
+        int row = task >> 3, kq = task & 7;
+        produce4(srcB, planeB, ob, 1, g, n0 + row, N, kbase + 4 * kq, tb, row, kq, BN * BK);
+      }
+      // generic-proxy smem writes -> visible to the tensor core (async proxy)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&full[s]);
+    }
+  } else if (warp == 4) {
+    if (lane == 0) {
+      // ---- MMA issuer ----
+      for (int i = 0; i < nkb; ++i) {
+        int s = i % STAGES;
+        uint32_t ph = (i / STAGES) & 1;
+        mbar_wait(&full[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        uint32_t a_base = smem_u32(sA + s * A_STAGE);
+        uint32_t b_base = smem_u32(sB + s * B_STAGE);
+#pragma unroll
+        for (int li = 0; li < 8; ++li) {
+          uint64_t da = umma_desc_sw32(a_base + li * (BM * BK));
+          int nblk = 8 - li;
+          int first = nblk > 4 ? 4 : nblk;
+          uint32_t acc = (i > 0 || li > 0) ? 1u : 0u;
+          mma_i8(tmem + li * BN, da, umma_desc_sw32(b_base), idesc_i8(first * BN), acc);
+          if (nblk > 4)
+            mma_i8(tmem + (li + 4) * BN, da, umma_desc_sw32(b_base + 4 * (BN * BK)), idesc_i8((nblk - 4) * BN),
+                   acc);
+        }
+        mma_commit(&empty[s]);
+      }
+      mma_commit(tmem_full);
+    }
+  } else {
+    // ---- epilogue (warps 5-8 cover TMEM lane quadrants 1,2,3,0) ----
+    const int wq = warp % 4;
+    const int64_t row = m0 + wq * 32 + lane;
+    uint64_t* crow = C + (int64_t)g * c_group + row * ldc;
+    if (nkb > 0) {
+      mbar_wait(tmem_full, 0);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+    }
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 8) {
+      uint64_t acc[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = 0;
+      if (nkb > 0) {
+#pragma unroll
+        for (int d = 0; d < 8; ++d) {
+          uint32_t r[8];
+          uint32_t taddr = tmem + ((uint32_t)(wq * 32) << 16) + d * BN + c0;
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+              : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] += (uint64_t)r[e] << (8 * d);
+        }
+      }
+      if (row < M) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          int64_t col = n0 + c0 + e;
+          if (col < N) {
+            if (splits > 1)
+              atomicAdd(reinterpret_cast<unsigned long long*>(crow + col), (unsigned long long)acc[e]);
+            else
+              crow[col] = acc[e];
+          }
+        }
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+  }
+  __syncthreads();
+  if (warp == 4) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host: tensor maps via the driver entry point (no -lcuda link needed)
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -388,6 +592,32 @@ int mpc3_ring_gemm_packed(const uint8_t* A, const uint8_t* B, uint64_t* C, int g
   dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)(groups * splits));
   gemm_tc_kernel<<<grid, 256, SMEM_BYTES, as_stream(stream)>>>(ta, tb, C, M, N, kp, ldc, c_group, splits, kbs);
   return check_launch("ring_gemm_tc");
+}
+
+int mpc3_ring_gemm_cross(const uint64_t* src_a, int64_t plane_a, const mpc3_operand* op_a, const uint64_t* src_b,
+                         int64_t plane_b, const mpc3_operand* op_b, uint64_t* C, int64_t ldc, int64_t c_group,
+                         int splits, void* stream) {
+  if (!op_a || !op_b || splits < 1) return MPC3_ERR_CONFIG;
+  if (op_a->k != op_b->k || op_a->k < 0 || op_a->rows < 0 || op_b->rows < 0) return MPC3_ERR_SHAPE;
+  if (op_a->mode < 0 || op_a->mode > 2 || op_b->mode < 0 || op_b->mode > 2) return MPC3_ERR_CONFIG;
+  int64_t M = op_a->rows, N = op_b->rows;
+  if (M == 0 || N == 0) return MPC3_OK;
+  if (M > (1 << 30) || N > (1 << 30)) return MPC3_ERR_SHAPE;
+  Operand oa = to_operand(op_a), ob = to_operand(op_b);
+  int64_t kp = 2 * op_a->k;
+  int nkb = (int)((kp + BK - 1) / BK);
+  int kbs = (nkb + splits - 1) / splits;
+  if ((int64_t)kbs * BK > MAX_SPLIT_K) return MPC3_ERR_EXACTNESS;  // caller must split longer K
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(gemm_ig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess)
+      return check_launch("gemm_ig attr");
+    attr_set = true;
+  }
+  dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)(3 * splits));
+  gemm_ig_kernel<<<grid, IG_THREADS, SMEM_BYTES, as_stream(stream)>>>(src_a, plane_a, oa, src_b, plane_b, ob, C, M,
+                                                                      N, ldc, c_group, splits, kbs);
+  return check_launch("ring_gemm_cross");
 }
 
 int mpc3_ring_gemm_simt(const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t M, int64_t N, int64_t K,

@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -40,6 +41,7 @@ from .transport import Ledger
 
 U64 = np.uint64
 MAX_SPLIT_K = 16384  # per-split K bound of the int8-limb GEMM (exactness of S_3)
+PACKED_GEMM = os.environ.get("MPC3_PACKED_GEMM", "0") == "1"
 SMS = 148
 
 
@@ -443,7 +445,15 @@ class TrioSession:
     # -- bilinear layers (protocols.py:97-136, nn.py:435-484) --
     def _cross_gemm(self, a_src, a_op, b_src, b_op, M, N, Kd) -> torch.Tensor:
         """z_i = (x_i + x_{i+1}) y_i + x_i y_{i+1} for the three parties, as one
-        batched ring GEMM with inner length 2K (protocols.py:110-115)."""
+        batched ring GEMM with inner length 2K (protocols.py:110-115).
+        Default: the implicit GEMM (gather + limb split inside the kernel);
+        MPC3_PACKED_GEMM=1 selects the explicit pack + TMA path."""
+        if not PACKED_GEMM:
+            splits = gemm_splits(M, N, 2 * Kd, groups=3)
+            z = (torch.zeros if splits > 1 else torch.empty)(3 * M * N, dtype=torch.int64, device=_dev())
+            K.call("mpc3_ring_gemm_cross", a_src.data_ptr(), a_src.stride(0), C.byref(a_op), b_src.data_ptr(),
+                   b_src.stride(0), C.byref(b_op), z.data_ptr(), N, M * N, splits, _stream())
+            return z
         kp = _round_up(2 * Kd, 16)
         A = torch.empty(3 * 8 * M * kp, dtype=torch.uint8, device=_dev())
         B = torch.empty(3 * 8 * N * kp, dtype=torch.uint8, device=_dev())

@@ -212,6 +212,50 @@ def test_avgpool_kernels():
     assert np.array_equal(host(outb).reshape(refb.shape), refb)
 
 
+@pytest.mark.parametrize("M,K,Nn,splits", [(1, 1, 1, 1), (9, 33, 7, 1), (130, 101, 70, 1), (300, 257, 129, 3),
+                                           (37, 9000, 40, 2), (200, 4608, 512, 1)])
+def test_implicit_cross_gemm_matches_cross_terms(M, K, Nn, splits):
+    """mpc3_ring_gemm_cross == (x_i + x_{i+1}) y_i + x_i y_{i+1} per party."""
+    rng = np.random.default_rng(M + K)
+    x = rnd(rng, (3, M, K))
+    y = rnd(rng, (3, K, Nn))
+    xd, yd = dev(x), dev(y)
+    a_op = _capi.dense_operand(M, K, s_r=K, t2=1)
+    b_op = _capi.dense_operand(Nn, K, s_r=1, t2=Nn)
+    Cm = torch.zeros(3 * M * Nn, dtype=torch.int64, device="cuda")
+    _capi.call("mpc3_ring_gemm_cross", p(xd), M * K, C.byref(a_op), p(yd), K * Nn, C.byref(b_op), p(Cm), Nn, M * Nn,
+               splits, stream())
+    got = host(Cm).reshape(3, M, Nn)
+    if M * K * Nn <= 20_000_000:
+        ref = R._bilinear3(R.wrap_matmul, x, y)
+        assert np.array_equal(got, ref)
+    else:  # compare with the explicit-pack TMA path
+        kp = (2 * K + 15) // 16 * 16
+        A = _pack(xd, M * K, a_op, 0, kp)
+        B = _pack(yd, K * Nn, b_op, 1, kp)
+        assert np.array_equal(got, _gemm_packed(A, B, 3, M, Nn, kp, 1))
+
+
+def test_implicit_cross_gemm_conv_geometries():
+    rng = np.random.default_rng(8)
+    for xs_, ks_, st, pd in [((2, 3, 10, 10), (4, 3, 3, 3), (2, 2), (1, 1)), ((4, 3, 32, 32), (96, 3, 11, 11), (4, 4), (9, 9))]:
+        n, c, h, w = xs_
+        o, _, kh, kw = ks_
+        oh, ow = R.conv_out_hw(h, w, kh, kw, st, pd)
+        x, k = rnd(rng, (3,) + xs_), rnd(rng, (3,) + ks_)
+        xd, kd = dev(x), dev(k)
+        Kc = c * kh * kw
+        a_op = _capi.conv_operand(_capi.GATHER_IM2COL, n * oh * ow, Kc, n, c, h, w, (c * h * w, h * w, w, 1), kh, kw,
+                                  st[0], st[1], pd[0], pd[1], oh, ow)
+        b_op = _capi.dense_operand(o, Kc, s_r=Kc, t2=1)
+        M = n * oh * ow
+        Cm = torch.zeros(3 * M * o, dtype=torch.int64, device="cuda")
+        _capi.call("mpc3_ring_gemm_cross", p(xd), x[0].size, C.byref(a_op), p(kd), k[0].size, C.byref(b_op), p(Cm), o,
+                   M * o, 1, stream())
+        got = host(Cm).reshape(3, n, oh, ow, o).transpose(0, 1, 4, 2, 3)
+        assert np.array_equal(got, R._bilinear3(lambda a, b: R.wrap_conv2d(a, b, st, pd), x, k))
+
+
 @pytest.mark.parametrize("n", [1, 31, 32, 33, 100003])
 def test_device_dealer_matches_numpy_pcg64(n):
     from paper_2104_10949_b200.engine import TrioSession
