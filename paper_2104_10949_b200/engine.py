@@ -41,7 +41,10 @@ from .transport import Ledger
 
 U64 = np.uint64
 MAX_SPLIT_K = 16384  # per-split K bound of the int8-limb GEMM (exactness of S_3)
-PACKED_GEMM = os.environ.get("MPC3_PACKED_GEMM", "0") == "1"
+# explicit pack + TMA GEMM by default; MPC3_IMPLICIT_GEMM=1 selects the in-kernel
+# gather variant (gemm_ig_kernel: 3-25x slower on the AlexNet/ResNet shapes,
+# profiles/r01_launches_alexnet_implicit.txt)
+IMPLICIT_GEMM = os.environ.get("MPC3_IMPLICIT_GEMM", "0") == "1"
 SMS = 148
 
 
@@ -446,9 +449,9 @@ class TrioSession:
     def _cross_gemm(self, a_src, a_op, b_src, b_op, M, N, Kd) -> torch.Tensor:
         """z_i = (x_i + x_{i+1}) y_i + x_i y_{i+1} for the three parties, as one
         batched ring GEMM with inner length 2K (protocols.py:110-115).
-        Default: the implicit GEMM (gather + limb split inside the kernel);
-        MPC3_PACKED_GEMM=1 selects the explicit pack + TMA path."""
-        if not PACKED_GEMM:
+        Default: pack_kernel writes the byte-limb planes, the TMA-fed tcgen05
+        GEMM consumes them; MPC3_IMPLICIT_GEMM=1 selects the in-kernel gather."""
+        if IMPLICIT_GEMM:
             splits = gemm_splits(M, N, 2 * Kd, groups=3)
             z = (torch.zeros if splits > 1 else torch.empty)(3 * M * N, dtype=torch.int64, device=_dev())
             K.call("mpc3_ring_gemm_cross", a_src.data_ptr(), a_src.stride(0), C.byref(a_op), b_src.data_ptr(),

@@ -9,7 +9,7 @@ def main(path, skip_frac=0.5):
     hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h, data = rows[hi], rows[hi + 1:]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
-    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
     data = data[int(len(data) * skip_frac):]  # drop the warm-up step
     tot, cnt, allt = collections.defaultdict(float), collections.Counter(), 0.0
     for r in data:

@@ -104,12 +104,22 @@ def protocol_rates():
     y = torch.empty_like(x)
     m = torch.empty_like(x)
     med, _ = timeit(lambda: _capi.call("mpc3_rss_sign", p(rk), None, 3, 0, 0, 0, p(x), p(y), p(m), n, n, 0, st()), iters=5)
-    res["relu"] = {"n": n, "ms": med * 1e3, "gelem_s": n / med / 1e9, "aes_gblocks_s": 23 * n / 2 / med / 1e9 * 2 / 2,
+    # 23 AES-128 blocks per element (46 PRF words: BIN 1, XOR 36, ARITH 9)
+    res["relu"] = {"n": n, "ms": med * 1e3, "gelem_s": n / med / 1e9, "aes_gblocks_s": 23 * n / med / 1e9,
                    "hbm_gbs": 72 * n / med / 1e9}
     med, _ = timeit(lambda: _capi.call("mpc3_rss_truncate", p(rk), None, 0, 0, 20, p(x), p(y), n, 0, st()), iters=5)
     res["truncate"] = {"n": n, "ms": med * 1e3, "gelem_s": n / med / 1e9, "hbm_gbs": 48 * n / med / 1e9}
     med, _ = timeit(lambda: _capi.call("mpc3_rss_mul", p(rk), None, 0, p(x), p(x), p(y), n, 0, st()), iters=5)
     res["mul"] = {"n": n, "ms": med * 1e3, "gelem_s": n / med / 1e9, "hbm_gbs": 72 * n / med / 1e9}
+    # launch latency of the small launches of a training step (no L2 flush)
+    for small in (64, 1024, 16384, 262144):
+        xs, ys, ms = x[:3 * small], y[:3 * small], m[:3 * small]
+        med, _ = timeit(lambda: _capi.call("mpc3_rss_sign", p(rk), None, 3, 0, 0, 0, p(xs), p(ys), p(ms), small, small,
+                                           0, st()), iters=20, flush=False)
+        res[f"relu_n{small}_us"] = med * 1e6
+        med, _ = timeit(lambda: _capi.call("mpc3_rss_mul", p(rk), None, 0, p(xs), p(xs), p(ys), small, 0, st()),
+                        iters=20, flush=False)
+        res[f"mul_n{small}_us"] = med * 1e6
     return res
 
 

@@ -1,0 +1,47 @@
+"""Launch one kernel a few times for an `ncu --set full` capture.
+
+python tools/ncu_target.py gemm 4096      # mpc3_ring_gemm_packed, M=N=K=n (packed limb planes)
+python tools/ncu_target.py sign 16777216  # fused sign/ReLU circuit on n elements
+python tools/ncu_target.py pack 4096      # dense cross-term pack, 3 parties, M=K=n
+"""
+import ctypes as C
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2104_10949_b200 import _capi  # noqa: E402
+from tools.microbench import p, rk3, st  # noqa: E402
+
+
+def main(kind, n, reps=3):
+    if kind == "gemm":
+        kp = (n + 15) // 16 * 16
+        A = torch.randint(0, 256, (8 * n * kp,), dtype=torch.uint8, device="cuda")
+        B = torch.randint(0, 256, (8 * n * kp,), dtype=torch.uint8, device="cuda")
+        Cm = torch.empty(n * n, dtype=torch.int64, device="cuda")
+        for _ in range(reps):
+            _capi.call("mpc3_ring_gemm_packed", p(A), p(B), p(Cm), 1, n, n, kp, n, 0, 1, st())
+    elif kind == "sign":
+        rk = rk3()
+        x = torch.randint(-(1 << 40), 1 << 40, (3 * n,), dtype=torch.int64, device="cuda")
+        y, m = torch.empty_like(x), torch.empty_like(x)
+        for _ in range(reps):
+            _capi.call("mpc3_rss_sign", p(rk), None, 3, 0, 0, 0, p(x), p(y), p(m), n, n, 0, st())
+    elif kind == "pack":
+        x = torch.randint(-(1 << 62), 1 << 62, (3 * n * n,), dtype=torch.int64, device="cuda")
+        kp = 2 * n
+        out = torch.empty(3 * 8 * n * kp, dtype=torch.uint8, device="cuda")
+        op = _capi.Operand()
+        op.mode, op.rows, op.k, op.s_r, op.t2 = 0, n, n, n, 1
+        for _ in range(reps):
+            _capi.call("mpc3_ring_pack", p(x), n * n, C.byref(op), 0, p(out), kp, st())
+    else:
+        raise SystemExit(f"unknown kernel {kind}")
+    torch.cuda.synchronize()
+    print("ok", kind, n)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], int(sys.argv[2]))
