@@ -133,6 +133,27 @@ int mpc3_rss_mul_truncate(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_a
                           const uint64_t* x, const uint64_t* y, uint64_t* out, uint64_t n, uint64_t elem_off,
                           void* stream);
 
+/* Fused elementwise chain over a per-element trio z (starts as x), the chain
+ * input x and a temporary t; replaces the launch-per-call sequences of
+ * exp_approx (add_const + squarings, protocols.py:414-424) and reciprocal
+ * (Newton iterations, protocols.py:427-440).  The k-th SQ/SQT/MULX step uses
+ * counters j_arith + k, j_rho + k, j_r + k (the counters the unfused
+ * mul_truncate calls take).  Output: z. */
+#define MPC3_CHAIN_MAX_STEPS 48
+#define MPC3_CHAIN_ADDC 0   /* z.c0 += c (public constant into component 0, protocols.py:57-62) */
+#define MPC3_CHAIN_SETC 1   /* z = (c, 0, 0) (const_share, sharing.py:184-187) */
+#define MPC3_CHAIN_SQ 2     /* z = truncate(mul(z, z), bits) */
+#define MPC3_CHAIN_MULX 3   /* t = truncate(mul(x, t), bits) */
+#define MPC3_CHAIN_NEWTON 4 /* z = 2 z - t */
+#define MPC3_CHAIN_SQT 5    /* t = truncate(mul(z, z), bits) */
+typedef struct {
+  int op, bits;
+  uint64_t c;
+} MPC3ChainStep;
+int mpc3_rss_chain(const uint32_t* rk3, const uint64_t* ctr, const MPC3ChainStep* steps, int nsteps, uint64_t j_arith,
+                   uint64_t j_rho, uint64_t j_r, const uint64_t* x, uint64_t* out, uint64_t n, uint64_t elem_off,
+                   void* stream);
+
 /* Sign circuit (protocols.py:266-348): a2b + 64-bit Kogge-Stone + msb +
  * bit_inject + relu, fused, all 11 rounds in registers.
  * mode 0 = a2b (out: XOR trio of x), 1 = msb (XOR trio of the sign bit),

@@ -52,6 +52,23 @@ class Operand(C.Structure):
     _fields_ = [("mode", C.c_int)] + _fields_
 
 
+class ChainStep(C.Structure):
+    """MPC3ChainStep (include/mpc3_b200.h): one step of a fused elementwise chain."""
+    _fields_ = [("op", C.c_int), ("bits", C.c_int), ("c", C.c_uint64)]
+
+
+CHAIN_ADDC, CHAIN_SETC, CHAIN_SQ, CHAIN_MULX, CHAIN_NEWTON, CHAIN_SQT = range(6)
+CHAIN_MAX_STEPS = 48
+
+
+def chain_program(steps):
+    """[(op, bits, c), ...] -> (ctypes array, count)."""
+    arr = (ChainStep * max(1, len(steps)))()
+    for i, (op, bits, c) in enumerate(steps):
+        arr[i].op, arr[i].bits, arr[i].c = int(op), int(bits), int(c) % (1 << 64)
+    return arr, len(steps)
+
+
 def make_view(full, crop=None, z_stride=None, out_stride=None, z_plane=None, out_plane=None,
               origin=None) -> View4:
     full = [int(v) for v in full]
@@ -135,6 +152,7 @@ _SIGS = {
     "mpc3_rss_truncate": (C.c_int, [_P, _P, _U64, _U64, C.c_int, _P, _P, _U64, _U64, _P]),
     "mpc3_rss_mul_truncate": (C.c_int, [_P, _P, _U64, _U64, _U64, C.c_int, _P, _P, _P, _U64, _U64, _P]),
     "mpc3_rss_sign": (C.c_int, [_P, _P, C.c_int, _U64, _U64, _U64, _P, _P, _P, _U64, _U64, _U64, _P]),
+    "mpc3_rss_chain": (C.c_int, [_P, _P, _P, C.c_int, _U64, _U64, _U64, _P, _P, _U64, _U64, _P]),
     "mpc3_rss_bit_inject": (C.c_int, [_P, _P, _U64, _P, _P, _U64, _P]),
     "mpc3_rss_reshare_truncate": (C.c_int, [_P, _P, _U64, _U64, _U64, C.c_int, _P, C.POINTER(View4), _P, _U64,
                                             _P]),

@@ -168,37 +168,79 @@ struct HostTables {
 #endif
 
 #if defined(__CUDACC__)
-// Shared-memory tables, built once per CTA.
-// Bank-conflict-free lookups: the 1 KiB table is stored 32 times, interleaved
-// so that entry e of lane l's copy sits at word 32 e + l, i.e. always in bank
-// l.  A warp's 32 data-dependent lookups then take one shared-memory
-// wavefront instead of ~4 (random indices over 32 banks).  The final round's
-// S-box is byte 2 of Te0 (Te0[x] = (2S, S, S, 3S)), so no second table.
+// Te0 as a compile-time constant table (1 KiB, constant bank): the source
+// the per-CTA shared tables are expanded from.
+struct Te0Table {
+  uint32_t v[256];
+};
+constexpr uint8_t kSbox[256] = {MPC3_SBOX_BYTES};
+constexpr uint32_t xtime_c(uint32_t b) { return ((b << 1) ^ ((b & 0x80) ? 0x1b : 0)) & 0xff; }
+constexpr Te0Table make_te0() {
+  Te0Table t{};
+  for (int i = 0; i < 256; ++i) {
+    uint32_t s = kSbox[i], s2 = xtime_c(s);
+    t.v[i] = (s2 << 24) | (s << 16) | (s << 8) | (s2 ^ s);
+  }
+  return t;
+}
+__constant__ Te0Table c_te0 = make_te0();
+
+// Shared-memory tables (64 KiB, dynamic shared memory), one per CTA.
+// Entry x occupies 256 bytes: words [64x + l] = Te0[x] and [64x + 32 + l] =
+// Te1[x] = ror8(Te0[x]) for lane l, i.e. lane l's copies always sit in bank l
+// (a warp's 32 data-dependent lookups are one shared-memory wavefront).  The
+// tables start at shared-window offset kAesTableOff (the first byte of dynamic
+// shared memory after the 1 KiB the hardware reserves; checked at run time),
+// so the address of lane l's Te0[x] is hi | x << 8 | 4 l, plus kAesTableOff,
+// with hi = the window's CTA bits: ONE PRMT of the state word with (hi | 4 l)
+// forms it, the offset is the LDS immediate, and Te1 is 128 bytes further.
+// With Te0 and Te1 a column is Te0[a] ^ Te1[b] ^ ror16(Te0[c] ^ Te1[d]) ^ k
+// (ror distributes over xor): 16 PRMT + 16 LDS + 16 logic ops per round.
 struct SmemTables {
-  const uint32_t* te;  // &table[lane]
-  DEV uint32_t t0(uint32_t i) const { return te[i * 32]; }
-  DEV uint32_t sb(uint32_t i) const { return (te[i * 32] >> 8) & 0xff; }
+  uint32_t hl;  // (shared window base & 0xff000000) | 4 * lane
 };
 
-// Shared layout for protocol kernels: lane-interleaved T-table and the
-// three key schedules (33.3 KiB).
 struct __align__(16) AesSmem {
-  uint32_t te[256 * 32];
+  uint32_t te[256 * 64];
   uint32_t rk[3][44];
+  uint64_t extra[16];  // per-kernel uniform data (stream heads)
 };
+constexpr int kAesSmemBytes = (int)sizeof(AesSmem);
+constexpr uint32_t kAesTableOff = 1024;
 
-// Device rounds on the lane-interleaved table: each lookup is one byte
-// extract (PRMT / SHF), one LEA (idx * 128 B + lane base) and one LDS; the
-// generic template above is the host self-check path.
+// The protocol kernels' dynamic shared memory: an AesSmem at offset 0 (these
+// kernels declare no static shared memory, so it starts at kAesTableOff).
+extern __shared__ __align__(16) uint8_t mpc3_dsm[];
+
+DEV uint32_t lds_te0(uint32_t a) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1+1024];" : "=r"(v) : "r"(a));
+  return v;
+}
+DEV uint32_t lds_te1(uint32_t a) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1+1152];" : "=r"(v) : "r"(a));
+  return v;
+}
+
+#define MPC3_I3(x) __byte_perm((x), hl, 0x7634)
+#define MPC3_I2(x) __byte_perm((x), hl, 0x7624)
+#define MPC3_I1(x) __byte_perm((x), hl, 0x7614)
+#define MPC3_I0(x) __byte_perm((x), hl, 0x7604)
+// one output column of rounds 1-9
+#define MPC3_COL(a, b, c, d, kk)                                                                     \
+  (lds_te0(MPC3_I3(a)) ^ lds_te1(MPC3_I2(b)) ^                                                       \
+   __byte_perm(lds_te0(MPC3_I1(c)) ^ lds_te1(MPC3_I0(d)), 0, 0x1032) ^ (kk))
+// final round column: S[x] is byte 2 (and 1) of Te0[x] = (2S, S, S, 3S)
+#define MPC3_FIN(a, b, c, d, kk)                                                                     \
+  (__byte_perm(__byte_perm(lds_te0(MPC3_I3(a)), lds_te0(MPC3_I2(b)), 0x2600),                        \
+               __byte_perm(lds_te0(MPC3_I1(c)), lds_te0(MPC3_I0(d)), 0x0015), 0x3254) ^                \
+   (kk))
+
 HD void aes128_block(const SmemTables& tab, const uint32_t* rk, uint32_t& s0, uint32_t& s1, uint32_t& s2,
                      uint32_t& s3) {
 #if defined(__CUDA_ARCH__)
-  const uint32_t* T = tab.te;
-#define LK(x) T[(x) << 5]
-#define B3(x) ((x) >> 24)
-#define B2(x) __byte_perm((x), 0, 0x4442)
-#define B1(x) __byte_perm((x), 0, 0x4441)
-#define B0(x) ((x)&0xffu)
+  const uint32_t hl = tab.hl;
   s0 ^= rk[0];
   s1 ^= rk[1];
   s2 ^= rk[2];
@@ -206,38 +248,24 @@ HD void aes128_block(const SmemTables& tab, const uint32_t* rk, uint32_t& s0, ui
 #pragma unroll 1
   for (int r = 1; r < 10; ++r) {
     const uint4 k = *reinterpret_cast<const uint4*>(rk + 4 * r);
-    uint32_t t0 = LK(B3(s0)) ^ __funnelshift_r(LK(B2(s1)), LK(B2(s1)), 8) ^
-                  __funnelshift_r(LK(B1(s2)), LK(B1(s2)), 16) ^ __funnelshift_r(LK(B0(s3)), LK(B0(s3)), 24) ^ k.x;
-    uint32_t t1 = LK(B3(s1)) ^ __funnelshift_r(LK(B2(s2)), LK(B2(s2)), 8) ^
-                  __funnelshift_r(LK(B1(s3)), LK(B1(s3)), 16) ^ __funnelshift_r(LK(B0(s0)), LK(B0(s0)), 24) ^ k.y;
-    uint32_t t2 = LK(B3(s2)) ^ __funnelshift_r(LK(B2(s3)), LK(B2(s3)), 8) ^
-                  __funnelshift_r(LK(B1(s0)), LK(B1(s0)), 16) ^ __funnelshift_r(LK(B0(s1)), LK(B0(s1)), 24) ^ k.z;
-    uint32_t t3 = LK(B3(s3)) ^ __funnelshift_r(LK(B2(s0)), LK(B2(s0)), 8) ^
-                  __funnelshift_r(LK(B1(s1)), LK(B1(s1)), 16) ^ __funnelshift_r(LK(B0(s2)), LK(B0(s2)), 24) ^ k.w;
+    uint32_t t0 = MPC3_COL(s0, s1, s2, s3, k.x);
+    uint32_t t1 = MPC3_COL(s1, s2, s3, s0, k.y);
+    uint32_t t2 = MPC3_COL(s2, s3, s0, s1, k.z);
+    uint32_t t3 = MPC3_COL(s3, s0, s1, s2, k.w);
     s0 = t0;
     s1 = t1;
     s2 = t2;
     s3 = t3;
   }
-  // final round: S[x] is byte 2 of Te0[x] = (2S, S, S, 3S)
   const uint4 k = *reinterpret_cast<const uint4*>(rk + 40);
-  uint32_t t0 = (LK(B3(s0)) & 0x00ff0000u) << 8 | (LK(B2(s1)) & 0x00ff0000u) | (LK(B1(s2)) & 0x0000ff00u) |
-                (LK(B0(s3)) >> 8 & 0xffu);
-  uint32_t t1 = (LK(B3(s1)) & 0x00ff0000u) << 8 | (LK(B2(s2)) & 0x00ff0000u) | (LK(B1(s3)) & 0x0000ff00u) |
-                (LK(B0(s0)) >> 8 & 0xffu);
-  uint32_t t2 = (LK(B3(s2)) & 0x00ff0000u) << 8 | (LK(B2(s3)) & 0x00ff0000u) | (LK(B1(s0)) & 0x0000ff00u) |
-                (LK(B0(s1)) >> 8 & 0xffu);
-  uint32_t t3 = (LK(B3(s3)) & 0x00ff0000u) << 8 | (LK(B2(s0)) & 0x00ff0000u) | (LK(B1(s1)) & 0x0000ff00u) |
-                (LK(B0(s2)) >> 8 & 0xffu);
-  s0 = t0 ^ k.x;
-  s1 = t1 ^ k.y;
-  s2 = t2 ^ k.z;
-  s3 = t3 ^ k.w;
-#undef LK
-#undef B3
-#undef B2
-#undef B1
-#undef B0
+  uint32_t t0 = MPC3_FIN(s0, s1, s2, s3, k.x);
+  uint32_t t1 = MPC3_FIN(s1, s2, s3, s0, k.y);
+  uint32_t t2 = MPC3_FIN(s2, s3, s0, s1, k.z);
+  uint32_t t3 = MPC3_FIN(s3, s0, s1, s2, k.w);
+  s0 = t0;
+  s1 = t1;
+  s2 = t2;
+  s3 = t3;
 #endif
 }
 
@@ -246,13 +274,7 @@ HD void aes128_block(const SmemTables& tab, const uint32_t* rk, uint32_t& s0, ui
 // (sharing.py:233-250), and the three independent dependency chains triple
 // the instruction-level parallelism of the table rounds.
 DEV void aes128_block3(const SmemTables& tab, const uint32_t* rk3, uint32_t s[3][4]) {
-  const uint32_t* T = tab.te;
-#define LK(x) T[(x) << 5]
-#define B2(x) __byte_perm((x), 0, 0x4442)
-#define B1(x) __byte_perm((x), 0, 0x4441)
-#define ROUND_COL(a, b, c, d, kk) \
-  (LK((a) >> 24) ^ __funnelshift_r(LK(B2(b)), LK(B2(b)), 8) ^ __funnelshift_r(LK(B1(c)), LK(B1(c)), 16) ^ \
-   __funnelshift_r(LK((d)&0xffu), LK((d)&0xffu), 24) ^ (kk))
+  const uint32_t hl = tab.hl;
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -262,10 +284,10 @@ DEV void aes128_block3(const SmemTables& tab, const uint32_t* rk3, uint32_t s[3]
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
       const uint4 k = *reinterpret_cast<const uint4*>(rk3 + 44 * i + 4 * r);
-      uint32_t t0 = ROUND_COL(s[i][0], s[i][1], s[i][2], s[i][3], k.x);
-      uint32_t t1 = ROUND_COL(s[i][1], s[i][2], s[i][3], s[i][0], k.y);
-      uint32_t t2 = ROUND_COL(s[i][2], s[i][3], s[i][0], s[i][1], k.z);
-      uint32_t t3 = ROUND_COL(s[i][3], s[i][0], s[i][1], s[i][2], k.w);
+      uint32_t t0 = MPC3_COL(s[i][0], s[i][1], s[i][2], s[i][3], k.x);
+      uint32_t t1 = MPC3_COL(s[i][1], s[i][2], s[i][3], s[i][0], k.y);
+      uint32_t t2 = MPC3_COL(s[i][2], s[i][3], s[i][0], s[i][1], k.z);
+      uint32_t t3 = MPC3_COL(s[i][3], s[i][0], s[i][1], s[i][2], k.w);
       s[i][0] = t0;
       s[i][1] = t1;
       s[i][2] = t2;
@@ -276,30 +298,39 @@ DEV void aes128_block3(const SmemTables& tab, const uint32_t* rk3, uint32_t s[3]
   for (int i = 0; i < 3; ++i) {
     const uint4 k = *reinterpret_cast<const uint4*>(rk3 + 44 * i + 40);
     uint32_t a = s[i][0], b = s[i][1], c = s[i][2], d = s[i][3];
-#define FIN(w, x, y, z) \
-  ((LK((w) >> 24) & 0x00ff0000u) << 8 | (LK(B2(x)) & 0x00ff0000u) | (LK(B1(y)) & 0x0000ff00u) | \
-   (LK((z)&0xffu) >> 8 & 0xffu))
-    s[i][0] = FIN(a, b, c, d) ^ k.x;
-    s[i][1] = FIN(b, c, d, a) ^ k.y;
-    s[i][2] = FIN(c, d, a, b) ^ k.z;
-    s[i][3] = FIN(d, a, b, c) ^ k.w;
-#undef FIN
+    s[i][0] = MPC3_FIN(a, b, c, d, k.x);
+    s[i][1] = MPC3_FIN(b, c, d, a, k.y);
+    s[i][2] = MPC3_FIN(c, d, a, b, k.z);
+    s[i][3] = MPC3_FIN(d, a, b, c, k.w);
   }
-#undef ROUND_COL
-#undef LK
-#undef B2
-#undef B1
 }
+#undef MPC3_I3
+#undef MPC3_I2
+#undef MPC3_I1
+#undef MPC3_I0
+#undef MPC3_COL
+#undef MPC3_FIN
 
-// rk_dev: 3 x 44 round-key words (k_0, k_1, k_2 of the session).
+// Expand the tables into this CTA's dynamic shared memory (16-byte stores of
+// four lane copies; Te0 from the constant bank) and stage the key schedules.
+// rk_dev: nkeys x 44 round-key words (k_0, k_1, k_2 of the session).
 __device__ inline SmemTables aes_smem_init(AesSmem& sm, const uint32_t* __restrict__ rk_dev, int nkeys) {
-  for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) sm.te[i] = te0_entry(i >> 5);
+  uint4* dst = reinterpret_cast<uint4*>(sm.te);
+  for (int i = threadIdx.x; i < 256 * 16; i += blockDim.x) {
+    uint32_t v = c_te0.v[i >> 4];
+    if (i & 8) v = __funnelshift_r(v, v, 8);  // words 32-63 of the entry: Te1
+    dst[i] = make_uint4(v, v, v, v);
+  }
   for (int i = threadIdx.x; i < nkeys * 44; i += blockDim.x) (&sm.rk[0][0])[i] = rk_dev[i];
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(mpc3_dsm);
+  if ((base & 0x00ffffffu) != kAesTableOff) __trap();  // the LDS immediates assume this layout
   __syncthreads();
   SmemTables t;
-  t.te = sm.te + (threadIdx.x & 31);
+  t.hl = (base & 0xff000000u) | ((threadIdx.x & 31) * 4);
   return t;
 }
+
+#define MPC3_AES_SMEM() AesSmem& sm = *reinterpret_cast<AesSmem*>(mpc3_dsm)
 #endif
 
 }  // namespace mpc3

@@ -3,7 +3,12 @@
 // Every kernel walks PRF *blocks*: thread item b owns the element pair
 // (2b, 2b+1), because one AES block yields two adjacent stream words
 // (prf.py:40-49).  Randomness is generated inline and never touches HBM.
+#include <stdlib.h>
 #include <string.h>
+
+#include <mutex>
+#include <set>
+#include <utility>
 
 #include "launch.cuh"
 #include "items.cuh"
@@ -17,6 +22,32 @@ void set_last_error(const char* msg) {
 }
 
 constexpr int kThreads = 256;
+constexpr uint64_t kSign2MaxPairs = 200000;  // measured crossover (profiles/README.md)
+// MPC3_SIGN_FUSED=1 selects the single-phase sign kernel (AES inline in the circuit)
+static const bool g_sign_fused = [] {
+  const char* e = getenv("MPC3_SIGN_FUSED");
+  return e && e[0] == '1';
+}();
+
+// Protocol kernels take 64 KiB+ of dynamic shared memory (the AES tables):
+// opt in once per (device, kernel).
+static bool aes_attr(const void* fn, int bytes = kAesSmemBytes) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count({dev, fn})) return true;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess)
+    return false;
+  done.insert({dev, fn});
+  return true;
+}
+#define AES_LAUNCH(kern, grid, stream, ...)                                                \
+  do {                                                                                     \
+    if (!aes_attr((const void*)kern)) return check_launch(#kern " smem attribute");        \
+    kern<<<(grid), kThreads, kAesSmemBytes, (stream)>>>(__VA_ARGS__);                      \
+  } while (0)
 
 // Stream counters may be offset by a device-resident per-purpose base
 // (ctr[purpose], nullable) so a captured CUDA graph advances its PRF counters
@@ -45,7 +76,7 @@ HD StreamRef sref(uint32_t purpose, uint64_t j) {
 __global__ void __launch_bounds__(kThreads) prf_words_kernel(const uint32_t* __restrict__ rk_dev,
                                                             StreamHead h, uint64_t word_off,
                                                             uint64_t count, uint64_t* __restrict__ out) {
-  __shared__ AesSmem sm;
+  MPC3_AES_SMEM();
   SmemTables tab = aes_smem_init(sm, rk_dev, 1);
   uint64_t nblk = ((word_off + count - 1) >> 1) - (word_off >> 1) + 1;
   GRID_LOOP(t, nblk) prf_words_item(tab, sm.rk[0], h, word_off, count, out, t);
@@ -54,7 +85,7 @@ __global__ void __launch_bounds__(kThreads) prf_words_kernel(const uint32_t* __r
 __global__ void __launch_bounds__(kThreads) zero_share_kernel(const uint32_t* __restrict__ rk3,
                                                              const uint64_t* __restrict__ ctr, StreamRef rh,
                                                              int xor_mode, uint64_t n, uint64_t* __restrict__ out) {
-  __shared__ AesSmem sm;
+  MPC3_AES_SMEM();
   StreamHead h = resolve(rh, ctr);
   SmemTables tab = aes_smem_init(sm, rk3, 3);
   GRID_LOOP(b, (n + 1) >> 1) zero_share_item(tab, &sm.rk[0][0], h, xor_mode, n, out, b);
@@ -108,7 +139,7 @@ __global__ void __launch_bounds__(kThreads) arith_kernel(int kind, const uint32_
                                                         StreamRef rrho, StreamRef rr, int bits, const uint64_t* __restrict__ x,
                                                         const uint64_t* __restrict__ y,
                                                         uint64_t* __restrict__ out, uint64_t n, uint64_t pb0) {
-  __shared__ AesSmem sm;
+  MPC3_AES_SMEM();
   SmemTables tab = aes_smem_init(sm, rk3, 3);
   StreamHead ha = resolve(ra, ctr), hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
   GRID_LOOP(b, (n + 1) >> 1) arith_item(tab, &sm.rk[0][0], kind, ha, hrho, hr, bits, x, y, out, n, b, pb0);
@@ -118,14 +149,18 @@ struct SignArgs {
   uint64_t jbin, jxor, ja;
 };
 
-__global__ void __launch_bounds__(kThreads, 3) sign_kernel(const uint32_t* __restrict__ rk3,
+#ifndef MPC3_SIGN_MINB
+#define MPC3_SIGN_MINB 2  // CTAs per SM the register budget targets (2: 128 regs, no spill)
+#endif
+__global__ void __launch_bounds__(kThreads, MPC3_SIGN_MINB) sign_kernel(const uint32_t* __restrict__ rk3,
                                                           const uint64_t* __restrict__ ctr, SignArgs args,
                                                           int mode, const uint64_t* __restrict__ x,
                                                           uint64_t* __restrict__ out,
                                                           uint64_t* __restrict__ mask, uint64_t n,
                                                           uint64_t n_total, uint64_t elem_off) {
-  __shared__ AesSmem sm;
-  __shared__ SignStreams st;  // uniform stream heads, indexed by level from shared memory
+  MPC3_AES_SMEM();
+  static_assert(sizeof(SignStreams) <= sizeof(sm.extra), "stream heads fit the AesSmem extra area");
+  SignStreams& st = *reinterpret_cast<SignStreams*>(sm.extra);  // uniform stream heads, indexed by level
   if (threadIdx.x == 0) {
     st.bin = resolve(sref(BIN_INPUT, args.jbin), ctr);
     for (int l = 0; l < 7; ++l) st.x[l] = resolve(sref(XOR_ZERO, args.jxor + l), ctr);
@@ -135,11 +170,171 @@ __global__ void __launch_bounds__(kThreads, 3) sign_kernel(const uint32_t* __res
   GRID_LOOP(b, (n + 1) >> 1) sign_item(tab, &sm.rk[0][0], st, mode, x, out, mask, n, n_total, elem_off, b);
 }
 
+// Two-phase sign circuit.  The 46 AES blocks an element pair consumes do not
+// depend on the data, so phase 1 computes them for P pairs with all 256
+// threads in parallel (one three-key block per (slot, pair) item, a warp per
+// 32 pairs of one slot) into shared memory, and phase 2 runs the circuit of
+// each pair (one thread per pair) replaying those words.  A pair's latency
+// is then ~1/4 of its AES work instead of all 16 dependent AES groups, which
+// is what bounds the many small ReLU / max_tree launches of a training step;
+// at large n it is throughput-bound like sign_kernel.
+// Slots, in the circuit's call order: 0 = BIN (k_0 only); 1 = XOR level 0;
+// then per level l = 1..5: g-half, p-half (two slots when n_total is odd: the
+// pair straddles two blocks); then level 6's g-half; then the 3 ARITH muls.
+constexpr int SW_SLOT_BYTES = 3 * (int)sizeof(Word2);
+HD int sign_slots(bool straddle) { return straddle ? 21 : 16; }
+
+__global__ void __launch_bounds__(kThreads, 2) sign2_kernel(const uint32_t* __restrict__ rk3,
+                                                           const uint64_t* __restrict__ ctr, SignArgs args, int mode,
+                                                           const uint64_t* __restrict__ x, uint64_t* __restrict__ out,
+                                                           uint64_t* __restrict__ mask, uint64_t n, uint64_t n_total,
+                                                           uint64_t elem_off, int P) {
+  MPC3_AES_SMEM();
+  SignStreams& st = *reinterpret_cast<SignStreams*>(sm.extra);
+  if (threadIdx.x == 0) {
+    st.bin = resolve(sref(BIN_INPUT, args.jbin), ctr);
+    for (int l = 0; l < 7; ++l) st.x[l] = resolve(sref(XOR_ZERO, args.jxor + l), ctr);
+    for (int l = 0; l < 3; ++l) st.a[l] = resolve(sref(ARITH_ZERO, args.ja + l), ctr);
+  }
+  SmemTables tab = aes_smem_init(sm, rk3, 3);
+  Word2* slots = reinterpret_cast<Word2*>(mpc3_dsm + sizeof(AesSmem));
+  const bool straddle = (n_total & 1) != 0;
+  const int L = straddle ? 3 : 2;  // slots per level 1..5
+  const int nslots = sign_slots(straddle);
+  const int used = mode <= MODE_MSB ? nslots - 3 : (mode == MODE_DRELU ? nslots - 1 : nslots);
+  const uint64_t npairs = (n + 1) >> 1;
+  for (uint64_t c0 = (uint64_t)blockIdx.x * P; c0 < npairs; c0 += (uint64_t)gridDim.x * P) {
+    for (int q = threadIdx.x; q < used * P; q += blockDim.x) {
+      const int s = q / P, p = q % P;
+      if (c0 + p >= npairs) continue;
+      const uint64_t blk = (elem_off >> 1) + c0 + p;
+      Word2* dst = slots + ((size_t)s * P + p) * 3;
+      if (s == 0) {
+        dst[0] = prf_block(tab, &sm.rk[0][0], st.bin, blk);
+        continue;
+      }
+      StreamHead h;
+      uint64_t b = blk;
+      if (s == 1) {
+        h = st.x[0];
+      } else if (s < 2 + 5 * L) {
+        const int lvl = (s - 2) / L + 1, r = (s - 2) % L;
+        h = st.x[lvl];
+        if (r > 0) b = ((n_total + 2 * blk) >> 1) + (r - 1);  // p-half words n_total + 2 blk (+1)
+      } else if (s == 2 + 5 * L) {
+        h = st.x[6];
+      } else {
+        h = st.a[s - 3 - 5 * L];
+      }
+      Word2 w[3];
+      prf_block3(tab, &sm.rk[0][0], h, b, w);
+      dst[0] = w[0];
+      dst[1] = w[1];
+      dst[2] = w[2];
+    }
+    __syncthreads();
+    if (threadIdx.x < P && c0 + threadIdx.x < npairs) {
+      Replay rp;
+      rp.w = slots;
+      rp.P = P;
+      rp.p = threadIdx.x;
+      rp.slot = 0;
+      sign_item(rp, &sm.rk[0][0], st, mode, x, out, mask, n, n_total, elem_off, c0 + threadIdx.x);
+    }
+    __syncthreads();
+  }
+}
+
+// Fused elementwise chain (exp_approx's squarings, reciprocal's Newton
+// iterations, protocols.py:414-440): a short program over a per-element
+// register trio z, the chain input x and a temporary t, whose k-th mul+truncate
+// uses ARITH_ZERO j_a + k, TRUNC_RHO j_rho + k and TRUNC_R j_r + k, exactly the
+// counters the unfused sequence of mul_truncate calls takes.  Two phases as in
+// sign2_kernel: the 5 AES blocks per (mul, pair) are computed by all threads
+// into shared memory, then one thread per pair runs the program.
+struct ChainProgram {
+  int nsteps, nmul;
+  MPC3ChainStep s[MPC3_CHAIN_MAX_STEPS];
+};
+constexpr int CH_SLOT_WORDS = 5;  // ARITH k0..k2, RHO (k2), R (k1)
+
+__global__ void __launch_bounds__(kThreads, 1) chain_kernel(const uint32_t* __restrict__ rk3,
+                                                           const uint64_t* __restrict__ ctr, ChainProgram prog,
+                                                           uint64_t ja, uint64_t jrho, uint64_t jr,
+                                                           const uint64_t* __restrict__ x, uint64_t* __restrict__ out,
+                                                           uint64_t n, uint64_t pb0, int P) {
+  MPC3_AES_SMEM();
+  SmemTables tab = aes_smem_init(sm, rk3, 3);
+  Word2* slots = reinterpret_cast<Word2*>(mpc3_dsm + sizeof(AesSmem));
+  const uint64_t npairs = (n + 1) >> 1;
+  const uint32_t* rk = &sm.rk[0][0];
+  for (uint64_t c0 = (uint64_t)blockIdx.x * P; c0 < npairs; c0 += (uint64_t)gridDim.x * P) {
+    for (int q = threadIdx.x; q < prog.nmul * P; q += blockDim.x) {
+      const int k = q / P, p = q % P;
+      if (c0 + p >= npairs) continue;
+      const uint64_t blk = pb0 + c0 + p;
+      Word2* dst = slots + ((size_t)k * P + p) * CH_SLOT_WORDS;
+      Word2 w[3];
+      prf_block3(tab, rk, resolve(sref(ARITH_ZERO, ja + k), ctr), blk, w);
+      dst[0] = w[0];
+      dst[1] = w[1];
+      dst[2] = w[2];
+      dst[3] = prf_block(tab, rk + 2 * 44, resolve(sref(TRUNC_RHO, jrho + k), ctr), blk);
+      dst[4] = prf_block(tab, rk + 1 * 44, resolve(sref(TRUNC_R, jr + k), ctr), blk);
+    }
+    __syncthreads();
+    const int p = threadIdx.x;
+    const uint64_t b = c0 + p;
+    if (p < P && b < npairs) {
+      const bool two = 2 * b + 1 < n;
+      Trio xv[2], z[2], t[2];
+      xv[0] = load_trio(x, n, 2 * b);
+      xv[1] = two ? load_trio(x, n, 2 * b + 1) : xv[0];
+      z[0] = xv[0];
+      z[1] = xv[1];
+      t[0] = t[1] = z[0];
+      int k = 0;
+      for (int i = 0; i < prog.nsteps; ++i) {
+        const MPC3ChainStep st = prog.s[i];
+        if (st.op == MPC3_CHAIN_ADDC) {
+          z[0].c[0] += st.c;
+          z[1].c[0] += st.c;
+        } else if (st.op == MPC3_CHAIN_SETC) {
+          for (int e = 0; e < 2; ++e) z[e] = Trio{{st.c, 0, 0}};
+        } else if (st.op == MPC3_CHAIN_NEWTON) {
+          for (int e = 0; e < 2; ++e)
+            for (int c = 0; c < 3; ++c) z[e].c[c] = 2 * z[e].c[c] - t[e].c[c];
+        } else {  // SQ: z = trunc(z * z); SQT: t = trunc(z * z); MULX: t = trunc(x * t)
+          const Word2* sl = slots + ((size_t)k * P + p) * CH_SLOT_WORDS;
+          KeyWords f0, f1;
+          for (int c = 0; c < 3; ++c) {
+            f0.k[c] = sl[c].w0;
+            f1.k[c] = sl[c].w1;
+          }
+          const Word2 rho = sl[3], r = sl[4];
+          for (int e = 0; e < 2; ++e) {
+            Trio v = st.op == MPC3_CHAIN_MULX ? trio_mul(xv[e], t[e], e ? f1 : f0) : trio_mul(z[e], z[e], e ? f1 : f0);
+            v = trio_truncate(v, e ? rho.w1 : rho.w0, e ? r.w1 : r.w0, st.bits);
+            if (st.op == MPC3_CHAIN_SQ)
+              z[e] = v;
+            else
+              t[e] = v;
+          }
+          ++k;
+        }
+      }
+      store_trio(out, n, 2 * b, z[0]);
+      if (two) store_trio(out, n, 2 * b + 1, z[1]);
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) inject_kernel(const uint32_t* __restrict__ rk3,
                                                          const uint64_t* __restrict__ ctr, StreamRef r0,
                                                          StreamRef r1, const uint64_t* __restrict__ bits,
                                                          uint64_t* __restrict__ out, uint64_t n) {
-  __shared__ AesSmem sm;
+  MPC3_AES_SMEM();
   SmemTables tab = aes_smem_init(sm, rk3, 3);
   StreamHead a0 = resolve(r0, ctr), a1 = resolve(r1, ctr);
   GRID_LOOP(b, (n + 1) >> 1) inject_item(tab, &sm.rk[0][0], a0, a1, bits, out, n, b);
@@ -151,7 +346,7 @@ __global__ void __launch_bounds__(kThreads) reshare_trunc_kernel(const uint32_t*
                                                                 const uint64_t* __restrict__ z, View4 v,
                                                                 uint64_t* __restrict__ out, uint64_t n,
                                                                 uint64_t pb0) {
-  __shared__ AesSmem sm;
+  MPC3_AES_SMEM();
   SmemTables tab = aes_smem_init(sm, rk3, 3);
   StreamHead ha = resolve(ra, ctr), hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
   GRID_LOOP(b, (n + 1) >> 1) reshare_trunc_item(tab, &sm.rk[0][0], ha, hrho, hr, bits, z, v, out, n, b, pb0);
@@ -163,7 +358,7 @@ __global__ void __launch_bounds__(kThreads) pool_kernel(const uint32_t* __restri
                                                        const uint64_t* __restrict__ x,
                                                        uint64_t* __restrict__ out, PoolGeom p, uint64_t n,
                                                        uint64_t pb0) {
-  __shared__ AesSmem sm;
+  MPC3_AES_SMEM();
   SmemTables tab = aes_smem_init(sm, rk3, 3);
   StreamHead hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
   GRID_LOOP(b, (n + 1) >> 1) pool_item(tab, &sm.rk[0][0], backward != 0, hrho, hr, bits, mulc, x, out, p, b, pb0);
@@ -174,7 +369,7 @@ __global__ void __launch_bounds__(kThreads) col2im_kernel(const uint32_t* __rest
                                                          StreamRef rrho, StreamRef rr, int bits,
                                                          const uint64_t* __restrict__ z, Col2Im g,
                                                          uint64_t* __restrict__ out, uint64_t n, uint64_t pb0) {
-  __shared__ AesSmem sm;
+  MPC3_AES_SMEM();
   SmemTables tab = aes_smem_init(sm, rk3, 3);
   StreamHead ha = resolve(ra, ctr), hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
   GRID_LOOP(b, (n + 1) >> 1) col2im_item(tab, &sm.rk[0][0], ha, hrho, hr, bits, z, g, out, b, pb0);
@@ -236,7 +431,7 @@ int mpc3_prf_words(const uint32_t* rk, uint32_t purpose, uint64_t index, uint64_
   if (st) return st;
   if (count == 0) return MPC3_OK;
   uint64_t nblk = ((word_off + count - 1) >> 1) - (word_off >> 1) + 1;
-  prf_words_kernel<<<grid_for(nblk, kThreads), kThreads, 0, as_stream(stream)>>>(
+  AES_LAUNCH(prf_words_kernel, grid_for(nblk, kThreads), as_stream(stream), 
       rk, stream_head(purpose, index), word_off, count, words);
   return check_launch("prf_words");
 }
@@ -246,7 +441,7 @@ int mpc3_rss_zero_share(const uint32_t* rk3, const uint64_t* ctr, uint32_t purpo
   int st = check_stream_args(purpose, index);
   if (st) return st;
   if (n == 0) return MPC3_OK;
-  zero_share_kernel<<<grid_for((n + 1) / 2, kThreads), kThreads, 0, as_stream(stream)>>>(
+  AES_LAUNCH(zero_share_kernel, grid_for((n + 1) / 2, kThreads), as_stream(stream), 
       rk3, ctr, sref(purpose, index), xor_mode, n, out);
   return check_launch("zero_share");
 }
@@ -280,7 +475,7 @@ static int arith_launch(int kind, const uint32_t* rk3, const uint64_t* ctr, uint
   if (ja >= (1ull << 48) || jrho >= (1ull << 48) || jr >= (1ull << 48)) return MPC3_ERR_RANGE;
   if (elem_off & 1) return MPC3_ERR_CONFIG;
   if (n == 0) return MPC3_OK;
-  arith_kernel<<<grid_for((n + 1) / 2, kThreads), kThreads, 0, as_stream(stream)>>>(
+  AES_LAUNCH(arith_kernel, grid_for((n + 1) / 2, kThreads), as_stream(stream), 
       kind, rk3, ctr, sref(ARITH_ZERO, ja), sref(TRUNC_RHO, jrho), sref(TRUNC_R, jr), bits, x, y, out, n,
       elem_off >> 1);
   return check_launch("rss_arith");
@@ -302,6 +497,38 @@ int mpc3_rss_mul_truncate(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_a
   return arith_launch(2, rk3, ctr, j_arith, j_rho, j_r, bits, x, y, out, n, elem_off, stream);
 }
 
+int mpc3_rss_chain(const uint32_t* rk3, const uint64_t* ctr, const MPC3ChainStep* steps, int nsteps, uint64_t j_arith,
+                   uint64_t j_rho, uint64_t j_r, const uint64_t* x, uint64_t* out, uint64_t n, uint64_t elem_off,
+                   void* stream) {
+  if (!steps || nsteps < 0 || nsteps > MPC3_CHAIN_MAX_STEPS) return MPC3_ERR_CONFIG;
+  if (elem_off & 1) return MPC3_ERR_CONFIG;
+  ChainProgram prog;
+  prog.nsteps = nsteps;
+  prog.nmul = 0;
+  for (int i = 0; i < nsteps; ++i) {
+    prog.s[i] = steps[i];
+    const int op = steps[i].op;
+    if (op < MPC3_CHAIN_ADDC || op > MPC3_CHAIN_SQT) return MPC3_ERR_CONFIG;
+    if (op == MPC3_CHAIN_SQ || op == MPC3_CHAIN_MULX || op == MPC3_CHAIN_SQT) {
+      if (steps[i].bits < 1 || steps[i].bits > 61) return MPC3_ERR_RANGE;  // protocols.py:185-186
+      ++prog.nmul;
+    }
+  }
+  if (j_arith + prog.nmul >= (1ull << 48) || j_rho + prog.nmul >= (1ull << 48) || j_r + prog.nmul >= (1ull << 48))
+    return MPC3_ERR_RANGE;
+  if (n == 0) return MPC3_OK;
+  int P = 64;
+  while (P > 8 && P * prog.nmul * CH_SLOT_WORDS * (int)sizeof(Word2) > 96 * 1024) P >>= 1;
+  if (P * (prog.nmul > 0 ? prog.nmul : 1) * CH_SLOT_WORDS * (int)sizeof(Word2) > 96 * 1024) return MPC3_ERR_CONFIG;
+  const int smem = kAesSmemBytes + P * prog.nmul * CH_SLOT_WORDS * (int)sizeof(Word2);
+  if (!aes_attr((const void*)chain_kernel, kAesSmemBytes + 96 * 1024)) return check_launch("chain smem attribute");
+  uint64_t chunks = ((n + 1) / 2 + P - 1) / P;
+  unsigned grid = (unsigned)(chunks < 148 * 8 ? chunks : 148 * 8);
+  chain_kernel<<<grid, kThreads, smem, as_stream(stream)>>>(rk3, ctr, prog, j_arith, j_rho, j_r, x, out, n,
+                                                            elem_off >> 1, P);
+  return check_launch("rss_chain");
+}
+
 int mpc3_rss_sign(const uint32_t* rk3, const uint64_t* ctr, int mode, uint64_t j_bin, uint64_t j_xor, uint64_t j_arith,
                   const uint64_t* x, uint64_t* out, uint64_t* mask, uint64_t n, uint64_t n_total,
                   uint64_t elem_off, void* stream) {
@@ -315,7 +542,23 @@ int mpc3_rss_sign(const uint32_t* rk3, const uint64_t* ctr, int mode, uint64_t j
   a.jbin = j_bin;
   a.jxor = j_xor;
   a.ja = j_arith;
-  sign_kernel<<<grid_for((n + 1) / 2, kThreads, 16), kThreads, 0, as_stream(stream)>>>(
+  // large tensors: the single-phase kernel (throughput-bound, all threads in
+  // the circuit); small ones: the two-phase kernel (latency-bound launches)
+  if (!g_sign_fused && (n + 1) / 2 <= kSign2MaxPairs) {
+    // two-phase kernel: P pairs per chunk (64; 32 when the p-half straddles
+    // blocks), tables + keystream slots in dynamic shared memory
+    const bool straddle = (n_total & 1) != 0;
+    const int P = straddle ? 32 : 64;
+    const int smem = kAesSmemBytes + P * sign_slots(straddle) * SW_SLOT_BYTES;
+    if (!aes_attr((const void*)sign2_kernel, kAesSmemBytes + 64 * sign_slots(false) * SW_SLOT_BYTES))
+      return check_launch("sign2 smem attribute");
+    uint64_t chunks = ((n + 1) / 2 + P - 1) / P;
+    unsigned grid = (unsigned)(chunks < 148 * 2 * 8 ? chunks : 148 * 2 * 8);
+    sign2_kernel<<<grid, kThreads, smem, as_stream(stream)>>>(rk3, ctr, a, mode, x, out, mask, n, n_total, elem_off,
+                                                             P);
+    return check_launch("rss_sign2");
+  }
+  AES_LAUNCH(sign_kernel, grid_for((n + 1) / 2, kThreads, 16), as_stream(stream), 
       rk3, ctr, a, mode, x, out, mask, n, n_total, elem_off);
   return check_launch("rss_sign");
 }
@@ -324,7 +567,7 @@ int mpc3_rss_bit_inject(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_ari
                         uint64_t n, void* stream) {
   if (j_arith + 1 >= (1ull << 48)) return MPC3_ERR_RANGE;
   if (n == 0) return MPC3_OK;
-  inject_kernel<<<grid_for((n + 1) / 2, kThreads), kThreads, 0, as_stream(stream)>>>(
+  AES_LAUNCH(inject_kernel, grid_for((n + 1) / 2, kThreads), as_stream(stream), 
       rk3, ctr, sref(ARITH_ZERO, j_arith), sref(ARITH_ZERO, j_arith + 1), bits, out, n);
   return check_launch("rss_bit_inject");
 }
@@ -348,7 +591,7 @@ int mpc3_rss_reshare_truncate(const uint32_t* rk3, const uint64_t* ctr, uint64_t
   v.zp = view->z_plane;
   v.op = view->out_plane;
   if (n == 0) return MPC3_OK;
-  reshare_trunc_kernel<<<grid_for((n + 1) / 2, kThreads), kThreads, 0, as_stream(stream)>>>(
+  AES_LAUNCH(reshare_trunc_kernel, grid_for((n + 1) / 2, kThreads), as_stream(stream), 
       rk3, ctr, sref(ARITH_ZERO, j_arith), sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, z, v, out, n,
       elem_off >> 1);
   return check_launch("rss_reshare_truncate");
@@ -372,7 +615,7 @@ int mpc3_rss_avgpool(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_rho, u
   int64_t OH = (H + 2 * ph - kh) / sh + 1, OW = (W + 2 * pw - kw) / sw + 1;
   uint64_t n = (uint64_t)N * C * OH * OW;
   if (n == 0) return MPC3_OK;
-  pool_kernel<<<grid_for((n + 1) / 2, kThreads), kThreads, 0, as_stream(stream)>>>(
+  AES_LAUNCH(pool_kernel, grid_for((n + 1) / 2, kThreads), as_stream(stream), 
       rk3, ctr, 0, sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, mulc, x, out,
       pool_geom(N, C, H, W, OH, OW, kh, kw, sh, sw, ph, pw), n, elem_off >> 1);
   return check_launch("rss_avgpool");
@@ -387,7 +630,7 @@ int mpc3_rss_avgpool_backward(const uint32_t* rk3, const uint64_t* ctr, uint64_t
   if (kh < 1 || kw < 1 || sh < 1 || sw < 1 || ph < 0 || pw < 0) return MPC3_ERR_SHAPE;
   uint64_t n = (uint64_t)N * C * H * W;
   if (n == 0) return MPC3_OK;
-  pool_kernel<<<grid_for((n + 1) / 2, kThreads), kThreads, 0, as_stream(stream)>>>(
+  AES_LAUNCH(pool_kernel, grid_for((n + 1) / 2, kThreads), as_stream(stream), 
       rk3, ctr, 1, sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, mulc, g, out,
       pool_geom(N, C, H, W, OH, OW, kh, kw, sh, sw, ph, pw), n, elem_off >> 1);
   return check_launch("rss_avgpool_backward");
@@ -407,7 +650,7 @@ int mpc3_rss_col2im_reshare_truncate(const uint32_t* rk3, const uint64_t* ctr, u
   g.wf = (OW - 1) * sw + kw;
   uint64_t n = (uint64_t)N * C * g.hf * g.wf;
   if (n == 0) return MPC3_OK;
-  col2im_kernel<<<grid_for((n + 1) / 2, kThreads), kThreads, 0, as_stream(stream)>>>(
+  AES_LAUNCH(col2im_kernel, grid_for((n + 1) / 2, kThreads), as_stream(stream), 
       rk3, ctr, sref(ARITH_ZERO, j_arith), sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, z, g, out, n,
       elem_off >> 1);
   return check_launch("rss_col2im_reshare_truncate");

@@ -40,6 +40,133 @@ __global__ void pack_kernel(const uint64_t* __restrict__ src, int64_t plane, Ope
     pack_item(src, plane, o, role, out, kp, t);
 }
 
+// Tiled operand packing.  One CTA packs a PT_R x PT_K tile of the packed
+// operand (rows x packed columns kk of [first half | second half], 2K long for
+// the cross-term roles).  The gather offset of v(r, k) splits into a row part
+// and a column part (dense: off + r s_r + sum k_i t_i; im2col: n sN + c sC +
+// (y sh - ph + u) sH + (x sw - pw + v) sW with bounds; wgrad: the same with the
+// roles of (n, y, x) and (c, u, v) swapped), computed once per tile row and
+// column into shared memory, so an element costs two adds, two multiply-adds
+// and two loads.  Phase 1 walks the tile in the source's contiguous direction
+// (rows for im2col and row-strided dense views, columns otherwise) so the
+// loads coalesce; phase 2 reads 8 consecutive packed values of one row back
+// from shared memory, byte-transposes them (PRMT) and writes one 8-byte word
+// per limb plane, consecutive threads covering consecutive columns.
+constexpr int PT_R = 64, PT_K = 64, PT_THREADS = 256;
+
+struct PackTileArgs {
+  int64_t rows, K, kp, lim;  // lim: packed columns with data (K or 2K)
+  int64_t H, W, sH, sW;      // bounds / strides of the (y, x) part (dense: no bounds, 0 strides)
+  int r_fast;                // phase-1 thread order: 1 = along rows, 0 = along columns
+};
+
+__global__ void __launch_bounds__(PT_THREADS) pack_tile_kernel(const uint64_t* __restrict__ src, int64_t plane,
+                                                               Operand o, int role, PackTileArgs a,
+                                                               uint8_t* __restrict__ out) {
+  __shared__ uint64_t tile[PT_R][PT_K + 1];
+  __shared__ int64_t rb[PT_R], kb[PT_K];
+  __shared__ int32_t ry[PT_R], rx[PT_R], ky[PT_K], kx[PT_K], khalf[PT_K];
+  const int g = blockIdx.z;
+  const int64_t r0 = (int64_t)blockIdx.y * PT_R, c0 = (int64_t)blockIdx.x * PT_K;
+  const int t = threadIdx.x;
+  if (t < PT_R) {
+    int64_t r = r0 + t;
+    int64_t b = 0;
+    int32_t y = 0, x = 0;
+    if (r < a.rows) {
+      if (o.mode == MPC3_GATHER_DENSE) {
+        b = o.off + r * o.s_r;
+      } else if (o.mode == MPC3_GATHER_IM2COL) {  // r = (n, y, x)
+        int64_t xx = r % o.ow, q = r / o.ow;
+        int64_t yy = q % o.oh, n = q / o.oh;
+        b = n * o.sN;
+        y = (int32_t)(yy * o.sh - o.ph);
+        x = (int32_t)(xx * o.sw - o.pw);
+      } else {  // WGRAD: r = (c, u, v)
+        int64_t v = r % o.kw, q = r / o.kw;
+        int64_t u = q % o.kh, c = q / o.kh;
+        b = c * o.sC;
+        y = (int32_t)(u - o.ph);
+        x = (int32_t)(v - o.pw);
+      }
+    }
+    rb[t] = b;
+    ry[t] = y;
+    rx[t] = x;
+  } else if (t < PT_R + PT_K) {
+    const int j = t - PT_R;
+    int64_t kk = c0 + j;
+    int half = -1;  // -1: zero padding
+    int64_t k = 0;
+    if (kk < a.lim) {
+      half = kk >= a.K ? 1 : 0;
+      k = kk - half * a.K;
+    }
+    int64_t b = 0;
+    int32_t y = 0, x = 0;
+    if (half >= 0) {
+      if (o.mode == MPC3_GATHER_DENSE) {
+        int64_t k2 = k % o.K2, q = k / o.K2;
+        b = (q / o.K1) * o.t0 + (q % o.K1) * o.t1 + k2 * o.t2;
+      } else if (o.mode == MPC3_GATHER_IM2COL) {  // k = (c, u, v)
+        int64_t v = k % o.kw, q = k / o.kw;
+        int64_t u = q % o.kh, c = q / o.kh;
+        b = c * o.sC;
+        y = (int32_t)u;
+        x = (int32_t)v;
+      } else {  // WGRAD: k = (n, y, x)
+        int64_t xx = k % o.ow, q = k / o.ow;
+        int64_t yy = q % o.oh, n = q / o.oh;
+        b = n * o.sN;
+        y = (int32_t)(yy * o.sh);
+        x = (int32_t)(xx * o.sw);
+      }
+    }
+    kb[j] = b;
+    ky[j] = y;
+    kx[j] = x;
+    khalf[j] = half;
+  }
+  __syncthreads();
+  // phase 1: gather the packed values of the tile
+  const uint64_t* sg = src + (int64_t)g * plane;
+  const uint64_t* sn = src + (int64_t)((g + 1) % 3) * plane;
+#pragma unroll 4
+  for (int e = t; e < PT_R * PT_K; e += PT_THREADS) {
+    const int i = a.r_fast ? (e % PT_R) : (e / PT_K);
+    const int j = a.r_fast ? (e / PT_R) : (e % PT_K);
+    uint64_t v = 0;
+    const int half = khalf[j];
+    if (half >= 0 && r0 + i < a.rows) {
+      const int32_t yy = ry[i] + ky[j], xx = rx[i] + kx[j];
+      if (yy >= 0 && xx >= 0 && yy < a.H && xx < a.W) {
+        const int64_t off = rb[i] + kb[j] + (int64_t)yy * a.sH + (int64_t)xx * a.sW;
+        if (role == 2) {
+          v = __ldg(src + off);
+        } else {
+          const uint64_t self = __ldg(sg + off), nxt = __ldg(sn + off);
+          v = role == 0 ? (half == 0 ? self + nxt : self) : (half == 0 ? self : nxt);  // protocols.py:110-115
+        }
+      }
+    }
+    tile[i][j] = v;
+  }
+  __syncthreads();
+  // phase 2: 8 consecutive columns of one row -> one u64 per limb plane
+  for (int e = t; e < PT_R * (PT_K / 8); e += PT_THREADS) {
+    const int i = e / (PT_K / 8), ch = e % (PT_K / 8);
+    const int64_t r = r0 + i, kk = c0 + ch * 8;
+    if (r >= a.rows || kk >= a.kp) continue;
+    uint64_t v[8], w[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = tile[i][ch * 8 + q];
+    byte_transpose8(v, w);
+    uint8_t* base = out + ((int64_t)g * 8 * a.rows + r) * a.kp + kk;
+#pragma unroll
+    for (int l = 0; l < 8; ++l) *reinterpret_cast<uint64_t*>(base + (int64_t)l * a.rows * a.kp) = w[l];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // SIMT reference kernel (64-bit IMAD on CUDA cores)
 
@@ -564,6 +691,30 @@ int mpc3_ring_pack(const uint64_t* src, int64_t src_plane, const mpc3_operand* o
   int groups = role == 2 ? 1 : 3;
   int64_t total = (int64_t)groups * o.rows * (kp / 8);
   if (total == 0) return MPC3_OK;
+  const bool dilated = o.mode == MPC3_GATHER_IM2COL && (o.dh != 1 || o.dw != 1);
+  const int64_t row_tiles = (o.rows + PT_R - 1) / PT_R;
+  if (!dilated && row_tiles < 65536 && o.h < (1 << 30) && o.w < (1 << 30)) {
+    PackTileArgs a;
+    a.rows = o.rows;
+    a.K = o.k;
+    a.kp = kp;
+    a.lim = role == 2 ? o.k : 2 * o.k;
+    if (o.mode == MPC3_GATHER_DENSE) {
+      a.H = a.W = 1;
+      a.sH = a.sW = 0;
+      int64_t sk = o.K2 > 1 || o.K1 == 1 ? o.t2 : o.t1;  // stride of the fastest k digit
+      a.r_fast = (o.s_r < 0 ? -o.s_r : o.s_r) < (sk < 0 ? -sk : sk) ? 1 : 0;
+    } else {
+      a.H = o.h;
+      a.W = o.w;
+      a.sH = o.sH;
+      a.sW = o.sW;
+      a.r_fast = o.mode == MPC3_GATHER_IM2COL ? 1 : 0;
+    }
+    dim3 grid((unsigned)((kp + PT_K - 1) / PT_K), (unsigned)row_tiles, (unsigned)groups);
+    pack_tile_kernel<<<grid, PT_THREADS, 0, as_stream(stream)>>>(src, src_plane, o, role, a, out);
+    return check_launch("ring_pack_tile");
+  }
   pack_kernel<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(src, src_plane, o, role, groups, out, kp);
   return check_launch("ring_pack");
 }

@@ -125,6 +125,26 @@ HD void prf_block3(const SmemTables& tab, const uint32_t* rk3, StreamHead h, uin
 }
 #endif
 
+#if defined(__CUDACC__)
+// Keystream replay: a circuit templated on the table type runs unchanged on
+// words an earlier phase computed into shared memory, one slot per AES call
+// in call order (slot s of pair p at w[(s * P + p) * 3 + key]).
+struct Replay {
+  const Word2* w;
+  int P, p;
+  mutable int slot;
+};
+DEV Word2 prf_block(const Replay& t, const uint32_t*, StreamHead, uint64_t) {
+  return t.w[((size_t)t.slot++ * t.P + t.p) * 3];
+}
+DEV void prf_block3(const Replay& t, const uint32_t*, StreamHead, uint64_t, Word2 w[3]) {
+  const Word2* s = t.w + ((size_t)t.slot++ * t.P + t.p) * 3;
+  w[0] = s[0];
+  w[1] = s[1];
+  w[2] = s[2];
+}
+#endif
+
 // Key-word provider over a pair of adjacent elements (words 2b, 2b+1 of each
 // stream share one AES block per key).
 template <class T>
@@ -212,6 +232,24 @@ HD void fold_words(const T& tab, const uint32_t* rk3, StreamHead h, uint64_t w, 
   for (int k = 0; k < 3; ++k) fold_word(z[1], k, a[k].w0, xor_mode);
 }
 
+// Fold the three keys' words of one AES block into a pair's local products:
+// sel 0 = aligned (element 0 <- word 2b, element 1 <- word 2b+1), 1 = element
+// 0 <- word 2b+1 only, 2 = element 1 <- word 2b only (a pair straddling two
+// blocks, the Kogge-Stone p-half at an odd n_total).
+HD void fold_sel(Trio z[2], const Word2 w[3], int sel, bool xor_mode) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (sel == 0) {
+      fold_word(z[0], k, w[k].w0, xor_mode);
+      fold_word(z[1], k, w[k].w1, xor_mode);
+    } else if (sel == 1) {
+      fold_word(z[0], k, w[k].w1, xor_mode);
+    } else {
+      fold_word(z[1], k, w[k].w0, xor_mode);
+    }
+  }
+}
+
 // The fused sign circuit for the element pair (2*blk, 2*blk+1) of a tensor of
 // n_total elements (n_total sets where the Kogge-Stone p-half lives, word
 // n_total + e, protocols.py:247-259).  x is read through `ld` (local element
@@ -222,40 +260,59 @@ HD void fold_words(const T& tab, const uint32_t* rk3, StreamHead h, uint64_t w, 
 // AES blocks per element pair: BIN 1, XOR 3 + 6*(3 + 3) - 3 (the last
 // level's p-half is dead: p is never read after the loop, protocols.py:259-263),
 // ARITH 3 per mul.
+//
+// Code shape: the 12 Kogge-Stone AND rounds are one loop of "jobs" (job 0 =
+// g = a AND b; odd job 2l-1 = level l's g-half; even job 2l = level l's
+// p-half) around ONE three-key AES call site, and the three arithmetic
+// multiplications (2 x bit_inject, the ReLU mask) a second loop around another:
+// the kernel stays small enough for the instruction cache (the fully inlined
+// circuit was 5,192 instructions and stalled on instruction fetch).
 template <class T, class Ld>
 HD void sign_circuit_pair(const T& tab, const uint32_t* rk3, const SignStreams& st, uint64_t n_total,
                           uint64_t blk, int mode, const Ld& ld, Trio out[2], Trio mask[2]) {
   // a2b input sharing (protocols.py:278-295): w = ((c0+c1)^r, r, 0), x2 = (0,0,c2)
   const Word2 rb = prf_block(tab, rk3 + 0 * 44, st.bin, blk);
   Trio p[2], g[2];
-  for (int e = 0; e < 2; ++e) {
-    Trio x = ld(e);
-    uint64_t r = e ? rb.w1 : rb.w0;
-    Trio a = {{(x.c[0] + x.c[1]) ^ r, r, 0}};
-    Trio b = {{0, 0, x.c[2]}};
-    p[e] = trio_xor(a, b);
-    g[e] = and_local(a, b);
-  }
-  fold_pair(tab, rk3, st.x[0], blk, g, true);
-  g[0] = relabel(g[0]);
-  g[1] = relabel(g[1]);
+  const uint64_t pw = n_total + 2 * blk;  // stream word of element 0's p-half
 #if defined(__CUDA_ARCH__)
 #pragma unroll 1
 #endif
-  for (int lvl = 1; lvl <= 6; ++lvl) {
-    const int d = 1 << (lvl - 1);
+  for (int job = 0; job < 12; ++job) {
+    const int lvl = (job + 1) >> 1;  // 0, 1, 1, 2, 2, ..., 6
+    const int d = lvl > 0 ? 1 << (lvl - 1) : 0;
+    const bool phalf = job > 0 && (job & 1) == 0;
     Trio t[2];
-    t[0] = and_local(p[0], trio_shl(g[0], d));
-    t[1] = and_local(p[1], trio_shl(g[1], d));
-    fold_pair(tab, rk3, st.x[lvl], blk, t, true);
-    g[0] = trio_xor(g[0], relabel(t[0]));
-    g[1] = trio_xor(g[1], relabel(t[1]));
-    if (lvl < 6) {
-      t[0] = and_local(p[0], trio_shl(p[0], d));
-      t[1] = and_local(p[1], trio_shl(p[1], d));
-      fold_words(tab, rk3, st.x[lvl], n_total + 2 * blk, t, true);
-      p[0] = relabel(t[0]);
-      p[1] = relabel(t[1]);
+    if (job == 0) {
+      for (int e = 0; e < 2; ++e) {
+        Trio x = ld(e);
+        uint64_t r = e ? rb.w1 : rb.w0;
+        Trio a = {{(x.c[0] + x.c[1]) ^ r, r, 0}};
+        Trio b = {{0, 0, x.c[2]}};
+        p[e] = trio_xor(a, b);
+        t[e] = and_local(a, b);
+      }
+    } else {
+      for (int e = 0; e < 2; ++e) t[e] = and_local(p[e], trio_shl(phalf ? p[e] : g[e], d));
+    }
+    const StreamHead h = st.x[lvl];
+    const bool straddle = phalf && (pw & 1);
+    const uint64_t b0 = phalf ? (pw >> 1) : blk;
+#if defined(__CUDA_ARCH__)
+#pragma unroll 1
+#endif
+    for (int sub = 0; sub < (straddle ? 2 : 1); ++sub) {
+      Word2 w[3];
+      prf_block3(tab, rk3, h, b0 + sub, w);
+      fold_sel(t, w, straddle ? 1 + sub : 0, true);
+    }
+    for (int e = 0; e < 2; ++e) {
+      Trio r = relabel(t[e]);
+      if (job == 0)
+        g[e] = r;
+      else if (phalf)
+        p[e] = r;
+      else
+        g[e] = trio_xor(g[e], r);
     }
   }
   Trio s[2];
@@ -278,38 +335,49 @@ HD void sign_circuit_pair(const T& tab, const uint32_t* rk3, const SignStreams& 
     out[1] = bit[1];
     return;
   }
-  // bit_inject (protocols.py:304-331): u = s0 + s1 - 2 mul(s0, s1); v = u + s2 - 2 mul(u, s2)
+  // bit_inject (protocols.py:304-331): u = s0 + s1 - 2 mul(s0, s1); v = u + s2 - 2 mul(u, s2);
+  // drelu = 1 - v (protocols.py:57-66, 334-337); relu = mul(x, drelu) (protocols.py:340-348)
+  const int nmul = mode == MODE_DRELU ? 2 : 3;
   Trio u[2], m[2];
-  for (int e = 0; e < 2; ++e) {
-    Trio t0 = {{bit[e].c[0], 0, 0}}, t1 = {{0, bit[e].c[1], 0}};
-    u[e] = mul_local(t0, t1);
-  }
-  fold_pair(tab, rk3, st.a[0], blk, u, false);
-  for (int e = 0; e < 2; ++e) {
-    Trio pr = relabel(u[e]);
-    Trio t0 = {{bit[e].c[0], 0, 0}}, t1 = {{0, bit[e].c[1], 0}};
-    for (int i = 0; i < 3; ++i) u[e].c[i] = t0.c[i] + t1.c[i] - 2 * pr.c[i];
-    Trio t2 = {{0, 0, bit[e].c[2]}};
-    m[e] = mul_local(u[e], t2);
-  }
-  fold_pair(tab, rk3, st.a[1], blk, m, false);
-  for (int e = 0; e < 2; ++e) {
-    Trio pv = relabel(m[e]);
-    // drelu = 1 - v: negate, constant into component 0 (protocols.py:57-66, 334-337)
-    m[e].c[0] = 1 - (u[e].c[0] - 2 * pv.c[0]);
-    m[e].c[1] = 0 - (u[e].c[1] - 2 * pv.c[1]);
-    m[e].c[2] = 0 - (u[e].c[2] + bit[e].c[2] - 2 * pv.c[2]);
+#if defined(__CUDA_ARCH__)
+#pragma unroll 1
+#endif
+  for (int k = 0; k < nmul; ++k) {
+    Trio t[2];
+    for (int e = 0; e < 2; ++e) {
+      if (k == 0) {
+        Trio t0 = {{bit[e].c[0], 0, 0}}, t1 = {{0, bit[e].c[1], 0}};
+        t[e] = mul_local(t0, t1);
+      } else if (k == 1) {
+        Trio t2 = {{0, 0, bit[e].c[2]}};
+        t[e] = mul_local(u[e], t2);
+      } else {
+        t[e] = mul_local(ld(e), m[e]);
+      }
+    }
+    Word2 w[3];
+    prf_block3(tab, rk3, st.a[k], blk, w);
+    fold_sel(t, w, 0, false);
+    for (int e = 0; e < 2; ++e) {
+      Trio pr = relabel(t[e]);
+      if (k == 0) {
+        u[e].c[0] = bit[e].c[0] - 2 * pr.c[0];
+        u[e].c[1] = bit[e].c[1] - 2 * pr.c[1];
+        u[e].c[2] = 0 - 2 * pr.c[2];
+      } else if (k == 1) {
+        m[e].c[0] = 1 - (u[e].c[0] - 2 * pr.c[0]);
+        m[e].c[1] = 0 - (u[e].c[1] - 2 * pr.c[1]);
+        m[e].c[2] = 0 - (u[e].c[2] + bit[e].c[2] - 2 * pr.c[2]);
+      } else {
+        out[e] = pr;
+      }
+    }
   }
   if (mode == MODE_DRELU) {
     out[0] = m[0];
     out[1] = m[1];
     return;
   }
-  Trio z[2];
-  for (int e = 0; e < 2; ++e) z[e] = mul_local(ld(e), m[e]);
-  fold_pair(tab, rk3, st.a[2], blk, z, false);
-  out[0] = relabel(z[0]);
-  out[1] = relabel(z[1]);
   mask[0] = m[0];
   mask[1] = m[1];
 }

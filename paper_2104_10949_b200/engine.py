@@ -675,19 +675,37 @@ class TrioSession:
         s = cfg.squarings
         if self.fp.t + 2 * s > 61:
             raise ConfigError(f"m={cfg.m} too large for t={self.fp.t}")
-        y = self.add_const(x, fx_encode(float(cfg.m), self.fp))
-        y = self.mul_truncate(y, y, self.fp.t + 2 * s)
-        for _ in range(s - 1):
-            y = self.mul_truncate(y, y)
-        return y
+        steps = [(K.CHAIN_ADDC, 0, int(fx_encode(float(cfg.m), self.fp)))]
+        steps += [(K.CHAIN_SQ, self.fp.t + 2 * s if i == 0 else self.fp.t, 0) for i in range(s)]
+        return self._chain(x, steps)
 
     def reciprocal(self, y: RssTensor, cfg: ReciprocalConfig = ReciprocalConfig()) -> RssTensor:
-        z = self.const_share(fx_encode(1.0 / cfg.Y, self.fp), y.shape)
+        steps = [(K.CHAIN_SETC, 0, int(fx_encode(1.0 / cfg.Y, self.fp)))]
         for _ in range(cfg.iterations):
-            z2 = self.mul_truncate(z, z)
-            yz2 = self.mul_truncate(y, z2)
-            z = self.sub(self.mul_const(z, 2), yz2)
-        return z
+            steps += [(K.CHAIN_SQT, self.fp.t, 0), (K.CHAIN_MULX, self.fp.t, 0), (K.CHAIN_NEWTON, 0, 0)]
+        return self._chain(y, steps)
+
+    def _chain(self, x: RssTensor, steps) -> RssTensor:
+        """One launch for a chain of local ops and mul+truncates on the same
+        elements (mpc3_rss_chain); counters, accounting and results are those
+        of the unfused sequence of mul_truncate calls."""
+        muls = (K.CHAIN_SQ, K.CHAIN_MULX, K.CHAIN_SQT)
+        nmul = sum(1 for op, _, _ in steps if op in muls)
+        if len(steps) > K.CHAIN_MAX_STEPS:
+            raise ConfigError(f"chain of {len(steps)} steps exceeds {K.CHAIN_MAX_STEPS}")
+        for op, bits, _ in steps:
+            if op in muls and not 1 <= bits <= 61:
+                raise RangeError(f"truncation by {bits} bits outside [1, 61]")
+        x = x.contiguous()
+        out = empty(x.shape, x.fp)
+        ja, jr, jq = self.take(ARITH, nmul), self.take(TR_RHO, nmul), self.take(TR_R, nmul)
+        prog, count = K.chain_program(steps)
+        K.call("mpc3_rss_chain", self.rk, self.ctr_ptr, prog, count, ja, jr, jq, x.data.data_ptr(),
+               out.data.data_ptr(), x.numel, self.shard_offset(x.numel)[0], _stream())
+        for _ in range(nmul):
+            self.ledger.ring("mul.reshare", x.numel)
+            self._charge_trunc(x.numel)
+        return out
 
     def division(self, x, y, cfg: ReciprocalConfig = ReciprocalConfig()):
         return self.mul_truncate(x, self.reciprocal(y, cfg))

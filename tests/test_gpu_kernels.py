@@ -119,6 +119,30 @@ def test_sign_modes(n):
     assert np.array_equal(host(mask).reshape(3, n), rm)
 
 
+@pytest.mark.parametrize("n", [600000, 600001])
+def test_sign_single_phase_equals_two_phase_shards(n):
+    """Large tensors run the single-phase sign kernel, small ones the two-phase
+    (keystream-then-circuit) kernel: the full call and its batch shards
+    (elem_off / n_total, 3 shards below the crossover) agree share for share,
+    odd n_total included (Kogge-Stone p-half straddling AES blocks)."""
+    rng = np.random.default_rng(n)
+    xs = rng.integers(0, 1 << 64, size=(3, n), dtype=U64)
+    rk = rk3(R.Session(4).keys)
+    xd = dev(xs)
+    full, fmask = torch.empty(3 * n, dtype=torch.int64, device="cuda"), torch.empty(3 * n, dtype=torch.int64,
+                                                                                   device="cuda")
+    _capi.call("mpc3_rss_sign", p(rk), None, 3, 2, 5, 7, p(xd), p(full), p(fmask), n, n, 0, stream())
+    bounds = [0, 200000, 400000, n]
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        m = b - a
+        xsh = dev(np.ascontiguousarray(xs[:, a:b]))
+        o, mk = torch.empty(3 * m, dtype=torch.int64, device="cuda"), torch.empty(3 * m, dtype=torch.int64,
+                                                                                   device="cuda")
+        _capi.call("mpc3_rss_sign", p(rk), None, 3, 2, 5, 7, p(xsh), p(o), p(mk), m, n, a, stream())
+        assert np.array_equal(host(o).reshape(3, m), host(full).reshape(3, n)[:, a:b])
+        assert np.array_equal(host(mk).reshape(3, m), host(fmask).reshape(3, n)[:, a:b])
+
+
 def _gemm_packed(A, B, groups, M, Nn, kp, splits):
     Cm = torch.zeros(groups * M * Nn, dtype=torch.int64, device="cuda")
     _capi.call("mpc3_ring_gemm_packed", p(A), p(B), p(Cm), groups, M, Nn, kp, Nn, M * Nn, splits, stream())
