@@ -52,20 +52,27 @@ __global__ void pack_kernel(const uint64_t* __restrict__ src, int64_t plane, Ope
 // loads coalesce; phase 2 reads 8 consecutive packed values of one row back
 // from shared memory, byte-transposes them (PRMT) and writes one 8-byte word
 // per limb plane, consecutive threads covering consecutive columns.
-constexpr int PT_R = 64, PT_K = 64, PT_THREADS = 256;
+constexpr int PT_R = 64, PT_K = 64, PT_THREADS = 512;
 
 struct PackTileArgs {
   int64_t rows, K, kp, lim;  // lim: packed columns with data (K or 2K)
-  int64_t H, W, sH, sW;      // bounds / strides of the (y, x) part (dense: no bounds, 0 strides)
-  int r_fast;                // phase-1 thread order: 1 = along rows, 0 = along columns
+  int32_t H, W, sH, sW;      // bounds / strides of the (y, x) part (dense: no bounds, 0 strides)
 };
 
+// Conflict-free shared layout of the 64 x 64 u64 tile for the three access
+// patterns (phase 1 along rows, phase 1 along columns, phase 2 eight
+// consecutive columns of 4 rows per warp), found by exhaustive search:
+// within each 8-column chunk rotate by chunk + row, then XOR the chunk with
+// row bits 3-5.
+DEV int pt_swz(int i, int j) { return ((j & ~7) + (((j & 7) + (j >> 3) + (i & 7)) & 7)) ^ (((i >> 3) & 7) << 3); }
+
+template <bool R_FAST>
 __global__ void __launch_bounds__(PT_THREADS) pack_tile_kernel(const uint64_t* __restrict__ src, int64_t plane,
                                                                Operand o, int role, PackTileArgs a,
                                                                uint8_t* __restrict__ out) {
-  __shared__ uint64_t tile[PT_R][PT_K + 1];
-  __shared__ int64_t rb[PT_R], kb[PT_K];
-  __shared__ int32_t ry[PT_R], rx[PT_R], ky[PT_K], kx[PT_K], khalf[PT_K];
+  __shared__ uint64_t tile[PT_R * PT_K];
+  __shared__ int32_t rb[PT_R], ry[PT_R], rx[PT_R];
+  __shared__ int32_t kb[PT_K], ky[PT_K], kx[PT_K], khalf[PT_K];
   const int g = blockIdx.z;
   const int64_t r0 = (int64_t)blockIdx.y * PT_R, c0 = (int64_t)blockIdx.x * PT_K;
   const int t = threadIdx.x;
@@ -89,8 +96,10 @@ __global__ void __launch_bounds__(PT_THREADS) pack_tile_kernel(const uint64_t* _
         y = (int32_t)(u - o.ph);
         x = (int32_t)(v - o.pw);
       }
+    } else {
+      y = -(1 << 30);  // rows past the end read nothing
     }
-    rb[t] = b;
+    rb[t] = (int32_t)b;
     ry[t] = y;
     rx[t] = x;
   } else if (t < PT_R + PT_K) {
@@ -122,44 +131,63 @@ __global__ void __launch_bounds__(PT_THREADS) pack_tile_kernel(const uint64_t* _
         x = (int32_t)(xx * o.sw);
       }
     }
-    kb[j] = b;
+    kb[j] = (int32_t)b;
     ky[j] = y;
     kx[j] = x;
     khalf[j] = half;
   }
   __syncthreads();
-  // phase 1: gather the packed values of the tile
+  // phase 1: gather the packed values of the tile.  Each thread keeps one
+  // row (R_FAST) or one column fixed in registers; a warp's 32 lanes walk
+  // the source's contiguous direction.
   const uint64_t* sg = src + (int64_t)g * plane;
   const uint64_t* sn = src + (int64_t)((g + 1) % 3) * plane;
-#pragma unroll 4
-  for (int e = t; e < PT_R * PT_K; e += PT_THREADS) {
-    const int i = a.r_fast ? (e % PT_R) : (e / PT_K);
-    const int j = a.r_fast ? (e / PT_R) : (e % PT_K);
+  const int fixed = R_FAST ? (t % PT_R) : (t % PT_K);
+  const int32_t fb = R_FAST ? rb[fixed] : kb[fixed];
+  const int32_t fy = R_FAST ? ry[fixed] : ky[fixed];
+  const int32_t fx = R_FAST ? rx[fixed] : kx[fixed];
+  const int fh = R_FAST ? 0 : khalf[fixed];
+  // all loads of the thread first (16 in flight), then combine and store
+  constexpr int PER = (PT_R * PT_K) / PT_THREADS;
+  uint64_t vs[PER], vn[PER];
+  int hv[PER];
+#pragma unroll
+  for (int it = 0; it < PER; ++it) {
+    const int var = t / (R_FAST ? PT_R : PT_K) + it * (PT_THREADS / (R_FAST ? PT_R : PT_K));
+    const int i = R_FAST ? fixed : var, j = R_FAST ? var : fixed;
+    const int half = R_FAST ? khalf[j] : fh;
+    const int32_t yy = fy + (R_FAST ? ky[j] : ry[i]), xx = fx + (R_FAST ? kx[j] : rx[i]);
+    const bool ok = half >= 0 && yy >= 0 && xx >= 0 && yy < a.H && xx < a.W;
+    const int32_t off = ok ? fb + (R_FAST ? kb[j] : rb[i]) + yy * a.sH + xx * a.sW : 0;
+    hv[it] = ok ? half : -1;
+    vs[it] = ok ? __ldg((role == 2 ? src : sg) + off) : 0;
+    vn[it] = (ok && role != 2) ? __ldg(sn + off) : 0;
+  }
+#pragma unroll
+  for (int it = 0; it < PER; ++it) {
+    const int var = t / (R_FAST ? PT_R : PT_K) + it * (PT_THREADS / (R_FAST ? PT_R : PT_K));
+    const int i = R_FAST ? fixed : var, j = R_FAST ? var : fixed;
     uint64_t v = 0;
-    const int half = khalf[j];
-    if (half >= 0 && r0 + i < a.rows) {
-      const int32_t yy = ry[i] + ky[j], xx = rx[i] + kx[j];
-      if (yy >= 0 && xx >= 0 && yy < a.H && xx < a.W) {
-        const int64_t off = rb[i] + kb[j] + (int64_t)yy * a.sH + (int64_t)xx * a.sW;
-        if (role == 2) {
-          v = __ldg(src + off);
-        } else {
-          const uint64_t self = __ldg(sg + off), nxt = __ldg(sn + off);
-          v = role == 0 ? (half == 0 ? self + nxt : self) : (half == 0 ? self : nxt);  // protocols.py:110-115
-        }
-      }
+    if (hv[it] >= 0) {
+      if (role == 2)
+        v = vs[it];
+      else if (role == 0)
+        v = hv[it] == 0 ? vs[it] + vn[it] : vs[it];  // [x_i + x_{i+1} | x_i]  (protocols.py:110-115)
+      else
+        v = hv[it] == 0 ? vs[it] : vn[it];  // [y_i | y_{i+1}]
     }
-    tile[i][j] = v;
+    tile[i * PT_K + pt_swz(i, j)] = v;
   }
   __syncthreads();
   // phase 2: 8 consecutive columns of one row -> one u64 per limb plane
+#pragma unroll 1
   for (int e = t; e < PT_R * (PT_K / 8); e += PT_THREADS) {
     const int i = e / (PT_K / 8), ch = e % (PT_K / 8);
     const int64_t r = r0 + i, kk = c0 + ch * 8;
     if (r >= a.rows || kk >= a.kp) continue;
     uint64_t v[8], w[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = tile[i][ch * 8 + q];
+    for (int q = 0; q < 8; ++q) v[q] = tile[i * PT_K + pt_swz(i, ch * 8 + q)];
     byte_transpose8(v, w);
     uint8_t* base = out + ((int64_t)g * 8 * a.rows + r) * a.kp + kk;
 #pragma unroll
@@ -693,26 +721,33 @@ int mpc3_ring_pack(const uint64_t* src, int64_t src_plane, const mpc3_operand* o
   if (total == 0) return MPC3_OK;
   const bool dilated = o.mode == MPC3_GATHER_IM2COL && (o.dh != 1 || o.dw != 1);
   const int64_t row_tiles = (o.rows + PT_R - 1) / PT_R;
-  if (!dilated && row_tiles < 65536 && o.h < (1 << 30) && o.w < (1 << 30)) {
+  // the tiled kernel addresses a component plane with 32-bit offsets
+  const bool small = src_plane < (1ll << 31) && o.h < (1 << 30) && o.w < (1 << 30) &&
+                     (o.mode != MPC3_GATHER_DENSE || (o.off >= 0 && o.s_r >= 0 && o.t0 >= 0 && o.t1 >= 0 && o.t2 >= 0));
+  if (!dilated && small && row_tiles < 65536) {
     PackTileArgs a;
     a.rows = o.rows;
     a.K = o.k;
     a.kp = kp;
     a.lim = role == 2 ? o.k : 2 * o.k;
+    bool r_fast;
     if (o.mode == MPC3_GATHER_DENSE) {
       a.H = a.W = 1;
       a.sH = a.sW = 0;
       int64_t sk = o.K2 > 1 || o.K1 == 1 ? o.t2 : o.t1;  // stride of the fastest k digit
-      a.r_fast = (o.s_r < 0 ? -o.s_r : o.s_r) < (sk < 0 ? -sk : sk) ? 1 : 0;
+      r_fast = o.s_r < sk;
     } else {
-      a.H = o.h;
-      a.W = o.w;
-      a.sH = o.sH;
-      a.sW = o.sW;
-      a.r_fast = o.mode == MPC3_GATHER_IM2COL ? 1 : 0;
+      a.H = (int32_t)o.h;
+      a.W = (int32_t)o.w;
+      a.sH = (int32_t)o.sH;
+      a.sW = (int32_t)o.sW;
+      r_fast = o.mode == MPC3_GATHER_IM2COL;
     }
     dim3 grid((unsigned)((kp + PT_K - 1) / PT_K), (unsigned)row_tiles, (unsigned)groups);
-    pack_tile_kernel<<<grid, PT_THREADS, 0, as_stream(stream)>>>(src, src_plane, o, role, a, out);
+    if (r_fast)
+      pack_tile_kernel<true><<<grid, PT_THREADS, 0, as_stream(stream)>>>(src, src_plane, o, role, a, out);
+    else
+      pack_tile_kernel<false><<<grid, PT_THREADS, 0, as_stream(stream)>>>(src, src_plane, o, role, a, out);
     return check_launch("ring_pack_tile");
   }
   pack_kernel<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(src, src_plane, o, role, groups, out, kp);

@@ -733,7 +733,7 @@ def gemm_splits(M: int, N: int, kp: int, groups: int) -> int:
     nkb = (kp + 31) // 32
     need = max(1, math.ceil(nkb * 32 / MAX_SPLIT_K))
     tiles = math.ceil(M / 128) * math.ceil(N / 64) * groups
-    occ = max(1, min(math.ceil(SMS / tiles), nkb // 8))
+    occ = max(1, min(SMS // tiles, nkb // 8))  # at most one wave of CTAs
     return max(need, occ)
 
 
