@@ -242,17 +242,25 @@ def run_b200(args, ws, rank, local):
         return orig_call(name, *a)
 
     # roofline instrumentation: CUDA events around every launch of the
-    # dominant kernel (the fused sign / ReLU kernel) on its launch stream
-    sign_events = []
-    instrument = {"on": False}
+    # dominant kernel (the tcgen05 ring GEMM) and of the fused sign circuit,
+    # on their launch stream (torch's current stream)
+    gemm_events, sign_events = [], []
+    instrument = {"on": False, "k": 0}
 
     def traced_call(name, *a):
-        if instrument["on"] and name == "mpc3_rss_sign":
+        if instrument["on"] and name == "mpc3_ring_pack" and a[3] == 0:
+            instrument["k"] = int(a[2]._obj.k)  # logical K of the cross-term operand (inner length 2K)
+        if instrument["on"] and name in ("mpc3_rss_sign", "mpc3_ring_gemm_packed"):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             counting_call(name, *a)
             e1.record()
-            sign_events.append((e0, e1, int(a[9])))
+            if name == "mpc3_rss_sign":
+                sign_events.append((e0, e1, int(a[9])))
+            else:  # groups x M x N x 2K ring MACs, 72 int8 ops each (36 limb-pair MACs)
+                groups, M, N = int(a[3]), int(a[4]), int(a[5])
+                sign_k = instrument["k"] if instrument["k"] else int(a[6]) // 2
+                gemm_events.append((e0, e1, 72 * groups * M * N * 2 * sign_k))
             return
         return counting_call(name, *a)
 
@@ -315,26 +323,41 @@ def run_b200(args, ws, rank, local):
         torch.distributed.barrier()
     value = b * args.steps * ws / (total_ms / 1e3)
 
-    # roofline of the dominant kernel: fused sign circuit (HBM 72 B/elem algorithmic)
-    sign_ms = sum(a.elapsed_time(c) for a, c, _ in sign_events)
-    sign_elems = sum(n for _, _, n in sign_events)
+    # roofline of the dominant kernel (largest share of the step): the
+    # tcgen05 ring GEMM, tensor-bound.  Algorithmic work per launch =
+    # 72 int8 ops (36 u8 x u8 limb-pair MACs) per ring MAC x groups * M * N * 2K.
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except OSError:
         pass
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    nlaunch = max(1, len(sign_events))
-    achieved = (72.0 * sign_elems / nlaunch) / (sign_ms / nlaunch / 1e3) / 1e9 if sign_ms else None
-    roofline = {"kernel": "mpc3_rss_sign (fused a2b + Kogge-Stone + bit_inject + ReLU, AES-CTR inline)",
-                "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": (achieved / hbm_peak) if achieved else None, "traffic": None,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650 GB/s",
-                "share_of_step": sign_ms / max(total_ms / args.steps, 1e-9),
-                "eager_step_ms": eager_ms,
-                "measured": "per-launch CUDA events in one eager step after the graph-timed region",
-                "aes_gblocks_s": 23 * sign_elems / (sign_ms / 1e3) / 1e9 if sign_ms else None,
-                "algorithmic_bytes_per_elem": 72}
+    gemm_ms = sum(a.elapsed_time(c) for a, c, _ in gemm_events)
+    gemm_ops = sum(w for _, _, w in gemm_events)
+    nl = max(1, len(gemm_events))
+    int8_peak = 2.0 * peaks.get("bf16_tflops", 2250.0 * 0.7225)  # dense int8 = 2x dense bf16 on B200
+    achieved = (gemm_ops / nl) / (gemm_ms / nl / 1e3) / 1e12 if gemm_ms else None
+    roofline = {"kernel": "gemm_tc_kernel (tcgen05.mma kind::i8, 8 TMEM diagonal accumulators, TMA SWIZZLE_32B)",
+                "bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TFLOP/s",
+                "frac": (achieved / int8_peak) if achieved else None,
+                "traffic": None,
+                "peak_source": ("2 x MEASURED_PEAKS.json bf16_tflops (dense int8 = 2x dense bf16 on B200; "
+                                "cuBLASLt int8 measured 2,924-3,063 TOPS, profiles/r01_microbench_quick.json)"),
+                "launches": len(gemm_events), "kernel_ms_per_step": gemm_ms,
+                "share_of_step": gemm_ms / max(total_ms / args.steps, 1e-9),
+                "algorithmic": "72 int8 ops per ring MAC x groups*M*N*2K per launch (TOPS; TFLOP/s column = int8 TOPS)",
+                "measured": "per-launch CUDA events on the launch stream in one eager step after the graph-timed region"}
+    # secondary bound: the nonlinear layers are AES-bound (23 AES-128 blocks
+    # per ReLU element); peak = the standalone AES-CTR keystream kernel's rate
+    sign_ms = sum(a.elapsed_time(c) for a, c, _ in sign_events)
+    sign_elems = sum(n for _, _, n in sign_events)
+    aes_peak = _aes_peak_gblocks()
+    aes_rate = 23 * sign_elems / (sign_ms / 1e3) / 1e9 if sign_ms else None
+    roofline["secondary"] = {"kernel": "sign circuit (a2b + Kogge-Stone + bit_inject + ReLU, AES-CTR inline)",
+                             "bound": "aes", "achieved": aes_rate, "peak": aes_peak, "unit": "G AES blocks/s",
+                             "frac": aes_rate / aes_peak if aes_rate and aes_peak else None,
+                             "share_of_step": sign_ms / max(total_ms / args.steps, 1e-9),
+                             "hbm_gbs": 72.0 * sign_elems / (sign_ms / 1e3) / 1e9 if sign_ms else None,
+                             "peak_source": "mpc3_prf_words AES-128-CTR keystream kernel, 2^27 blocks, this run"}
 
     # end-to-end through the public API with host inputs
     e2e = None
@@ -394,6 +417,11 @@ def run_b200(args, ws, rank, local):
     also = {}
     if not args.no_resnet:
         try:
+            also["lenet_b64"] = lenet_inference(dev)
+            also["vgg16_ti_b32"] = vgg16_ti(dev)
+        except Exception as e:  # noqa: BLE001 - reported, not fatal to the headline
+            also["side_error"] = repr(e)[:300]
+        try:
             also["resnet50_b64"] = resnet50_inference(dev, 64, 2, use_graph=False)
             also["resnet50_b1"] = resnet50_inference(dev, 1, 5, use_graph=True)
         except Exception as e:  # noqa: BLE001 - reported, not fatal to the headline
@@ -412,6 +440,93 @@ def run_b200(args, ws, rank, local):
         print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
+
+
+def _aes_peak_gblocks():
+    """Measured rate of the standalone AES-128-CTR keystream kernel (the
+    nonlinear protocols' roofline): 2^27 blocks, CUDA events, best of 3."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2104_10949_b200 import _capi
+
+    rk = np.zeros((3, 44), np.uint32)
+    for i in range(3):
+        _capi.check(_capi.lib().mpc3_aes128_expand(C.c_char_p(bytes([i]) * 16), rk[i].ctypes.data_as(C.c_void_p)))
+    rkd = torch.from_numpy(rk.view(np.int32)).cuda()
+    count = 1 << 28
+    out = torch.empty(count, dtype=torch.int64, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    best = None
+    for _ in range(4):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _capi.call("mpc3_prf_words", rkd.data_ptr(), 1, 0, 0, count, out.data_ptr(), st)
+        e1.record()
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
+        best = ms if best is None else min(best, ms)
+    return count / 2 / (best / 1e3) / 1e9
+
+
+def lenet_inference(dev, batch: int = 64, steps: int = 5):
+    """LeNet private inference (configs[0]), MNIST shape, device-resident input."""
+    import torch
+
+    import paper_2104_10949_b200 as M
+    from paper_2104_10949_b200.nn import InferenceGraph
+
+    sess = M.TrioSession(seed=3)
+    model = M.lenet()
+    rng = np.random.default_rng(3)
+    params = [sess.share(w, rng) for w in M.init_params(model, seed=3)]
+    x = sess.share(M.fx_encode(rng.uniform(0, 1, (batch, 1, 28, 28))), rng)
+    g = InferenceGraph(sess, model, params, x)
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        g.replay()
+    e1.record()
+    e1.synchronize()
+    t = e0.elapsed_time(e1) / steps
+    return {"workload": f"LeNet private inference, MNIST 1x28x28, batch {batch}", "value": batch / (t / 1e3),
+            "unit": "images/s", "ms_per_batch": t, "steps": steps, "cuda_graph": True}
+
+
+def vgg16_ti(dev, batch: int = 32, steps: int = 2):
+    """VGG-16 (avg-pool variant) on Tiny-ImageNet shape (configs[2]): private
+    inference and one private training step (SGD), batch 32, images/s."""
+    import torch
+
+    import paper_2104_10949_b200 as M
+    from paper_2104_10949_b200.nn import TrainState, TrioNet, one_hot
+
+    sess = M.TrioSession(seed=5)
+    model = M.models.vgg16()
+    rng = np.random.default_rng(5)
+    imgs, labels = rng.uniform(0, 1, (batch, 3, 64, 64)), rng.integers(0, 200, batch)
+    st = TrainState(sess, model, M.TrainConfig(0.01, batch, steps + 1, seed=5))
+    xb = st.deal_batch(M.fx_encode(imgs), M.fx_encode(one_hot(labels, 200)))
+    net = TrioNet(sess)
+    net.forward(model, st.params, xb[0], record=False)
+    st.step(*xb)
+    torch.cuda.synchronize()
+    res = {}
+    for kind, fn in (("inference", lambda: net.forward(model, st.params, xb[0], record=False)),
+                     ("training_step", lambda: st.step(*xb))):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            fn()
+        e1.record()
+        e1.synchronize()
+        t = e0.elapsed_time(e1) / steps
+        res[kind] = {"value": batch / (t / 1e3), "unit": "images/s", "ms_per_batch": t}
+    res["workload"] = f"VGG-16 (avg-pool) Tiny-ImageNet 3x64x64, 200 classes, batch {batch}, eager"
+    return res
 
 
 def resnet50_inference(dev, batch: int, steps: int, use_graph: bool):
