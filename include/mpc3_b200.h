@@ -268,6 +268,15 @@ int mpc3_ring_pack(const uint64_t* src, int64_t src_plane, const mpc3_operand* o
 int mpc3_ring_gemm_packed(const uint8_t* A, const uint8_t* B, uint64_t* C, int groups, int64_t M,
                           int64_t N, int64_t kp, int64_t ldc, int64_t c_group, int splits, void* stream);
 
+/* Same with the C layout chosen: c_layout 0 = C[g][m][ldc] (as above),
+ * 1 = C[g][n][ldc] (column-major: element (m, n) at n*ldc + m).  The
+ * column-major form makes an NCHW conv output's (y, x) runs contiguous in C,
+ * so the following reshare/truncate reads coalesce, and the epilogue's
+ * stores coalesce across a warp's 32 rows. */
+int mpc3_ring_gemm_packed_layout(const uint8_t* A, const uint8_t* B, uint64_t* C, int groups, int64_t M,
+                                 int64_t N, int64_t kp, int64_t ldc, int64_t c_group, int splits, int c_layout,
+                                 void* stream);
+
 /* The secure layer's per-party cross terms as ONE implicit ring GEMM per
  * party (protocols.py:110-115):
  *   C[g] = [a_g + a_{g+1} | a_g] . [b_g | b_{g+1}]^T,  g = 0, 1, 2,

@@ -269,21 +269,21 @@ HD void aes128_block(const SmemTables& tab, const uint32_t* rk, uint32_t& s0, ui
 #endif
 }
 
-// Three blocks with the same counter under k_0, k_1, k_2, interleaved round by
-// round: every zero share needs all three keys' words at one position
-// (sharing.py:233-250), and the three independent dependency chains triple
-// the instruction-level parallelism of the table rounds.
-DEV void aes128_block3(const SmemTables& tab, const uint32_t* rk3, uint32_t s[3][4]) {
+// NB independent blocks interleaved round by round (key schedule of block i
+// at rks[i]): the independent dependency chains multiply the instruction-
+// level parallelism of the table rounds.
+template <int NB>
+DEV void aes128_multi(const SmemTables& tab, const uint32_t* const rks[NB], uint32_t s[NB][4]) {
   const uint32_t hl = tab.hl;
 #pragma unroll
-  for (int i = 0; i < 3; ++i)
+  for (int i = 0; i < NB; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) s[i][j] ^= rk3[44 * i + j];
+    for (int j = 0; j < 4; ++j) s[i][j] ^= rks[i][j];
 #pragma unroll 1
   for (int r = 1; r < 10; ++r) {
 #pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      const uint4 k = *reinterpret_cast<const uint4*>(rk3 + 44 * i + 4 * r);
+    for (int i = 0; i < NB; ++i) {
+      const uint4 k = *reinterpret_cast<const uint4*>(rks[i] + 4 * r);
       uint32_t t0 = MPC3_COL(s[i][0], s[i][1], s[i][2], s[i][3], k.x);
       uint32_t t1 = MPC3_COL(s[i][1], s[i][2], s[i][3], s[i][0], k.y);
       uint32_t t2 = MPC3_COL(s[i][2], s[i][3], s[i][0], s[i][1], k.z);
@@ -295,14 +295,21 @@ DEV void aes128_block3(const SmemTables& tab, const uint32_t* rk3, uint32_t s[3]
     }
   }
 #pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    const uint4 k = *reinterpret_cast<const uint4*>(rk3 + 44 * i + 40);
+  for (int i = 0; i < NB; ++i) {
+    const uint4 k = *reinterpret_cast<const uint4*>(rks[i] + 40);
     uint32_t a = s[i][0], b = s[i][1], c = s[i][2], d = s[i][3];
     s[i][0] = MPC3_FIN(a, b, c, d, k.x);
     s[i][1] = MPC3_FIN(b, c, d, a, k.y);
     s[i][2] = MPC3_FIN(c, d, a, b, k.z);
     s[i][3] = MPC3_FIN(d, a, b, c, k.w);
   }
+}
+
+// Three blocks with the same counter under k_0, k_1, k_2: every zero share
+// needs all three keys' words at one position (sharing.py:233-250).
+DEV void aes128_block3(const SmemTables& tab, const uint32_t* rk3, uint32_t s[3][4]) {
+  const uint32_t* rks[3] = {rk3, rk3 + 44, rk3 + 88};
+  aes128_multi<3>(tab, rks, s);
 }
 #undef MPC3_I3
 #undef MPC3_I2
@@ -314,7 +321,11 @@ DEV void aes128_block3(const SmemTables& tab, const uint32_t* rk3, uint32_t s[3]
 // Expand the tables into this CTA's dynamic shared memory (16-byte stores of
 // four lane copies; Te0 from the constant bank) and stage the key schedules.
 // rk_dev: nkeys x 44 round-key words (k_0, k_1, k_2 of the session).
+// Programmatic dependent launch: the table expansion only reads the constant
+// bank and the session keys, so it runs before griddep_wait() and overlaps
+// the previous kernel's tail; every protocol kernel goes through here.
 __device__ inline SmemTables aes_smem_init(AesSmem& sm, const uint32_t* __restrict__ rk_dev, int nkeys) {
+  griddep_launch();
   uint4* dst = reinterpret_cast<uint4*>(sm.te);
   for (int i = threadIdx.x; i < 256 * 16; i += blockDim.x) {
     uint32_t v = c_te0.v[i >> 4];
@@ -325,6 +336,7 @@ __device__ inline SmemTables aes_smem_init(AesSmem& sm, const uint32_t* __restri
   const uint32_t base = (uint32_t)__cvta_generic_to_shared(mpc3_dsm);
   if ((base & 0x00ffffffu) != kAesTableOff) __trap();  // the LDS immediates assume this layout
   __syncthreads();
+  griddep_wait();
   SmemTables t;
   t.hl = (base & 0xff000000u) | ((threadIdx.x & 31) * 4);
   return t;

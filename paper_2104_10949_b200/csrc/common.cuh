@@ -24,6 +24,24 @@ enum Purpose : uint32_t {
   BIN_INPUT = 5,
 };
 
+#if defined(__CUDACC__)
+// Programmatic dependent launch (sm_90+): a kernel lets the next one in the
+// stream start launching CTAs (prologue: AES table expansion, barrier / TMEM
+// setup) while its own last CTAs run, and waits for its predecessor's
+// results only at griddep_wait().  Every thread calls griddep_wait() before
+// its first global read or write of kernel-produced data.
+DEV void griddep_launch() {
+#if defined(__CUDA_ARCH__)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+DEV void griddep_wait() {
+#if defined(__CUDA_ARCH__)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+#endif
+
 // Arithmetic right shift of the two's-complement view (ring.py:75-79).
 HD uint64_t sar(uint64_t v, int bits) { return (uint64_t)(((int64_t)v) >> bits); }
 

@@ -22,6 +22,14 @@ void set_last_error(const char* msg) {
 }
 
 constexpr int kThreads = 256;
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("MPC3_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 constexpr uint64_t kSign2MaxPairs = 200000;  // measured crossover (profiles/README.md)
 // MPC3_SIGN_FUSED=1 selects the single-phase sign kernel (AES inline in the circuit)
 static const bool g_sign_fused = [] {
@@ -46,7 +54,8 @@ static bool aes_attr(const void* fn, int bytes = kAesSmemBytes) {
 #define AES_LAUNCH(kern, grid, stream, ...)                                                \
   do {                                                                                     \
     if (!aes_attr((const void*)kern)) return check_launch(#kern " smem attribute");        \
-    kern<<<(grid), kThreads, kAesSmemBytes, (stream)>>>(__VA_ARGS__);                      \
+    if (launch_pdl(kern, dim3(grid), dim3(kThreads), kAesSmemBytes, (stream), __VA_ARGS__) != cudaSuccess) \
+      return check_launch(#kern);                                                          \
   } while (0)
 
 // Stream counters may be offset by a device-resident per-purpose base
@@ -96,6 +105,8 @@ __global__ void __launch_bounds__(kThreads) zero_share_kernel(const uint32_t* __
 
 __global__ void ring_ew_kernel(int op, const uint64_t* __restrict__ a, const uint64_t* __restrict__ b,
                                uint64_t c, uint64_t* __restrict__ out, uint64_t n) {
+  griddep_launch();
+  griddep_wait();
   GRID_LOOP(i, n) {
     uint64_t x = a[i], r;
     switch (op) {
@@ -116,6 +127,8 @@ __global__ void ring_ew_kernel(int op, const uint64_t* __restrict__ a, const uin
 
 __global__ void ring_rowop_kernel(int op, const uint64_t* __restrict__ a, const uint64_t* __restrict__ b,
                                   uint64_t* __restrict__ out, uint64_t rows, uint64_t cols) {
+  griddep_launch();
+  griddep_wait();
   GRID_LOOP(i, rows * cols) {
     uint64_t v = b[i / cols];
     out[i] = op == MPC3_EW_SUB ? a[i] - v : a[i] + v;
@@ -124,6 +137,8 @@ __global__ void ring_rowop_kernel(int op, const uint64_t* __restrict__ a, const 
 
 __global__ void ring_rowsum_kernel(const uint64_t* __restrict__ a, uint64_t* __restrict__ out,
                                    uint64_t rows, uint64_t cols) {
+  griddep_launch();
+  griddep_wait();
   GRID_LOOP(r, rows) {
     uint64_t s = 0;
     for (uint64_t j = 0; j < cols; ++j) s += a[r * cols + j];
@@ -279,8 +294,8 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const uint32_t* __re
       dst[0] = w[0];
       dst[1] = w[1];
       dst[2] = w[2];
-      dst[3] = prf_block(tab, rk + 2 * 44, resolve(sref(TRUNC_RHO, jrho + k), ctr), blk);
-      dst[4] = prf_block(tab, rk + 1 * 44, resolve(sref(TRUNC_R, jr + k), ctr), blk);
+      trunc_words(tab, rk, resolve(sref(TRUNC_RHO, jrho + k), ctr), resolve(sref(TRUNC_R, jr + k), ctr), blk, dst[3],
+                  dst[4]);
     }
     __syncthreads();
     const int p = threadIdx.x;
@@ -349,7 +364,11 @@ __global__ void __launch_bounds__(kThreads) reshare_trunc_kernel(const uint32_t*
   MPC3_AES_SMEM();
   SmemTables tab = aes_smem_init(sm, rk3, 3);
   StreamHead ha = resolve(ra, ctr), hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
-  GRID_LOOP(b, (n + 1) >> 1) reshare_trunc_item(tab, &sm.rk[0][0], ha, hrho, hr, bits, z, v, out, n, b, pb0);
+  if (n < (1ull << 32))
+    GRID_LOOP(b, (n + 1) >> 1) reshare_trunc_item<SmemTables, uint32_t>(tab, &sm.rk[0][0], ha, hrho, hr, bits, z, v, out,
+                                                                         n, b, pb0);
+  else
+    GRID_LOOP(b, (n + 1) >> 1) reshare_trunc_item(tab, &sm.rk[0][0], ha, hrho, hr, bits, z, v, out, n, b, pb0);
 }
 
 __global__ void __launch_bounds__(kThreads) pool_kernel(const uint32_t* __restrict__ rk3,
@@ -361,7 +380,11 @@ __global__ void __launch_bounds__(kThreads) pool_kernel(const uint32_t* __restri
   MPC3_AES_SMEM();
   SmemTables tab = aes_smem_init(sm, rk3, 3);
   StreamHead hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
-  GRID_LOOP(b, (n + 1) >> 1) pool_item(tab, &sm.rk[0][0], backward != 0, hrho, hr, bits, mulc, x, out, p, b, pb0);
+  if (2 * n < (1ull << 32) && (uint64_t)p.N * p.C * p.H * p.W < (1ull << 32))
+    GRID_LOOP(b, (n + 1) >> 1) pool_item<SmemTables, uint32_t>(tab, &sm.rk[0][0], backward != 0, hrho, hr, bits, mulc, x,
+                                                                out, p, b, pb0);
+  else
+    GRID_LOOP(b, (n + 1) >> 1) pool_item(tab, &sm.rk[0][0], backward != 0, hrho, hr, bits, mulc, x, out, p, b, pb0);
 }
 
 __global__ void __launch_bounds__(kThreads) col2im_kernel(const uint32_t* __restrict__ rk3,
@@ -372,7 +395,11 @@ __global__ void __launch_bounds__(kThreads) col2im_kernel(const uint32_t* __rest
   MPC3_AES_SMEM();
   SmemTables tab = aes_smem_init(sm, rk3, 3);
   StreamHead ha = resolve(ra, ctr), hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
-  GRID_LOOP(b, (n + 1) >> 1) col2im_item(tab, &sm.rk[0][0], ha, hrho, hr, bits, z, g, out, b, pb0);
+  if (2 * n < (1ull << 32))
+    GRID_LOOP(b, (n + 1) >> 1) col2im_item<SmemTables, uint32_t>(tab, &sm.rk[0][0], ha, hrho, hr, bits, z, g, out, b,
+                                                                  pb0);
+  else
+    GRID_LOOP(b, (n + 1) >> 1) col2im_item(tab, &sm.rk[0][0], ha, hrho, hr, bits, z, g, out, b, pb0);
 }
 
 __global__ void sumpool_kernel(const uint64_t* __restrict__ x, uint64_t* __restrict__ out, PoolGeom p) {
@@ -451,20 +478,21 @@ int mpc3_ring_ew(int op, const uint64_t* a, const uint64_t* b, uint64_t c, uint6
   if (op < 0 || op > MPC3_EW_AXPY) return MPC3_ERR_CONFIG;
   if ((op == MPC3_EW_SHL || op == MPC3_EW_SHR || op == MPC3_EW_SAR) && c >= 64) return MPC3_ERR_RANGE;
   if (n == 0) return MPC3_OK;
-  ring_ew_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(op, a, b, c, out, n);
+  launch_pdl(ring_ew_kernel, dim3(grid_for(n, 256)), dim3(256), 0, as_stream(stream), op, a, b, c, out, n);
   return check_launch("ring_ew");
 }
 
 int mpc3_ring_rowop(int op, const uint64_t* a, const uint64_t* b, uint64_t* out, uint64_t rows, uint64_t cols,
                     void* stream) {
   if (rows * cols == 0) return MPC3_OK;
-  ring_rowop_kernel<<<grid_for(rows * cols, 256), 256, 0, as_stream(stream)>>>(op, a, b, out, rows, cols);
+  launch_pdl(ring_rowop_kernel, dim3(grid_for(rows * cols, 256)), dim3(256), 0, as_stream(stream), op, a, b, out, rows,
+             cols);
   return check_launch("ring_rowop");
 }
 
 int mpc3_ring_rowsum(const uint64_t* a, uint64_t* out, uint64_t rows, uint64_t cols, void* stream) {
   if (rows == 0) return MPC3_OK;
-  ring_rowsum_kernel<<<grid_for(rows, 128), 128, 0, as_stream(stream)>>>(a, out, rows, cols);
+  launch_pdl(ring_rowsum_kernel, dim3(grid_for(rows, 128)), dim3(128), 0, as_stream(stream), a, out, rows, cols);
   return check_launch("ring_rowsum");
 }
 
@@ -524,8 +552,8 @@ int mpc3_rss_chain(const uint32_t* rk3, const uint64_t* ctr, const MPC3ChainStep
   if (!aes_attr((const void*)chain_kernel, kAesSmemBytes + 96 * 1024)) return check_launch("chain smem attribute");
   uint64_t chunks = ((n + 1) / 2 + P - 1) / P;
   unsigned grid = (unsigned)(chunks < 148 * 8 ? chunks : 148 * 8);
-  chain_kernel<<<grid, kThreads, smem, as_stream(stream)>>>(rk3, ctr, prog, j_arith, j_rho, j_r, x, out, n,
-                                                            elem_off >> 1, P);
+  launch_pdl(chain_kernel, dim3(grid), dim3(kThreads), smem, as_stream(stream), rk3, ctr, prog, j_arith, j_rho, j_r,
+             x, out, n, elem_off >> 1, P);
   return check_launch("rss_chain");
 }
 
@@ -554,8 +582,8 @@ int mpc3_rss_sign(const uint32_t* rk3, const uint64_t* ctr, int mode, uint64_t j
       return check_launch("sign2 smem attribute");
     uint64_t chunks = ((n + 1) / 2 + P - 1) / P;
     unsigned grid = (unsigned)(chunks < 148 * 2 * 8 ? chunks : 148 * 2 * 8);
-    sign2_kernel<<<grid, kThreads, smem, as_stream(stream)>>>(rk3, ctr, a, mode, x, out, mask, n, n_total, elem_off,
-                                                             P);
+    launch_pdl(sign2_kernel, dim3(grid), dim3(kThreads), smem, as_stream(stream), rk3, ctr, a, mode, x, out, mask, n,
+               n_total, elem_off, P);
     return check_launch("rss_sign2");
   }
   AES_LAUNCH(sign_kernel, grid_for((n + 1) / 2, kThreads, 16), as_stream(stream), 

@@ -73,6 +73,7 @@ __global__ void __launch_bounds__(PT_THREADS) pack_tile_kernel(const uint64_t* _
   __shared__ uint64_t tile[PT_R * PT_K];
   __shared__ int32_t rb[PT_R], ry[PT_R], rx[PT_R];
   __shared__ int32_t kb[PT_K], ky[PT_K], kx[PT_K], khalf[PT_K];
+  griddep_launch();
   const int g = blockIdx.z;
   const int64_t r0 = (int64_t)blockIdx.y * PT_R, c0 = (int64_t)blockIdx.x * PT_K;
   const int t = threadIdx.x;
@@ -137,6 +138,7 @@ __global__ void __launch_bounds__(PT_THREADS) pack_tile_kernel(const uint64_t* _
     khalf[j] = half;
   }
   __syncthreads();
+  griddep_wait();  // the source tensor is the previous kernel's output
   // phase 1: gather the packed values of the tile.  Each thread keeps one
   // row (R_FAST) or one column fixed in registers; a warp's 32 lanes walk
   // the source's contiguous direction.
@@ -302,7 +304,8 @@ DEV void mma_commit(uint64_t* bar) {
 __global__ void __launch_bounds__(256, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    uint64_t* __restrict__ C, int64_t M, int64_t N, int64_t kp, int64_t ldc, int64_t c_group,
-                   int splits, int kb_per_split) {
+                   int splits, int kb_per_split, int c_col) {
+  griddep_launch();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -337,6 +340,7 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
+  griddep_wait();  // packed operands and C are the previous kernels' data
 
   if (warp == 0 && lane == 0) {
     // ---- TMA producer ----
@@ -379,7 +383,9 @@ __global__ void __launch_bounds__(256, 1)
     // ---- epilogue: TMEM -> registers -> recombine -> global ----
     const int wq = warp - 4;  // TMEM lanes 32 wq .. 32 wq + 31
     const int64_t row = m0 + wq * 32 + lane;
-    uint64_t* crow = C + (int64_t)g * c_group + row * ldc;
+    uint64_t* cg = C + (int64_t)g * c_group;
+    // element (row, col) at row*ldc + col (row-major) or col*ldc + row
+    const int64_t rs = c_col ? 1 : ldc, cs = c_col ? ldc : 1;
     if (nkb > 0) {
       mbar_wait(tmem_full, 0);
       asm volatile("tcgen05.fence::after_thread_sync;");
@@ -408,10 +414,11 @@ __global__ void __launch_bounds__(256, 1)
         for (int e = 0; e < 8; ++e) {
           int64_t col = n0 + c0 + e;
           if (col < N) {
+            uint64_t* dst = cg + row * rs + col * cs;
             if (splits > 1)
-              atomicAdd(reinterpret_cast<unsigned long long*>(crow + col), (unsigned long long)acc[e]);
+              atomicAdd(reinterpret_cast<unsigned long long*>(dst), (unsigned long long)acc[e]);
             else
-              crow[col] = acc[e];
+              *dst = acc[e];
           }
         }
       }
@@ -745,9 +752,9 @@ int mpc3_ring_pack(const uint64_t* src, int64_t src_plane, const mpc3_operand* o
     }
     dim3 grid((unsigned)((kp + PT_K - 1) / PT_K), (unsigned)row_tiles, (unsigned)groups);
     if (r_fast)
-      pack_tile_kernel<true><<<grid, PT_THREADS, 0, as_stream(stream)>>>(src, src_plane, o, role, a, out);
+      launch_pdl(pack_tile_kernel<true>, grid, dim3(PT_THREADS), 0, as_stream(stream), src, src_plane, o, role, a, out);
     else
-      pack_tile_kernel<false><<<grid, PT_THREADS, 0, as_stream(stream)>>>(src, src_plane, o, role, a, out);
+      launch_pdl(pack_tile_kernel<false>, grid, dim3(PT_THREADS), 0, as_stream(stream), src, src_plane, o, role, a, out);
     return check_launch("ring_pack_tile");
   }
   pack_kernel<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(src, src_plane, o, role, groups, out, kp);
@@ -756,6 +763,12 @@ int mpc3_ring_pack(const uint64_t* src, int64_t src_plane, const mpc3_operand* o
 
 int mpc3_ring_gemm_packed(const uint8_t* A, const uint8_t* B, uint64_t* C, int groups, int64_t M, int64_t N,
                           int64_t kp, int64_t ldc, int64_t c_group, int splits, void* stream) {
+  return mpc3_ring_gemm_packed_layout(A, B, C, groups, M, N, kp, ldc, c_group, splits, 0, stream);
+}
+
+int mpc3_ring_gemm_packed_layout(const uint8_t* A, const uint8_t* B, uint64_t* C, int groups, int64_t M, int64_t N,
+                                 int64_t kp, int64_t ldc, int64_t c_group, int splits, int c_layout, void* stream) {
+  if (c_layout != 0 && c_layout != 1) return MPC3_ERR_CONFIG;
   if (groups < 1 || M < 0 || N < 0 || kp < 0 || splits < 1) return MPC3_ERR_SHAPE;
   if (kp % 16) return MPC3_ERR_SHAPE;
   if (M == 0 || N == 0) return MPC3_OK;
@@ -776,7 +789,8 @@ int mpc3_ring_gemm_packed(const uint8_t* A, const uint8_t* B, uint64_t* C, int g
   st = make_map(&tb, B, kp, N, (int64_t)groups * 8, BN);
   if (st) return st;
   dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)(groups * splits));
-  gemm_tc_kernel<<<grid, 256, SMEM_BYTES, as_stream(stream)>>>(ta, tb, C, M, N, kp, ldc, c_group, splits, kbs);
+  launch_pdl(gemm_tc_kernel, grid, dim3(256), SMEM_BYTES, as_stream(stream), ta, tb, C, M, N, kp, ldc, c_group, splits,
+             kbs, c_layout);
   return check_launch("ring_gemm_tc");
 }
 

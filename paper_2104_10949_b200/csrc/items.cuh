@@ -68,8 +68,8 @@ HD void arith_item(const T& tab, const uint32_t* rk3, int kind, StreamHead ha, S
     v[1] = trio_mul(v[1], w[1], f1);
   }
   if (kind != 0) {
-    Word2 rho = prf_block(tab, rk3 + 2 * 44, hrho, pb);
-    Word2 r = prf_block(tab, rk3 + 1 * 44, hr, pb);
+    Word2 rho, r;
+    trunc_words(tab, rk3, hrho, hr, pb, rho, r);
     v[0] = trio_truncate(v[0], rho.w0, r.w0, bits);
     v[1] = trio_truncate(v[1], rho.w1, r.w1, bits);
   }
@@ -113,7 +113,10 @@ struct View4 {
   int64_t full[4], org[4], crop[4], zs[4], os[4], zp, op;
 };
 
-template <class T>
+// I: index arithmetic type (uint32_t when every extent fits: the kernels pick
+// it on the host, which turns the 64-bit division calls into short inline
+// sequences).
+template <class T, class I = uint64_t>
 HD void reshare_trunc_item(const T& tab, const uint32_t* rk3, StreamHead ha, StreamHead hrho, StreamHead hr,
                            int bits, const uint64_t* z, const View4& v, uint64_t* out, uint64_t n, uint64_t b,
                            uint64_t pb0 = 0) {
@@ -123,13 +126,14 @@ HD void reshare_trunc_item(const T& tab, const uint32_t* rk3, StreamHead ha, Str
   for (int e = 0; e < 2; ++e) {
     uint64_t f = 2 * b + e;
     ok[e] = f < n;
-    uint64_t r = f;
-    int64_t i3 = r % v.full[3];
-    r /= v.full[3];
-    int64_t i2 = r % v.full[2];
-    r /= v.full[2];
-    int64_t i1 = r % v.full[1];
-    int64_t i0 = r / v.full[1];
+    I r = (I)f;
+    const I f3 = (I)v.full[3], f2 = (I)v.full[2], f1 = (I)v.full[1];
+    int64_t i3 = (int64_t)(r % f3);
+    r /= f3;
+    int64_t i2 = (int64_t)(r % f2);
+    r /= f2;
+    int64_t i1 = (int64_t)(r % f1);
+    int64_t i0 = (int64_t)(r / f1);
     zoff[e] = i0 * v.zs[0] + i1 * v.zs[1] + i2 * v.zs[2] + i3 * v.zs[3];
     i0 -= v.org[0];
     i1 -= v.org[1];
@@ -144,8 +148,7 @@ HD void reshare_trunc_item(const T& tab, const uint32_t* rk3, StreamHead ha, Str
   key_words_pair(tab, rk3, ha, pb, f0, f1);
   Word2 rho = {0, 0}, r = {0, 0};
   if (bits) {
-    rho = prf_block(tab, rk3 + 2 * 44, hrho, pb);
-    r = prf_block(tab, rk3 + 1 * 44, hr, pb);
+    trunc_words(tab, rk3, hrho, hr, pb, rho, r);
   }
   for (int e = 0; e < 2; ++e) {
     if (!ok[e]) continue;
@@ -167,7 +170,7 @@ struct Col2Im {
   int kh, kw, sh, sw, ph, pw;
 };
 
-template <class T>
+template <class T, class I = uint64_t>
 HD void col2im_item(const T& tab, const uint32_t* rk3, StreamHead ha, StreamHead hrho, StreamHead hr, int bits,
                     const uint64_t* z, const Col2Im& g, uint64_t* out, uint64_t b, uint64_t pb0 = 0) {
   const uint64_t pb = pb0 + b;
@@ -181,8 +184,10 @@ HD void col2im_item(const T& tab, const uint32_t* rk3, StreamHead ha, StreamHead
     uint64_t f = 2 * b + e;
     s[e].c[0] = s[e].c[1] = s[e].c[2] = 0;
     if (f >= n_full) continue;
-    int64_t xq = f % g.wf, yq = (f / g.wf) % g.hf;
-    int64_t c = (f / (g.wf * g.hf)) % g.C, n = f / (g.wf * g.hf * g.C);
+    const I fi = (I)f, wf = (I)g.wf, hf = (I)g.hf, Cc = (I)g.C;
+    const I q1 = fi / wf, q2 = q1 / hf;
+    int64_t xq = (int64_t)(fi - q1 * wf), yq = (int64_t)(q1 - q2 * hf);
+    int64_t c = (int64_t)(q2 % Cc), n = (int64_t)(q2 / Cc);
     int64_t yo = yq - g.ph, xo = xq - g.pw;
     if (yo < 0 || xo < 0 || yo >= g.H || xo >= g.W) continue;
     ooff[e] = ((n * g.C + c) * g.H + yo) * g.W + xo;
@@ -206,8 +211,8 @@ HD void col2im_item(const T& tab, const uint32_t* rk3, StreamHead ha, StreamHead
   if (ooff[0] < 0 && ooff[1] < 0) return;
   KeyWords f0, f1;
   key_words_pair(tab, rk3, ha, pb, f0, f1);
-  Word2 rho = prf_block(tab, rk3 + 2 * 44, hrho, pb);
-  Word2 r = prf_block(tab, rk3 + 1 * 44, hr, pb);
+  Word2 rho, r;
+  trunc_words(tab, rk3, hrho, hr, pb, rho, r);
   for (int e = 0; e < 2; ++e) {
     if (ooff[e] < 0) continue;
     Trio t = trio_reshare(s[e], e ? f1 : f0);
@@ -223,7 +228,7 @@ struct PoolGeom {
 };
 
 // fused window sum (x mulc) + truncate; backward = scatter-add then the same
-template <class T>
+template <class T, class I = uint64_t>
 HD void pool_item(const T& tab, const uint32_t* rk3, bool backward, StreamHead hrho, StreamHead hr, int bits,
                   uint64_t mulc, const uint64_t* x, uint64_t* out, const PoolGeom& p, uint64_t b, uint64_t pb0 = 0) {
   const uint64_t pb = pb0 + b;
@@ -235,7 +240,8 @@ HD void pool_item(const T& tab, const uint32_t* rk3, bool backward, StreamHead h
     s[e].c[0] = s[e].c[1] = s[e].c[2] = 0;
     if (f >= n) continue;
     if (!backward) {
-      int64_t ox = f % p.OW, oy = (f / p.OW) % p.OH, nc = f / (p.OW * p.OH);
+      const I fi = (I)f, q1 = fi / (I)p.OW;
+      int64_t ox = (int64_t)(fi - q1 * (I)p.OW), oy = (int64_t)(q1 % (I)p.OH), nc = (int64_t)(q1 / (I)p.OH);
       int64_t y0 = oy * p.sh - p.ph, x0 = ox * p.sw - p.pw;
       const uint64_t* base = x + nc * p.H * p.W;
       for (int u = 0; u < p.kh; ++u) {
@@ -249,7 +255,9 @@ HD void pool_item(const T& tab, const uint32_t* rk3, bool backward, StreamHead h
       }
     } else {
       // windows (oy, ox) with oy*sh - ph <= iy < oy*sh - ph + kh, oy < OH (nn.py:487-499)
-      int64_t ix = f % p.W + p.pw, iy = (f / p.W) % p.H + p.ph, nc = f / (p.W * p.H);
+      const I fi = (I)f, q1 = fi / (I)p.W;
+      int64_t ix = (int64_t)(fi - q1 * (I)p.W) + p.pw, iy = (int64_t)(q1 % (I)p.H) + p.ph,
+              nc = (int64_t)(q1 / (I)p.H);
       for (int64_t oy = iy / p.sh; oy >= 0 && oy * p.sh + p.kh > iy; --oy) {
         if (oy >= p.OH) continue;
         for (int64_t ox = ix / p.sw; ox >= 0 && ox * p.sw + p.kw > ix; --ox) {
@@ -261,8 +269,8 @@ HD void pool_item(const T& tab, const uint32_t* rk3, bool backward, StreamHead h
     }
     for (int i = 0; i < 3; ++i) s[e].c[i] *= mulc;
   }
-  Word2 rho = prf_block(tab, rk3 + 2 * 44, hrho, pb);
-  Word2 r = prf_block(tab, rk3 + 1 * 44, hr, pb);
+  Word2 rho, r;
+  trunc_words(tab, rk3, hrho, hr, pb, rho, r);
   for (int e = 0; e < 2; ++e) {
     uint64_t f = 2 * b + e;
     if (f >= n) break;

@@ -145,6 +145,31 @@ DEV void prf_block3(const Replay& t, const uint32_t*, StreamHead, uint64_t, Word
 }
 #endif
 
+// The truncation pair of one block position: rho from k_2 (TRUNC_RHO) and r
+// from k_1 (TRUNC_R) (protocols.py:166-216), two blocks interleaved on the
+// device.
+template <class T>
+HD void trunc_words(const T& tab, const uint32_t* rk3, StreamHead hrho, StreamHead hr, uint64_t blk, Word2& rho,
+                    Word2& r) {
+  rho = prf_block(tab, rk3 + 2 * 44, hrho, blk);
+  r = prf_block(tab, rk3 + 1 * 44, hr, blk);
+}
+#if defined(__CUDACC__)
+HD void trunc_words(const SmemTables& tab, const uint32_t* rk3, StreamHead hrho, StreamHead hr, uint64_t blk,
+                    Word2& rho, Word2& r) {
+#if defined(__CUDA_ARCH__)
+  uint32_t s[2][4] = {{hrho.s0, hrho.s1, (uint32_t)(blk >> 32), (uint32_t)blk},
+                      {hr.s0, hr.s1, (uint32_t)(blk >> 32), (uint32_t)blk}};
+  const uint32_t* rks[2] = {rk3 + 2 * 44, rk3 + 1 * 44};
+  aes128_multi<2>(tab, rks, s);
+  rho.w0 = (uint64_t)bswap32(s[0][0]) | ((uint64_t)bswap32(s[0][1]) << 32);
+  rho.w1 = (uint64_t)bswap32(s[0][2]) | ((uint64_t)bswap32(s[0][3]) << 32);
+  r.w0 = (uint64_t)bswap32(s[1][0]) | ((uint64_t)bswap32(s[1][1]) << 32);
+  r.w1 = (uint64_t)bswap32(s[1][2]) | ((uint64_t)bswap32(s[1][3]) << 32);
+#endif
+}
+#endif
+
 // Key-word provider over a pair of adjacent elements (words 2b, 2b+1 of each
 // stream share one AES block per key).
 template <class T>

@@ -446,11 +446,13 @@ class TrioSession:
         return out
 
     # -- bilinear layers (protocols.py:97-136, nn.py:435-484) --
-    def _cross_gemm(self, a_src, a_op, b_src, b_op, M, N, Kd) -> torch.Tensor:
+    def _cross_gemm(self, a_src, a_op, b_src, b_op, M, N, Kd, c_col: bool = False) -> torch.Tensor:
         """z_i = (x_i + x_{i+1}) y_i + x_i y_{i+1} for the three parties, as one
         batched ring GEMM with inner length 2K (protocols.py:110-115).
         Default: pack_kernel writes the byte-limb planes, the TMA-fed tcgen05
-        GEMM consumes them; MPC3_IMPLICIT_GEMM=1 selects the in-kernel gather."""
+        GEMM consumes them; MPC3_IMPLICIT_GEMM=1 selects the in-kernel gather.
+        c_col: z[g] column-major (element (m, n) at n*M + m) — only on the
+        packed path; callers check `self.c_col_ok` before asking for it."""
         if IMPLICIT_GEMM:
             splits = gemm_splits(M, N, 2 * Kd, groups=3)
             z = (torch.zeros if splits > 1 else torch.empty)(3 * M * N, dtype=torch.int64, device=_dev())
@@ -465,8 +467,13 @@ class TrioSession:
         K.call("mpc3_ring_pack", b_src.data_ptr(), b_src.stride(0), C.byref(b_op), 1, B.data_ptr(), kp, st)
         splits = gemm_splits(M, N, kp, groups=3)
         z = (torch.zeros if splits > 1 else torch.empty)(3 * M * N, dtype=torch.int64, device=_dev())
-        K.call("mpc3_ring_gemm_packed", A.data_ptr(), B.data_ptr(), z.data_ptr(), 3, M, N, kp, N, M * N, splits, st)
+        K.call("mpc3_ring_gemm_packed_layout", A.data_ptr(), B.data_ptr(), z.data_ptr(), 3, M, N, kp,
+               M if c_col else N, M * N, splits, 1 if c_col else 0, st)
         return z
+
+    @property
+    def c_col_ok(self) -> bool:
+        return not IMPLICIT_GEMM
 
     def _finish(self, z, view, out: RssTensor, bits, label):
         ja = self.take(ARITH)
@@ -522,9 +529,13 @@ class TrioSession:
         a_op = K.conv_operand(K.GATHER_IM2COL, nb * oh * ow, c * kh * kw, nb, c, h, w, xs[1:], kh, kw, sh, sw, ph, pw,
                               oh, ow)
         b_op = K.dense_operand(o, c * kh * kw, s_r=ks[1], t0=ks[2], t1=ks[3], t2=ks[4], K1=kh, K2=kw)
-        z = self._cross_gemm(x.data, a_op, k.data, b_op, nb * oh * ow, o, c * kh * kw)
+        col = self.c_col_ok
+        M = nb * oh * ow
+        z = self._cross_gemm(x.data, a_op, k.data, b_op, M, o, c * kh * kw, c_col=col)
         out = empty((nb, o, oh, ow), x.fp)
-        view = K.make_view((nb, o, oh, ow), z_stride=(oh * ow * o, 1, ow * o, o))
+        # z[(n, y, x), o]: column-major keeps each (n, o) plane's (y, x) run contiguous
+        zs = (oh * ow, M, ow, 1) if col else (oh * ow * o, 1, ow * o, o)
+        view = K.make_view((nb, o, oh, ow), z_stride=zs)
         return self._finish(z, view, out, bits, "mul.reshare")
 
     def conv2d_wgrad(self, x: RssTensor, g: RssTensor, kernel, stride, padding, bits) -> RssTensor:
@@ -546,9 +557,12 @@ class TrioSession:
         a_op = K.conv_operand(K.GATHER_WGRAD, c * kh * kw, nb * oh * ow, nb, c, h, w, xs[1:], kh, kw, sh, sw, ph, pw,
                               oh, ow)
         b_op = K.dense_operand(o, nb * oh * ow, s_r=gs[2], t0=gs[1], t1=gs[3], t2=gs[4], K1=oh, K2=ow)
-        z = self._cross_gemm(x.data, a_op, g.data, b_op, c * kh * kw, o, nb * oh * ow)
+        col = self.c_col_ok
+        M = c * kh * kw
+        z = self._cross_gemm(x.data, a_op, g.data, b_op, M, o, nb * oh * ow, c_col=col)
         out = empty((o, c, kh, kw), x.fp)
-        view = K.make_view((c, o, fh, fw), crop=(c, o, kh, kw), z_stride=(kh * kw * o, 1, kw * o, o),
+        zs = (kh * kw, M, kw, 1) if col else (kh * kw * o, 1, kw * o, o)
+        view = K.make_view((c, o, fh, fw), crop=(c, o, kh, kw), z_stride=zs,
                            out_stride=(kh * kw, c * kh * kw, kw, 1), z_plane=c * kh * kw * o)
         self._reduce_cross_terms(z)  # sum over the batch shards before reshare / truncate
         with self.replicated():

@@ -187,6 +187,21 @@ def test_ring_matmul_all_ones_worst_case_and_split():
         assert np.all(got == U64(K % (1 << 64)))  # (-1)(-1) K = K
 
 
+@pytest.mark.parametrize("splits", [1, 3])
+def test_ring_gemm_column_major_output(splits):
+    """c_layout 1 writes element (m, n) at n*ldc + m: the transpose of the
+    row-major result, split-K included."""
+    rng = np.random.default_rng(11 + splits)
+    M, K, Nn = 300, 1000, 96
+    a, b = rnd(rng, (M, K)), rnd(rng, (K, Nn))
+    kp = (K + 15) // 16 * 16
+    A = _pack(dev(a), 0, _capi.dense_operand(M, K, s_r=K, t2=1), 2, kp)
+    B = _pack(dev(b), 0, _capi.dense_operand(Nn, K, s_r=1, t2=Nn), 2, kp)
+    Cm = torch.zeros(M * Nn, dtype=torch.int64, device="cuda")
+    _capi.call("mpc3_ring_gemm_packed_layout", p(A), p(B), p(Cm), 1, M, Nn, kp, M, M * Nn, splits, 1, stream())
+    assert np.array_equal(host(Cm).reshape(Nn, M).T, R.wrap_matmul(a, b))
+
+
 def test_ring_matmul_u64_convenience():
     rng = np.random.default_rng(3)
     M, K, Nn = 77, 20000, 33
