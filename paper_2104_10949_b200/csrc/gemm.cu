@@ -66,134 +66,122 @@ struct PackTileArgs {
 // row bits 3-5.
 DEV int pt_swz(int i, int j) { return ((j & ~7) + (((j & 7) + (j >> 3) + (i & 7)) & 7)) ^ (((i >> 3) & 7) << 3); }
 
-template <bool R_FAST>
+// Row / column part of the gather offset: {base, y, x, half}.  Columns past
+// the data (zero padding) and rows past the end get y = -2^30, which fails
+// the unsigned bounds check, so no separate flag is tested per element.
+DEV int4 pack_row_part(const Operand& o, int64_t r, int64_t rows) {
+  int64_t b = 0;
+  int32_t y = 0, x = 0;
+  if (r >= rows) return make_int4(0, -(1 << 30), 0, 0);
+  if (o.mode == MPC3_GATHER_DENSE) {
+    b = o.off + r * o.s_r;
+  } else if (o.mode == MPC3_GATHER_IM2COL) {  // r = (n, y, x)
+    int64_t xx = r % o.ow, q = r / o.ow;
+    int64_t yy = q % o.oh, n = q / o.oh;
+    b = n * o.sN;
+    y = (int32_t)(yy * o.sh - o.ph);
+    x = (int32_t)(xx * o.sw - o.pw);
+  } else {  // WGRAD: r = (c, u, v)
+    int64_t v = r % o.kw, q = r / o.kw;
+    int64_t u = q % o.kh, c = q / o.kh;
+    b = c * o.sC;
+    y = (int32_t)(u - o.ph);
+    x = (int32_t)(v - o.pw);
+  }
+  return make_int4((int32_t)b, y, x, 0);
+}
+DEV int4 pack_col_part(const Operand& o, int64_t kk, int64_t K, int64_t lim) {
+  if (kk >= lim) return make_int4(0, -(1 << 30), 0, 0);
+  const int half = kk >= K ? 1 : 0;
+  const int64_t k = kk - half * K;
+  int64_t b = 0;
+  int32_t y = 0, x = 0;
+  if (o.mode == MPC3_GATHER_DENSE) {
+    int64_t k2 = k % o.K2, q = k / o.K2;
+    b = (q / o.K1) * o.t0 + (q % o.K1) * o.t1 + k2 * o.t2;
+  } else if (o.mode == MPC3_GATHER_IM2COL) {  // k = (c, u, v)
+    int64_t v = k % o.kw, q = k / o.kw;
+    int64_t u = q % o.kh, c = q / o.kh;
+    b = c * o.sC;
+    y = (int32_t)u;
+    x = (int32_t)v;
+  } else {  // WGRAD: k = (n, y, x)
+    int64_t xx = k % o.ow, q = k / o.ow;
+    int64_t yy = q % o.oh, n = q / o.oh;
+    b = n * o.sN;
+    y = (int32_t)(yy * o.sh);
+    x = (int32_t)(xx * o.sw);
+  }
+  return make_int4((int32_t)b, y, x, half);
+}
+
+template <bool R_FAST, int ROLE>
 __global__ void __launch_bounds__(PT_THREADS) pack_tile_kernel(const uint64_t* __restrict__ src, int64_t plane,
-                                                               Operand o, int role, PackTileArgs a,
+                                                               Operand o, PackTileArgs a,
                                                                uint8_t* __restrict__ out) {
   __shared__ uint64_t tile[PT_R * PT_K];
-  __shared__ int32_t rb[PT_R], ry[PT_R], rx[PT_R];
-  __shared__ int32_t kb[PT_K], ky[PT_K], kx[PT_K], khalf[PT_K];
+  __shared__ int4 rpart[PT_R], cpart[PT_K];
   griddep_launch();
   const int g = blockIdx.z;
   const int64_t r0 = (int64_t)blockIdx.y * PT_R, c0 = (int64_t)blockIdx.x * PT_K;
   const int t = threadIdx.x;
-  if (t < PT_R) {
-    int64_t r = r0 + t;
-    int64_t b = 0;
-    int32_t y = 0, x = 0;
-    if (r < a.rows) {
-      if (o.mode == MPC3_GATHER_DENSE) {
-        b = o.off + r * o.s_r;
-      } else if (o.mode == MPC3_GATHER_IM2COL) {  // r = (n, y, x)
-        int64_t xx = r % o.ow, q = r / o.ow;
-        int64_t yy = q % o.oh, n = q / o.oh;
-        b = n * o.sN;
-        y = (int32_t)(yy * o.sh - o.ph);
-        x = (int32_t)(xx * o.sw - o.pw);
-      } else {  // WGRAD: r = (c, u, v)
-        int64_t v = r % o.kw, q = r / o.kw;
-        int64_t u = q % o.kh, c = q / o.kh;
-        b = c * o.sC;
-        y = (int32_t)(u - o.ph);
-        x = (int32_t)(v - o.pw);
-      }
-    } else {
-      y = -(1 << 30);  // rows past the end read nothing
-    }
-    rb[t] = (int32_t)b;
-    ry[t] = y;
-    rx[t] = x;
-  } else if (t < PT_R + PT_K) {
-    const int j = t - PT_R;
-    int64_t kk = c0 + j;
-    int half = -1;  // -1: zero padding
-    int64_t k = 0;
-    if (kk < a.lim) {
-      half = kk >= a.K ? 1 : 0;
-      k = kk - half * a.K;
-    }
-    int64_t b = 0;
-    int32_t y = 0, x = 0;
-    if (half >= 0) {
-      if (o.mode == MPC3_GATHER_DENSE) {
-        int64_t k2 = k % o.K2, q = k / o.K2;
-        b = (q / o.K1) * o.t0 + (q % o.K1) * o.t1 + k2 * o.t2;
-      } else if (o.mode == MPC3_GATHER_IM2COL) {  // k = (c, u, v)
-        int64_t v = k % o.kw, q = k / o.kw;
-        int64_t u = q % o.kh, c = q / o.kh;
-        b = c * o.sC;
-        y = (int32_t)u;
-        x = (int32_t)v;
-      } else {  // WGRAD: k = (n, y, x)
-        int64_t xx = k % o.ow, q = k / o.ow;
-        int64_t yy = q % o.oh, n = q / o.oh;
-        b = n * o.sN;
-        y = (int32_t)(yy * o.sh);
-        x = (int32_t)(xx * o.sw);
-      }
-    }
-    kb[j] = (int32_t)b;
-    ky[j] = y;
-    kx[j] = x;
-    khalf[j] = half;
-  }
+  if (t < PT_R)
+    rpart[t] = pack_row_part(o, r0 + t, a.rows);
+  else if (t < PT_R + PT_K)
+    cpart[t - PT_R] = pack_col_part(o, c0 + (t - PT_R), a.K, a.lim);
   __syncthreads();
   griddep_wait();  // the source tensor is the previous kernel's output
   // phase 1: gather the packed values of the tile.  Each thread keeps one
   // row (R_FAST) or one column fixed in registers; a warp's 32 lanes walk
-  // the source's contiguous direction.
-  const uint64_t* sg = src + (int64_t)g * plane;
+  // the source's contiguous direction.  All loads first (16 in flight).
+  const uint64_t* sg = src + (ROLE == 2 ? 0 : (int64_t)g * plane);
   const uint64_t* sn = src + (int64_t)((g + 1) % 3) * plane;
   const int fixed = R_FAST ? (t % PT_R) : (t % PT_K);
-  const int32_t fb = R_FAST ? rb[fixed] : kb[fixed];
-  const int32_t fy = R_FAST ? ry[fixed] : ky[fixed];
-  const int32_t fx = R_FAST ? rx[fixed] : kx[fixed];
-  const int fh = R_FAST ? 0 : khalf[fixed];
-  // all loads of the thread first (16 in flight), then combine and store
+  const int4 fp = R_FAST ? rpart[fixed] : cpart[fixed];
   constexpr int PER = (PT_R * PT_K) / PT_THREADS;
+  constexpr int STEP = PT_THREADS / (R_FAST ? PT_R : PT_K);
+  const int var0 = t / (R_FAST ? PT_R : PT_K);
+  const uint32_t H = (uint32_t)a.H, W = (uint32_t)a.W;
   uint64_t vs[PER], vn[PER];
-  int hv[PER];
 #pragma unroll
   for (int it = 0; it < PER; ++it) {
-    const int var = t / (R_FAST ? PT_R : PT_K) + it * (PT_THREADS / (R_FAST ? PT_R : PT_K));
-    const int i = R_FAST ? fixed : var, j = R_FAST ? var : fixed;
-    const int half = R_FAST ? khalf[j] : fh;
-    const int32_t yy = fy + (R_FAST ? ky[j] : ry[i]), xx = fx + (R_FAST ? kx[j] : rx[i]);
-    const bool ok = half >= 0 && yy >= 0 && xx >= 0 && yy < a.H && xx < a.W;
-    const int32_t off = ok ? fb + (R_FAST ? kb[j] : rb[i]) + yy * a.sH + xx * a.sW : 0;
-    hv[it] = ok ? half : -1;
-    vs[it] = ok ? __ldg((role == 2 ? src : sg) + off) : 0;
-    vn[it] = (ok && role != 2) ? __ldg(sn + off) : 0;
+    const int4 vp = R_FAST ? cpart[var0 + it * STEP] : rpart[var0 + it * STEP];
+    const int32_t yy = fp.y + vp.y, xx = fp.z + vp.z;
+    const bool ok = (uint32_t)yy < H && (uint32_t)xx < W;
+    const uint32_t off = ok ? (uint32_t)(fp.x + vp.x + yy * a.sH + xx * a.sW) : 0u;
+    vs[it] = ok ? __ldg(sg + off) : 0ull;
+    if (ROLE != 2) vn[it] = ok ? __ldg(sn + off) : 0ull;
   }
 #pragma unroll
   for (int it = 0; it < PER; ++it) {
-    const int var = t / (R_FAST ? PT_R : PT_K) + it * (PT_THREADS / (R_FAST ? PT_R : PT_K));
+    const int var = var0 + it * STEP;
     const int i = R_FAST ? fixed : var, j = R_FAST ? var : fixed;
-    uint64_t v = 0;
-    if (hv[it] >= 0) {
-      if (role == 2)
-        v = vs[it];
-      else if (role == 0)
-        v = hv[it] == 0 ? vs[it] + vn[it] : vs[it];  // [x_i + x_{i+1} | x_i]  (protocols.py:110-115)
-      else
-        v = hv[it] == 0 ? vs[it] : vn[it];  // [y_i | y_{i+1}]
-    }
+    const int half = R_FAST ? cpart[j].w : fp.w;
+    uint64_t v;
+    if (ROLE == 2)
+      v = vs[it];
+    else if (ROLE == 0)
+      v = half == 0 ? vs[it] + vn[it] : vs[it];  // [x_i + x_{i+1} | x_i]  (protocols.py:110-115)
+    else
+      v = half == 0 ? vs[it] : vn[it];  // [y_i | y_{i+1}]
     tile[i * PT_K + pt_swz(i, j)] = v;
   }
   __syncthreads();
   // phase 2: 8 consecutive columns of one row -> one u64 per limb plane
+  const int64_t pstride = a.rows * a.kp;
 #pragma unroll 1
   for (int e = t; e < PT_R * (PT_K / 8); e += PT_THREADS) {
     const int i = e / (PT_K / 8), ch = e % (PT_K / 8);
     const int64_t r = r0 + i, kk = c0 + ch * 8;
     if (r >= a.rows || kk >= a.kp) continue;
+    const int cb = (ch * 8) ^ (((i >> 3) & 7) << 3), rot = (ch + i) & 7;
     uint64_t v[8], w[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = tile[i * PT_K + pt_swz(i, ch * 8 + q)];
+    for (int q = 0; q < 8; ++q) v[q] = tile[i * PT_K + cb + ((q + rot) & 7)];
     byte_transpose8(v, w);
-    uint8_t* base = out + ((int64_t)g * 8 * a.rows + r) * a.kp + kk;
+    uint64_t* dst = reinterpret_cast<uint64_t*>(out + ((int64_t)g * 8 * a.rows + r) * a.kp + kk);
 #pragma unroll
-    for (int l = 0; l < 8; ++l) *reinterpret_cast<uint64_t*>(base + (int64_t)l * a.rows * a.kp) = w[l];
+    for (int l = 0; l < 8; ++l) dst[l * (pstride >> 3)] = w[l];
   }
 }
 
@@ -751,10 +739,11 @@ int mpc3_ring_pack(const uint64_t* src, int64_t src_plane, const mpc3_operand* o
       r_fast = o.mode == MPC3_GATHER_IM2COL;
     }
     dim3 grid((unsigned)((kp + PT_K - 1) / PT_K), (unsigned)row_tiles, (unsigned)groups);
-    if (r_fast)
-      launch_pdl(pack_tile_kernel<true>, grid, dim3(PT_THREADS), 0, as_stream(stream), src, src_plane, o, role, a, out);
-    else
-      launch_pdl(pack_tile_kernel<false>, grid, dim3(PT_THREADS), 0, as_stream(stream), src, src_plane, o, role, a, out);
+    void (*k)(const uint64_t*, int64_t, Operand, PackTileArgs, uint8_t*) =
+        r_fast ? (role == 0 ? pack_tile_kernel<true, 0> : role == 1 ? pack_tile_kernel<true, 1> : pack_tile_kernel<true, 2>)
+               : (role == 0 ? pack_tile_kernel<false, 0>
+                            : role == 1 ? pack_tile_kernel<false, 1> : pack_tile_kernel<false, 2>);
+    launch_pdl(k, grid, dim3(PT_THREADS), 0, as_stream(stream), src, src_plane, o, a, out);
     return check_launch("ring_pack_tile");
   }
   pack_kernel<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(src, src_plane, o, role, groups, out, kp);
