@@ -244,7 +244,7 @@ def run_b200(args, ws, rank, local):
     # roofline instrumentation: CUDA events around every launch of the
     # dominant kernel (the tcgen05 ring GEMM) and of the fused sign circuit,
     # on their launch stream (torch's current stream)
-    gemm_events, sign_events = [], []
+    gemm_events, sign_events, gemm_bytes = [], [], []
     instrument = {"on": False, "k": 0}
 
     def traced_call(name, *a):
@@ -260,7 +260,9 @@ def run_b200(args, ws, rank, local):
             else:  # groups x M x N x 2K ring MACs, 72 int8 ops each (36 limb-pair MACs)
                 groups, M, N = int(a[3]), int(a[4]), int(a[5])
                 sign_k = instrument["k"] if instrument["k"] else int(a[6]) // 2
+                kp = int(a[6])
                 gemm_events.append((e0, e1, 72 * groups * M * N * 2 * sign_k))
+                gemm_bytes.append(groups * ((M + N) * 8 * kp + M * N * 8))  # packed A, B (8 limb planes) + C
             return
         return counting_call(name, *a)
 
@@ -331,6 +333,14 @@ def run_b200(args, ws, rank, local):
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except OSError:
         pass
+    traffic = {}
+    try:  # one ncu capture of the same step's GEMM launches (tools/traffic.py)
+        tj = json.load(open(os.path.join(ROOT, "profiles", "r01_gemm_traffic.json")))
+        traffic = {"traffic_bytes_per_launch": tj["traffic_bytes_per_launch"],
+                   "source_note": "profiles/r01_gemm_traffic.json: ncu dram__bytes_read.sum + dram__bytes_write.sum, "
+                                  f"mean over the {tj['launches']} GEMM launches of one AlexNet step"}
+    except (OSError, KeyError, ValueError):
+        pass
     gemm_ms = sum(a.elapsed_time(c) for a, c, _ in gemm_events)
     gemm_ops = sum(w for _, _, w in gemm_events)
     nl = max(1, len(gemm_events))
@@ -339,7 +349,9 @@ def run_b200(args, ws, rank, local):
     roofline = {"kernel": "gemm_tc_kernel (tcgen05.mma kind::i8, 8 TMEM diagonal accumulators, TMA SWIZZLE_32B)",
                 "bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TFLOP/s",
                 "frac": (achieved / int8_peak) if achieved else None,
-                "traffic": None,
+                "traffic": traffic.get("traffic_bytes_per_launch"),
+                "traffic_source": traffic.get("source_note"),
+                "operand_bytes_per_launch": sum(gemm_bytes) / nl if gemm_bytes else None,
                 "peak_source": ("2 x MEASURED_PEAKS.json bf16_tflops (dense int8 = 2x dense bf16 on B200; "
                                 "cuBLASLt int8 measured 2,924-3,063 TOPS, profiles/r01_microbench_quick.json)"),
                 "launches": len(gemm_events), "kernel_ms_per_step": gemm_ms,
