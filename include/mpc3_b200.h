@@ -277,6 +277,14 @@ int mpc3_ring_gemm_packed_layout(const uint8_t* A, const uint8_t* B, uint64_t* C
                                  int64_t N, int64_t kp, int64_t ldc, int64_t c_group, int splits, int c_layout,
                                  void* stream);
 
+/* Stream-K form of mpc3_ring_gemm_packed_layout for GEMMs with few tiles:
+ * `ctas` persistent CTAs (<= the SM count) take equal contiguous ranges of the
+ * (group, m-tile, n-tile, K-block) iterations and atomically add their
+ * partial tiles, so C must be zeroed.  Exact for any kp (segments are capped
+ * at 16384 K). */
+int mpc3_ring_gemm_streamk(const uint8_t* A, const uint8_t* B, uint64_t* C, int groups, int64_t M, int64_t N,
+                           int64_t kp, int64_t ldc, int64_t c_group, int ctas, int c_layout, void* stream);
+
 /* The secure layer's per-party cross terms as ONE implicit ring GEMM per
  * party (protocols.py:110-115):
  *   C[g] = [a_g + a_{g+1} | a_g] . [b_g | b_{g+1}]^T,  g = 0, 1, 2,

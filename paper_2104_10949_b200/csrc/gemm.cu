@@ -260,6 +260,10 @@ DEV void tma_load_3d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, i
       : "memory");
 }
 
+DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 // K-major, 32-byte-swizzled UMMA shared-memory descriptor (atom 8 rows x 32 B).
 DEV uint64_t umma_desc_sw32(uint32_t saddr) {
   uint64_t d = 0;
@@ -384,18 +388,22 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
       for (int e = 0; e < 8; ++e) acc[e] = 0;
       if (nkb > 0) {
+        // all 8 diagonals of this 8-column chunk in flight, one wait
+        uint32_t r[8][8];
 #pragma unroll
         for (int d = 0; d < 8; ++d) {
-          uint32_t r[8];
           uint32_t taddr = tmem + ((uint32_t)(wq * 32) << 16) + d * BN + c0;
           asm volatile(
               "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+              : "=r"(r[d][0]), "=r"(r[d][1]), "=r"(r[d][2]), "=r"(r[d][3]), "=r"(r[d][4]), "=r"(r[d][5]),
+                "=r"(r[d][6]), "=r"(r[d][7])
               : "r"(taddr));
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-          for (int e = 0; e < 8; ++e) acc[e] += (uint64_t)r[e] << (8 * d);
         }
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int d = 0; d < 8; ++d)
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] += (uint64_t)r[d][e] << (8 * d);
       }
       if (row < M) {
 #pragma unroll
@@ -412,6 +420,169 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
+  }
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Stream-K variant for GEMMs with fewer tiles than a few waves: the
+// (group, m-tile, n-tile, K-block) iteration space is cut into equal
+// contiguous ranges, one per persistent CTA (<= 148), so no SM idles in a
+// last partial wave.  A CTA's range crosses tile boundaries; each maximal run
+// inside one tile (at most MAX_SPLIT_K/BK K-blocks, the exactness bound) is a
+// segment whose partial sum is atomically added into the zeroed C.  The TMA /
+// MMA pipeline runs across segments; TMEM is handed back by the epilogue
+// through tmem_empty.
+struct SkSeg {
+  int tile, kb0, nkb;
+};
+DEV SkSeg sk_seg(int64_t it, int64_t it_end, int nkb_total) {
+  SkSeg sg;
+  sg.tile = (int)(it / nkb_total);
+  sg.kb0 = (int)(it % nkb_total);
+  int64_t rem_tile = nkb_total - sg.kb0, rem = it_end - it;
+  int64_t n = rem_tile < rem ? rem_tile : rem;
+  const int cap = MAX_SPLIT_K / BK;
+  sg.nkb = (int)(n < cap ? n : cap);
+  return sg;
+}
+
+__global__ void __launch_bounds__(256, 1)
+    gemm_sk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   uint64_t* __restrict__ C, int64_t M, int64_t N, int64_t kp, int64_t ldc, int64_t c_group,
+                   int mt, int nt, int64_t total_iters, int c_col) {
+  griddep_launch();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint64_t* tmem_empty = tmem_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int nkb_total = (int)((kp + BK - 1) / BK);
+  const int64_t it_begin = total_iters * blockIdx.x / gridDim.x;
+  const int64_t it_end = total_iters * (blockIdx.x + 1) / gridDim.x;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    mbar_init(tmem_empty, 128);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+  griddep_wait();  // packed operands and the zeroed C are the previous kernels' data
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer: all segments back to back ----
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    int i = 0;
+    for (int64_t it = it_begin; it < it_end;) {
+      const SkSeg sg = sk_seg(it, it_end, nkb_total);
+      const int g = sg.tile / (mt * nt), mn = sg.tile % (mt * nt);
+      const int m0 = (mn / nt) * BM, n0 = (mn % nt) * BN;
+      for (int k = 0; k < sg.nkb; ++k, ++i) {
+        const int s = i % STAGES;
+        const uint32_t ph = (i / STAGES) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        mbar_expect_tx(&full[s], A_STAGE + B_STAGE);
+        const int kc = (sg.kb0 + k) * BK;
+        tma_load_3d(&tmA, &full[s], sA + s * A_STAGE, kc, m0, g * 8);
+        tma_load_3d(&tmB, &full[s], sB + s * B_STAGE, kc, n0, g * 8);
+      }
+      it += sg.nkb;
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer ----
+    int i = 0, seg = 0;
+    for (int64_t it = it_begin; it < it_end; ++seg) {
+      const SkSeg sg = sk_seg(it, it_end, nkb_total);
+      if (seg > 0) {  // the epilogue has drained the previous segment's accumulators
+        mbar_wait(tmem_empty, (seg - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+      }
+      for (int k = 0; k < sg.nkb; ++k, ++i) {
+        const int s = i % STAGES;
+        const uint32_t ph = (i / STAGES) & 1;
+        mbar_wait(&full[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t a_base = smem_u32(sA + s * A_STAGE);
+        const uint32_t b_base = smem_u32(sB + s * B_STAGE);
+#pragma unroll
+        for (int li = 0; li < 8; ++li) {
+          const uint64_t da = umma_desc_sw32(a_base + li * (BM * BK));
+          const int nblk = 8 - li;
+          const int first = nblk > 4 ? 4 : nblk;
+          const uint32_t acc = (k > 0 || li > 0) ? 1u : 0u;
+          mma_i8(tmem + li * BN, da, umma_desc_sw32(b_base), idesc_i8(first * BN), acc);
+          if (nblk > 4)
+            mma_i8(tmem + (li + 4) * BN, da, umma_desc_sw32(b_base + 4 * (BN * BK)), idesc_i8((nblk - 4) * BN),
+                   acc);
+        }
+        mma_commit(&empty[s]);
+      }
+      mma_commit(tmem_full);
+      it += sg.nkb;
+    }
+  } else if (warp >= 4) {
+    // ---- epilogue: TMEM -> registers -> recombine -> atomic add into C ----
+    const int wq = warp - 4;
+    const int64_t rs = c_col ? 1 : ldc, cs = c_col ? ldc : 1;
+    int seg = 0;
+    for (int64_t it = it_begin; it < it_end; ++seg) {
+      const SkSeg sg = sk_seg(it, it_end, nkb_total);
+      const int g = sg.tile / (mt * nt), mn = sg.tile % (mt * nt);
+      const int64_t m0 = (int64_t)(mn / nt) * BM, n0 = (int64_t)(mn % nt) * BN;
+      const int64_t row = m0 + wq * 32 + lane;
+      uint64_t* cg = C + (int64_t)g * c_group;
+      mbar_wait(tmem_full, seg & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 8) {
+        uint32_t r[8][8];
+#pragma unroll
+        for (int d = 0; d < 8; ++d) {
+          const uint32_t taddr = tmem + ((uint32_t)(wq * 32) << 16) + d * BN + c0;
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+              : "=r"(r[d][0]), "=r"(r[d][1]), "=r"(r[d][2]), "=r"(r[d][3]), "=r"(r[d][4]), "=r"(r[d][5]),
+                "=r"(r[d][6]), "=r"(r[d][7])
+              : "r"(taddr));
+        }
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (row < M) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            uint64_t acc = 0;
+#pragma unroll
+            for (int d = 0; d < 8; ++d) acc += (uint64_t)r[d][e] << (8 * d);
+            const int64_t col = n0 + c0 + e;
+            if (col < N) atomicAdd(reinterpret_cast<unsigned long long*>(cg + row * rs + col * cs), acc);
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      mbar_arrive(tmem_empty);
+      it += sg.nkb;
+    }
   }
   __syncthreads();
   if (warp == 2) {
@@ -438,9 +609,6 @@ DEV uint32_t sw32_off(int row, int kq) {
   return off ^ ((((uint32_t)row >> 2) & 1u) << 4);
 }
 
-DEV void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 
 // 4 consecutive packed values (k .. k+3 of the 2K-long cross-term row) ->
 // 8 limb words of 4 bytes each, stored into the limb planes of one tile.
@@ -589,18 +757,22 @@ __global__ void __launch_bounds__(IG_THREADS, 1)
 #pragma unroll
       for (int e = 0; e < 8; ++e) acc[e] = 0;
       if (nkb > 0) {
+        // all 8 diagonals of this 8-column chunk in flight, one wait
+        uint32_t r[8][8];
 #pragma unroll
         for (int d = 0; d < 8; ++d) {
-          uint32_t r[8];
           uint32_t taddr = tmem + ((uint32_t)(wq * 32) << 16) + d * BN + c0;
           asm volatile(
               "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+              : "=r"(r[d][0]), "=r"(r[d][1]), "=r"(r[d][2]), "=r"(r[d][3]), "=r"(r[d][4]), "=r"(r[d][5]),
+                "=r"(r[d][6]), "=r"(r[d][7])
               : "r"(taddr));
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-          for (int e = 0; e < 8; ++e) acc[e] += (uint64_t)r[e] << (8 * d);
         }
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int d = 0; d < 8; ++d)
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] += (uint64_t)r[d][e] << (8 * d);
       }
       if (row < M) {
 #pragma unroll
@@ -781,6 +953,33 @@ int mpc3_ring_gemm_packed_layout(const uint8_t* A, const uint8_t* B, uint64_t* C
   launch_pdl(gemm_tc_kernel, grid, dim3(256), SMEM_BYTES, as_stream(stream), ta, tb, C, M, N, kp, ldc, c_group, splits,
              kbs, c_layout);
   return check_launch("ring_gemm_tc");
+}
+
+int mpc3_ring_gemm_streamk(const uint8_t* A, const uint8_t* B, uint64_t* C, int groups, int64_t M, int64_t N,
+                           int64_t kp, int64_t ldc, int64_t c_group, int ctas, int c_layout, void* stream) {
+  if (groups < 1 || M < 0 || N < 0 || kp < 0 || ctas < 1) return MPC3_ERR_SHAPE;
+  if (kp % 16) return MPC3_ERR_SHAPE;
+  if (c_layout != 0 && c_layout != 1) return MPC3_ERR_CONFIG;
+  if (M == 0 || N == 0 || kp == 0) return MPC3_OK;
+  if (M > (1 << 30) || N > (1 << 30)) return MPC3_ERR_SHAPE;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(gemm_sk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess)
+      return check_launch("gemm_sk attr");
+    attr_set = true;
+  }
+  CUtensorMap ta, tb;
+  int st = make_map(&ta, A, kp, M, (int64_t)groups * 8, BM);
+  if (st) return st;
+  st = make_map(&tb, B, kp, N, (int64_t)groups * 8, BN);
+  if (st) return st;
+  const int mt = (int)((M + BM - 1) / BM), nt = (int)((N + BN - 1) / BN);
+  const int64_t nkb = (kp + BK - 1) / BK;
+  const int64_t total = (int64_t)groups * mt * nt * nkb;
+  if (ctas > total) ctas = (int)total;
+  launch_pdl(gemm_sk_kernel, dim3(ctas), dim3(256), SMEM_BYTES, as_stream(stream), ta, tb, C, M, N, kp, ldc, c_group,
+             mt, nt, total, c_layout);
+  return check_launch("ring_gemm_streamk");
 }
 
 int mpc3_ring_gemm_cross(const uint64_t* src_a, int64_t plane_a, const mpc3_operand* op_a, const uint64_t* src_b,

@@ -202,6 +202,23 @@ def test_ring_gemm_column_major_output(splits):
     assert np.array_equal(host(Cm).reshape(Nn, M).T, R.wrap_matmul(a, b))
 
 
+@pytest.mark.parametrize("M,K,Nn,ctas,layout", [(300, 1000, 96, 148, 1), (128, 20000, 64, 37, 0),
+                                                 (1000, 300, 200, 148, 0), (64, 40, 8, 5, 1)])
+def test_ring_gemm_streamk(M, K, Nn, ctas, layout):
+    """Stream-K: equal (tile, K-block) ranges per CTA, segments crossing tile
+    boundaries and the 16384-K exactness cap, partials atomically added."""
+    rng = np.random.default_rng(M + K + Nn)
+    a, b = rnd(rng, (M, K)), rnd(rng, (K, Nn))
+    kp = (K + 15) // 16 * 16
+    A = _pack(dev(a), 0, _capi.dense_operand(M, K, s_r=K, t2=1), 2, kp)
+    B = _pack(dev(b), 0, _capi.dense_operand(Nn, K, s_r=1, t2=Nn), 2, kp)
+    Cm = torch.zeros(M * Nn, dtype=torch.int64, device="cuda")
+    ld = M if layout else Nn
+    _capi.call("mpc3_ring_gemm_streamk", p(A), p(B), p(Cm), 1, M, Nn, kp, ld, M * Nn, ctas, layout, stream())
+    got = host(Cm).reshape(Nn, M).T if layout else host(Cm).reshape(M, Nn)
+    assert np.array_equal(got, R.wrap_matmul(a, b))
+
+
 def test_ring_matmul_u64_convenience():
     rng = np.random.default_rng(3)
     M, K, Nn = 77, 20000, 33
