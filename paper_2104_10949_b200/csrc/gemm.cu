@@ -69,50 +69,45 @@ DEV int pt_swz(int i, int j) { return ((j & ~7) + (((j & 7) + (j >> 3) + (i & 7)
 // Row / column part of the gather offset: {base, y, x, half}.  Columns past
 // the data (zero padding) and rows past the end get y = -2^30, which fails
 // the unsigned bounds check, so no separate flag is tested per element.
-DEV int4 pack_row_part(const Operand& o, int64_t r, int64_t rows) {
-  int64_t b = 0;
-  int32_t y = 0, x = 0;
-  if (r >= rows) return make_int4(0, -(1 << 30), 0, 0);
-  if (o.mode == MPC3_GATHER_DENSE) {
-    b = o.off + r * o.s_r;
-  } else if (o.mode == MPC3_GATHER_IM2COL) {  // r = (n, y, x)
-    int64_t xx = r % o.ow, q = r / o.ow;
-    int64_t yy = q % o.oh, n = q / o.oh;
-    b = n * o.sN;
-    y = (int32_t)(yy * o.sh - o.ph);
-    x = (int32_t)(xx * o.sw - o.pw);
-  } else {  // WGRAD: r = (c, u, v)
-    int64_t v = r % o.kw, q = r / o.kw;
-    int64_t u = q % o.kh, c = q / o.kh;
-    b = c * o.sC;
-    y = (int32_t)(u - o.ph);
-    x = (int32_t)(v - o.pw);
+// (32-bit index arithmetic: the host only routes operands whose rows, K and
+// component planes are below 2^31 here.)
+DEV int4 pack_row_part(const Operand& o, int64_t r64, int64_t rows) {
+  if (r64 >= rows) return make_int4(0, -(1 << 30), 0, 0);
+  const uint32_t r = (uint32_t)r64;
+  if (o.mode == MPC3_GATHER_DENSE) return make_int4((int32_t)(o.off + r64 * o.s_r), 0, 0, 0);
+  if (o.mode == MPC3_GATHER_IM2COL) {  // r = (n, y, x)
+    const uint32_t ow = (uint32_t)o.ow, oh = (uint32_t)o.oh;
+    const uint32_t q = r / ow, xx = r - q * ow;
+    const uint32_t n = q / oh, yy = q - n * oh;
+    return make_int4((int32_t)(n * o.sN), (int32_t)(yy * o.sh - o.ph), (int32_t)(xx * o.sw - o.pw), 0);
   }
-  return make_int4((int32_t)b, y, x, 0);
+  // WGRAD: r = (c, u, v)
+  const uint32_t kw = (uint32_t)o.kw, kh = (uint32_t)o.kh;
+  const uint32_t q = r / kw, v = r - q * kw;
+  const uint32_t c = q / kh, u = q - c * kh;
+  return make_int4((int32_t)(c * o.sC), (int32_t)(u - o.ph), (int32_t)(v - o.pw), 0);
 }
 DEV int4 pack_col_part(const Operand& o, int64_t kk, int64_t K, int64_t lim) {
   if (kk >= lim) return make_int4(0, -(1 << 30), 0, 0);
   const int half = kk >= K ? 1 : 0;
-  const int64_t k = kk - half * K;
-  int64_t b = 0;
-  int32_t y = 0, x = 0;
+  const uint32_t k = (uint32_t)(kk - half * K);
   if (o.mode == MPC3_GATHER_DENSE) {
-    int64_t k2 = k % o.K2, q = k / o.K2;
-    b = (q / o.K1) * o.t0 + (q % o.K1) * o.t1 + k2 * o.t2;
-  } else if (o.mode == MPC3_GATHER_IM2COL) {  // k = (c, u, v)
-    int64_t v = k % o.kw, q = k / o.kw;
-    int64_t u = q % o.kh, c = q / o.kh;
-    b = c * o.sC;
-    y = (int32_t)u;
-    x = (int32_t)v;
-  } else {  // WGRAD: k = (n, y, x)
-    int64_t xx = k % o.ow, q = k / o.ow;
-    int64_t yy = q % o.oh, n = q / o.oh;
-    b = n * o.sN;
-    y = (int32_t)(yy * o.sh);
-    x = (int32_t)(xx * o.sw);
+    const uint32_t K2 = (uint32_t)o.K2, K1 = (uint32_t)o.K1;
+    const uint32_t q = k / K2, k2 = k - q * K2;
+    const uint32_t k0 = q / K1, k1 = q - k0 * K1;
+    return make_int4((int32_t)(k0 * o.t0 + k1 * o.t1 + k2 * o.t2), 0, 0, half);
   }
-  return make_int4((int32_t)b, y, x, half);
+  if (o.mode == MPC3_GATHER_IM2COL) {  // k = (c, u, v)
+    const uint32_t kw = (uint32_t)o.kw, kh = (uint32_t)o.kh;
+    const uint32_t q = k / kw, v = k - q * kw;
+    const uint32_t c = q / kh, u = q - c * kh;
+    return make_int4((int32_t)(c * o.sC), (int32_t)u, (int32_t)v, half);
+  }
+  // WGRAD: k = (n, y, x)
+  const uint32_t ow = (uint32_t)o.ow, oh = (uint32_t)o.oh;
+  const uint32_t q = k / ow, xx = k - q * ow;
+  const uint32_t n = q / oh, yy = q - n * oh;
+  return make_int4((int32_t)(n * o.sN), (int32_t)(yy * o.sh), (int32_t)(xx * o.sw), half);
 }
 
 template <bool R_FAST, int ROLE>
@@ -889,7 +884,8 @@ int mpc3_ring_pack(const uint64_t* src, int64_t src_plane, const mpc3_operand* o
   const bool dilated = o.mode == MPC3_GATHER_IM2COL && (o.dh != 1 || o.dw != 1);
   const int64_t row_tiles = (o.rows + PT_R - 1) / PT_R;
   // the tiled kernel addresses a component plane with 32-bit offsets
-  const bool small = src_plane < (1ll << 31) && o.h < (1 << 30) && o.w < (1 << 30) &&
+  const bool small = src_plane < (1ll << 31) && o.h < (1 << 30) && o.w < (1 << 30) && o.rows < (1ll << 31) &&
+                     o.k < (1ll << 30) &&
                      (o.mode != MPC3_GATHER_DENSE || (o.off >= 0 && o.s_r >= 0 && o.t0 >= 0 && o.t1 >= 0 && o.t2 >= 0));
   if (!dilated && small && row_tiles < 65536) {
     PackTileArgs a;
