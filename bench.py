@@ -250,7 +250,7 @@ def run_b200(args, ws, rank, local):
     def traced_call(name, *a):
         if instrument["on"] and name == "mpc3_ring_pack" and a[3] == 0:
             instrument["k"] = int(a[2]._obj.k)  # logical K of the cross-term operand (inner length 2K)
-        if instrument["on"] and name in ("mpc3_rss_sign", "mpc3_ring_gemm_packed", "mpc3_ring_gemm_packed_layout"):
+        if instrument["on"] and name in ("mpc3_rss_sign", "mpc3_ring_gemm_auto"):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             counting_call(name, *a)

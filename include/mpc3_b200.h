@@ -285,6 +285,14 @@ int mpc3_ring_gemm_packed_layout(const uint8_t* A, const uint8_t* B, uint64_t* C
 int mpc3_ring_gemm_streamk(const uint8_t* A, const uint8_t* B, uint64_t* C, int groups, int64_t M, int64_t N,
                            int64_t kp, int64_t ldc, int64_t c_group, int ctas, int c_layout, void* stream);
 
+/* C[g] = A[g] . B[g]^T with the launch shape chosen for the size: split-K
+ * (exactness above 16384 K, occupancy for few tiles, <= one wave) or
+ * stream-K when that grid would leave SMs idle.  C is dense ([g][M][N], or
+ * [g][N][M] for c_layout 1) and is zeroed here when partial sums are
+ * accumulated atomically. */
+int mpc3_ring_gemm_auto(const uint8_t* A, const uint8_t* B, uint64_t* C, int groups, int64_t M, int64_t N,
+                        int64_t kp, int c_layout, void* stream);
+
 /* The secure layer's per-party cross terms as ONE implicit ring GEMM per
  * party (protocols.py:110-115):
  *   C[g] = [a_g + a_{g+1} | a_g] . [b_g | b_{g+1}]^T,  g = 0, 1, 2,

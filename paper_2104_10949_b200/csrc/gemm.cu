@@ -303,7 +303,20 @@ __global__ void __launch_bounds__(256, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int64_t n0 = (int64_t)blockIdx.x * BN, m0 = (int64_t)blockIdx.y * BM;
+  // grouped rasterisation: consecutive CTAs sweep a band of GROUP_M m-tiles
+  // column by column, so the CTAs resident at once share A and B K-slices in
+  // L2 (row-major order streams all of B once per m-tile row)
+  int64_t n0, m0;
+  {
+    constexpr int GROUP_M = 8;
+    const int nt = gridDim.x, mt = gridDim.y;
+    const int id = blockIdx.y * nt + blockIdx.x;
+    const int band = id / (GROUP_M * nt), first_m = band * GROUP_M;
+    const int gm = mt - first_m < GROUP_M ? mt - first_m : GROUP_M;
+    const int in_band = id - band * GROUP_M * nt;
+    m0 = (int64_t)(first_m + in_band % gm) * BM;
+    n0 = (int64_t)(in_band / gm) * BN;
+  }
   const int g = blockIdx.z / splits, split = blockIdx.z % splits;
   const int nkb_total = (int)((kp + BK - 1) / BK);
   const int kb0 = split * kb_per_split;
@@ -978,6 +991,36 @@ int mpc3_ring_gemm_streamk(const uint8_t* A, const uint8_t* B, uint64_t* C, int 
   return check_launch("ring_gemm_streamk");
 }
 
+int mpc3_ring_gemm_auto(const uint8_t* A, const uint8_t* B, uint64_t* C, int groups, int64_t M, int64_t N,
+                        int64_t kp, int c_layout, void* stream) {
+  if (groups < 1 || M < 0 || N < 0 || kp < 0) return MPC3_ERR_SHAPE;
+  if (kp % 16) return MPC3_ERR_SHAPE;
+  if (c_layout != 0 && c_layout != 1) return MPC3_ERR_CONFIG;
+  if (M == 0 || N == 0) return MPC3_OK;
+  const int64_t sms = 148;
+  const int64_t ldc = c_layout ? M : N, c_group = M * N;
+  const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * groups;
+  const int64_t nkb = (kp + BK - 1) / BK;
+  const int64_t need = (nkb * BK + MAX_SPLIT_K - 1) / MAX_SPLIT_K;  // exactness
+  int64_t occ = sms / tiles;                                         // <= one wave, >= 4 K-blocks per split
+  if (occ > nkb / 4) occ = nkb / 4;
+  if (occ < 1) occ = 1;
+  const int64_t splits = need > occ ? need : occ;
+  const int64_t ctas = tiles * splits;
+  const double eff = (double)ctas / (double)(((ctas + sms - 1) / sms) * sms);
+  const size_t cbytes = (size_t)groups * M * N * 8;
+  if (nkb == 0 || eff < 0.8 || splits > 1) {
+    if (cudaMemsetAsync(C, 0, cbytes, as_stream(stream)) != cudaSuccess) return check_launch("gemm C memset");
+    if (nkb == 0) return MPC3_OK;
+  }
+  if (eff < 0.8) {  // the split-K grid would leave SMs idle: stream-K over every SM
+    int64_t iters = tiles * nkb;
+    int64_t c = iters / 2 < sms ? iters / 2 : sms;
+    return mpc3_ring_gemm_streamk(A, B, C, groups, M, N, kp, ldc, c_group, (int)(c < 1 ? 1 : c), c_layout, stream);
+  }
+  return mpc3_ring_gemm_packed_layout(A, B, C, groups, M, N, kp, ldc, c_group, (int)splits, c_layout, stream);
+}
+
 int mpc3_ring_gemm_cross(const uint64_t* src_a, int64_t plane_a, const mpc3_operand* op_a, const uint64_t* src_b,
                          int64_t plane_b, const mpc3_operand* op_b, uint64_t* C, int64_t ldc, int64_t c_group,
                          int splits, void* stream) {
@@ -1040,12 +1083,7 @@ int mpc3_ring_matmul_u64(const uint64_t* A, const uint64_t* B, uint64_t* C, int6
   if (st) return st;
   st = mpc3_ring_pack(B, 0, &ob, 2, pb, kp, stream);
   if (st) return st;
-  int nkb = (int)((kp + BK - 1) / BK);
-  int splits = (int)((nkb * (int64_t)BK + MAX_SPLIT_K - 1) / MAX_SPLIT_K);
-  if (splits > 1) {
-    if (cudaMemsetAsync(C, 0, (size_t)M * N * 8, as_stream(stream)) != cudaSuccess) return check_launch("memset");
-  }
-  return mpc3_ring_gemm_packed(pa, pb, C, 1, M, N, kp, N, 0, splits, stream);
+  return mpc3_ring_gemm_auto(pa, pb, C, 1, M, N, kp, 0, stream);
 }
 
 }  // extern "C"

@@ -45,8 +45,6 @@ MAX_SPLIT_K = 16384  # per-split K bound of the int8-limb GEMM (exactness of S_3
 # gather variant (gemm_ig_kernel: 3-25x slower on the AlexNet/ResNet shapes,
 # profiles/r01_launches_alexnet_implicit.txt)
 IMPLICIT_GEMM = os.environ.get("MPC3_IMPLICIT_GEMM", "0") == "1"
-# stream-K ring GEMM for layers with fewer than two waves of tiles (MPC3_STREAM_K=0: plain split-K grid)
-STREAM_K = os.environ.get("MPC3_STREAM_K", "1") == "1"
 SMS = 148
 
 
@@ -467,20 +465,8 @@ class TrioSession:
         st = _stream()
         K.call("mpc3_ring_pack", a_src.data_ptr(), a_src.stride(0), C.byref(a_op), 0, A.data_ptr(), kp, st)
         K.call("mpc3_ring_pack", b_src.data_ptr(), b_src.stride(0), C.byref(b_op), 1, B.data_ptr(), kp, st)
-        splits = gemm_splits(M, N, kp, groups=3)
-        tiles = math.ceil(M / 128) * math.ceil(N / 64) * 3
-        ctas = tiles * splits
-        if STREAM_K and ctas / (math.ceil(ctas / SMS) * SMS) < 0.8:
-            # the split-K grid would leave SMs idle (a partial last wave or too few
-            # CTAs): equal (tile, K-block) ranges on every SM instead
-            z = torch.zeros(3 * M * N, dtype=torch.int64, device=_dev())
-            iters = tiles * ((kp + 31) // 32)
-            K.call("mpc3_ring_gemm_streamk", A.data_ptr(), B.data_ptr(), z.data_ptr(), 3, M, N, kp,
-                   M if c_col else N, M * N, max(1, min(SMS, iters // 2)), 1 if c_col else 0, st)
-            return z
-        z = (torch.zeros if splits > 1 else torch.empty)(3 * M * N, dtype=torch.int64, device=_dev())
-        K.call("mpc3_ring_gemm_packed_layout", A.data_ptr(), B.data_ptr(), z.data_ptr(), 3, M, N, kp,
-               M if c_col else N, M * N, splits, 1 if c_col else 0, st)
+        z = torch.empty(3 * M * N, dtype=torch.int64, device=_dev())
+        K.call("mpc3_ring_gemm_auto", A.data_ptr(), B.data_ptr(), z.data_ptr(), 3, M, N, kp, 1 if c_col else 0, st)
         return z
 
     @property
@@ -852,9 +838,8 @@ def plain_conv2d(x: np.ndarray, k: np.ndarray, stride, padding) -> np.ndarray:
     st = _stream()
     K.call("mpc3_ring_pack", dx.data_ptr(), 0, C.byref(a_op), 2, A.data_ptr(), kp, st)
     K.call("mpc3_ring_pack", dk.data_ptr(), 0, C.byref(b_op), 2, B.data_ptr(), kp, st)
-    splits = gemm_splits(M, o, kp, 1)
-    z = (torch.zeros if splits > 1 else torch.empty)(M * o, dtype=torch.int64, device=_dev())
-    K.call("mpc3_ring_gemm_packed", A.data_ptr(), B.data_ptr(), z.data_ptr(), 1, M, o, kp, o, M * o, splits, st)
+    z = torch.empty(M * o, dtype=torch.int64, device=_dev())
+    K.call("mpc3_ring_gemm_auto", A.data_ptr(), B.data_ptr(), z.data_ptr(), 1, M, o, kp, 0, st)
     return to_host(z).reshape(nb, oh, ow, o).transpose(0, 3, 1, 2).copy()
 
 

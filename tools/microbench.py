@@ -65,7 +65,7 @@ def gemm_sweep(sizes):
         Cm = torch.empty(n * n, dtype=torch.int64, device="cuda")
 
         def run():
-            _capi.call("mpc3_ring_gemm_packed", p(A), p(B), p(Cm), 1, n, n, kp, n, 0, 1, st())
+            _capi.call("mpc3_ring_gemm_auto", p(A), p(B), p(Cm), 1, n, n, kp, 0, st())
 
         med, best = timeit(run, iters=5 if n >= 4096 else 10)
         ring_macs = n ** 3
