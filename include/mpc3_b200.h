@@ -133,6 +133,19 @@ int mpc3_rss_mul_truncate(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_a
                           const uint64_t* x, const uint64_t* y, uint64_t* out, uint64_t n, uint64_t elem_off,
                           void* stream);
 
+/* SGD update of every parameter in one launch (nn.py:539-543):
+ * param_i <- param_i - truncate(c * grad_i, bits), in place, tensor i's
+ * truncation words from TRUNC_RHO j_rho and TRUNC_R j_r (the counters its
+ * own truncate call would take).  Trio tensors: 3 planes of n words. */
+#define MPC3_SGD_MAX_TENSORS 64
+typedef struct {
+  uint64_t* param;
+  const uint64_t* grad;
+  uint64_t n, j_rho, j_r;
+} MPC3SgdTensor;
+int mpc3_rss_sgd_multi(const uint32_t* rk3, const uint64_t* ctr, const MPC3SgdTensor* ts, int nt, int bits,
+                       uint64_t c, void* stream);
+
 /* Fused elementwise chain over a per-element trio z (starts as x), the chain
  * input x and a temporary t; replaces the launch-per-call sequences of
  * exp_approx (add_const + squarings, protocols.py:414-424) and reciprocal

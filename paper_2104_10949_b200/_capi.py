@@ -52,6 +52,15 @@ class Operand(C.Structure):
     _fields_ = [("mode", C.c_int)] + _fields_
 
 
+class SgdTensor(C.Structure):
+    """MPC3SgdTensor (include/mpc3_b200.h)."""
+    _fields_ = [("param", C.c_void_p), ("grad", C.c_void_p), ("n", C.c_uint64), ("j_rho", C.c_uint64),
+                ("j_r", C.c_uint64)]
+
+
+SGD_MAX_TENSORS = 64
+
+
 class ChainStep(C.Structure):
     """MPC3ChainStep (include/mpc3_b200.h): one step of a fused elementwise chain."""
     _fields_ = [("op", C.c_int), ("bits", C.c_int), ("c", C.c_uint64)]
@@ -152,6 +161,7 @@ _SIGS = {
     "mpc3_rss_truncate": (C.c_int, [_P, _P, _U64, _U64, C.c_int, _P, _P, _U64, _U64, _P]),
     "mpc3_rss_mul_truncate": (C.c_int, [_P, _P, _U64, _U64, _U64, C.c_int, _P, _P, _P, _U64, _U64, _P]),
     "mpc3_rss_sign": (C.c_int, [_P, _P, C.c_int, _U64, _U64, _U64, _P, _P, _P, _U64, _U64, _U64, _P]),
+    "mpc3_rss_sgd_multi": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, _U64, _P]),
     "mpc3_rss_chain": (C.c_int, [_P, _P, _P, C.c_int, _U64, _U64, _U64, _P, _P, _U64, _U64, _P]),
     "mpc3_rss_bit_inject": (C.c_int, [_P, _P, _U64, _P, _P, _U64, _P]),
     "mpc3_rss_reshare_truncate": (C.c_int, [_P, _P, _U64, _U64, _U64, C.c_int, _P, C.POINTER(View4), _P, _U64,

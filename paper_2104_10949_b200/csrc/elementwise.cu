@@ -345,6 +345,43 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const uint32_t* __re
   }
 }
 
+// SGD on every parameter in one launch (nn.py:539-543, the reference's
+// W <- W - truncate(c * grad) per parameter): tensor i's elements use its own
+// TRUNC_RHO / TRUNC_R counters; the pair space of all tensors is one
+// grid-stride range (prefix sums in the launch parameters).
+struct SgdTable {
+  int nt;
+  MPC3SgdTensor t[MPC3_SGD_MAX_TENSORS];
+  uint64_t pair0[MPC3_SGD_MAX_TENSORS + 1];  // first pair of tensor i in the flattened range
+};
+
+__global__ void __launch_bounds__(kThreads) sgd_kernel(const uint32_t* __restrict__ rk3,
+                                                      const uint64_t* __restrict__ ctr, SgdTable tb, int bits,
+                                                      uint64_t c) {
+  MPC3_AES_SMEM();
+  SmemTables tab = aes_smem_init(sm, rk3, 3);
+  const uint64_t total = tb.pair0[tb.nt];
+  GRID_LOOP(q, total) {
+    int i = 0;
+    while (q >= tb.pair0[i + 1]) ++i;  // few tensors: linear scan
+    const MPC3SgdTensor& T = tb.t[i];
+    const uint64_t b = q - tb.pair0[i], n = T.n;
+    Word2 rho, r;
+    trunc_words(tab, &sm.rk[0][0], resolve(sref(TRUNC_RHO, T.j_rho), ctr), resolve(sref(TRUNC_R, T.j_r), ctr), b, rho,
+                r);
+    for (int e = 0; e < 2; ++e) {
+      const uint64_t f = 2 * b + e;
+      if (f >= n) break;
+      Trio g = load_trio(T.grad, n, f);
+      for (int k = 0; k < 3; ++k) g.c[k] *= c;
+      const Trio v = trio_truncate(g, e ? rho.w1 : rho.w0, e ? r.w1 : r.w0, bits);
+      Trio w = load_trio(T.param, n, f);
+      for (int k = 0; k < 3; ++k) w.c[k] -= v.c[k];
+      store_trio(T.param, n, f, w);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) inject_kernel(const uint32_t* __restrict__ rk3,
                                                          const uint64_t* __restrict__ ctr, StreamRef r0,
                                                          StreamRef r1, const uint64_t* __restrict__ bits,
@@ -523,6 +560,23 @@ int mpc3_rss_mul_truncate(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_a
                           const uint64_t* x, const uint64_t* y, uint64_t* out, uint64_t n, uint64_t elem_off,
                           void* stream) {
   return arith_launch(2, rk3, ctr, j_arith, j_rho, j_r, bits, x, y, out, n, elem_off, stream);
+}
+
+int mpc3_rss_sgd_multi(const uint32_t* rk3, const uint64_t* ctr, const MPC3SgdTensor* ts, int nt, int bits,
+                       uint64_t c, void* stream) {
+  if (!ts || nt < 0 || nt > MPC3_SGD_MAX_TENSORS) return MPC3_ERR_CONFIG;
+  if (bits < 1 || bits > 61) return MPC3_ERR_RANGE;
+  SgdTable tb;
+  tb.nt = nt;
+  tb.pair0[0] = 0;
+  for (int i = 0; i < nt; ++i) {
+    if (ts[i].j_rho >= (1ull << 48) || ts[i].j_r >= (1ull << 48)) return MPC3_ERR_RANGE;
+    tb.t[i] = ts[i];
+    tb.pair0[i + 1] = tb.pair0[i] + (ts[i].n + 1) / 2;
+  }
+  if (tb.pair0[nt] == 0) return MPC3_OK;
+  AES_LAUNCH(sgd_kernel, grid_for(tb.pair0[nt], kThreads), as_stream(stream), rk3, ctr, tb, bits, c);
+  return check_launch("rss_sgd_multi");
 }
 
 int mpc3_rss_chain(const uint32_t* rk3, const uint64_t* ctr, const MPC3ChainStep* steps, int nsteps, uint64_t j_arith,

@@ -199,9 +199,16 @@ class TrioSession:
         self.ledger = Ledger()
         self.ctr = None  # optional device per-purpose counter base (CUDA-graph replay)
         self.dp = None  # DataParallel: this session computes one batch shard
+        self._side = None  # side stream for independent launches (weight gradients)
         self._replicated = 0
 
     # -- data parallelism --
+    def side_stream(self):
+        """A second CUDA stream on this session's device (lazily created)."""
+        if self._side is None:
+            self._side = torch.cuda.Stream(device=_dev())
+        return self._side
+
     def shard_offset(self, numel: int) -> tuple[int, int]:
         """(global word offset of this shard's element 0, global element count)
         of a batch-major tensor whose local part has `numel` elements.  Every
@@ -372,6 +379,28 @@ class TrioSession:
                x.numel, self.shard_offset(x.numel)[0], _stream())
         self._charge_trunc(x.numel)
         return out
+
+    def sgd_inplace(self, params, grads, c: int, bits: int | None = None) -> None:
+        """params[i] -= truncate(mul_const(grads[i], c)) for all i in ONE launch
+        (mpc3_rss_sgd_multi); the counters and accounting are those of the
+        per-parameter truncate calls, in order."""
+        bits = self.fp.t if bits is None else bits
+        if not 1 <= bits <= 61:
+            raise RangeError(f"truncation by {bits} bits outside [1, 61]")
+        for i in range(0, len(params), K.SGD_MAX_TENSORS):
+            chunk = list(zip(params[i:i + K.SGD_MAX_TENSORS], grads[i:i + K.SGD_MAX_TENSORS]))
+            arr = (K.SgdTensor * max(1, len(chunk)))()
+            held = []  # contiguous gradient copies stay alive until the launch
+            for e, (p, g) in enumerate(chunk):
+                if not p.data.is_contiguous() or p.shape != g.shape:
+                    raise ShapeError("in-place SGD needs contiguous parameters of the gradient's shape")
+                g = g.contiguous()
+                held.append(g)
+                jr, jq = self.take(TR_RHO), self.take(TR_R)
+                arr[e].param, arr[e].grad, arr[e].n, arr[e].j_rho, arr[e].j_r = (
+                    p.data.data_ptr(), g.data.data_ptr(), p.numel, jr, jq)
+                self._charge_trunc(p.numel)
+            K.call("mpc3_rss_sgd_multi", self.rk, self.ctr_ptr, arr, len(chunk), bits, int(c) % (1 << 64), _stream())
 
     def mul_truncate(self, x, y, bits=None, label="mul.reshare") -> RssTensor:
         """truncate(mul(x, y)) in one launch; same counters and accounting."""

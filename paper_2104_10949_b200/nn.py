@@ -17,9 +17,11 @@ results — and per-party shares — are bit-identical to the reference.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
+import torch
 
 from . import engine as E
 from .engine import ReciprocalConfig, RssTensor, TrioSession
@@ -36,6 +38,8 @@ FLATTEN = "Flatten"
 # composed from its primitives: bias = local add after the truncation,
 # residual = local add of two branches, padded avg-pool = zero pad + avg-pool)
 RESIDUAL = "Residual"
+# MPC3_OVERLAP=0: weight gradients on the main stream (no side-stream overlap)
+OVERLAP = os.environ.get("MPC3_OVERLAP", "1") == "1"
 
 
 def _pair(v) -> tuple:
@@ -277,19 +281,41 @@ class TrioNet:
         plist = [i for i, s in enumerate(model.layers) if s.kind in (CONV2D, FULLY_CONNECTED)]
         grads = [None] * len(plist)
         pi, g = len(plist), grad_out
+        # The weight gradient of a layer and the input-gradient chain below it
+        # are independent: wgrads run on a side stream (forked from the main
+        # stream once g is ready) while the chain continues on the main stream.
+        # Counters are taken on the host in program order, so results, shares
+        # and accounting are unchanged; the inputs of each side-stream launch
+        # stay referenced until the join (no allocator reuse under it).
+        main = torch.cuda.current_stream()
+        side = S.side_stream() if OVERLAP else None
+        keep = []
+
+        def wgrad(fn, *args):
+            if side is None:
+                return fn(*args)
+            ev = torch.cuda.Event()
+            ev.record(main)
+            side.wait_event(ev)
+            keep.append(args)
+            with torch.cuda.stream(side):
+                return fn(*args)
+
         for li in range(len(model.layers) - 1, -1, -1):
             spec, cached = model.layers[li], acts[li]
             if spec.kind == FULLY_CONNECTED:
                 x, w = cached
                 pi -= 1
-                grads[pi] = S.matmul(g.apply(lambda d: d.transpose(1, 2)), x, bits=t + batch_bits, wgrad=True)
+                grads[pi] = wgrad(lambda gg, xx: S.matmul(gg.apply(lambda d: d.transpose(1, 2)), xx,
+                                                          bits=t + batch_bits, wgrad=True), g, x)
                 if li == plist[0]:
                     break
                 g = S.matmul(g, w)
             elif spec.kind == CONV2D:
                 x, k = cached
                 pi -= 1
-                grads[pi] = S.conv2d_wgrad(x, g, spec.kernel, spec.stride, spec.padding, bits=t + batch_bits)
+                grads[pi] = wgrad(lambda xx, gg: S.conv2d_wgrad(xx, gg, spec.kernel, spec.stride, spec.padding,
+                                                                bits=t + batch_bits), x, g)
                 if li == plist[0]:
                     break
                 g = S.conv2d_dgrad(g, k, spec.stride, spec.padding, x.shape, bits=t)
@@ -299,6 +325,9 @@ class TrioNet:
                 g = S.mul(g, cached[0], "mul.mask")
             elif spec.kind == FLATTEN:
                 g = g.contiguous().reshape(cached[0])
+        if side is not None:
+            main.wait_stream(side)
+        del keep
         return grads
 
     def sgd(self, params: list, grads: list, lr: float, inplace: bool = False) -> list:
@@ -310,6 +339,9 @@ class TrioNet:
             return list(params)
         S = self.s
         with S.replicated():  # parameters are replicated, not batch-sharded
+            if inplace:  # every parameter in one launch, in place
+                S.sgd_inplace(params, grads, c)
+                return list(params)
             return [S.sub(p, S.truncate(S.mul_const(g, c)), out=p if inplace else None)
                     for p, g in zip(params, grads)]
 
