@@ -45,6 +45,8 @@ MAX_SPLIT_K = 16384  # per-split K bound of the int8-limb GEMM (exactness of S_3
 # gather variant (gemm_ig_kernel: 3-25x slower on the AlexNet/ResNet shapes,
 # profiles/r01_launches_alexnet_implicit.txt)
 IMPLICIT_GEMM = os.environ.get("MPC3_IMPLICIT_GEMM", "0") == "1"
+# MPC3_OVERLAP_PACK=0: pack both GEMM operands on the calling stream
+OVERLAP_PACK = os.environ.get("MPC3_OVERLAP_PACK", "1") == "1"
 SMS = 148
 
 
@@ -200,9 +202,16 @@ class TrioSession:
         self.ctr = None  # optional device per-purpose counter base (CUDA-graph replay)
         self.dp = None  # DataParallel: this session computes one batch shard
         self._side = None  # side stream for independent launches (weight gradients)
+        self._pack = None  # stream for the B-operand pack of a GEMM
         self._replicated = 0
 
     # -- data parallelism --
+    def pack_stream(self):
+        """The stream that packs a GEMM's B operand while A packs (lazily created)."""
+        if self._pack is None:
+            self._pack = torch.cuda.Stream(device=_dev())
+        return self._pack
+
     def side_stream(self):
         """A second CUDA stream on this session's device (lazily created)."""
         if self._side is None:
@@ -492,8 +501,22 @@ class TrioSession:
         A = torch.empty(3 * 8 * M * kp, dtype=torch.uint8, device=_dev())
         B = torch.empty(3 * 8 * N * kp, dtype=torch.uint8, device=_dev())
         st = _stream()
-        K.call("mpc3_ring_pack", a_src.data_ptr(), a_src.stride(0), C.byref(a_op), 0, A.data_ptr(), kp, st)
-        K.call("mpc3_ring_pack", b_src.data_ptr(), b_src.stride(0), C.byref(b_op), 1, B.data_ptr(), kp, st)
+        # the two operand packs are independent: B on the pack stream, A here
+        main = torch.cuda.current_stream()
+        ps = self.pack_stream() if OVERLAP_PACK else None
+        if ps is not None and ps != main:
+            ev = torch.cuda.Event()
+            ev.record(main)
+            ps.wait_event(ev)
+            K.call("mpc3_ring_pack", b_src.data_ptr(), b_src.stride(0), C.byref(b_op), 1, B.data_ptr(), kp,
+                   ps.cuda_stream)
+            K.call("mpc3_ring_pack", a_src.data_ptr(), a_src.stride(0), C.byref(a_op), 0, A.data_ptr(), kp, st)
+            ev2 = torch.cuda.Event()
+            ev2.record(ps)
+            main.wait_event(ev2)
+        else:
+            K.call("mpc3_ring_pack", a_src.data_ptr(), a_src.stride(0), C.byref(a_op), 0, A.data_ptr(), kp, st)
+            K.call("mpc3_ring_pack", b_src.data_ptr(), b_src.stride(0), C.byref(b_op), 1, B.data_ptr(), kp, st)
         z = torch.empty(3 * M * N, dtype=torch.int64, device=_dev())
         K.call("mpc3_ring_gemm_auto", A.data_ptr(), B.data_ptr(), z.data_ptr(), 3, M, N, kp, 1 if c_col else 0, st)
         return z
