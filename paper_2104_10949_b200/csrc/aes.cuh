@@ -130,7 +130,10 @@ HD void aes128_block(const T& tab, const uint32_t* rk, uint32_t& s0, uint32_t& s
 
 #if defined(__CUDACC__)
 struct SmemTables;
+struct SmemTables4;
 HD void aes128_block(const SmemTables& tab, const uint32_t* rk, uint32_t& s0, uint32_t& s1, uint32_t& s2,
+                     uint32_t& s3);
+HD void aes128_block(const SmemTables4& tab, const uint32_t* rk, uint32_t& s0, uint32_t& s1, uint32_t& s2,
                      uint32_t& s3);
 #endif
 
@@ -198,6 +201,16 @@ __constant__ Te0Table c_te0 = make_te0();
 // (ror distributes over xor): 16 PRMT + 16 LDS + 16 logic ops per round.
 struct SmemTables {
   uint32_t hl;  // (shared window base & 0xff000000) | 4 * lane
+  static constexpr bool kFour = false;
+};
+// Four-table variant (128 KiB): a second 64 KiB region holds Te2 / Te3 with
+// the same entry layout, so Te2[x] and Te3[x] are the same PRMT address plus
+// 0x10000 (+128): a column is Te0[a] ^ Te1[b] ^ Te2[c] ^ Te3[d] ^ k with no
+// rotation — 4 fewer ALU ops per round, for the kernels that are nothing but
+// AES (one 512-thread CTA per SM).
+struct SmemTables4 {
+  uint32_t hl;
+  static constexpr bool kFour = true;
 };
 
 struct __align__(16) AesSmem {
@@ -206,6 +219,12 @@ struct __align__(16) AesSmem {
   uint64_t extra[16];  // per-kernel uniform data (stream heads)
 };
 constexpr int kAesSmemBytes = (int)sizeof(AesSmem);
+struct __align__(16) AesSmem4 {
+  uint32_t te[2][256 * 64];
+  uint32_t rk[3][44];
+  uint64_t extra[16];
+};
+constexpr int kAesSmem4Bytes = (int)sizeof(AesSmem4);
 constexpr uint32_t kAesTableOff = 1024;
 
 // The protocol kernels' dynamic shared memory: an AesSmem at offset 0 (these
@@ -222,6 +241,16 @@ DEV uint32_t lds_te1(uint32_t a) {
   asm("ld.shared.u32 %0, [%1+1152];" : "=r"(v) : "r"(a));
   return v;
 }
+DEV uint32_t lds_te2(uint32_t a) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1+66560];" : "=r"(v) : "r"(a));
+  return v;
+}
+DEV uint32_t lds_te3(uint32_t a) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1+66688];" : "=r"(v) : "r"(a));
+  return v;
+}
 
 #define MPC3_I3(x) __byte_perm((x), hl, 0x7634)
 #define MPC3_I2(x) __byte_perm((x), hl, 0x7624)
@@ -229,17 +258,20 @@ DEV uint32_t lds_te1(uint32_t a) {
 #define MPC3_I0(x) __byte_perm((x), hl, 0x7604)
 // one output column of rounds 1-9
 #define MPC3_COL(a, b, c, d, kk)                                                                     \
-  (lds_te0(MPC3_I3(a)) ^ lds_te1(MPC3_I2(b)) ^                                                       \
-   __byte_perm(lds_te0(MPC3_I1(c)) ^ lds_te1(MPC3_I0(d)), 0, 0x1032) ^ (kk))
+  (FOUR ? (lds_te0(MPC3_I3(a)) ^ lds_te1(MPC3_I2(b)) ^ lds_te2(MPC3_I1(c)) ^ lds_te3(MPC3_I0(d)) ^ (kk)) \
+        : (lds_te0(MPC3_I3(a)) ^ lds_te1(MPC3_I2(b)) ^                                               \
+           __byte_perm(lds_te0(MPC3_I1(c)) ^ lds_te1(MPC3_I0(d)), 0, 0x1032) ^ (kk)))
 // final round column: S[x] is byte 2 (and 1) of Te0[x] = (2S, S, S, 3S)
 #define MPC3_FIN(a, b, c, d, kk)                                                                     \
   (__byte_perm(__byte_perm(lds_te0(MPC3_I3(a)), lds_te0(MPC3_I2(b)), 0x2600),                        \
                __byte_perm(lds_te0(MPC3_I1(c)), lds_te0(MPC3_I0(d)), 0x0015), 0x3254) ^                \
    (kk))
 
-HD void aes128_block(const SmemTables& tab, const uint32_t* rk, uint32_t& s0, uint32_t& s1, uint32_t& s2,
-                     uint32_t& s3) {
+template <class TT>
+HD void aes128_block_dev(const TT& tab, const uint32_t* rk, uint32_t& s0, uint32_t& s1, uint32_t& s2,
+                          uint32_t& s3) {
 #if defined(__CUDA_ARCH__)
+  constexpr bool FOUR = TT::kFour;
   const uint32_t hl = tab.hl;
   s0 ^= rk[0];
   s1 ^= rk[1];
@@ -268,12 +300,21 @@ HD void aes128_block(const SmemTables& tab, const uint32_t* rk, uint32_t& s0, ui
   s3 = t3;
 #endif
 }
+HD void aes128_block(const SmemTables& tab, const uint32_t* rk, uint32_t& s0, uint32_t& s1, uint32_t& s2,
+                     uint32_t& s3) {
+  aes128_block_dev(tab, rk, s0, s1, s2, s3);
+}
+HD void aes128_block(const SmemTables4& tab, const uint32_t* rk, uint32_t& s0, uint32_t& s1, uint32_t& s2,
+                     uint32_t& s3) {
+  aes128_block_dev(tab, rk, s0, s1, s2, s3);
+}
 
 // NB independent blocks interleaved round by round (key schedule of block i
 // at rks[i]): the independent dependency chains multiply the instruction-
 // level parallelism of the table rounds.
-template <int NB>
-DEV void aes128_multi(const SmemTables& tab, const uint32_t* const rks[NB], uint32_t s[NB][4]) {
+template <int NB, class TT>
+DEV void aes128_multi(const TT& tab, const uint32_t* const rks[NB], uint32_t s[NB][4]) {
+  constexpr bool FOUR = TT::kFour;
   const uint32_t hl = tab.hl;
 #pragma unroll
   for (int i = 0; i < NB; ++i)
@@ -307,7 +348,8 @@ DEV void aes128_multi(const SmemTables& tab, const uint32_t* const rks[NB], uint
 
 // Three blocks with the same counter under k_0, k_1, k_2: every zero share
 // needs all three keys' words at one position (sharing.py:233-250).
-DEV void aes128_block3(const SmemTables& tab, const uint32_t* rk3, uint32_t s[3][4]) {
+template <class TT>
+DEV void aes128_block3(const TT& tab, const uint32_t* rk3, uint32_t s[3][4]) {
   const uint32_t* rks[3] = {rk3, rk3 + 44, rk3 + 88};
   aes128_multi<3>(tab, rks, s);
 }
@@ -342,7 +384,29 @@ __device__ inline SmemTables aes_smem_init(AesSmem& sm, const uint32_t* __restri
   return t;
 }
 
+// Four-table expansion (Te0/Te1 in region 0, Te2/Te3 = ror16 of them in region 1).
+__device__ inline SmemTables4 aes_smem_init4(AesSmem4& sm, const uint32_t* __restrict__ rk_dev, int nkeys) {
+  griddep_launch();
+  uint4* dst = reinterpret_cast<uint4*>(&sm.te[0][0]);
+  for (int i = threadIdx.x; i < 2 * 256 * 16; i += blockDim.x) {
+    const int e = i & (256 * 16 - 1);
+    uint32_t v = c_te0.v[e >> 4];
+    const int rot = ((e & 8) ? 8 : 0) + (i >= 256 * 16 ? 16 : 0);  // Te1 / Te2 / Te3 = ror 8 / 16 / 24
+    v = __funnelshift_r(v, v, rot);
+    dst[i] = make_uint4(v, v, v, v);
+  }
+  for (int i = threadIdx.x; i < nkeys * 44; i += blockDim.x) (&sm.rk[0][0])[i] = rk_dev[i];
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(mpc3_dsm);
+  if ((base & 0x00ffffffu) != kAesTableOff) __trap();
+  __syncthreads();
+  griddep_wait();
+  SmemTables4 t;
+  t.hl = (base & 0xff000000u) | ((threadIdx.x & 31) * 4);
+  return t;
+}
+
 #define MPC3_AES_SMEM() AesSmem& sm = *reinterpret_cast<AesSmem*>(mpc3_dsm)
+#define MPC3_AES_SMEM4() AesSmem4& sm = *reinterpret_cast<AesSmem4*>(mpc3_dsm)
 #endif
 
 }  // namespace mpc3

@@ -22,6 +22,7 @@ void set_last_error(const char* msg) {
 }
 
 constexpr int kThreads = 256;
+constexpr int kSignThreads = 512;  // four-table AES kernels: one CTA per SM
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = getenv("MPC3_PDL");
@@ -82,11 +83,11 @@ HD StreamRef sref(uint32_t purpose, uint64_t j) {
 // ---------------------------------------------------------------------------
 // PRF streams
 
-__global__ void __launch_bounds__(kThreads) prf_words_kernel(const uint32_t* __restrict__ rk_dev,
-                                                            StreamHead h, uint64_t word_off,
-                                                            uint64_t count, uint64_t* __restrict__ out) {
-  MPC3_AES_SMEM();
-  SmemTables tab = aes_smem_init(sm, rk_dev, 1);
+__global__ void __launch_bounds__(kSignThreads, 1) prf_words_kernel(const uint32_t* __restrict__ rk_dev,
+                                                                   StreamHead h, uint64_t word_off,
+                                                                   uint64_t count, uint64_t* __restrict__ out) {
+  MPC3_AES_SMEM4();
+  SmemTables4 tab = aes_smem_init4(sm, rk_dev, 1);
   uint64_t nblk = ((word_off + count - 1) >> 1) - (word_off >> 1) + 1;
   GRID_LOOP(t, nblk) prf_words_item(tab, sm.rk[0], h, word_off, count, out, t);
 }
@@ -164,16 +165,15 @@ struct SignArgs {
   uint64_t jbin, jxor, ja;
 };
 
-#ifndef MPC3_SIGN_MINB
-#define MPC3_SIGN_MINB 2  // CTAs per SM the register budget targets (2: 128 regs, no spill)
-#endif
-__global__ void __launch_bounds__(kThreads, MPC3_SIGN_MINB) sign_kernel(const uint32_t* __restrict__ rk3,
+// Large tensors: one 512-thread CTA per SM with the four-table AES layout
+// (128 KiB) — the kernel is nothing but AES rounds.
+__global__ void __launch_bounds__(kSignThreads, 1) sign_kernel(const uint32_t* __restrict__ rk3,
                                                           const uint64_t* __restrict__ ctr, SignArgs args,
                                                           int mode, const uint64_t* __restrict__ x,
                                                           uint64_t* __restrict__ out,
                                                           uint64_t* __restrict__ mask, uint64_t n,
                                                           uint64_t n_total, uint64_t elem_off) {
-  MPC3_AES_SMEM();
+  MPC3_AES_SMEM4();
   static_assert(sizeof(SignStreams) <= sizeof(sm.extra), "stream heads fit the AesSmem extra area");
   SignStreams& st = *reinterpret_cast<SignStreams*>(sm.extra);  // uniform stream heads, indexed by level
   if (threadIdx.x == 0) {
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(kThreads, MPC3_SIGN_MINB) sign_kernel(const ui
     for (int l = 0; l < 7; ++l) st.x[l] = resolve(sref(XOR_ZERO, args.jxor + l), ctr);
     for (int l = 0; l < 3; ++l) st.a[l] = resolve(sref(ARITH_ZERO, args.ja + l), ctr);
   }
-  SmemTables tab = aes_smem_init(sm, rk3, 3);  // includes the barrier
+  SmemTables4 tab = aes_smem_init4(sm, rk3, 3);  // includes the barrier
   GRID_LOOP(b, (n + 1) >> 1) sign_item(tab, &sm.rk[0][0], st, mode, x, out, mask, n, n_total, elem_off, b);
 }
 
@@ -495,8 +495,9 @@ int mpc3_prf_words(const uint32_t* rk, uint32_t purpose, uint64_t index, uint64_
   if (st) return st;
   if (count == 0) return MPC3_OK;
   uint64_t nblk = ((word_off + count - 1) >> 1) - (word_off >> 1) + 1;
-  AES_LAUNCH(prf_words_kernel, grid_for(nblk, kThreads), as_stream(stream), 
-      rk, stream_head(purpose, index), word_off, count, words);
+  if (!aes_attr((const void*)prf_words_kernel, kAesSmem4Bytes)) return check_launch("prf smem attribute");
+  launch_pdl(prf_words_kernel, dim3(grid_for(nblk, kSignThreads, 8)), dim3(kSignThreads), kAesSmem4Bytes,
+             as_stream(stream), rk, stream_head(purpose, index), word_off, count, words);
   return check_launch("prf_words");
 }
 
@@ -640,8 +641,9 @@ int mpc3_rss_sign(const uint32_t* rk3, const uint64_t* ctr, int mode, uint64_t j
                n_total, elem_off, P);
     return check_launch("rss_sign2");
   }
-  AES_LAUNCH(sign_kernel, grid_for((n + 1) / 2, kThreads, 16), as_stream(stream), 
-      rk3, ctr, a, mode, x, out, mask, n, n_total, elem_off);
+  if (!aes_attr((const void*)sign_kernel, kAesSmem4Bytes)) return check_launch("sign smem attribute");
+  launch_pdl(sign_kernel, dim3(grid_for((n + 1) / 2, kSignThreads, 8)), dim3(kSignThreads), kAesSmem4Bytes,
+             as_stream(stream), rk3, ctr, a, mode, x, out, mask, n, n_total, elem_off);
   return check_launch("rss_sign");
 }
 

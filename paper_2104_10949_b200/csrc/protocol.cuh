@@ -105,7 +105,8 @@ HD void prf_block3(const T& tab, const uint32_t* rk3, StreamHead h, uint64_t blk
   for (int i = 0; i < 3; ++i) w[i] = prf_block(tab, rk3 + 44 * i, h, blk);
 }
 #if defined(__CUDACC__)
-HD void prf_block3(const SmemTables& tab, const uint32_t* rk3, StreamHead h, uint64_t blk, Word2 w[3]) {
+template <class TT>
+HD void prf_block3_dev(const TT& tab, const uint32_t* rk3, StreamHead h, uint64_t blk, Word2 w[3]) {
 #if defined(__CUDA_ARCH__)
   uint32_t s[3][4];
 #pragma unroll
@@ -122,6 +123,12 @@ HD void prf_block3(const SmemTables& tab, const uint32_t* rk3, StreamHead h, uin
     w[i].w1 = (uint64_t)bswap32(s[i][2]) | ((uint64_t)bswap32(s[i][3]) << 32);
   }
 #endif
+}
+HD void prf_block3(const SmemTables& tab, const uint32_t* rk3, StreamHead h, uint64_t blk, Word2 w[3]) {
+  prf_block3_dev(tab, rk3, h, blk, w);
+}
+HD void prf_block3(const SmemTables4& tab, const uint32_t* rk3, StreamHead h, uint64_t blk, Word2 w[3]) {
+  prf_block3_dev(tab, rk3, h, blk, w);
 }
 #endif
 
