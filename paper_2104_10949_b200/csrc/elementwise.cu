@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kSignThreads, 1) sign_kernel(const uint32_t* _
                                                           int mode, const uint64_t* __restrict__ x,
                                                           uint64_t* __restrict__ out,
                                                           uint64_t* __restrict__ mask, uint64_t n,
-                                                          uint64_t n_total, uint64_t elem_off) {
+                                                          uint64_t n_total, uint64_t elem_off, uint64_t plane) {
   MPC3_AES_SMEM4();
   static_assert(sizeof(SignStreams) <= sizeof(sm.extra), "stream heads fit the AesSmem extra area");
   SignStreams& st = *reinterpret_cast<SignStreams*>(sm.extra);  // uniform stream heads, indexed by level
@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(kSignThreads, 1) sign_kernel(const uint32_t* _
     for (int l = 0; l < 3; ++l) st.a[l] = resolve(sref(ARITH_ZERO, args.ja + l), ctr);
   }
   SmemTables4 tab = aes_smem_init4(sm, rk3, 3);  // includes the barrier
-  GRID_LOOP(b, (n + 1) >> 1) sign_item(tab, &sm.rk[0][0], st, mode, x, out, mask, n, n_total, elem_off, b);
+  GRID_LOOP(b, (n + 1) >> 1) sign_item(tab, &sm.rk[0][0], st, mode, x, out, mask, n, n_total, elem_off, b, plane);
 }
 
 // Two-phase sign circuit.  The 46 AES blocks an element pair consumes do not
@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(kThreads, 2) sign2_kernel(const uint32_t* __re
                                                            const uint64_t* __restrict__ ctr, SignArgs args, int mode,
                                                            const uint64_t* __restrict__ x, uint64_t* __restrict__ out,
                                                            uint64_t* __restrict__ mask, uint64_t n, uint64_t n_total,
-                                                           uint64_t elem_off, int P) {
+                                                           uint64_t elem_off, int P, uint64_t plane) {
   MPC3_AES_SMEM();
   SignStreams& st = *reinterpret_cast<SignStreams*>(sm.extra);
   if (threadIdx.x == 0) {
@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, 2) sign2_kernel(const uint32_t* __re
       rp.P = P;
       rp.p = threadIdx.x;
       rp.slot = 0;
-      sign_item(rp, &sm.rk[0][0], st, mode, x, out, mask, n, n_total, elem_off, c0 + threadIdx.x);
+      sign_item(rp, &sm.rk[0][0], st, mode, x, out, mask, n, n_total, elem_off, c0 + threadIdx.x, plane);
     }
     __syncthreads();
   }
@@ -626,25 +626,38 @@ int mpc3_rss_sign(const uint32_t* rk3, const uint64_t* ctr, int mode, uint64_t j
   a.jxor = j_xor;
   a.ja = j_arith;
   // large tensors: the single-phase kernel (throughput-bound, all threads in
-  // the circuit); small ones: the two-phase kernel (latency-bound launches)
-  if (!g_sign_fused && (n + 1) / 2 <= kSign2MaxPairs) {
+  // the circuit) on a persistent grid, one 512-thread CTA per SM, every
+  // thread exactly k pairs (no partial wave, no CTA-boundary bubbles); the
+  // remainder and small tensors: the two-phase kernel (latency-bound work)
+  const uint64_t pairs = (n + 1) / 2;
+  const uint64_t persist = 148ull * kSignThreads;
+  uint64_t main_pairs = 0;
+  if (!g_sign_fused && pairs > kSign2MaxPairs) main_pairs = pairs / persist * persist;
+  if (g_sign_fused) main_pairs = pairs;
+  if (main_pairs) {
+    const uint64_t nm = main_pairs == pairs ? n : 2 * main_pairs;
+    const unsigned grid = g_sign_fused ? grid_for(pairs, kSignThreads, 8) : 148;
+    if (!aes_attr((const void*)sign_kernel, kAesSmem4Bytes)) return check_launch("sign smem attribute");
+    launch_pdl(sign_kernel, dim3(grid), dim3(kSignThreads), kAesSmem4Bytes, as_stream(stream), rk3, ctr, a, mode, x,
+               out, mask, nm, n_total, elem_off, n);
+    if (check_launch("rss_sign")) return MPC3_ERR_CUDA;
+  }
+  if (main_pairs < pairs) {
     // two-phase kernel: P pairs per chunk (64; 32 when the p-half straddles
     // blocks), tables + keystream slots in dynamic shared memory
+    const uint64_t e0 = 2 * main_pairs, nr = n - e0;
     const bool straddle = (n_total & 1) != 0;
     const int P = straddle ? 32 : 64;
     const int smem = kAesSmemBytes + P * sign_slots(straddle) * SW_SLOT_BYTES;
     if (!aes_attr((const void*)sign2_kernel, kAesSmemBytes + 64 * sign_slots(false) * SW_SLOT_BYTES))
       return check_launch("sign2 smem attribute");
-    uint64_t chunks = ((n + 1) / 2 + P - 1) / P;
+    uint64_t chunks = ((nr + 1) / 2 + P - 1) / P;
     unsigned grid = (unsigned)(chunks < 148 * 2 * 8 ? chunks : 148 * 2 * 8);
-    launch_pdl(sign2_kernel, dim3(grid), dim3(kThreads), smem, as_stream(stream), rk3, ctr, a, mode, x, out, mask, n,
-               n_total, elem_off, P);
+    launch_pdl(sign2_kernel, dim3(grid), dim3(kThreads), smem, as_stream(stream), rk3, ctr, a, mode, x + e0, out + e0,
+               mask ? mask + e0 : mask, nr, n_total, elem_off + e0, P, n);
     return check_launch("rss_sign2");
   }
-  if (!aes_attr((const void*)sign_kernel, kAesSmem4Bytes)) return check_launch("sign smem attribute");
-  launch_pdl(sign_kernel, dim3(grid_for((n + 1) / 2, kSignThreads, 8)), dim3(kSignThreads), kAesSmem4Bytes,
-             as_stream(stream), rk3, ctr, a, mode, x, out, mask, n, n_total, elem_off);
-  return check_launch("rss_sign");
+  return MPC3_OK;
 }
 
 int mpc3_rss_bit_inject(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, const uint64_t* bits, uint64_t* out,

@@ -77,23 +77,27 @@ HD void arith_item(const T& tab, const uint32_t* rk3, int kind, StreamHead ha, S
   if (two) store_trio(out, n, 2 * b + 1, v[1]);
 }
 
+// plane: component stride of x / out / mask (0: n, the tensor is the whole
+// range; a launch over a sub-range of a larger tensor passes the full plane).
 template <class T>
 HD void sign_item(const T& tab, const uint32_t* rk3, const SignStreams& st, int mode, const uint64_t* x,
-                  uint64_t* out, uint64_t* mask, uint64_t n, uint64_t n_total, uint64_t elem_off, uint64_t b) {
+                  uint64_t* out, uint64_t* mask, uint64_t n, uint64_t n_total, uint64_t elem_off, uint64_t b,
+                  uint64_t plane = 0) {
+  const uint64_t pl = plane ? plane : n;
   bool two = 2 * b + 1 < n;
   Trio o[2], m[2];
   struct Loader {
     const uint64_t* x;
-    uint64_t n, e0;
+    uint64_t pl, e0;
     bool two;
-    HD Trio operator()(int e) const { return load_trio(x, n, (e && two) ? e0 + 1 : e0); }
-  } ld{x, n, 2 * b, two};
+    HD Trio operator()(int e) const { return load_trio(x, pl, (e && two) ? e0 + 1 : e0); }
+  } ld{x, pl, 2 * b, two};
   sign_circuit_pair(tab, rk3, st, n_total, (elem_off >> 1) + b, mode, ld, o, m);
-  store_trio(out, n, 2 * b, o[0]);
-  if (two) store_trio(out, n, 2 * b + 1, o[1]);
+  store_trio(out, pl, 2 * b, o[0]);
+  if (two) store_trio(out, pl, 2 * b + 1, o[1]);
   if (mode == MODE_RELU && mask) {
-    store_trio(mask, n, 2 * b, m[0]);
-    if (two) store_trio(mask, n, 2 * b + 1, m[1]);
+    store_trio(mask, pl, 2 * b, m[0]);
+    if (two) store_trio(mask, pl, 2 * b + 1, m[1]);
   }
 }
 
