@@ -22,7 +22,7 @@ void set_last_error(const char* msg) {
 }
 
 constexpr int kThreads = 256;
-constexpr int kSignThreads = 512;  // four-table AES kernels: one CTA per SM
+constexpr int kSignThreads = 384;  // four-table AES kernels: one CTA per SM
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = getenv("MPC3_PDL");
