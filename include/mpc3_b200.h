@@ -217,6 +217,14 @@ int mpc3_rss_col2im_reshare_truncate(const uint32_t* rk3, const uint64_t* ctr, u
                                      uint64_t j_r, int bits, const uint64_t* z, int64_t N, int64_t C, int64_t OH,
                                      int64_t OW, int kh, int kw, int sh, int sw, int ph, int pw, int64_t H,
                                      int64_t W, uint64_t* out, uint64_t elem_off, void* stream);
+/* Same with z's layout chosen: z_layout 1 = column-major cols (element
+ * ((n,y,x), (c,a,b)) at ((c*kh+a)*kw+b) * N*OH*OW + (n*OH+y)*OW + x, the
+ * GEMM's c_layout 1), so a warp's gathers for consecutive x coalesce. */
+int mpc3_rss_col2im_reshare_truncate_layout(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith,
+                                            uint64_t j_rho, uint64_t j_r, int bits, const uint64_t* z, int z_layout,
+                                            int64_t N, int64_t C, int64_t OH, int64_t OW, int kh, int kw, int sh,
+                                            int sw, int ph, int pw, int64_t H, int64_t W, uint64_t* out,
+                                            uint64_t elem_off, void* stream);
 
 /* avgpool (protocols.py:139-159): window sums, then truncate(log2 area) when
  * the area is a power of two, else mul_const(mulc) + truncate(t).  x/out are

@@ -174,6 +174,9 @@ _SIGS = {
     "mpc3_rss_col2im_reshare_truncate": (C.c_int, [_P, _P, _U64, _U64, _U64, C.c_int, _P, _I64, _I64, _I64, _I64,
                                                    C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _I64,
                                                    _I64, _P, _U64, _P]),
+    "mpc3_rss_col2im_reshare_truncate_layout": (C.c_int, [_P, _P, _U64, _U64, _U64, C.c_int, _P, C.c_int, _I64, _I64,
+                                                          _I64, _I64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                                          C.c_int, _I64, _I64, _P, _U64, _P]),
     "mpc3_ring_sumpool": (C.c_int, [_P, _P, _I64, _I64, _I64, _I64, C.c_int, C.c_int, C.c_int, C.c_int, _P]),
     "mpc3_ring_pack": (C.c_int, [_P, _I64, C.POINTER(Operand), C.c_int, _P, _I64, _P]),
     "mpc3_ring_gemm_packed": (C.c_int, [_P, _P, _P, C.c_int, _I64, _I64, _I64, _I64, _I64, C.c_int, _P]),

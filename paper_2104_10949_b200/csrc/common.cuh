@@ -42,6 +42,8 @@ DEV void griddep_wait() {
 }
 #endif
 
+HD int32_t imin32(int32_t a, int32_t b) { return a < b ? a : b; }
+
 // Arithmetic right shift of the two's-complement view (ring.py:75-79).
 HD uint64_t sar(uint64_t v, int bits) { return (uint64_t)(((int64_t)v) >> bits); }
 

@@ -737,12 +737,23 @@ int mpc3_rss_col2im_reshare_truncate(const uint32_t* rk3, const uint64_t* ctr, u
                                      uint64_t j_r, int bits, const uint64_t* z, int64_t N, int64_t C, int64_t OH,
                                      int64_t OW, int kh, int kw, int sh, int sw, int ph, int pw, int64_t H,
                                      int64_t W, uint64_t* out, uint64_t elem_off, void* stream) {
+  return mpc3_rss_col2im_reshare_truncate_layout(rk3, ctr, j_arith, j_rho, j_r, bits, z, 0, N, C, OH, OW, kh, kw, sh,
+                                                 sw, ph, pw, H, W, out, elem_off, stream);
+}
+
+int mpc3_rss_col2im_reshare_truncate_layout(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith,
+                                            uint64_t j_rho, uint64_t j_r, int bits, const uint64_t* z, int z_layout,
+                                            int64_t N, int64_t C, int64_t OH, int64_t OW, int kh, int kw, int sh,
+                                            int sw, int ph, int pw, int64_t H, int64_t W, uint64_t* out,
+                                            uint64_t elem_off, void* stream) {
+  if (z_layout != 0 && z_layout != 1) return MPC3_ERR_CONFIG;
   if (bits < 1 || bits > 61) return MPC3_ERR_RANGE;
   if (elem_off & 1) return MPC3_ERR_CONFIG;
   if (kh < 1 || kw < 1 || sh < 1 || sw < 1 || ph < 0 || pw < 0) return MPC3_ERR_SHAPE;
   Col2Im g;
   g.N = N; g.C = C; g.OH = OH; g.OW = OW; g.H = H; g.W = W;
   g.kh = kh; g.kw = kw; g.sh = sh; g.sw = sw; g.ph = ph; g.pw = pw;
+  g.zcol = z_layout;
   g.hf = (OH - 1) * sh + kh;
   g.wf = (OW - 1) * sw + kw;
   uint64_t n = (uint64_t)N * C * g.hf * g.wf;

@@ -106,6 +106,7 @@ void hc_col2im(const uint8_t* keys48, uint64_t ja, uint64_t jrho, uint64_t jr, i
   uint32_t rk[132];
   expand3(keys48, rk);
   Col2Im g;
+  g.zcol = 0;
   g.N = N; g.C = C; g.OH = OH; g.OW = OW; g.H = H; g.W = W;
   g.kh = kh; g.kw = kw; g.sh = sh; g.sw = sw; g.ph = ph; g.pw = pw;
   g.hf = (OH - 1) * sh + kh;

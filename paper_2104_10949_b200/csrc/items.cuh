@@ -172,6 +172,7 @@ HD void reshare_trunc_item(const T& tab, const uint32_t* rk3, StreamHead ha, Str
 struct Col2Im {
   int64_t N, C, OH, OW, hf, wf, H, W;
   int kh, kw, sh, sw, ph, pw;
+  int zcol;  // z column-major: cols[(n,y,x), (c,a,b)] at ((c*kh+a)*kw+b) * N*OH*OW + (n*OH+y)*OW + x
 };
 
 template <class T, class I = uint64_t>
@@ -195,19 +196,18 @@ HD void col2im_item(const T& tab, const uint32_t* rk3, StreamHead ha, StreamHead
     int64_t yo = yq - g.ph, xo = xq - g.pw;
     if (yo < 0 || xo < 0 || yo >= g.H || xo >= g.W) continue;
     ooff[e] = ((n * g.C + c) * g.H + yo) * g.W + xo;
-    for (int a = 0; a < g.kh; ++a) {
-      int64_t ty = yq - a;
-      if (ty < 0) break;
-      if (ty % g.sh) continue;
-      int64_t y = ty / g.sh;
-      if (y >= g.OH) continue;
-      for (int bb = 0; bb < g.kw; ++bb) {
-        int64_t tx = xq - bb;
-        if (tx < 0) break;
-        if (tx % g.sw) continue;
-        int64_t x = tx / g.sw;
-        if (x >= g.OW) continue;
-        int64_t zi = ((n * g.OH + y) * g.OW + x) * ncols + (c * g.kh + a) * g.kw + bb;
+    // the (y, x) of the gradient whose window covers (yq, xq): yq = y*sh + a,
+    // 0 <= a < kh, 0 <= y < OH (same for x); walked directly, no modulo tests
+    const int32_t yqi = (int32_t)yq, xqi = (int32_t)xq, sh = g.sh, sw = g.sw;
+    const int32_t y_hi = imin32(yqi / sh, (int32_t)g.OH - 1), x_hi = imin32(xqi / sw, (int32_t)g.OW - 1);
+    const int32_t y_lo = yqi >= g.kh ? (yqi - g.kh + sh) / sh : 0, x_lo = xqi >= g.kw ? (xqi - g.kw + sw) / sw : 0;
+    const int64_t mrows = g.N * g.OH * g.OW;
+    for (int32_t y = y_lo; y <= y_hi; ++y) {
+      const int32_t a = yqi - y * sh;
+      for (int32_t x = x_lo; x <= x_hi; ++x) {
+        const int32_t bb = xqi - x * sw;
+        const int64_t zr = (n * g.OH + y) * g.OW + x, zc = (c * g.kh + a) * g.kw + bb;
+        const int64_t zi = g.zcol ? zc * mrows + zr : zr * ncols + zc;
         for (int i = 0; i < 3; ++i) s[e].c[i] += z[i * zplane + zi];
       }
     }

@@ -635,14 +635,16 @@ class TrioSession:
         a_op = K.conv_operand(K.GATHER_IM2COL, nb * oh * ow, o, nb, o, oh, ow, gs[1:], 1, 1, 1, 1, 0, 0, oh, ow)
         ncols = c * kh * kw
         b_op = K.dense_operand(ncols, o, s_r=1, t2=ncols)
-        z = self._cross_gemm(g.data, a_op, k.data, b_op, nb * oh * ow, ncols, o)
+        col = self.c_col_ok  # column-major cols: the col2im gathers along x coalesce
+        z = self._cross_gemm(g.data, a_op, k.data, b_op, nb * oh * ow, ncols, o, c_col=col)
         out = zeros((nb, c, h, w), g.fp)
         ja = self.take(ARITH)
         jr, jq = self.take(TR_RHO), self.take(TR_R)
         hf, wf = (oh - 1) * sh + kh, (ow - 1) * sw + kw
         full = nb * c * hf * wf
-        K.call("mpc3_rss_col2im_reshare_truncate", self.rk, self.ctr_ptr, ja, jr, jq, bits, z.data_ptr(), nb, c, oh,
-               ow, kh, kw, sh, sw, ph, pw, h, w, out.data.data_ptr(), self.shard_offset(full)[0], _stream())
+        K.call("mpc3_rss_col2im_reshare_truncate_layout", self.rk, self.ctr_ptr, ja, jr, jq, bits, z.data_ptr(),
+               1 if col else 0, nb, c, oh, ow, kh, kw, sh, sw, ph, pw, h, w, out.data.data_ptr(),
+               self.shard_offset(full)[0], _stream())
         self.ledger.ring("mul.reshare", full)
         self._charge_trunc(full)
         return out
