@@ -246,15 +246,16 @@ HD void pool_item(const T& tab, const uint32_t* rk3, bool backward, StreamHead h
     if (!backward) {
       const I fi = (I)f, q1 = fi / (I)p.OW;
       int64_t ox = (int64_t)(fi - q1 * (I)p.OW), oy = (int64_t)(q1 % (I)p.OH), nc = (int64_t)(q1 / (I)p.OH);
-      int64_t y0 = oy * p.sh - p.ph, x0 = ox * p.sw - p.pw;
+      const int32_t y0 = (int32_t)(oy * p.sh - p.ph), x0 = (int32_t)(ox * p.sw - p.pw);
+      const int32_t H = (int32_t)p.H, W = (int32_t)p.W;
       const uint64_t* base = x + nc * p.H * p.W;
       for (int u = 0; u < p.kh; ++u) {
-        int64_t iy = y0 + u;
-        if (iy < 0 || iy >= p.H) continue;
+        const int32_t iy = y0 + u;
+        if (iy < 0 || iy >= H) continue;
         for (int q = 0; q < p.kw; ++q) {
-          int64_t ix = x0 + q;
-          if (ix < 0 || ix >= p.W) continue;
-          for (int i = 0; i < 3; ++i) s[e].c[i] += base[i * nin + iy * p.W + ix];
+          const int32_t ix = x0 + q;
+          if (ix < 0 || ix >= W) continue;
+          for (int i = 0; i < 3; ++i) s[e].c[i] += base[i * nin + (uint64_t)(iy * W + ix)];
         }
       }
     } else {
@@ -262,11 +263,13 @@ HD void pool_item(const T& tab, const uint32_t* rk3, bool backward, StreamHead h
       const I fi = (I)f, q1 = fi / (I)p.W;
       int64_t ix = (int64_t)(fi - q1 * (I)p.W) + p.pw, iy = (int64_t)(q1 % (I)p.H) + p.ph,
               nc = (int64_t)(q1 / (I)p.H);
-      for (int64_t oy = iy / p.sh; oy >= 0 && oy * p.sh + p.kh > iy; --oy) {
+      const int32_t iyi = (int32_t)iy, ixi = (int32_t)ix, sh = p.sh, sw = p.sw;
+      const uint64_t gbase = (uint64_t)nc * p.OH * p.OW;
+      for (int32_t oy = iyi / sh; oy >= 0 && oy * sh + p.kh > iyi; --oy) {
         if (oy >= p.OH) continue;
-        for (int64_t ox = ix / p.sw; ox >= 0 && ox * p.sw + p.kw > ix; --ox) {
+        for (int32_t ox = ixi / sw; ox >= 0 && ox * sw + p.kw > ixi; --ox) {
           if (ox >= p.OW) continue;
-          uint64_t gi = nc * p.OH * p.OW + oy * p.OW + ox;
+          const uint64_t gi = gbase + (uint64_t)oy * p.OW + ox;
           for (int i = 0; i < 3; ++i) s[e].c[i] += x[i * nin + gi];
         }
       }
