@@ -23,6 +23,25 @@ void set_last_error(const char* msg) {
 
 constexpr int kThreads = 256;
 constexpr int kSignThreads = 384;  // four-table AES kernels: one CTA per SM
+// The protocol kernels (everything but the sign / sign2 / chain kernels):
+// two-table AES at 3 x 256-thread CTAs per SM by default.  The four-table
+// layout (one 384-thread CTA per SM, one wave) measured slower for these
+// (reshare 514 -> 540 us, SGD 127 -> 156 us per AlexNet step): they mix AES
+// with memory traffic and need the resident warps more than the ALU slots.
+#ifndef MPC3_PROTO_TABLES4
+#define MPC3_PROTO_TABLES4 0
+#endif
+#if MPC3_PROTO_TABLES4
+#define MPC3_PROTO_SMEM() MPC3_AES_SMEM4()
+#define MPC3_PROTO_INIT(sm, rk, nk) aes_smem_init4(sm, rk, nk)
+using ProtoTables = SmemTables4;
+constexpr int kProtoThreads = kSignThreads, kProtoSmem = kAesSmem4Bytes, kProtoCtasPerSm = 1;
+#else
+#define MPC3_PROTO_SMEM() MPC3_AES_SMEM()
+#define MPC3_PROTO_INIT(sm, rk, nk) aes_smem_init(sm, rk, nk)
+using ProtoTables = SmemTables;
+constexpr int kProtoThreads = kThreads, kProtoSmem = kAesSmemBytes, kProtoCtasPerSm = 8;
+#endif
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = getenv("MPC3_PDL");
@@ -54,8 +73,8 @@ static bool aes_attr(const void* fn, int bytes = kAesSmemBytes) {
 }
 #define AES_LAUNCH(kern, grid, stream, ...)                                                \
   do {                                                                                     \
-    if (!aes_attr((const void*)kern)) return check_launch(#kern " smem attribute");        \
-    if (launch_pdl(kern, dim3(grid), dim3(kThreads), kAesSmemBytes, (stream), __VA_ARGS__) != cudaSuccess) \
+    if (!aes_attr((const void*)kern, kProtoSmem)) return check_launch(#kern " smem attribute"); \
+    if (launch_pdl(kern, dim3(grid), dim3(kProtoThreads), kProtoSmem, (stream), __VA_ARGS__) != cudaSuccess) \
       return check_launch(#kern);                                                          \
   } while (0)
 
@@ -92,12 +111,12 @@ __global__ void __launch_bounds__(kSignThreads, 1) prf_words_kernel(const uint32
   GRID_LOOP(t, nblk) prf_words_item(tab, sm.rk[0], h, word_off, count, out, t);
 }
 
-__global__ void __launch_bounds__(kThreads) zero_share_kernel(const uint32_t* __restrict__ rk3,
+__global__ void __launch_bounds__(kProtoThreads) zero_share_kernel(const uint32_t* __restrict__ rk3,
                                                              const uint64_t* __restrict__ ctr, StreamRef rh,
                                                              int xor_mode, uint64_t n, uint64_t* __restrict__ out) {
-  MPC3_AES_SMEM();
+  MPC3_PROTO_SMEM();
   StreamHead h = resolve(rh, ctr);
-  SmemTables tab = aes_smem_init(sm, rk3, 3);
+  ProtoTables tab = MPC3_PROTO_INIT(sm, rk3, 3);
   GRID_LOOP(b, (n + 1) >> 1) zero_share_item(tab, &sm.rk[0][0], h, xor_mode, n, out, b);
 }
 
@@ -150,13 +169,13 @@ __global__ void ring_rowsum_kernel(const uint64_t* __restrict__ a, uint64_t* __r
 // ---------------------------------------------------------------------------
 // protocols
 
-__global__ void __launch_bounds__(kThreads) arith_kernel(int kind, const uint32_t* __restrict__ rk3,
+__global__ void __launch_bounds__(kProtoThreads) arith_kernel(int kind, const uint32_t* __restrict__ rk3,
                                                         const uint64_t* __restrict__ ctr, StreamRef ra,
                                                         StreamRef rrho, StreamRef rr, int bits, const uint64_t* __restrict__ x,
                                                         const uint64_t* __restrict__ y,
                                                         uint64_t* __restrict__ out, uint64_t n, uint64_t pb0) {
-  MPC3_AES_SMEM();
-  SmemTables tab = aes_smem_init(sm, rk3, 3);
+  MPC3_PROTO_SMEM();
+  ProtoTables tab = MPC3_PROTO_INIT(sm, rk3, 3);
   StreamHead ha = resolve(ra, ctr), hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
   GRID_LOOP(b, (n + 1) >> 1) arith_item(tab, &sm.rk[0][0], kind, ha, hrho, hr, bits, x, y, out, n, b, pb0);
 }
@@ -355,11 +374,11 @@ struct SgdTable {
   uint64_t pair0[MPC3_SGD_MAX_TENSORS + 1];  // first pair of tensor i in the flattened range
 };
 
-__global__ void __launch_bounds__(kThreads) sgd_kernel(const uint32_t* __restrict__ rk3,
+__global__ void __launch_bounds__(kProtoThreads) sgd_kernel(const uint32_t* __restrict__ rk3,
                                                       const uint64_t* __restrict__ ctr, SgdTable tb, int bits,
                                                       uint64_t c) {
-  MPC3_AES_SMEM();
-  SmemTables tab = aes_smem_init(sm, rk3, 3);
+  MPC3_PROTO_SMEM();
+  ProtoTables tab = MPC3_PROTO_INIT(sm, rk3, 3);
   const uint64_t total = tb.pair0[tb.nt];
   GRID_LOOP(q, total) {
     int i = 0;
@@ -382,58 +401,58 @@ __global__ void __launch_bounds__(kThreads) sgd_kernel(const uint32_t* __restric
   }
 }
 
-__global__ void __launch_bounds__(kThreads) inject_kernel(const uint32_t* __restrict__ rk3,
+__global__ void __launch_bounds__(kProtoThreads) inject_kernel(const uint32_t* __restrict__ rk3,
                                                          const uint64_t* __restrict__ ctr, StreamRef r0,
                                                          StreamRef r1, const uint64_t* __restrict__ bits,
                                                          uint64_t* __restrict__ out, uint64_t n) {
-  MPC3_AES_SMEM();
-  SmemTables tab = aes_smem_init(sm, rk3, 3);
+  MPC3_PROTO_SMEM();
+  ProtoTables tab = MPC3_PROTO_INIT(sm, rk3, 3);
   StreamHead a0 = resolve(r0, ctr), a1 = resolve(r1, ctr);
   GRID_LOOP(b, (n + 1) >> 1) inject_item(tab, &sm.rk[0][0], a0, a1, bits, out, n, b);
 }
 
-__global__ void __launch_bounds__(kThreads) reshare_trunc_kernel(const uint32_t* __restrict__ rk3,
+__global__ void __launch_bounds__(kProtoThreads) reshare_trunc_kernel(const uint32_t* __restrict__ rk3,
                                                                 const uint64_t* __restrict__ ctr, StreamRef ra,
                                                                 StreamRef rrho, StreamRef rr, int bits,
                                                                 const uint64_t* __restrict__ z, View4 v,
                                                                 uint64_t* __restrict__ out, uint64_t n,
                                                                 uint64_t pb0) {
-  MPC3_AES_SMEM();
-  SmemTables tab = aes_smem_init(sm, rk3, 3);
+  MPC3_PROTO_SMEM();
+  ProtoTables tab = MPC3_PROTO_INIT(sm, rk3, 3);
   StreamHead ha = resolve(ra, ctr), hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
   if (n < (1ull << 32))
-    GRID_LOOP(b, (n + 1) >> 1) reshare_trunc_item<SmemTables, uint32_t>(tab, &sm.rk[0][0], ha, hrho, hr, bits, z, v, out,
+    GRID_LOOP(b, (n + 1) >> 1) reshare_trunc_item<ProtoTables, uint32_t>(tab, &sm.rk[0][0], ha, hrho, hr, bits, z, v, out,
                                                                          n, b, pb0);
   else
     GRID_LOOP(b, (n + 1) >> 1) reshare_trunc_item(tab, &sm.rk[0][0], ha, hrho, hr, bits, z, v, out, n, b, pb0);
 }
 
-__global__ void __launch_bounds__(kThreads) pool_kernel(const uint32_t* __restrict__ rk3,
+__global__ void __launch_bounds__(kProtoThreads) pool_kernel(const uint32_t* __restrict__ rk3,
                                                        const uint64_t* __restrict__ ctr, int backward,
                                                        StreamRef rrho, StreamRef rr, int bits, uint64_t mulc,
                                                        const uint64_t* __restrict__ x,
                                                        uint64_t* __restrict__ out, PoolGeom p, uint64_t n,
                                                        uint64_t pb0) {
-  MPC3_AES_SMEM();
-  SmemTables tab = aes_smem_init(sm, rk3, 3);
+  MPC3_PROTO_SMEM();
+  ProtoTables tab = MPC3_PROTO_INIT(sm, rk3, 3);
   StreamHead hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
   if (2 * n < (1ull << 32) && (uint64_t)p.N * p.C * p.H * p.W < (1ull << 32))
-    GRID_LOOP(b, (n + 1) >> 1) pool_item<SmemTables, uint32_t>(tab, &sm.rk[0][0], backward != 0, hrho, hr, bits, mulc, x,
+    GRID_LOOP(b, (n + 1) >> 1) pool_item<ProtoTables, uint32_t>(tab, &sm.rk[0][0], backward != 0, hrho, hr, bits, mulc, x,
                                                                 out, p, b, pb0);
   else
     GRID_LOOP(b, (n + 1) >> 1) pool_item(tab, &sm.rk[0][0], backward != 0, hrho, hr, bits, mulc, x, out, p, b, pb0);
 }
 
-__global__ void __launch_bounds__(kThreads) col2im_kernel(const uint32_t* __restrict__ rk3,
+__global__ void __launch_bounds__(kProtoThreads) col2im_kernel(const uint32_t* __restrict__ rk3,
                                                          const uint64_t* __restrict__ ctr, StreamRef ra,
                                                          StreamRef rrho, StreamRef rr, int bits,
                                                          const uint64_t* __restrict__ z, Col2Im g,
                                                          uint64_t* __restrict__ out, uint64_t n, uint64_t pb0) {
-  MPC3_AES_SMEM();
-  SmemTables tab = aes_smem_init(sm, rk3, 3);
+  MPC3_PROTO_SMEM();
+  ProtoTables tab = MPC3_PROTO_INIT(sm, rk3, 3);
   StreamHead ha = resolve(ra, ctr), hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
   if (2 * n < (1ull << 32))
-    GRID_LOOP(b, (n + 1) >> 1) col2im_item<SmemTables, uint32_t>(tab, &sm.rk[0][0], ha, hrho, hr, bits, z, g, out, b,
+    GRID_LOOP(b, (n + 1) >> 1) col2im_item<ProtoTables, uint32_t>(tab, &sm.rk[0][0], ha, hrho, hr, bits, z, g, out, b,
                                                                   pb0);
   else
     GRID_LOOP(b, (n + 1) >> 1) col2im_item(tab, &sm.rk[0][0], ha, hrho, hr, bits, z, g, out, b, pb0);
@@ -506,7 +525,7 @@ int mpc3_rss_zero_share(const uint32_t* rk3, const uint64_t* ctr, uint32_t purpo
   int st = check_stream_args(purpose, index);
   if (st) return st;
   if (n == 0) return MPC3_OK;
-  AES_LAUNCH(zero_share_kernel, grid_for((n + 1) / 2, kThreads), as_stream(stream), 
+  AES_LAUNCH(zero_share_kernel, grid_for((n + 1) / 2, kProtoThreads, kProtoCtasPerSm), as_stream(stream), 
       rk3, ctr, sref(purpose, index), xor_mode, n, out);
   return check_launch("zero_share");
 }
@@ -541,7 +560,7 @@ static int arith_launch(int kind, const uint32_t* rk3, const uint64_t* ctr, uint
   if (ja >= (1ull << 48) || jrho >= (1ull << 48) || jr >= (1ull << 48)) return MPC3_ERR_RANGE;
   if (elem_off & 1) return MPC3_ERR_CONFIG;
   if (n == 0) return MPC3_OK;
-  AES_LAUNCH(arith_kernel, grid_for((n + 1) / 2, kThreads), as_stream(stream), 
+  AES_LAUNCH(arith_kernel, grid_for((n + 1) / 2, kProtoThreads, kProtoCtasPerSm), as_stream(stream), 
       kind, rk3, ctr, sref(ARITH_ZERO, ja), sref(TRUNC_RHO, jrho), sref(TRUNC_R, jr), bits, x, y, out, n,
       elem_off >> 1);
   return check_launch("rss_arith");
@@ -576,7 +595,7 @@ int mpc3_rss_sgd_multi(const uint32_t* rk3, const uint64_t* ctr, const MPC3SgdTe
     tb.pair0[i + 1] = tb.pair0[i] + (ts[i].n + 1) / 2;
   }
   if (tb.pair0[nt] == 0) return MPC3_OK;
-  AES_LAUNCH(sgd_kernel, grid_for(tb.pair0[nt], kThreads), as_stream(stream), rk3, ctr, tb, bits, c);
+  AES_LAUNCH(sgd_kernel, grid_for(tb.pair0[nt], kProtoThreads, kProtoCtasPerSm), as_stream(stream), rk3, ctr, tb, bits, c);
   return check_launch("rss_sgd_multi");
 }
 
@@ -664,7 +683,7 @@ int mpc3_rss_bit_inject(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_ari
                         uint64_t n, void* stream) {
   if (j_arith + 1 >= (1ull << 48)) return MPC3_ERR_RANGE;
   if (n == 0) return MPC3_OK;
-  AES_LAUNCH(inject_kernel, grid_for((n + 1) / 2, kThreads), as_stream(stream), 
+  AES_LAUNCH(inject_kernel, grid_for((n + 1) / 2, kProtoThreads, kProtoCtasPerSm), as_stream(stream), 
       rk3, ctr, sref(ARITH_ZERO, j_arith), sref(ARITH_ZERO, j_arith + 1), bits, out, n);
   return check_launch("rss_bit_inject");
 }
@@ -688,7 +707,7 @@ int mpc3_rss_reshare_truncate(const uint32_t* rk3, const uint64_t* ctr, uint64_t
   v.zp = view->z_plane;
   v.op = view->out_plane;
   if (n == 0) return MPC3_OK;
-  AES_LAUNCH(reshare_trunc_kernel, grid_for((n + 1) / 2, kThreads), as_stream(stream), 
+  AES_LAUNCH(reshare_trunc_kernel, grid_for((n + 1) / 2, kProtoThreads, kProtoCtasPerSm), as_stream(stream), 
       rk3, ctr, sref(ARITH_ZERO, j_arith), sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, z, v, out, n,
       elem_off >> 1);
   return check_launch("rss_reshare_truncate");
@@ -712,7 +731,7 @@ int mpc3_rss_avgpool(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_rho, u
   int64_t OH = (H + 2 * ph - kh) / sh + 1, OW = (W + 2 * pw - kw) / sw + 1;
   uint64_t n = (uint64_t)N * C * OH * OW;
   if (n == 0) return MPC3_OK;
-  AES_LAUNCH(pool_kernel, grid_for((n + 1) / 2, kThreads), as_stream(stream), 
+  AES_LAUNCH(pool_kernel, grid_for((n + 1) / 2, kProtoThreads, kProtoCtasPerSm), as_stream(stream), 
       rk3, ctr, 0, sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, mulc, x, out,
       pool_geom(N, C, H, W, OH, OW, kh, kw, sh, sw, ph, pw), n, elem_off >> 1);
   return check_launch("rss_avgpool");
@@ -727,7 +746,7 @@ int mpc3_rss_avgpool_backward(const uint32_t* rk3, const uint64_t* ctr, uint64_t
   if (kh < 1 || kw < 1 || sh < 1 || sw < 1 || ph < 0 || pw < 0) return MPC3_ERR_SHAPE;
   uint64_t n = (uint64_t)N * C * H * W;
   if (n == 0) return MPC3_OK;
-  AES_LAUNCH(pool_kernel, grid_for((n + 1) / 2, kThreads), as_stream(stream), 
+  AES_LAUNCH(pool_kernel, grid_for((n + 1) / 2, kProtoThreads, kProtoCtasPerSm), as_stream(stream), 
       rk3, ctr, 1, sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, mulc, g, out,
       pool_geom(N, C, H, W, OH, OW, kh, kw, sh, sw, ph, pw), n, elem_off >> 1);
   return check_launch("rss_avgpool_backward");
@@ -758,7 +777,7 @@ int mpc3_rss_col2im_reshare_truncate_layout(const uint32_t* rk3, const uint64_t*
   g.wf = (OW - 1) * sw + kw;
   uint64_t n = (uint64_t)N * C * g.hf * g.wf;
   if (n == 0) return MPC3_OK;
-  AES_LAUNCH(col2im_kernel, grid_for((n + 1) / 2, kThreads), as_stream(stream), 
+  AES_LAUNCH(col2im_kernel, grid_for((n + 1) / 2, kProtoThreads, kProtoCtasPerSm), as_stream(stream), 
       rk3, ctr, sref(ARITH_ZERO, j_arith), sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, z, g, out, n,
       elem_off >> 1);
   return check_launch("rss_col2im_reshare_truncate");

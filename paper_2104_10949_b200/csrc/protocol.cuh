@@ -162,8 +162,9 @@ HD void trunc_words(const T& tab, const uint32_t* rk3, StreamHead hrho, StreamHe
   r = prf_block(tab, rk3 + 1 * 44, hr, blk);
 }
 #if defined(__CUDACC__)
-HD void trunc_words(const SmemTables& tab, const uint32_t* rk3, StreamHead hrho, StreamHead hr, uint64_t blk,
-                    Word2& rho, Word2& r) {
+template <class TT>
+HD void trunc_words_dev(const TT& tab, const uint32_t* rk3, StreamHead hrho, StreamHead hr, uint64_t blk,
+                        Word2& rho, Word2& r) {
 #if defined(__CUDA_ARCH__)
   uint32_t s[2][4] = {{hrho.s0, hrho.s1, (uint32_t)(blk >> 32), (uint32_t)blk},
                       {hr.s0, hr.s1, (uint32_t)(blk >> 32), (uint32_t)blk}};
@@ -174,6 +175,14 @@ HD void trunc_words(const SmemTables& tab, const uint32_t* rk3, StreamHead hrho,
   r.w0 = (uint64_t)bswap32(s[1][0]) | ((uint64_t)bswap32(s[1][1]) << 32);
   r.w1 = (uint64_t)bswap32(s[1][2]) | ((uint64_t)bswap32(s[1][3]) << 32);
 #endif
+}
+HD void trunc_words(const SmemTables& tab, const uint32_t* rk3, StreamHead hrho, StreamHead hr, uint64_t blk,
+                    Word2& rho, Word2& r) {
+  trunc_words_dev(tab, rk3, hrho, hr, blk, rho, r);
+}
+HD void trunc_words(const SmemTables4& tab, const uint32_t* rk3, StreamHead hrho, StreamHead hr, uint64_t blk,
+                    Word2& rho, Word2& r) {
+  trunc_words_dev(tab, rk3, hrho, hr, blk, rho, r);
 }
 #endif
 
