@@ -475,6 +475,11 @@ def run_b200(args, ws, rank, local):
         except Exception as e:  # noqa: BLE001 - reported, not fatal to the headline
             also["resnet50_error"] = repr(e)[:300]
 
+    if ws > 1 and not args.no_resnet:
+        try:
+            tp = resnet50_b1_tp(dev)
+        except Exception as e:  # noqa: BLE001
+            tp = {"error": repr(e)[:300]}
     if ws > 1 and also:
         # every rank ran the same side workloads as an independent replica:
         # report the aggregate (sum of batches / slowest rank), weak scaling
@@ -486,6 +491,8 @@ def run_b200(args, ws, rank, local):
                     sub["value"] = sub["value"] * sub["ms_per_batch"] / float(t.item()) * ws
                     sub["ms_per_batch"] = float(t.item())
                     sub["scaling"] = f"weak: {ws} independent replicas, slowest rank"
+    if ws > 1 and not args.no_resnet:
+        also["resnet50_b1_tensor_parallel"] = tp
     if rank == 0:
         line = {
             "also": also,
@@ -625,6 +632,38 @@ def resnet50_inference(dev, batch: int, steps: int, use_graph: bool):
     return {"workload": f"ResNet-50 v1.5 private inference, ImageNet 3x224x224, batch {batch}",
             "value": batch / (t / 1e3), "unit": "images/s", "ms_per_batch": t, "steps": steps,
             "cuda_graph": use_graph, "data": "synthetic (random-init folded-BN weights, U(0,1) images)"}
+
+
+def resnet50_b1_tp(dev, steps: int = 5):
+    """ResNet-50 b=1 private inference with output-channel slabs across all
+    ranks (nn.TensorParallel, NCCL all-gather between layers); the result is
+    bit-identical to the one-GPU run.  Latency, slowest rank."""
+    import torch
+
+    import paper_2104_10949_b200 as M
+    from paper_2104_10949_b200.nn import TensorParallel, TPNet
+
+    sess = M.TrioSession(seed=11)
+    model = M.models.resnet50()
+    rng = np.random.default_rng(11)
+    params = [sess.share(w, rng) for w in M.init_params(model, seed=11)]
+    x = sess.share(M.fx_encode(rng.uniform(0, 1, (1, 3, 224, 224))), rng)
+    net = TPNet(sess, TensorParallel.from_process_group())
+    net.forward_tp(model, params, x)
+    torch.cuda.synchronize()
+    torch.distributed.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        net.forward_tp(model, params, x)
+    e1.record()
+    e1.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / steps], device=dev, dtype=torch.float64)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms = float(t.item())
+    return {"workload": "ResNet-50 v1.5 private inference, batch 1, output channels sharded over all ranks "
+                        "(NCCL all-gather per layer), eager",
+            "value": 1.0 / (ms / 1e3), "unit": "images/s", "latency_ms": ms, "steps": steps}
 
 
 def main():

@@ -17,6 +17,7 @@ results — and per-party shares — are bit-identical to the reference.
 
 from __future__ import annotations
 
+import contextlib
 import os
 from dataclasses import dataclass, field
 
@@ -537,6 +538,127 @@ class DataParallel:
             raise ConfigError(f"global batch {global_batch} not divisible by {self.world} ranks")
         b = global_batch // self.world
         return slice(self.rank * b, (self.rank + 1) * b)
+
+
+class TensorParallel:
+    """Output-channel sharding of batch-1 private inference (SURVEY.md 8(e),
+    ResNet-50 b=1): every rank computes an equal slab of each conv / FC
+    layer's output channels from the full (replicated) input.  With batch 1
+    a channel slab is one contiguous range of the reference's flat output,
+    so the reshare / truncation / ReLU / pooling PRF words are drawn at the
+    slab's global offset exactly like a batch shard (TrioSession.shard_offset)
+    and the gathered activations are bit-identical to the single-GPU run.
+    The one exchange per layer is an all-gather of the slabs before the next
+    layer that needs every input channel.  `allgather(t)` takes an int64
+    (3, S) CUDA tensor and returns (world, 3, S) in rank order."""
+
+    def __init__(self, rank: int, world: int, allgather):
+        self.rank, self.world, self.allgather = rank, world, allgather
+
+    @classmethod
+    def from_process_group(cls, group=None):
+        import torch.distributed as dist
+
+        world = dist.get_world_size(group)
+
+        def allgather(t):
+            out = torch.empty((world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+            dist.all_gather_into_tensor(out, t.contiguous(), group=group)
+            return out.view((world,) + tuple(t.shape))
+
+        return cls(dist.get_rank(group), world, allgather)
+
+    def slab(self, n: int) -> slice:
+        if n % self.world:
+            raise ConfigError(f"{n} channels not divisible by {self.world} ranks")
+        b = n // self.world
+        return slice(self.rank * b, (self.rank + 1) * b)
+
+    def gather(self, h: RssTensor) -> RssTensor:
+        """Slab (3, 1, c, ...) -> full (3, 1, world*c, ...) in channel order."""
+        shp = h.shape
+        g = self.allgather(h.data.reshape(3, -1))  # (world, 3, S)
+        full = g.permute(1, 0, 2).contiguous()
+        return RssTensor(full.reshape((3, shp[0], shp[1] * self.world) + tuple(shp[2:])), h.fp)
+
+
+class TPNet(TrioNet):
+    """Batch-1 private inference with output-channel slabs (TensorParallel)."""
+
+    def __init__(self, sess: TrioSession, tp: TensorParallel):
+        super().__init__(sess)
+        self.tp = tp
+
+    def forward_tp(self, model: ModelGraph, params: list, x: RssTensor) -> RssTensor:
+        if x.shape[0] != 1:
+            raise ConfigError("output-channel sharding is defined for batch 1")
+        S = self.s
+        saved = S.dp
+        S.dp = DataParallel(self.tp.rank, self.tp.world, None)  # slab offsets = batch-shard offsets
+        try:
+            h, slab = self._run_tp(model.layers, iter(params), x, False)
+            return self.tp.gather(h) if slab else h
+        finally:
+            S.dp = saved
+
+    def _full(self, h, slab):
+        return self.tp.gather(h) if slab else h
+
+    def _run_tp(self, layers, it, h: RssTensor, slab: bool):
+        """Returns (h, is_slab)."""
+        S, tp = self.s, self.tp
+        for spec in layers:
+            if spec.kind in (CONV2D, FULLY_CONNECTED):
+                k = next(it)
+                b = next(it) if spec.bias else None
+                h = self._full(h, slab)
+                if spec.kind == CONV2D:
+                    (kh, kw), (sh, sw), (ph, pw) = k.shape[2:], spec.stride, spec.padding
+                    spatial = ((h.shape[2] + 2 * ph - kh) // sh + 1) * ((h.shape[3] + 2 * pw - kw) // sw + 1)
+                else:
+                    spatial = 1
+                # shard only into slabs whose PRF words start at an even word (one
+                # AES block = two adjacent elements); otherwise compute replicated
+                split = k.shape[0] % tp.world == 0 and (k.shape[0] // tp.world * spatial) % 2 == 0
+                cs = tp.slab(k.shape[0]) if split else slice(None)
+                kk = RssTensor(k.data[:, cs], k.fp)
+                ctx = contextlib.nullcontext() if split else S.replicated()
+                with ctx:
+                    if spec.kind == CONV2D:
+                        h = S.conv2d(h, kk, spec.stride, spec.padding)
+                    else:
+                        h = S.matmul(h, kk.apply(lambda d: d.transpose(1, 2)))
+                if b is not None:
+                    h = self._bias(h, RssTensor(b.data[:, cs], b.fp))
+                if not split:  # replicated output: this rank's slab for the slab-local layers after it
+                    if h.shape[1] % tp.world == 0 and (h.numel // tp.world) % 2 == 0:
+                        h = RssTensor(h.data[:, :, tp.slab(h.shape[1])].contiguous(), h.fp)
+                        split = True
+                slab = split
+            elif spec.kind == AVGPOOL:
+                if slab:
+                    h = S.avgpool(h, spec.window, spec.stride, spec.padding)
+                else:
+                    with S.replicated():
+                        h = S.avgpool(h, spec.window, spec.stride, spec.padding)
+            elif spec.kind == RELU:
+                if slab:
+                    h = S.relu(h)
+                else:
+                    with S.replicated():
+                        h = S.relu(h)
+            elif spec.kind == FLATTEN:
+                h = h.contiguous().reshape(h.shape[0], -1)
+            elif spec.kind == RESIDUAL:
+                full = self._full(h, slab)
+                hm, ms = self._run_tp(spec.main, it, full, False) if spec.main else (full, False)
+                hs, ss = self._run_tp(spec.shortcut, it, full, False) if spec.shortcut else (full, False)
+                if not ms:
+                    hm = RssTensor(hm.data[:, :, tp.slab(hm.shape[1])].contiguous(), hm.fp)
+                if not ss:
+                    hs = RssTensor(hs.data[:, :, tp.slab(hs.shape[1])].contiguous(), hs.fp)
+                h, slab = S.add(hm, hs), True
+        return h, slab
 
 
 class InferenceGraph:

@@ -70,3 +70,39 @@ def test_gloo_allreduce_wraps_and_shards_partition():
 def test_shard_rows_requires_divisible_batch():
     with pytest.raises(Exception):
         DataParallel(0, 3, None).shard_rows(8)
+
+
+def _tp_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2104_10949_b200.engine import RssTensor
+        from paper_2104_10949_b200.nn import TensorParallel
+
+        tp = TensorParallel.from_process_group()
+        full = np.arange(3 * 1 * 8 * 2 * 3, dtype=np.int64).reshape(3, 1, 8, 2, 3)
+        sl = tp.slab(8)
+        slab = RssTensor(torch.from_numpy(np.ascontiguousarray(full[:, :, sl])))
+        got = tp.gather(slab).data.numpy()
+        q.put((rank, np.array_equal(got, full), (sl.start, sl.stop)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_tensor_parallel_gather_restores_channel_order():
+    """TensorParallel (ResNet-50 b=1 output-channel slabs): the all-gather of
+    per-rank channel slabs rebuilds the full (3, 1, C, H, W) activation."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_tp_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, sl in res:
+        assert ok
+        assert sl == (rank * 4, rank * 4 + 4)
