@@ -204,6 +204,14 @@ typedef struct {
 int mpc3_rss_reshare_truncate(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, uint64_t j_rho, uint64_t j_r,
                               int bits, const uint64_t* z, const mpc3_view4* view, uint64_t* out,
                               uint64_t elem_off, void* stream);
+/* Same, then a shared bias added component-wise (the inference extension's
+ * folded-BN / FC bias: out = truncate(reshare(z)) + bias, a local add):
+ * element i of the view gets bias[k * bias_plane + i_{bias_dim}] in
+ * component k.  bias = NULL: no bias. */
+int mpc3_rss_reshare_truncate_bias(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, uint64_t j_rho,
+                                   uint64_t j_r, int bits, const uint64_t* z, const mpc3_view4* view,
+                                   const uint64_t* bias, int64_t bias_plane, int bias_dim, uint64_t* out,
+                                   uint64_t elem_off, void* stream);
 
 /* Input gradient epilogue (nn.py:460-484): z holds per-party cross terms
  * cols[(n,y,x), (c,a,b)] = sum_o g[n,o,y,x] k[o,c,a,b] (a GEMM with inner

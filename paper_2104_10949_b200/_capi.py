@@ -166,6 +166,8 @@ _SIGS = {
     "mpc3_rss_bit_inject": (C.c_int, [_P, _P, _U64, _P, _P, _U64, _P]),
     "mpc3_rss_reshare_truncate": (C.c_int, [_P, _P, _U64, _U64, _U64, C.c_int, _P, C.POINTER(View4), _P, _U64,
                                             _P]),
+    "mpc3_rss_reshare_truncate_bias": (C.c_int, [_P, _P, _U64, _U64, _U64, C.c_int, _P, C.POINTER(View4), _P, _I64,
+                                                 C.c_int, _P, _U64, _P]),
     "mpc3_rss_avgpool": (C.c_int, [_P, _P, _U64, _U64, C.c_int, _U64, _P, _P, _I64, _I64, _I64, _I64,
                                    C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _U64, _P]),
     "mpc3_rss_avgpool_backward": (C.c_int, [_P, _P, _U64, _U64, C.c_int, _U64, _P, _P, _I64, _I64, _I64, _I64,

@@ -691,7 +691,16 @@ int mpc3_rss_bit_inject(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_ari
 int mpc3_rss_reshare_truncate(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, uint64_t j_rho, uint64_t j_r, int bits,
                               const uint64_t* z, const mpc3_view4* view, uint64_t* out, uint64_t elem_off,
                               void* stream) {
+  return mpc3_rss_reshare_truncate_bias(rk3, ctr, j_arith, j_rho, j_r, bits, z, view, nullptr, 0, 0, out, elem_off,
+                                        stream);
+}
+
+int mpc3_rss_reshare_truncate_bias(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, uint64_t j_rho,
+                                   uint64_t j_r, int bits, const uint64_t* z, const mpc3_view4* view,
+                                   const uint64_t* bias, int64_t bias_plane, int bias_dim, uint64_t* out,
+                                   uint64_t elem_off, void* stream) {
   if (bits != 0 && (bits < 1 || bits > 61)) return MPC3_ERR_RANGE;
+  if (bias && (bias_dim < 0 || bias_dim > 3 || bias_plane < 0)) return MPC3_ERR_CONFIG;
   if (!view || (elem_off & 1)) return MPC3_ERR_CONFIG;
   View4 v;
   uint64_t n = 1;
@@ -706,6 +715,9 @@ int mpc3_rss_reshare_truncate(const uint32_t* rk3, const uint64_t* ctr, uint64_t
   }
   v.zp = view->z_plane;
   v.op = view->out_plane;
+  v.bias = bias;
+  v.bias_plane = bias_plane;
+  v.bias_dim = bias_dim;
   if (n == 0) return MPC3_OK;
   AES_LAUNCH(reshare_trunc_kernel, grid_for((n + 1) / 2, kProtoThreads, kProtoCtasPerSm), as_stream(stream), 
       rk3, ctr, sref(ARITH_ZERO, j_arith), sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, z, v, out, n,

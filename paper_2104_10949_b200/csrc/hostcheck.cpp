@@ -81,6 +81,9 @@ void hc_reshare_truncate(const uint8_t* keys48, uint64_t ja, uint64_t jrho, uint
   }
   v.zp = view->z_plane;
   v.op = view->out_plane;
+  v.bias = nullptr;
+  v.bias_plane = 0;
+  v.bias_dim = 0;
   for (uint64_t b = 0; b < (n + 1) / 2; ++b)
     reshare_trunc_item(tabs(), rk, stream_head(ARITH_ZERO, ja), stream_head(TRUNC_RHO, jrho), stream_head(TRUNC_R, jr),
                        bits, z, v, out, n, b);

@@ -115,6 +115,9 @@ HD void inject_item(const T& tab, const uint32_t* rk3, StreamHead a0, StreamHead
 
 struct View4 {
   int64_t full[4], org[4], crop[4], zs[4], os[4], zp, op;
+  const uint64_t* bias;  // optional shared bias added after the truncation: bias[k * bias_plane + i_{bias_dim}]
+  int64_t bias_plane;
+  int bias_dim;
 };
 
 // I: index arithmetic type (uint32_t when every extent fits: the kernels pick
@@ -125,7 +128,7 @@ HD void reshare_trunc_item(const T& tab, const uint32_t* rk3, StreamHead ha, Str
                            int bits, const uint64_t* z, const View4& v, uint64_t* out, uint64_t n, uint64_t b,
                            uint64_t pb0 = 0) {
   const uint64_t pb = pb0 + b;
-  int64_t zoff[2] = {0, 0}, ooff[2] = {0, 0};
+  int64_t zoff[2] = {0, 0}, ooff[2] = {0, 0}, bidx[2] = {0, 0};
   bool ok[2];
   for (int e = 0; e < 2; ++e) {
     uint64_t f = 2 * b + e;
@@ -139,6 +142,7 @@ HD void reshare_trunc_item(const T& tab, const uint32_t* rk3, StreamHead ha, Str
     int64_t i1 = (int64_t)(r % f1);
     int64_t i0 = (int64_t)(r / f1);
     zoff[e] = i0 * v.zs[0] + i1 * v.zs[1] + i2 * v.zs[2] + i3 * v.zs[3];
+    bidx[e] = v.bias_dim == 0 ? i0 : v.bias_dim == 1 ? i1 : v.bias_dim == 2 ? i2 : i3;
     i0 -= v.org[0];
     i1 -= v.org[1];
     i2 -= v.org[2];
@@ -159,6 +163,9 @@ HD void reshare_trunc_item(const T& tab, const uint32_t* rk3, StreamHead ha, Str
     Trio t = load_trio(z + zoff[e], v.zp, 0);
     t = trio_reshare(t, e ? f1 : f0);
     if (bits) t = trio_truncate(t, e ? rho.w1 : rho.w0, e ? r.w1 : r.w0, bits);
+    if (v.bias) {  // local add of the bias shares (component-wise), as a separate add would
+      for (int k = 0; k < 3; ++k) t.c[k] += v.bias[k * v.bias_plane + bidx[e]];
+    }
     store_trio(out + ooff[e], v.op, 0, t);
   }
 }

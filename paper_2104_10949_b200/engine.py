@@ -525,20 +525,28 @@ class TrioSession:
     def c_col_ok(self) -> bool:
         return not IMPLICIT_GEMM
 
-    def _finish(self, z, view, out: RssTensor, bits, label):
+    def _finish(self, z, view, out: RssTensor, bits, label, bias: RssTensor | None = None, bias_dim: int = 1):
         ja = self.take(ARITH)
         jr = jq = 0
         if bits:
             jr, jq = self.take(TR_RHO), self.take(TR_R)
         full = int(np.prod(view.full))
-        K.call("mpc3_rss_reshare_truncate", self.rk, self.ctr_ptr, ja, jr, jq, bits, z.data_ptr(), C.byref(view),
-               out.data.data_ptr(), self.shard_offset(full)[0], _stream())
+        if bias is None:
+            K.call("mpc3_rss_reshare_truncate", self.rk, self.ctr_ptr, ja, jr, jq, bits, z.data_ptr(), C.byref(view),
+                   out.data.data_ptr(), self.shard_offset(full)[0], _stream())
+        else:  # the shared bias added in the same pass (a local add, nn.py bias extension)
+            if bias.ndim != 1 or bias.data.stride(1) != 1:
+                raise ShapeError("bias must be a 1-d shared vector with unit stride")
+            K.call("mpc3_rss_reshare_truncate_bias", self.rk, self.ctr_ptr, ja, jr, jq, bits, z.data_ptr(),
+                   C.byref(view), bias.data.data_ptr(), bias.data.stride(0), bias_dim, out.data.data_ptr(),
+                   self.shard_offset(full)[0], _stream())
         self.ledger.ring(label, full)
         if bits:
             self._charge_trunc(full)
         return out
 
-    def matmul(self, x: RssTensor, y: RssTensor, bits: int | None = None, wgrad: bool = False) -> RssTensor:
+    def matmul(self, x: RssTensor, y: RssTensor, bits: int | None = None, wgrad: bool = False,
+               bias: RssTensor | None = None) -> RssTensor:
         """matmul_shares (protocols.py:97-117): cross terms, reshare, truncate.
         wgrad=True marks a weight gradient g^T x whose inner dimension is the
         batch: under data parallelism the shards' cross terms are summed
@@ -560,10 +568,13 @@ class TrioSession:
             self._reduce_cross_terms(z)
             with self.replicated():
                 return self._finish(z, K.make_view((1, 1, m, n)), out, bits, "mul.reshare")
-        return self._finish(z, K.make_view((1, 1, m, n)), out, bits, "mul.reshare")
+        return self._finish(z, K.make_view((1, 1, m, n)), out, bits, "mul.reshare", bias=bias, bias_dim=3)
 
-    def conv2d(self, x: RssTensor, k: RssTensor, stride=(1, 1), padding=(0, 0), bits=None) -> RssTensor:
-        """conv2d_shares (protocols.py:120-136), NCHW cross-correlation."""
+    def conv2d(self, x: RssTensor, k: RssTensor, stride=(1, 1), padding=(0, 0), bits=None,
+               bias: RssTensor | None = None) -> RssTensor:
+        """conv2d_shares (protocols.py:120-136), NCHW cross-correlation;
+        `bias` (inference extension) is added per output channel after the
+        truncation in the same kernel."""
         if x.ndim != 4 or k.ndim != 4 or x.shape[1] != k.shape[1]:
             raise ShapeError(f"kernel {k.shape} incompatible with input {x.shape}")
         nb, c, h, w = x.shape
@@ -586,7 +597,7 @@ class TrioSession:
         # z[(n, y, x), o]: column-major keeps each (n, o) plane's (y, x) run contiguous
         zs = (oh * ow, M, ow, 1) if col else (oh * ow * o, 1, ow * o, o)
         view = K.make_view((nb, o, oh, ow), z_stride=zs)
-        return self._finish(z, view, out, bits, "mul.reshare")
+        return self._finish(z, view, out, bits, "mul.reshare", bias=bias, bias_dim=1)
 
     def conv2d_wgrad(self, x: RssTensor, g: RssTensor, kernel, stride, padding, bits) -> RssTensor:
         """Kernel gradient (nn.py:435-457) as one direct implicit GEMM with

@@ -245,15 +245,11 @@ class TrioNet:
             if spec.kind == CONV2D:
                 k = next(it)
                 acts.append((h, k) if record else None)
-                h = S.conv2d(h, k, spec.stride, spec.padding)
-                if spec.bias:
-                    h = self._bias(h, next(it))
+                h = S.conv2d(h, k, spec.stride, spec.padding, bias=next(it) if spec.bias else None)
             elif spec.kind == FULLY_CONNECTED:
                 w = next(it)
                 acts.append((h, w) if record else None)
-                h = S.matmul(h, w.apply(lambda d: d.transpose(1, 2)))
-                if spec.bias:
-                    h = self._bias(h, next(it))
+                h = S.matmul(h, w.apply(lambda d: d.transpose(1, 2)), bias=next(it) if spec.bias else None)
             elif spec.kind == AVGPOOL:
                 acts.append((h.shape,) if record else None)
                 h = S.avgpool(h, spec.window, spec.stride, spec.padding)
@@ -623,13 +619,12 @@ class TPNet(TrioNet):
                 cs = tp.slab(k.shape[0]) if split else slice(None)
                 kk = RssTensor(k.data[:, cs], k.fp)
                 ctx = contextlib.nullcontext() if split else S.replicated()
+                bb = RssTensor(b.data[:, cs], b.fp) if b is not None else None
                 with ctx:
                     if spec.kind == CONV2D:
-                        h = S.conv2d(h, kk, spec.stride, spec.padding)
+                        h = S.conv2d(h, kk, spec.stride, spec.padding, bias=bb)
                     else:
-                        h = S.matmul(h, kk.apply(lambda d: d.transpose(1, 2)))
-                if b is not None:
-                    h = self._bias(h, RssTensor(b.data[:, cs], b.fp))
+                        h = S.matmul(h, kk.apply(lambda d: d.transpose(1, 2)), bias=bb)
                 if not split:  # replicated output: this rank's slab for the slab-local layers after it
                     if h.shape[1] % tp.world == 0 and (h.numel // tp.world) % 2 == 0:
                         h = RssTensor(h.data[:, :, tp.slab(h.shape[1])].contiguous(), h.fp)
