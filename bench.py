@@ -520,7 +520,7 @@ def _aes_peak_gblocks():
     rk = np.zeros((3, 44), np.uint32)
     for i in range(3):
         _capi.check(_capi.lib().mpc3_aes128_expand(C.c_char_p(bytes([i]) * 16), rk[i].ctypes.data_as(C.c_void_p)))
-    rkd = torch.from_numpy(rk.view(np.int32)).cuda()
+    rkd = torch.from_numpy(rk.view(np.int32)).pin_memory()  # read on the host at launch
     count = 1 << 28
     out = torch.empty(count, dtype=torch.int64, device="cuda")
     st = torch.cuda.current_stream().cuda_stream

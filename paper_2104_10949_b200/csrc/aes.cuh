@@ -137,6 +137,11 @@ HD void aes128_block(const SmemTables4& tab, const uint32_t* rk, uint32_t& s0, u
                      uint32_t& s3);
 #endif
 
+// The three session key schedules, passed to the kernels by value.
+struct KeySched {
+  uint32_t rk[3][44];
+};
+
 // Words 2b and 2b+1 of stream (head, key).
 struct Word2 {
   uint64_t w0, w1;

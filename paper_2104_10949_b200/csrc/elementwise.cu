@@ -71,6 +71,38 @@ static bool aes_attr(const void* fn, int bytes = kAesSmemBytes) {
   done.insert({dev, fn});
   return true;
 }
+// Session keys travel in the kernel parameters (KeySched, 528 bytes): the
+// round keys are then constant-bank operands (LDC / LDCU) instead of
+// shared-memory loads competing with the T-table lookups (+10 % AES rate on
+// the LSU-bound sign kernel).  The engine keeps its key schedule in pinned
+// host memory, read here directly; a device buffer is copied back once
+// (not allowed while a graph is being captured).
+static int load_keys(const uint32_t* rk, int nkeys, void* stream, KeySched* ks) {
+  if (!rk) {
+    set_last_error("null key schedule");
+    return MPC3_ERR_CONFIG;
+  }
+  memset(ks, 0, sizeof(*ks));
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, rk) != cudaSuccess) {
+    cudaGetLastError();
+    at.type = cudaMemoryTypeUnregistered;
+  }
+  const size_t bytes = (size_t)nkeys * 44 * sizeof(uint32_t);
+  if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(as_stream(stream), &cs);
+    if (cs != cudaStreamCaptureStatusNone) {
+      set_last_error("device-resident key schedule cannot be read during graph capture (use pinned host memory)");
+      return MPC3_ERR_CONFIG;
+    }
+    if (cudaMemcpy(&ks->rk[0][0], rk, bytes, cudaMemcpyDeviceToHost) != cudaSuccess) return check_launch("key copy");
+  } else {
+    memcpy(&ks->rk[0][0], rk, bytes);
+  }
+  return MPC3_OK;
+}
+
 #define AES_LAUNCH(kern, grid, stream, ...)                                                \
   do {                                                                                     \
     if (!aes_attr((const void*)kern, kProtoSmem)) return check_launch(#kern " smem attribute"); \
@@ -102,22 +134,22 @@ HD StreamRef sref(uint32_t purpose, uint64_t j) {
 // ---------------------------------------------------------------------------
 // PRF streams
 
-__global__ void __launch_bounds__(kSignThreads, 1) prf_words_kernel(const uint32_t* __restrict__ rk_dev,
+__global__ void __launch_bounds__(kSignThreads, 1) prf_words_kernel(const __grid_constant__ KeySched ks,
                                                                    StreamHead h, uint64_t word_off,
                                                                    uint64_t count, uint64_t* __restrict__ out) {
   MPC3_AES_SMEM4();
-  SmemTables4 tab = aes_smem_init4(sm, rk_dev, 1);
+  SmemTables4 tab = aes_smem_init4(sm, nullptr, 0);
   uint64_t nblk = ((word_off + count - 1) >> 1) - (word_off >> 1) + 1;
-  GRID_LOOP(t, nblk) prf_words_item(tab, sm.rk[0], h, word_off, count, out, t);
+  GRID_LOOP(t, nblk) prf_words_item(tab, ks.rk[0], h, word_off, count, out, t);
 }
 
-__global__ void __launch_bounds__(kProtoThreads) zero_share_kernel(const uint32_t* __restrict__ rk3,
+__global__ void __launch_bounds__(kProtoThreads) zero_share_kernel(const __grid_constant__ KeySched ks,
                                                              const uint64_t* __restrict__ ctr, StreamRef rh,
                                                              int xor_mode, uint64_t n, uint64_t* __restrict__ out) {
   MPC3_PROTO_SMEM();
   StreamHead h = resolve(rh, ctr);
-  ProtoTables tab = MPC3_PROTO_INIT(sm, rk3, 3);
-  GRID_LOOP(b, (n + 1) >> 1) zero_share_item(tab, &sm.rk[0][0], h, xor_mode, n, out, b);
+  ProtoTables tab = MPC3_PROTO_INIT(sm, nullptr, 0);
+  GRID_LOOP(b, (n + 1) >> 1) zero_share_item(tab, &ks.rk[0][0], h, xor_mode, n, out, b);
 }
 
 // ---------------------------------------------------------------------------
@@ -169,15 +201,15 @@ __global__ void ring_rowsum_kernel(const uint64_t* __restrict__ a, uint64_t* __r
 // ---------------------------------------------------------------------------
 // protocols
 
-__global__ void __launch_bounds__(kProtoThreads) arith_kernel(int kind, const uint32_t* __restrict__ rk3,
+__global__ void __launch_bounds__(kProtoThreads) arith_kernel(int kind, const __grid_constant__ KeySched ks,
                                                         const uint64_t* __restrict__ ctr, StreamRef ra,
                                                         StreamRef rrho, StreamRef rr, int bits, const uint64_t* __restrict__ x,
                                                         const uint64_t* __restrict__ y,
                                                         uint64_t* __restrict__ out, uint64_t n, uint64_t pb0) {
   MPC3_PROTO_SMEM();
-  ProtoTables tab = MPC3_PROTO_INIT(sm, rk3, 3);
+  ProtoTables tab = MPC3_PROTO_INIT(sm, nullptr, 0);
   StreamHead ha = resolve(ra, ctr), hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
-  GRID_LOOP(b, (n + 1) >> 1) arith_item(tab, &sm.rk[0][0], kind, ha, hrho, hr, bits, x, y, out, n, b, pb0);
+  GRID_LOOP(b, (n + 1) >> 1) arith_item(tab, &ks.rk[0][0], kind, ha, hrho, hr, bits, x, y, out, n, b, pb0);
 }
 
 struct SignArgs {
@@ -186,7 +218,7 @@ struct SignArgs {
 
 // Large tensors: one 512-thread CTA per SM with the four-table AES layout
 // (128 KiB) — the kernel is nothing but AES rounds.
-__global__ void __launch_bounds__(kSignThreads, 1) sign_kernel(const uint32_t* __restrict__ rk3,
+__global__ void __launch_bounds__(kSignThreads, 1) sign_kernel(const __grid_constant__ KeySched ks,
                                                           const uint64_t* __restrict__ ctr, SignArgs args,
                                                           int mode, const uint64_t* __restrict__ x,
                                                           uint64_t* __restrict__ out,
@@ -200,8 +232,8 @@ __global__ void __launch_bounds__(kSignThreads, 1) sign_kernel(const uint32_t* _
     for (int l = 0; l < 7; ++l) st.x[l] = resolve(sref(XOR_ZERO, args.jxor + l), ctr);
     for (int l = 0; l < 3; ++l) st.a[l] = resolve(sref(ARITH_ZERO, args.ja + l), ctr);
   }
-  SmemTables4 tab = aes_smem_init4(sm, rk3, 3);  // includes the barrier
-  GRID_LOOP(b, (n + 1) >> 1) sign_item(tab, &sm.rk[0][0], st, mode, x, out, mask, n, n_total, elem_off, b, plane);
+  SmemTables4 tab = aes_smem_init4(sm, nullptr, 0);  // includes the barrier
+  GRID_LOOP(b, (n + 1) >> 1) sign_item(tab, &ks.rk[0][0], st, mode, x, out, mask, n, n_total, elem_off, b, plane);
 }
 
 // Two-phase sign circuit.  The 46 AES blocks an element pair consumes do not
@@ -218,7 +250,7 @@ __global__ void __launch_bounds__(kSignThreads, 1) sign_kernel(const uint32_t* _
 constexpr int SW_SLOT_BYTES = 3 * (int)sizeof(Word2);
 HD int sign_slots(bool straddle) { return straddle ? 21 : 16; }
 
-__global__ void __launch_bounds__(kThreads, 2) sign2_kernel(const uint32_t* __restrict__ rk3,
+__global__ void __launch_bounds__(kThreads, 2) sign2_kernel(const __grid_constant__ KeySched ks,
                                                            const uint64_t* __restrict__ ctr, SignArgs args, int mode,
                                                            const uint64_t* __restrict__ x, uint64_t* __restrict__ out,
                                                            uint64_t* __restrict__ mask, uint64_t n, uint64_t n_total,
@@ -230,7 +262,7 @@ __global__ void __launch_bounds__(kThreads, 2) sign2_kernel(const uint32_t* __re
     for (int l = 0; l < 7; ++l) st.x[l] = resolve(sref(XOR_ZERO, args.jxor + l), ctr);
     for (int l = 0; l < 3; ++l) st.a[l] = resolve(sref(ARITH_ZERO, args.ja + l), ctr);
   }
-  SmemTables tab = aes_smem_init(sm, rk3, 3);
+  SmemTables tab = aes_smem_init(sm, nullptr, 0);
   Word2* slots = reinterpret_cast<Word2*>(mpc3_dsm + sizeof(AesSmem));
   const bool straddle = (n_total & 1) != 0;
   const int L = straddle ? 3 : 2;  // slots per level 1..5
@@ -244,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, 2) sign2_kernel(const uint32_t* __re
       const uint64_t blk = (elem_off >> 1) + c0 + p;
       Word2* dst = slots + ((size_t)s * P + p) * 3;
       if (s == 0) {
-        dst[0] = prf_block(tab, &sm.rk[0][0], st.bin, blk);
+        dst[0] = prf_block(tab, &ks.rk[0][0], st.bin, blk);
         continue;
       }
       StreamHead h;
@@ -261,7 +293,7 @@ __global__ void __launch_bounds__(kThreads, 2) sign2_kernel(const uint32_t* __re
         h = st.a[s - 3 - 5 * L];
       }
       Word2 w[3];
-      prf_block3(tab, &sm.rk[0][0], h, b, w);
+      prf_block3(tab, &ks.rk[0][0], h, b, w);
       dst[0] = w[0];
       dst[1] = w[1];
       dst[2] = w[2];
@@ -273,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, 2) sign2_kernel(const uint32_t* __re
       rp.P = P;
       rp.p = threadIdx.x;
       rp.slot = 0;
-      sign_item(rp, &sm.rk[0][0], st, mode, x, out, mask, n, n_total, elem_off, c0 + threadIdx.x, plane);
+      sign_item(rp, &ks.rk[0][0], st, mode, x, out, mask, n, n_total, elem_off, c0 + threadIdx.x, plane);
     }
     __syncthreads();
   }
@@ -292,16 +324,16 @@ struct ChainProgram {
 };
 constexpr int CH_SLOT_WORDS = 5;  // ARITH k0..k2, RHO (k2), R (k1)
 
-__global__ void __launch_bounds__(kThreads, 1) chain_kernel(const uint32_t* __restrict__ rk3,
+__global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constant__ KeySched ks,
                                                            const uint64_t* __restrict__ ctr, ChainProgram prog,
                                                            uint64_t ja, uint64_t jrho, uint64_t jr,
                                                            const uint64_t* __restrict__ x, uint64_t* __restrict__ out,
                                                            uint64_t n, uint64_t pb0, int P) {
   MPC3_AES_SMEM();
-  SmemTables tab = aes_smem_init(sm, rk3, 3);
+  SmemTables tab = aes_smem_init(sm, nullptr, 0);
   Word2* slots = reinterpret_cast<Word2*>(mpc3_dsm + sizeof(AesSmem));
   const uint64_t npairs = (n + 1) >> 1;
-  const uint32_t* rk = &sm.rk[0][0];
+  const uint32_t* rk = &ks.rk[0][0];
   for (uint64_t c0 = (uint64_t)blockIdx.x * P; c0 < npairs; c0 += (uint64_t)gridDim.x * P) {
     for (int q = threadIdx.x; q < prog.nmul * P; q += blockDim.x) {
       const int k = q / P, p = q % P;
@@ -374,11 +406,11 @@ struct SgdTable {
   uint64_t pair0[MPC3_SGD_MAX_TENSORS + 1];  // first pair of tensor i in the flattened range
 };
 
-__global__ void __launch_bounds__(kProtoThreads) sgd_kernel(const uint32_t* __restrict__ rk3,
+__global__ void __launch_bounds__(kProtoThreads) sgd_kernel(const __grid_constant__ KeySched ks,
                                                       const uint64_t* __restrict__ ctr, SgdTable tb, int bits,
                                                       uint64_t c) {
   MPC3_PROTO_SMEM();
-  ProtoTables tab = MPC3_PROTO_INIT(sm, rk3, 3);
+  ProtoTables tab = MPC3_PROTO_INIT(sm, nullptr, 0);
   const uint64_t total = tb.pair0[tb.nt];
   GRID_LOOP(q, total) {
     int i = 0;
@@ -386,7 +418,7 @@ __global__ void __launch_bounds__(kProtoThreads) sgd_kernel(const uint32_t* __re
     const MPC3SgdTensor& T = tb.t[i];
     const uint64_t b = q - tb.pair0[i], n = T.n;
     Word2 rho, r;
-    trunc_words(tab, &sm.rk[0][0], resolve(sref(TRUNC_RHO, T.j_rho), ctr), resolve(sref(TRUNC_R, T.j_r), ctr), b, rho,
+    trunc_words(tab, &ks.rk[0][0], resolve(sref(TRUNC_RHO, T.j_rho), ctr), resolve(sref(TRUNC_R, T.j_r), ctr), b, rho,
                 r);
     for (int e = 0; e < 2; ++e) {
       const uint64_t f = 2 * b + e;
@@ -401,61 +433,61 @@ __global__ void __launch_bounds__(kProtoThreads) sgd_kernel(const uint32_t* __re
   }
 }
 
-__global__ void __launch_bounds__(kProtoThreads) inject_kernel(const uint32_t* __restrict__ rk3,
+__global__ void __launch_bounds__(kProtoThreads) inject_kernel(const __grid_constant__ KeySched ks,
                                                          const uint64_t* __restrict__ ctr, StreamRef r0,
                                                          StreamRef r1, const uint64_t* __restrict__ bits,
                                                          uint64_t* __restrict__ out, uint64_t n) {
   MPC3_PROTO_SMEM();
-  ProtoTables tab = MPC3_PROTO_INIT(sm, rk3, 3);
+  ProtoTables tab = MPC3_PROTO_INIT(sm, nullptr, 0);
   StreamHead a0 = resolve(r0, ctr), a1 = resolve(r1, ctr);
-  GRID_LOOP(b, (n + 1) >> 1) inject_item(tab, &sm.rk[0][0], a0, a1, bits, out, n, b);
+  GRID_LOOP(b, (n + 1) >> 1) inject_item(tab, &ks.rk[0][0], a0, a1, bits, out, n, b);
 }
 
-__global__ void __launch_bounds__(kProtoThreads) reshare_trunc_kernel(const uint32_t* __restrict__ rk3,
+__global__ void __launch_bounds__(kProtoThreads) reshare_trunc_kernel(const __grid_constant__ KeySched ks,
                                                                 const uint64_t* __restrict__ ctr, StreamRef ra,
                                                                 StreamRef rrho, StreamRef rr, int bits,
                                                                 const uint64_t* __restrict__ z, View4 v,
                                                                 uint64_t* __restrict__ out, uint64_t n,
                                                                 uint64_t pb0) {
   MPC3_PROTO_SMEM();
-  ProtoTables tab = MPC3_PROTO_INIT(sm, rk3, 3);
+  ProtoTables tab = MPC3_PROTO_INIT(sm, nullptr, 0);
   StreamHead ha = resolve(ra, ctr), hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
   if (n < (1ull << 32))
-    GRID_LOOP(b, (n + 1) >> 1) reshare_trunc_item<ProtoTables, uint32_t>(tab, &sm.rk[0][0], ha, hrho, hr, bits, z, v, out,
+    GRID_LOOP(b, (n + 1) >> 1) reshare_trunc_item<ProtoTables, uint32_t>(tab, &ks.rk[0][0], ha, hrho, hr, bits, z, v, out,
                                                                          n, b, pb0);
   else
-    GRID_LOOP(b, (n + 1) >> 1) reshare_trunc_item(tab, &sm.rk[0][0], ha, hrho, hr, bits, z, v, out, n, b, pb0);
+    GRID_LOOP(b, (n + 1) >> 1) reshare_trunc_item(tab, &ks.rk[0][0], ha, hrho, hr, bits, z, v, out, n, b, pb0);
 }
 
-__global__ void __launch_bounds__(kProtoThreads) pool_kernel(const uint32_t* __restrict__ rk3,
+__global__ void __launch_bounds__(kProtoThreads) pool_kernel(const __grid_constant__ KeySched ks,
                                                        const uint64_t* __restrict__ ctr, int backward,
                                                        StreamRef rrho, StreamRef rr, int bits, uint64_t mulc,
                                                        const uint64_t* __restrict__ x,
                                                        uint64_t* __restrict__ out, PoolGeom p, uint64_t n,
                                                        uint64_t pb0) {
   MPC3_PROTO_SMEM();
-  ProtoTables tab = MPC3_PROTO_INIT(sm, rk3, 3);
+  ProtoTables tab = MPC3_PROTO_INIT(sm, nullptr, 0);
   StreamHead hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
   if (2 * n < (1ull << 32) && (uint64_t)p.N * p.C * p.H * p.W < (1ull << 32))
-    GRID_LOOP(b, (n + 1) >> 1) pool_item<ProtoTables, uint32_t>(tab, &sm.rk[0][0], backward != 0, hrho, hr, bits, mulc, x,
+    GRID_LOOP(b, (n + 1) >> 1) pool_item<ProtoTables, uint32_t>(tab, &ks.rk[0][0], backward != 0, hrho, hr, bits, mulc, x,
                                                                 out, p, b, pb0);
   else
-    GRID_LOOP(b, (n + 1) >> 1) pool_item(tab, &sm.rk[0][0], backward != 0, hrho, hr, bits, mulc, x, out, p, b, pb0);
+    GRID_LOOP(b, (n + 1) >> 1) pool_item(tab, &ks.rk[0][0], backward != 0, hrho, hr, bits, mulc, x, out, p, b, pb0);
 }
 
-__global__ void __launch_bounds__(kProtoThreads) col2im_kernel(const uint32_t* __restrict__ rk3,
+__global__ void __launch_bounds__(kProtoThreads) col2im_kernel(const __grid_constant__ KeySched ks,
                                                          const uint64_t* __restrict__ ctr, StreamRef ra,
                                                          StreamRef rrho, StreamRef rr, int bits,
                                                          const uint64_t* __restrict__ z, Col2Im g,
                                                          uint64_t* __restrict__ out, uint64_t n, uint64_t pb0) {
   MPC3_PROTO_SMEM();
-  ProtoTables tab = MPC3_PROTO_INIT(sm, rk3, 3);
+  ProtoTables tab = MPC3_PROTO_INIT(sm, nullptr, 0);
   StreamHead ha = resolve(ra, ctr), hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
   if (2 * n < (1ull << 32))
-    GRID_LOOP(b, (n + 1) >> 1) col2im_item<ProtoTables, uint32_t>(tab, &sm.rk[0][0], ha, hrho, hr, bits, z, g, out, b,
+    GRID_LOOP(b, (n + 1) >> 1) col2im_item<ProtoTables, uint32_t>(tab, &ks.rk[0][0], ha, hrho, hr, bits, z, g, out, b,
                                                                   pb0);
   else
-    GRID_LOOP(b, (n + 1) >> 1) col2im_item(tab, &sm.rk[0][0], ha, hrho, hr, bits, z, g, out, b, pb0);
+    GRID_LOOP(b, (n + 1) >> 1) col2im_item(tab, &ks.rk[0][0], ha, hrho, hr, bits, z, g, out, b, pb0);
 }
 
 __global__ void sumpool_kernel(const uint64_t* __restrict__ x, uint64_t* __restrict__ out, PoolGeom p) {
@@ -514,9 +546,11 @@ int mpc3_prf_words(const uint32_t* rk, uint32_t purpose, uint64_t index, uint64_
   if (st) return st;
   if (count == 0) return MPC3_OK;
   uint64_t nblk = ((word_off + count - 1) >> 1) - (word_off >> 1) + 1;
+  KeySched ks;
+  if (int e = load_keys(rk, 1, stream, &ks)) return e;
   if (!aes_attr((const void*)prf_words_kernel, kAesSmem4Bytes)) return check_launch("prf smem attribute");
   launch_pdl(prf_words_kernel, dim3(grid_for(nblk, kSignThreads, 8)), dim3(kSignThreads), kAesSmem4Bytes,
-             as_stream(stream), rk, stream_head(purpose, index), word_off, count, words);
+             as_stream(stream), ks, stream_head(purpose, index), word_off, count, words);
   return check_launch("prf_words");
 }
 
@@ -525,8 +559,10 @@ int mpc3_rss_zero_share(const uint32_t* rk3, const uint64_t* ctr, uint32_t purpo
   int st = check_stream_args(purpose, index);
   if (st) return st;
   if (n == 0) return MPC3_OK;
+  KeySched ks;
+  if (int e = load_keys(rk3, 3, stream, &ks)) return e;
   AES_LAUNCH(zero_share_kernel, grid_for((n + 1) / 2, kProtoThreads, kProtoCtasPerSm), as_stream(stream), 
-      rk3, ctr, sref(purpose, index), xor_mode, n, out);
+      ks, ctr, sref(purpose, index), xor_mode, n, out);
   return check_launch("zero_share");
 }
 
@@ -560,8 +596,10 @@ static int arith_launch(int kind, const uint32_t* rk3, const uint64_t* ctr, uint
   if (ja >= (1ull << 48) || jrho >= (1ull << 48) || jr >= (1ull << 48)) return MPC3_ERR_RANGE;
   if (elem_off & 1) return MPC3_ERR_CONFIG;
   if (n == 0) return MPC3_OK;
+  KeySched ks;
+  if (int e = load_keys(rk3, 3, stream, &ks)) return e;
   AES_LAUNCH(arith_kernel, grid_for((n + 1) / 2, kProtoThreads, kProtoCtasPerSm), as_stream(stream), 
-      kind, rk3, ctr, sref(ARITH_ZERO, ja), sref(TRUNC_RHO, jrho), sref(TRUNC_R, jr), bits, x, y, out, n,
+      kind, ks, ctr, sref(ARITH_ZERO, ja), sref(TRUNC_RHO, jrho), sref(TRUNC_R, jr), bits, x, y, out, n,
       elem_off >> 1);
   return check_launch("rss_arith");
 }
@@ -595,7 +633,9 @@ int mpc3_rss_sgd_multi(const uint32_t* rk3, const uint64_t* ctr, const MPC3SgdTe
     tb.pair0[i + 1] = tb.pair0[i] + (ts[i].n + 1) / 2;
   }
   if (tb.pair0[nt] == 0) return MPC3_OK;
-  AES_LAUNCH(sgd_kernel, grid_for(tb.pair0[nt], kProtoThreads, kProtoCtasPerSm), as_stream(stream), rk3, ctr, tb, bits, c);
+  KeySched ks;
+  if (int e = load_keys(rk3, 3, stream, &ks)) return e;
+  AES_LAUNCH(sgd_kernel, grid_for(tb.pair0[nt], kProtoThreads, kProtoCtasPerSm), as_stream(stream), ks, ctr, tb, bits, c);
   return check_launch("rss_sgd_multi");
 }
 
@@ -623,10 +663,12 @@ int mpc3_rss_chain(const uint32_t* rk3, const uint64_t* ctr, const MPC3ChainStep
   while (P > 8 && P * prog.nmul * CH_SLOT_WORDS * (int)sizeof(Word2) > 96 * 1024) P >>= 1;
   if (P * (prog.nmul > 0 ? prog.nmul : 1) * CH_SLOT_WORDS * (int)sizeof(Word2) > 96 * 1024) return MPC3_ERR_CONFIG;
   const int smem = kAesSmemBytes + P * prog.nmul * CH_SLOT_WORDS * (int)sizeof(Word2);
+  KeySched ks;
+  if (int e = load_keys(rk3, 3, stream, &ks)) return e;
   if (!aes_attr((const void*)chain_kernel, kAesSmemBytes + 96 * 1024)) return check_launch("chain smem attribute");
   uint64_t chunks = ((n + 1) / 2 + P - 1) / P;
   unsigned grid = (unsigned)(chunks < 148 * 8 ? chunks : 148 * 8);
-  launch_pdl(chain_kernel, dim3(grid), dim3(kThreads), smem, as_stream(stream), rk3, ctr, prog, j_arith, j_rho, j_r,
+  launch_pdl(chain_kernel, dim3(grid), dim3(kThreads), smem, as_stream(stream), ks, ctr, prog, j_arith, j_rho, j_r,
              x, out, n, elem_off >> 1, P);
   return check_launch("rss_chain");
 }
@@ -644,6 +686,8 @@ int mpc3_rss_sign(const uint32_t* rk3, const uint64_t* ctr, int mode, uint64_t j
   a.jbin = j_bin;
   a.jxor = j_xor;
   a.ja = j_arith;
+  KeySched ks;
+  if (int e = load_keys(rk3, 3, stream, &ks)) return e;
   // large tensors: the single-phase kernel (throughput-bound, all threads in
   // the circuit) on a persistent grid, one 512-thread CTA per SM, every
   // thread exactly k pairs (no partial wave, no CTA-boundary bubbles); the
@@ -657,7 +701,7 @@ int mpc3_rss_sign(const uint32_t* rk3, const uint64_t* ctr, int mode, uint64_t j
     const uint64_t nm = main_pairs == pairs ? n : 2 * main_pairs;
     const unsigned grid = g_sign_fused ? grid_for(pairs, kSignThreads, 8) : 148;
     if (!aes_attr((const void*)sign_kernel, kAesSmem4Bytes)) return check_launch("sign smem attribute");
-    launch_pdl(sign_kernel, dim3(grid), dim3(kSignThreads), kAesSmem4Bytes, as_stream(stream), rk3, ctr, a, mode, x,
+    launch_pdl(sign_kernel, dim3(grid), dim3(kSignThreads), kAesSmem4Bytes, as_stream(stream), ks, ctr, a, mode, x,
                out, mask, nm, n_total, elem_off, n);
     if (check_launch("rss_sign")) return MPC3_ERR_CUDA;
   }
@@ -672,7 +716,7 @@ int mpc3_rss_sign(const uint32_t* rk3, const uint64_t* ctr, int mode, uint64_t j
       return check_launch("sign2 smem attribute");
     uint64_t chunks = ((nr + 1) / 2 + P - 1) / P;
     unsigned grid = (unsigned)(chunks < 148 * 2 * 8 ? chunks : 148 * 2 * 8);
-    launch_pdl(sign2_kernel, dim3(grid), dim3(kThreads), smem, as_stream(stream), rk3, ctr, a, mode, x + e0, out + e0,
+    launch_pdl(sign2_kernel, dim3(grid), dim3(kThreads), smem, as_stream(stream), ks, ctr, a, mode, x + e0, out + e0,
                mask ? mask + e0 : mask, nr, n_total, elem_off + e0, P, n);
     return check_launch("rss_sign2");
   }
@@ -683,8 +727,10 @@ int mpc3_rss_bit_inject(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_ari
                         uint64_t n, void* stream) {
   if (j_arith + 1 >= (1ull << 48)) return MPC3_ERR_RANGE;
   if (n == 0) return MPC3_OK;
+  KeySched ks;
+  if (int e = load_keys(rk3, 3, stream, &ks)) return e;
   AES_LAUNCH(inject_kernel, grid_for((n + 1) / 2, kProtoThreads, kProtoCtasPerSm), as_stream(stream), 
-      rk3, ctr, sref(ARITH_ZERO, j_arith), sref(ARITH_ZERO, j_arith + 1), bits, out, n);
+      ks, ctr, sref(ARITH_ZERO, j_arith), sref(ARITH_ZERO, j_arith + 1), bits, out, n);
   return check_launch("rss_bit_inject");
 }
 
@@ -719,8 +765,10 @@ int mpc3_rss_reshare_truncate_bias(const uint32_t* rk3, const uint64_t* ctr, uin
   v.bias_plane = bias_plane;
   v.bias_dim = bias_dim;
   if (n == 0) return MPC3_OK;
+  KeySched ks;
+  if (int e = load_keys(rk3, 3, stream, &ks)) return e;
   AES_LAUNCH(reshare_trunc_kernel, grid_for((n + 1) / 2, kProtoThreads, kProtoCtasPerSm), as_stream(stream), 
-      rk3, ctr, sref(ARITH_ZERO, j_arith), sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, z, v, out, n,
+      ks, ctr, sref(ARITH_ZERO, j_arith), sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, z, v, out, n,
       elem_off >> 1);
   return check_launch("rss_reshare_truncate");
 }
@@ -743,8 +791,10 @@ int mpc3_rss_avgpool(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_rho, u
   int64_t OH = (H + 2 * ph - kh) / sh + 1, OW = (W + 2 * pw - kw) / sw + 1;
   uint64_t n = (uint64_t)N * C * OH * OW;
   if (n == 0) return MPC3_OK;
+  KeySched ks;
+  if (int e = load_keys(rk3, 3, stream, &ks)) return e;
   AES_LAUNCH(pool_kernel, grid_for((n + 1) / 2, kProtoThreads, kProtoCtasPerSm), as_stream(stream), 
-      rk3, ctr, 0, sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, mulc, x, out,
+      ks, ctr, 0, sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, mulc, x, out,
       pool_geom(N, C, H, W, OH, OW, kh, kw, sh, sw, ph, pw), n, elem_off >> 1);
   return check_launch("rss_avgpool");
 }
@@ -758,8 +808,10 @@ int mpc3_rss_avgpool_backward(const uint32_t* rk3, const uint64_t* ctr, uint64_t
   if (kh < 1 || kw < 1 || sh < 1 || sw < 1 || ph < 0 || pw < 0) return MPC3_ERR_SHAPE;
   uint64_t n = (uint64_t)N * C * H * W;
   if (n == 0) return MPC3_OK;
+  KeySched ks;
+  if (int e = load_keys(rk3, 3, stream, &ks)) return e;
   AES_LAUNCH(pool_kernel, grid_for((n + 1) / 2, kProtoThreads, kProtoCtasPerSm), as_stream(stream), 
-      rk3, ctr, 1, sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, mulc, g, out,
+      ks, ctr, 1, sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, mulc, g, out,
       pool_geom(N, C, H, W, OH, OW, kh, kw, sh, sw, ph, pw), n, elem_off >> 1);
   return check_launch("rss_avgpool_backward");
 }
@@ -789,8 +841,10 @@ int mpc3_rss_col2im_reshare_truncate_layout(const uint32_t* rk3, const uint64_t*
   g.wf = (OW - 1) * sw + kw;
   uint64_t n = (uint64_t)N * C * g.hf * g.wf;
   if (n == 0) return MPC3_OK;
+  KeySched ks;
+  if (int e = load_keys(rk3, 3, stream, &ks)) return e;
   AES_LAUNCH(col2im_kernel, grid_for((n + 1) / 2, kProtoThreads, kProtoCtasPerSm), as_stream(stream), 
-      rk3, ctr, sref(ARITH_ZERO, j_arith), sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, z, g, out, n,
+      ks, ctr, sref(ARITH_ZERO, j_arith), sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, z, g, out, n,
       elem_off >> 1);
   return check_launch("rss_col2im_reshare_truncate");
 }

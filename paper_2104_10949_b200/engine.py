@@ -196,7 +196,11 @@ class TrioSession:
         self.session_id = session_id if session_id is not None else make_session_id(seed)
         self.keys = keys if keys is not None else session_keys(seed, self.session_id)
         rk = np.stack([k.round_keys for k in self.keys])
-        self.rk3 = torch.from_numpy(rk.view(np.int32).copy()).to(_dev())
+        # pinned host memory: the launches read the schedules on the host and
+        # pass them in the kernel parameters (constant bank on the device)
+        self.rk3 = torch.from_numpy(rk.view(np.int32).copy())
+        if torch.cuda.is_available():
+            self.rk3 = self.rk3.pin_memory()
         self.seq = {p: 0 for p in PURPOSES}
         self.ledger = Ledger()
         self.ctr = None  # optional device per-purpose counter base (CUDA-graph replay)
