@@ -1009,11 +1009,11 @@ int mpc3_ring_gemm_auto(const uint8_t* A, const uint8_t* B, uint64_t* C, int gro
   const int64_t ctas = tiles * splits;
   const double eff = (double)ctas / (double)(((ctas + sms - 1) / sms) * sms);
   const size_t cbytes = (size_t)groups * M * N * 8;
-  if (nkb == 0 || eff < 0.8 || splits > 1) {
+  if (nkb == 0 || eff < 0.85 || splits > 1) {
     if (cudaMemsetAsync(C, 0, cbytes, as_stream(stream)) != cudaSuccess) return check_launch("gemm C memset");
     if (nkb == 0) return MPC3_OK;
   }
-  if (eff < 0.8) {  // the split-K grid would leave SMs idle: stream-K over every SM
+  if (eff < 0.85) {  // the split-K grid would leave SMs idle: stream-K over every SM
     int64_t iters = tiles * nkb;
     int64_t c = iters / 2 < sms ? iters / 2 : sms;
     return mpc3_ring_gemm_streamk(A, B, C, groups, M, N, kp, ldc, c_group, (int)(c < 1 ? 1 : c), c_layout, stream);
