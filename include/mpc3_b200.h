@@ -146,6 +146,17 @@ typedef struct {
 int mpc3_rss_sgd_multi(const uint32_t* rk3, const uint64_t* ctr, const MPC3SgdTensor* ts, int nt, int bits,
                        uint64_t c, void* stream);
 
+/* One level of max_tree (protocols.py:356-380) on a (rows, m) trio tensor v
+ * (3 planes of rows*m words): out[r, j] = v[r, 2j+1] + relu(v[r, 2j] -
+ * v[r, 2j+1]) for j < m/2, and out[r, m/2] = v[r, m-1] when m is odd; out is
+ * (rows, m/2 + m%2).  The relu draws its words as mpc3_rss_sign mode 3 on the
+ * (rows, m/2) difference tensor (counters j_bin, j_xor..+6, j_arith..+2;
+ * elem_off / n_total for batch shards).  One launch instead of the
+ * slice / sub / relu / add / concat sequence. */
+int mpc3_rss_max_level(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_bin, uint64_t j_xor, uint64_t j_arith,
+                       const uint64_t* v, uint64_t* out, uint64_t rows, uint64_t m, uint64_t elem_off,
+                       uint64_t n_total, void* stream);
+
 /* Fused elementwise chain over a per-element trio z (starts as x), the chain
  * input x and a temporary t; replaces the launch-per-call sequences of
  * exp_approx (add_const + squarings, protocols.py:414-424) and reciprocal

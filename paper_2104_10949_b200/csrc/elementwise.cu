@@ -250,11 +250,12 @@ __global__ void __launch_bounds__(kSignThreads, 1) sign_kernel(const __grid_cons
 constexpr int SW_SLOT_BYTES = 3 * (int)sizeof(Word2);
 HD int sign_slots(bool straddle) { return straddle ? 21 : 16; }
 
+template <bool MAXL>
 __global__ void __launch_bounds__(kThreads, 2) sign2_kernel(const __grid_constant__ KeySched ks,
                                                            const uint64_t* __restrict__ ctr, SignArgs args, int mode,
                                                            const uint64_t* __restrict__ x, uint64_t* __restrict__ out,
                                                            uint64_t* __restrict__ mask, uint64_t n, uint64_t n_total,
-                                                           uint64_t elem_off, int P, uint64_t plane) {
+                                                           uint64_t elem_off, int P, uint64_t plane, MaxGeom mg) {
   MPC3_AES_SMEM();
   SignStreams& st = *reinterpret_cast<SignStreams*>(sm.extra);
   if (threadIdx.x == 0) {
@@ -305,9 +306,20 @@ __global__ void __launch_bounds__(kThreads, 2) sign2_kernel(const __grid_constan
       rp.P = P;
       rp.p = threadIdx.x;
       rp.slot = 0;
-      sign_item(rp, &ks.rk[0][0], st, mode, x, out, mask, n, n_total, elem_off, c0 + threadIdx.x, plane);
+      if constexpr (MAXL)
+        maxlevel_item(rp, &ks.rk[0][0], st, x, out, mg, n, n_total, elem_off, c0 + threadIdx.x);
+      else
+        sign_item(rp, &ks.rk[0][0], st, mode, x, out, mask, n, n_total, elem_off, c0 + threadIdx.x, plane);
     }
     __syncthreads();
+  }
+  if constexpr (MAXL) {  // odd m: the last column passes through to the last output column
+    if (mg.m & 1) {
+      const uint64_t pv = mg.rows * mg.m, mo = mg.k + 1, po = mg.rows * mo;
+      for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < mg.rows;
+           r += (uint64_t)gridDim.x * blockDim.x)
+        store_trio(out, po, r * mo + mg.k, load_trio(x, pv, r * mg.m + mg.m - 1));
+    }
   }
 }
 
@@ -712,15 +724,42 @@ int mpc3_rss_sign(const uint32_t* rk3, const uint64_t* ctr, int mode, uint64_t j
     const bool straddle = (n_total & 1) != 0;
     const int P = straddle ? 32 : 64;
     const int smem = kAesSmemBytes + P * sign_slots(straddle) * SW_SLOT_BYTES;
-    if (!aes_attr((const void*)sign2_kernel, kAesSmemBytes + 64 * sign_slots(false) * SW_SLOT_BYTES))
+    if (!aes_attr((const void*)sign2_kernel<false>, kAesSmemBytes + 64 * sign_slots(false) * SW_SLOT_BYTES))
       return check_launch("sign2 smem attribute");
     uint64_t chunks = ((nr + 1) / 2 + P - 1) / P;
     unsigned grid = (unsigned)(chunks < 148 * 2 * 8 ? chunks : 148 * 2 * 8);
-    launch_pdl(sign2_kernel, dim3(grid), dim3(kThreads), smem, as_stream(stream), ks, ctr, a, mode, x + e0, out + e0,
-               mask ? mask + e0 : mask, nr, n_total, elem_off + e0, P, n);
+    launch_pdl(sign2_kernel<false>, dim3(grid), dim3(kThreads), smem, as_stream(stream), ks, ctr, a, mode, x + e0,
+               out + e0, mask ? mask + e0 : mask, nr, n_total, elem_off + e0, P, n, MaxGeom{0, 0, 1});
     return check_launch("rss_sign2");
   }
   return MPC3_OK;
+}
+
+int mpc3_rss_max_level(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_bin, uint64_t j_xor, uint64_t j_arith,
+                       const uint64_t* v, uint64_t* out, uint64_t rows, uint64_t m, uint64_t elem_off,
+                       uint64_t n_total, void* stream) {
+  if (m < 2) return MPC3_ERR_SHAPE;
+  if (elem_off & 1) return MPC3_ERR_CONFIG;
+  const uint64_t k = m / 2, n = rows * k;
+  if (elem_off + n > n_total) return MPC3_ERR_SHAPE;
+  if (j_bin >= (1ull << 48) || j_xor + 6 >= (1ull << 48) || j_arith + 2 >= (1ull << 48)) return MPC3_ERR_RANGE;
+  if (n == 0) return MPC3_OK;
+  KeySched ks;
+  if (int e = load_keys(rk3, 3, stream, &ks)) return e;
+  SignArgs a;
+  a.jbin = j_bin;
+  a.jxor = j_xor;
+  a.ja = j_arith;
+  const bool straddle = (n_total & 1) != 0;
+  const int P = straddle ? 32 : 64;
+  const int smem = kAesSmemBytes + P * sign_slots(straddle) * SW_SLOT_BYTES;
+  if (!aes_attr((const void*)sign2_kernel<true>, kAesSmemBytes + 64 * sign_slots(false) * SW_SLOT_BYTES))
+    return check_launch("max_level smem attribute");
+  uint64_t chunks = ((n + 1) / 2 + P - 1) / P;
+  unsigned grid = (unsigned)(chunks < 148 * 2 * 8 ? chunks : 148 * 2 * 8);
+  launch_pdl(sign2_kernel<true>, dim3(grid), dim3(kThreads), smem, as_stream(stream), ks, ctr, a, (int)MODE_RELU, v,
+             out, (uint64_t*)nullptr, n, n_total, elem_off, P, (uint64_t)0, MaxGeom{rows, m, k});
+  return check_launch("rss_max_level");
 }
 
 int mpc3_rss_bit_inject(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, const uint64_t* bits, uint64_t* out,

@@ -101,6 +101,43 @@ HD void sign_item(const T& tab, const uint32_t* rk3, const SignStreams& st, int 
   }
 }
 
+// One max_tree level (protocols.py:356-380) on rows of a (rows, m) trio
+// tensor v: element f = (row, j), j < k = m / 2, is relu(v[row, 2j] -
+// v[row, 2j+1]) with the relu's PRF words at flat index f of the (rows, k)
+// difference tensor; the output max is v[row, 2j+1] + that relu, written to
+// out[row, j] of the (rows, k + m % 2) result.
+struct MaxGeom {
+  uint64_t rows, m, k;
+};
+template <class T>
+HD void maxlevel_item(const T& tab, const uint32_t* rk3, const SignStreams& st, const uint64_t* v, uint64_t* out,
+                      const MaxGeom& g, uint64_t n, uint64_t n_total, uint64_t elem_off, uint64_t b) {
+  const bool two = 2 * b + 1 < n;
+  const uint64_t pv = g.rows * g.m, mo = g.k + (g.m & 1), po = g.rows * mo;
+  struct Loader {
+    const uint64_t* v;
+    uint64_t pv, m, k, e0;
+    bool two;
+    HD Trio operator()(int e) const {
+      const uint64_t f = (e && two) ? e0 + 1 : e0;
+      const uint64_t row = f / k, j = f - row * k;
+      const Trio a = load_trio(v, pv, row * m + 2 * j), c = load_trio(v, pv, row * m + 2 * j + 1);
+      Trio d;
+      for (int i = 0; i < 3; ++i) d.c[i] = a.c[i] - c.c[i];
+      return d;
+    }
+  } ld{v, pv, g.m, g.k, 2 * b, two};
+  Trio o[2], mk[2];
+  sign_circuit_pair(tab, rk3, st, n_total, (elem_off >> 1) + b, MODE_RELU, ld, o, mk);
+  for (int e = 0; e < (two ? 2 : 1); ++e) {
+    const uint64_t f = 2 * b + e, row = f / g.k, j = f - row * g.k;
+    const Trio c = load_trio(v, pv, row * g.m + 2 * j + 1);
+    Trio r;
+    for (int i = 0; i < 3; ++i) r.c[i] = c.c[i] + o[e].c[i];
+    store_trio(out, po, row * mo + j, r);
+  }
+}
+
 template <class T>
 HD void inject_item(const T& tab, const uint32_t* rk3, StreamHead a0, StreamHead a1, const uint64_t* bits,
                     uint64_t* out, uint64_t n, uint64_t b) {

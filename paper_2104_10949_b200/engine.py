@@ -447,6 +447,11 @@ class TrioSession:
         off, n_total = self.shard_offset(n)
         K.call("mpc3_rss_sign", self.rk, self.ctr_ptr, mode, jb, jx, ja, x.data.data_ptr(), out.data.data_ptr(),
                None if mask is None else mask.data.data_ptr(), n, n_total, off, _stream())
+        self._charge_sign(n, mode)
+        return out, mask
+
+    def _charge_sign(self, n: int, mode: int) -> None:
+        """Rounds / bytes of the a2b + Kogge-Stone + inject + mask circuit."""
         L = self.ledger
         L.round("share.a2b", [(0, 2, n)])
         L.ring("and.ks.g", n)
@@ -457,7 +462,6 @@ class TrioSession:
             L.ring("mul.inject", n)
         if mode == K.MODE_RELU:
             L.ring("mul.mask", n)
-        return out, mask
 
     def a2b(self, x):
         return self._sign(x, K.MODE_A2B)[0]
@@ -741,15 +745,24 @@ class TrioSession:
         m = v.shape[-1] if v.ndim else 0
         if m < 1:
             raise ShapeError("max_tree needs at least one element")
+        lead = v.shape[:-1]
+        rows = int(np.prod(lead, dtype=np.int64)) if lead else 1
+        v = v.contiguous()
         while m > 1:
-            k = m // 2
-            a = v.apply(lambda d: d[..., 0:2 * k:2].contiguous())
-            b = v.apply(lambda d: d[..., 1:2 * k:2].contiguous())
-            mx = self.add(b, self.relu(self.sub(a, b)))
-            if m % 2:
-                mx = RssTensor(torch.cat([mx.data, v.data[..., -1:]], dim=-1), v.fp)
-            v = mx
-            m = v.shape[-1]
+            # one launch per level: b + relu(a - b) over the (even, odd) column
+            # pairs, the odd tail passed through (mpc3_rss_max_level); counters
+            # and accounting are those of the relu on the (rows, m/2) difference
+            k, mo = m // 2, m // 2 + m % 2
+            out = empty(lead + (mo,), v.fp)
+            n = rows * k
+            jb = self.take(BIN)
+            jx = self.take(XOR, 7)
+            ja = self.take(ARITH, 3)
+            off, n_total = self.shard_offset(n)
+            K.call("mpc3_rss_max_level", self.rk, self.ctr_ptr, jb, jx, ja, v.data.data_ptr(), out.data.data_ptr(),
+                   rows, m, off, n_total, _stream())
+            self._charge_sign(n, K.MODE_RELU)
+            v, m = out, mo
         return v.apply(lambda d: d[..., 0].contiguous())
 
     def exp_approx(self, x: RssTensor, cfg: ExpConfig = ExpConfig()) -> RssTensor:
