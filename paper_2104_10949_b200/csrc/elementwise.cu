@@ -707,11 +707,16 @@ int mpc3_rss_sign(const uint32_t* rk3, const uint64_t* ctr, int mode, uint64_t j
   const uint64_t pairs = (n + 1) / 2;
   const uint64_t persist = 148ull * kSignThreads;
   uint64_t main_pairs = 0;
-  if (!g_sign_fused && pairs > kSign2MaxPairs) main_pairs = pairs / persist * persist;
+  if (!g_sign_fused && pairs > kSign2MaxPairs) {
+    main_pairs = pairs / persist * persist;
+    // a remainder above half a round costs more in the two-phase kernel than
+    // one more pair for part of the persistent threads
+    if ((pairs - main_pairs) * 2 > persist) main_pairs = pairs;
+  }
   if (g_sign_fused) main_pairs = pairs;
   if (main_pairs) {
     const uint64_t nm = main_pairs == pairs ? n : 2 * main_pairs;
-    const unsigned grid = g_sign_fused ? grid_for(pairs, kSignThreads, 8) : 148;
+    const unsigned grid = g_sign_fused ? grid_for(pairs, kSignThreads, 8) : grid_for(main_pairs, kSignThreads, 1);
     if (!aes_attr((const void*)sign_kernel, kAesSmem4Bytes)) return check_launch("sign smem attribute");
     launch_pdl(sign_kernel, dim3(grid), dim3(kSignThreads), kAesSmem4Bytes, as_stream(stream), ks, ctr, a, mode, x,
                out, mask, nm, n_total, elem_off, n);
