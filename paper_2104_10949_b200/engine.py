@@ -397,23 +397,39 @@ class TrioSession:
         """params[i] -= truncate(mul_const(grads[i], c)) for all i in ONE launch
         (mpc3_rss_sgd_multi); the counters and accounting are those of the
         per-parameter truncate calls, in order."""
+        self.sgd_launch(self.sgd_plan(params, grads, bits), range(len(params)), c)
+
+    def sgd_plan(self, params, grads, bits: int | None = None):
+        """Take every parameter's truncation counters, in parameter order (the
+        order the per-parameter truncate calls would take them), so that the
+        updates can then be launched in any grouping (sgd_launch)."""
         bits = self.fp.t if bits is None else bits
         if not 1 <= bits <= 61:
             raise RangeError(f"truncation by {bits} bits outside [1, 61]")
-        for i in range(0, len(params), K.SGD_MAX_TENSORS):
-            chunk = list(zip(params[i:i + K.SGD_MAX_TENSORS], grads[i:i + K.SGD_MAX_TENSORS]))
-            arr = (K.SgdTensor * max(1, len(chunk)))()
+        plan = []
+        for p, g in zip(params, grads):
+            if not p.data.is_contiguous() or p.shape != g.shape:
+                raise ShapeError("in-place SGD needs contiguous parameters of the gradient's shape")
+            jr, jq = self.take(TR_RHO), self.take(TR_R)
+            self._charge_trunc(p.numel)
+            plan.append((p, g, jr, jq, bits))
+        return plan
+
+    def sgd_launch(self, plan, which, c: int) -> None:
+        idx = list(which)
+        for i in range(0, len(idx), K.SGD_MAX_TENSORS):
+            chunk = [plan[j] for j in idx[i:i + K.SGD_MAX_TENSORS]]
+            if not chunk:
+                continue
+            arr = (K.SgdTensor * len(chunk))()
             held = []  # contiguous gradient copies stay alive until the launch
-            for e, (p, g) in enumerate(chunk):
-                if not p.data.is_contiguous() or p.shape != g.shape:
-                    raise ShapeError("in-place SGD needs contiguous parameters of the gradient's shape")
+            for e, (p, g, jr, jq, _) in enumerate(chunk):
                 g = g.contiguous()
                 held.append(g)
-                jr, jq = self.take(TR_RHO), self.take(TR_R)
                 arr[e].param, arr[e].grad, arr[e].n, arr[e].j_rho, arr[e].j_r = (
                     p.data.data_ptr(), g.data.data_ptr(), p.numel, jr, jq)
-                self._charge_trunc(p.numel)
-            K.call("mpc3_rss_sgd_multi", self.rk, self.ctr_ptr, arr, len(chunk), bits, int(c) % (1 << 64), _stream())
+            K.call("mpc3_rss_sgd_multi", self.rk, self.ctr_ptr, arr, len(chunk), chunk[0][4], int(c) % (1 << 64),
+                   _stream())
 
     def mul_truncate(self, x, y, bits=None, label="mul.reshare") -> RssTensor:
         """truncate(mul(x, y)) in one launch; same counters and accounting."""

@@ -267,8 +267,11 @@ class TrioNet:
                 acts.append(("residual",) if record else None)
         return h, acts
 
-    def backward(self, model: ModelGraph, acts, grad_out: RssTensor, batch_bits: int = 0) -> list:
-        """nn.py:502-536."""
+    def backward(self, model: ModelGraph, acts, grad_out: RssTensor, batch_bits: int = 0, sgd=None) -> list:
+        """nn.py:502-536.  sgd = (params, lr): also apply the in-place SGD
+        update (nn.py:539-543) — every parameter but the first layer's is
+        updated on the main stream while the first layer's weight gradient
+        (the last one, on the side stream) is still running."""
         if acts is None or len(acts) != len(model.layers) or any(a is None for a in acts):
             raise ProtocolError("missing activation cache; run the forward pass with recording")
         if not model.trainable:
@@ -298,8 +301,18 @@ class TrioNet:
             with torch.cuda.stream(side):
                 return fn(*args)
 
+        rest_done = None  # side-stream event: every weight gradient but the first layer's
+
+        def mark_rest():
+            nonlocal rest_done
+            if side is not None:
+                rest_done = torch.cuda.Event()
+                rest_done.record(side)
+
         for li in range(len(model.layers) - 1, -1, -1):
             spec, cached = model.layers[li], acts[li]
+            if li == plist[0]:
+                mark_rest()
             if spec.kind == FULLY_CONNECTED:
                 x, w = cached
                 pi -= 1
@@ -322,8 +335,24 @@ class TrioNet:
                 g = S.mul(g, cached[0], "mul.mask")
             elif spec.kind == FLATTEN:
                 g = g.contiguous().reshape(cached[0])
+        plan = None
+        if sgd is not None:
+            params, lr = sgd
+            c = int(fx_encode(lr, S.fp))
+            if c != 0:
+                with S.replicated():  # parameters are replicated, not batch-sharded
+                    plan = S.sgd_plan(params, grads)
+                    if rest_done is not None and len(params) > 1:
+                        main.wait_event(rest_done)
+                        S.sgd_launch(plan, range(1, len(params)), c)  # overlaps the first layer's wgrad
+                        rest = [0]
+                    else:
+                        rest = range(len(params))
         if side is not None:
             main.wait_stream(side)
+        if plan is not None:
+            with S.replicated():
+                S.sgd_launch(plan, rest, c)
         del keep
         return grads
 
@@ -433,8 +462,7 @@ class TrainState:
         g = net.loss_grad(logits, ys)
         if self.bbits == 0:
             g = S.truncate(S.mul_const(g, self.inv_b))
-        grads = net.backward(self.model, acts, g, self.bbits)
-        self.params = net.sgd(self.params, grads, self.cfg.learning_rate, inplace=True)
+        net.backward(self.model, acts, g, self.bbits, sgd=(self.params, self.cfg.learning_rate))
         return logits
 
     def capture(self, xs: RssTensor, ys: RssTensor) -> "GraphStep":
