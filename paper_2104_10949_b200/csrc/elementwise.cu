@@ -50,7 +50,6 @@ bool pdl_enabled() {
   return on;
 }
 
-constexpr uint64_t kSign2MaxPairs = 200000;  // measured crossover (profiles/README.md)
 // MPC3_SIGN_FUSED=1 selects the single-phase sign kernel (AES inline in the circuit)
 static const bool g_sign_fused = [] {
   const char* e = getenv("MPC3_SIGN_FUSED");
@@ -707,11 +706,14 @@ int mpc3_rss_sign(const uint32_t* rk3, const uint64_t* ctr, int mode, uint64_t j
   const uint64_t pairs = (n + 1) / 2;
   const uint64_t persist = 148ull * kSignThreads;
   uint64_t main_pairs = 0;
-  if (!g_sign_fused && pairs > kSign2MaxPairs) {
+  if (!g_sign_fused) {
+    // whole rounds of the persistent grid (one pair per thread per round; a
+    // lone pair's 46 dependent AES blocks take ~55 us, so tensors below one
+    // round go to the two-phase kernel entirely); a remainder above half a
+    // round costs more in the two-phase kernel than one more pair for part of
+    // the persistent threads
     main_pairs = pairs / persist * persist;
-    // a remainder above half a round costs more in the two-phase kernel than
-    // one more pair for part of the persistent threads
-    if ((pairs - main_pairs) * 2 > persist) main_pairs = pairs;
+    if (main_pairs && (pairs - main_pairs) * 2 > persist) main_pairs = pairs;
   }
   if (g_sign_fused) main_pairs = pairs;
   if (main_pairs) {
