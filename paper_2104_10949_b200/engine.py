@@ -654,11 +654,26 @@ class TrioSession:
             return self._finish(z, view, out, bits, "mul.reshare")
 
     def conv2d_dgrad(self, g: RssTensor, k: RssTensor, stride, padding, in_shape, bits) -> RssTensor:
-        """Input gradient (nn.py:460-484) as a transposed convolution: one
-        ring GEMM cols = g^T-rows x k (inner length O) and a fused
-        col2im + reshare + truncate + embed kernel.  Equal mod 2^64 to the
-        reference's correlation of the dilated, padded gradient with the
-        flipped kernel, with the PRF words at the reference's flat indices."""
+        """Input gradient (nn.py:460-484).  Two bit-identical formulations
+        (same ring values, same PRF words at the reference's flat indices of
+        the full (N, C, hf, wf) correlation); the cheaper one for the shape:
+        the transposed convolution (GEMM with inner length O + col2im) when O
+        is large relative to the spatial size, the reference's correlation of
+        the padded gradient with the flipped kernel (GEMM with inner length
+        O*kh*kw, no col2im) for stride 1 when O is small — e.g. VGG's 64-channel
+        layers, where the first would be a K=64 GEMM writing kh*kw times the
+        input gradient."""
+        nb, o, oh, ow = g.shape
+        o2, c, kh, kw = k.shape
+        if stride == (1, 1) or tuple(stride) == (1, 1):
+            if _dgrad_cost_im2col(nb, o, oh, ow, c, kh, kw, padding) < _dgrad_cost_col2im(nb, o, oh, ow, c, kh, kw):
+                return self.conv2d_dgrad_im2col(g, k, stride, padding, in_shape, bits)
+        return self.conv2d_dgrad_col2im(g, k, stride, padding, in_shape, bits)
+
+    def conv2d_dgrad_col2im(self, g: RssTensor, k: RssTensor, stride, padding, in_shape, bits) -> RssTensor:
+        """Input gradient as a transposed convolution: one ring GEMM
+        cols = g^T-rows x k (inner length O) and a fused col2im + reshare +
+        truncate + embed kernel."""
         nb, o, oh, ow = g.shape
         o2, c, kh, kw = k.shape
         sh, sw = stride
@@ -835,6 +850,29 @@ class TrioSession:
 
 # ---------------------------------------------------------------------------
 # kernel helpers
+
+
+def _gemm_us(M, N, K2):
+    """Rough ring-GEMM time (us): 72 int8 ops per ring MAC for 3 parties at
+    ~3 POPS, 64-column tiles, ~8 K-blocks of prologue / epilogue per tile."""
+    nkb = max(1, (K2 + 31) // 32)
+    ncol = math.ceil(N / 64) * 64
+    return 3 * M * ncol * K2 * 72 / 3.0e15 * 1e6 * (nkb + 8) / nkb
+
+
+# Both dgrad formulations pay the same AES work (reshare + truncation of the
+# full correlation); the costs below are what differs, calibrated on B200
+# (VGG-16-TI b32 conv1_2 / conv2_2: col2im path 1.9 / 1.6 ms vs im2col path
+# 2.5 / 2.1 ms — the im2col operand pack at ~2.5 TB/s outweighs the better GEMM).
+def _dgrad_cost_col2im(nb, o, oh, ow, c, kh, kw):
+    M, N = nb * oh * ow, c * kh * kw
+    return _gemm_us(M, N, 2 * o) + 3 * M * N * 8 / 6.0e12 * 1e6 + 48 * M * o / 4.0e12 * 1e6
+
+
+def _dgrad_cost_im2col(nb, o, oh, ow, c, kh, kw, padding):
+    hf, wf = oh + kh - 1, ow + kw - 1  # stride 1
+    M, K = nb * hf * wf, o * kh * kw
+    return _gemm_us(M, c, 2 * K) + 48 * M * K / 2.5e12 * 1e6 + 3 * M * c * 8 / 4.0e12 * 1e6
 
 
 def gemm_splits(M: int, N: int, kp: int, groups: int) -> int:

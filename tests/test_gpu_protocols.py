@@ -197,3 +197,28 @@ def test_tiny_resnet_inference_bit_exact_vs_composed_oracle(batch):
     assert np.array_equal(got.data.cpu().numpy().view(U64), ref)
     # and the decoded logits track a float64 evaluation of the same network
     assert got.shape == (batch, 10)
+
+
+@pytest.mark.parametrize("nb,o,oh,ow,c,kh,kw,ph", [(2, 8, 5, 6, 3, 3, 3, 1), (3, 4, 4, 4, 5, 5, 5, 2),
+                                                  (1, 16, 7, 3, 8, 3, 2, 0), (4, 2, 6, 6, 2, 1, 1, 0)])
+def test_dgrad_formulations_share_for_share(nb, o, oh, ow, c, kh, kw, ph):
+    """The transposed-convolution (col2im) and padded-correlation (im2col)
+    input gradients are the same ring values with the same PRF words: every
+    party's share equal, same counters consumed (stride 1)."""
+    import torch
+
+    from paper_2104_10949_b200.engine import RssTensor, TrioSession
+
+    rng = np.random.default_rng(nb * 100 + o)
+    h, w = oh + kh - 1 - 2 * ph, ow + kw - 1 - 2 * ph
+    g = rng.integers(0, 1 << 64, size=(3, nb, o, oh, ow), dtype=np.uint64)
+    k = rng.integers(0, 1 << 64, size=(3, o, c, kh, kw), dtype=np.uint64)
+    outs = []
+    for path in ("conv2d_dgrad_col2im", "conv2d_dgrad_im2col"):
+        s = TrioSession(8)
+        gd = RssTensor(torch.from_numpy(g.view(np.int64)).cuda())
+        kd = RssTensor(torch.from_numpy(k.view(np.int64)).cuda())
+        y = getattr(s, path)(gd, kd, (1, 1), (ph, ph), (nb, c, h, w), 20)
+        outs.append((y.data.cpu().numpy().view(np.uint64), dict(s.seq)))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert outs[0][1] == outs[1][1]
