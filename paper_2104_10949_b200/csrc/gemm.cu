@@ -917,7 +917,7 @@ int mpc3_ring_pack(const uint64_t* src, int64_t src_plane, const mpc3_operand* o
       a.W = (int32_t)o.w;
       a.sH = (int32_t)o.sH;
       a.sW = (int32_t)o.sW;
-      r_fast = o.mode == MPC3_GATHER_IM2COL;
+      r_fast = o.mode == MPC3_GATHER_IM2COL && o.sw <= 2;  // strided windows: walk the kernel row (contiguous input x)
     }
     dim3 grid((unsigned)((kp + PT_K - 1) / PT_K), (unsigned)row_tiles, (unsigned)groups);
     void (*k)(const uint64_t*, int64_t, Operand, PackTileArgs, uint8_t*) =
