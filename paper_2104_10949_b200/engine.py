@@ -207,9 +207,29 @@ class TrioSession:
         self.dp = None  # DataParallel: this session computes one batch shard
         self._side = None  # side stream for independent launches (weight gradients)
         self._pack = None  # stream for the B-operand pack of a GEMM
+        self._wcache = None  # packed weight operands under frozen_weights()
         self._replicated = 0
 
     # -- data parallelism --
+    def frozen_weights(self):
+        """Context: the weight operands (GEMM B side) do not change, so their
+        packed limb planes are built once and reused (inference; a weight
+        modified in place gets a new tensor version and is repacked)."""
+        sess = self
+
+        class _Ctx:
+            def __enter__(self_inner):
+                self_inner.prev = sess._wcache
+                if sess._wcache is None:
+                    sess._wcache = {}
+                return sess
+
+            def __exit__(self_inner, *exc):
+                sess._wcache = self_inner.prev
+                return False
+
+        return _Ctx()
+
     def pack_stream(self):
         """The stream that packs a GEMM's B operand while A packs (lazily created)."""
         if self._pack is None:
@@ -523,8 +543,21 @@ class TrioSession:
             return z
         kp = _round_up(2 * Kd, 16)
         A = torch.empty(3 * 8 * M * kp, dtype=torch.uint8, device=_dev())
-        B = torch.empty(3 * 8 * N * kp, dtype=torch.uint8, device=_dev())
         st = _stream()
+        if self._wcache is not None:  # frozen weights (inference): B packed once per weight version
+            key = (b_src.data_ptr(), b_src._version, tuple(b_src.shape), tuple(b_src.stride()), kp,
+                   tuple(getattr(b_op, f) for f, _ in b_op._fields_))
+            B = self._wcache.get(key)
+            if B is None:
+                B = torch.empty(3 * 8 * N * kp, dtype=torch.uint8, device=_dev())
+                K.call("mpc3_ring_pack", b_src.data_ptr(), b_src.stride(0), C.byref(b_op), 1, B.data_ptr(), kp, st)
+                self._wcache[key] = B
+            K.call("mpc3_ring_pack", a_src.data_ptr(), a_src.stride(0), C.byref(a_op), 0, A.data_ptr(), kp, st)
+            z = torch.empty(3 * M * N, dtype=torch.int64, device=_dev())
+            K.call("mpc3_ring_gemm_auto", A.data_ptr(), B.data_ptr(), z.data_ptr(), 3, M, N, kp, 1 if c_col else 0,
+                   st)
+            return z
+        B = torch.empty(3 * 8 * N * kp, dtype=torch.uint8, device=_dev())
         # the two operand packs are independent: B on the pack stream, A here
         main = torch.cuda.current_stream()
         ps = self.pack_stream() if OVERLAP_PACK else None

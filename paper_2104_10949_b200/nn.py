@@ -697,17 +697,23 @@ class InferenceGraph:
         self.seq0 = dict(sess.seq)
         self.ctr = sess.ctr = torch.zeros(8, dtype=torch.int64, device=x.data.device)
         net = TrioNet(sess)
-        net.forward(model, params, x, record=False)  # warm allocations outside capture
-        self.seq0 = dict(sess.seq)
-        self.graph = torch.cuda.CUDAGraph()
-        on = sess.ledger.enabled
-        sess.ledger.enabled = False
+        self._frozen = sess.frozen_weights()
+        self._frozen.__enter__()  # weights packed once (here, outside the graph) and reused by every replay
         try:
-            with torch.cuda.graph(self.graph):
-                self.logits = net.forward(model, params, x, record=False)[0]
+            net.forward(model, params, x, record=False)  # warm allocations + weight packs outside capture
+            self.seq0 = dict(sess.seq)
+            self.graph = torch.cuda.CUDAGraph()
+            on = sess.ledger.enabled
+            sess.ledger.enabled = False
+            try:
+                with torch.cuda.graph(self.graph):
+                    self.logits = net.forward(model, params, x, record=False)[0]
+            finally:
+                sess.ledger.enabled = on
+                sess.ctr = None
         finally:
-            sess.ledger.enabled = on
-            sess.ctr = None
+            self._wpacks = sess._wcache  # the graph reads these buffers: keep them alive
+            self._frozen.__exit__(None, None, None)
         self.delta = {p: sess.seq[p] - self.seq0[p] for p in sess.seq}
         sess.seq = dict(self.seq0)
         self._host = torch.zeros(8, dtype=torch.int64).pin_memory()

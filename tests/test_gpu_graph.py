@@ -41,3 +41,48 @@ def test_graph_replay_matches_eager_steps(batch):
     for a, b in zip(eager_w, [sess_b.reveal(p) for p in st_b.params]):
         assert np.array_equal(a, b)
     assert sess_a.seq == sess_b.seq
+
+
+def test_inference_graph_with_packed_weights_matches_eager():
+    """InferenceGraph packs the weight operands once (frozen_weights) and
+    every replay reproduces the eager forward's logits and consumes the same
+    counters; a weight changed in place is repacked under frozen_weights."""
+    import torch
+
+    import paper_2104_10949_b200 as M
+    from paper_2104_10949_b200.engine import TrioSession
+    from paper_2104_10949_b200.nn import InferenceGraph, TrioNet
+
+    model = M.models.tiny_resnet()
+    rng = np.random.default_rng(4)
+    w = M.init_params(model, seed=4)
+    x_plain = M.fx_encode(rng.uniform(0, 1, (2,) + model.input_shape))
+
+    def setup():
+        s = TrioSession(6)
+        r = np.random.default_rng(1)
+        return s, [s.share(v, r) for v in w], s.share(x_plain, r)
+
+    s0, p0, x0 = setup()
+    net0 = TrioNet(s0)
+    ref = [net0.forward(model, p0, x0, record=False)[0].data.cpu().numpy() for _ in range(3)]
+
+    s1, p1, x1 = setup()
+    g = InferenceGraph(s1, model, p1, x1)
+    got = [g.replay().data.cpu().numpy() for _ in range(3)]
+    # replay k equals eager call k (the graph was captured after one warm-up forward)
+    assert np.array_equal(got[0], ref[1]) and np.array_equal(got[1], ref[2])
+
+    s2, p2, x2 = setup()
+    net2 = TrioNet(s2)
+    with s2.frozen_weights():
+        a = net2.forward(model, p2, x2, record=False)[0].data.clone()
+        p2[0].data.add_(1)  # in place: new tensor version -> repacked
+        b = net2.forward(model, p2, x2, record=False)[0].data.clone()
+    s3, p3, x3 = setup()
+    net3 = TrioNet(s3)
+    a3 = net3.forward(model, p3, x3, record=False)[0].data.clone()
+    p3[0].data.add_(1)
+    b3 = net3.forward(model, p3, x3, record=False)[0].data.clone()
+    torch.cuda.synchronize()
+    assert torch.equal(a, a3) and torch.equal(b, b3)
