@@ -684,6 +684,18 @@ int mpc3_rss_chain(const uint32_t* rk3, const uint64_t* ctr, const MPC3ChainStep
   return check_launch("rss_chain");
 }
 
+// Two-phase chunk size: at most 64 pairs (32 when the p-half straddles
+// blocks: more keystream slots), and just enough that the CTA count fills
+// whole waves of the 2 x 148 resident CTAs (a 1.3-wave grid would leave most
+// SMs idle for the second wave).
+static int sign2_chunk(uint64_t pairs, bool straddle) {
+  const uint64_t pmax = straddle ? 32 : 64, slots = 2 * 148;
+  const uint64_t waves = (pairs + slots * pmax - 1) / (slots * pmax);
+  uint64_t P = (pairs + waves * slots - 1) / (waves * slots);
+  if (P < 8) P = 8;
+  return (int)(P > pmax ? pmax : P);
+}
+
 int mpc3_rss_sign(const uint32_t* rk3, const uint64_t* ctr, int mode, uint64_t j_bin, uint64_t j_xor, uint64_t j_arith,
                   const uint64_t* x, uint64_t* out, uint64_t* mask, uint64_t n, uint64_t n_total,
                   uint64_t elem_off, void* stream) {
@@ -729,7 +741,7 @@ int mpc3_rss_sign(const uint32_t* rk3, const uint64_t* ctr, int mode, uint64_t j
     // blocks), tables + keystream slots in dynamic shared memory
     const uint64_t e0 = 2 * main_pairs, nr = n - e0;
     const bool straddle = (n_total & 1) != 0;
-    const int P = straddle ? 32 : 64;
+    const int P = sign2_chunk((nr + 1) / 2, straddle);
     const int smem = kAesSmemBytes + P * sign_slots(straddle) * SW_SLOT_BYTES;
     if (!aes_attr((const void*)sign2_kernel<false>, kAesSmemBytes + 64 * sign_slots(false) * SW_SLOT_BYTES))
       return check_launch("sign2 smem attribute");
@@ -758,7 +770,7 @@ int mpc3_rss_max_level(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_bin,
   a.jxor = j_xor;
   a.ja = j_arith;
   const bool straddle = (n_total & 1) != 0;
-  const int P = straddle ? 32 : 64;
+  const int P = sign2_chunk((n + 1) / 2, straddle);
   const int smem = kAesSmemBytes + P * sign_slots(straddle) * SW_SLOT_BYTES;
   if (!aes_attr((const void*)sign2_kernel<true>, kAesSmemBytes + 64 * sign_slots(false) * SW_SLOT_BYTES))
     return check_launch("max_level smem attribute");
