@@ -301,6 +301,12 @@ typedef struct {
 int mpc3_ring_pack(const uint64_t* src, int64_t src_plane, const mpc3_operand* op, int role,
                    uint8_t* out, int64_t kp, void* stream);
 
+/* mpc3_ring_pack with the second half at packed column kh >= K (zeros in
+ * [K, kh)), kp >= kh + K: a 16-aligned kh lets another GEMM read the halves
+ * in place as MN operands (mpc3_ring_gemm_t); kh = K is mpc3_ring_pack. */
+int mpc3_ring_pack_halves(const uint64_t* src, int64_t src_plane, const mpc3_operand* op, int role,
+                          uint8_t* out, int64_t kp, int64_t kh, void* stream);
+
 /* C[g] (+)= A[g] . B[g]^T over Z_2^64 (tcgen05 kind::i8, TMA-fed).
  * A: [groups][8][M][kp] u8, B: [groups][8][N][kp] u8, C: rows M, cols N,
  * leading dim ldc, group stride c_group.  splits > 1 requires C zeroed (the
@@ -332,6 +338,22 @@ int mpc3_ring_gemm_streamk(const uint8_t* A, const uint8_t* B, uint64_t* C, int 
  * accumulated atomically. */
 int mpc3_ring_gemm_auto(const uint8_t* A, const uint8_t* B, uint64_t* C, int groups, int64_t M, int64_t N,
                         int64_t kp, int c_layout, void* stream);
+
+/* C[g] = A[g] . B[g]^T where either operand may be read in place from
+ * another GEMM's packed buffer, transposed ("MN" operand): the weight
+ * gradient dW = g^T x of a layer consumes the input-gradient pass's role-0
+ * pack of g and the forward pass's role-1 pack of x directly (nn.py:435-484).
+ * The contraction runs over two halves of kc_half (a multiple of 32) each:
+ *   MN operand  (x_mn = 1): source [groups][8][x_rows][x_kp] (x_rows <=
+ *     kc_half, the rest zero), output row/column j of half h reads source
+ *     column h * x_half + j; x_half % 16 == 0 (mpc3_ring_pack_halves);
+ *   K-major     (x_mn = 0): a normal pack with x_rows = M (or N) and
+ *     x_kp = 2 * kc_half, half h at columns [h * kc_half, (h+1) * kc_half).
+ * C dense [g][M][N] (c_layout 0) or [g][N][M] (1); zeroed here when the
+ * split-K partials add atomically. */
+int mpc3_ring_gemm_t(const uint8_t* A, int a_mn, int64_t a_rows, int64_t a_kp, int64_t a_half, const uint8_t* B,
+                     int b_mn, int64_t b_rows, int64_t b_kp, int64_t b_half, uint64_t* C, int groups, int64_t M,
+                     int64_t N, int64_t kc_half, int c_layout, void* stream);
 
 /* The secure layer's per-party cross terms as ONE implicit ring GEMM per
  * party (protocols.py:110-115):

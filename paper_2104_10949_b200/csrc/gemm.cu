@@ -33,11 +33,11 @@ namespace mpc3 {
 // operand packing: u64 gather -> 8 byte-limb planes [g][limb][row][kp]
 
 __global__ void pack_kernel(const uint64_t* __restrict__ src, int64_t plane, Operand o, int role, int groups,
-                            uint8_t* __restrict__ out, int64_t kp) {
+                            uint8_t* __restrict__ out, int64_t kp, int64_t kh) {
   int64_t total = (int64_t)groups * o.rows * (kp / 8);
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x)
-    pack_item(src, plane, o, role, out, kp, t);
+    pack_item(src, plane, o, role, out, kp, t, kh);
 }
 
 // Tiled operand packing.  One CTA packs a PT_R x PT_K tile of the packed
@@ -55,7 +55,8 @@ __global__ void pack_kernel(const uint64_t* __restrict__ src, int64_t plane, Ope
 constexpr int PT_R = 64, PT_K = 64, PT_THREADS = 512;
 
 struct PackTileArgs {
-  int64_t rows, K, kp, lim;  // lim: packed columns with data (K or 2K)
+  int64_t rows, K, kp, lim;  // lim: packed columns with data (K or kh + K)
+  int64_t kh;                // first packed column of the second half
   int32_t H, W, sH, sW;      // bounds / strides of the (y, x) part (dense: no bounds, 0 strides)
 };
 
@@ -87,10 +88,10 @@ DEV int4 pack_row_part(const Operand& o, int64_t r64, int64_t rows) {
   const uint32_t c = q / kh, u = q - c * kh;
   return make_int4((int32_t)(c * o.sC), (int32_t)(u - o.ph), (int32_t)(v - o.pw), 0);
 }
-DEV int4 pack_col_part(const Operand& o, int64_t kk, int64_t K, int64_t lim) {
-  if (kk >= lim) return make_int4(0, -(1 << 30), 0, 0);
-  const int half = kk >= K ? 1 : 0;
-  const uint32_t k = (uint32_t)(kk - half * K);
+DEV int4 pack_col_part(const Operand& o, int64_t kk, int64_t K, int64_t lim, int64_t kh) {
+  const int half = kk >= kh ? 1 : 0;
+  if (kk >= lim || (!half && kk >= K)) return make_int4(0, -(1 << 30), 0, 0);
+  const uint32_t k = (uint32_t)(kk - half * kh);
   if (o.mode == MPC3_GATHER_DENSE) {
     const uint32_t K2 = (uint32_t)o.K2, K1 = (uint32_t)o.K1;
     const uint32_t q = k / K2, k2 = k - q * K2;
@@ -123,7 +124,7 @@ __global__ void __launch_bounds__(PT_THREADS) pack_tile_kernel(const uint64_t* _
   if (t < PT_R)
     rpart[t] = pack_row_part(o, r0 + t, a.rows);
   else if (t < PT_R + PT_K)
-    cpart[t - PT_R] = pack_col_part(o, c0 + (t - PT_R), a.K, a.lim);
+    cpart[t - PT_R] = pack_col_part(o, c0 + (t - PT_R), a.K, a.lim, a.kh);
   __syncthreads();
   griddep_wait();  // the source tensor is the previous kernel's output
   // phase 1: gather the packed values of the tile.  Each thread keeps one
@@ -288,10 +289,41 @@ DEV void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
+// Operands read in place from another GEMM's packed buffer ("MN-major"): the
+// contraction index is the SOURCE's row index and this GEMM's rows / columns
+// are a source column range, so a weight gradient consumes the forward pass's
+// packed activations and the input-gradient pass's packed gradient directly
+// (transposed views, no repack).  Per half h of the cross-term concatenation
+// the contraction runs over source rows [0, kc_half) (zero-filled past the
+// source's rows) at source columns h * half + tile offset.  tcgen05 reads
+// such tiles MN-major (instruction-descriptor bits 15 / 16): A as 128-byte
+// SWIZZLE_128B rows (8-row atoms, SBO 1 KiB), B limb tiles as 64-byte
+// SWIZZLE_64B rows (SBO 512 B, the next limb tile = the next 64-wide MN atom,
+// LBO 2 KiB).
+struct MnArgs {
+  int a_mn, b_mn;
+  int a_half, b_half;  // source column of half 1
+  int nkb_half;        // contraction K-blocks per half
+};
+
+DEV uint64_t umma_desc_mn(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3fff);
+  d |= (uint64_t)((lbo >> 4) & 0x3fff) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3fff) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)layout << 61;
+  return d;
+}
+DEV uint64_t desc_a(uint32_t addr, bool mn) { return mn ? umma_desc_mn(addr, 0, 1024, 2) : umma_desc_sw32(addr); }
+DEV uint64_t desc_b(uint32_t addr, bool mn) {
+  return mn ? umma_desc_mn(addr, BN * BK, 8 * BN, 4) : umma_desc_sw32(addr);
+}
+
 __global__ void __launch_bounds__(256, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    uint64_t* __restrict__ C, int64_t M, int64_t N, int64_t kp, int64_t ldc, int64_t c_group,
-                   int splits, int kb_per_split, int c_col) {
+                   int splits, int kb_per_split, int c_col, MnArgs mn) {
   griddep_launch();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -351,12 +383,21 @@ __global__ void __launch_bounds__(256, 1)
       uint32_t ph = (i / STAGES) & 1;
       mbar_wait(&empty[s], ph ^ 1);
       mbar_expect_tx(&full[s], A_STAGE + B_STAGE);
-      int kc = (kb0 + i) * BK;
-      tma_load_3d(&tmA, &full[s], sA + s * A_STAGE, kc, (int)m0, g * 8);
-      tma_load_3d(&tmB, &full[s], sB + s * B_STAGE, kc, (int)n0, g * 8);
+      const int kb = kb0 + i;
+      const int kc = kb * BK;
+      const int h = kb >= mn.nkb_half ? 1 : 0, r = (kb - h * mn.nkb_half) * BK;  // MN: source rows / half
+      if (mn.a_mn)
+        tma_load_3d(&tmA, &full[s], sA + s * A_STAGE, h * mn.a_half + (int)m0, r, g * 8);
+      else
+        tma_load_3d(&tmA, &full[s], sA + s * A_STAGE, kc, (int)m0, g * 8);
+      if (mn.b_mn)
+        tma_load_3d(&tmB, &full[s], sB + s * B_STAGE, h * mn.b_half + (int)n0, r, g * 8);
+      else
+        tma_load_3d(&tmB, &full[s], sB + s * B_STAGE, kc, (int)n0, g * 8);
     }
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer ----
+    const uint32_t idesc_mn = ((uint32_t)(mn.a_mn != 0) << 15) | ((uint32_t)(mn.b_mn != 0) << 16);
     for (int i = 0; i < nkb; ++i) {
       int s = i % STAGES;
       uint32_t ph = (i / STAGES) & 1;
@@ -366,14 +407,14 @@ __global__ void __launch_bounds__(256, 1)
       uint32_t b_base = smem_u32(sB + s * B_STAGE);
 #pragma unroll
       for (int li = 0; li < 8; ++li) {
-        uint64_t da = umma_desc_sw32(a_base + li * (BM * BK));
+        uint64_t da = desc_a(a_base + li * (BM * BK), mn.a_mn);
         int nblk = 8 - li;  // limb blocks j = 0 .. 7 - li  ->  diagonals li .. 7
         int first = nblk > 4 ? 4 : nblk;
         uint32_t acc = (i > 0 || li > 0) ? 1u : 0u;
-        mma_i8(tmem + li * BN, da, umma_desc_sw32(b_base), idesc_i8(first * BN), acc);
+        mma_i8(tmem + li * BN, da, desc_b(b_base, mn.b_mn), idesc_i8(first * BN) | idesc_mn, acc);
         if (nblk > 4) {
-          mma_i8(tmem + (li + 4) * BN, da, umma_desc_sw32(b_base + 4 * (BN * BK)), idesc_i8((nblk - 4) * BN),
-                 acc);
+          mma_i8(tmem + (li + 4) * BN, da, desc_b(b_base + 4 * (BN * BK), mn.b_mn),
+                 idesc_i8((nblk - 4) * BN) | idesc_mn, acc);
         }
       }
       mma_commit(&empty[s]);
@@ -844,6 +885,29 @@ static int make_map(CUtensorMap* map, const uint8_t* base, int64_t kp, int64_t r
   return MPC3_OK;
 }
 
+// Tensor map of an MN-read operand: the source packed buffer
+// [planes][rows][kp] with a box of `cols` bytes along kp x 32 rows x 8 limbs.
+static int make_map_mn(CUtensorMap* map, const uint8_t* base, int64_t kp, int64_t rows, int64_t planes, int cols,
+                       CUtensorMapSwizzle swz) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) {
+    set_last_error("cuTensorMapEncodeTiled unavailable");
+    return MPC3_ERR_CUDA;
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)kp, (cuuint64_t)rows, (cuuint64_t)planes};
+  cuuint64_t strides[2] = {(cuuint64_t)kp, (cuuint64_t)(kp * rows)};
+  cuuint32_t box[3] = {(cuuint32_t)cols, (cuuint32_t)BK, 8};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)base, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_last_error("cuTensorMapEncodeTiled (MN) failed");
+    return MPC3_ERR_CUDA;
+  }
+  return MPC3_OK;
+}
+
 static Operand to_operand(const mpc3_operand* o) {
   Operand p;
   p.mode = o->mode;
@@ -885,10 +949,17 @@ extern "C" {
 
 int mpc3_ring_pack(const uint64_t* src, int64_t src_plane, const mpc3_operand* op, int role, uint8_t* out,
                    int64_t kp, void* stream) {
+  if (!op) return MPC3_ERR_CONFIG;
+  return mpc3_ring_pack_halves(src, src_plane, op, role, out, kp, op->k, stream);
+}
+
+int mpc3_ring_pack_halves(const uint64_t* src, int64_t src_plane, const mpc3_operand* op, int role, uint8_t* out,
+                          int64_t kp, int64_t kh, void* stream) {
   if (!op || role < 0 || role > 2) return MPC3_ERR_CONFIG;
   if (kp % 16) return MPC3_ERR_SHAPE;
-  int64_t kneed = role == 2 ? op->k : 2 * op->k;
-  if (kp < kneed || op->rows < 0 || op->k < 0) return MPC3_ERR_SHAPE;
+  if (role == 2) kh = op->k;
+  int64_t kneed = role == 2 ? op->k : kh + op->k;
+  if (kh < op->k || kp < kneed || op->rows < 0 || op->k < 0) return MPC3_ERR_SHAPE;
   if (op->mode < 0 || op->mode > 2) return MPC3_ERR_CONFIG;
   Operand o = to_operand(op);
   int groups = role == 2 ? 1 : 3;
@@ -905,7 +976,8 @@ int mpc3_ring_pack(const uint64_t* src, int64_t src_plane, const mpc3_operand* o
     a.rows = o.rows;
     a.K = o.k;
     a.kp = kp;
-    a.lim = role == 2 ? o.k : 2 * o.k;
+    a.lim = kneed;
+    a.kh = kh;
     bool r_fast;
     if (o.mode == MPC3_GATHER_DENSE) {
       a.H = a.W = 1;
@@ -927,7 +999,7 @@ int mpc3_ring_pack(const uint64_t* src, int64_t src_plane, const mpc3_operand* o
     launch_pdl(k, grid, dim3(PT_THREADS), 0, as_stream(stream), src, src_plane, o, a, out);
     return check_launch("ring_pack_tile");
   }
-  pack_kernel<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(src, src_plane, o, role, groups, out, kp);
+  pack_kernel<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(src, src_plane, o, role, groups, out, kp, kh);
   return check_launch("ring_pack");
 }
 
@@ -959,8 +1031,9 @@ int mpc3_ring_gemm_packed_layout(const uint8_t* A, const uint8_t* B, uint64_t* C
   st = make_map(&tb, B, kp, N, (int64_t)groups * 8, BN);
   if (st) return st;
   dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)(groups * splits));
+  MnArgs mn0 = {0, 0, 0, 0, 1 << 30};
   launch_pdl(gemm_tc_kernel, grid, dim3(256), SMEM_BYTES, as_stream(stream), ta, tb, C, M, N, kp, ldc, c_group, splits,
-             kbs, c_layout);
+             kbs, c_layout, mn0);
   return check_launch("ring_gemm_tc");
 }
 
@@ -1019,6 +1092,55 @@ int mpc3_ring_gemm_auto(const uint8_t* A, const uint8_t* B, uint64_t* C, int gro
     return mpc3_ring_gemm_streamk(A, B, C, groups, M, N, kp, ldc, c_group, (int)(c < 1 ? 1 : c), c_layout, stream);
   }
   return mpc3_ring_gemm_packed_layout(A, B, C, groups, M, N, kp, ldc, c_group, (int)splits, c_layout, stream);
+}
+
+int mpc3_ring_gemm_t(const uint8_t* A, int a_mn, int64_t a_rows, int64_t a_kp, int64_t a_half, const uint8_t* B,
+                     int b_mn, int64_t b_rows, int64_t b_kp, int64_t b_half, uint64_t* C, int groups, int64_t M,
+                     int64_t N, int64_t kc_half, int c_layout, void* stream) {
+  if (groups < 1 || M < 0 || N < 0 || kc_half < 0 || (kc_half % BK)) return MPC3_ERR_SHAPE;
+  if (c_layout != 0 && c_layout != 1) return MPC3_ERR_CONFIG;
+  if (M == 0 || N == 0) return MPC3_OK;
+  if (M > (1 << 30) || N > (1 << 30) || a_half > (1 << 30) || b_half > (1 << 30)) return MPC3_ERR_SHAPE;
+  const int64_t kp = 2 * kc_half;
+  if ((!a_mn && (a_kp != kp || a_rows != M)) || (!b_mn && (b_kp != kp || b_rows != N))) return MPC3_ERR_SHAPE;
+  // an MN operand's half offset is a TMA box start along the 16-byte-granular
+  // inner dimension (pack with mpc3_ring_pack_halves, kh % 16 == 0)
+  if ((a_mn && (a_kp % 16 || a_rows > kc_half || a_half % 16)) ||
+      (b_mn && (b_kp % 16 || b_rows > kc_half || b_half % 16)))
+    return MPC3_ERR_SHAPE;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess)
+      return check_launch("gemm_tc attr");
+    attr_set = true;
+  }
+  CUtensorMap ta, tb;
+  int st = a_mn ? make_map_mn(&ta, A, a_kp, a_rows, (int64_t)groups * 8, BM, CU_TENSOR_MAP_SWIZZLE_128B)
+                : make_map(&ta, A, kp, M, (int64_t)groups * 8, BM);
+  if (st) return st;
+  st = b_mn ? make_map_mn(&tb, B, b_kp, b_rows, (int64_t)groups * 8, BN, CU_TENSOR_MAP_SWIZZLE_64B)
+            : make_map(&tb, B, kp, N, (int64_t)groups * 8, BN);
+  if (st) return st;
+  const int64_t sms = 148;
+  const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * groups;
+  const int64_t nkb = kp / BK;
+  const int64_t need = (nkb * BK + MAX_SPLIT_K - 1) / MAX_SPLIT_K;
+  int64_t occ = sms / tiles;
+  if (occ > nkb / 4) occ = nkb / 4;
+  if (occ < 1) occ = 1;
+  const int64_t splits = need > occ ? need : occ;
+  const int kbs = (int)((nkb + splits - 1) / splits);
+  if ((int64_t)kbs * BK > MAX_SPLIT_K) return MPC3_ERR_EXACTNESS;
+  if (nkb == 0 || splits > 1) {
+    if (cudaMemsetAsync(C, 0, (size_t)groups * M * N * 8, as_stream(stream)) != cudaSuccess)
+      return check_launch("gemm C memset");
+    if (nkb == 0) return MPC3_OK;
+  }
+  MnArgs mn = {a_mn ? 1 : 0, b_mn ? 1 : 0, (int)a_half, (int)b_half, (int)(kc_half / BK)};
+  dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)(groups * splits));
+  launch_pdl(gemm_tc_kernel, grid, dim3(256), SMEM_BYTES, as_stream(stream), ta, tb, C, M, N, kp,
+             c_layout ? M : N, M * N, (int)splits, kbs, c_layout, mn);
+  return check_launch("ring_gemm_t");
 }
 
 int mpc3_ring_gemm_cross(const uint64_t* src_a, int64_t plane_a, const mpc3_operand* op_a, const uint64_t* src_b,

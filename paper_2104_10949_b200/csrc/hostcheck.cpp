@@ -120,7 +120,8 @@ void hc_col2im(const uint8_t* keys48, uint64_t ja, uint64_t jrho, uint64_t jr, i
                 z, g, out, b);
 }
 
-void hc_pack(const uint64_t* src, int64_t plane, const mpc3_operand* op, int role, uint8_t* out, int64_t kp) {
+void hc_pack(const uint64_t* src, int64_t plane, const mpc3_operand* op, int role, uint8_t* out, int64_t kp,
+             int64_t kh) {
   Operand o;
   memset(&o, 0, sizeof(o));
   o.mode = op->mode; o.rows = op->rows; o.k = op->k; o.off = op->off; o.s_r = op->s_r;
@@ -131,7 +132,7 @@ void hc_pack(const uint64_t* src, int64_t plane, const mpc3_operand* op, int rol
   o.dw = op->dw > 0 ? op->dw : 1; o.oh = op->oh > 0 ? op->oh : 1; o.ow = op->ow > 0 ? op->ow : 1;
   int groups = role == 2 ? 1 : 3;
   int64_t total = (int64_t)groups * o.rows * (kp / 8);
-  for (int64_t t = 0; t < total; ++t) pack_item(src, plane, o, role, out, kp, t);
+  for (int64_t t = 0; t < total; ++t) pack_item(src, plane, o, role, out, kp, t, kh < 0 ? o.k : kh);
 }
 
 // Emulates the tensor-core GEMM on packed limbs: 8 int32 (wrapping) diagonal

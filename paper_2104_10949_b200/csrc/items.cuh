@@ -330,15 +330,17 @@ HD void pool_item(const T& tab, const uint32_t* rk3, bool backward, StreamHead h
 }
 
 // packing item: 8 consecutive kk of one (g, r) -> one u64 per limb plane
+// kh: packed column of the second half's first element (K for the adjacent
+// [first | second] layout; larger leaves zero columns [K, kh) between them).
 HD void pack_item(const uint64_t* src, int64_t plane, const Operand& o, int role, uint8_t* out, int64_t kp,
-                  int64_t t) {
+                  int64_t t, int64_t kh) {
   int64_t chunks = kp / 8;
   int64_t ch = t % chunks;
   int64_t q = t / chunks;
   int64_t r = q % o.rows;
   int g = (int)(q / o.rows);
   uint64_t v[8];
-  const int64_t K = o.k, lim = role == 2 ? K : 2 * K;
+  const int64_t K = o.k, lim = role == 2 ? K : kh + K;
   const int gn = (g + 1) % 3;
   GatherCursor cur;
   int half = -1;
@@ -348,9 +350,13 @@ HD void pack_item(const uint64_t* src, int64_t plane, const Operand& o, int role
       v[e] = 0;
       continue;
     }
-    int h = (role != 2 && kk >= K) ? 1 : 0;
+    int h = (role != 2 && kk >= kh) ? 1 : 0;
+    if (h == 0 && kk >= K) {  // gap between the halves
+      v[e] = 0;
+      continue;
+    }
     if (h != half) {  // (re)start the cursor at this half's first k
-      cur.init(o, r, h ? kk - K : kk);
+      cur.init(o, r, h ? kk - kh : kk);
       half = h;
     }
     int64_t off = cur.offset(o);

@@ -87,11 +87,12 @@ def pool(keys, backward, jrho, jr, bits, mulc, x, N, Cc, H, W, OH, OW, kh, kw, s
     return out
 
 
-def pack(src, plane, op, role, kp):
+def pack(src, plane, op, role, kp, kh=-1):
+    """kh: first packed column of the second half (-1: K, the adjacent layout)."""
     src = np.ascontiguousarray(src, np.uint64)
     groups = 1 if role == 2 else 3
     out = np.zeros((groups, 8, op.rows, kp), np.uint8)
-    lib().hc_pack(ptr(src), C.c_int64(plane), C.byref(op), C.c_int(role), ptr(out), C.c_int64(kp))
+    lib().hc_pack(ptr(src), C.c_int64(plane), C.byref(op), C.c_int(role), ptr(out), C.c_int64(kp), C.c_int64(kh))
     return out
 
 

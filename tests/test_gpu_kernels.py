@@ -219,6 +219,48 @@ def test_ring_gemm_streamk(M, K, Nn, ctas, layout):
     assert np.array_equal(got, R.wrap_matmul(a, b))
 
 
+def _pack_halves(src, plane, op, role, kp, kh):
+    out = torch.empty(3 * 8 * op.rows * kp, dtype=torch.uint8, device="cuda")
+    _capi.call("mpc3_ring_pack_halves", p(src), plane, C.byref(op), role, p(out), kp, kh, stream())
+    return out
+
+
+@pytest.mark.parametrize("Rn,O,Kc,a_mn,b_mn,layout", [(300, 70, 150, 1, 1, 0), (4096, 200, 100, 1, 1, 1),
+                                                      (20000, 64, 96, 1, 1, 0), (250, 130, 70, 1, 0, 0),
+                                                      (96, 40, 300, 0, 1, 1), (1, 3, 5, 1, 1, 0),
+                                                      (1000, 256, 4608, 1, 1, 1)])
+def test_ring_gemm_transposed_operands(Rn, O, Kc, a_mn, b_mn, layout):
+    """mpc3_ring_gemm_t reads operands in place from other GEMMs' packed
+    buffers (MN-major tiles): the weight-gradient cross terms
+      dW[g] = (g_g + g_{g+1})^T x_g + g_g^T x_{g+1}
+    from the role-0 pack of g (rows R, K = O) and the role-1 pack of x (rows R,
+    K = Kc), halves at 16-aligned columns, contraction over R zero-filled to a
+    multiple of 32; K-major partners hold their halves at kc_half."""
+    rng = np.random.default_rng(Rn + O + Kc + 2 * a_mn + b_mn)
+    gt, xt = rnd(rng, (3, Rn, O)), rnd(rng, (3, Rn, Kc))
+    kc_half = (Rn + 31) // 32 * 32
+    r16 = lambda v: (v + 15) // 16 * 16  # noqa: E731
+    if a_mn:
+        A = _pack_halves(dev(gt), Rn * O, _capi.dense_operand(Rn, O, s_r=O, t2=1), 0, r16(r16(O) + O), r16(O))
+        a_args = (1, Rn, r16(r16(O) + O), r16(O))
+    else:
+        A = _pack_halves(dev(gt), Rn * O, _capi.dense_operand(O, Rn, s_r=1, t2=O), 0, 2 * kc_half, kc_half)
+        a_args = (0, O, 2 * kc_half, 0)
+    if b_mn:
+        B = _pack_halves(dev(xt), Rn * Kc, _capi.dense_operand(Rn, Kc, s_r=Kc, t2=1), 1, r16(r16(Kc) + Kc), r16(Kc))
+        b_args = (1, Rn, r16(r16(Kc) + Kc), r16(Kc))
+    else:
+        B = _pack_halves(dev(xt), Rn * Kc, _capi.dense_operand(Kc, Rn, s_r=1, t2=Kc), 1, 2 * kc_half, kc_half)
+        b_args = (0, Kc, 2 * kc_half, 0)
+    Cm = torch.full((3 * O * Kc,), -1, dtype=torch.int64, device="cuda")
+    _capi.call("mpc3_ring_gemm_t", p(A), *a_args, p(B), *b_args, p(Cm), 3, O, Kc, kc_half, layout, stream())
+    got = host(Cm).reshape(3, Kc, O).transpose(0, 2, 1) if layout else host(Cm).reshape(3, O, Kc)
+    for g in range(3):
+        h = (g + 1) % 3
+        want = R.wrap_matmul(gt[g].T + gt[h].T, xt[g]) + R.wrap_matmul(gt[g].T, xt[h])
+        assert np.array_equal(got[g], want), g
+
+
 def test_ring_matmul_u64_convenience():
     rng = np.random.default_rng(3)
     M, K, Nn = 77, 20000, 33

@@ -241,3 +241,55 @@ def test_dgrad_gemm_col2im_matches_reference_schedule(geom):
     z = H.gemm_packed(A, B)
     got = H.col2im(R.Session(4).keys, 0, 0, 0, 20, z, n, c, oh, ow, kh, kw, st[0], st[1], pd[0], pd[1], h, w)
     assert np.array_equal(got, ref)
+
+
+def _mn_to_kmajor(src, half, n, kc_half):
+    """K-major packed operand equivalent to reading the packed buffer `src`
+    ([g][8][rows][kp]) transposed, as mpc3_ring_gemm_t's MN operands do:
+    element (j, h * kc_half + r) = src[..., r, h * half + j]."""
+    g, _, rows, kp = src.shape
+    out = np.zeros((g, 8, n, 2 * kc_half), np.uint8)
+    for h in range(2):
+        cols = np.arange(n) + h * half
+        ok = cols < kp
+        blk = np.zeros((g, 8, rows, n), np.uint8)
+        blk[..., ok] = src[..., cols[ok]]
+        out[..., h * kc_half:h * kc_half + rows] = blk.transpose(0, 1, 3, 2)
+    return out
+
+
+@pytest.mark.parametrize("Rn,O,Kc", [(50, 7, 20), (64, 16, 33)])
+def test_pack_halves_and_transposed_gemm_semantics(Rn, O, Kc):
+    """Packs with the second half at a 16-aligned column (zero gap) give the
+    same cross terms, and reading the role-0 pack of g and the role-1 pack of
+    x transposed (the weight-gradient GEMM mpc3_ring_gemm_t) gives
+    dW[g] = (g_g + g_{g+1})^T x_g + g_g^T x_{g+1}."""
+    rng = np.random.default_rng(Rn * O)
+    gt = rng.integers(0, 1 << 64, size=(3, Rn, O), dtype=np.uint64)
+    xt = rng.integers(0, 1 << 64, size=(3, Rn, Kc), dtype=np.uint64)
+    kha, khb = (O + 15) // 16 * 16, (Kc + 15) // 16 * 16
+    kpa, kpb = (kha + O + 15) // 16 * 16, (khb + Kc + 15) // 16 * 16
+    A = H.pack(gt, Rn * O, _capi.dense_operand(Rn, O, s_r=O, t2=1), 0, kpa, kha)
+    B = H.pack(xt, Rn * Kc, _capi.dense_operand(Rn, Kc, s_r=Kc, t2=1), 1, kpb, khb)
+    assert not A[..., O:kha].any() and not B[..., Kc:khb].any()
+    Aadj = H.pack(gt, Rn * O, _capi.dense_operand(Rn, O, s_r=O, t2=1), 0, (2 * O + 15) // 16 * 16)
+    assert np.array_equal(A[..., kha:kha + O], Aadj[..., O:2 * O]) and np.array_equal(A[..., :O], Aadj[..., :O])
+    kc_half = (Rn + 31) // 32 * 32
+    z = H.gemm_packed(_mn_to_kmajor(A, kha, O, kc_half), _mn_to_kmajor(B, khb, Kc, kc_half))
+    for g in range(3):
+        h = (g + 1) % 3
+        want = R.wrap_matmul(gt[g].T + gt[h].T, xt[g]) + R.wrap_matmul(gt[g].T, xt[h])
+        assert np.array_equal(z[g], want)
+
+
+def test_gemm_t_rejects_unaligned_half():
+    import ctypes as C
+
+    lib = _capi.lib()
+    nul = C.c_void_p(0)
+    # MN operand whose half offset is not a 16-byte TMA granule
+    assert lib.mpc3_ring_gemm_t(nul, 1, 64, 160, 70, nul, 1, 64, 160, 64, nul, 3, 70, 64, 64, 0, nul) == \
+        2  # MPC3_ERR_SHAPE
+    # K-major partner must hold the halves at kc_half
+    assert lib.mpc3_ring_gemm_t(nul, 1, 64, 160, 80, nul, 0, 64, 96, 0, nul, 3, 70, 64, 64, 0, nul) == \
+        2  # MPC3_ERR_SHAPE
