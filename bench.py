@@ -248,15 +248,19 @@ def run_b200(args, ws, rank, local):
     instrument = {"on": False, "k": 0}
 
     def traced_call(name, *a):
-        if instrument["on"] and name == "mpc3_ring_pack" and a[3] == 0:
+        if instrument["on"] and name in ("mpc3_ring_pack", "mpc3_ring_pack_halves") and a[3] in (0, 1):
             instrument["k"] = int(a[2]._obj.k)  # logical K of the cross-term operand (inner length 2K)
-        if instrument["on"] and name in ("mpc3_rss_sign", "mpc3_ring_gemm_auto"):
+        if instrument["on"] and name in ("mpc3_rss_sign", "mpc3_ring_gemm_auto", "mpc3_ring_gemm_t"):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             counting_call(name, *a)
             e1.record()
             if name == "mpc3_rss_sign":
                 sign_events.append((e0, e1, int(a[9])))
+            elif name == "mpc3_ring_gemm_t":  # weight gradient: contraction over the a_rows batch positions
+                groups, M, N, rows, kc_half = int(a[11]), int(a[12]), int(a[13]), int(a[2]), int(a[14])
+                gemm_events.append((e0, e1, 72 * groups * M * N * 2 * rows))
+                gemm_bytes.append(groups * ((M + N) * 8 * 2 * kc_half + M * N * 8))
             else:  # groups x M x N x 2K ring MACs, 72 int8 ops each (36 limb-pair MACs)
                 groups, M, N = int(a[3]), int(a[4]), int(a[5])
                 sign_k = instrument["k"] if instrument["k"] else int(a[6]) // 2

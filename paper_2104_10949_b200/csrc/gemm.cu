@@ -315,16 +315,98 @@ DEV uint64_t umma_desc_mn(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t l
   d |= (uint64_t)layout << 61;
   return d;
 }
-DEV uint64_t desc_a(uint32_t addr, bool mn) { return mn ? umma_desc_mn(addr, 0, 1024, 2) : umma_desc_sw32(addr); }
+// A operand: mode 0 = K-major SWIZZLE_32B limb tiles [limb][row][32 B];
+// mode 1 = MN-major SWIZZLE_128B (transposed read, see MnArgs).  The 128-byte
+// rows of mode 1 spread the tensor core's shared-memory reads over every bank
+// group; the 32-byte rows of mode 0 meet 2-way conflicts (1.17x slower at
+// M=N=K=4096, profiles/README.md).  (A K-major 4-limb interleave through a 4-D
+// box with a 32-byte inner extent does not work: TMA pads each 32-byte box row
+// to the 128-byte swizzle span.)
+DEV uint64_t desc_a(uint32_t addr, int mode) {
+  return mode ? umma_desc_mn(addr, 0, 1024, 2) : umma_desc_sw32(addr);
+}
 DEV uint64_t desc_b(uint32_t addr, bool mn) {
   return mn ? umma_desc_mn(addr, BN * BK, 8 * BN, 4) : umma_desc_sw32(addr);
 }
 
-__global__ void __launch_bounds__(256, 1)
+// Epilogue of one 128 x BN tile: TMEM -> registers -> recombine the 8
+// diagonal int32 accumulators (sum S_d << 8d) -> C.  EPI_WARPS warps share a
+// tile: warp ew reads TMEM lane quadrant ew % 4 (its rows) and the column
+// range (ew / 4) of BN split EPI_WARPS / 4 ways.  With c_col the 32 lanes of a
+// warp store 32 consecutive words per column.
+constexpr int EPI_WARPS = 8;
+constexpr int GEMM_THREADS = 128 + 32 * EPI_WARPS;  // warps 0-3: TMA, MMA, TMEM alloc, idle
+DEV void epilogue_tile(uint32_t tmem, int ew, int lane, bool have_acc, uint64_t* cg, int64_t m0, int64_t n0,
+                       int64_t M, int64_t N, int64_t rs, int64_t cs, bool atomic) {
+  const int q = ew & 3;
+  constexpr int COLS = BN / (EPI_WARPS / 4);
+  const int cbeg = (ew >> 2) * COLS;
+  const int64_t row = m0 + q * 32 + lane;
+#pragma unroll 1
+  for (int c0 = cbeg; c0 < cbeg + COLS; c0 += 8) {
+    uint64_t acc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = 0;
+    if (have_acc) {
+      // all 8 diagonals of this 8-column chunk in flight, one wait
+      uint32_t r[8][8];
+#pragma unroll
+      for (int d = 0; d < 8; ++d) {
+        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + d * BN + c0;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+            : "=r"(r[d][0]), "=r"(r[d][1]), "=r"(r[d][2]), "=r"(r[d][3]), "=r"(r[d][4]), "=r"(r[d][5]),
+              "=r"(r[d][6]), "=r"(r[d][7])
+            : "r"(taddr));
+      }
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int d = 0; d < 8; ++d)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] += (uint64_t)r[d][e] << (8 * d);
+    }
+    if (row < M) {
+      uint64_t* dst = cg + row * rs + (n0 + c0) * cs;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        if (n0 + c0 + e < N) {
+          if (atomic)
+            atomicAdd(reinterpret_cast<unsigned long long*>(dst + e * cs), (unsigned long long)acc[e]);
+          else
+            dst[e * cs] = acc[e];
+        }
+      }
+    }
+  }
+}
+
+#ifdef MPC3_GEMM_TRACE
+// debug build only (tools/dbg/gemm_trace.py): per-CTA phase timestamps
+__device__ unsigned long long g_trace[8192][8];
+DEV unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRACE(slot) g_trace[cta_lin & 8191][slot] = gtime()
+#else
+#define TRACE(slot)
+#endif
+
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    uint64_t* __restrict__ C, int64_t M, int64_t N, int64_t kp, int64_t ldc, int64_t c_group,
                    int splits, int kb_per_split, int c_col, MnArgs mn) {
   griddep_launch();
+#ifdef MPC3_GEMM_TRACE
+  const int cta_lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  if (threadIdx.x == 0) {
+    TRACE(0);
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    g_trace[cta_lin & 8191][7] = smid;
+  }
+#endif
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -373,6 +455,7 @@ __global__ void __launch_bounds__(256, 1)
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
   griddep_wait();  // packed operands and C are the previous kernels' data
+  if (threadIdx.x == 0) TRACE(1);
 
   if (warp == 0 && lane == 0) {
     // ---- TMA producer ----
@@ -402,6 +485,7 @@ __global__ void __launch_bounds__(256, 1)
       int s = i % STAGES;
       uint32_t ph = (i / STAGES) & 1;
       mbar_wait(&full[s], ph);
+      if (i == 0) TRACE(2);
       asm volatile("tcgen05.fence::after_thread_sync;");
       uint32_t a_base = smem_u32(sA + s * A_STAGE);
       uint32_t b_base = smem_u32(sB + s * B_STAGE);
@@ -422,55 +506,19 @@ __global__ void __launch_bounds__(256, 1)
     mma_commit(tmem_full);
   } else if (warp >= 4) {
     // ---- epilogue: TMEM -> registers -> recombine -> global ----
-    const int wq = warp - 4;  // TMEM lanes 32 wq .. 32 wq + 31
-    const int64_t row = m0 + wq * 32 + lane;
-    uint64_t* cg = C + (int64_t)g * c_group;
     // element (row, col) at row*ldc + col (row-major) or col*ldc + row
     const int64_t rs = c_col ? 1 : ldc, cs = c_col ? ldc : 1;
     if (nkb > 0) {
       mbar_wait(tmem_full, 0);
       asm volatile("tcgen05.fence::after_thread_sync;");
     }
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 8) {
-      uint64_t acc[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) acc[e] = 0;
-      if (nkb > 0) {
-        // all 8 diagonals of this 8-column chunk in flight, one wait
-        uint32_t r[8][8];
-#pragma unroll
-        for (int d = 0; d < 8; ++d) {
-          uint32_t taddr = tmem + ((uint32_t)(wq * 32) << 16) + d * BN + c0;
-          asm volatile(
-              "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-              : "=r"(r[d][0]), "=r"(r[d][1]), "=r"(r[d][2]), "=r"(r[d][3]), "=r"(r[d][4]), "=r"(r[d][5]),
-                "=r"(r[d][6]), "=r"(r[d][7])
-              : "r"(taddr));
-        }
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-        for (int d = 0; d < 8; ++d)
-#pragma unroll
-          for (int e = 0; e < 8; ++e) acc[e] += (uint64_t)r[d][e] << (8 * d);
-      }
-      if (row < M) {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          int64_t col = n0 + c0 + e;
-          if (col < N) {
-            uint64_t* dst = cg + row * rs + col * cs;
-            if (splits > 1)
-              atomicAdd(reinterpret_cast<unsigned long long*>(dst), (unsigned long long)acc[e]);
-            else
-              *dst = acc[e];
-          }
-        }
-      }
-    }
+    if (warp == 4 && lane == 0) TRACE(3);
+    epilogue_tile(tmem, warp - 4, lane, nkb > 0, C + (int64_t)g * c_group, m0, n0, M, N, rs, cs, splits > 1);
     asm volatile("tcgen05.fence::before_thread_sync;");
+    if (warp == 4 && lane == 0) TRACE(4);
   }
   __syncthreads();
+  if (threadIdx.x == 0) TRACE(5);
   if (warp == 2) {
     asm volatile("tcgen05.fence::after_thread_sync;");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
@@ -500,7 +548,7 @@ DEV SkSeg sk_seg(int64_t it, int64_t it_end, int nkb_total) {
   return sg;
 }
 
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_sk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    uint64_t* __restrict__ C, int64_t M, int64_t N, int64_t kp, int64_t ldc, int64_t c_group,
                    int mt, int nt, int64_t total_iters, int c_col) {
@@ -526,7 +574,7 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(tmem_full, 1);
-    mbar_init(tmem_empty, 128);
+    mbar_init(tmem_empty, 32 * EPI_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -593,41 +641,15 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp >= 4) {
     // ---- epilogue: TMEM -> registers -> recombine -> atomic add into C ----
-    const int wq = warp - 4;
     const int64_t rs = c_col ? 1 : ldc, cs = c_col ? ldc : 1;
     int seg = 0;
     for (int64_t it = it_begin; it < it_end; ++seg) {
       const SkSeg sg = sk_seg(it, it_end, nkb_total);
       const int g = sg.tile / (mt * nt), mn = sg.tile % (mt * nt);
       const int64_t m0 = (int64_t)(mn / nt) * BM, n0 = (int64_t)(mn % nt) * BN;
-      const int64_t row = m0 + wq * 32 + lane;
-      uint64_t* cg = C + (int64_t)g * c_group;
       mbar_wait(tmem_full, seg & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 8) {
-        uint32_t r[8][8];
-#pragma unroll
-        for (int d = 0; d < 8; ++d) {
-          const uint32_t taddr = tmem + ((uint32_t)(wq * 32) << 16) + d * BN + c0;
-          asm volatile(
-              "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-              : "=r"(r[d][0]), "=r"(r[d][1]), "=r"(r[d][2]), "=r"(r[d][3]), "=r"(r[d][4]), "=r"(r[d][5]),
-                "=r"(r[d][6]), "=r"(r[d][7])
-              : "r"(taddr));
-        }
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (row < M) {
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            uint64_t acc = 0;
-#pragma unroll
-            for (int d = 0; d < 8; ++d) acc += (uint64_t)r[d][e] << (8 * d);
-            const int64_t col = n0 + c0 + e;
-            if (col < N) atomicAdd(reinterpret_cast<unsigned long long*>(cg + row * rs + col * cs), acc);
-          }
-        }
-      }
+      epilogue_tile(tmem, warp - 4, lane, true, C + (int64_t)g * c_group, m0, n0, M, N, rs, cs, true);
       asm volatile("tcgen05.fence::before_thread_sync;");
       mbar_arrive(tmem_empty);
       it += sg.nkb;
@@ -1032,7 +1054,7 @@ int mpc3_ring_gemm_packed_layout(const uint8_t* A, const uint8_t* B, uint64_t* C
   if (st) return st;
   dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)(groups * splits));
   MnArgs mn0 = {0, 0, 0, 0, 1 << 30};
-  launch_pdl(gemm_tc_kernel, grid, dim3(256), SMEM_BYTES, as_stream(stream), ta, tb, C, M, N, kp, ldc, c_group, splits,
+  launch_pdl(gemm_tc_kernel, grid, dim3(GEMM_THREADS), SMEM_BYTES, as_stream(stream), ta, tb, C, M, N, kp, ldc, c_group, splits,
              kbs, c_layout, mn0);
   return check_launch("ring_gemm_tc");
 }
@@ -1059,7 +1081,7 @@ int mpc3_ring_gemm_streamk(const uint8_t* A, const uint8_t* B, uint64_t* C, int 
   const int64_t nkb = (kp + BK - 1) / BK;
   const int64_t total = (int64_t)groups * mt * nt * nkb;
   if (ctas > total) ctas = (int)total;
-  launch_pdl(gemm_sk_kernel, dim3(ctas), dim3(256), SMEM_BYTES, as_stream(stream), ta, tb, C, M, N, kp, ldc, c_group,
+  launch_pdl(gemm_sk_kernel, dim3(ctas), dim3(GEMM_THREADS), SMEM_BYTES, as_stream(stream), ta, tb, C, M, N, kp, ldc, c_group,
              mt, nt, total, c_layout);
   return check_launch("ring_gemm_streamk");
 }
@@ -1093,6 +1115,12 @@ int mpc3_ring_gemm_auto(const uint8_t* A, const uint8_t* B, uint64_t* C, int gro
   }
   return mpc3_ring_gemm_packed_layout(A, B, C, groups, M, N, kp, ldc, c_group, (int)splits, c_layout, stream);
 }
+
+#ifdef MPC3_GEMM_TRACE
+int mpc3_debug_gemm_trace(void* out) {
+  return cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace)) == cudaSuccess ? 0 : MPC3_ERR_CUDA;
+}
+#endif
 
 int mpc3_ring_gemm_t(const uint8_t* A, int a_mn, int64_t a_rows, int64_t a_kp, int64_t a_half, const uint8_t* B,
                      int b_mn, int64_t b_rows, int64_t b_kp, int64_t b_half, uint64_t* C, int groups, int64_t M,
@@ -1138,7 +1166,7 @@ int mpc3_ring_gemm_t(const uint8_t* A, int a_mn, int64_t a_rows, int64_t a_kp, i
   }
   MnArgs mn = {a_mn ? 1 : 0, b_mn ? 1 : 0, (int)a_half, (int)b_half, (int)(kc_half / BK)};
   dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)(groups * splits));
-  launch_pdl(gemm_tc_kernel, grid, dim3(256), SMEM_BYTES, as_stream(stream), ta, tb, C, M, N, kp,
+  launch_pdl(gemm_tc_kernel, grid, dim3(GEMM_THREADS), SMEM_BYTES, as_stream(stream), ta, tb, C, M, N, kp,
              c_layout ? M : N, M * N, (int)splits, kbs, c_layout, mn);
   return check_launch("ring_gemm_t");
 }

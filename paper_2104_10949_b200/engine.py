@@ -48,6 +48,28 @@ IMPLICIT_GEMM = os.environ.get("MPC3_IMPLICIT_GEMM", "0") == "1"
 # MPC3_OVERLAP_PACK=0: pack both GEMM operands on the calling stream
 OVERLAP_PACK = os.environ.get("MPC3_OVERLAP_PACK", "1") == "1"
 SMS = 148
+# MPC3_REUSE_PACKS=0: weight gradients pack their own operands instead of
+# reading the forward / input-gradient packs in place (mpc3_ring_gemm_t)
+REUSE_PACKS = os.environ.get("MPC3_REUSE_PACKS", "1") == "1"
+
+
+@dataclass
+class Packed:
+    """A cross-term operand packed for the ring GEMM, kept for reuse: byte-limb
+    planes [3][8][rows][kp] of [first half | second half] with the second half
+    at the 16-aligned column kh, role 0 ([x_i + x_{i+1} | x_i]) or 1
+    ([x_i | x_{i+1}]).  A weight gradient reads two of these transposed."""
+    buf: torch.Tensor
+    rows: int
+    k: int
+    kh: int
+    kp: int
+    role: int
+
+    @staticmethod
+    def geometry(k: int) -> tuple[int, int]:
+        kh = _round_up(k, 16)
+        return kh, _round_up(kh + k, 16)
 
 
 def _stream() -> int:
@@ -528,13 +550,66 @@ class TrioSession:
         return out
 
     # -- bilinear layers (protocols.py:97-136, nn.py:435-484) --
-    def _cross_gemm(self, a_src, a_op, b_src, b_op, M, N, Kd, c_col: bool = False) -> torch.Tensor:
+    def pack(self, src: torch.Tensor, op, rows: int, k: int, role: int) -> Packed:
+        """Pack one cross-term operand in the reusable layout (see Packed)."""
+        kh, kp = Packed.geometry(k)
+        buf = torch.empty(3 * 8 * rows * kp, dtype=torch.uint8, device=_dev())
+        K.call("mpc3_ring_pack_halves", src.data_ptr(), src.stride(0), C.byref(op), role, buf.data_ptr(), kp, kh,
+               _stream())
+        return Packed(buf, rows, k, kh, kp, role)
+
+    def _cross_gemm_kept(self, a_src, a_op, b_src, b_op, M, N, Kd, c_col, a_role, keep, a_packed):
+        """_cross_gemm in the Packed layout: A packed with role a_role (or
+        given), B with the other role, the A pack appended to `keep`."""
+        kh, kp = Packed.geometry(Kd)
+        st = _stream()
+        if a_packed is not None:
+            if (a_packed.rows, a_packed.k, a_packed.kh, a_packed.kp, a_packed.role) != (M, Kd, kh, kp, a_role):
+                raise ShapeError("packed operand does not match the GEMM")
+            A = a_packed
+        else:
+            A = self.pack(a_src, a_op, M, Kd, a_role)
+        B = torch.empty(3 * 8 * N * kp, dtype=torch.uint8, device=_dev())
+        K.call("mpc3_ring_pack_halves", b_src.data_ptr(), b_src.stride(0), C.byref(b_op), 1 - a_role, B.data_ptr(),
+               kp, kh, st)
+        z = torch.empty(3 * M * N, dtype=torch.int64, device=_dev())
+        K.call("mpc3_ring_gemm_auto", A.buf.data_ptr(), B.data_ptr(), z.data_ptr(), 3, M, N, kp, 1 if c_col else 0,
+               st)
+        if keep is not None:
+            keep.append(A)
+        return z
+
+    def wgrad_packed(self, gp: Packed, xp: Packed) -> torch.Tensor:
+        """Weight-gradient cross terms dW_i = (g_i + g_{i+1})^T x_i + g_i^T x_{i+1}
+        (protocols.py:110-115 with nn.py:435-457's operands) straight from the
+        input-gradient pass's role-0 pack of g and the forward pass's role-1
+        pack of x, both read transposed: no operand is packed here.  z is
+        [3][gp.k][xp.k] row-major."""
+        if gp.role != 0 or xp.role != 1 or gp.rows != xp.rows:
+            raise ShapeError("weight-gradient packs do not match")
+        # computed as x^T g (A = x, B = g) into the column-major layout, which
+        # is the same memory and keeps the epilogue's stores coalesced
+        M, N = xp.k, gp.k
+        z = torch.empty(3 * M * N, dtype=torch.int64, device=_dev())
+        K.call("mpc3_ring_gemm_t", xp.buf.data_ptr(), 1, xp.rows, xp.kp, xp.kh, gp.buf.data_ptr(), 1, gp.rows, gp.kp,
+               gp.kh, z.data_ptr(), 3, M, N, _round_up(gp.rows, 32), 1, _stream())
+        return z
+
+    def _cross_gemm(self, a_src, a_op, b_src, b_op, M, N, Kd, c_col: bool = False, a_role: int = 0,
+                    keep: list | None = None, a_packed: Packed | None = None) -> torch.Tensor:
         """z_i = (x_i + x_{i+1}) y_i + x_i y_{i+1} for the three parties, as one
         batched ring GEMM with inner length 2K (protocols.py:110-115).
         Default: pack_kernel writes the byte-limb planes, the TMA-fed tcgen05
         GEMM consumes them; MPC3_IMPLICIT_GEMM=1 selects the in-kernel gather.
         c_col: z[g] column-major (element (m, n) at n*M + m) — only on the
-        packed path; callers check `self.c_col_ok` before asking for it."""
+        packed path; callers check `self.c_col_ok` before asking for it.
+        keep / a_packed / a_role: pack A in the reusable Packed layout with
+        the given role (the operand roles are symmetric), append it to `keep`,
+        or take it ready-packed (training: the weight gradient reuses it)."""
+        if keep is not None or a_packed is not None:
+            if IMPLICIT_GEMM:
+                raise ConfigError("packed-operand reuse needs the explicit pack path")
+            return self._cross_gemm_kept(a_src, a_op, b_src, b_op, M, N, Kd, c_col, a_role, keep, a_packed)
         if IMPLICIT_GEMM:
             splits = gemm_splits(M, N, 2 * Kd, groups=3)
             z = (torch.zeros if splits > 1 else torch.empty)(3 * M * N, dtype=torch.int64, device=_dev())
@@ -603,11 +678,13 @@ class TrioSession:
         return out
 
     def matmul(self, x: RssTensor, y: RssTensor, bits: int | None = None, wgrad: bool = False,
-               bias: RssTensor | None = None) -> RssTensor:
+               bias: RssTensor | None = None, keep: list | None = None, x_packed: Packed | None = None,
+               x_role: int = 0) -> RssTensor:
         """matmul_shares (protocols.py:97-117): cross terms, reshare, truncate.
         wgrad=True marks a weight gradient g^T x whose inner dimension is the
         batch: under data parallelism the shards' cross terms are summed
-        before the (replicated) reshare + truncate."""
+        before the (replicated) reshare + truncate.  keep / x_packed / x_role:
+        see _cross_gemm."""
         if x.ndim != 2 or y.ndim != 2 or x.shape[1] != y.shape[0]:
             raise ShapeError(f"matmul shapes {x.shape} x {y.shape}")
         m, k = x.shape
@@ -619,7 +696,7 @@ class TrioSession:
         xs, ys = x.data.stride(), y.data.stride()
         a_op = K.dense_operand(m, k, s_r=xs[1], t2=xs[2])
         b_op = K.dense_operand(n, k, s_r=ys[2], t2=ys[1])
-        z = self._cross_gemm(x.data, a_op, y.data, b_op, m, n, k)
+        z = self._cross_gemm(x.data, a_op, y.data, b_op, m, n, k, a_role=x_role, keep=keep, a_packed=x_packed)
         out = empty((m, n), x.fp)
         if wgrad:
             self._reduce_cross_terms(z)
@@ -627,8 +704,19 @@ class TrioSession:
                 return self._finish(z, K.make_view((1, 1, m, n)), out, bits, "mul.reshare")
         return self._finish(z, K.make_view((1, 1, m, n)), out, bits, "mul.reshare", bias=bias, bias_dim=3)
 
+    def fc_wgrad_packed(self, gp: Packed, xp: Packed, bits: int) -> RssTensor:
+        """Fully-connected weight gradient g^T x (nn.py:525-527) from the
+        packs of g (rows: batch, K: out) and x (rows: batch, K: in)."""
+        check_accumulation(gp.rows * (self.dp.world if self.dp else 1))
+        m, n = gp.k, xp.k
+        z = self.wgrad_packed(gp, xp)
+        out = empty((m, n), self.fp)
+        self._reduce_cross_terms(z)
+        with self.replicated():
+            return self._finish(z, K.make_view((1, 1, m, n)), out, bits, "mul.reshare")
+
     def conv2d(self, x: RssTensor, k: RssTensor, stride=(1, 1), padding=(0, 0), bits=None,
-               bias: RssTensor | None = None) -> RssTensor:
+               bias: RssTensor | None = None, keep: list | None = None) -> RssTensor:
         """conv2d_shares (protocols.py:120-136), NCHW cross-correlation;
         `bias` (inference extension) is added per output channel after the
         truncation in the same kernel."""
@@ -649,18 +737,22 @@ class TrioSession:
         b_op = K.dense_operand(o, c * kh * kw, s_r=ks[1], t0=ks[2], t1=ks[3], t2=ks[4], K1=kh, K2=kw)
         col = self.c_col_ok
         M = nb * oh * ow
-        z = self._cross_gemm(x.data, a_op, k.data, b_op, M, o, c * kh * kw, c_col=col)
+        # keep: x's im2col pack (role 1) is left for the weight gradient
+        z = self._cross_gemm(x.data, a_op, k.data, b_op, M, o, c * kh * kw, c_col=col, a_role=1 if keep is not None
+                             else 0, keep=keep)
         out = empty((nb, o, oh, ow), x.fp)
         # z[(n, y, x), o]: column-major keeps each (n, o) plane's (y, x) run contiguous
         zs = (oh * ow, M, ow, 1) if col else (oh * ow * o, 1, ow * o, o)
         view = K.make_view((nb, o, oh, ow), z_stride=zs)
         return self._finish(z, view, out, bits, "mul.reshare", bias=bias, bias_dim=1)
 
-    def conv2d_wgrad(self, x: RssTensor, g: RssTensor, kernel, stride, padding, bits) -> RssTensor:
+    def conv2d_wgrad(self, x: RssTensor, g: RssTensor, kernel, stride, padding, bits,
+                     packs: tuple[Packed, Packed] | None = None) -> RssTensor:
         """Kernel gradient (nn.py:435-457) as one direct implicit GEMM with
         K = N*OH*OW; the reference's dilated zeros contribute nothing, and the
         zero shares / truncation words are indexed over its full (C,O,fh,fw)
-        output so the result is bit-exact."""
+        output so the result is bit-exact.  packs = (pack of g, im2col pack
+        of x) from the surrounding passes: the GEMM reads them transposed."""
         nb, c, h, w = x.shape
         nb2, o, oh, ow = g.shape
         kh, kw = kernel
@@ -677,7 +769,13 @@ class TrioSession:
         b_op = K.dense_operand(o, nb * oh * ow, s_r=gs[2], t0=gs[1], t1=gs[3], t2=gs[4], K1=oh, K2=ow)
         col = self.c_col_ok
         M = c * kh * kw
-        z = self._cross_gemm(x.data, a_op, g.data, b_op, M, o, nb * oh * ow, c_col=col)
+        if packs is not None:  # z[o][(c, u, v)]: the column-major layout below
+            gp, xp = packs
+            if (gp.rows, gp.k, xp.rows, xp.k) != (nb * oh * ow, o, nb * oh * ow, M):
+                raise ShapeError("weight-gradient packs do not match the layer")
+            z, col = self.wgrad_packed(gp, xp), True
+        else:
+            z = self._cross_gemm(x.data, a_op, g.data, b_op, M, o, nb * oh * ow, c_col=col)
         out = empty((o, c, kh, kw), x.fp)
         zs = (kh * kw, M, kw, 1) if col else (kh * kw * o, 1, kw * o, o)
         view = K.make_view((c, o, fh, fw), crop=(c, o, kh, kw), z_stride=zs,
@@ -686,7 +784,25 @@ class TrioSession:
         with self.replicated():
             return self._finish(z, view, out, bits, "mul.reshare")
 
-    def conv2d_dgrad(self, g: RssTensor, k: RssTensor, stride, padding, in_shape, bits) -> RssTensor:
+    def grad_operand(self, g: RssTensor):
+        """(operand, rows, K) of an output gradient as the left operand of its
+        layer's input-gradient GEMM: rows are the batch positions (n, y, x),
+        K the output channels (the layout both that GEMM and the weight
+        gradient read)."""
+        gs = g.data.stride()
+        if g.ndim == 2:
+            b, o = g.shape
+            return K.dense_operand(b, o, s_r=gs[1], t2=gs[2]), b, o
+        nb, o, oh, ow = g.shape
+        return (K.conv_operand(K.GATHER_IM2COL, nb * oh * ow, o, nb, o, oh, ow, gs[1:], 1, 1, 1, 1, 0, 0, oh, ow),
+                nb * oh * ow, o)
+
+    def pack_grad(self, g: RssTensor) -> Packed:
+        op, rows, k = self.grad_operand(g)
+        return self.pack(g.data, op, rows, k, 0)
+
+    def conv2d_dgrad(self, g: RssTensor, k: RssTensor, stride, padding, in_shape, bits,
+                     g_packed: Packed | None = None) -> RssTensor:
         """Input gradient (nn.py:460-484).  Two bit-identical formulations
         (same ring values, same PRF words at the reference's flat indices of
         the full (N, C, hf, wf) correlation); the cheaper one for the shape:
@@ -701,9 +817,10 @@ class TrioSession:
         if stride == (1, 1) or tuple(stride) == (1, 1):
             if _dgrad_cost_im2col(nb, o, oh, ow, c, kh, kw, padding) < _dgrad_cost_col2im(nb, o, oh, ow, c, kh, kw):
                 return self.conv2d_dgrad_im2col(g, k, stride, padding, in_shape, bits)
-        return self.conv2d_dgrad_col2im(g, k, stride, padding, in_shape, bits)
+        return self.conv2d_dgrad_col2im(g, k, stride, padding, in_shape, bits, g_packed=g_packed)
 
-    def conv2d_dgrad_col2im(self, g: RssTensor, k: RssTensor, stride, padding, in_shape, bits) -> RssTensor:
+    def conv2d_dgrad_col2im(self, g: RssTensor, k: RssTensor, stride, padding, in_shape, bits,
+                            g_packed: Packed | None = None) -> RssTensor:
         """Input gradient as a transposed convolution: one ring GEMM
         cols = g^T-rows x k (inner length O) and a fused col2im + reshare +
         truncate + embed kernel."""
@@ -719,7 +836,7 @@ class TrioSession:
         ncols = c * kh * kw
         b_op = K.dense_operand(ncols, o, s_r=1, t2=ncols)
         col = self.c_col_ok  # column-major cols: the col2im gathers along x coalesce
-        z = self._cross_gemm(g.data, a_op, k.data, b_op, nb * oh * ow, ncols, o, c_col=col)
+        z = self._cross_gemm(g.data, a_op, k.data, b_op, nb * oh * ow, ncols, o, c_col=col, a_packed=g_packed)
         out = zeros((nb, c, h, w), g.fp)
         ja = self.take(ARITH)
         jr, jq = self.take(TR_RHO), self.take(TR_R)

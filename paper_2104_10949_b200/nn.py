@@ -242,14 +242,20 @@ class TrioNet:
     def _run(self, layers, it, h: RssTensor, record: bool):
         S, acts = self.s, []
         for spec in layers:
+            # recording keeps each layer input's packed GEMM operand (role 1)
+            # for the weight gradient, which reads it in place
+            keep = [] if record and E.REUSE_PACKS and not E.IMPLICIT_GEMM else None
             if spec.kind == CONV2D:
                 k = next(it)
-                acts.append((h, k) if record else None)
-                h = S.conv2d(h, k, spec.stride, spec.padding, bias=next(it) if spec.bias else None)
+                x = h
+                h = S.conv2d(h, k, spec.stride, spec.padding, bias=next(it) if spec.bias else None, keep=keep)
+                acts.append(((x, k) + tuple(keep or ())) if record else None)
             elif spec.kind == FULLY_CONNECTED:
                 w = next(it)
-                acts.append((h, w) if record else None)
-                h = S.matmul(h, w.apply(lambda d: d.transpose(1, 2)), bias=next(it) if spec.bias else None)
+                x = h
+                h = S.matmul(h, w.apply(lambda d: d.transpose(1, 2)), bias=next(it) if spec.bias else None,
+                             keep=keep, x_role=1 if keep is not None else 0)
+                acts.append(((x, w) + tuple(keep or ())) if record else None)
             elif spec.kind == AVGPOOL:
                 acts.append((h.shape,) if record else None)
                 h = S.avgpool(h, spec.window, spec.stride, spec.padding)
@@ -314,21 +320,29 @@ class TrioNet:
             if li == plist[0]:
                 mark_rest()
             if spec.kind == FULLY_CONNECTED:
-                x, w = cached
+                x, w = cached[:2]
+                xp = cached[2] if len(cached) > 2 else None
+                gp = S.pack_grad(g) if xp is not None else None  # shared by dgrad and wgrad
                 pi -= 1
-                grads[pi] = wgrad(lambda gg, xx: S.matmul(gg.apply(lambda d: d.transpose(1, 2)), xx,
-                                                          bits=t + batch_bits, wgrad=True), g, x)
+                if xp is not None:
+                    grads[pi] = wgrad(lambda a, b: S.fc_wgrad_packed(a, b, t + batch_bits), gp, xp)
+                else:
+                    grads[pi] = wgrad(lambda gg, xx: S.matmul(gg.apply(lambda d: d.transpose(1, 2)), xx,
+                                                              bits=t + batch_bits, wgrad=True), g, x)
                 if li == plist[0]:
                     break
-                g = S.matmul(g, w)
+                g = S.matmul(g, w, x_packed=gp)
             elif spec.kind == CONV2D:
-                x, k = cached
+                x, k = cached[:2]
+                xp = cached[2] if len(cached) > 2 else None
+                gp = S.pack_grad(g) if xp is not None else None
                 pi -= 1
-                grads[pi] = wgrad(lambda xx, gg: S.conv2d_wgrad(xx, gg, spec.kernel, spec.stride, spec.padding,
-                                                                bits=t + batch_bits), x, g)
+                grads[pi] = wgrad(lambda xx, gg, a, b: S.conv2d_wgrad(
+                    xx, gg, spec.kernel, spec.stride, spec.padding, bits=t + batch_bits,
+                    packs=None if b is None else (a, b)), x, g, gp, xp)
                 if li == plist[0]:
                     break
-                g = S.conv2d_dgrad(g, k, spec.stride, spec.padding, x.shape, bits=t)
+                g = S.conv2d_dgrad(g, k, spec.stride, spec.padding, x.shape, bits=t, g_packed=gp)
             elif spec.kind == AVGPOOL:
                 g = S.avgpool_backward(g, spec.window, spec.stride, cached[0])
             elif spec.kind == RELU:
@@ -801,7 +815,9 @@ def _split_acts(acts):
             if a is None:
                 per[p].append(None)
             else:
-                per[p].append(tuple(split_trio(v)[p] if isinstance(v, RssTensor) else v for v in a))
+                # packed trio operands (E.Packed) hold every party's share: not split out
+                per[p].append(tuple(split_trio(v)[p] if isinstance(v, RssTensor) else v for v in a
+                                    if not isinstance(v, E.Packed)))
     return [_Acts(v) for v in per]
 
 

@@ -76,6 +76,33 @@ def gemm_sweep(sizes):
     return out
 
 
+def gemm_t_compare(shapes):
+    """Weight-gradient GEMM read transposed from packed buffers (mpc3_ring_gemm_t,
+    MN-major tiles) vs the same product from K-major packs (gemm_auto)."""
+    out = []
+    for (M, N, R) in shapes:
+        kc = (R + 31) // 32 * 32
+        kha, khb = (M + 15) // 16 * 16, (N + 15) // 16 * 16
+        kpa, kpb = (kha + M + 15) // 16 * 16, (khb + N + 15) // 16 * 16
+        A = torch.randint(0, 256, (3 * 8 * R * kpa,), dtype=torch.uint8, device="cuda")
+        B = torch.randint(0, 256, (3 * 8 * R * kpb,), dtype=torch.uint8, device="cuda")
+        Ak = torch.randint(0, 256, (3 * 8 * M * 2 * kc,), dtype=torch.uint8, device="cuda")
+        Bk = torch.randint(0, 256, (3 * 8 * N * 2 * kc,), dtype=torch.uint8, device="cuda")
+        Cm = torch.empty(3 * M * N, dtype=torch.int64, device="cuda")
+        t_mn = graph_us(lambda: _capi.call("mpc3_ring_gemm_t", p(A), 1, R, kpa, kha, p(B), 1, R, kpb, khb, p(Cm), 3,
+                                           M, N, kc, 0, st()), reps=5)
+        t_k = graph_us(lambda: _capi.call("mpc3_ring_gemm_auto", p(Ak), p(Bk), p(Cm), 3, M, N, 2 * kc, 0, st()), reps=5)
+        t_amn = graph_us(lambda: _capi.call("mpc3_ring_gemm_t", p(A), 1, R, kpa, kha, p(Bk), 0, N, 2 * kc, 0, p(Cm),
+                                            3, M, N, kc, 0, st()), reps=5)
+        t_bmn = graph_us(lambda: _capi.call("mpc3_ring_gemm_t", p(Ak), 0, M, 2 * kc, 0, p(B), 1, R, kpb, khb, p(Cm),
+                                            3, M, N, kc, 0, st()), reps=5)
+        ops = 72 * 3 * M * N * 2 * R
+        out.append({"M": M, "N": N, "R": R, "mn_us": t_mn, "kmajor_us": t_k, "mn_tops": ops / t_mn / 1e6,
+                    "kmajor_tops": ops / t_k / 1e6, "a_mn_tops": ops / t_amn / 1e6, "b_mn_tops": ops / t_bmn / 1e6})
+        print("gemm_t", out[-1], flush=True)
+    return out
+
+
 def int8_peak():
     n = 8192
     a = torch.randint(-128, 127, (n, n), dtype=torch.int8, device="cuda")
@@ -137,7 +164,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="gpurun_out/microbench.json")
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--gemm-t", action="store_true", help="only the transposed-operand GEMM comparison")
     args = ap.parse_args()
+    if args.gemm_t:
+        res = gemm_t_compare([(256, 3456, 128), (384, 3456, 128), (96, 363, 12800), (256, 2400, 512),
+                              (256, 256, 128), (1024, 1024, 4096), (4096, 4096, 4096)])
+        with open(args.out, "w") as f:
+            json.dump(res, f, indent=1)
+        return
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     res = {"device": torch.cuda.get_device_name(), "when": time.time()}
     res["aes"] = aes_rate()

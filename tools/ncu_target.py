@@ -3,6 +3,7 @@
 python tools/ncu_target.py gemm 4096      # mpc3_ring_gemm_packed, M=N=K=n (packed limb planes)
 python tools/ncu_target.py sign 16777216  # fused sign/ReLU circuit on n elements
 python tools/ncu_target.py pack 4096      # dense cross-term pack, 3 parties, M=K=n
+python tools/ncu_target.py wgrad 128      # transposed-operand GEMM, AlexNet conv5 weight gradient (R=n)
 """
 import ctypes as C
 import os
@@ -37,6 +38,16 @@ def main(kind, n, reps=3):
         op.mode, op.rows, op.k, op.s_r, op.t2 = 0, n, n, n, 1
         for _ in range(reps):
             _capi.call("mpc3_ring_pack", p(x), n * n, C.byref(op), 0, p(out), kp, st())
+    elif kind == "wgrad":  # M = 256 (O), N = 2304 (C*3*3), contraction R = n rows, MN-read packs
+        M, N, R = 256, 2304, n
+        kc = (R + 31) // 32 * 32
+        kha, khb = M, N
+        kpa, kpb = 2 * M, 2 * N
+        A = torch.randint(0, 256, (3 * 8 * R * kpa,), dtype=torch.uint8, device="cuda")
+        B = torch.randint(0, 256, (3 * 8 * R * kpb,), dtype=torch.uint8, device="cuda")
+        Cm = torch.empty(3 * M * N, dtype=torch.int64, device="cuda")
+        for _ in range(reps):
+            _capi.call("mpc3_ring_gemm_t", p(B), 1, R, kpb, khb, p(A), 1, R, kpa, kha, p(Cm), 3, N, M, kc, 1, st())
     else:
         raise SystemExit(f"unknown kernel {kind}")
     torch.cuda.synchronize()
