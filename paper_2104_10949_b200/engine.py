@@ -560,23 +560,56 @@ class TrioSession:
 
     def _cross_gemm_kept(self, a_src, a_op, b_src, b_op, M, N, Kd, c_col, a_role, keep, a_packed):
         """_cross_gemm in the Packed layout: A packed with role a_role (or
-        given), B with the other role, the A pack appended to `keep`."""
+        given), B with the other role; both packs appended to `keep` (the
+        backward pass reads them transposed)."""
         kh, kp = Packed.geometry(Kd)
         st = _stream()
+        B = torch.empty(3 * 8 * N * kp, dtype=torch.uint8, device=_dev())
+        main = torch.cuda.current_stream()
+        ps = self.pack_stream() if OVERLAP_PACK else None
+        if ps is not None and ps != main:  # B on the pack stream, A here
+            ev = torch.cuda.Event()
+            ev.record(main)
+            ps.wait_event(ev)
+            K.call("mpc3_ring_pack_halves", b_src.data_ptr(), b_src.stride(0), C.byref(b_op), 1 - a_role,
+                   B.data_ptr(), kp, kh, ps.cuda_stream)
+        else:
+            K.call("mpc3_ring_pack_halves", b_src.data_ptr(), b_src.stride(0), C.byref(b_op), 1 - a_role,
+                   B.data_ptr(), kp, kh, st)
         if a_packed is not None:
             if (a_packed.rows, a_packed.k, a_packed.kh, a_packed.kp, a_packed.role) != (M, Kd, kh, kp, a_role):
                 raise ShapeError("packed operand does not match the GEMM")
             A = a_packed
         else:
             A = self.pack(a_src, a_op, M, Kd, a_role)
-        B = torch.empty(3 * 8 * N * kp, dtype=torch.uint8, device=_dev())
-        K.call("mpc3_ring_pack_halves", b_src.data_ptr(), b_src.stride(0), C.byref(b_op), 1 - a_role, B.data_ptr(),
-               kp, kh, st)
+        if ps is not None and ps != main:
+            ev2 = torch.cuda.Event()
+            ev2.record(ps)
+            main.wait_event(ev2)
         z = torch.empty(3 * M * N, dtype=torch.int64, device=_dev())
         K.call("mpc3_ring_gemm_auto", A.buf.data_ptr(), B.data_ptr(), z.data_ptr(), 3, M, N, kp, 1 if c_col else 0,
                st)
         if keep is not None:
-            keep.append(A)
+            keep.extend([A, Packed(B, N, Kd, kh, kp, 1 - a_role)])
+        return z
+
+    def dgrad_packed(self, g_src: torch.Tensor, g_op, rows: int, o: int, wp: Packed, c_col: bool) -> torch.Tensor:
+        """Input-gradient cross terms z_i = g_i (W_i + W_{i+1}) + g_{i+1} W_i
+        (protocols.py:110-115 for nn.py:460-484 / 525-530's g . W) with W read
+        transposed from the forward pass's role-0 weight pack (no W^T pack):
+        g is packed role 1 with its halves at kc_half = roundup(O, 32), the
+        contraction of the MN-read weight rows.  z: [3][rows][wp.k] (or
+        column-major)."""
+        if wp.role != 0 or wp.rows != o:
+            raise ShapeError("weight pack does not match the input gradient")
+        kc = _round_up(o, 32)
+        A = torch.empty(3 * 8 * rows * 2 * kc, dtype=torch.uint8, device=_dev())
+        st = _stream()
+        K.call("mpc3_ring_pack_halves", g_src.data_ptr(), g_src.stride(0), C.byref(g_op), 1, A.data_ptr(), 2 * kc, kc,
+               st)
+        z = torch.empty(3 * rows * wp.k, dtype=torch.int64, device=_dev())
+        K.call("mpc3_ring_gemm_t", A.data_ptr(), 0, rows, 2 * kc, 0, wp.buf.data_ptr(), 1, wp.rows, wp.kp, wp.kh,
+               z.data_ptr(), 3, rows, wp.k, kc, 1 if c_col else 0, st)
         return z
 
     def wgrad_packed(self, gp: Packed, xp: Packed) -> torch.Tensor:
@@ -715,6 +748,17 @@ class TrioSession:
         with self.replicated():
             return self._finish(z, K.make_view((1, 1, m, n)), out, bits, "mul.reshare")
 
+    def fc_dgrad_packed(self, g: RssTensor, wp: Packed, bits: int | None = None) -> RssTensor:
+        """g . W for a fully-connected layer (nn.py:529-530) with W from its
+        forward pack; the same reshare + truncate as matmul."""
+        b, o = g.shape
+        bits = self.fp.t if bits is None else bits
+        check_accumulation(o)
+        op, rows, k = self.grad_operand(g)
+        z = self.dgrad_packed(g.data, op, rows, o, wp, False)
+        out = empty((b, wp.k), g.fp)
+        return self._finish(z, K.make_view((1, 1, b, wp.k)), out, bits, "mul.reshare")
+
     def conv2d(self, x: RssTensor, k: RssTensor, stride=(1, 1), padding=(0, 0), bits=None,
                bias: RssTensor | None = None, keep: list | None = None) -> RssTensor:
         """conv2d_shares (protocols.py:120-136), NCHW cross-correlation;
@@ -802,7 +846,7 @@ class TrioSession:
         return self.pack(g.data, op, rows, k, 0)
 
     def conv2d_dgrad(self, g: RssTensor, k: RssTensor, stride, padding, in_shape, bits,
-                     g_packed: Packed | None = None) -> RssTensor:
+                     w_packed: Packed | None = None) -> RssTensor:
         """Input gradient (nn.py:460-484).  Two bit-identical formulations
         (same ring values, same PRF words at the reference's flat indices of
         the full (N, C, hf, wf) correlation); the cheaper one for the shape:
@@ -817,10 +861,10 @@ class TrioSession:
         if stride == (1, 1) or tuple(stride) == (1, 1):
             if _dgrad_cost_im2col(nb, o, oh, ow, c, kh, kw, padding) < _dgrad_cost_col2im(nb, o, oh, ow, c, kh, kw):
                 return self.conv2d_dgrad_im2col(g, k, stride, padding, in_shape, bits)
-        return self.conv2d_dgrad_col2im(g, k, stride, padding, in_shape, bits, g_packed=g_packed)
+        return self.conv2d_dgrad_col2im(g, k, stride, padding, in_shape, bits, w_packed=w_packed)
 
     def conv2d_dgrad_col2im(self, g: RssTensor, k: RssTensor, stride, padding, in_shape, bits,
-                            g_packed: Packed | None = None) -> RssTensor:
+                            w_packed: Packed | None = None) -> RssTensor:
         """Input gradient as a transposed convolution: one ring GEMM
         cols = g^T-rows x k (inner length O) and a fused col2im + reshare +
         truncate + embed kernel."""
@@ -836,7 +880,12 @@ class TrioSession:
         ncols = c * kh * kw
         b_op = K.dense_operand(ncols, o, s_r=1, t2=ncols)
         col = self.c_col_ok  # column-major cols: the col2im gathers along x coalesce
-        z = self._cross_gemm(g.data, a_op, k.data, b_op, nb * oh * ow, ncols, o, c_col=col, a_packed=g_packed)
+        if w_packed is not None:  # the forward pass's weight pack, read transposed
+            if w_packed.k != ncols:
+                raise ShapeError("weight pack does not match the layer")
+            z = self.dgrad_packed(g.data, a_op, nb * oh * ow, o, w_packed, col)
+        else:
+            z = self._cross_gemm(g.data, a_op, k.data, b_op, nb * oh * ow, ncols, o, c_col=col)
         out = zeros((nb, c, h, w), g.fp)
         ja = self.take(ARITH)
         jr, jq = self.take(TR_RHO), self.take(TR_R)

@@ -321,8 +321,8 @@ class TrioNet:
                 mark_rest()
             if spec.kind == FULLY_CONNECTED:
                 x, w = cached[:2]
-                xp = cached[2] if len(cached) > 2 else None
-                gp = S.pack_grad(g) if xp is not None else None  # shared by dgrad and wgrad
+                xp, wp = cached[2:4] if len(cached) > 3 else (None, None)
+                gp = S.pack_grad(g) if xp is not None else None
                 pi -= 1
                 if xp is not None:
                     grads[pi] = wgrad(lambda a, b: S.fc_wgrad_packed(a, b, t + batch_bits), gp, xp)
@@ -331,10 +331,10 @@ class TrioNet:
                                                               bits=t + batch_bits, wgrad=True), g, x)
                 if li == plist[0]:
                     break
-                g = S.matmul(g, w, x_packed=gp)
+                g = S.fc_dgrad_packed(g, wp) if wp is not None else S.matmul(g, w)
             elif spec.kind == CONV2D:
                 x, k = cached[:2]
-                xp = cached[2] if len(cached) > 2 else None
+                xp, wp = cached[2:4] if len(cached) > 3 else (None, None)
                 gp = S.pack_grad(g) if xp is not None else None
                 pi -= 1
                 grads[pi] = wgrad(lambda xx, gg, a, b: S.conv2d_wgrad(
@@ -342,7 +342,7 @@ class TrioNet:
                     packs=None if b is None else (a, b)), x, g, gp, xp)
                 if li == plist[0]:
                     break
-                g = S.conv2d_dgrad(g, k, spec.stride, spec.padding, x.shape, bits=t, g_packed=gp)
+                g = S.conv2d_dgrad(g, k, spec.stride, spec.padding, x.shape, bits=t, w_packed=wp)
             elif spec.kind == AVGPOOL:
                 g = S.avgpool_backward(g, spec.window, spec.stride, cached[0])
             elif spec.kind == RELU:
