@@ -329,6 +329,40 @@ DEV uint64_t desc_b(uint32_t addr, bool mn) {
   return mn ? umma_desc_mn(addr, BN * BK, 8 * BN, 4) : umma_desc_sw32(addr);
 }
 
+// One pipeline stage: the A and B limb tiles of K-block kb of tile (m0, n0),
+// group g (MN operands: source rows / half of the transposed read).
+DEV void load_stage(const CUtensorMap* tmA, const CUtensorMap* tmB, uint64_t* bar, uint8_t* sa, uint8_t* sb, int kb,
+                    int m0, int n0, int g, const MnArgs& mn) {
+  mbar_expect_tx(bar, A_STAGE + B_STAGE);
+  const int kc = kb * BK;
+  const int h = kb >= mn.nkb_half ? 1 : 0, r = (kb - h * mn.nkb_half) * BK;
+  if (mn.a_mn)
+    tma_load_3d(tmA, bar, sa, h * mn.a_half + m0, r, g * 8);
+  else
+    tma_load_3d(tmA, bar, sa, kc, m0, g * 8);
+  if (mn.b_mn)
+    tma_load_3d(tmB, bar, sb, h * mn.b_half + n0, r, g * 8);
+  else
+    tma_load_3d(tmB, bar, sb, kc, n0, g * 8);
+}
+
+// The 36 limb-pair products of one stage as 12 MMAs into the 8 diagonal
+// accumulators (diagonal d = li + lj at TMEM columns d * BN).
+DEV void mma_stage(uint32_t tmem, uint32_t a_base, uint32_t b_base, bool first, const MnArgs& mn) {
+  const uint32_t idesc_mn = ((uint32_t)(mn.a_mn != 0) << 15) | ((uint32_t)(mn.b_mn != 0) << 16);
+#pragma unroll
+  for (int li = 0; li < 8; ++li) {
+    const uint64_t da = desc_a(a_base + li * (BM * BK), mn.a_mn);
+    const int nblk = 8 - li;  // limb blocks j = 0 .. 7 - li  ->  diagonals li .. 7
+    const int nfirst = nblk > 4 ? 4 : nblk;
+    const uint32_t acc = (!first || li > 0) ? 1u : 0u;
+    mma_i8(tmem + li * BN, da, desc_b(b_base, mn.b_mn), idesc_i8(nfirst * BN) | idesc_mn, acc);
+    if (nblk > 4)
+      mma_i8(tmem + (li + 4) * BN, da, desc_b(b_base + 4 * (BN * BK), mn.b_mn), idesc_i8((nblk - 4) * BN) | idesc_mn,
+             acc);
+  }
+}
+
 // Epilogue of one 128 x BN tile: TMEM -> registers -> recombine the 8
 // diagonal int32 accumulators (sum S_d << 8d) -> C.  EPI_WARPS warps share a
 // tile: warp ew reads TMEM lane quadrant ew % 4 (its rows) and the column
@@ -462,45 +496,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
     for (int i = 0; i < nkb; ++i) {
-      int s = i % STAGES;
-      uint32_t ph = (i / STAGES) & 1;
-      mbar_wait(&empty[s], ph ^ 1);
-      mbar_expect_tx(&full[s], A_STAGE + B_STAGE);
-      const int kb = kb0 + i;
-      const int kc = kb * BK;
-      const int h = kb >= mn.nkb_half ? 1 : 0, r = (kb - h * mn.nkb_half) * BK;  // MN: source rows / half
-      if (mn.a_mn)
-        tma_load_3d(&tmA, &full[s], sA + s * A_STAGE, h * mn.a_half + (int)m0, r, g * 8);
-      else
-        tma_load_3d(&tmA, &full[s], sA + s * A_STAGE, kc, (int)m0, g * 8);
-      if (mn.b_mn)
-        tma_load_3d(&tmB, &full[s], sB + s * B_STAGE, h * mn.b_half + (int)n0, r, g * 8);
-      else
-        tma_load_3d(&tmB, &full[s], sB + s * B_STAGE, kc, (int)n0, g * 8);
+      const int s = i % STAGES;
+      mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+      load_stage(&tmA, &tmB, &full[s], sA + s * A_STAGE, sB + s * B_STAGE, kb0 + i, (int)m0, (int)n0, g, mn);
     }
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer ----
-    const uint32_t idesc_mn = ((uint32_t)(mn.a_mn != 0) << 15) | ((uint32_t)(mn.b_mn != 0) << 16);
     for (int i = 0; i < nkb; ++i) {
-      int s = i % STAGES;
-      uint32_t ph = (i / STAGES) & 1;
-      mbar_wait(&full[s], ph);
+      const int s = i % STAGES;
+      mbar_wait(&full[s], (i / STAGES) & 1);
       if (i == 0) TRACE(2);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      uint32_t a_base = smem_u32(sA + s * A_STAGE);
-      uint32_t b_base = smem_u32(sB + s * B_STAGE);
-#pragma unroll
-      for (int li = 0; li < 8; ++li) {
-        uint64_t da = desc_a(a_base + li * (BM * BK), mn.a_mn);
-        int nblk = 8 - li;  // limb blocks j = 0 .. 7 - li  ->  diagonals li .. 7
-        int first = nblk > 4 ? 4 : nblk;
-        uint32_t acc = (i > 0 || li > 0) ? 1u : 0u;
-        mma_i8(tmem + li * BN, da, desc_b(b_base, mn.b_mn), idesc_i8(first * BN) | idesc_mn, acc);
-        if (nblk > 4) {
-          mma_i8(tmem + (li + 4) * BN, da, desc_b(b_base + 4 * (BN * BK), mn.b_mn),
-                 idesc_i8((nblk - 4) * BN) | idesc_mn, acc);
-        }
-      }
+      mma_stage(tmem, smem_u32(sA + s * A_STAGE), smem_u32(sB + s * B_STAGE), i == 0, mn);
       mma_commit(&empty[s]);
     }
     mma_commit(tmem_full);
@@ -551,7 +558,7 @@ DEV SkSeg sk_seg(int64_t it, int64_t it_end, int nkb_total) {
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_sk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    uint64_t* __restrict__ C, int64_t M, int64_t N, int64_t kp, int64_t ldc, int64_t c_group,
-                   int mt, int nt, int64_t total_iters, int c_col) {
+                   int mt, int nt, int64_t total_iters, int c_col, MnArgs mn) {
   griddep_launch();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -594,16 +601,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     int i = 0;
     for (int64_t it = it_begin; it < it_end;) {
       const SkSeg sg = sk_seg(it, it_end, nkb_total);
-      const int g = sg.tile / (mt * nt), mn = sg.tile % (mt * nt);
-      const int m0 = (mn / nt) * BM, n0 = (mn % nt) * BN;
+      const int g = sg.tile / (mt * nt), tmn = sg.tile % (mt * nt);
+      const int m0 = (tmn / nt) * BM, n0 = (tmn % nt) * BN;
       for (int k = 0; k < sg.nkb; ++k, ++i) {
         const int s = i % STAGES;
-        const uint32_t ph = (i / STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        mbar_expect_tx(&full[s], A_STAGE + B_STAGE);
-        const int kc = (sg.kb0 + k) * BK;
-        tma_load_3d(&tmA, &full[s], sA + s * A_STAGE, kc, m0, g * 8);
-        tma_load_3d(&tmB, &full[s], sB + s * B_STAGE, kc, n0, g * 8);
+        mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+        load_stage(&tmA, &tmB, &full[s], sA + s * A_STAGE, sB + s * B_STAGE, sg.kb0 + k, m0, n0, g, mn);
       }
       it += sg.nkb;
     }
@@ -621,19 +624,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const uint32_t ph = (i / STAGES) & 1;
         mbar_wait(&full[s], ph);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t a_base = smem_u32(sA + s * A_STAGE);
-        const uint32_t b_base = smem_u32(sB + s * B_STAGE);
-#pragma unroll
-        for (int li = 0; li < 8; ++li) {
-          const uint64_t da = umma_desc_sw32(a_base + li * (BM * BK));
-          const int nblk = 8 - li;
-          const int first = nblk > 4 ? 4 : nblk;
-          const uint32_t acc = (k > 0 || li > 0) ? 1u : 0u;
-          mma_i8(tmem + li * BN, da, umma_desc_sw32(b_base), idesc_i8(first * BN), acc);
-          if (nblk > 4)
-            mma_i8(tmem + (li + 4) * BN, da, umma_desc_sw32(b_base + 4 * (BN * BK)), idesc_i8((nblk - 4) * BN),
-                   acc);
-        }
+        mma_stage(tmem, smem_u32(sA + s * A_STAGE), smem_u32(sB + s * B_STAGE), k == 0, mn);
         mma_commit(&empty[s]);
       }
       mma_commit(tmem_full);
@@ -645,8 +636,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     int seg = 0;
     for (int64_t it = it_begin; it < it_end; ++seg) {
       const SkSeg sg = sk_seg(it, it_end, nkb_total);
-      const int g = sg.tile / (mt * nt), mn = sg.tile % (mt * nt);
-      const int64_t m0 = (int64_t)(mn / nt) * BM, n0 = (int64_t)(mn % nt) * BN;
+      const int g = sg.tile / (mt * nt), tmn = sg.tile % (mt * nt);
+      const int64_t m0 = (int64_t)(tmn / nt) * BM, n0 = (int64_t)(tmn % nt) * BN;
       mbar_wait(tmem_full, seg & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       epilogue_tile(tmem, warp - 4, lane, true, C + (int64_t)g * c_group, m0, n0, M, N, rs, cs, true);
@@ -1081,8 +1072,9 @@ int mpc3_ring_gemm_streamk(const uint8_t* A, const uint8_t* B, uint64_t* C, int 
   const int64_t nkb = (kp + BK - 1) / BK;
   const int64_t total = (int64_t)groups * mt * nt * nkb;
   if (ctas > total) ctas = (int)total;
+  MnArgs mn0 = {0, 0, 0, 0, 1 << 30};
   launch_pdl(gemm_sk_kernel, dim3(ctas), dim3(GEMM_THREADS), SMEM_BYTES, as_stream(stream), ta, tb, C, M, N, kp, ldc, c_group,
-             mt, nt, total, c_layout);
+             mt, nt, total, c_layout, mn0);
   return check_launch("ring_gemm_streamk");
 }
 
@@ -1104,11 +1096,12 @@ int mpc3_ring_gemm_auto(const uint8_t* A, const uint8_t* B, uint64_t* C, int gro
   const int64_t ctas = tiles * splits;
   const double eff = (double)ctas / (double)(((ctas + sms - 1) / sms) * sms);
   const size_t cbytes = (size_t)groups * M * N * 8;
-  if (nkb == 0 || eff < 0.85 || splits > 1) {
+  static const double sk_eff = getenv("MPC3_GEMM_SK") ? atof(getenv("MPC3_GEMM_SK")) : 0.85;
+  if (nkb == 0 || eff < sk_eff || splits > 1) {
     if (cudaMemsetAsync(C, 0, cbytes, as_stream(stream)) != cudaSuccess) return check_launch("gemm C memset");
     if (nkb == 0) return MPC3_OK;
   }
-  if (eff < 0.85) {  // the split-K grid would leave SMs idle: stream-K over every SM
+  if (eff < sk_eff) {  // the split-K grid would leave SMs idle: stream-K over every SM
     int64_t iters = tiles * nkb;
     int64_t c = iters / 2 < sms ? iters / 2 : sms;
     return mpc3_ring_gemm_streamk(A, B, C, groups, M, N, kp, ldc, c_group, (int)(c < 1 ? 1 : c), c_layout, stream);
@@ -1159,12 +1152,33 @@ int mpc3_ring_gemm_t(const uint8_t* A, int a_mn, int64_t a_rows, int64_t a_kp, i
   const int64_t splits = need > occ ? need : occ;
   const int kbs = (int)((nkb + splits - 1) / splits);
   if ((int64_t)kbs * BK > MAX_SPLIT_K) return MPC3_ERR_EXACTNESS;
-  if (nkb == 0 || splits > 1) {
+  const int64_t ctas = tiles * splits;
+  const double eff = (double)ctas / (double)(((ctas + sms - 1) / sms) * sms);
+  MnArgs mn = {a_mn ? 1 : 0, b_mn ? 1 : 0, (int)a_half, (int)b_half, (int)(kc_half / BK)};
+  // stream-K off by default here: the weight gradients run on the side stream
+  // beside the input-gradient chain, which a persistent all-SM grid would
+  // block (AlexNet step 2.79 ms without, 2.84 ms with stream-K at eff < 0.85)
+  static const double sk_eff = getenv("MPC3_GEMM_T_SK") ? atof(getenv("MPC3_GEMM_T_SK")) : 0.0;
+  if (nkb == 0 || splits > 1 || eff < sk_eff) {
     if (cudaMemsetAsync(C, 0, (size_t)groups * M * N * 8, as_stream(stream)) != cudaSuccess)
       return check_launch("gemm C memset");
     if (nkb == 0) return MPC3_OK;
   }
-  MnArgs mn = {a_mn ? 1 : 0, b_mn ? 1 : 0, (int)a_half, (int)b_half, (int)(kc_half / BK)};
+  if (eff < sk_eff) {  // the split-K grid would leave SMs idle in its last wave: stream-K
+    static bool sk_attr = false;
+    if (!sk_attr) {
+      if (cudaFuncSetAttribute(gemm_sk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess)
+        return check_launch("gemm_sk attr");
+      sk_attr = true;
+    }
+    const int mt = (int)((M + BM - 1) / BM), nt = (int)((N + BN - 1) / BN);
+    const int64_t total = tiles * nkb;
+    int64_t c = total / 2 < sms ? total / 2 : sms;
+    if (c < 1) c = 1;
+    launch_pdl(gemm_sk_kernel, dim3((unsigned)c), dim3(GEMM_THREADS), SMEM_BYTES, as_stream(stream), ta, tb, C, M, N,
+               kp, c_layout ? M : N, M * N, mt, nt, total, c_layout, mn);
+    return check_launch("ring_gemm_t streamk");
+  }
   dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)(groups * splits));
   launch_pdl(gemm_tc_kernel, grid, dim3(GEMM_THREADS), SMEM_BYTES, as_stream(stream), ta, tb, C, M, N, kp,
              c_layout ? M : N, M * N, (int)splits, kbs, c_layout, mn);
