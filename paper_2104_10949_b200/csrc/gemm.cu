@@ -138,28 +138,25 @@ __global__ void __launch_bounds__(PT_THREADS) pack_tile_kernel(const uint64_t* _
   constexpr int STEP = PT_THREADS / (R_FAST ? PT_R : PT_K);
   const int var0 = t / (R_FAST ? PT_R : PT_K);
   const uint32_t H = (uint32_t)a.H, W = (uint32_t)a.W;
-  uint64_t vs[PER], vn[PER];
+  uint64_t vs[PER], vn[PER > 0 && ROLE == 0 ? PER : 1];
+  // only the components a half needs are loaded: role 1 reads x_i (first
+  // half) or x_{i+1} (second), role 0 reads x_{i+1} for the first half only
 #pragma unroll
   for (int it = 0; it < PER; ++it) {
     const int4 vp = R_FAST ? cpart[var0 + it * STEP] : rpart[var0 + it * STEP];
+    const int half = R_FAST ? vp.w : fp.w;
     const int32_t yy = fp.y + vp.y, xx = fp.z + vp.z;
     const bool ok = (uint32_t)yy < H && (uint32_t)xx < W;
     const uint32_t off = ok ? (uint32_t)(fp.x + vp.x + yy * a.sH + xx * a.sW) : 0u;
-    vs[it] = ok ? __ldg(sg + off) : 0ull;
-    if (ROLE != 2) vn[it] = ok ? __ldg(sn + off) : 0ull;
+    vs[it] = ok ? __ldg((ROLE == 1 && half ? sn : sg) + off) : 0ull;
+    if (ROLE == 0) vn[it] = ok && !half ? __ldg(sn + off) : 0ull;
   }
 #pragma unroll
   for (int it = 0; it < PER; ++it) {
     const int var = var0 + it * STEP;
     const int i = R_FAST ? fixed : var, j = R_FAST ? var : fixed;
-    const int half = R_FAST ? cpart[j].w : fp.w;
-    uint64_t v;
-    if (ROLE == 2)
-      v = vs[it];
-    else if (ROLE == 0)
-      v = half == 0 ? vs[it] + vn[it] : vs[it];  // [x_i + x_{i+1} | x_i]  (protocols.py:110-115)
-    else
-      v = half == 0 ? vs[it] : vn[it];  // [y_i | y_{i+1}]
+    // [x_i + x_{i+1} | x_i] (role 0) / [y_i | y_{i+1}] (role 1)  (protocols.py:110-115)
+    const uint64_t v = ROLE == 0 ? vs[it] + vn[it] : vs[it];
     tile[i * PT_K + pt_swz(i, j)] = v;
   }
   __syncthreads();
@@ -1003,6 +1000,8 @@ int mpc3_ring_pack_halves(const uint64_t* src, int64_t src_plane, const mpc3_ope
       a.sH = (int32_t)o.sH;
       a.sW = (int32_t)o.sW;
       r_fast = o.mode == MPC3_GATHER_IM2COL && o.sw <= 2;  // strided windows: walk the kernel row (contiguous input x)
+      static const char* force = getenv("MPC3_PACK_RFAST");
+      if (force) r_fast = force[0] == '1';
     }
     dim3 grid((unsigned)((kp + PT_K - 1) / PT_K), (unsigned)row_tiles, (unsigned)groups);
     void (*k)(const uint64_t*, int64_t, Operand, PackTileArgs, uint8_t*) =

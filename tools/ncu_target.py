@@ -38,6 +38,15 @@ def main(kind, n, reps=3):
         op.mode, op.rows, op.k, op.s_r, op.t2 = 0, n, n, n, 1
         for _ in range(reps):
             _capi.call("mpc3_ring_pack", p(x), n * n, C.byref(op), 0, p(out), kp, st())
+    elif kind == "pack_conv1":  # AlexNet conv1 im2col pack: x (n,3,32,32), 11x11 stride 4 pad 9, role 1
+        nb = n
+        x = torch.randint(-(1 << 62), 1 << 62, (3 * nb * 3 * 32 * 32,), dtype=torch.int64, device="cuda")
+        op = _capi.conv_operand(_capi.GATHER_IM2COL, nb * 100, 363, nb, 3, 32, 32, (3 * 1024, 1024, 32, 1), 11, 11,
+                                4, 4, 9, 9, 10, 10)
+        kh, kp = 368, 736
+        out = torch.empty(3 * 8 * nb * 100 * kp, dtype=torch.uint8, device="cuda")
+        for _ in range(reps):
+            _capi.call("mpc3_ring_pack_halves", p(x), nb * 3 * 1024, C.byref(op), 1, p(out), kp, kh, st())
     elif kind == "wgrad":  # M = 256 (O), N = 2304 (C*3*3), contraction R = n rows, MN-read packs
         M, N, R = 256, 2304, n
         kc = (R + 31) // 32 * 32
