@@ -52,7 +52,7 @@ __global__ void pack_kernel(const uint64_t* __restrict__ src, int64_t plane, Ope
 // loads coalesce; phase 2 reads 8 consecutive packed values of one row back
 // from shared memory, byte-transposes them (PRMT) and writes one 8-byte word
 // per limb plane, consecutive threads covering consecutive columns.
-constexpr int PT_R = 64, PT_K = 64, PT_THREADS = 512;
+constexpr int PT_R = 64, PT_K = 64, PT_THREADS = 256;
 
 struct PackTileArgs {
   int64_t rows, K, kp, lim;  // lim: packed columns with data (K or kh + K)
