@@ -40,7 +40,16 @@ constexpr int kProtoThreads = kSignThreads, kProtoSmem = kAesSmem4Bytes, kProtoC
 #define MPC3_PROTO_SMEM() MPC3_AES_SMEM()
 #define MPC3_PROTO_INIT(sm, rk, nk) aes_smem_init(sm, rk, nk)
 using ProtoTables = SmemTables;
-constexpr int kProtoThreads = kThreads, kProtoSmem = kAesSmemBytes, kProtoCtasPerSm = 8;
+#ifndef MPC3_PROTO_THREADS
+#define MPC3_PROTO_THREADS 256
+#endif
+#ifndef MPC3_PROTO_CTAS
+#define MPC3_PROTO_CTAS 8
+#endif
+#ifndef MPC3_PROTO_MINB
+#define MPC3_PROTO_MINB 1
+#endif
+constexpr int kProtoThreads = MPC3_PROTO_THREADS, kProtoSmem = kAesSmemBytes, kProtoCtasPerSm = MPC3_PROTO_CTAS;
 #endif
 bool pdl_enabled() {
   static const bool on = [] {
@@ -142,7 +151,7 @@ __global__ void __launch_bounds__(kSignThreads, 1) prf_words_kernel(const __grid
   GRID_LOOP(t, nblk) prf_words_item(tab, ks.rk[0], h, word_off, count, out, t);
 }
 
-__global__ void __launch_bounds__(kProtoThreads) zero_share_kernel(const __grid_constant__ KeySched ks,
+__global__ void __launch_bounds__(kProtoThreads, MPC3_PROTO_MINB) zero_share_kernel(const __grid_constant__ KeySched ks,
                                                              const uint64_t* __restrict__ ctr, StreamRef rh,
                                                              int xor_mode, uint64_t n, uint64_t* __restrict__ out) {
   MPC3_PROTO_SMEM();
@@ -200,7 +209,7 @@ __global__ void ring_rowsum_kernel(const uint64_t* __restrict__ a, uint64_t* __r
 // ---------------------------------------------------------------------------
 // protocols
 
-__global__ void __launch_bounds__(kProtoThreads) arith_kernel(int kind, const __grid_constant__ KeySched ks,
+__global__ void __launch_bounds__(kProtoThreads, MPC3_PROTO_MINB) arith_kernel(int kind, const __grid_constant__ KeySched ks,
                                                         const uint64_t* __restrict__ ctr, StreamRef ra,
                                                         StreamRef rrho, StreamRef rr, int bits, const uint64_t* __restrict__ x,
                                                         const uint64_t* __restrict__ y,
@@ -417,7 +426,7 @@ struct SgdTable {
   uint64_t pair0[MPC3_SGD_MAX_TENSORS + 1];  // first pair of tensor i in the flattened range
 };
 
-__global__ void __launch_bounds__(kProtoThreads) sgd_kernel(const __grid_constant__ KeySched ks,
+__global__ void __launch_bounds__(kProtoThreads, MPC3_PROTO_MINB) sgd_kernel(const __grid_constant__ KeySched ks,
                                                       const uint64_t* __restrict__ ctr, SgdTable tb, int bits,
                                                       uint64_t c) {
   MPC3_PROTO_SMEM();
@@ -444,7 +453,7 @@ __global__ void __launch_bounds__(kProtoThreads) sgd_kernel(const __grid_constan
   }
 }
 
-__global__ void __launch_bounds__(kProtoThreads) inject_kernel(const __grid_constant__ KeySched ks,
+__global__ void __launch_bounds__(kProtoThreads, MPC3_PROTO_MINB) inject_kernel(const __grid_constant__ KeySched ks,
                                                          const uint64_t* __restrict__ ctr, StreamRef r0,
                                                          StreamRef r1, const uint64_t* __restrict__ bits,
                                                          uint64_t* __restrict__ out, uint64_t n) {
@@ -454,7 +463,7 @@ __global__ void __launch_bounds__(kProtoThreads) inject_kernel(const __grid_cons
   GRID_LOOP(b, (n + 1) >> 1) inject_item(tab, &ks.rk[0][0], a0, a1, bits, out, n, b);
 }
 
-__global__ void __launch_bounds__(kProtoThreads) reshare_trunc_kernel(const __grid_constant__ KeySched ks,
+__global__ void __launch_bounds__(kProtoThreads, MPC3_PROTO_MINB) reshare_trunc_kernel(const __grid_constant__ KeySched ks,
                                                                 const uint64_t* __restrict__ ctr, StreamRef ra,
                                                                 StreamRef rrho, StreamRef rr, int bits,
                                                                 const uint64_t* __restrict__ z, View4 v,
@@ -470,7 +479,7 @@ __global__ void __launch_bounds__(kProtoThreads) reshare_trunc_kernel(const __gr
     GRID_LOOP(b, (n + 1) >> 1) reshare_trunc_item(tab, &ks.rk[0][0], ha, hrho, hr, bits, z, v, out, n, b, pb0);
 }
 
-__global__ void __launch_bounds__(kProtoThreads) pool_kernel(const __grid_constant__ KeySched ks,
+__global__ void __launch_bounds__(kProtoThreads, MPC3_PROTO_MINB) pool_kernel(const __grid_constant__ KeySched ks,
                                                        const uint64_t* __restrict__ ctr, int backward,
                                                        StreamRef rrho, StreamRef rr, int bits, uint64_t mulc,
                                                        const uint64_t* __restrict__ x,
@@ -486,7 +495,7 @@ __global__ void __launch_bounds__(kProtoThreads) pool_kernel(const __grid_consta
     GRID_LOOP(b, (n + 1) >> 1) pool_item(tab, &ks.rk[0][0], backward != 0, hrho, hr, bits, mulc, x, out, p, b, pb0);
 }
 
-__global__ void __launch_bounds__(kProtoThreads) col2im_kernel(const __grid_constant__ KeySched ks,
+__global__ void __launch_bounds__(kProtoThreads, MPC3_PROTO_MINB) col2im_kernel(const __grid_constant__ KeySched ks,
                                                          const uint64_t* __restrict__ ctr, StreamRef ra,
                                                          StreamRef rrho, StreamRef rr, int bits,
                                                          const uint64_t* __restrict__ z, Col2Im g,

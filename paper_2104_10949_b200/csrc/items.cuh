@@ -190,10 +190,17 @@ HD void reshare_trunc_item(const T& tab, const uint32_t* rk3, StreamHead ha, Str
   }
   if (!ok[0] && !ok[1]) return;
   KeyWords f0, f1;
-  key_words_pair(tab, rk3, ha, pb, f0, f1);
   Word2 rho = {0, 0}, r = {0, 0};
   if (bits) {
-    trunc_words(tab, rk3, hrho, hr, pb, rho, r);
+    Word2 w[3];
+    reshare_trunc_words(tab, rk3, ha, hrho, hr, pb, w, rho, r);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      f0.k[i] = w[i].w0;
+      f1.k[i] = w[i].w1;
+    }
+  } else {
+    key_words_pair(tab, rk3, ha, pb, f0, f1);
   }
   for (int e = 0; e < 2; ++e) {
     if (!ok[e]) continue;
@@ -258,9 +265,13 @@ HD void col2im_item(const T& tab, const uint32_t* rk3, StreamHead ha, StreamHead
   }
   if (ooff[0] < 0 && ooff[1] < 0) return;
   KeyWords f0, f1;
-  key_words_pair(tab, rk3, ha, pb, f0, f1);
-  Word2 rho, r;
-  trunc_words(tab, rk3, hrho, hr, pb, rho, r);
+  Word2 rho, r, w[3];
+  reshare_trunc_words(tab, rk3, ha, hrho, hr, pb, w, rho, r);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    f0.k[i] = w[i].w0;
+    f1.k[i] = w[i].w1;
+  }
   for (int e = 0; e < 2; ++e) {
     if (ooff[e] < 0) continue;
     Trio t = trio_reshare(s[e], e ? f1 : f0);

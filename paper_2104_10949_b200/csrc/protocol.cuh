@@ -186,6 +186,51 @@ HD void trunc_words(const SmemTables4& tab, const uint32_t* rk3, StreamHead hrho
 }
 #endif
 
+// The zero-share words of a pair (3 keys) and its truncation words (rho, r)
+// together: on the device the five AES blocks run interleaved in one call
+// (five independent T-table chains per thread instead of three then two).
+template <class T>
+HD void reshare_trunc_words(const T& tab, const uint32_t* rk3, StreamHead ha, StreamHead hrho, StreamHead hr,
+                            uint64_t blk, Word2 w[3], Word2& rho, Word2& r) {
+  prf_block3(tab, rk3, ha, blk, w);
+  trunc_words(tab, rk3, hrho, hr, blk, rho, r);
+}
+#if defined(__CUDACC__)
+template <class TT>
+HD void reshare_trunc_words_dev(const TT& tab, const uint32_t* rk3, StreamHead ha, StreamHead hrho, StreamHead hr,
+                                uint64_t blk, Word2 w[3], Word2& rho, Word2& r) {
+#if defined(__CUDA_ARCH__)
+  const uint32_t hi = (uint32_t)(blk >> 32), lo = (uint32_t)blk;
+  uint32_t s[5][4] = {{ha.s0, ha.s1, hi, lo},
+                      {ha.s0, ha.s1, hi, lo},
+                      {ha.s0, ha.s1, hi, lo},
+                      {hrho.s0, hrho.s1, hi, lo},
+                      {hr.s0, hr.s1, hi, lo}};
+  const uint32_t* rks[5] = {rk3, rk3 + 44, rk3 + 2 * 44, rk3 + 2 * 44, rk3 + 1 * 44};
+  aes128_multi<5>(tab, rks, s);
+  Word2 o[5];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    o[i].w0 = (uint64_t)bswap32(s[i][0]) | ((uint64_t)bswap32(s[i][1]) << 32);
+    o[i].w1 = (uint64_t)bswap32(s[i][2]) | ((uint64_t)bswap32(s[i][3]) << 32);
+  }
+  w[0] = o[0];
+  w[1] = o[1];
+  w[2] = o[2];
+  rho = o[3];
+  r = o[4];
+#endif
+}
+HD void reshare_trunc_words(const SmemTables& tab, const uint32_t* rk3, StreamHead ha, StreamHead hrho, StreamHead hr,
+                            uint64_t blk, Word2 w[3], Word2& rho, Word2& r) {
+  reshare_trunc_words_dev(tab, rk3, ha, hrho, hr, blk, w, rho, r);
+}
+HD void reshare_trunc_words(const SmemTables4& tab, const uint32_t* rk3, StreamHead ha, StreamHead hrho,
+                            StreamHead hr, uint64_t blk, Word2 w[3], Word2& rho, Word2& r) {
+  reshare_trunc_words_dev(tab, rk3, ha, hrho, hr, blk, w, rho, r);
+}
+#endif
+
 // Key-word provider over a pair of adjacent elements (words 2b, 2b+1 of each
 // stream share one AES block per key).
 template <class T>

@@ -47,6 +47,12 @@ def main(kind, n, reps=3):
         out = torch.empty(3 * 8 * nb * 100 * kp, dtype=torch.uint8, device="cuda")
         for _ in range(reps):
             _capi.call("mpc3_ring_pack_halves", p(x), nb * 3 * 1024, C.byref(op), 1, p(out), kp, kh, st())
+    elif kind == "mul":  # RSS mul (reshare), n elements
+        rk = rk3()
+        x = torch.randint(-(1 << 62), 1 << 62, (3 * n,), dtype=torch.int64, device="cuda")
+        y = torch.empty_like(x)
+        for _ in range(reps):
+            _capi.call("mpc3_rss_mul", p(rk), None, 0, p(x), p(x), p(y), n, 0, st())
     elif kind == "wgrad":  # M = 256 (O), N = 2304 (C*3*3), contraction R = n rows, MN-read packs
         M, N, R = 256, 2304, n
         kc = (R + 31) // 32 * 32
