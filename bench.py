@@ -244,7 +244,7 @@ def run_b200(args, ws, rank, local):
     # roofline instrumentation: CUDA events around every launch of the
     # dominant kernel (the tcgen05 ring GEMM) and of the fused sign circuit,
     # on their launch stream (torch's current stream)
-    gemm_events, sign_events, gemm_bytes = [], [], []
+    gemm_events, sign_events, gemm_bytes, gemm_shapes = [], [], [], []
     instrument = {"on": False, "k": 0}
 
     def traced_call(name, *a):
@@ -257,16 +257,19 @@ def run_b200(args, ws, rank, local):
             e1.record()
             if name == "mpc3_rss_sign":
                 sign_events.append((e0, e1, int(a[9])))
-            elif name == "mpc3_ring_gemm_t":  # weight gradient: contraction over the a_rows batch positions
-                groups, M, N, rows, kc_half = int(a[11]), int(a[12]), int(a[13]), int(a[2]), int(a[14])
+            elif name == "mpc3_ring_gemm_t":  # transposed operands: the contraction is an MN operand's source rows
+                groups, M, N, kc_half = int(a[11]), int(a[12]), int(a[13]), int(a[14])
+                rows = int(a[2]) if a[1] else (int(a[7]) if a[6] else kc_half)
                 gemm_events.append((e0, e1, 72 * groups * M * N * 2 * rows))
                 gemm_bytes.append(groups * ((M + N) * 8 * 2 * kc_half + M * N * 8))
+                gemm_shapes.append((name, groups, M, N, 2 * rows))
             else:  # groups x M x N x 2K ring MACs, 72 int8 ops each (36 limb-pair MACs)
                 groups, M, N = int(a[3]), int(a[4]), int(a[5])
                 sign_k = instrument["k"] if instrument["k"] else int(a[6]) // 2
                 kp = int(a[6])
                 gemm_events.append((e0, e1, 72 * groups * M * N * 2 * sign_k))
                 gemm_bytes.append(groups * ((M + N) * 8 * kp + M * N * 8))  # packed A, B (8 limb planes) + C
+                gemm_shapes.append((name, groups, M, N, 2 * sign_k))
             return
         return counting_call(name, *a)
 
@@ -370,6 +373,10 @@ def run_b200(args, ws, rank, local):
                 "peak_source": ("2 x MEASURED_PEAKS.json bf16_tflops (dense int8 = 2x dense bf16 on B200; "
                                 "cuBLASLt int8 measured 2,924-3,063 TOPS, profiles/r01_microbench_quick.json)"),
                 "launches": len(gemm_events), "kernel_ms_per_step": gemm_ms,
+                "per_launch": [{"call": nm[len("mpc3_ring_"):], "groups": g_, "M": m_, "N": n_, "K2": k_,
+                                "us": round(a.elapsed_time(c) * 1e3, 2),
+                                "tops": round(w / (a.elapsed_time(c) / 1e3) / 1e12, 1)}
+                               for (a, c, w), (nm, g_, m_, n_, k_) in zip(gemm_events, gemm_shapes)],
                 "share_of_step": gemm_ms / max(total_ms / args.steps, 1e-9),
                 "algorithmic": "72 int8 ops per ring MAC x groups*M*N*2K per launch (TOPS; TFLOP/s column = int8 TOPS)",
                 "measured": "per-launch CUDA events on the launch stream in one eager step after the graph-timed region "

@@ -355,6 +355,17 @@ int mpc3_ring_gemm_t(const uint8_t* A, int a_mn, int64_t a_rows, int64_t a_kp, i
                      int b_mn, int64_t b_rows, int64_t b_kp, int64_t b_half, uint64_t* C, int groups, int64_t M,
                      int64_t N, int64_t kc_half, int c_layout, void* stream);
 
+/* The three parties' cross terms of a SMALL secure layer on the CUDA cores
+ * (64-bit IMAD, no limb packs / TMA / TMEM set-up):
+ *   z[g] = [a_g + a_{g+1} | a_g] . [b_g | b_{g+1}]^T,  g = 0, 1, 2,
+ * gathered through the operand descriptors (op_a->k == op_b->k = K).
+ * z: 3 x op_a->rows x op_b->rows, row-major (c_layout 0) or column-major (1).
+ * Exact mod 2^64 for any K.  The engine routes layers below ~2^22 ring MACs
+ * per party here (the fully-connected tails). */
+int mpc3_ring_gemm_cross_simt(const uint64_t* src_a, int64_t plane_a, const mpc3_operand* op_a,
+                              const uint64_t* src_b, int64_t plane_b, const mpc3_operand* op_b, uint64_t* z,
+                              int c_layout, void* stream);
+
 /* The secure layer's per-party cross terms as ONE implicit ring GEMM per
  * party (protocols.py:110-115):
  *   C[g] = [a_g + a_{g+1} | a_g] . [b_g | b_{g+1}]^T,  g = 0, 1, 2,

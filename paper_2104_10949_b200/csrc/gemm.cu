@@ -215,6 +215,78 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const uint64_t* __restri
   }
 }
 
+// Small secure layers (the fully-connected tails, K2 * M * N below a few
+// million ring MACs per party): the three parties' cross terms
+//   z_g = [a_g + a_{g+1} | a_g] . [b_g | b_{g+1}]^T
+// with 64-bit IMADs straight from the trio tensors (operand descriptors, any
+// view): no limb packs, no TMA / TMEM set-up, ~3 us instead of the tensor
+// path's ~10 us fixed cost (prologue, first stage, epilogue) plus two packs.
+constexpr int CS_T = 64, CS_K = 16;
+__global__ void __launch_bounds__(256) gemm_cross_simt_kernel(const uint64_t* __restrict__ sa_src, int64_t plane_a,
+                                                              Operand oa, const uint64_t* __restrict__ sb_src,
+                                                              int64_t plane_b, Operand ob, uint64_t* __restrict__ z,
+                                                              int64_t M, int64_t N, int c_col, int64_t kspl,
+                                                              int splits) {
+  __shared__ uint64_t sa[CS_K][CS_T + 1], sb[CS_K][CS_T + 1];
+  const int g = blockIdx.z / splits, gn = (g + 1) % 3, split = blockIdx.z % splits;
+  const int t = threadIdx.x, tx = t % 16, ty = t / 16;
+  const int64_t m0 = (int64_t)blockIdx.y * CS_T, n0 = (int64_t)blockIdx.x * CS_T;
+  const int64_t K = oa.k, K2 = 2 * K;
+  const int64_t kbeg = split * kspl, kend = kbeg + kspl < K2 ? kbeg + kspl : K2;
+  uint64_t acc[4][4] = {};
+  griddep_wait();
+  for (int64_t k0 = kbeg; k0 < kend; k0 += CS_K) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int e = t + 256 * i, kk = e % CS_K, rr = e / CS_K;
+      const int64_t kp = k0 + kk, h = kp >= K, k = kp - h * K;
+      uint64_t va = 0, vb = 0;
+      if (kp < kend) {
+        const int64_t m = m0 + rr, n = n0 + rr;
+        if (m < M) {
+          const int64_t off = gather_offset(oa, m, k);
+          if (off >= 0) va = h ? sa_src[g * plane_a + off] : sa_src[g * plane_a + off] + sa_src[gn * plane_a + off];
+        }
+        if (n < N) {
+          const int64_t off = gather_offset(ob, n, k);
+          if (off >= 0) vb = sb_src[(h ? gn : g) * plane_b + off];
+        }
+      }
+      sa[kk][rr] = va;
+      sb[kk][rr] = vb;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < CS_K; ++kk) {
+      uint64_t a[4], b[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) a[r] = sa[kk][ty + 16 * r];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) b[c] = sb[kk][tx + 16 * c];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] += a[r] * b[c];
+    }
+    __syncthreads();
+  }
+  griddep_launch();
+  uint64_t* zg = z + (int64_t)g * M * N;
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int64_t m = m0 + ty + 16 * r, n = n0 + tx + 16 * c;
+      if (m < M && n < N) {
+        uint64_t* dst = zg + (c_col ? n * M + m : m * N + n);
+        if (splits > 1)
+          atomicAdd(reinterpret_cast<unsigned long long*>(dst), (unsigned long long)acc[r][c]);
+        else
+          *dst = acc[r][c];
+      }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // tcgen05 kernel
 
@@ -1208,6 +1280,34 @@ int mpc3_ring_gemm_cross(const uint64_t* src_a, int64_t plane_a, const mpc3_oper
   gemm_ig_kernel<<<grid, IG_THREADS, SMEM_BYTES, as_stream(stream)>>>(src_a, plane_a, oa, src_b, plane_b, ob, C, M,
                                                                       N, ldc, c_group, splits, kbs);
   return check_launch("ring_gemm_cross");
+}
+
+int mpc3_ring_gemm_cross_simt(const uint64_t* src_a, int64_t plane_a, const mpc3_operand* op_a,
+                              const uint64_t* src_b, int64_t plane_b, const mpc3_operand* op_b, uint64_t* z,
+                              int c_layout, void* stream) {
+  if (!op_a || !op_b) return MPC3_ERR_CONFIG;
+  if (c_layout != 0 && c_layout != 1) return MPC3_ERR_CONFIG;
+  if (op_a->k != op_b->k || op_a->rows < 0 || op_b->rows < 0 || op_a->k < 0) return MPC3_ERR_SHAPE;
+  if (op_a->mode < 0 || op_a->mode > 2 || op_b->mode < 0 || op_b->mode > 2) return MPC3_ERR_CONFIG;
+  const int64_t M = op_a->rows, N = op_b->rows;
+  if (M == 0 || N == 0) return MPC3_OK;
+  if ((M + CS_T - 1) / CS_T > 65535) return MPC3_ERR_SHAPE;
+  Operand oa = to_operand(op_a), ob = to_operand(op_b);
+  // split the 2K contraction until ~2 CTAs per SM (>= 64 k per split; the
+  // splits add atomically into the zeroed z)
+  const int64_t tiles = ((N + CS_T - 1) / CS_T) * ((M + CS_T - 1) / CS_T) * 3, K2 = 2 * op_a->k;
+  int64_t splits = (2 * 148 + tiles - 1) / tiles;
+  if (splits > (K2 + 63) / 64) splits = (K2 + 63) / 64;
+  if (splits < 1) splits = 1;
+  const int64_t kspl = ((K2 + splits - 1) / splits + CS_K - 1) / CS_K * CS_K;
+  splits = (K2 + kspl - 1) / kspl;
+  if (splits < 1) splits = 1;
+  if (splits > 1 && cudaMemsetAsync(z, 0, (size_t)3 * M * N * 8, as_stream(stream)) != cudaSuccess)
+    return check_launch("cross_simt memset");
+  dim3 grid((unsigned)((N + CS_T - 1) / CS_T), (unsigned)((M + CS_T - 1) / CS_T), (unsigned)(3 * splits));
+  launch_pdl(gemm_cross_simt_kernel, grid, dim3(256), 0, as_stream(stream), src_a, plane_a, oa, src_b, plane_b, ob,
+             z, M, N, c_layout, kspl > 0 ? kspl : 1, (int)splits);
+  return check_launch("ring_gemm_cross_simt");
 }
 
 int mpc3_ring_gemm_simt(const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t M, int64_t N, int64_t K,

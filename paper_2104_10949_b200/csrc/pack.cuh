@@ -15,6 +15,8 @@ struct Operand {
 
 // Element offset of v(r, k) in one component plane, or -1 for a structural zero.
 HD int64_t gather_offset(const Operand& o, int64_t r, int64_t k) {
+  if (o.mode == MPC3_GATHER_DENSE && o.K1 == 1 && o.K2 >= o.k)  // plain 2-d view: no digit split
+    return o.off + r * o.s_r + k * o.t2;
   if (o.mode == MPC3_GATHER_DENSE) {
     int64_t k2 = k % o.K2;
     int64_t q = k / o.K2;

@@ -51,6 +51,12 @@ SMS = 148
 # MPC3_REUSE_PACKS=0: weight gradients pack their own operands instead of
 # reading the forward / input-gradient packs in place (mpc3_ring_gemm_t)
 REUSE_PACKS = os.environ.get("MPC3_REUSE_PACKS", "1") == "1"
+# secure layers with at most this many ring MACs (3 parties x M x N x 2K) run
+# on the CUDA cores (mpc3_ring_gemm_cross_simt).  Off by default: measured
+# slower than pack + pack + tcgen05 even for the AlexNet FC layers (128x256x256:
+# 38 vs 22 us; 64-bit IMAD chains at ~7 thread-instructions per ring MAC), and
+# the AlexNet step went 2.71 -> 2.82 ms with the FC layers routed there
+SIMT_MACS = int(os.environ.get("MPC3_SIMT_MACS", "0"))
 
 
 @dataclass
@@ -639,6 +645,11 @@ class TrioSession:
         keep / a_packed / a_role: pack A in the reusable Packed layout with
         the given role (the operand roles are symmetric), append it to `keep`,
         or take it ready-packed (training: the weight gradient reuses it)."""
+        if a_packed is None and 3 * M * N * 2 * Kd <= SIMT_MACS:
+            z = torch.empty(3 * M * N, dtype=torch.int64, device=_dev())
+            K.call("mpc3_ring_gemm_cross_simt", a_src.data_ptr(), a_src.stride(0), C.byref(a_op), b_src.data_ptr(),
+                   b_src.stride(0), C.byref(b_op), z.data_ptr(), 1 if c_col else 0, _stream())
+            return z  # (nothing packed: `keep` stays empty and the backward pass packs nothing either)
         if keep is not None or a_packed is not None:
             if IMPLICIT_GEMM:
                 raise ConfigError("packed-operand reuse needs the explicit pack path")

@@ -261,6 +261,21 @@ def test_ring_gemm_transposed_operands(Rn, O, Kc, a_mn, b_mn, layout):
         assert np.array_equal(got[g], want), g
 
 
+@pytest.mark.parametrize("M,K,Nn,layout", [(1, 1, 1, 0), (128, 256, 10, 0), (77, 300, 130, 1), (200, 5000, 64, 0)])
+def test_ring_gemm_cross_simt(M, K, Nn, layout):
+    """Small-layer cross terms on the CUDA cores:
+    z[g] = (x_g + x_{g+1}) y_g + x_g y_{g+1}, y read through a transposed view."""
+    rng = np.random.default_rng(M + K + Nn)
+    xt, yt = rnd(rng, (3, M, K)), rnd(rng, (3, K, Nn))
+    z = torch.full((3 * M * Nn,), -1, dtype=torch.int64, device="cuda")
+    _capi.call("mpc3_ring_gemm_cross_simt", p(dev(xt)), M * K, C.byref(_capi.dense_operand(M, K, s_r=K, t2=1)),
+               p(dev(yt)), K * Nn, C.byref(_capi.dense_operand(Nn, K, s_r=1, t2=Nn)), p(z), layout, stream())
+    got = host(z).reshape(3, Nn, M).transpose(0, 2, 1) if layout else host(z).reshape(3, M, Nn)
+    for g in range(3):
+        h = (g + 1) % 3
+        assert np.array_equal(got[g], R.wrap_matmul(xt[g] + xt[h], yt[g]) + R.wrap_matmul(xt[g], yt[h])), g
+
+
 def test_ring_matmul_u64_convenience():
     rng = np.random.default_rng(3)
     M, K, Nn = 77, 20000, 33
