@@ -236,6 +236,7 @@ class TrioSession:
         self._side = None  # side stream for independent launches (weight gradients)
         self._pack = None  # stream for the B-operand pack of a GEMM
         self._wcache = None  # packed weight operands under frozen_weights()
+        self._prepacked = {}  # weight packs made ahead of their layer (prepack): key -> (Packed, event)
         self._replicated = 0
 
     # -- data parallelism --
@@ -564,22 +565,54 @@ class TrioSession:
                _stream())
         return Packed(buf, rows, k, kh, kp, role)
 
+    @staticmethod
+    def _pack_key(src: torch.Tensor, op, role: int):
+        return (src.data_ptr(), src._version, tuple(src.shape), tuple(src.stride()), role,
+                tuple(getattr(op, f) for f, _ in op._fields_))
+
+    def prepack(self, items) -> None:
+        """Pack weight operands (role 0) ahead of the layers that use them, on
+        the pack stream: items = [(src, op, rows, k)].  _cross_gemm_kept takes
+        a matching prepacked B instead of packing it on the critical path."""
+        main = torch.cuda.current_stream()
+        ps = self.pack_stream()
+        ev = torch.cuda.Event()
+        ev.record(main)
+        ps.wait_event(ev)
+        with torch.cuda.stream(ps):
+            packs = [(self._pack_key(src, op, 0), self.pack(src, op, rows, k, 0)) for src, op, rows, k in items]
+        done = torch.cuda.Event()
+        done.record(ps)
+        for key, pk in packs:
+            self._prepacked[key] = (pk, done)
+
+    def clear_prepacked(self) -> None:
+        self._prepacked.clear()
+
     def _cross_gemm_kept(self, a_src, a_op, b_src, b_op, M, N, Kd, c_col, a_role, keep, a_packed):
         """_cross_gemm in the Packed layout: A packed with role a_role (or
         given), B with the other role; both packs appended to `keep` (the
         backward pass reads them transposed)."""
         kh, kp = Packed.geometry(Kd)
         st = _stream()
-        B = torch.empty(3 * 8 * N * kp, dtype=torch.uint8, device=_dev())
         main = torch.cuda.current_stream()
-        ps = self.pack_stream() if OVERLAP_PACK else None
-        if ps is not None and ps != main:  # B on the pack stream, A here
+        pre = self._prepacked.pop(self._pack_key(b_src, b_op, 1 - a_role), None) if self._prepacked else None
+        if pre is not None:
+            pre, done = pre
+            if (pre.rows, pre.k, pre.kh, pre.kp) != (N, Kd, kh, kp):
+                raise ShapeError("prepacked operand does not match the GEMM")
+            main.wait_event(done)
+            B = pre.buf
+        else:
+            B = torch.empty(3 * 8 * N * kp, dtype=torch.uint8, device=_dev())
+        ps = self.pack_stream() if OVERLAP_PACK and pre is None else None
+        if pre is None and ps is not None and ps != main:  # B on the pack stream, A here
             ev = torch.cuda.Event()
             ev.record(main)
             ps.wait_event(ev)
             K.call("mpc3_ring_pack_halves", b_src.data_ptr(), b_src.stride(0), C.byref(b_op), 1 - a_role,
                    B.data_ptr(), kp, kh, ps.cuda_stream)
-        else:
+        elif pre is None:
             K.call("mpc3_ring_pack_halves", b_src.data_ptr(), b_src.stride(0), C.byref(b_op), 1 - a_role,
                    B.data_ptr(), kp, kh, st)
         if a_packed is not None:
@@ -739,7 +772,7 @@ class TrioSession:
             raise RangeError(f"truncation by {bits} bits outside [1, 61]")
         xs, ys = x.data.stride(), y.data.stride()
         a_op = K.dense_operand(m, k, s_r=xs[1], t2=xs[2])
-        b_op = K.dense_operand(n, k, s_r=ys[2], t2=ys[1])
+        b_op = self.matmul_weight_operand(y)[0]
         z = self._cross_gemm(x.data, a_op, y.data, b_op, m, n, k, a_role=x_role, keep=keep, a_packed=x_packed)
         out = empty((m, n), x.fp)
         if wgrad:
@@ -770,6 +803,19 @@ class TrioSession:
         out = empty((b, wp.k), g.fp)
         return self._finish(z, K.make_view((1, 1, b, wp.k)), out, bits, "mul.reshare")
 
+    @staticmethod
+    def conv_weight_operand(k: RssTensor):
+        """(operand, rows, K) of a conv kernel (O, C, kh, kw) as the GEMM's B."""
+        ks = k.data.stride()
+        o, c, kh, kw = k.shape
+        return K.dense_operand(o, c * kh * kw, s_r=ks[1], t0=ks[2], t1=ks[3], t2=ks[4], K1=kh, K2=kw), o, c * kh * kw
+
+    @staticmethod
+    def matmul_weight_operand(y: RssTensor):
+        """(operand, rows, K) of the right matmul operand y (k, n) as the GEMM's B."""
+        ys = y.data.stride()
+        return K.dense_operand(y.shape[1], y.shape[0], s_r=ys[2], t2=ys[1]), y.shape[1], y.shape[0]
+
     def conv2d(self, x: RssTensor, k: RssTensor, stride=(1, 1), padding=(0, 0), bits=None,
                bias: RssTensor | None = None, keep: list | None = None) -> RssTensor:
         """conv2d_shares (protocols.py:120-136), NCHW cross-correlation;
@@ -789,7 +835,7 @@ class TrioSession:
         xs, ks = x.data.stride(), k.data.stride()
         a_op = K.conv_operand(K.GATHER_IM2COL, nb * oh * ow, c * kh * kw, nb, c, h, w, xs[1:], kh, kw, sh, sw, ph, pw,
                               oh, ow)
-        b_op = K.dense_operand(o, c * kh * kw, s_r=ks[1], t0=ks[2], t1=ks[3], t2=ks[4], K1=kh, K2=kw)
+        b_op = self.conv_weight_operand(k)[0]
         col = self.c_col_ok
         M = nb * oh * ow
         # keep: x's im2col pack (role 1) is left for the weight gradient

@@ -229,10 +229,34 @@ class TrioNet:
     def __init__(self, sess: TrioSession):
         self.s = sess
         self.t = sess.fp.t
+        self._ahead = []  # weight operands still to be prepacked (training forward)
 
     def forward(self, model: ModelGraph, params: list, x: RssTensor, record: bool):
-        """nn.py:405-432 (plus the inference-only bias / residual / padded pool)."""
-        return self._run(model.layers, iter(params), x, record)
+        """nn.py:405-432 (plus the inference-only bias / residual / padded pool).
+        Recording (training): each layer's weight is packed on the pack
+        stream while the layer before it runs, off the critical path."""
+        S = self.s
+        if record and E.REUSE_PACKS and not E.IMPLICIT_GEMM and E.OVERLAP_PACK and E.SIMT_MACS == 0 \
+                and all(sp.kind != RESIDUAL for sp in model.layers):
+            items, it = [], iter(params)
+            for spec in model.layers:
+                if spec.kind == CONV2D:
+                    k = next(it)
+                    items.append((k.data,) + S.conv_weight_operand(k))
+                elif spec.kind == FULLY_CONNECTED:
+                    y = next(it).apply(lambda d: d.transpose(1, 2))  # the view _run hands to matmul
+                    items.append((y.data,) + S.matmul_weight_operand(y))
+                else:
+                    continue
+                if spec.bias:
+                    next(it)
+            S.prepack(items[:1])
+            self._ahead = items[1:]  # packed one layer ahead (_run), beside the layer before
+        try:
+            return self._run(model.layers, iter(params), x, record)
+        finally:
+            S.clear_prepacked()
+            self._ahead = []
 
     def _bias(self, h: RssTensor, b: RssTensor) -> RssTensor:
         """Shared bias, local add after the truncation (scale t)."""
@@ -250,12 +274,16 @@ class TrioNet:
                 x = h
                 h = S.conv2d(h, k, spec.stride, spec.padding, bias=next(it) if spec.bias else None, keep=keep)
                 acts.append(((x, k) + tuple(keep or ())) if record else None)
+                if self._ahead:
+                    S.prepack([self._ahead.pop(0)])
             elif spec.kind == FULLY_CONNECTED:
                 w = next(it)
                 x = h
                 h = S.matmul(h, w.apply(lambda d: d.transpose(1, 2)), bias=next(it) if spec.bias else None,
                              keep=keep, x_role=1 if keep is not None else 0)
                 acts.append(((x, w) + tuple(keep or ())) if record else None)
+                if self._ahead:
+                    S.prepack([self._ahead.pop(0)])
             elif spec.kind == AVGPOOL:
                 acts.append((h.shape,) if record else None)
                 h = S.avgpool(h, spec.window, spec.stride, spec.padding)
@@ -322,10 +350,9 @@ class TrioNet:
             if spec.kind == FULLY_CONNECTED:
                 x, w = cached[:2]
                 xp, wp = cached[2:4] if len(cached) > 3 else (None, None)
-                gp = S.pack_grad(g) if xp is not None else None
                 pi -= 1
-                if xp is not None:
-                    grads[pi] = wgrad(lambda a, b: S.fc_wgrad_packed(a, b, t + batch_bits), gp, xp)
+                if xp is not None:  # g's role-0 pack is made on the side stream, beside the input gradient
+                    grads[pi] = wgrad(lambda gg, b: S.fc_wgrad_packed(S.pack_grad(gg), b, t + batch_bits), g, xp)
                 else:
                     grads[pi] = wgrad(lambda gg, xx: S.matmul(gg.apply(lambda d: d.transpose(1, 2)), xx,
                                                               bits=t + batch_bits, wgrad=True), g, x)
@@ -335,11 +362,10 @@ class TrioNet:
             elif spec.kind == CONV2D:
                 x, k = cached[:2]
                 xp, wp = cached[2:4] if len(cached) > 3 else (None, None)
-                gp = S.pack_grad(g) if xp is not None else None
                 pi -= 1
-                grads[pi] = wgrad(lambda xx, gg, a, b: S.conv2d_wgrad(
+                grads[pi] = wgrad(lambda xx, gg, b: S.conv2d_wgrad(
                     xx, gg, spec.kernel, spec.stride, spec.padding, bits=t + batch_bits,
-                    packs=None if b is None else (a, b)), x, g, gp, xp)
+                    packs=None if b is None else (S.pack_grad(gg), b)), x, g, xp)
                 if li == plist[0]:
                     break
                 g = S.conv2d_dgrad(g, k, spec.stride, spec.padding, x.shape, bits=t, w_packed=wp)

@@ -17,4 +17,5 @@ for (M, K, N) in [(128, 256, 256), (128, 256, 10), (256, 128, 256), (10, 128, 25
         _capi.call("mpc3_ring_pack", p(y), K * N, C.byref(ob), 1, p(B), kp, st())
         _capi.call("mpc3_ring_gemm_auto", p(A), p(B), p(z), 3, M, N, kp, 0, st())
     t2 = graph_us(tc, reps=10)
-    print(f"M={M} K={K} N={N}: simt {t:6.1f} us   pack+pack+tcgen05 {t2:6.1f} us", flush=True)
+    t3 = graph_us(lambda: _capi.call("mpc3_ring_gemm_cross", p(x), M * K, C.byref(oa), p(y), K * N, C.byref(ob), p(z), N, M * N, 1, st()), reps=10)
+    print(f"M={M} K={K} N={N}: simt {t:6.1f} us   pack+pack+tcgen05 {t2:6.1f} us   implicit {t3:6.1f} us", flush=True)
