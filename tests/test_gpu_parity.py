@@ -119,6 +119,24 @@ def test_alexnet_train_step_digest_bit_exact():
     assert np.allclose(res.ce_history, META["train_alexnet_ce"])
 
 
+@pytest.mark.parametrize("flags", [{"REUSE_PACKS": False}, {"OVERLAP_PACK": False}, {"nn.OVERLAP": False},
+                                   {"REUSE_PACKS": False, "nn.OVERLAP": False}])
+def test_alexnet_train_step_digest_under_schedule_variants(flags, monkeypatch):
+    """The engine's schedule choices (packs reused across the three GEMMs of a
+    layer, weight packs one layer ahead, side-stream weight gradients, pack
+    stream) change no share: the reference's digest under each variant."""
+    from paper_2104_10949_b200 import engine as E
+
+    for k, v in flags.items():
+        mod, name = (nn, k[3:]) if k.startswith("nn.") else (E, k)
+        monkeypatch.setattr(mod, name, v)
+    s = TrioSession(0)
+    cfg = M.TrainConfig(0.01, 4, 1, 5)
+    res = nn.train_trio(s, M.alexnet_cifar(), cfg, G["train_alexnet_images"], G["train_alexnet_labels"])
+    d = hashlib.sha256(b"".join(np.ascontiguousarray(x, "<u8").tobytes() for x in res.weights)).hexdigest()
+    assert d == META["train_alexnet_digest"]
+
+
 def test_bilinear_exact_device_matches_golden():
     assert np.array_equal(M.bilinear_exact(G["mm_a"], G["mm_b"], M.matmul_spec(9, 33, 7)), G["mm_out"])
     assert np.array_equal(M.bilinear_exact(G["cv_x"], G["cv_k"], M.conv2d_spec(3, (3, 3), (2, 2), (1, 1))),
