@@ -24,18 +24,27 @@ void set_last_error(const char* msg) {
 constexpr int kThreads = 256;
 constexpr int kSignThreads = 384;  // four-table AES kernels: one CTA per SM
 // The protocol kernels (everything but the sign / sign2 / chain kernels):
-// two-table AES at 3 x 256-thread CTAs per SM by default.  The four-table
-// layout (one 384-thread CTA per SM, one wave) measured slower for these
-// (reshare 514 -> 540 us, SGD 127 -> 156 us per AlexNet step): they mix AES
-// with memory traffic and need the resident warps more than the ALU slots.
+// four-table AES (128 KiB, no rotations) in one 384-thread CTA per SM on a
+// persistent grid.  Measured against the two-table layout at 3 x 256-thread
+// CTAs per SM (tools/dbg/run_variants.sh): reshare+truncate 1.2 M elements
+// 73 -> 65 us (42 -> 47 G AES blocks/s), mul 50 -> 44 us, AlexNet step
+// 2.68 -> 2.60 ms; 512 / 640 / 768 threads win only above ~4 M elements.
+// (Before the round keys moved into the kernel parameters the two-table
+// layout was ahead: the key loads competed for the same shared-memory pipe.)
 #ifndef MPC3_PROTO_TABLES4
-#define MPC3_PROTO_TABLES4 0
+#define MPC3_PROTO_TABLES4 1
 #endif
 #if MPC3_PROTO_TABLES4
 #define MPC3_PROTO_SMEM() MPC3_AES_SMEM4()
 #define MPC3_PROTO_INIT(sm, rk, nk) aes_smem_init4(sm, rk, nk)
 using ProtoTables = SmemTables4;
-constexpr int kProtoThreads = kSignThreads, kProtoSmem = kAesSmem4Bytes, kProtoCtasPerSm = 1;
+#ifndef MPC3_PROTO_THREADS
+#define MPC3_PROTO_THREADS kSignThreads
+#endif
+#ifndef MPC3_PROTO_MINB
+#define MPC3_PROTO_MINB 1
+#endif
+constexpr int kProtoThreads = MPC3_PROTO_THREADS, kProtoSmem = kAesSmem4Bytes, kProtoCtasPerSm = 1;
 #else
 #define MPC3_PROTO_SMEM() MPC3_AES_SMEM()
 #define MPC3_PROTO_INIT(sm, rk, nk) aes_smem_init(sm, rk, nk)

@@ -167,8 +167,12 @@ def main():
     ap.add_argument("--gemm-t", action="store_true", help="only the transposed-operand GEMM comparison")
     args = ap.parse_args()
     if args.gemm_t:
-        res = gemm_t_compare([(256, 3456, 128), (384, 3456, 128), (96, 363, 12800), (256, 2400, 512),
-                              (256, 256, 128), (1024, 1024, 4096), (4096, 4096, 4096)])
+        shapes = [(256, 3456, 128), (384, 3456, 128), (96, 363, 12800), (256, 2400, 512),
+                  (256, 256, 128), (1024, 1024, 4096), (4096, 4096, 4096)]
+        if os.environ.get("GEMM_T_FWD"):  # the AlexNet forward / input-gradient shapes (M, N, contraction)
+            shapes = [(12800, 96, 384), (512, 256, 2400), (128, 384, 2304), (128, 384, 3456), (128, 3456, 256),
+                      (512, 2400, 256)]
+        res = gemm_t_compare(shapes)
         with open(args.out, "w") as f:
             json.dump(res, f, indent=1)
         return
