@@ -23,43 +23,37 @@ void set_last_error(const char* msg) {
 
 constexpr int kThreads = 256;
 constexpr int kSignThreads = 384;  // four-table AES kernels: one CTA per SM
-// The protocol kernels (everything but the sign / sign2 / chain kernels):
-// four-table AES (128 KiB, no rotations) in one 384-thread CTA per SM on a
-// persistent grid.  Measured against the two-table layout at 3 x 256-thread
-// CTAs per SM (tools/dbg/run_variants.sh): reshare+truncate 1.2 M elements
-// 73 -> 65 us (42 -> 47 G AES blocks/s), mul 50 -> 44 us, AlexNet step
-// 2.68 -> 2.60 ms; 512 / 640 / 768 threads win only above ~4 M elements.
-// (Before the round keys moved into the kernel parameters the two-table
-// layout was ahead: the key loads competed for the same shared-memory pipe.)
-#ifndef MPC3_PROTO_TABLES4
-#define MPC3_PROTO_TABLES4 1
+// The protocol kernels (everything but the sign / sign2 / chain kernels) come
+// in two AES table layouts, chosen per launch by size:
+//  * four-table (128 KiB, no rotations), one 384-thread CTA per SM on a
+//    persistent grid: the throughput layout (reshare+truncate at 1.2 M
+//    elements 73 -> 65 us, 42 -> 47 G AES blocks/s; AlexNet step 2.68 ->
+//    2.60 ms when every launch used it);
+//  * two-table (64 KiB), 256-thread CTAs, up to 3 per SM: ~2 us less fixed
+//    cost per launch standalone (half the table to expand; reshare at 32 K
+//    elements 8.6 -> 6.9 us), kept for the tiny tensors only: in the AlexNet
+//    step a crossover at 65 K / 262 K pairs measured 2.68 / 2.67 ms against
+//    2.59 ms at 16 K pairs or with every launch four-table, and 2.71 ms with
+//    every launch two-table (tools/dbg/run_variants.sh).
+constexpr int kProto4Threads = kSignThreads, kProto2Threads = kThreads, kProto2CtasPerSm = 8;
+#ifndef MPC3_FOUR_MIN_PAIRS
+#define MPC3_FOUR_MIN_PAIRS 16384
 #endif
-#if MPC3_PROTO_TABLES4
-#define MPC3_PROTO_SMEM() MPC3_AES_SMEM4()
-#define MPC3_PROTO_INIT(sm, rk, nk) aes_smem_init4(sm, rk, nk)
-using ProtoTables = SmemTables4;
-#ifndef MPC3_PROTO_THREADS
-#define MPC3_PROTO_THREADS kSignThreads
-#endif
-#ifndef MPC3_PROTO_MINB
-#define MPC3_PROTO_MINB 1
-#endif
-constexpr int kProtoThreads = MPC3_PROTO_THREADS, kProtoSmem = kAesSmem4Bytes, kProtoCtasPerSm = 1;
-#else
-#define MPC3_PROTO_SMEM() MPC3_AES_SMEM()
-#define MPC3_PROTO_INIT(sm, rk, nk) aes_smem_init(sm, rk, nk)
-using ProtoTables = SmemTables;
-#ifndef MPC3_PROTO_THREADS
-#define MPC3_PROTO_THREADS 256
-#endif
-#ifndef MPC3_PROTO_CTAS
-#define MPC3_PROTO_CTAS 8
-#endif
-#ifndef MPC3_PROTO_MINB
-#define MPC3_PROTO_MINB 1
-#endif
-constexpr int kProtoThreads = MPC3_PROTO_THREADS, kProtoSmem = kAesSmemBytes, kProtoCtasPerSm = MPC3_PROTO_CTAS;
-#endif
+constexpr uint64_t kFourMinPairs = MPC3_FOUR_MIN_PAIRS;
+template <bool F>
+struct Proto;
+template <>
+struct Proto<true> {
+  using TT = SmemTables4;
+  static constexpr int threads = kProto4Threads, min_ctas = 1;
+  DEV static TT init() { return aes_smem_init4(*reinterpret_cast<AesSmem4*>(mpc3_dsm), nullptr, 0); }
+};
+template <>
+struct Proto<false> {
+  using TT = SmemTables;
+  static constexpr int threads = kProto2Threads, min_ctas = 3;  // 3 x 64 KiB tables per SM
+  DEV static TT init() { return aes_smem_init(*reinterpret_cast<AesSmem*>(mpc3_dsm), nullptr, 0); }
+};
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = getenv("MPC3_PDL");
@@ -120,11 +114,20 @@ static int load_keys(const uint32_t* rk, int nkeys, void* stream, KeySched* ks) 
   return MPC3_OK;
 }
 
-#define AES_LAUNCH(kern, grid, stream, ...)                                                \
-  do {                                                                                     \
-    if (!aes_attr((const void*)kern, kProtoSmem)) return check_launch(#kern " smem attribute"); \
-    if (launch_pdl(kern, dim3(grid), dim3(kProtoThreads), kProtoSmem, (stream), __VA_ARGS__) != cudaSuccess) \
-      return check_launch(#kern);                                                          \
+#define AES_LAUNCH(kern, pairs, stream, ...)                                                              \
+  do {                                                                                                     \
+    const uint64_t pairs_ = (pairs);                                                                       \
+    if (pairs_ >= kFourMinPairs) {                                                                         \
+      if (!aes_attr((const void*)kern<true>, kAesSmem4Bytes)) return check_launch(#kern " smem attribute"); \
+      if (launch_pdl(kern<true>, dim3(grid_for(pairs_, kProto4Threads, 1)), dim3(kProto4Threads),          \
+                     kAesSmem4Bytes, (stream), __VA_ARGS__) != cudaSuccess)                                \
+        return check_launch(#kern);                                                                        \
+    } else {                                                                                               \
+      if (!aes_attr((const void*)kern<false>, kAesSmemBytes)) return check_launch(#kern " smem attribute"); \
+      if (launch_pdl(kern<false>, dim3(grid_for(pairs_, kProto2Threads, kProto2CtasPerSm)),               \
+                     dim3(kProto2Threads), kAesSmemBytes, (stream), __VA_ARGS__) != cudaSuccess)          \
+        return check_launch(#kern);                                                                        \
+    }                                                                                                      \
   } while (0)
 
 // Stream counters may be offset by a device-resident per-purpose base
@@ -160,12 +163,12 @@ __global__ void __launch_bounds__(kSignThreads, 1) prf_words_kernel(const __grid
   GRID_LOOP(t, nblk) prf_words_item(tab, ks.rk[0], h, word_off, count, out, t);
 }
 
-__global__ void __launch_bounds__(kProtoThreads, MPC3_PROTO_MINB) zero_share_kernel(const __grid_constant__ KeySched ks,
+template <bool F>
+__global__ void __launch_bounds__(Proto<F>::threads, Proto<F>::min_ctas) zero_share_kernel(const __grid_constant__ KeySched ks,
                                                              const uint64_t* __restrict__ ctr, StreamRef rh,
                                                              int xor_mode, uint64_t n, uint64_t* __restrict__ out) {
-  MPC3_PROTO_SMEM();
   StreamHead h = resolve(rh, ctr);
-  ProtoTables tab = MPC3_PROTO_INIT(sm, nullptr, 0);
+  auto tab = Proto<F>::init();
   GRID_LOOP(b, (n + 1) >> 1) zero_share_item(tab, &ks.rk[0][0], h, xor_mode, n, out, b);
 }
 
@@ -218,13 +221,13 @@ __global__ void ring_rowsum_kernel(const uint64_t* __restrict__ a, uint64_t* __r
 // ---------------------------------------------------------------------------
 // protocols
 
-__global__ void __launch_bounds__(kProtoThreads, MPC3_PROTO_MINB) arith_kernel(int kind, const __grid_constant__ KeySched ks,
+template <bool F>
+__global__ void __launch_bounds__(Proto<F>::threads, Proto<F>::min_ctas) arith_kernel(int kind, const __grid_constant__ KeySched ks,
                                                         const uint64_t* __restrict__ ctr, StreamRef ra,
                                                         StreamRef rrho, StreamRef rr, int bits, const uint64_t* __restrict__ x,
                                                         const uint64_t* __restrict__ y,
                                                         uint64_t* __restrict__ out, uint64_t n, uint64_t pb0) {
-  MPC3_PROTO_SMEM();
-  ProtoTables tab = MPC3_PROTO_INIT(sm, nullptr, 0);
+  auto tab = Proto<F>::init();
   StreamHead ha = resolve(ra, ctr), hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
   GRID_LOOP(b, (n + 1) >> 1) arith_item(tab, &ks.rk[0][0], kind, ha, hrho, hr, bits, x, y, out, n, b, pb0);
 }
@@ -435,11 +438,11 @@ struct SgdTable {
   uint64_t pair0[MPC3_SGD_MAX_TENSORS + 1];  // first pair of tensor i in the flattened range
 };
 
-__global__ void __launch_bounds__(kProtoThreads, MPC3_PROTO_MINB) sgd_kernel(const __grid_constant__ KeySched ks,
+template <bool F>
+__global__ void __launch_bounds__(Proto<F>::threads, Proto<F>::min_ctas) sgd_kernel(const __grid_constant__ KeySched ks,
                                                       const uint64_t* __restrict__ ctr, SgdTable tb, int bits,
                                                       uint64_t c) {
-  MPC3_PROTO_SMEM();
-  ProtoTables tab = MPC3_PROTO_INIT(sm, nullptr, 0);
+  auto tab = Proto<F>::init();
   const uint64_t total = tb.pair0[tb.nt];
   GRID_LOOP(q, total) {
     int i = 0;
@@ -462,58 +465,58 @@ __global__ void __launch_bounds__(kProtoThreads, MPC3_PROTO_MINB) sgd_kernel(con
   }
 }
 
-__global__ void __launch_bounds__(kProtoThreads, MPC3_PROTO_MINB) inject_kernel(const __grid_constant__ KeySched ks,
+template <bool F>
+__global__ void __launch_bounds__(Proto<F>::threads, Proto<F>::min_ctas) inject_kernel(const __grid_constant__ KeySched ks,
                                                          const uint64_t* __restrict__ ctr, StreamRef r0,
                                                          StreamRef r1, const uint64_t* __restrict__ bits,
                                                          uint64_t* __restrict__ out, uint64_t n) {
-  MPC3_PROTO_SMEM();
-  ProtoTables tab = MPC3_PROTO_INIT(sm, nullptr, 0);
+  auto tab = Proto<F>::init();
   StreamHead a0 = resolve(r0, ctr), a1 = resolve(r1, ctr);
   GRID_LOOP(b, (n + 1) >> 1) inject_item(tab, &ks.rk[0][0], a0, a1, bits, out, n, b);
 }
 
-__global__ void __launch_bounds__(kProtoThreads, MPC3_PROTO_MINB) reshare_trunc_kernel(const __grid_constant__ KeySched ks,
+template <bool F>
+__global__ void __launch_bounds__(Proto<F>::threads, Proto<F>::min_ctas) reshare_trunc_kernel(const __grid_constant__ KeySched ks,
                                                                 const uint64_t* __restrict__ ctr, StreamRef ra,
                                                                 StreamRef rrho, StreamRef rr, int bits,
                                                                 const uint64_t* __restrict__ z, View4 v,
                                                                 uint64_t* __restrict__ out, uint64_t n,
                                                                 uint64_t pb0) {
-  MPC3_PROTO_SMEM();
-  ProtoTables tab = MPC3_PROTO_INIT(sm, nullptr, 0);
+  auto tab = Proto<F>::init();
   StreamHead ha = resolve(ra, ctr), hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
   if (n < (1ull << 32))
-    GRID_LOOP(b, (n + 1) >> 1) reshare_trunc_item<ProtoTables, uint32_t>(tab, &ks.rk[0][0], ha, hrho, hr, bits, z, v, out,
+    GRID_LOOP(b, (n + 1) >> 1) reshare_trunc_item<typename Proto<F>::TT, uint32_t>(tab, &ks.rk[0][0], ha, hrho, hr, bits, z, v, out,
                                                                          n, b, pb0);
   else
     GRID_LOOP(b, (n + 1) >> 1) reshare_trunc_item(tab, &ks.rk[0][0], ha, hrho, hr, bits, z, v, out, n, b, pb0);
 }
 
-__global__ void __launch_bounds__(kProtoThreads, MPC3_PROTO_MINB) pool_kernel(const __grid_constant__ KeySched ks,
+template <bool F>
+__global__ void __launch_bounds__(Proto<F>::threads, Proto<F>::min_ctas) pool_kernel(const __grid_constant__ KeySched ks,
                                                        const uint64_t* __restrict__ ctr, int backward,
                                                        StreamRef rrho, StreamRef rr, int bits, uint64_t mulc,
                                                        const uint64_t* __restrict__ x,
                                                        uint64_t* __restrict__ out, PoolGeom p, uint64_t n,
                                                        uint64_t pb0) {
-  MPC3_PROTO_SMEM();
-  ProtoTables tab = MPC3_PROTO_INIT(sm, nullptr, 0);
+  auto tab = Proto<F>::init();
   StreamHead hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
   if (2 * n < (1ull << 32) && (uint64_t)p.N * p.C * p.H * p.W < (1ull << 32))
-    GRID_LOOP(b, (n + 1) >> 1) pool_item<ProtoTables, uint32_t>(tab, &ks.rk[0][0], backward != 0, hrho, hr, bits, mulc, x,
+    GRID_LOOP(b, (n + 1) >> 1) pool_item<typename Proto<F>::TT, uint32_t>(tab, &ks.rk[0][0], backward != 0, hrho, hr, bits, mulc, x,
                                                                 out, p, b, pb0);
   else
     GRID_LOOP(b, (n + 1) >> 1) pool_item(tab, &ks.rk[0][0], backward != 0, hrho, hr, bits, mulc, x, out, p, b, pb0);
 }
 
-__global__ void __launch_bounds__(kProtoThreads, MPC3_PROTO_MINB) col2im_kernel(const __grid_constant__ KeySched ks,
+template <bool F>
+__global__ void __launch_bounds__(Proto<F>::threads, Proto<F>::min_ctas) col2im_kernel(const __grid_constant__ KeySched ks,
                                                          const uint64_t* __restrict__ ctr, StreamRef ra,
                                                          StreamRef rrho, StreamRef rr, int bits,
                                                          const uint64_t* __restrict__ z, Col2Im g,
                                                          uint64_t* __restrict__ out, uint64_t n, uint64_t pb0) {
-  MPC3_PROTO_SMEM();
-  ProtoTables tab = MPC3_PROTO_INIT(sm, nullptr, 0);
+  auto tab = Proto<F>::init();
   StreamHead ha = resolve(ra, ctr), hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
   if (2 * n < (1ull << 32))
-    GRID_LOOP(b, (n + 1) >> 1) col2im_item<ProtoTables, uint32_t>(tab, &ks.rk[0][0], ha, hrho, hr, bits, z, g, out, b,
+    GRID_LOOP(b, (n + 1) >> 1) col2im_item<typename Proto<F>::TT, uint32_t>(tab, &ks.rk[0][0], ha, hrho, hr, bits, z, g, out, b,
                                                                   pb0);
   else
     GRID_LOOP(b, (n + 1) >> 1) col2im_item(tab, &ks.rk[0][0], ha, hrho, hr, bits, z, g, out, b, pb0);
@@ -590,7 +593,7 @@ int mpc3_rss_zero_share(const uint32_t* rk3, const uint64_t* ctr, uint32_t purpo
   if (n == 0) return MPC3_OK;
   KeySched ks;
   if (int e = load_keys(rk3, 3, stream, &ks)) return e;
-  AES_LAUNCH(zero_share_kernel, grid_for((n + 1) / 2, kProtoThreads, kProtoCtasPerSm), as_stream(stream), 
+  AES_LAUNCH(zero_share_kernel, (n + 1) / 2, as_stream(stream), 
       ks, ctr, sref(purpose, index), xor_mode, n, out);
   return check_launch("zero_share");
 }
@@ -627,7 +630,7 @@ static int arith_launch(int kind, const uint32_t* rk3, const uint64_t* ctr, uint
   if (n == 0) return MPC3_OK;
   KeySched ks;
   if (int e = load_keys(rk3, 3, stream, &ks)) return e;
-  AES_LAUNCH(arith_kernel, grid_for((n + 1) / 2, kProtoThreads, kProtoCtasPerSm), as_stream(stream), 
+  AES_LAUNCH(arith_kernel, (n + 1) / 2, as_stream(stream), 
       kind, ks, ctr, sref(ARITH_ZERO, ja), sref(TRUNC_RHO, jrho), sref(TRUNC_R, jr), bits, x, y, out, n,
       elem_off >> 1);
   return check_launch("rss_arith");
@@ -664,7 +667,7 @@ int mpc3_rss_sgd_multi(const uint32_t* rk3, const uint64_t* ctr, const MPC3SgdTe
   if (tb.pair0[nt] == 0) return MPC3_OK;
   KeySched ks;
   if (int e = load_keys(rk3, 3, stream, &ks)) return e;
-  AES_LAUNCH(sgd_kernel, grid_for(tb.pair0[nt], kProtoThreads, kProtoCtasPerSm), as_stream(stream), ks, ctr, tb, bits, c);
+  AES_LAUNCH(sgd_kernel, tb.pair0[nt], as_stream(stream), ks, ctr, tb, bits, c);
   return check_launch("rss_sgd_multi");
 }
 
@@ -805,7 +808,7 @@ int mpc3_rss_bit_inject(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_ari
   if (n == 0) return MPC3_OK;
   KeySched ks;
   if (int e = load_keys(rk3, 3, stream, &ks)) return e;
-  AES_LAUNCH(inject_kernel, grid_for((n + 1) / 2, kProtoThreads, kProtoCtasPerSm), as_stream(stream), 
+  AES_LAUNCH(inject_kernel, (n + 1) / 2, as_stream(stream), 
       ks, ctr, sref(ARITH_ZERO, j_arith), sref(ARITH_ZERO, j_arith + 1), bits, out, n);
   return check_launch("rss_bit_inject");
 }
@@ -843,7 +846,7 @@ int mpc3_rss_reshare_truncate_bias(const uint32_t* rk3, const uint64_t* ctr, uin
   if (n == 0) return MPC3_OK;
   KeySched ks;
   if (int e = load_keys(rk3, 3, stream, &ks)) return e;
-  AES_LAUNCH(reshare_trunc_kernel, grid_for((n + 1) / 2, kProtoThreads, kProtoCtasPerSm), as_stream(stream), 
+  AES_LAUNCH(reshare_trunc_kernel, (n + 1) / 2, as_stream(stream), 
       ks, ctr, sref(ARITH_ZERO, j_arith), sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, z, v, out, n,
       elem_off >> 1);
   return check_launch("rss_reshare_truncate");
@@ -869,7 +872,7 @@ int mpc3_rss_avgpool(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_rho, u
   if (n == 0) return MPC3_OK;
   KeySched ks;
   if (int e = load_keys(rk3, 3, stream, &ks)) return e;
-  AES_LAUNCH(pool_kernel, grid_for((n + 1) / 2, kProtoThreads, kProtoCtasPerSm), as_stream(stream), 
+  AES_LAUNCH(pool_kernel, (n + 1) / 2, as_stream(stream), 
       ks, ctr, 0, sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, mulc, x, out,
       pool_geom(N, C, H, W, OH, OW, kh, kw, sh, sw, ph, pw), n, elem_off >> 1);
   return check_launch("rss_avgpool");
@@ -886,7 +889,7 @@ int mpc3_rss_avgpool_backward(const uint32_t* rk3, const uint64_t* ctr, uint64_t
   if (n == 0) return MPC3_OK;
   KeySched ks;
   if (int e = load_keys(rk3, 3, stream, &ks)) return e;
-  AES_LAUNCH(pool_kernel, grid_for((n + 1) / 2, kProtoThreads, kProtoCtasPerSm), as_stream(stream), 
+  AES_LAUNCH(pool_kernel, (n + 1) / 2, as_stream(stream), 
       ks, ctr, 1, sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, mulc, g, out,
       pool_geom(N, C, H, W, OH, OW, kh, kw, sh, sw, ph, pw), n, elem_off >> 1);
   return check_launch("rss_avgpool_backward");
@@ -919,7 +922,7 @@ int mpc3_rss_col2im_reshare_truncate_layout(const uint32_t* rk3, const uint64_t*
   if (n == 0) return MPC3_OK;
   KeySched ks;
   if (int e = load_keys(rk3, 3, stream, &ks)) return e;
-  AES_LAUNCH(col2im_kernel, grid_for((n + 1) / 2, kProtoThreads, kProtoCtasPerSm), as_stream(stream), 
+  AES_LAUNCH(col2im_kernel, (n + 1) / 2, as_stream(stream), 
       ks, ctr, sref(ARITH_ZERO, j_arith), sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, z, g, out, n,
       elem_off >> 1);
   return check_launch("rss_col2im_reshare_truncate");

@@ -5,7 +5,7 @@ import torch
 from paper_2104_10949_b200 import _capi
 from tools.microbench import graph_us, p, st, rk3
 rk = rk3()
-for n in (1228800 // 4, 1228800, 4 * 1228800):
+for n in [int(v) for v in sys.argv[1:]] or (1228800 // 4, 1228800, 4 * 1228800):
     z = torch.randint(-(1 << 62), 1 << 62, (3 * n,), dtype=torch.int64, device="cuda")
     out = torch.empty_like(z)
     view = _capi.make_view((n // 9600, 96, 10, 10), z_stride=(100, 96 * 100 * n // 9600 // 96, 10, 1))
