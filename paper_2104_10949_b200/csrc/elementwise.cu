@@ -270,21 +270,22 @@ __global__ void __launch_bounds__(kSignThreads, 1) sign_kernel(const __grid_cons
 constexpr int SW_SLOT_BYTES = 3 * (int)sizeof(Word2);
 HD int sign_slots(bool straddle) { return straddle ? 21 : 16; }
 
-template <bool MAXL>
-__global__ void __launch_bounds__(kThreads, 2) sign2_kernel(const __grid_constant__ KeySched ks,
-                                                           const uint64_t* __restrict__ ctr, SignArgs args, int mode,
-                                                           const uint64_t* __restrict__ x, uint64_t* __restrict__ out,
-                                                           uint64_t* __restrict__ mask, uint64_t n, uint64_t n_total,
-                                                           uint64_t elem_off, int P, uint64_t plane, MaxGeom mg) {
-  MPC3_AES_SMEM();
-  SignStreams& st = *reinterpret_cast<SignStreams*>(sm.extra);
+// F: four-table AES (one 384-thread CTA per SM, up to 128 pairs per chunk)
+// or two-table (two 256-thread CTAs per SM, up to 64 pairs each).
+template <bool MAXL, bool F>
+__global__ void __launch_bounds__(F ? kSignThreads : kThreads, F ? 1 : 2)
+    sign2_kernel(const __grid_constant__ KeySched ks, const uint64_t* __restrict__ ctr, SignArgs args, int mode,
+                 const uint64_t* __restrict__ x, uint64_t* __restrict__ out, uint64_t* __restrict__ mask, uint64_t n,
+                 uint64_t n_total, uint64_t elem_off, int P, uint64_t plane, MaxGeom mg) {
+  SignStreams& st = *reinterpret_cast<SignStreams*>(F ? reinterpret_cast<AesSmem4*>(mpc3_dsm)->extra
+                                                      : reinterpret_cast<AesSmem*>(mpc3_dsm)->extra);
   if (threadIdx.x == 0) {
     st.bin = resolve(sref(BIN_INPUT, args.jbin), ctr);
     for (int l = 0; l < 7; ++l) st.x[l] = resolve(sref(XOR_ZERO, args.jxor + l), ctr);
     for (int l = 0; l < 3; ++l) st.a[l] = resolve(sref(ARITH_ZERO, args.ja + l), ctr);
   }
-  SmemTables tab = aes_smem_init(sm, nullptr, 0);
-  Word2* slots = reinterpret_cast<Word2*>(mpc3_dsm + sizeof(AesSmem));
+  auto tab = Proto<F>::init();  // (its __syncthreads publishes st)
+  Word2* slots = reinterpret_cast<Word2*>(mpc3_dsm + (F ? sizeof(AesSmem4) : sizeof(AesSmem)));
   const bool straddle = (n_total & 1) != 0;
   const int L = straddle ? 3 : 2;  // slots per level 1..5
   const int nslots = sign_slots(straddle);
@@ -709,12 +710,26 @@ int mpc3_rss_chain(const uint32_t* rk3, const uint64_t* ctr, const MPC3ChainStep
 // blocks: more keystream slots), and just enough that the CTA count fills
 // whole waves of the 2 x 148 resident CTAs (a 1.3-wave grid would leave most
 // SMs idle for the second wave).
+// sign2 with the four-table layout (one 384-thread CTA per SM, 128-pair
+// chunks) measured the same as two-table in the AlexNet step (2.597 vs 2.593
+// ms): the two-phase kernel is latency-bound, not lookup-bound
+#ifndef MPC3_SIGN2_FOUR
+#define MPC3_SIGN2_FOUR 0
+#endif
+constexpr bool kSign2Four = MPC3_SIGN2_FOUR;
 static int sign2_chunk(uint64_t pairs, bool straddle) {
-  const uint64_t pmax = straddle ? 32 : 64, slots = 2 * 148;
+  const uint64_t pmax = (straddle ? 32 : 64) * (kSign2Four ? 2 : 1), slots = (kSign2Four ? 1 : 2) * 148;
   const uint64_t waves = (pairs + slots * pmax - 1) / (slots * pmax);
   uint64_t P = (pairs + waves * slots - 1) / (waves * slots);
   if (P < 8) P = 8;
   return (int)(P > pmax ? pmax : P);
+}
+
+static int sign2_smem(int P, bool straddle) {
+  return (kSign2Four ? kAesSmem4Bytes : kAesSmemBytes) + P * sign_slots(straddle) * SW_SLOT_BYTES;
+}
+static int sign2_smem_max() {  // the largest chunk either layout uses (P * slots is the same with or without straddle)
+  return sign2_smem(kSign2Four ? 128 : 64, false);
 }
 
 int mpc3_rss_sign(const uint32_t* rk3, const uint64_t* ctr, int mode, uint64_t j_bin, uint64_t j_xor, uint64_t j_arith,
@@ -763,13 +778,13 @@ int mpc3_rss_sign(const uint32_t* rk3, const uint64_t* ctr, int mode, uint64_t j
     const uint64_t e0 = 2 * main_pairs, nr = n - e0;
     const bool straddle = (n_total & 1) != 0;
     const int P = sign2_chunk((nr + 1) / 2, straddle);
-    const int smem = kAesSmemBytes + P * sign_slots(straddle) * SW_SLOT_BYTES;
-    if (!aes_attr((const void*)sign2_kernel<false>, kAesSmemBytes + 64 * sign_slots(false) * SW_SLOT_BYTES))
-      return check_launch("sign2 smem attribute");
+    const int smem = sign2_smem(P, straddle);
+    auto kern = kSign2Four ? sign2_kernel<false, true> : sign2_kernel<false, false>;
+    if (!aes_attr((const void*)kern, sign2_smem_max())) return check_launch("sign2 smem attribute");
     uint64_t chunks = ((nr + 1) / 2 + P - 1) / P;
     unsigned grid = (unsigned)(chunks < 148 * 2 * 8 ? chunks : 148 * 2 * 8);
-    launch_pdl(sign2_kernel<false>, dim3(grid), dim3(kThreads), smem, as_stream(stream), ks, ctr, a, mode, x + e0,
-               out + e0, mask ? mask + e0 : mask, nr, n_total, elem_off + e0, P, n, MaxGeom{0, 0, 1});
+    launch_pdl(kern, dim3(grid), dim3(kSign2Four ? kSignThreads : kThreads), smem, as_stream(stream), ks, ctr, a, mode,
+               x + e0, out + e0, mask ? mask + e0 : mask, nr, n_total, elem_off + e0, P, n, MaxGeom{0, 0, 1});
     return check_launch("rss_sign2");
   }
   return MPC3_OK;
@@ -792,13 +807,13 @@ int mpc3_rss_max_level(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_bin,
   a.ja = j_arith;
   const bool straddle = (n_total & 1) != 0;
   const int P = sign2_chunk((n + 1) / 2, straddle);
-  const int smem = kAesSmemBytes + P * sign_slots(straddle) * SW_SLOT_BYTES;
-  if (!aes_attr((const void*)sign2_kernel<true>, kAesSmemBytes + 64 * sign_slots(false) * SW_SLOT_BYTES))
-    return check_launch("max_level smem attribute");
+  const int smem = sign2_smem(P, straddle);
+  auto kern = kSign2Four ? sign2_kernel<true, true> : sign2_kernel<true, false>;
+  if (!aes_attr((const void*)kern, sign2_smem_max())) return check_launch("max_level smem attribute");
   uint64_t chunks = ((n + 1) / 2 + P - 1) / P;
   unsigned grid = (unsigned)(chunks < 148 * 2 * 8 ? chunks : 148 * 2 * 8);
-  launch_pdl(sign2_kernel<true>, dim3(grid), dim3(kThreads), smem, as_stream(stream), ks, ctr, a, (int)MODE_RELU, v,
-             out, (uint64_t*)nullptr, n, n_total, elem_off, P, (uint64_t)0, MaxGeom{rows, m, k});
+  launch_pdl(kern, dim3(grid), dim3(kSign2Four ? kSignThreads : kThreads), smem, as_stream(stream), ks, ctr, a,
+             (int)MODE_RELU, v, out, (uint64_t*)nullptr, n, n_total, elem_off, P, (uint64_t)0, MaxGeom{rows, m, k});
   return check_launch("rss_max_level");
 }
 
