@@ -943,10 +943,13 @@ class TrioSession:
             z = self.dgrad_packed(g.data, a_op, nb * oh * ow, o, w_packed, col)
         else:
             z = self._cross_gemm(g.data, a_op, k.data, b_op, nb * oh * ow, ncols, o, c_col=col)
-        out = zeros((nb, c, h, w), g.fp)
+        hf, wf = (oh - 1) * sh + kh, (ow - 1) * sw + kw
+        # every input position is some correlation element's embedding unless
+        # the forward conv dropped trailing rows / columns (floor division):
+        # only then do the uncovered positions need zeros
+        out = (empty if h + ph <= hf and w + pw <= wf else zeros)((nb, c, h, w), g.fp)
         ja = self.take(ARITH)
         jr, jq = self.take(TR_RHO), self.take(TR_R)
-        hf, wf = (oh - 1) * sh + kh, (ow - 1) * sw + kw
         full = nb * c * hf * wf
         K.call("mpc3_rss_col2im_reshare_truncate_layout", self.rk, self.ctr_ptr, ja, jr, jq, bits, z.data_ptr(),
                1 if col else 0, nb, c, oh, ow, kh, kw, sh, sw, ph, pw, h, w, out.data.data_ptr(),
@@ -971,7 +974,7 @@ class TrioSession:
         b_op = K.dense_operand(c, o * kh * kw, s_r=ks[2], off=(kh - 1) * ks[3] + (kw - 1) * ks[4], t0=ks[1],
                                t1=-ks[3], t2=-ks[4], K1=kh, K2=kw)
         z = self._cross_gemm(g.data, a_op, k.data, b_op, nb * hf * wf, c, o * kh * kw)
-        out = zeros((nb, c, h, w), g.fp)
+        out = (empty if h + ph <= hf and w + pw <= wf else zeros)((nb, c, h, w), g.fp)
         crop = (nb, c, max(0, min(h, hf - ph)), max(0, min(w, wf - pw)))
         view = K.make_view((nb, c, hf, wf), crop=crop, origin=(0, 0, ph, pw), z_stride=(hf * wf * c, 1, wf * c, c),
                            out_stride=(c * h * w, h * w, w, 1), out_plane=nb * c * h * w, z_plane=nb * hf * wf * c)
