@@ -307,6 +307,19 @@ int mpc3_ring_pack(const uint64_t* src, int64_t src_plane, const mpc3_operand* o
 int mpc3_ring_pack_halves(const uint64_t* src, int64_t src_plane, const mpc3_operand* op, int role,
                           uint8_t* out, int64_t kp, int64_t kh, void* stream);
 
+/* mpc3_ring_pack_halves that also clears zero[0 .. zero_words) (after the
+ * previous kernel has finished): the C of the GEMM that follows, when that
+ * GEMM accumulates atomically (mpc3_ring_gemm_needs_zero), so it needs no
+ * memset launch of its own.  zero may be NULL (zero_words 0). */
+int mpc3_ring_pack_halves_z(const uint64_t* src, int64_t src_plane, const mpc3_operand* op, int role,
+                            uint8_t* out, int64_t kp, int64_t kh, uint64_t* zero, int64_t zero_words,
+                            void* stream);
+
+/* 1 if mpc3_ring_gemm_auto (transposed 0, kp = packed inner length) or
+ * mpc3_ring_gemm_t (transposed 1, kp = 2 * kc_half) accumulates into C
+ * atomically for this shape (so C must start at zero), else 0. */
+int mpc3_ring_gemm_needs_zero(int transposed, int groups, int64_t M, int64_t N, int64_t kp);
+
 /* C[g] (+)= A[g] . B[g]^T over Z_2^64 (tcgen05 kind::i8, TMA-fed).
  * A: [groups][8][M][kp] u8, B: [groups][8][N][kp] u8, C: rows M, cols N,
  * leading dim ldc, group stride c_group.  splits > 1 requires C zeroed (the
@@ -338,6 +351,10 @@ int mpc3_ring_gemm_streamk(const uint8_t* A, const uint8_t* B, uint64_t* C, int 
  * accumulated atomically. */
 int mpc3_ring_gemm_auto(const uint8_t* A, const uint8_t* B, uint64_t* C, int groups, int64_t M, int64_t N,
                         int64_t kp, int c_layout, void* stream);
+/* Same; c_zeroed = 1 promises C is already zero where the launch needs it
+ * (no memset issued). */
+int mpc3_ring_gemm_auto_z(const uint8_t* A, const uint8_t* B, uint64_t* C, int groups, int64_t M, int64_t N,
+                          int64_t kp, int c_layout, int c_zeroed, void* stream);
 
 /* C[g] = A[g] . B[g]^T where either operand may be read in place from
  * another GEMM's packed buffer, transposed ("MN" operand): the weight
@@ -354,6 +371,9 @@ int mpc3_ring_gemm_auto(const uint8_t* A, const uint8_t* B, uint64_t* C, int gro
 int mpc3_ring_gemm_t(const uint8_t* A, int a_mn, int64_t a_rows, int64_t a_kp, int64_t a_half, const uint8_t* B,
                      int b_mn, int64_t b_rows, int64_t b_kp, int64_t b_half, uint64_t* C, int groups, int64_t M,
                      int64_t N, int64_t kc_half, int c_layout, void* stream);
+int mpc3_ring_gemm_t_z(const uint8_t* A, int a_mn, int64_t a_rows, int64_t a_kp, int64_t a_half, const uint8_t* B,
+                       int b_mn, int64_t b_rows, int64_t b_kp, int64_t b_half, uint64_t* C, int groups, int64_t M,
+                       int64_t N, int64_t kc_half, int c_layout, int c_zeroed, void* stream);
 
 /* The three parties' cross terms of a SMALL secure layer on the CUDA cores
  * (64-bit IMAD, no limb packs / TMA / TMEM set-up):

@@ -183,6 +183,11 @@ _SIGS = {
     "mpc3_ring_sumpool": (C.c_int, [_P, _P, _I64, _I64, _I64, _I64, C.c_int, C.c_int, C.c_int, C.c_int, _P]),
     "mpc3_ring_pack": (C.c_int, [_P, _I64, C.POINTER(Operand), C.c_int, _P, _I64, _P]),
     "mpc3_ring_pack_halves": (C.c_int, [_P, _I64, C.POINTER(Operand), C.c_int, _P, _I64, _I64, _P]),
+    "mpc3_ring_pack_halves_z": (C.c_int, [_P, _I64, C.POINTER(Operand), C.c_int, _P, _I64, _I64, _P, _I64, _P]),
+    "mpc3_ring_gemm_needs_zero": (C.c_int, [C.c_int, C.c_int, _I64, _I64, _I64]),
+    "mpc3_ring_gemm_auto_z": (C.c_int, [_P, _P, _P, C.c_int, _I64, _I64, _I64, C.c_int, C.c_int, _P]),
+    "mpc3_ring_gemm_t_z": (C.c_int, [_P, C.c_int, _I64, _I64, _I64, _P, C.c_int, _I64, _I64, _I64, _P, C.c_int, _I64,
+                                     _I64, _I64, C.c_int, C.c_int, _P]),
     "mpc3_ring_gemm_packed": (C.c_int, [_P, _P, _P, C.c_int, _I64, _I64, _I64, _I64, _I64, C.c_int, _P]),
     "mpc3_ring_gemm_auto": (C.c_int, [_P, _P, _P, C.c_int, _I64, _I64, _I64, C.c_int, _P]),
     "mpc3_ring_gemm_t": (C.c_int, [_P, C.c_int, _I64, _I64, _I64, _P, C.c_int, _I64, _I64, _I64, _P, C.c_int, _I64,

@@ -57,6 +57,8 @@ constexpr int PT_R = 64, PT_K = 64, PT_THREADS = 256;
 struct PackTileArgs {
   int64_t rows, K, kp, lim;  // lim: packed columns with data (K or kh + K)
   int64_t kh;                // first packed column of the second half
+  uint64_t* zero;            // optional: words the next GEMM accumulates into atomically,
+  int64_t zero_words;        //   cleared here so it needs no memset launch of its own
   int32_t H, W, sH, sW;      // bounds / strides of the (y, x) part (dense: no bounds, 0 strides)
 };
 
@@ -127,6 +129,11 @@ __global__ void __launch_bounds__(PT_THREADS) pack_tile_kernel(const uint64_t* _
     cpart[t - PT_R] = pack_col_part(o, c0 + (t - PT_R), a.K, a.lim, a.kh);
   __syncthreads();
   griddep_wait();  // the source tensor is the previous kernel's output
+  if (a.zero) {
+    const int64_t nblk = (int64_t)gridDim.x * gridDim.y * gridDim.z;
+    const int64_t bid = blockIdx.x + (int64_t)gridDim.x * (blockIdx.y + (int64_t)gridDim.y * blockIdx.z);
+    for (int64_t i = bid * PT_THREADS + t; i < a.zero_words; i += nblk * PT_THREADS) a.zero[i] = 0;
+  }
   // phase 1: gather the packed values of the tile.  Each thread keeps one
   // row (R_FAST) or one column fixed in registers; a warp's 32 lanes walk
   // the source's contiguous direction.  All loads first (16 in flight).
@@ -1037,6 +1044,12 @@ int mpc3_ring_pack(const uint64_t* src, int64_t src_plane, const mpc3_operand* o
 
 int mpc3_ring_pack_halves(const uint64_t* src, int64_t src_plane, const mpc3_operand* op, int role, uint8_t* out,
                           int64_t kp, int64_t kh, void* stream) {
+  return mpc3_ring_pack_halves_z(src, src_plane, op, role, out, kp, kh, nullptr, 0, stream);
+}
+
+int mpc3_ring_pack_halves_z(const uint64_t* src, int64_t src_plane, const mpc3_operand* op, int role, uint8_t* out,
+                            int64_t kp, int64_t kh, uint64_t* zero, int64_t zero_words, void* stream) {
+  if (zero_words < 0 || (zero_words && !zero)) return MPC3_ERR_CONFIG;
   if (!op || role < 0 || role > 2) return MPC3_ERR_CONFIG;
   if (kp % 16) return MPC3_ERR_SHAPE;
   if (role == 2) kh = op->k;
@@ -1046,7 +1059,11 @@ int mpc3_ring_pack_halves(const uint64_t* src, int64_t src_plane, const mpc3_ope
   Operand o = to_operand(op);
   int groups = role == 2 ? 1 : 3;
   int64_t total = (int64_t)groups * o.rows * (kp / 8);
-  if (total == 0) return MPC3_OK;
+  if (total == 0) {
+    if (zero_words && cudaMemsetAsync(zero, 0, (size_t)zero_words * 8, as_stream(stream)) != cudaSuccess)
+      return check_launch("pack zero memset");
+    return MPC3_OK;
+  }
   const bool dilated = o.mode == MPC3_GATHER_IM2COL && (o.dh != 1 || o.dw != 1);
   const int64_t row_tiles = (o.rows + PT_R - 1) / PT_R;
   // the tiled kernel addresses a component plane with 32-bit offsets
@@ -1060,6 +1077,8 @@ int mpc3_ring_pack_halves(const uint64_t* src, int64_t src_plane, const mpc3_ope
     a.kp = kp;
     a.lim = kneed;
     a.kh = kh;
+    a.zero = zero;
+    a.zero_words = zero_words;
     bool r_fast;
     if (o.mode == MPC3_GATHER_DENSE) {
       a.H = a.W = 1;
@@ -1083,6 +1102,8 @@ int mpc3_ring_pack_halves(const uint64_t* src, int64_t src_plane, const mpc3_ope
     launch_pdl(k, grid, dim3(PT_THREADS), 0, as_stream(stream), src, src_plane, o, a, out);
     return check_launch("ring_pack_tile");
   }
+  if (zero_words && cudaMemsetAsync(zero, 0, (size_t)zero_words * 8, as_stream(stream)) != cudaSuccess)
+    return check_launch("pack zero memset");
   pack_kernel<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(src, src_plane, o, role, groups, out, kp, kh);
   return check_launch("ring_pack");
 }
@@ -1149,46 +1170,96 @@ int mpc3_ring_gemm_streamk(const uint8_t* A, const uint8_t* B, uint64_t* C, int 
   return check_launch("ring_gemm_streamk");
 }
 
-int mpc3_ring_gemm_auto(const uint8_t* A, const uint8_t* B, uint64_t* C, int groups, int64_t M, int64_t N,
-                        int64_t kp, int c_layout, void* stream) {
-  if (groups < 1 || M < 0 || N < 0 || kp < 0) return MPC3_ERR_SHAPE;
-  if (kp % 16) return MPC3_ERR_SHAPE;
-  if (c_layout != 0 && c_layout != 1) return MPC3_ERR_CONFIG;
-  if (M == 0 || N == 0) return MPC3_OK;
+// Launch shape of mpc3_ring_gemm_auto: split-K count, stream-K, and whether
+// C must start at zero (atomic accumulation).
+struct AutoPlan {
+  int64_t splits;
+  bool streamk, zero;
+};
+static AutoPlan auto_plan(int groups, int64_t M, int64_t N, int64_t kp) {
   const int64_t sms = 148;
-  const int64_t ldc = c_layout ? M : N, c_group = M * N;
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * groups;
   const int64_t nkb = (kp + BK - 1) / BK;
   const int64_t need = (nkb * BK + MAX_SPLIT_K - 1) / MAX_SPLIT_K;  // exactness
   int64_t occ = sms / tiles;                                         // <= one wave, >= 4 K-blocks per split
   if (occ > nkb / 4) occ = nkb / 4;
   if (occ < 1) occ = 1;
-  const int64_t splits = need > occ ? need : occ;
-  const int64_t ctas = tiles * splits;
+  AutoPlan p;
+  p.splits = need > occ ? need : occ;
+  const int64_t ctas = tiles * p.splits;
   const double eff = (double)ctas / (double)(((ctas + sms - 1) / sms) * sms);
-  const size_t cbytes = (size_t)groups * M * N * 8;
   static const double sk_eff = getenv("MPC3_GEMM_SK") ? atof(getenv("MPC3_GEMM_SK")) : 0.85;
-  if (nkb == 0 || eff < sk_eff || splits > 1) {
-    if (cudaMemsetAsync(C, 0, cbytes, as_stream(stream)) != cudaSuccess) return check_launch("gemm C memset");
-    if (nkb == 0) return MPC3_OK;
+  p.streamk = nkb > 0 && eff < sk_eff;
+  p.zero = nkb == 0 || p.streamk || p.splits > 1;
+  return p;
+}
+
+int mpc3_ring_gemm_auto(const uint8_t* A, const uint8_t* B, uint64_t* C, int groups, int64_t M, int64_t N,
+                        int64_t kp, int c_layout, void* stream) {
+  return mpc3_ring_gemm_auto_z(A, B, C, groups, M, N, kp, c_layout, 0, stream);
+}
+
+int mpc3_ring_gemm_auto_z(const uint8_t* A, const uint8_t* B, uint64_t* C, int groups, int64_t M, int64_t N,
+                          int64_t kp, int c_layout, int c_zeroed, void* stream) {
+  if (groups < 1 || M < 0 || N < 0 || kp < 0) return MPC3_ERR_SHAPE;
+  if (kp % 16) return MPC3_ERR_SHAPE;
+  if (c_layout != 0 && c_layout != 1) return MPC3_ERR_CONFIG;
+  if (M == 0 || N == 0) return MPC3_OK;
+  const int64_t sms = 148;
+  const int64_t ldc = c_layout ? M : N, c_group = M * N;
+  const AutoPlan p = auto_plan(groups, M, N, kp);
+  const int64_t nkb = (kp + BK - 1) / BK;
+  if (p.zero && !c_zeroed) {
+    if (cudaMemsetAsync(C, 0, (size_t)groups * M * N * 8, as_stream(stream)) != cudaSuccess)
+      return check_launch("gemm C memset");
   }
-  if (eff < sk_eff) {  // the split-K grid would leave SMs idle: stream-K over every SM
-    int64_t iters = tiles * nkb;
+  if (nkb == 0) return MPC3_OK;
+  if (p.streamk) {  // the split-K grid would leave SMs idle: stream-K over every SM
+    const int64_t iters = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * groups * nkb;
     int64_t c = iters / 2 < sms ? iters / 2 : sms;
     return mpc3_ring_gemm_streamk(A, B, C, groups, M, N, kp, ldc, c_group, (int)(c < 1 ? 1 : c), c_layout, stream);
   }
-  return mpc3_ring_gemm_packed_layout(A, B, C, groups, M, N, kp, ldc, c_group, (int)splits, c_layout, stream);
+  return mpc3_ring_gemm_packed_layout(A, B, C, groups, M, N, kp, ldc, c_group, (int)p.splits, c_layout, stream);
 }
 
-#ifdef MPC3_GEMM_TRACE
-int mpc3_debug_gemm_trace(void* out) {
-  return cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace)) == cudaSuccess ? 0 : MPC3_ERR_CUDA;
+// Launch shape of mpc3_ring_gemm_t (split-K only unless MPC3_GEMM_T_SK).
+static AutoPlan t_plan(int groups, int64_t M, int64_t N, int64_t kp) {
+  const int64_t sms = 148;
+  const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * groups;
+  const int64_t nkb = kp / BK;
+  const int64_t need = (nkb * BK + MAX_SPLIT_K - 1) / MAX_SPLIT_K;
+  int64_t occ = sms / tiles;
+  if (occ > nkb / 4) occ = nkb / 4;
+  if (occ < 1) occ = 1;
+  AutoPlan p;
+  p.splits = need > occ ? need : occ;
+  const int64_t ctas = tiles * p.splits;
+  const double eff = (double)ctas / (double)(((ctas + sms - 1) / sms) * sms);
+  // stream-K off by default here: the weight gradients run on the side stream
+  // beside the input-gradient chain, which a persistent all-SM grid would
+  // block (AlexNet step 2.79 ms without, 2.84 ms with stream-K at eff < 0.85)
+  static const double sk_eff = getenv("MPC3_GEMM_T_SK") ? atof(getenv("MPC3_GEMM_T_SK")) : 0.0;
+  p.streamk = nkb > 0 && eff < sk_eff;
+  p.zero = nkb == 0 || p.splits > 1 || p.streamk;
+  return p;
 }
-#endif
+
+int mpc3_ring_gemm_needs_zero(int transposed, int groups, int64_t M, int64_t N, int64_t kp) {
+  if (groups < 1 || M < 0 || N < 0 || kp < 0) return MPC3_ERR_SHAPE;
+  if (M == 0 || N == 0) return 0;
+  return (transposed ? t_plan(groups, M, N, kp) : auto_plan(groups, M, N, kp)).zero ? 1 : 0;
+}
 
 int mpc3_ring_gemm_t(const uint8_t* A, int a_mn, int64_t a_rows, int64_t a_kp, int64_t a_half, const uint8_t* B,
                      int b_mn, int64_t b_rows, int64_t b_kp, int64_t b_half, uint64_t* C, int groups, int64_t M,
                      int64_t N, int64_t kc_half, int c_layout, void* stream) {
+  return mpc3_ring_gemm_t_z(A, a_mn, a_rows, a_kp, a_half, B, b_mn, b_rows, b_kp, b_half, C, groups, M, N, kc_half,
+                            c_layout, 0, stream);
+}
+
+int mpc3_ring_gemm_t_z(const uint8_t* A, int a_mn, int64_t a_rows, int64_t a_kp, int64_t a_half, const uint8_t* B,
+                       int b_mn, int64_t b_rows, int64_t b_kp, int64_t b_half, uint64_t* C, int groups, int64_t M,
+                       int64_t N, int64_t kc_half, int c_layout, int c_zeroed, void* stream) {
   if (groups < 1 || M < 0 || N < 0 || kc_half < 0 || (kc_half % BK)) return MPC3_ERR_SHAPE;
   if (c_layout != 0 && c_layout != 1) return MPC3_ERR_CONFIG;
   if (M == 0 || N == 0) return MPC3_OK;
@@ -1216,26 +1287,17 @@ int mpc3_ring_gemm_t(const uint8_t* A, int a_mn, int64_t a_rows, int64_t a_kp, i
   const int64_t sms = 148;
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * groups;
   const int64_t nkb = kp / BK;
-  const int64_t need = (nkb * BK + MAX_SPLIT_K - 1) / MAX_SPLIT_K;
-  int64_t occ = sms / tiles;
-  if (occ > nkb / 4) occ = nkb / 4;
-  if (occ < 1) occ = 1;
-  const int64_t splits = need > occ ? need : occ;
+  const AutoPlan p = t_plan(groups, M, N, kp);
+  const int64_t splits = p.splits;
   const int kbs = (int)((nkb + splits - 1) / splits);
   if ((int64_t)kbs * BK > MAX_SPLIT_K) return MPC3_ERR_EXACTNESS;
-  const int64_t ctas = tiles * splits;
-  const double eff = (double)ctas / (double)(((ctas + sms - 1) / sms) * sms);
-  MnArgs mn = {a_mn ? 1 : 0, b_mn ? 1 : 0, (int)a_half, (int)b_half, (int)(kc_half / BK)};
-  // stream-K off by default here: the weight gradients run on the side stream
-  // beside the input-gradient chain, which a persistent all-SM grid would
-  // block (AlexNet step 2.79 ms without, 2.84 ms with stream-K at eff < 0.85)
-  static const double sk_eff = getenv("MPC3_GEMM_T_SK") ? atof(getenv("MPC3_GEMM_T_SK")) : 0.0;
-  if (nkb == 0 || splits > 1 || eff < sk_eff) {
+  if (p.zero && !c_zeroed) {
     if (cudaMemsetAsync(C, 0, (size_t)groups * M * N * 8, as_stream(stream)) != cudaSuccess)
       return check_launch("gemm C memset");
-    if (nkb == 0) return MPC3_OK;
   }
-  if (eff < sk_eff) {  // the split-K grid would leave SMs idle in its last wave: stream-K
+  if (nkb == 0) return MPC3_OK;
+  MnArgs mn = {a_mn ? 1 : 0, b_mn ? 1 : 0, (int)a_half, (int)b_half, (int)(kc_half / BK)};
+  if (p.streamk) {  // the split-K grid would leave SMs idle in its last wave: stream-K
     static bool sk_attr = false;
     if (!sk_attr) {
       if (cudaFuncSetAttribute(gemm_sk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess)

@@ -557,13 +557,19 @@ class TrioSession:
         return out
 
     # -- bilinear layers (protocols.py:97-136, nn.py:435-484) --
-    def pack(self, src: torch.Tensor, op, rows: int, k: int, role: int) -> Packed:
-        """Pack one cross-term operand in the reusable layout (see Packed)."""
+    def pack(self, src: torch.Tensor, op, rows: int, k: int, role: int, zero: torch.Tensor | None = None) -> Packed:
+        """Pack one cross-term operand in the reusable layout (see Packed);
+        `zero`: the next GEMM's C, cleared by the same launch when that GEMM
+        accumulates atomically."""
         kh, kp = Packed.geometry(k)
         buf = torch.empty(3 * 8 * rows * kp, dtype=torch.uint8, device=_dev())
-        K.call("mpc3_ring_pack_halves", src.data_ptr(), src.stride(0), C.byref(op), role, buf.data_ptr(), kp, kh,
-               _stream())
+        K.call("mpc3_ring_pack_halves_z", src.data_ptr(), src.stride(0), C.byref(op), role, buf.data_ptr(), kp, kh,
+               None if zero is None else zero.data_ptr(), 0 if zero is None else zero.numel(), _stream())
         return Packed(buf, rows, k, kh, kp, role)
+
+    @staticmethod
+    def _needs_zero(transposed: bool, M: int, N: int, kp: int) -> bool:
+        return K.lib().mpc3_ring_gemm_needs_zero(1 if transposed else 0, 3, M, N, kp) == 1
 
     @staticmethod
     def _pack_key(src: torch.Tensor, op, role: int):
@@ -615,19 +621,21 @@ class TrioSession:
         elif pre is None:
             K.call("mpc3_ring_pack_halves", b_src.data_ptr(), b_src.stride(0), C.byref(b_op), 1 - a_role,
                    B.data_ptr(), kp, kh, st)
+        z = torch.empty(3 * M * N, dtype=torch.int64, device=_dev())
+        zeroed = False
         if a_packed is not None:
             if (a_packed.rows, a_packed.k, a_packed.kh, a_packed.kp, a_packed.role) != (M, Kd, kh, kp, a_role):
                 raise ShapeError("packed operand does not match the GEMM")
             A = a_packed
-        else:
-            A = self.pack(a_src, a_op, M, Kd, a_role)
+        else:  # the A pack clears C when the GEMM accumulates atomically
+            zeroed = self._needs_zero(False, M, N, kp)
+            A = self.pack(a_src, a_op, M, Kd, a_role, zero=z if zeroed else None)
         if ps is not None and ps != main:
             ev2 = torch.cuda.Event()
             ev2.record(ps)
             main.wait_event(ev2)
-        z = torch.empty(3 * M * N, dtype=torch.int64, device=_dev())
-        K.call("mpc3_ring_gemm_auto", A.buf.data_ptr(), B.data_ptr(), z.data_ptr(), 3, M, N, kp, 1 if c_col else 0,
-               st)
+        K.call("mpc3_ring_gemm_auto_z", A.buf.data_ptr(), B.data_ptr(), z.data_ptr(), 3, M, N, kp, 1 if c_col else 0,
+               1 if zeroed else 0, st)
         if keep is not None:
             keep.extend([A, Packed(B, N, Kd, kh, kp, 1 - a_role)])
         return z
@@ -644,27 +652,30 @@ class TrioSession:
         kc = _round_up(o, 32)
         A = torch.empty(3 * 8 * rows * 2 * kc, dtype=torch.uint8, device=_dev())
         st = _stream()
-        K.call("mpc3_ring_pack_halves", g_src.data_ptr(), g_src.stride(0), C.byref(g_op), 1, A.data_ptr(), 2 * kc, kc,
-               st)
         z = torch.empty(3 * rows * wp.k, dtype=torch.int64, device=_dev())
-        K.call("mpc3_ring_gemm_t", A.data_ptr(), 0, rows, 2 * kc, 0, wp.buf.data_ptr(), 1, wp.rows, wp.kp, wp.kh,
-               z.data_ptr(), 3, rows, wp.k, kc, 1 if c_col else 0, st)
+        zeroed = self._needs_zero(True, rows, wp.k, 2 * kc)
+        K.call("mpc3_ring_pack_halves_z", g_src.data_ptr(), g_src.stride(0), C.byref(g_op), 1, A.data_ptr(), 2 * kc,
+               kc, z.data_ptr() if zeroed else None, z.numel() if zeroed else 0, st)
+        K.call("mpc3_ring_gemm_t_z", A.data_ptr(), 0, rows, 2 * kc, 0, wp.buf.data_ptr(), 1, wp.rows, wp.kp, wp.kh,
+               z.data_ptr(), 3, rows, wp.k, kc, 1 if c_col else 0, 1 if zeroed else 0, st)
         return z
 
-    def wgrad_packed(self, gp: Packed, xp: Packed) -> torch.Tensor:
+    def wgrad_packed(self, g: RssTensor, xp: Packed) -> torch.Tensor:
         """Weight-gradient cross terms dW_i = (g_i + g_{i+1})^T x_i + g_i^T x_{i+1}
-        (protocols.py:110-115 with nn.py:435-457's operands) straight from the
-        input-gradient pass's role-0 pack of g and the forward pass's role-1
-        pack of x, both read transposed: no operand is packed here.  z is
-        [3][gp.k][xp.k] row-major."""
-        if gp.role != 0 or xp.role != 1 or gp.rows != xp.rows:
+        (protocols.py:110-115 with nn.py:435-457's operands) from a role-0
+        pack of g and the forward pass's role-1 pack of x, both read
+        transposed.  z is [3][O][xp.k] row-major."""
+        op, rows, o = self.grad_operand(g)
+        if xp.role != 1 or xp.rows != rows:
             raise ShapeError("weight-gradient packs do not match")
         # computed as x^T g (A = x, B = g) into the column-major layout, which
         # is the same memory and keeps the epilogue's stores coalesced
-        M, N = xp.k, gp.k
+        M, N, kc = xp.k, o, _round_up(rows, 32)
         z = torch.empty(3 * M * N, dtype=torch.int64, device=_dev())
-        K.call("mpc3_ring_gemm_t", xp.buf.data_ptr(), 1, xp.rows, xp.kp, xp.kh, gp.buf.data_ptr(), 1, gp.rows, gp.kp,
-               gp.kh, z.data_ptr(), 3, M, N, _round_up(gp.rows, 32), 1, _stream())
+        zeroed = self._needs_zero(True, M, N, 2 * kc)
+        gp = self.pack(g.data, op, rows, o, 0, zero=z if zeroed else None)
+        K.call("mpc3_ring_gemm_t_z", xp.buf.data_ptr(), 1, xp.rows, xp.kp, xp.kh, gp.buf.data_ptr(), 1, gp.rows, gp.kp,
+               gp.kh, z.data_ptr(), 3, M, N, kc, 1, 1 if zeroed else 0, _stream())
         return z
 
     def _cross_gemm(self, a_src, a_op, b_src, b_op, M, N, Kd, c_col: bool = False, a_role: int = 0,
@@ -704,12 +715,15 @@ class TrioSession:
                 B = torch.empty(3 * 8 * N * kp, dtype=torch.uint8, device=_dev())
                 K.call("mpc3_ring_pack", b_src.data_ptr(), b_src.stride(0), C.byref(b_op), 1, B.data_ptr(), kp, st)
                 self._wcache[key] = B
-            K.call("mpc3_ring_pack", a_src.data_ptr(), a_src.stride(0), C.byref(a_op), 0, A.data_ptr(), kp, st)
             z = torch.empty(3 * M * N, dtype=torch.int64, device=_dev())
-            K.call("mpc3_ring_gemm_auto", A.data_ptr(), B.data_ptr(), z.data_ptr(), 3, M, N, kp, 1 if c_col else 0,
-                   st)
+            zeroed = self._needs_zero(False, M, N, kp)
+            self._pack_a_zero(a_src, a_op, A, kp, Kd, z, zeroed, st)
+            K.call("mpc3_ring_gemm_auto_z", A.data_ptr(), B.data_ptr(), z.data_ptr(), 3, M, N, kp, 1 if c_col else 0,
+                   1 if zeroed else 0, st)
             return z
         B = torch.empty(3 * 8 * N * kp, dtype=torch.uint8, device=_dev())
+        z = torch.empty(3 * M * N, dtype=torch.int64, device=_dev())
+        zeroed = self._needs_zero(False, M, N, kp)
         # the two operand packs are independent: B on the pack stream, A here
         main = torch.cuda.current_stream()
         ps = self.pack_stream() if OVERLAP_PACK else None
@@ -719,16 +733,22 @@ class TrioSession:
             ps.wait_event(ev)
             K.call("mpc3_ring_pack", b_src.data_ptr(), b_src.stride(0), C.byref(b_op), 1, B.data_ptr(), kp,
                    ps.cuda_stream)
-            K.call("mpc3_ring_pack", a_src.data_ptr(), a_src.stride(0), C.byref(a_op), 0, A.data_ptr(), kp, st)
+            self._pack_a_zero(a_src, a_op, A, kp, Kd, z, zeroed, st)
             ev2 = torch.cuda.Event()
             ev2.record(ps)
             main.wait_event(ev2)
         else:
-            K.call("mpc3_ring_pack", a_src.data_ptr(), a_src.stride(0), C.byref(a_op), 0, A.data_ptr(), kp, st)
+            self._pack_a_zero(a_src, a_op, A, kp, Kd, z, zeroed, st)
             K.call("mpc3_ring_pack", b_src.data_ptr(), b_src.stride(0), C.byref(b_op), 1, B.data_ptr(), kp, st)
-        z = torch.empty(3 * M * N, dtype=torch.int64, device=_dev())
-        K.call("mpc3_ring_gemm_auto", A.data_ptr(), B.data_ptr(), z.data_ptr(), 3, M, N, kp, 1 if c_col else 0, st)
+        K.call("mpc3_ring_gemm_auto_z", A.data_ptr(), B.data_ptr(), z.data_ptr(), 3, M, N, kp, 1 if c_col else 0,
+               1 if zeroed else 0, st)
         return z
+
+    @staticmethod
+    def _pack_a_zero(a_src, a_op, A, kp, Kd, z, zeroed, st):
+        """Role-0 pack of A (adjacent halves), clearing the GEMM's C with it when needed."""
+        K.call("mpc3_ring_pack_halves_z", a_src.data_ptr(), a_src.stride(0), C.byref(a_op), 0, A.data_ptr(), kp, Kd,
+               z.data_ptr() if zeroed else None, z.numel() if zeroed else 0, st)
 
     @property
     def c_col_ok(self) -> bool:
@@ -781,12 +801,12 @@ class TrioSession:
                 return self._finish(z, K.make_view((1, 1, m, n)), out, bits, "mul.reshare")
         return self._finish(z, K.make_view((1, 1, m, n)), out, bits, "mul.reshare", bias=bias, bias_dim=3)
 
-    def fc_wgrad_packed(self, gp: Packed, xp: Packed, bits: int) -> RssTensor:
-        """Fully-connected weight gradient g^T x (nn.py:525-527) from the
-        packs of g (rows: batch, K: out) and x (rows: batch, K: in)."""
-        check_accumulation(gp.rows * (self.dp.world if self.dp else 1))
-        m, n = gp.k, xp.k
-        z = self.wgrad_packed(gp, xp)
+    def fc_wgrad_packed(self, g: RssTensor, xp: Packed, bits: int) -> RssTensor:
+        """Fully-connected weight gradient g^T x (nn.py:525-527) from x's
+        forward pack (rows: batch, K: in)."""
+        check_accumulation(g.shape[0] * (self.dp.world if self.dp else 1))
+        m, n = g.shape[1], xp.k
+        z = self.wgrad_packed(g, xp)
         out = empty((m, n), self.fp)
         self._reduce_cross_terms(z)
         with self.replicated():
@@ -848,12 +868,12 @@ class TrioSession:
         return self._finish(z, view, out, bits, "mul.reshare", bias=bias, bias_dim=1)
 
     def conv2d_wgrad(self, x: RssTensor, g: RssTensor, kernel, stride, padding, bits,
-                     packs: tuple[Packed, Packed] | None = None) -> RssTensor:
+                     x_packed: Packed | None = None) -> RssTensor:
         """Kernel gradient (nn.py:435-457) as one direct implicit GEMM with
         K = N*OH*OW; the reference's dilated zeros contribute nothing, and the
         zero shares / truncation words are indexed over its full (C,O,fh,fw)
-        output so the result is bit-exact.  packs = (pack of g, im2col pack
-        of x) from the surrounding passes: the GEMM reads them transposed."""
+        output so the result is bit-exact.  x_packed: x's im2col pack from the
+        forward pass, read transposed beside a role-0 pack of g."""
         nb, c, h, w = x.shape
         nb2, o, oh, ow = g.shape
         kh, kw = kernel
@@ -870,11 +890,10 @@ class TrioSession:
         b_op = K.dense_operand(o, nb * oh * ow, s_r=gs[2], t0=gs[1], t1=gs[3], t2=gs[4], K1=oh, K2=ow)
         col = self.c_col_ok
         M = c * kh * kw
-        if packs is not None:  # z[o][(c, u, v)]: the column-major layout below
-            gp, xp = packs
-            if (gp.rows, gp.k, xp.rows, xp.k) != (nb * oh * ow, o, nb * oh * ow, M):
+        if x_packed is not None:  # z[o][(c, u, v)]: the column-major layout below
+            if (x_packed.rows, x_packed.k) != (nb * oh * ow, M):
                 raise ShapeError("weight-gradient packs do not match the layer")
-            z, col = self.wgrad_packed(gp, xp), True
+            z, col = self.wgrad_packed(g, x_packed), True
         else:
             z = self._cross_gemm(x.data, a_op, g.data, b_op, M, o, nb * oh * ow, c_col=col)
         out = empty((o, c, kh, kw), x.fp)
@@ -897,10 +916,6 @@ class TrioSession:
         nb, o, oh, ow = g.shape
         return (K.conv_operand(K.GATHER_IM2COL, nb * oh * ow, o, nb, o, oh, ow, gs[1:], 1, 1, 1, 1, 0, 0, oh, ow),
                 nb * oh * ow, o)
-
-    def pack_grad(self, g: RssTensor) -> Packed:
-        op, rows, k = self.grad_operand(g)
-        return self.pack(g.data, op, rows, k, 0)
 
     def conv2d_dgrad(self, g: RssTensor, k: RssTensor, stride, padding, in_shape, bits,
                      w_packed: Packed | None = None) -> RssTensor:

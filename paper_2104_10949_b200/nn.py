@@ -352,7 +352,7 @@ class TrioNet:
                 xp, wp = cached[2:4] if len(cached) > 3 else (None, None)
                 pi -= 1
                 if xp is not None:  # g's role-0 pack is made on the side stream, beside the input gradient
-                    grads[pi] = wgrad(lambda gg, b: S.fc_wgrad_packed(S.pack_grad(gg), b, t + batch_bits), g, xp)
+                    grads[pi] = wgrad(lambda gg, b: S.fc_wgrad_packed(gg, b, t + batch_bits), g, xp)
                 else:
                     grads[pi] = wgrad(lambda gg, xx: S.matmul(gg.apply(lambda d: d.transpose(1, 2)), xx,
                                                               bits=t + batch_bits, wgrad=True), g, x)
@@ -365,7 +365,7 @@ class TrioNet:
                 pi -= 1
                 grads[pi] = wgrad(lambda xx, gg, b: S.conv2d_wgrad(
                     xx, gg, spec.kernel, spec.stride, spec.padding, bits=t + batch_bits,
-                    packs=None if b is None else (S.pack_grad(gg), b)), x, g, xp)
+                    x_packed=b), x, g, xp)
                 if li == plist[0]:
                     break
                 g = S.conv2d_dgrad(g, k, spec.stride, spec.padding, x.shape, bits=t, w_packed=wp)
