@@ -189,6 +189,7 @@ int mpc3_rss_sign(const uint32_t* rk3, const uint64_t* ctr, int mode, uint64_t j
                   const uint64_t* x, uint64_t* out, uint64_t* mask, uint64_t n, uint64_t n_total,
                   uint64_t elem_off, void* stream);
 
+
 /* bit_inject of XOR-shared bits (protocols.py:304-331), 2 ARITH counters. */
 int mpc3_rss_bit_inject(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, const uint64_t* bits, uint64_t* out,
                         uint64_t n, void* stream);
@@ -223,6 +224,19 @@ int mpc3_rss_reshare_truncate_bias(const uint32_t* rk3, const uint64_t* ctr, uin
                                    uint64_t j_r, int bits, const uint64_t* z, const mpc3_view4* view,
                                    const uint64_t* bias, int64_t bias_plane, int bias_dim, uint64_t* out,
                                    uint64_t elem_off, void* stream);
+
+/* A secure layer's epilogue fused with the sign circuit after it
+ * (conv2d_shares / matmul_shares then relu, protocols.py:97-136, 334-353):
+ * the ReLU input is the layer's cross terms z (view: no crop / origin; bias
+ * optional, as mpc3_rss_reshare_truncate_bias) reshared with ARITH_ZERO j_ra
+ * and truncated by `bits` with TRUNC_RHO j_rho / TRUNC_R j_r in registers,
+ * then the circuit as mpc3_rss_sign (mode, j_bin, j_xor, j_arith).  Shares
+ * and PRF words are exactly those of the two separate calls; the reshared
+ * tensor itself is never written.  out / mask: the view's full size n. */
+int mpc3_rss_layer_sign(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_ra, uint64_t j_rho, uint64_t j_r,
+                        int bits, const uint64_t* z, const mpc3_view4* view, const uint64_t* bias, int64_t bias_plane,
+                        int bias_dim, int mode, uint64_t j_bin, uint64_t j_xor, uint64_t j_arith, uint64_t* out,
+                        uint64_t* mask, uint64_t elem_off, uint64_t n_total, void* stream);
 
 /* Input gradient epilogue (nn.py:460-484): z holds per-party cross terms
  * cols[(n,y,x), (c,a,b)] = sum_o g[n,o,y,x] k[o,c,a,b] (a GEMM with inner

@@ -234,26 +234,47 @@ __global__ void __launch_bounds__(Proto<F>::threads, Proto<F>::min_ctas) arith_k
 
 struct SignArgs {
   uint64_t jbin, jxor, ja;
+  uint64_t jra, jrho, jr;  // fused layer + ReLU: the layer's ARITH_ZERO / TRUNC_RHO / TRUNC_R counters
 };
+
+// the stream heads a sign launch needs, resolved by one thread into shared memory
+DEV void sign_streams(SignStreams& st, const SignArgs& args, const uint64_t* ctr, bool rs) {
+  st.bin = resolve(sref(BIN_INPUT, args.jbin), ctr);
+  for (int l = 0; l < 7; ++l) st.x[l] = resolve(sref(XOR_ZERO, args.jxor + l), ctr);
+  for (int l = 0; l < 3; ++l) st.a[l] = resolve(sref(ARITH_ZERO, args.ja + l), ctr);
+  if (rs) {
+    st.ra = resolve(sref(ARITH_ZERO, args.jra), ctr);
+    st.rrho = resolve(sref(TRUNC_RHO, args.jrho), ctr);
+    st.rr = resolve(sref(TRUNC_R, args.jr), ctr);
+  }
+}
 
 // Large tensors: one 512-thread CTA per SM with the four-table AES layout
 // (128 KiB) — the kernel is nothing but AES rounds.
+// RS: the input is a secure layer's cross terms (RsIn), reshared and
+// truncated in registers (fused layer + ReLU); otherwise the trio x.
+template <bool RS>
 __global__ void __launch_bounds__(kSignThreads, 1) sign_kernel(const __grid_constant__ KeySched ks,
                                                           const uint64_t* __restrict__ ctr, SignArgs args,
                                                           int mode, const uint64_t* __restrict__ x,
                                                           uint64_t* __restrict__ out,
                                                           uint64_t* __restrict__ mask, uint64_t n,
-                                                          uint64_t n_total, uint64_t elem_off, uint64_t plane) {
+                                                          uint64_t n_total, uint64_t elem_off, uint64_t plane,
+                                                          const __grid_constant__ RsIn rin) {
   MPC3_AES_SMEM4();
   static_assert(sizeof(SignStreams) <= sizeof(sm.extra), "stream heads fit the AesSmem extra area");
   SignStreams& st = *reinterpret_cast<SignStreams*>(sm.extra);  // uniform stream heads, indexed by level
-  if (threadIdx.x == 0) {
-    st.bin = resolve(sref(BIN_INPUT, args.jbin), ctr);
-    for (int l = 0; l < 7; ++l) st.x[l] = resolve(sref(XOR_ZERO, args.jxor + l), ctr);
-    for (int l = 0; l < 3; ++l) st.a[l] = resolve(sref(ARITH_ZERO, args.ja + l), ctr);
-  }
+  if (threadIdx.x == 0) sign_streams(st, args, ctr, RS);
   SmemTables4 tab = aes_smem_init4(sm, nullptr, 0);  // includes the barrier
-  GRID_LOOP(b, (n + 1) >> 1) sign_item(tab, &ks.rk[0][0], st, mode, x, out, mask, n, n_total, elem_off, b, plane);
+  if constexpr (RS) {
+    GRID_LOOP(b, (n + 1) >> 1) {
+      Word2 w3[3], rho, r;
+      reshare_trunc_words(tab, &ks.rk[0][0], st.ra, st.rrho, st.rr, (elem_off >> 1) + b, w3, rho, r);
+      sign_item_rs(tab, &ks.rk[0][0], st, mode, rin, w3, rho, r, out, mask, n, n_total, elem_off, b, plane);
+    }
+  } else {
+    GRID_LOOP(b, (n + 1) >> 1) sign_item(tab, &ks.rk[0][0], st, mode, x, out, mask, n, n_total, elem_off, b, plane);
+  }
 }
 
 // Two-phase sign circuit.  The 46 AES blocks an element pair consumes do not
@@ -272,30 +293,45 @@ HD int sign_slots(bool straddle) { return straddle ? 21 : 16; }
 
 // F: four-table AES (one 384-thread CTA per SM, up to 128 pairs per chunk)
 // or two-table (two 256-thread CTAs per SM, up to 64 pairs each).
-template <bool MAXL, bool F>
+// KIND: 0 sign / ReLU of x; 1 one max_tree level; 2 fused layer + ReLU (two
+// leading slots hold the pair's reshare words (3 keys) and truncation words
+// (rho, r); the circuit's slots follow).
+constexpr int S2_SIGN = 0, S2_MAXL = 1, S2_RS = 2;
+template <int KIND, bool F>
 __global__ void __launch_bounds__(F ? kSignThreads : kThreads, F ? 1 : 2)
     sign2_kernel(const __grid_constant__ KeySched ks, const uint64_t* __restrict__ ctr, SignArgs args, int mode,
                  const uint64_t* __restrict__ x, uint64_t* __restrict__ out, uint64_t* __restrict__ mask, uint64_t n,
-                 uint64_t n_total, uint64_t elem_off, int P, uint64_t plane, MaxGeom mg) {
+                 uint64_t n_total, uint64_t elem_off, int P, uint64_t plane, MaxGeom mg,
+                 const __grid_constant__ RsIn rin) {
+  constexpr bool MAXL = KIND == S2_MAXL;
+  constexpr int PRE = KIND == S2_RS ? 2 : 0;
   SignStreams& st = *reinterpret_cast<SignStreams*>(F ? reinterpret_cast<AesSmem4*>(mpc3_dsm)->extra
                                                       : reinterpret_cast<AesSmem*>(mpc3_dsm)->extra);
-  if (threadIdx.x == 0) {
-    st.bin = resolve(sref(BIN_INPUT, args.jbin), ctr);
-    for (int l = 0; l < 7; ++l) st.x[l] = resolve(sref(XOR_ZERO, args.jxor + l), ctr);
-    for (int l = 0; l < 3; ++l) st.a[l] = resolve(sref(ARITH_ZERO, args.ja + l), ctr);
-  }
+  if (threadIdx.x == 0) sign_streams(st, args, ctr, KIND == S2_RS);
   auto tab = Proto<F>::init();  // (its __syncthreads publishes st)
-  Word2* slots = reinterpret_cast<Word2*>(mpc3_dsm + (F ? sizeof(AesSmem4) : sizeof(AesSmem)));
+  Word2* pre = reinterpret_cast<Word2*>(mpc3_dsm + (F ? sizeof(AesSmem4) : sizeof(AesSmem)));
+  Word2* slots = pre + (size_t)PRE * P * 3;
   const bool straddle = (n_total & 1) != 0;
   const int L = straddle ? 3 : 2;  // slots per level 1..5
   const int nslots = sign_slots(straddle);
   const int used = mode <= MODE_MSB ? nslots - 3 : (mode == MODE_DRELU ? nslots - 1 : nslots);
   const uint64_t npairs = (n + 1) >> 1;
   for (uint64_t c0 = (uint64_t)blockIdx.x * P; c0 < npairs; c0 += (uint64_t)gridDim.x * P) {
-    for (int q = threadIdx.x; q < used * P; q += blockDim.x) {
-      const int s = q / P, p = q % P;
+    for (int q = threadIdx.x; q < (used + PRE) * P; q += blockDim.x) {
+      const int sa = q / P, p = q % P;
       if (c0 + p >= npairs) continue;
       const uint64_t blk = (elem_off >> 1) + c0 + p;
+      if (PRE && sa < PRE) {  // the fused layer's reshare / truncation words
+        Word2* dst = pre + ((size_t)sa * P + p) * 3;
+        if (sa == 0) {
+          prf_block3(tab, &ks.rk[0][0], st.ra, blk, dst);
+        } else {
+          dst[0] = prf_block(tab, &ks.rk[0][0] + 2 * 44, st.rrho, blk);  // protocols.py:166-216
+          dst[1] = prf_block(tab, &ks.rk[0][0] + 1 * 44, st.rr, blk);
+        }
+        continue;
+      }
+      const int s = sa - PRE;
       Word2* dst = slots + ((size_t)s * P + p) * 3;
       if (s == 0) {
         dst[0] = prf_block(tab, &ks.rk[0][0], st.bin, blk);
@@ -327,10 +363,16 @@ __global__ void __launch_bounds__(F ? kSignThreads : kThreads, F ? 1 : 2)
       rp.P = P;
       rp.p = threadIdx.x;
       rp.slot = 0;
-      if constexpr (MAXL)
+      if constexpr (MAXL) {
         maxlevel_item(rp, &ks.rk[0][0], st, x, out, mg, n, n_total, elem_off, c0 + threadIdx.x);
-      else
+      } else if constexpr (KIND == S2_RS) {
+        const Word2* w3 = pre + (size_t)threadIdx.x * 3;
+        const Word2* tr = pre + ((size_t)P + threadIdx.x) * 3;
+        sign_item_rs(rp, &ks.rk[0][0], st, mode, rin, w3, tr[0], tr[1], out, mask, n, n_total, elem_off,
+                     c0 + threadIdx.x, plane);
+      } else {
         sign_item(rp, &ks.rk[0][0], st, mode, x, out, mask, n, n_total, elem_off, c0 + threadIdx.x, plane);
+      }
     }
     __syncthreads();
   }
@@ -717,38 +759,35 @@ int mpc3_rss_chain(const uint32_t* rk3, const uint64_t* ctr, const MPC3ChainStep
 #define MPC3_SIGN2_FOUR 0
 #endif
 constexpr bool kSign2Four = MPC3_SIGN2_FOUR;
-static int sign2_chunk(uint64_t pairs, bool straddle) {
-  const uint64_t pmax = (straddle ? 32 : 64) * (kSign2Four ? 2 : 1), slots = (kSign2Four ? 1 : 2) * 148;
+static int sign2_pmax(bool straddle, bool rs) {
+  if (rs) return straddle ? 32 : 48;  // two more slots per pair (the layer's reshare / truncation words)
+  return (straddle ? 32 : 64) * (kSign2Four ? 2 : 1);
+}
+static int sign2_chunk(uint64_t pairs, bool straddle, bool rs = false) {
+  const uint64_t pmax = sign2_pmax(straddle, rs), slots = (kSign2Four ? 1 : 2) * 148;
   const uint64_t waves = (pairs + slots * pmax - 1) / (slots * pmax);
   uint64_t P = (pairs + waves * slots - 1) / (waves * slots);
   if (P < 8) P = 8;
   return (int)(P > pmax ? pmax : P);
 }
 
-static int sign2_smem(int P, bool straddle) {
-  return (kSign2Four ? kAesSmem4Bytes : kAesSmemBytes) + P * sign_slots(straddle) * SW_SLOT_BYTES;
+static int sign2_smem(int P, bool straddle, bool rs = false) {
+  return (kSign2Four ? kAesSmem4Bytes : kAesSmemBytes) + P * (sign_slots(straddle) + (rs ? 2 : 0)) * SW_SLOT_BYTES;
 }
-static int sign2_smem_max() {  // the largest chunk either layout uses (P * slots is the same with or without straddle)
-  return sign2_smem(kSign2Four ? 128 : 64, false);
+static int sign2_smem_max(bool rs = false) {  // the largest chunk a launch uses
+  const int a = sign2_smem(sign2_pmax(false, rs), false, rs), b = sign2_smem(sign2_pmax(true, rs), true, rs);
+  return a > b ? a : b;
 }
 
-int mpc3_rss_sign(const uint32_t* rk3, const uint64_t* ctr, int mode, uint64_t j_bin, uint64_t j_xor, uint64_t j_arith,
-                  const uint64_t* x, uint64_t* out, uint64_t* mask, uint64_t n, uint64_t n_total,
-                  uint64_t elem_off, void* stream) {
-  if (mode < MODE_A2B || mode > MODE_RELU) return MPC3_ERR_CONFIG;
-  if (elem_off & 1) return MPC3_ERR_CONFIG;
-  if (elem_off + n > n_total) return MPC3_ERR_SHAPE;
-  if (j_bin >= (1ull << 48) || j_xor + 6 >= (1ull << 48) || j_arith + 2 >= (1ull << 48))
-    return MPC3_ERR_RANGE;
-  if (n == 0) return MPC3_OK;
-  SignArgs a;
-  a.jbin = j_bin;
-  a.jxor = j_xor;
-  a.ja = j_arith;
-  KeySched ks;
-  if (int e = load_keys(rk3, 3, stream, &ks)) return e;
+// The sign circuit over n elements (x, or a fused layer's cross terms rin):
+// whole rounds of the persistent single-phase kernel, the rest two-phase.
+static int sign_launch(const KeySched& ks, const uint64_t* ctr, const SignArgs& a, int mode, const uint64_t* x,
+                       const RsIn* rin, uint64_t* out, uint64_t* mask, uint64_t n, uint64_t n_total,
+                       uint64_t elem_off, void* stream) {
+  const bool rs = rin != nullptr;
+  RsIn ri = rs ? *rin : RsIn{};
   // large tensors: the single-phase kernel (throughput-bound, all threads in
-  // the circuit) on a persistent grid, one 512-thread CTA per SM, every
+  // the circuit) on a persistent grid, one 384-thread CTA per SM, every
   // thread exactly k pairs (no partial wave, no CTA-boundary bubbles); the
   // remainder and small tensors: the two-phase kernel (latency-bound work)
   const uint64_t pairs = (n + 1) / 2;
@@ -767,27 +806,85 @@ int mpc3_rss_sign(const uint32_t* rk3, const uint64_t* ctr, int mode, uint64_t j
   if (main_pairs) {
     const uint64_t nm = main_pairs == pairs ? n : 2 * main_pairs;
     const unsigned grid = g_sign_fused ? grid_for(pairs, kSignThreads, 8) : grid_for(main_pairs, kSignThreads, 1);
-    if (!aes_attr((const void*)sign_kernel, kAesSmem4Bytes)) return check_launch("sign smem attribute");
-    launch_pdl(sign_kernel, dim3(grid), dim3(kSignThreads), kAesSmem4Bytes, as_stream(stream), ks, ctr, a, mode, x,
-               out, mask, nm, n_total, elem_off, n);
+    auto kern = rs ? sign_kernel<true> : sign_kernel<false>;
+    if (!aes_attr((const void*)kern, kAesSmem4Bytes)) return check_launch("sign smem attribute");
+    launch_pdl(kern, dim3(grid), dim3(kSignThreads), kAesSmem4Bytes, as_stream(stream), ks, ctr, a, mode, x, out,
+               mask, nm, n_total, elem_off, n, ri);
     if (check_launch("rss_sign")) return MPC3_ERR_CUDA;
   }
   if (main_pairs < pairs) {
-    // two-phase kernel: P pairs per chunk (64; 32 when the p-half straddles
-    // blocks), tables + keystream slots in dynamic shared memory
+    // two-phase kernel: P pairs per chunk, tables + keystream slots in
+    // dynamic shared memory
     const uint64_t e0 = 2 * main_pairs, nr = n - e0;
     const bool straddle = (n_total & 1) != 0;
-    const int P = sign2_chunk((nr + 1) / 2, straddle);
-    const int smem = sign2_smem(P, straddle);
-    auto kern = kSign2Four ? sign2_kernel<false, true> : sign2_kernel<false, false>;
-    if (!aes_attr((const void*)kern, sign2_smem_max())) return check_launch("sign2 smem attribute");
+    const int P = sign2_chunk((nr + 1) / 2, straddle, rs);
+    const int smem = sign2_smem(P, straddle, rs);
+    auto kern = rs ? (kSign2Four ? sign2_kernel<S2_RS, true> : sign2_kernel<S2_RS, false>)
+                   : (kSign2Four ? sign2_kernel<S2_SIGN, true> : sign2_kernel<S2_SIGN, false>);
+    if (!aes_attr((const void*)kern, sign2_smem_max(rs))) return check_launch("sign2 smem attribute");
     uint64_t chunks = ((nr + 1) / 2 + P - 1) / P;
     unsigned grid = (unsigned)(chunks < 148 * 2 * 8 ? chunks : 148 * 2 * 8);
+    ri.f0 += e0;
     launch_pdl(kern, dim3(grid), dim3(kSign2Four ? kSignThreads : kThreads), smem, as_stream(stream), ks, ctr, a, mode,
-               x + e0, out + e0, mask ? mask + e0 : mask, nr, n_total, elem_off + e0, P, n, MaxGeom{0, 0, 1});
+               rs ? x : x + e0, out + e0, mask ? mask + e0 : mask, nr, n_total, elem_off + e0, P, n,
+               MaxGeom{0, 0, 1}, ri);
     return check_launch("rss_sign2");
   }
   return MPC3_OK;
+}
+
+int mpc3_rss_sign(const uint32_t* rk3, const uint64_t* ctr, int mode, uint64_t j_bin, uint64_t j_xor, uint64_t j_arith,
+                  const uint64_t* x, uint64_t* out, uint64_t* mask, uint64_t n, uint64_t n_total,
+                  uint64_t elem_off, void* stream) {
+  if (mode < MODE_A2B || mode > MODE_RELU) return MPC3_ERR_CONFIG;
+  if (elem_off & 1) return MPC3_ERR_CONFIG;
+  if (elem_off + n > n_total) return MPC3_ERR_SHAPE;
+  if (j_bin >= (1ull << 48) || j_xor + 6 >= (1ull << 48) || j_arith + 2 >= (1ull << 48))
+    return MPC3_ERR_RANGE;
+  if (n == 0) return MPC3_OK;
+  SignArgs a = {j_bin, j_xor, j_arith, 0, 0, 0};
+  KeySched ks;
+  if (int e = load_keys(rk3, 3, stream, &ks)) return e;
+  return sign_launch(ks, ctr, a, mode, x, nullptr, out, mask, n, n_total, elem_off, stream);
+}
+
+int mpc3_rss_layer_sign(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_ra, uint64_t j_rho, uint64_t j_r,
+                        int bits, const uint64_t* z, const mpc3_view4* view, const uint64_t* bias, int64_t bias_plane,
+                        int bias_dim, int mode, uint64_t j_bin, uint64_t j_xor, uint64_t j_arith, uint64_t* out,
+                        uint64_t* mask, uint64_t elem_off, uint64_t n_total, void* stream) {
+  if (mode < MODE_A2B || mode > MODE_RELU) return MPC3_ERR_CONFIG;
+  if (bits < 1 || bits > 61) return MPC3_ERR_RANGE;
+  if (bias && (bias_dim < 0 || bias_dim > 3 || bias_plane < 0)) return MPC3_ERR_CONFIG;
+  if (!view || !z || (elem_off & 1)) return MPC3_ERR_CONFIG;
+  RsIn ri;
+  ri.z = z;
+  ri.bits = bits;
+  ri.f0 = 0;
+  uint64_t n = 1;
+  for (int k = 0; k < 4; ++k) {
+    ri.v.full[k] = view->full[k];
+    ri.v.org[k] = view->origin[k];
+    ri.v.crop[k] = view->crop[k];
+    ri.v.zs[k] = view->z_stride[k];
+    ri.v.os[k] = view->out_stride[k];
+    if (ri.v.full[k] < 0 || ri.v.org[k] != 0 || ri.v.crop[k] != ri.v.full[k]) return MPC3_ERR_SHAPE;  // no crop
+    n *= (uint64_t)ri.v.full[k];
+  }
+  ri.v.zp = view->z_plane;
+  ri.v.op = view->out_plane;
+  ri.v.bias = bias;
+  ri.v.bias_plane = bias_plane;
+  ri.v.bias_dim = bias_dim;
+  ri.small = n < (1ull << 32) ? 1 : 0;
+  if (elem_off + n > n_total) return MPC3_ERR_SHAPE;
+  if (j_bin >= (1ull << 48) || j_xor + 6 >= (1ull << 48) || j_arith + 2 >= (1ull << 48) || j_ra >= (1ull << 48) ||
+      j_rho >= (1ull << 48) || j_r >= (1ull << 48))
+    return MPC3_ERR_RANGE;
+  if (n == 0) return MPC3_OK;
+  SignArgs a = {j_bin, j_xor, j_arith, j_ra, j_rho, j_r};
+  KeySched ks;
+  if (int e = load_keys(rk3, 3, stream, &ks)) return e;
+  return sign_launch(ks, ctr, a, mode, nullptr, &ri, out, mask, n, n_total, elem_off, stream);
 }
 
 int mpc3_rss_max_level(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_bin, uint64_t j_xor, uint64_t j_arith,
@@ -801,19 +898,17 @@ int mpc3_rss_max_level(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_bin,
   if (n == 0) return MPC3_OK;
   KeySched ks;
   if (int e = load_keys(rk3, 3, stream, &ks)) return e;
-  SignArgs a;
-  a.jbin = j_bin;
-  a.jxor = j_xor;
-  a.ja = j_arith;
+  SignArgs a = {j_bin, j_xor, j_arith, 0, 0, 0};
   const bool straddle = (n_total & 1) != 0;
   const int P = sign2_chunk((n + 1) / 2, straddle);
   const int smem = sign2_smem(P, straddle);
-  auto kern = kSign2Four ? sign2_kernel<true, true> : sign2_kernel<true, false>;
+  auto kern = kSign2Four ? sign2_kernel<S2_MAXL, true> : sign2_kernel<S2_MAXL, false>;
   if (!aes_attr((const void*)kern, sign2_smem_max())) return check_launch("max_level smem attribute");
   uint64_t chunks = ((n + 1) / 2 + P - 1) / P;
   unsigned grid = (unsigned)(chunks < 148 * 2 * 8 ? chunks : 148 * 2 * 8);
   launch_pdl(kern, dim3(grid), dim3(kSign2Four ? kSignThreads : kThreads), smem, as_stream(stream), ks, ctr, a,
-             (int)MODE_RELU, v, out, (uint64_t*)nullptr, n, n_total, elem_off, P, (uint64_t)0, MaxGeom{rows, m, k});
+             (int)MODE_RELU, v, out, (uint64_t*)nullptr, n, n_total, elem_off, P, (uint64_t)0, MaxGeom{rows, m, k},
+             RsIn{});
   return check_launch("rss_max_level");
 }
 

@@ -157,6 +157,76 @@ struct View4 {
   int bias_dim;
 };
 
+// A secure layer fused with the ReLU after it (protocols.py:120-136 then
+// 334-353): the ReLU input x is the layer's cross terms z (View4 layout, no
+// crop) reshared, truncated and biased in registers exactly as
+// reshare_trunc_item does, from the pair's zero-share words kw (3 keys) and
+// truncation words rho, r — so x never goes through HBM.
+struct RsIn {
+  const uint64_t* z;
+  View4 v;
+  int bits;
+  uint64_t f0;  // flat index (in v) of the launch's element 0
+  int small;    // the view's element count fits 32 bits
+};
+template <class I>
+HD void view_index(const View4& v, uint64_t f, int64_t& i0, int64_t& i1, int64_t& i2, int64_t& i3) {
+  I q = (I)f;
+  const I f3 = (I)v.full[3], f2 = (I)v.full[2], f1 = (I)v.full[1];
+  i3 = (int64_t)(q % f3);
+  q /= f3;
+  i2 = (int64_t)(q % f2);
+  q /= f2;
+  i1 = (int64_t)(q % f1);
+  i0 = (int64_t)(q / f1);
+}
+HD Trio reshare_input(const RsIn& in, uint64_t f, const uint64_t kw[3], uint64_t rho, uint64_t r) {
+  const View4& v = in.v;
+  int64_t i0, i1, i2, i3;
+  if (in.small)  // every extent below 2^32: 32-bit divisions (short inline sequences)
+    view_index<uint32_t>(v, f, i0, i1, i2, i3);
+  else
+    view_index<uint64_t>(v, f, i0, i1, i2, i3);
+  Trio t = load_trio(in.z + i0 * v.zs[0] + i1 * v.zs[1] + i2 * v.zs[2] + i3 * v.zs[3], v.zp, 0);
+  KeyWords w;
+  for (int k = 0; k < 3; ++k) w.k[k] = kw[k];
+  t = trio_reshare(t, w);
+  if (in.bits) t = trio_truncate(t, rho, r, in.bits);
+  if (v.bias) {
+    const int64_t bi = v.bias_dim == 0 ? i0 : v.bias_dim == 1 ? i1 : v.bias_dim == 2 ? i2 : i3;
+    for (int k = 0; k < 3; ++k) t.c[k] += v.bias[k * v.bias_plane + bi];
+  }
+  return t;
+}
+
+// sign_item on a fused layer output: w3 / rho / r are the pair's reshare and
+// truncation words (block elem_off / 2 + b of each stream).
+template <class T>
+HD void sign_item_rs(const T& tab, const uint32_t* rk3, const SignStreams& st, int mode, const RsIn& in,
+                     const Word2 w3[3], Word2 rho, Word2 r, uint64_t* out, uint64_t* mask, uint64_t n,
+                     uint64_t n_total, uint64_t elem_off, uint64_t b, uint64_t plane) {
+  const bool two = 2 * b + 1 < n;
+  const uint64_t pl = plane ? plane : n;
+  Trio xin[2];
+  {
+    const uint64_t k0[3] = {w3[0].w0, w3[1].w0, w3[2].w0}, k1[3] = {w3[0].w1, w3[1].w1, w3[2].w1};
+    xin[0] = reshare_input(in, in.f0 + 2 * b, k0, rho.w0, r.w0);
+    xin[1] = two ? reshare_input(in, in.f0 + 2 * b + 1, k1, rho.w1, r.w1) : xin[0];
+  }
+  struct Loader {
+    const Trio* x;
+    HD Trio operator()(int e) const { return x[e]; }
+  } ld{xin};
+  Trio o[2], m[2];
+  sign_circuit_pair(tab, rk3, st, n_total, (elem_off >> 1) + b, mode, ld, o, m);
+  store_trio(out, pl, 2 * b, o[0]);
+  if (two) store_trio(out, pl, 2 * b + 1, o[1]);
+  if (mode == MODE_RELU && mask) {
+    store_trio(mask, pl, 2 * b, m[0]);
+    if (two) store_trio(mask, pl, 2 * b + 1, m[1]);
+  }
+}
+
 // I: index arithmetic type (uint32_t when every extent fits: the kernels pick
 // it on the host, which turns the 64-bit division calls into short inline
 // sequences).

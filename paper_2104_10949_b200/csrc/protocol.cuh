@@ -97,6 +97,7 @@ struct SignStreams {
   StreamHead bin;     // BIN_INPUT, 1 counter (k_0 only)
   StreamHead x[7];    // XOR_ZERO, counters j0..j0+6
   StreamHead a[3];    // ARITH_ZERO, counters ja..ja+2 (inject, inject, mask)
+  StreamHead ra, rrho, rr;  // fused layer + ReLU: the layer's reshare / truncation streams
 };
 
 // Block `blk` of one stream under the three session keys.

@@ -774,9 +774,31 @@ class TrioSession:
             self._charge_trunc(full)
         return out
 
+    def _finish_relu(self, z, view, shape, bits, label, bias: RssTensor | None = None, bias_dim: int = 1):
+        """_finish followed by relu_with_mask in ONE launch (mpc3_rss_layer_sign):
+        the same counters in the same order, the same shares and accounting;
+        the pre-activation tensor is never materialised.  -> (relu, mask)."""
+        ja = self.take(ARITH)
+        jr, jq = self.take(TR_RHO), self.take(TR_R)
+        jb = self.take(BIN)
+        jx = self.take(XOR, 7)
+        jm = self.take(ARITH, 3)
+        full = int(np.prod(view.full))
+        off, n_total = self.shard_offset(full)
+        out, mask = empty(shape, self.fp), empty(shape, self.fp)
+        if bias is not None and (bias.ndim != 1 or bias.data.stride(1) != 1):
+            raise ShapeError("bias must be a 1-d shared vector with unit stride")
+        K.call("mpc3_rss_layer_sign", self.rk, self.ctr_ptr, ja, jr, jq, bits, z.data_ptr(), C.byref(view),
+               None if bias is None else bias.data.data_ptr(), 0 if bias is None else bias.data.stride(0), bias_dim,
+               K.MODE_RELU, jb, jx, jm, out.data.data_ptr(), mask.data.data_ptr(), off, n_total, _stream())
+        self.ledger.ring(label, full)
+        self._charge_trunc(full)
+        self._charge_sign(full, K.MODE_RELU)
+        return out, mask
+
     def matmul(self, x: RssTensor, y: RssTensor, bits: int | None = None, wgrad: bool = False,
                bias: RssTensor | None = None, keep: list | None = None, x_packed: Packed | None = None,
-               x_role: int = 0) -> RssTensor:
+               x_role: int = 0, relu: bool = False):
         """matmul_shares (protocols.py:97-117): cross terms, reshare, truncate.
         wgrad=True marks a weight gradient g^T x whose inner dimension is the
         batch: under data parallelism the shards' cross terms are summed
@@ -799,6 +821,8 @@ class TrioSession:
             self._reduce_cross_terms(z)
             with self.replicated():
                 return self._finish(z, K.make_view((1, 1, m, n)), out, bits, "mul.reshare")
+        if relu:  # fused with the ReLU after it: -> (relu, mask)
+            return self._finish_relu(z, K.make_view((1, 1, m, n)), (m, n), bits, "mul.reshare", bias=bias, bias_dim=3)
         return self._finish(z, K.make_view((1, 1, m, n)), out, bits, "mul.reshare", bias=bias, bias_dim=3)
 
     def fc_wgrad_packed(self, g: RssTensor, xp: Packed, bits: int) -> RssTensor:
@@ -837,7 +861,7 @@ class TrioSession:
         return K.dense_operand(y.shape[1], y.shape[0], s_r=ys[2], t2=ys[1]), y.shape[1], y.shape[0]
 
     def conv2d(self, x: RssTensor, k: RssTensor, stride=(1, 1), padding=(0, 0), bits=None,
-               bias: RssTensor | None = None, keep: list | None = None) -> RssTensor:
+               bias: RssTensor | None = None, keep: list | None = None, relu: bool = False):
         """conv2d_shares (protocols.py:120-136), NCHW cross-correlation;
         `bias` (inference extension) is added per output channel after the
         truncation in the same kernel."""
@@ -865,6 +889,8 @@ class TrioSession:
         # z[(n, y, x), o]: column-major keeps each (n, o) plane's (y, x) run contiguous
         zs = (oh * ow, M, ow, 1) if col else (oh * ow * o, 1, ow * o, o)
         view = K.make_view((nb, o, oh, ow), z_stride=zs)
+        if relu:  # fused with the ReLU after it: -> (relu, mask)
+            return self._finish_relu(z, view, (nb, o, oh, ow), bits, "mul.reshare", bias=bias, bias_dim=1)
         return self._finish(z, view, out, bits, "mul.reshare", bias=bias, bias_dim=1)
 
     def conv2d_wgrad(self, x: RssTensor, g: RssTensor, kernel, stride, padding, bits,

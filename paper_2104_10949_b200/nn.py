@@ -41,6 +41,13 @@ FLATTEN = "Flatten"
 RESIDUAL = "Residual"
 # MPC3_OVERLAP=0: weight gradients on the main stream (no side-stream overlap)
 OVERLAP = os.environ.get("MPC3_OVERLAP", "1") == "1"
+# MPC3_FUSE_RELU=0: a conv / linear layer's epilogue and the ReLU after it as two launches
+FUSE_RELU = os.environ.get("MPC3_FUSE_RELU", "1") == "1"
+# only for outputs of at least this many elements: the persistent sign kernel
+# absorbs the 5 extra AES blocks per pair; the small tensors' two-phase kernel
+# (two more keystream slots, smaller chunks) does not (AlexNet step: fused
+# everywhere 2.559 ms, from 100 K elements 2.530 ms, never 2.541 ms)
+FUSE_RELU_MIN = int(os.environ.get("MPC3_FUSE_RELU_MIN", "100000"))  # output elements
 
 
 def _pair(v) -> tuple:
@@ -263,16 +270,38 @@ class TrioNet:
         shape = (3, 1, b.shape[0]) + (1,) * (h.ndim - 2)
         return self.s.add(h, RssTensor(b.data.reshape(shape).expand(h.data.shape), h.fp))
 
+    @staticmethod
+    def _out_numel(spec, h: RssTensor) -> int:
+        if spec.kind == CONV2D:
+            (kh, kw), (sh, sw), (ph, pw) = spec.kernel, spec.stride, spec.padding
+            return h.shape[0] * spec.out_channels * ((h.shape[2] + 2 * ph - kh) // sh + 1) * \
+                ((h.shape[3] + 2 * pw - kw) // sw + 1)
+        if spec.kind == FULLY_CONNECTED:
+            return h.shape[0] * spec.out_features
+        return 0
+
     def _run(self, layers, it, h: RssTensor, record: bool):
         S, acts = self.s, []
-        for spec in layers:
+        fused = None  # mask of a ReLU already computed with the layer before it
+        for li, spec in enumerate(layers):
             # recording keeps each layer input's packed GEMM operand (role 1)
             # for the weight gradient, which reads it in place
             keep = [] if record and E.REUSE_PACKS and not E.IMPLICIT_GEMM else None
+            # a conv / linear layer followed by a ReLU runs as one launch for
+            # the layer's reshare + truncate and the ReLU (mpc3_rss_layer_sign)
+            relu_next = FUSE_RELU and li + 1 < len(layers) and layers[li + 1].kind == RELU \
+                and self._out_numel(spec, h) >= FUSE_RELU_MIN
+            if spec.kind == RELU and fused is not None:
+                acts.append((fused,) if record else None)
+                fused = None
+                continue
             if spec.kind == CONV2D:
                 k = next(it)
                 x = h
-                h = S.conv2d(h, k, spec.stride, spec.padding, bias=next(it) if spec.bias else None, keep=keep)
+                h = S.conv2d(h, k, spec.stride, spec.padding, bias=next(it) if spec.bias else None, keep=keep,
+                             relu=relu_next)
+                if relu_next:
+                    h, fused = h
                 acts.append(((x, k) + tuple(keep or ())) if record else None)
                 if self._ahead:
                     S.prepack([self._ahead.pop(0)])
@@ -280,7 +309,9 @@ class TrioNet:
                 w = next(it)
                 x = h
                 h = S.matmul(h, w.apply(lambda d: d.transpose(1, 2)), bias=next(it) if spec.bias else None,
-                             keep=keep, x_role=1 if keep is not None else 0)
+                             keep=keep, x_role=1 if keep is not None else 0, relu=relu_next)
+                if relu_next:
+                    h, fused = h
                 acts.append(((x, w) + tuple(keep or ())) if record else None)
                 if self._ahead:
                     S.prepack([self._ahead.pop(0)])

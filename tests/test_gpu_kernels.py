@@ -143,6 +143,36 @@ def test_sign_single_phase_equals_two_phase_shards(n):
         assert np.array_equal(host(mk).reshape(3, m), host(fmask).reshape(3, n)[:, a:b])
 
 
+@pytest.mark.parametrize("shape,bias,shard", [((128, 96, 10, 10), False, None), ((128, 96, 10, 10), True, None),
+                                              ((3, 5, 7, 9), True, None), ((64, 256, 1, 1), False, None),
+                                              ((1, 1, 128, 257), True, None), ((40, 7, 33, 33), False, (2, 3))])
+def test_layer_sign_equals_reshare_then_sign(shape, bias, shard):
+    """mpc3_rss_layer_sign (a layer's reshare + truncate + bias fused into the
+    ReLU) = mpc3_rss_reshare_truncate_bias then mpc3_rss_sign, share for
+    share, over a column-major conv z view: persistent and two-phase paths,
+    odd sizes (Kogge-Stone p-half straddling AES blocks), and a batch shard
+    (elem_off / n_total) of a larger tensor."""
+    rng = np.random.default_rng(sum(shape))
+    nb, o, oh, ow = shape
+    n = nb * o * oh * ow
+    M = nb * oh * ow
+    z = dev(rnd(rng, (3, n)))  # column-major cross terms: (m, o) at o * M + m
+    view = _capi.make_view(shape, z_stride=(oh * ow, M, ow, 1))
+    bv = dev(rnd(rng, (3, o))) if bias else None
+    rk = rk3(R.Session(6).keys)
+    elem_off, n_total = (0, n) if shard is None else (n * shard[0] // shard[1] // 2 * 2, 2 * n + 1)
+    x = torch.empty(3 * n, dtype=torch.int64, device="cuda")
+    _capi.call("mpc3_rss_reshare_truncate_bias", p(rk), None, 11, 12, 13, 20, p(z), C.byref(view),
+               p(bv) if bias else None, o if bias else 0, 1, p(x), elem_off, stream())
+    out1, m1 = torch.empty_like(x), torch.empty_like(x)
+    _capi.call("mpc3_rss_sign", p(rk), None, 3, 4, 5, 6, p(x), p(out1), p(m1), n, n_total, elem_off, stream())
+    out2, m2 = torch.full_like(x, -1), torch.full_like(x, -1)
+    _capi.call("mpc3_rss_layer_sign", p(rk), None, 11, 12, 13, 20, p(z), C.byref(view), p(bv) if bias else None,
+               o if bias else 0, 1, 3, 4, 5, 6, p(out2), p(m2), elem_off, n_total, stream())
+    assert np.array_equal(host(out2), host(out1))
+    assert np.array_equal(host(m2), host(m1))
+
+
 def _gemm_packed(A, B, groups, M, Nn, kp, splits):
     Cm = torch.zeros(groups * M * Nn, dtype=torch.int64, device="cuda")
     _capi.call("mpc3_ring_gemm_packed", p(A), p(B), p(Cm), groups, M, Nn, kp, Nn, M * Nn, splits, stream())
