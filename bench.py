@@ -248,16 +248,23 @@ def run_b200(args, ws, rank, local):
     instrument = {"on": False, "k": 0}
 
     def traced_call(name, *a):
-        if instrument["on"] and name in ("mpc3_ring_pack", "mpc3_ring_pack_halves") and a[3] in (0, 1):
+        if instrument["on"] and name in ("mpc3_ring_pack", "mpc3_ring_pack_halves", "mpc3_ring_pack_halves_z") \
+                and a[3] in (0, 1):
             instrument["k"] = int(a[2]._obj.k)  # logical K of the cross-term operand (inner length 2K)
-        if instrument["on"] and name in ("mpc3_rss_sign", "mpc3_ring_gemm_auto", "mpc3_ring_gemm_t"):
+        if instrument["on"] and name in ("mpc3_rss_sign", "mpc3_rss_layer_sign", "mpc3_ring_gemm_auto",
+                                         "mpc3_ring_gemm_auto_z", "mpc3_ring_gemm_t", "mpc3_ring_gemm_t_z"):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             counting_call(name, *a)
             e1.record()
-            if name == "mpc3_rss_sign":
-                sign_events.append((e0, e1, int(a[9])))
-            elif name == "mpc3_ring_gemm_t":  # transposed operands: the contraction is an MN operand's source rows
+            if name == "mpc3_rss_sign":  # 23 AES blocks per element
+                sign_events.append((e0, e1, int(a[9]), 23.0 * int(a[9])))
+            elif name == "mpc3_rss_layer_sign":  # + the fused layer epilogue's 2.5 blocks per element
+                n_el = 1
+                for d in a[7]._obj.full:
+                    n_el *= int(d)
+                sign_events.append((e0, e1, n_el, 25.5 * n_el))
+            elif name.startswith("mpc3_ring_gemm_t"):  # transposed operands: the contraction is an MN operand's rows
                 groups, M, N, kc_half = int(a[11]), int(a[12]), int(a[13]), int(a[14])
                 rows = int(a[2]) if a[1] else (int(a[7]) if a[6] else kc_half)
                 gemm_events.append((e0, e1, 72 * groups * M * N * 2 * rows))
@@ -383,11 +390,13 @@ def run_b200(args, ws, rank, local):
                             "(streams serialised, enqueued behind a GPU spin: the events bracket each kernel alone)"}
     # secondary bound: the nonlinear layers are AES-bound (23 AES-128 blocks
     # per ReLU element); peak = the standalone AES-CTR keystream kernel's rate
-    sign_ms = sum(a.elapsed_time(c) for a, c, _ in sign_events)
-    sign_elems = sum(n for _, _, n in sign_events)
+    sign_ms = sum(a.elapsed_time(c) for a, c, _, _ in sign_events)
+    sign_elems = sum(n for _, _, n, _ in sign_events)
+    sign_blocks = sum(bl for _, _, _, bl in sign_events)
     aes_peak = _aes_peak_gblocks()
-    aes_rate = 23 * sign_elems / (sign_ms / 1e3) / 1e9 if sign_ms else None
-    roofline["secondary"] = {"kernel": "sign circuit (a2b + Kogge-Stone + bit_inject + ReLU, AES-CTR inline)",
+    aes_rate = sign_blocks / (sign_ms / 1e3) / 1e9 if sign_ms else None
+    roofline["secondary"] = {"kernel": "sign circuit (a2b + Kogge-Stone + bit_inject + ReLU, AES-CTR inline; "
+                                       "with the layer epilogue fused for large outputs: mpc3_rss_layer_sign)",
                              "bound": "aes", "achieved": aes_rate, "peak": aes_peak, "unit": "G AES blocks/s",
                              "frac": aes_rate / aes_peak if aes_rate and aes_peak else None,
                              "share_of_step": sign_ms / max(total_ms / args.steps, 1e-9),
