@@ -157,6 +157,16 @@ int mpc3_rss_max_level(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_bin,
                        const uint64_t* v, uint64_t* out, uint64_t rows, uint64_t m, uint64_t elem_off,
                        uint64_t n_total, void* stream);
 
+/* The whole max_tree (protocols.py:356-380) of rows x m in ONE launch:
+ * `levels` = the number of halvings of m down to 1; level l uses BIN
+ * j_bin[l], XOR_ZERO j_xor[l]..+6 and ARITH_ZERO j_arith[l]..+2 (host
+ * arrays), exactly the counters of mpc3_rss_max_level per level.  scratch:
+ * 2 * 3 * rows * ceil(m/2) words; out: (rows, 1).  row_off / rows_total: a
+ * batch shard of the rows (row_off even). */
+int mpc3_rss_max_tree(const uint32_t* rk3, const uint64_t* ctr, int levels, const uint64_t* j_bin,
+                      const uint64_t* j_xor, const uint64_t* j_arith, const uint64_t* v, uint64_t* scratch,
+                      uint64_t* out, uint64_t rows, uint64_t m, uint64_t row_off, uint64_t rows_total, void* stream);
+
 /* Fused elementwise chain over a per-element trio z (starts as x), the chain
  * input x and a temporary t; replaces the launch-per-call sequences of
  * exp_approx (add_const + squarings, protocols.py:414-424) and reciprocal

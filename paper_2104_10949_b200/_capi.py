@@ -161,6 +161,7 @@ _SIGS = {
     "mpc3_rss_truncate": (C.c_int, [_P, _P, _U64, _U64, C.c_int, _P, _P, _U64, _U64, _P]),
     "mpc3_rss_mul_truncate": (C.c_int, [_P, _P, _U64, _U64, _U64, C.c_int, _P, _P, _P, _U64, _U64, _P]),
     "mpc3_rss_sign": (C.c_int, [_P, _P, C.c_int, _U64, _U64, _U64, _P, _P, _P, _U64, _U64, _U64, _P]),
+    "mpc3_rss_max_tree": (C.c_int, [_P, _P, C.c_int, _P, _P, _P, _P, _P, _P, _U64, _U64, _U64, _U64, _P]),
     "mpc3_rss_layer_sign": (C.c_int, [_P, _P, _U64, _U64, _U64, C.c_int, _P, C.POINTER(View4), _P, _I64, C.c_int,
                                       C.c_int, _U64, _U64, _U64, _P, _P, _U64, _U64, _P]),
     "mpc3_rss_sgd_multi": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, _U64, _P]),

@@ -293,6 +293,35 @@ HD int sign_slots(bool straddle) { return straddle ? 21 : 16; }
 
 // F: four-table AES (one 384-thread CTA per SM, up to 128 pairs per chunk)
 // or two-table (two 256-thread CTAs per SM, up to 64 pairs each).
+// Keystream slot s (circuit call order, see above) of the pair at PRF block
+// blk: one three-key block, or BIN's single block.
+template <class TT>
+DEV void sign_slot_fill(const TT& tab, const uint32_t* rk, const SignStreams& st, int s, uint64_t blk,
+                        uint64_t n_total, int L, Word2* dst) {
+  if (s == 0) {
+    dst[0] = prf_block(tab, rk, st.bin, blk);
+    return;
+  }
+  StreamHead h;
+  uint64_t b = blk;
+  if (s == 1) {
+    h = st.x[0];
+  } else if (s < 2 + 5 * L) {
+    const int lvl = (s - 2) / L + 1, r = (s - 2) % L;
+    h = st.x[lvl];
+    if (r > 0) b = ((n_total + 2 * blk) >> 1) + (r - 1);  // p-half words n_total + 2 blk (+1)
+  } else if (s == 2 + 5 * L) {
+    h = st.x[6];
+  } else {
+    h = st.a[s - 3 - 5 * L];
+  }
+  Word2 w[3];
+  prf_block3(tab, rk, h, b, w);
+  dst[0] = w[0];
+  dst[1] = w[1];
+  dst[2] = w[2];
+}
+
 // KIND: 0 sign / ReLU of x; 1 one max_tree level; 2 fused layer + ReLU (two
 // leading slots hold the pair's reshare words (3 keys) and truncation words
 // (rho, r); the circuit's slots follow).
@@ -332,29 +361,7 @@ __global__ void __launch_bounds__(F ? kSignThreads : kThreads, F ? 1 : 2)
         continue;
       }
       const int s = sa - PRE;
-      Word2* dst = slots + ((size_t)s * P + p) * 3;
-      if (s == 0) {
-        dst[0] = prf_block(tab, &ks.rk[0][0], st.bin, blk);
-        continue;
-      }
-      StreamHead h;
-      uint64_t b = blk;
-      if (s == 1) {
-        h = st.x[0];
-      } else if (s < 2 + 5 * L) {
-        const int lvl = (s - 2) / L + 1, r = (s - 2) % L;
-        h = st.x[lvl];
-        if (r > 0) b = ((n_total + 2 * blk) >> 1) + (r - 1);  // p-half words n_total + 2 blk (+1)
-      } else if (s == 2 + 5 * L) {
-        h = st.x[6];
-      } else {
-        h = st.a[s - 3 - 5 * L];
-      }
-      Word2 w[3];
-      prf_block3(tab, &ks.rk[0][0], h, b, w);
-      dst[0] = w[0];
-      dst[1] = w[1];
-      dst[2] = w[2];
+      sign_slot_fill(tab, &ks.rk[0][0], st, s, blk, n_total, L, slots + ((size_t)s * P + p) * 3);
     }
     __syncthreads();
     if (threadIdx.x < P && c0 + threadIdx.x < npairs) {
@@ -383,6 +390,71 @@ __global__ void __launch_bounds__(F ? kSignThreads : kThreads, F ? 1 : 2)
            r += (uint64_t)gridDim.x * blockDim.x)
         store_trio(out, po, r * mo + mg.k, load_trio(x, pv, r * mg.m + mg.m - 1));
     }
+  }
+}
+
+// The whole max_tree (protocols.py:356-380) in one launch.  Rows are
+// independent, so each CTA takes R rows (R even: the rows' level tensors then
+// start on AES-block boundaries) through every level, two-phase per level as
+// sign2_kernel (keystream slots, then one thread per pair runs the circuit),
+// with __syncthreads between levels; the level outputs ping-pong through
+// global scratch.  Counters per level as the per-level launches.
+constexpr int MT_MAX_LEVELS = 16, MT_PMAX = 64;
+struct MaxTreeArgs {
+  int levels;
+  uint64_t jbin[MT_MAX_LEVELS], jxor[MT_MAX_LEVELS], ja[MT_MAX_LEVELS];
+  uint64_t rows_total, row_off;  // batch shard of the rows
+};
+__global__ void __launch_bounds__(kThreads, 1) maxtree_kernel(const __grid_constant__ KeySched ks,
+                                                            const uint64_t* __restrict__ ctr,
+                                                            const __grid_constant__ MaxTreeArgs ta,
+                                                            const uint64_t* __restrict__ v, uint64_t* s0, uint64_t* s1,
+                                                            uint64_t* __restrict__ out, uint64_t rows, uint64_t m0,
+                                                            int R) {
+  SignStreams& st = *reinterpret_cast<SignStreams*>(reinterpret_cast<AesSmem*>(mpc3_dsm)->extra);
+  auto tab = Proto<false>::init();
+  Word2* slots = reinterpret_cast<Word2*>(mpc3_dsm + sizeof(AesSmem));
+  const uint64_t r0 = (uint64_t)blockIdx.x * R;
+  const uint64_t rn = rows - r0 < (uint64_t)R ? rows - r0 : (uint64_t)R;
+  const uint64_t* in = v;
+  uint64_t m = m0;
+  for (int l = 0; l < ta.levels; ++l) {
+    const uint64_t k = m / 2, mo = k + (m & 1);
+    uint64_t* o = l == ta.levels - 1 ? out : ((l & 1) ? s1 : s0);
+    if (threadIdx.x == 0) {
+      const SignArgs a = {ta.jbin[l], ta.jxor[l], ta.ja[l], 0, 0, 0};
+      sign_streams(st, a, ctr, false);
+    }
+    __syncthreads();
+    const uint64_t n = rows * k, n_total = ta.rows_total * k, elem_off = ta.row_off * k;
+    const bool straddle = (n_total & 1) != 0;
+    const int L = straddle ? 3 : 2, used = sign_slots(straddle);
+    const uint64_t p0 = r0 * k / 2, P = (rn * k + 1) / 2;  // this CTA's pairs
+    const MaxGeom g = {rows, m, k};
+    for (uint64_t c = 0; c < P; c += MT_PMAX) {
+      const int Pc = (int)(P - c < (uint64_t)MT_PMAX ? P - c : (uint64_t)MT_PMAX);
+      for (int q = threadIdx.x; q < used * Pc; q += blockDim.x) {
+        const int s = q / Pc, p = q % Pc;
+        sign_slot_fill(tab, &ks.rk[0][0], st, s, (elem_off >> 1) + p0 + c + p, n_total, L,
+                       slots + ((size_t)s * Pc + p) * 3);
+      }
+      __syncthreads();
+      if (threadIdx.x < Pc) {
+        Replay rp;
+        rp.w = slots;
+        rp.P = Pc;
+        rp.p = threadIdx.x;
+        rp.slot = 0;
+        maxlevel_item(rp, &ks.rk[0][0], st, in, o, g, n, n_total, elem_off, p0 + c + threadIdx.x);
+      }
+      __syncthreads();
+    }
+    if (m & 1)  // odd m: the last column passes through to the last output column
+      for (uint64_t r = threadIdx.x; r < rn; r += blockDim.x)
+        store_trio(o, rows * mo, (r0 + r) * mo + k, load_trio(in, rows * m, (r0 + r) * m + m - 1));
+    __syncthreads();
+    in = o;
+    m = mo;
   }
 }
 
@@ -910,6 +982,37 @@ int mpc3_rss_max_level(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_bin,
              (int)MODE_RELU, v, out, (uint64_t*)nullptr, n, n_total, elem_off, P, (uint64_t)0, MaxGeom{rows, m, k},
              RsIn{});
   return check_launch("rss_max_level");
+}
+
+int mpc3_rss_max_tree(const uint32_t* rk3, const uint64_t* ctr, int levels, const uint64_t* j_bin,
+                      const uint64_t* j_xor, const uint64_t* j_arith, const uint64_t* v, uint64_t* scratch,
+                      uint64_t* out, uint64_t rows, uint64_t m, uint64_t row_off, uint64_t rows_total, void* stream) {
+  if (!j_bin || !j_xor || !j_arith || !v || !out) return MPC3_ERR_CONFIG;
+  int lv = 0;
+  for (uint64_t mm = m; mm > 1; mm = mm / 2 + mm % 2) ++lv;
+  if (m < 2 || levels != lv || levels > MT_MAX_LEVELS) return MPC3_ERR_SHAPE;
+  if (row_off + rows > rows_total || (row_off & 1)) return MPC3_ERR_SHAPE;
+  if (rows == 0) return MPC3_OK;
+  MaxTreeArgs ta;
+  ta.levels = levels;
+  for (int l = 0; l < levels; ++l) {
+    if (j_bin[l] >= (1ull << 48) || j_xor[l] + 6 >= (1ull << 48) || j_arith[l] + 2 >= (1ull << 48))
+      return MPC3_ERR_RANGE;
+    ta.jbin[l] = j_bin[l];
+    ta.jxor[l] = j_xor[l];
+    ta.ja[l] = j_arith[l];
+  }
+  ta.rows_total = rows_total;
+  ta.row_off = row_off;
+  KeySched ks;
+  if (int e = load_keys(rk3, 3, stream, &ks)) return e;
+  const int R = 2;
+  const uint64_t half = rows * ((m + 1) / 2) * 3;  // one level output, three components
+  const int smem = kAesSmemBytes + MT_PMAX * sign_slots(true) * SW_SLOT_BYTES;
+  if (!aes_attr((const void*)maxtree_kernel, smem)) return check_launch("max_tree smem attribute");
+  launch_pdl(maxtree_kernel, dim3((unsigned)((rows + R - 1) / R)), dim3(kThreads), smem, as_stream(stream), ks, ctr,
+             ta, v, scratch, scratch + half, out, rows, m, R);
+  return check_launch("rss_max_tree");
 }
 
 int mpc3_rss_bit_inject(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, const uint64_t* bits, uint64_t* out,

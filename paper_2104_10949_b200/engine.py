@@ -57,6 +57,8 @@ REUSE_PACKS = os.environ.get("MPC3_REUSE_PACKS", "1") == "1"
 # 38 vs 22 us; 64-bit IMAD chains at ~7 thread-instructions per ring MAC), and
 # the AlexNet step went 2.71 -> 2.82 ms with the FC layers routed there
 SIMT_MACS = int(os.environ.get("MPC3_SIMT_MACS", "0"))
+# MPC3_MAXTREE_FUSED=0: one launch per max_tree level instead of one for the whole tree
+MAXTREE_FUSED = os.environ.get("MPC3_MAXTREE_FUSED", "1") == "1"
 
 
 @dataclass
@@ -1079,6 +1081,23 @@ class TrioSession:
         lead = v.shape[:-1]
         rows = int(np.prod(lead, dtype=np.int64)) if lead else 1
         v = v.contiguous()
+        levels, mm = [], m
+        while mm > 1:
+            levels.append(mm)
+            mm = mm // 2 + mm % 2
+        row_off, rows_total = self.shard_offset(rows)
+        if MAXTREE_FUSED and levels and len(levels) <= 16 and row_off % 2 == 0:
+            # every level in one launch (mpc3_rss_max_tree), the same counters
+            jb, jx, ja = (np.zeros(len(levels), np.uint64) for _ in range(3))
+            for i, ml in enumerate(levels):
+                jb[i], jx[i], ja[i] = self.take(BIN), self.take(XOR, 7), self.take(ARITH, 3)
+                self._charge_sign(rows * (ml // 2), K.MODE_RELU)
+            scratch = torch.empty(2 * 3 * rows * ((m + 1) // 2), dtype=torch.int64, device=_dev())
+            out = empty(lead + (1,), v.fp)
+            K.call("mpc3_rss_max_tree", self.rk, self.ctr_ptr, len(levels), jb.ctypes.data, jx.ctypes.data,
+                   ja.ctypes.data, v.data.data_ptr(), scratch.data_ptr(), out.data.data_ptr(), rows, m, row_off,
+                   rows_total, _stream())
+            return out.apply(lambda d: d[..., 0].contiguous())
         while m > 1:
             # one launch per level: b + relu(a - b) over the (even, odd) column
             # pairs, the odd tail passed through (mpc3_rss_max_level); counters

@@ -173,6 +173,37 @@ def test_layer_sign_equals_reshare_then_sign(shape, bias, shard):
     assert np.array_equal(host(m2), host(m1))
 
 
+@pytest.mark.parametrize("rows,m,shard", [(128, 10, None), (7, 5, None), (32, 200, None), (3, 2, None),
+                                          (64, 37, (2, 6)), (1, 3, None)])
+def test_max_tree_one_launch_equals_levels(rows, m, shard):
+    """mpc3_rss_max_tree (every level in one launch, R rows per CTA) = one
+    mpc3_rss_max_level per level, share for share (odd m, odd rows, a batch
+    shard of the rows)."""
+    rng = np.random.default_rng(rows * m)
+    v = dev(rnd(rng, (3, rows, m)) >> U64(8))
+    rk = rk3(R.Session(8).keys)
+    row_off, rows_total = (0, rows) if shard is None else (shard[0] * rows // 2 * 2, shard[1] * rows)
+    levels, mm = [], m
+    while mm > 1:
+        levels.append(mm)
+        mm = mm // 2 + mm % 2
+    jb = np.array([3 + 11 * i for i in range(len(levels))], U64)
+    jx = jb + U64(1)
+    ja = jb + U64(8)
+    cur, cm = v, m
+    for i, ml in enumerate(levels):
+        k, mo = ml // 2, ml // 2 + ml % 2
+        o = torch.empty(3 * rows * mo, dtype=torch.int64, device="cuda")
+        _capi.call("mpc3_rss_max_level", p(rk), None, int(jb[i]), int(jx[i]), int(ja[i]), p(cur), p(o), rows, ml,
+                   row_off * k, rows_total * k, stream())
+        cur, cm = o, mo
+    scratch = torch.empty(2 * 3 * rows * ((m + 1) // 2), dtype=torch.int64, device="cuda")
+    out = torch.full((3 * rows,), -1, dtype=torch.int64, device="cuda")
+    _capi.call("mpc3_rss_max_tree", p(rk), None, len(levels), jb.ctypes.data, jx.ctypes.data, ja.ctypes.data,
+               p(v), p(scratch), p(out), rows, m, row_off, rows_total, stream())
+    assert np.array_equal(host(out), host(cur))
+
+
 def _gemm_packed(A, B, groups, M, Nn, kp, splits):
     Cm = torch.zeros(groups * M * Nn, dtype=torch.int64, device="cuda")
     _capi.call("mpc3_ring_gemm_packed", p(A), p(B), p(Cm), groups, M, Nn, kp, Nn, M * Nn, splits, stream())
