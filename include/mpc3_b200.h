@@ -286,6 +286,15 @@ int mpc3_rss_avgpool_backward(const uint32_t* rk3, const uint64_t* ctr, uint64_t
                               int64_t W, int64_t OH, int64_t OW, int kh, int kw, int sh, int sw, int ph, int pw,
                               uint64_t elem_off, void* stream);
 
+/* _avgpool_backward then the mask multiply of the ReLU before the pool
+ * (nn.py:487-499, 515-517) in one pass: out = reshare(truncate(pool_bwd(g))
+ * * mask) with TRUNC_RHO j_rho / TRUNC_R j_r then ARITH_ZERO j_arith, the
+ * counters and shares of the two separate calls. */
+int mpc3_rss_avgpool_backward_mask(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_rho, uint64_t j_r, int bits,
+                                   uint64_t mulc, const uint64_t* g, const uint64_t* mask, uint64_t j_arith,
+                                   uint64_t* out, int64_t N, int64_t C, int64_t H, int64_t W, int64_t OH, int64_t OW,
+                                   int kh, int kw, int sh, int sw, int ph, int pw, uint64_t elem_off, void* stream);
+
 /* Plain sum-pool of one ring tensor (ring.py:259-268). */
 int mpc3_ring_sumpool(const uint64_t* x, uint64_t* out, int64_t N, int64_t C, int64_t H, int64_t W,
                       int kh, int kw, int sh, int sw, void* stream);

@@ -177,6 +177,9 @@ _SIGS = {
     "mpc3_rss_avgpool_backward": (C.c_int, [_P, _P, _U64, _U64, C.c_int, _U64, _P, _P, _I64, _I64, _I64, _I64,
                                             _I64, _I64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _U64,
                                             _P]),
+    "mpc3_rss_avgpool_backward_mask": (C.c_int, [_P, _P, _U64, _U64, C.c_int, _U64, _P, _P, _U64, _P, _I64, _I64,
+                                                 _I64, _I64, _I64, _I64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                                 C.c_int, _U64, _P]),
     "mpc3_rss_col2im_reshare_truncate": (C.c_int, [_P, _P, _U64, _U64, _U64, C.c_int, _P, _I64, _I64, _I64, _I64,
                                                    C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _I64,
                                                    _I64, _P, _U64, _P]),

@@ -612,14 +612,16 @@ __global__ void __launch_bounds__(Proto<F>::threads, Proto<F>::min_ctas) pool_ke
                                                        StreamRef rrho, StreamRef rr, int bits, uint64_t mulc,
                                                        const uint64_t* __restrict__ x,
                                                        uint64_t* __restrict__ out, PoolGeom p, uint64_t n,
-                                                       uint64_t pb0) {
+                                                       uint64_t pb0, const uint64_t* __restrict__ mask,
+                                                       StreamRef ra) {
   auto tab = Proto<F>::init();
-  StreamHead hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
+  StreamHead hrho = resolve(rrho, ctr), hr = resolve(rr, ctr), ha = mask ? resolve(ra, ctr) : StreamHead{0, 0};
   if (2 * n < (1ull << 32) && (uint64_t)p.N * p.C * p.H * p.W < (1ull << 32))
     GRID_LOOP(b, (n + 1) >> 1) pool_item<typename Proto<F>::TT, uint32_t>(tab, &ks.rk[0][0], backward != 0, hrho, hr, bits, mulc, x,
-                                                                out, p, b, pb0);
+                                                                out, p, b, pb0, mask, ha);
   else
-    GRID_LOOP(b, (n + 1) >> 1) pool_item(tab, &ks.rk[0][0], backward != 0, hrho, hr, bits, mulc, x, out, p, b, pb0);
+    GRID_LOOP(b, (n + 1) >> 1) pool_item(tab, &ks.rk[0][0], backward != 0, hrho, hr, bits, mulc, x, out, p, b, pb0,
+                                         mask, ha);
 }
 
 template <bool F>
@@ -1087,7 +1089,8 @@ int mpc3_rss_avgpool(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_rho, u
   if (int e = load_keys(rk3, 3, stream, &ks)) return e;
   AES_LAUNCH(pool_kernel, (n + 1) / 2, as_stream(stream), 
       ks, ctr, 0, sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, mulc, x, out,
-      pool_geom(N, C, H, W, OH, OW, kh, kw, sh, sw, ph, pw), n, elem_off >> 1);
+      pool_geom(N, C, H, W, OH, OW, kh, kw, sh, sw, ph, pw), n, elem_off >> 1, (const uint64_t*)nullptr,
+      sref(ARITH_ZERO, 0));
   return check_launch("rss_avgpool");
 }
 
@@ -1104,8 +1107,27 @@ int mpc3_rss_avgpool_backward(const uint32_t* rk3, const uint64_t* ctr, uint64_t
   if (int e = load_keys(rk3, 3, stream, &ks)) return e;
   AES_LAUNCH(pool_kernel, (n + 1) / 2, as_stream(stream), 
       ks, ctr, 1, sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, mulc, g, out,
-      pool_geom(N, C, H, W, OH, OW, kh, kw, sh, sw, ph, pw), n, elem_off >> 1);
+      pool_geom(N, C, H, W, OH, OW, kh, kw, sh, sw, ph, pw), n, elem_off >> 1, (const uint64_t*)nullptr,
+      sref(ARITH_ZERO, 0));
   return check_launch("rss_avgpool_backward");
+}
+
+int mpc3_rss_avgpool_backward_mask(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_rho, uint64_t j_r, int bits,
+                                   uint64_t mulc, const uint64_t* g, const uint64_t* mask, uint64_t j_arith,
+                                   uint64_t* out, int64_t N, int64_t C, int64_t H, int64_t W, int64_t OH, int64_t OW,
+                                   int kh, int kw, int sh, int sw, int ph, int pw, uint64_t elem_off, void* stream) {
+  if (bits < 1 || bits > 61) return MPC3_ERR_RANGE;
+  if (!mask || (elem_off & 1)) return MPC3_ERR_CONFIG;
+  if (kh < 1 || kw < 1 || sh < 1 || sw < 1 || ph < 0 || pw < 0) return MPC3_ERR_SHAPE;
+  if (j_arith >= (1ull << 48)) return MPC3_ERR_RANGE;
+  uint64_t n = (uint64_t)N * C * H * W;
+  if (n == 0) return MPC3_OK;
+  KeySched ks;
+  if (int e = load_keys(rk3, 3, stream, &ks)) return e;
+  AES_LAUNCH(pool_kernel, (n + 1) / 2, as_stream(stream),
+      ks, ctr, 1, sref(TRUNC_RHO, j_rho), sref(TRUNC_R, j_r), bits, mulc, g, out,
+      pool_geom(N, C, H, W, OH, OW, kh, kw, sh, sw, ph, pw), n, elem_off >> 1, mask, sref(ARITH_ZERO, j_arith));
+  return check_launch("rss_avgpool_backward_mask");
 }
 
 int mpc3_rss_col2im_reshare_truncate(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, uint64_t j_rho,

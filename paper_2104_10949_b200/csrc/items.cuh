@@ -359,7 +359,8 @@ struct PoolGeom {
 // fused window sum (x mulc) + truncate; backward = scatter-add then the same
 template <class T, class I = uint64_t>
 HD void pool_item(const T& tab, const uint32_t* rk3, bool backward, StreamHead hrho, StreamHead hr, int bits,
-                  uint64_t mulc, const uint64_t* x, uint64_t* out, const PoolGeom& p, uint64_t b, uint64_t pb0 = 0) {
+                  uint64_t mulc, const uint64_t* x, uint64_t* out, const PoolGeom& p, uint64_t b, uint64_t pb0 = 0,
+                  const uint64_t* mask = nullptr, StreamHead ha = StreamHead{0, 0}) {
   const uint64_t pb = pb0 + b;
   uint64_t n = backward ? (uint64_t)p.N * p.C * p.H * p.W : (uint64_t)p.N * p.C * p.OH * p.OW;
   uint64_t nin = backward ? (uint64_t)p.N * p.C * p.OH * p.OW : (uint64_t)p.N * p.C * p.H * p.W;
@@ -402,11 +403,27 @@ HD void pool_item(const T& tab, const uint32_t* rk3, bool backward, StreamHead h
     for (int i = 0; i < 3; ++i) s[e].c[i] *= mulc;
   }
   Word2 rho, r;
-  trunc_words(tab, rk3, hrho, hr, pb, rho, r);
+  if (!mask) {
+    trunc_words(tab, rk3, hrho, hr, pb, rho, r);
+    for (int e = 0; e < 2; ++e) {
+      uint64_t f = 2 * b + e;
+      if (f >= n) break;
+      store_trio(out, n, f, trio_truncate(s[e], e ? rho.w1 : rho.w0, e ? r.w1 : r.w0, bits));
+    }
+    return;
+  }
+  // backward through the ReLU before the pool in the same pass: the truncated
+  // gradient times the ReLU's mask, reshared with ARITH_ZERO words (the
+  // "mul.mask" of nn.py:515-517) — five AES blocks per pair in one call
+  Word2 w[3];
+  reshare_trunc_words(tab, rk3, ha, hrho, hr, pb, w, rho, r);
   for (int e = 0; e < 2; ++e) {
     uint64_t f = 2 * b + e;
     if (f >= n) break;
-    store_trio(out, n, f, trio_truncate(s[e], e ? rho.w1 : rho.w0, e ? r.w1 : r.w0, bits));
+    const Trio t = trio_truncate(s[e], e ? rho.w1 : rho.w0, e ? r.w1 : r.w0, bits);
+    KeyWords kw;
+    for (int i = 0; i < 3; ++i) kw.k[i] = e ? w[i].w1 : w[i].w0;
+    store_trio(out, n, f, trio_mul(t, load_trio(mask, n, f), kw));
   }
 }
 

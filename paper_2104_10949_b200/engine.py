@@ -1048,7 +1048,11 @@ class TrioSession:
         self._charge_trunc(out.numel)
         return out
 
-    def avgpool_backward(self, g: RssTensor, window, stride, in_shape, padding=(0, 0)) -> RssTensor:
+    def avgpool_backward(self, g: RssTensor, window, stride, in_shape, padding=(0, 0),
+                         mask: RssTensor | None = None) -> RssTensor:
+        """nn.py:487-499; with `mask`, also the backward of the ReLU before the
+        pool (g * mask, "mul.mask") in the same pass: the same counters in the
+        same order (TRUNC_RHO, TRUNC_R, then ARITH_ZERO) and the same shares."""
         kh, kw = window
         sh, sw = stride
         ph, pw = padding
@@ -1058,10 +1062,21 @@ class TrioSession:
         bits, mulc = self._area_params(kh * kw)
         out = empty((nb, c, h, w), g.fp)
         jr, jq = self.take(TR_RHO), self.take(TR_R)
-        K.call("mpc3_rss_avgpool_backward", self.rk, self.ctr_ptr, jr, jq, bits, mulc, g.data.data_ptr(),
-               out.data.data_ptr(), nb, c, h, w, oh, ow, kh, kw, sh, sw, ph, pw, self.shard_offset(out.numel)[0],
+        off = self.shard_offset(out.numel)[0]
+        if mask is None:
+            K.call("mpc3_rss_avgpool_backward", self.rk, self.ctr_ptr, jr, jq, bits, mulc, g.data.data_ptr(),
+                   out.data.data_ptr(), nb, c, h, w, oh, ow, kh, kw, sh, sw, ph, pw, off, _stream())
+            self._charge_trunc(out.numel)
+            return out
+        mask = mask.contiguous()
+        if mask.shape != out.shape:
+            raise ShapeError(f"mask {mask.shape} does not match the pool input {out.shape}")
+        ja = self.take(ARITH)
+        K.call("mpc3_rss_avgpool_backward_mask", self.rk, self.ctr_ptr, jr, jq, bits, mulc, g.data.data_ptr(),
+               mask.data.data_ptr(), ja, out.data.data_ptr(), nb, c, h, w, oh, ow, kh, kw, sh, sw, ph, pw, off,
                _stream())
         self._charge_trunc(out.numel)
+        self.ledger.ring("mul.mask", out.numel)
         return out
 
     def div_area(self, x: RssTensor, area: int) -> RssTensor:

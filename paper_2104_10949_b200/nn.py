@@ -374,8 +374,12 @@ class TrioNet:
                 rest_done = torch.cuda.Event()
                 rest_done.record(side)
 
+        skip = False  # a ReLU whose backward already ran with the pool after it
         for li in range(len(model.layers) - 1, -1, -1):
             spec, cached = model.layers[li], acts[li]
+            if skip:
+                skip = False
+                continue
             if li == plist[0]:
                 mark_rest()
             if spec.kind == FULLY_CONNECTED:
@@ -401,7 +405,10 @@ class TrioNet:
                     break
                 g = S.conv2d_dgrad(g, k, spec.stride, spec.padding, x.shape, bits=t, w_packed=wp)
             elif spec.kind == AVGPOOL:
-                g = S.avgpool_backward(g, spec.window, spec.stride, cached[0])
+                # a ReLU right before the pool: its mask multiply runs in the pool's pass
+                skip = FUSE_RELU and li > 0 and model.layers[li - 1].kind == RELU
+                g = S.avgpool_backward(g, spec.window, spec.stride, cached[0],
+                                       mask=acts[li - 1][0] if skip else None)
             elif spec.kind == RELU:
                 g = S.mul(g, cached[0], "mul.mask")
             elif spec.kind == FLATTEN:

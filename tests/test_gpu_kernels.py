@@ -204,6 +204,32 @@ def test_max_tree_one_launch_equals_levels(rows, m, shard):
     assert np.array_equal(host(out), host(cur))
 
 
+@pytest.mark.parametrize("geom", [(128, 96, 10, 10, 3, 2, 0), (128, 256, 2, 2, 2, 1, 0), (3, 5, 7, 9, 2, 2, 1),
+                                  (2, 3, 6, 6, 3, 3, 0)])
+def test_avgpool_backward_mask_equals_two_calls(geom):
+    """The pool's backward with the ReLU-mask multiply in the same pass equals
+    mpc3_rss_avgpool_backward then mpc3_rss_mul, share for share (power-of-two
+    and general windows, padding)."""
+    nb, c, h, w, k, st, pd = geom
+    oh, ow = (h + 2 * pd - k) // st + 1, (w + 2 * pd - k) // st + 1
+    rng = np.random.default_rng(nb * c * h)
+    g = dev(rnd(rng, (3, nb * c * oh * ow)) >> U64(3))
+    mask = dev(rnd(rng, (3, nb * c * h * w)))
+    rk = rk3(R.Session(5).keys)
+    area = k * k
+    bits, mulc = (area.bit_length() - 1, 1) if area & (area - 1) == 0 else (20, round((1 << 20) / area))
+    n = nb * c * h * w
+    t = torch.empty(3 * n, dtype=torch.int64, device="cuda")
+    _capi.call("mpc3_rss_avgpool_backward", p(rk), None, 3, 4, bits, mulc, p(g), p(t), nb, c, h, w, oh, ow, k, k, st,
+               st, pd, pd, 0, stream())
+    want = torch.empty_like(t)
+    _capi.call("mpc3_rss_mul", p(rk), None, 9, p(t), p(mask), p(want), n, 0, stream())
+    got = torch.full_like(t, -1)
+    _capi.call("mpc3_rss_avgpool_backward_mask", p(rk), None, 3, 4, bits, mulc, p(g), p(mask), 9, p(got), nb, c, h, w,
+               oh, ow, k, k, st, st, pd, pd, 0, stream())
+    assert np.array_equal(host(got), host(want))
+
+
 def _gemm_packed(A, B, groups, M, Nn, kp, splits):
     Cm = torch.zeros(groups * M * Nn, dtype=torch.int64, device="cuda")
     _capi.call("mpc3_ring_gemm_packed", p(A), p(B), p(Cm), groups, M, Nn, kp, Nn, M * Nn, splits, stream())
