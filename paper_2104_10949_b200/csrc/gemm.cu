@@ -444,7 +444,10 @@ DEV void mma_stage(uint32_t tmem, uint32_t a_base, uint32_t b_base, bool first, 
 // tile: warp ew reads TMEM lane quadrant ew % 4 (its rows) and the column
 // range (ew / 4) of BN split EPI_WARPS / 4 ways.  With c_col the 32 lanes of a
 // warp store 32 consecutive words per column.
-constexpr int EPI_WARPS = 8;
+#ifndef MPC3_EPI_WARPS
+#define MPC3_EPI_WARPS 8
+#endif
+constexpr int EPI_WARPS = MPC3_EPI_WARPS;
 constexpr int GEMM_THREADS = 128 + 32 * EPI_WARPS;  // warps 0-3: TMA, MMA, TMEM alloc, idle
 DEV void epilogue_tile(uint32_t tmem, int ew, int lane, bool have_acc, uint64_t* cg, int64_t m0, int64_t n0,
                        int64_t M, int64_t N, int64_t rs, int64_t cs, bool atomic) {
