@@ -1191,7 +1191,10 @@ static AutoPlan auto_plan(int groups, int64_t M, int64_t N, int64_t kp) {
   p.splits = need > occ ? need : occ;
   const int64_t ctas = tiles * p.splits;
   const double eff = (double)ctas / (double)(((ctas + sms - 1) / sms) * sms);
-  static const double sk_eff = getenv("MPC3_GEMM_SK") ? atof(getenv("MPC3_GEMM_SK")) : 0.85;
+  // stream-K (eff < threshold) is off by default: its all-SM persistent grid
+  // blocks the pack / side streams' work beside it (AlexNet step 2.524 ms
+  // with stream-K below 0.85 wave efficiency, 2.514 ms without)
+  static const double sk_eff = getenv("MPC3_GEMM_SK") ? atof(getenv("MPC3_GEMM_SK")) : 0.0;
   p.streamk = nkb > 0 && eff < sk_eff;
   p.zero = nkb == 0 || p.streamk || p.splits > 1;
   return p;
