@@ -363,6 +363,21 @@ def test_ring_gemm_cross_simt(M, K, Nn, layout):
         assert np.array_equal(got[g], R.wrap_matmul(xt[g] + xt[h], yt[g]) + R.wrap_matmul(xt[g], yt[h])), g
 
 
+def test_pack_halves_z_clears_the_next_gemm_output():
+    """The pack's zero region (the following atomic GEMM's C) is cleared and
+    the pack itself is unchanged."""
+    rng = np.random.default_rng(3)
+    xt = rnd(rng, (3, 300, 70))
+    op = _capi.dense_operand(300, 70, s_r=70, t2=1)
+    ref = _pack_halves(dev(xt), 300 * 70, op, 1, 160, 80)
+    out = torch.empty_like(ref)
+    z = torch.full((12345,), -1, dtype=torch.int64, device="cuda")
+    _capi.call("mpc3_ring_pack_halves_z", p(dev(xt)), 300 * 70, C.byref(op), 1, p(out), 160, 80, p(z), z.numel(),
+               stream())
+    assert torch.equal(out, ref)
+    assert int(torch.count_nonzero(z)) == 0
+
+
 def test_ring_matmul_u64_convenience():
     rng = np.random.default_rng(3)
     M, K, Nn = 77, 20000, 33

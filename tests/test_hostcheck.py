@@ -293,3 +293,15 @@ def test_gemm_t_rejects_unaligned_half():
     # K-major partner must hold the halves at kc_half
     assert lib.mpc3_ring_gemm_t(nul, 1, 64, 160, 80, nul, 0, 64, 96, 0, nul, 3, 70, 64, 64, 0, nul) == \
         2  # MPC3_ERR_SHAPE
+
+
+def test_gemm_needs_zero_plan():
+    """mpc3_ring_gemm_needs_zero (host-only planner): C must be zeroed exactly
+    when the launch accumulates atomically — split-K beyond the 16384-K
+    exactness bound, or a contraction short enough to split for occupancy."""
+    lib = _capi.lib()
+    assert lib.mpc3_ring_gemm_needs_zero(0, 3, 4096, 4096, 1024) == 0  # many tiles, one split
+    assert lib.mpc3_ring_gemm_needs_zero(0, 1, 128, 64, 40000) == 1   # exactness split
+    assert lib.mpc3_ring_gemm_needs_zero(1, 3, 256, 256, 2 * 4096) == 1  # few tiles, long K: occupancy split
+    assert lib.mpc3_ring_gemm_needs_zero(1, 3, 0, 256, 64) == 0
+    assert lib.mpc3_ring_gemm_needs_zero(0, 0, 1, 1, 16) == 2  # MPC3_ERR_SHAPE
