@@ -328,7 +328,9 @@ typedef struct {
  *   role 0 (left operand):  row r of party i = [x_i + x_{i+1} | x_i]
  *   role 1 (right operand): row r of party i = [y_i | y_{i+1}]
  * so that z_i = x_i y_i + x_{i+1} y_i + x_i y_{i+1} is ONE ring GEMM with
- * inner length 2K.  role 2 packs a single plain operand (group count 1).
+ * inner length 2K.  role 2 packs a single plain operand (group count 1);
+ * role 3 packs the three components as planes of their own ([3][8][rows][kp],
+ * plane g = x_g, K columns): a role-1 operand stored once per component. 
  * src: trio planes (plane stride src_plane) or one plane for role 2.
  * out: [3 or 1][8][rows][kp], kp = roundup(K', 16). */
 int mpc3_ring_pack(const uint64_t* src, int64_t src_plane, const mpc3_operand* op, int role,
@@ -399,6 +401,11 @@ int mpc3_ring_gemm_auto_z(const uint8_t* A, const uint8_t* B, uint64_t* C, int g
  *     column h * x_half + j; x_half % 16 == 0 (mpc3_ring_pack_halves);
  *   K-major     (x_mn = 0): a normal pack with x_rows = M (or N) and
  *     x_kp = 2 * kc_half, half h at columns [h * kc_half, (h+1) * kc_half).
+ * a_mn bit 1 (values 2 / 3: K-major / MN): A is a role-3 pack (component
+ *   planes, mpc3_ring_pack_halves role 3) of a role-1 operand [x_g | x_{g+1}]:
+ *   half h of group g is read from component plane (g + h) % 3, at no column
+ *   offset (a_half unused; K-major: a_kp = the component pack's kp, the
+ *   contraction per half kc_half); groups must be 3.
  * C dense [g][M][N] (c_layout 0) or [g][N][M] (1); zeroed here when the
  * split-K partials add atomically. */
 int mpc3_ring_gemm_t(const uint8_t* A, int a_mn, int64_t a_rows, int64_t a_kp, int64_t a_half, const uint8_t* B,

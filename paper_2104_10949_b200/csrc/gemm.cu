@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(PT_THREADS) pack_tile_kernel(const uint64_t* _
     const int32_t yy = fp.y + vp.y, xx = fp.z + vp.z;
     const bool ok = (uint32_t)yy < H && (uint32_t)xx < W;
     const uint32_t off = ok ? (uint32_t)(fp.x + vp.x + yy * a.sH + xx * a.sW) : 0u;
-    vs[it] = ok ? __ldg((ROLE == 1 && half ? sn : sg) + off) : 0ull;
+    vs[it] = ok ? __ldg((ROLE == 1 && half ? sn : sg) + off) : 0ull;  // (ROLE 3: plane g only, no halves)
     if (ROLE == 0) vn[it] = ok && !half ? __ldg(sn + off) : 0ull;
   }
 #pragma unroll
@@ -380,6 +380,7 @@ struct MnArgs {
   int a_mn, b_mn;
   int a_half, b_half;  // source column of half 1
   int nkb_half;        // contraction K-blocks per half
+  int a_cs;            // A's halves are component planes g and g + 1 (role-3 pack of a role-1 operand)
 };
 
 DEV uint64_t umma_desc_mn(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
@@ -412,10 +413,17 @@ DEV void load_stage(const CUtensorMap* tmA, const CUtensorMap* tmB, uint64_t* ba
   mbar_expect_tx(bar, A_STAGE + B_STAGE);
   const int kc = kb * BK;
   const int h = kb >= mn.nkb_half ? 1 : 0, r = (kb - h * mn.nkb_half) * BK;
-  if (mn.a_mn)
+  if (mn.a_cs) {  // half h of [x_g | x_{g+1}] is component plane g + h
+    const int ap = ((g + h) % 3) * 8;
+    if (mn.a_mn)
+      tma_load_3d(tmA, bar, sa, m0, r, ap);
+    else
+      tma_load_3d(tmA, bar, sa, r, m0, ap);
+  } else if (mn.a_mn) {
     tma_load_3d(tmA, bar, sa, h * mn.a_half + m0, r, g * 8);
-  else
+  } else {
     tma_load_3d(tmA, bar, sa, kc, m0, g * 8);
+  }
   if (mn.b_mn)
     tma_load_3d(tmB, bar, sb, h * mn.b_half + n0, r, g * 8);
   else
@@ -1053,10 +1061,10 @@ int mpc3_ring_pack_halves(const uint64_t* src, int64_t src_plane, const mpc3_ope
 int mpc3_ring_pack_halves_z(const uint64_t* src, int64_t src_plane, const mpc3_operand* op, int role, uint8_t* out,
                             int64_t kp, int64_t kh, uint64_t* zero, int64_t zero_words, void* stream) {
   if (zero_words < 0 || (zero_words && !zero)) return MPC3_ERR_CONFIG;
-  if (!op || role < 0 || role > 2) return MPC3_ERR_CONFIG;
+  if (!op || role < 0 || role > 3) return MPC3_ERR_CONFIG;
   if (kp % 16) return MPC3_ERR_SHAPE;
-  if (role == 2) kh = op->k;
-  int64_t kneed = role == 2 ? op->k : kh + op->k;
+  if (role >= 2) kh = op->k;
+  int64_t kneed = role >= 2 ? op->k : kh + op->k;
   if (kh < op->k || kp < kneed || op->rows < 0 || op->k < 0) return MPC3_ERR_SHAPE;
   if (op->mode < 0 || op->mode > 2) return MPC3_ERR_CONFIG;
   Operand o = to_operand(op);
@@ -1099,9 +1107,14 @@ int mpc3_ring_pack_halves_z(const uint64_t* src, int64_t src_plane, const mpc3_o
     }
     dim3 grid((unsigned)((kp + PT_K - 1) / PT_K), (unsigned)row_tiles, (unsigned)groups);
     void (*k)(const uint64_t*, int64_t, Operand, PackTileArgs, uint8_t*) =
-        r_fast ? (role == 0 ? pack_tile_kernel<true, 0> : role == 1 ? pack_tile_kernel<true, 1> : pack_tile_kernel<true, 2>)
-               : (role == 0 ? pack_tile_kernel<false, 0>
-                            : role == 1 ? pack_tile_kernel<false, 1> : pack_tile_kernel<false, 2>);
+        r_fast ? (role == 0   ? pack_tile_kernel<true, 0>
+                  : role == 1 ? pack_tile_kernel<true, 1>
+                  : role == 2 ? pack_tile_kernel<true, 2>
+                              : pack_tile_kernel<true, 3>)
+               : (role == 0   ? pack_tile_kernel<false, 0>
+                  : role == 1 ? pack_tile_kernel<false, 1>
+                  : role == 2 ? pack_tile_kernel<false, 2>
+                              : pack_tile_kernel<false, 3>);
     launch_pdl(k, grid, dim3(PT_THREADS), 0, as_stream(stream), src, src_plane, o, a, out);
     return check_launch("ring_pack_tile");
   }
@@ -1139,7 +1152,7 @@ int mpc3_ring_gemm_packed_layout(const uint8_t* A, const uint8_t* B, uint64_t* C
   st = make_map(&tb, B, kp, N, (int64_t)groups * 8, BN);
   if (st) return st;
   dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)(groups * splits));
-  MnArgs mn0 = {0, 0, 0, 0, 1 << 30};
+  MnArgs mn0 = {0, 0, 0, 0, 1 << 30, 0};
   launch_pdl(gemm_tc_kernel, grid, dim3(GEMM_THREADS), SMEM_BYTES, as_stream(stream), ta, tb, C, M, N, kp, ldc, c_group, splits,
              kbs, c_layout, mn0);
   return check_launch("ring_gemm_tc");
@@ -1167,7 +1180,7 @@ int mpc3_ring_gemm_streamk(const uint8_t* A, const uint8_t* B, uint64_t* C, int 
   const int64_t nkb = (kp + BK - 1) / BK;
   const int64_t total = (int64_t)groups * mt * nt * nkb;
   if (ctas > total) ctas = (int)total;
-  MnArgs mn0 = {0, 0, 0, 0, 1 << 30};
+  MnArgs mn0 = {0, 0, 0, 0, 1 << 30, 0};
   launch_pdl(gemm_sk_kernel, dim3(ctas), dim3(GEMM_THREADS), SMEM_BYTES, as_stream(stream), ta, tb, C, M, N, kp, ldc, c_group,
              mt, nt, total, c_layout, mn0);
   return check_launch("ring_gemm_streamk");
@@ -1268,13 +1281,19 @@ int mpc3_ring_gemm_t_z(const uint8_t* A, int a_mn, int64_t a_rows, int64_t a_kp,
                        int64_t N, int64_t kc_half, int c_layout, int c_zeroed, void* stream) {
   if (groups < 1 || M < 0 || N < 0 || kc_half < 0 || (kc_half % BK)) return MPC3_ERR_SHAPE;
   if (c_layout != 0 && c_layout != 1) return MPC3_ERR_CONFIG;
+  if (a_mn < 0 || a_mn > 3 || b_mn < 0 || b_mn > 1) return MPC3_ERR_CONFIG;
+  const int a_cs = a_mn >> 1;  // bit 1: component-plane halves (role-3 pack)
+  a_mn &= 1;
+  if (a_cs && (groups != 3 || a_kp % 16)) return MPC3_ERR_CONFIG;
   if (M == 0 || N == 0) return MPC3_OK;
   if (M > (1 << 30) || N > (1 << 30) || a_half > (1 << 30) || b_half > (1 << 30)) return MPC3_ERR_SHAPE;
   const int64_t kp = 2 * kc_half;
-  if ((!a_mn && (a_kp != kp || a_rows != M)) || (!b_mn && (b_kp != kp || b_rows != N))) return MPC3_ERR_SHAPE;
+  if ((!a_mn && !a_cs && (a_kp != kp || a_rows != M)) || (!a_mn && a_cs && a_rows != M) ||
+      (!b_mn && (b_kp != kp || b_rows != N)))
+    return MPC3_ERR_SHAPE;
   // an MN operand's half offset is a TMA box start along the 16-byte-granular
   // inner dimension (pack with mpc3_ring_pack_halves, kh % 16 == 0)
-  if ((a_mn && (a_kp % 16 || a_rows > kc_half || a_half % 16)) ||
+  if ((a_mn && (a_kp % 16 || a_rows > kc_half || (!a_cs && a_half % 16))) ||
       (b_mn && (b_kp % 16 || b_rows > kc_half || b_half % 16)))
     return MPC3_ERR_SHAPE;
   static bool attr_set = false;
@@ -1285,7 +1304,7 @@ int mpc3_ring_gemm_t_z(const uint8_t* A, int a_mn, int64_t a_rows, int64_t a_kp,
   }
   CUtensorMap ta, tb;
   int st = a_mn ? make_map_mn(&ta, A, a_kp, a_rows, (int64_t)groups * 8, BM, CU_TENSOR_MAP_SWIZZLE_128B)
-                : make_map(&ta, A, kp, M, (int64_t)groups * 8, BM);
+                : make_map(&ta, A, a_cs ? a_kp : kp, M, (int64_t)groups * 8, BM);
   if (st) return st;
   st = b_mn ? make_map_mn(&tb, B, b_kp, b_rows, (int64_t)groups * 8, BN, CU_TENSOR_MAP_SWIZZLE_64B)
             : make_map(&tb, B, kp, N, (int64_t)groups * 8, BN);
@@ -1302,7 +1321,7 @@ int mpc3_ring_gemm_t_z(const uint8_t* A, int a_mn, int64_t a_rows, int64_t a_kp,
       return check_launch("gemm C memset");
   }
   if (nkb == 0) return MPC3_OK;
-  MnArgs mn = {a_mn ? 1 : 0, b_mn ? 1 : 0, (int)a_half, (int)b_half, (int)(kc_half / BK)};
+  MnArgs mn = {a_mn ? 1 : 0, b_mn ? 1 : 0, (int)a_half, (int)b_half, (int)(kc_half / BK), a_cs};
   if (p.streamk) {  // the split-K grid would leave SMs idle in its last wave: stream-K
     static bool sk_attr = false;
     if (!sk_attr) {

@@ -438,7 +438,9 @@ HD void pack_item(const uint64_t* src, int64_t plane, const Operand& o, int role
   int64_t r = q % o.rows;
   int g = (int)(q / o.rows);
   uint64_t v[8];
-  const int64_t K = o.k, lim = role == 2 ? K : kh + K;
+  // role 3: component planes (plane g = x_g, no halves) — the role-1 operand
+  // [x_g | x_{g+1}] stored once per component, its halves read from planes g, g+1
+  const int64_t K = o.k, lim = role >= 2 ? K : kh + K;
   const int gn = (g + 1) % 3;
   GatherCursor cur;
   int half = -1;
@@ -448,7 +450,7 @@ HD void pack_item(const uint64_t* src, int64_t plane, const Operand& o, int role
       v[e] = 0;
       continue;
     }
-    int h = (role != 2 && kk >= kh) ? 1 : 0;
+    int h = (role < 2 && kk >= kh) ? 1 : 0;
     if (h == 0 && kk >= K) {  // gap between the halves
       v[e] = 0;
       continue;
@@ -462,6 +464,8 @@ HD void pack_item(const uint64_t* src, int64_t plane, const Operand& o, int role
     if (off >= 0) {
       if (role == 2) {
         val = src[off];
+      } else if (role == 3) {
+        val = src[g * plane + off];
       } else {
         uint64_t self = src[g * plane + off], nxt = src[gn * plane + off];
         val = role == 0 ? (h == 0 ? self + nxt : self) : (h == 0 ? self : nxt);  // protocols.py:110-115

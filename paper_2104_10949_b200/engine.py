@@ -51,6 +51,9 @@ SMS = 148
 # MPC3_REUSE_PACKS=0: weight gradients pack their own operands instead of
 # reading the forward / input-gradient packs in place (mpc3_ring_gemm_t)
 REUSE_PACKS = os.environ.get("MPC3_REUSE_PACKS", "1") == "1"
+# MPC3_CS_PACKS=0: role-1 operands of the training step packed with both halves
+# instead of once per component (role 3: half the pack's writes)
+CS_PACKS = os.environ.get("MPC3_CS_PACKS", "1") == "1"
 # secure layers with at most this many ring MACs (3 parties x M x N x 2K) run
 # on the CUDA cores (mpc3_ring_gemm_cross_simt).  Off by default: measured
 # slower than pack + pack + tcgen05 even for the AlexNet FC layers (128x256x256:
@@ -66,7 +69,9 @@ class Packed:
     """A cross-term operand packed for the ring GEMM, kept for reuse: byte-limb
     planes [3][8][rows][kp] of [first half | second half] with the second half
     at the 16-aligned column kh, role 0 ([x_i + x_{i+1} | x_i]) or 1
-    ([x_i | x_{i+1}]).  A weight gradient reads two of these transposed."""
+    ([x_i | x_{i+1}]); or role 3, a role-1 operand stored once per component
+    (plane i = x_i, K columns, kh = k unused) whose halves the GEMM reads from
+    planes i and i + 1.  A weight gradient reads two of these transposed."""
     buf: torch.Tensor
     rows: int
     k: int
@@ -78,6 +83,13 @@ class Packed:
     def geometry(k: int) -> tuple[int, int]:
         kh = _round_up(k, 16)
         return kh, _round_up(kh + k, 16)
+
+    @staticmethod
+    def geometry_cs(k: int) -> tuple[int, int]:
+        """(kh, kp) of the role-0 partner of a role-3 operand: halves at the
+        32-aligned column kc_half (whole K-blocks per half)."""
+        kc = _round_up(k, 32)
+        return kc, 2 * kc
 
 
 def _stream() -> int:
@@ -559,11 +571,15 @@ class TrioSession:
         return out
 
     # -- bilinear layers (protocols.py:97-136, nn.py:435-484) --
-    def pack(self, src: torch.Tensor, op, rows: int, k: int, role: int, zero: torch.Tensor | None = None) -> Packed:
+    def pack(self, src: torch.Tensor, op, rows: int, k: int, role: int, zero: torch.Tensor | None = None,
+             geom: tuple[int, int] | None = None) -> Packed:
         """Pack one cross-term operand in the reusable layout (see Packed);
         `zero`: the next GEMM's C, cleared by the same launch when that GEMM
-        accumulates atomically."""
-        kh, kp = Packed.geometry(k)
+        accumulates atomically; `geom`: (kh, kp) other than Packed.geometry."""
+        if role == 3:
+            kh, kp = k, _round_up(k, 16)
+        else:
+            kh, kp = geom if geom is not None else Packed.geometry(k)
         buf = torch.empty(3 * 8 * rows * kp, dtype=torch.uint8, device=_dev())
         K.call("mpc3_ring_pack_halves_z", src.data_ptr(), src.stride(0), C.byref(op), role, buf.data_ptr(), kp, kh,
                None if zero is None else zero.data_ptr(), 0 if zero is None else zero.numel(), _stream())
@@ -588,7 +604,9 @@ class TrioSession:
         ev.record(main)
         ps.wait_event(ev)
         with torch.cuda.stream(ps):
-            packs = [(self._pack_key(src, op, 0), self.pack(src, op, rows, k, 0)) for src, op, rows, k in items]
+            packs = [(self._pack_key(src, op, 0),
+                      self.pack(src, op, rows, k, 0, geom=Packed.geometry_cs(k) if CS_PACKS else None))
+                     for src, op, rows, k in items]
         done = torch.cuda.Event()
         done.record(ps)
         for key, pk in packs:
@@ -600,8 +618,10 @@ class TrioSession:
     def _cross_gemm_kept(self, a_src, a_op, b_src, b_op, M, N, Kd, c_col, a_role, keep, a_packed):
         """_cross_gemm in the Packed layout: A packed with role a_role (or
         given), B with the other role; both packs appended to `keep` (the
-        backward pass reads them transposed)."""
-        kh, kp = Packed.geometry(Kd)
+        backward pass reads them transposed).  A role-1 A is packed once per
+        component (role 3) under CS_PACKS."""
+        cs = CS_PACKS and a_role == 1 and a_packed is None
+        kh, kp = Packed.geometry_cs(Kd) if cs else Packed.geometry(Kd)
         st = _stream()
         main = torch.cuda.current_stream()
         pre = self._prepacked.pop(self._pack_key(b_src, b_op, 1 - a_role), None) if self._prepacked else None
@@ -630,14 +650,18 @@ class TrioSession:
                 raise ShapeError("packed operand does not match the GEMM")
             A = a_packed
         else:  # the A pack clears C when the GEMM accumulates atomically
-            zeroed = self._needs_zero(False, M, N, kp)
-            A = self.pack(a_src, a_op, M, Kd, a_role, zero=z if zeroed else None)
+            zeroed = self._needs_zero(cs, M, N, kp)
+            A = self.pack(a_src, a_op, M, Kd, 3 if cs else a_role, zero=z if zeroed else None)
         if ps is not None and ps != main:
             ev2 = torch.cuda.Event()
             ev2.record(ps)
             main.wait_event(ev2)
-        K.call("mpc3_ring_gemm_auto_z", A.buf.data_ptr(), B.data_ptr(), z.data_ptr(), 3, M, N, kp, 1 if c_col else 0,
-               1 if zeroed else 0, st)
+        if cs:  # A's halves from component planes g, g + 1; B role 0 with halves at kh = kc_half
+            K.call("mpc3_ring_gemm_t_z", A.buf.data_ptr(), 2, M, A.kp, 0, B.data_ptr(), 0, N, kp, 0, z.data_ptr(), 3,
+                   M, N, kh, 1 if c_col else 0, 1 if zeroed else 0, st)
+        else:
+            K.call("mpc3_ring_gemm_auto_z", A.buf.data_ptr(), B.data_ptr(), z.data_ptr(), 3, M, N, kp,
+                   1 if c_col else 0, 1 if zeroed else 0, st)
         if keep is not None:
             keep.extend([A, Packed(B, N, Kd, kh, kp, 1 - a_role)])
         return z
@@ -652,10 +676,15 @@ class TrioSession:
         if wp.role != 0 or wp.rows != o:
             raise ShapeError("weight pack does not match the input gradient")
         kc = _round_up(o, 32)
-        A = torch.empty(3 * 8 * rows * 2 * kc, dtype=torch.uint8, device=_dev())
         st = _stream()
         z = torch.empty(3 * rows * wp.k, dtype=torch.int64, device=_dev())
         zeroed = self._needs_zero(True, rows, wp.k, 2 * kc)
+        if CS_PACKS:  # g once per component (role 3): the GEMM reads half h from plane g + h
+            A = self.pack(g_src, g_op, rows, o, 3, zero=z if zeroed else None)
+            K.call("mpc3_ring_gemm_t_z", A.buf.data_ptr(), 2, rows, A.kp, 0, wp.buf.data_ptr(), 1, wp.rows, wp.kp,
+                   wp.kh, z.data_ptr(), 3, rows, wp.k, kc, 1 if c_col else 0, 1 if zeroed else 0, st)
+            return z
+        A = torch.empty(3 * 8 * rows * 2 * kc, dtype=torch.uint8, device=_dev())
         K.call("mpc3_ring_pack_halves_z", g_src.data_ptr(), g_src.stride(0), C.byref(g_op), 1, A.data_ptr(), 2 * kc,
                kc, z.data_ptr() if zeroed else None, z.numel() if zeroed else 0, st)
         K.call("mpc3_ring_gemm_t_z", A.data_ptr(), 0, rows, 2 * kc, 0, wp.buf.data_ptr(), 1, wp.rows, wp.kp, wp.kh,
@@ -668,7 +697,7 @@ class TrioSession:
         pack of g and the forward pass's role-1 pack of x, both read
         transposed.  z is [3][O][xp.k] row-major."""
         op, rows, o = self.grad_operand(g)
-        if xp.role != 1 or xp.rows != rows:
+        if xp.role not in (1, 3) or xp.rows != rows:
             raise ShapeError("weight-gradient packs do not match")
         # computed as x^T g (A = x, B = g) into the column-major layout, which
         # is the same memory and keeps the epilogue's stores coalesced
@@ -676,8 +705,9 @@ class TrioSession:
         z = torch.empty(3 * M * N, dtype=torch.int64, device=_dev())
         zeroed = self._needs_zero(True, M, N, 2 * kc)
         gp = self.pack(g.data, op, rows, o, 0, zero=z if zeroed else None)
-        K.call("mpc3_ring_gemm_t_z", xp.buf.data_ptr(), 1, xp.rows, xp.kp, xp.kh, gp.buf.data_ptr(), 1, gp.rows, gp.kp,
-               gp.kh, z.data_ptr(), 3, M, N, kc, 1, 1 if zeroed else 0, _stream())
+        K.call("mpc3_ring_gemm_t_z", xp.buf.data_ptr(), 3 if xp.role == 3 else 1, xp.rows, xp.kp,
+               0 if xp.role == 3 else xp.kh, gp.buf.data_ptr(), 1, gp.rows, gp.kp, gp.kh, z.data_ptr(), 3, M, N, kc, 1,
+               1 if zeroed else 0, _stream())
         return z
 
     def _cross_gemm(self, a_src, a_op, b_src, b_op, M, N, Kd, c_col: bool = False, a_role: int = 0,

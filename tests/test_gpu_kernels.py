@@ -363,6 +363,51 @@ def test_ring_gemm_cross_simt(M, K, Nn, layout):
         assert np.array_equal(got[g], R.wrap_matmul(xt[g] + xt[h], yt[g]) + R.wrap_matmul(xt[g], yt[h])), g
 
 
+@pytest.mark.parametrize("Mm,K,Nn,layout", [(300, 70, 150, 0), (12800, 363, 96, 1), (5, 3, 7, 1), (128, 2304, 384, 1)])
+def test_gemm_component_plane_operand_kmajor(Mm, K, Nn, layout):
+    """A role-1 operand [x_g | x_{g+1}] stored once per component (role-3
+    pack) and read K-major with its second half from plane g + 1
+    (mpc3_ring_gemm_t a_mn = 2): C[g] = x_g (W_g + W_{g+1})^T + x_{g+1} W_g^T."""
+    rng = np.random.default_rng(Mm + K + Nn)
+    xt, wt = rnd(rng, (3, Mm, K)), rnd(rng, (3, Nn, K))
+    kc = (K + 31) // 32 * 32
+    kpc = (K + 15) // 16 * 16
+    A = torch.empty(3 * 8 * Mm * kpc, dtype=torch.uint8, device="cuda")
+    _capi.call("mpc3_ring_pack_halves", p(dev(xt)), Mm * K, C.byref(_capi.dense_operand(Mm, K, s_r=K, t2=1)), 3,
+               p(A), kpc, K, stream())
+    B = _pack_halves(dev(wt), Nn * K, _capi.dense_operand(Nn, K, s_r=K, t2=1), 0, 2 * kc, kc)
+    Cm = torch.full((3 * Mm * Nn,), -1, dtype=torch.int64, device="cuda")
+    _capi.call("mpc3_ring_gemm_t", p(A), 2, Mm, kpc, 0, p(B), 0, Nn, 2 * kc, 0, p(Cm), 3, Mm, Nn, kc, layout, stream())
+    got = host(Cm).reshape(3, Nn, Mm).transpose(0, 2, 1) if layout else host(Cm).reshape(3, Mm, Nn)
+    for g in range(3):
+        h = (g + 1) % 3
+        want = R.wrap_matmul(xt[g], (wt[g] + wt[h]).T) + R.wrap_matmul(xt[h], wt[g].T)
+        assert np.array_equal(got[g], want), g
+
+
+@pytest.mark.parametrize("Rn,Kc,O", [(300, 150, 70), (12800, 363, 96), (1, 5, 3)])
+def test_gemm_component_plane_operand_mn(Rn, Kc, O):
+    """The same role-3 pack read MN-major (a_mn = 3, the weight gradient):
+    C[g] = x_g^T (g_g + g_{g+1}) + x_{g+1}^T g_g, column-major."""
+    rng = np.random.default_rng(Rn + Kc + O)
+    xt, gt = rnd(rng, (3, Rn, Kc)), rnd(rng, (3, Rn, O))
+    kc = (Rn + 31) // 32 * 32
+    kpc = (Kc + 15) // 16 * 16
+    A = torch.empty(3 * 8 * Rn * kpc, dtype=torch.uint8, device="cuda")
+    _capi.call("mpc3_ring_pack_halves", p(dev(xt)), Rn * Kc, C.byref(_capi.dense_operand(Rn, Kc, s_r=Kc, t2=1)), 3,
+               p(A), kpc, Kc, stream())
+    kh = (O + 15) // 16 * 16
+    B = _pack_halves(dev(gt), Rn * O, _capi.dense_operand(Rn, O, s_r=O, t2=1), 0, (kh + O + 15) // 16 * 16, kh)
+    Cm = torch.full((3 * Kc * O,), -1, dtype=torch.int64, device="cuda")
+    _capi.call("mpc3_ring_gemm_t", p(A), 3, Rn, kpc, 0, p(B), 1, Rn, (kh + O + 15) // 16 * 16, kh, p(Cm), 3, Kc, O,
+               kc, 1, stream())
+    got = host(Cm).reshape(3, O, Kc).transpose(0, 2, 1)
+    for g in range(3):
+        h = (g + 1) % 3
+        want = R.wrap_matmul(xt[g].T, gt[g] + gt[h]) + R.wrap_matmul(xt[h].T, gt[g])
+        assert np.array_equal(got[g], want), g
+
+
 def test_pack_halves_z_clears_the_next_gemm_output():
     """The pack's zero region (the following atomic GEMM's C) is cleared and
     the pack itself is unchanged."""

@@ -121,7 +121,7 @@ def test_alexnet_train_step_digest_bit_exact():
 
 @pytest.mark.parametrize("flags", [{"REUSE_PACKS": False}, {"OVERLAP_PACK": False}, {"nn.OVERLAP": False},
                                    {"REUSE_PACKS": False, "nn.OVERLAP": False}, {"nn.FUSE_RELU": False},
-                                   {"nn.FUSE_RELU_MIN": 0}, {"MAXTREE_FUSED": False}])
+                                   {"nn.FUSE_RELU_MIN": 0}, {"MAXTREE_FUSED": False}, {"CS_PACKS": False}])
 def test_alexnet_train_step_digest_under_schedule_variants(flags, monkeypatch):
     """The engine's schedule choices (packs reused across the three GEMMs of a
     layer, weight packs one layer ahead, side-stream weight gradients, pack
