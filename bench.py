@@ -249,7 +249,7 @@ def run_b200(args, ws, rank, local):
 
     def traced_call(name, *a):
         if instrument["on"] and name in ("mpc3_ring_pack", "mpc3_ring_pack_halves", "mpc3_ring_pack_halves_z") \
-                and a[3] in (0, 1):
+                and a[3] in (0, 1, 3):
             instrument["k"] = int(a[2]._obj.k)  # logical K of the cross-term operand (inner length 2K)
         if instrument["on"] and name in ("mpc3_rss_sign", "mpc3_rss_layer_sign", "mpc3_ring_gemm_auto",
                                          "mpc3_ring_gemm_auto_z", "mpc3_ring_gemm_t", "mpc3_ring_gemm_t_z"):
@@ -266,7 +266,9 @@ def run_b200(args, ws, rank, local):
                 sign_events.append((e0, e1, n_el, 25.5 * n_el))
             elif name.startswith("mpc3_ring_gemm_t"):  # transposed operands: the contraction is an MN operand's rows
                 groups, M, N, kc_half = int(a[11]), int(a[12]), int(a[13]), int(a[14])
-                rows = int(a[2]) if a[1] else (int(a[7]) if a[6] else kc_half)
+                # contraction per half: an MN operand's source rows, else the logical K of the
+                # operand packed just before (a_mn bit 1 = component-plane A, K-major when bit 0 is 0)
+                rows = int(a[2]) if int(a[1]) & 1 else (int(a[7]) if a[6] else (instrument["k"] or kc_half))
                 gemm_events.append((e0, e1, 72 * groups * M * N * 2 * rows))
                 gemm_bytes.append(groups * ((M + N) * 8 * 2 * kc_half + M * N * 8))
                 gemm_shapes.append((name, groups, M, N, 2 * rows))

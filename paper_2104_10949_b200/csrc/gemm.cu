@@ -1407,7 +1407,7 @@ int mpc3_ring_gemm_simt(const uint64_t* A, const uint64_t* B, uint64_t* C, int64
 }
 
 size_t mpc3_ring_matmul_workspace(int64_t M, int64_t N, int64_t K) {
-  int64_t kp = (K + 15) / 16 * 16;
+  int64_t kp = (K + 31) / 32 * 32;  // whole 32-byte K-blocks (partial TMA boxes are slow)
   return (size_t)(8 * M * kp + 8 * N * kp);
 }
 
@@ -1415,7 +1415,7 @@ int mpc3_ring_matmul_u64(const uint64_t* A, const uint64_t* B, uint64_t* C, int6
                          void* workspace, void* stream) {
   if (M < 0 || N < 0 || K < 0) return MPC3_ERR_SHAPE;
   if (M == 0 || N == 0) return MPC3_OK;
-  int64_t kp = (K + 15) / 16 * 16;
+  int64_t kp = (K + 31) / 32 * 32;
   uint8_t* pa = reinterpret_cast<uint8_t*>(workspace);
   uint8_t* pb = pa + 8 * M * kp;
   mpc3_operand oa;

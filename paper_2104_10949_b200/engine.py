@@ -82,7 +82,7 @@ class Packed:
     @staticmethod
     def geometry(k: int) -> tuple[int, int]:
         kh = _round_up(k, 16)
-        return kh, _round_up(kh + k, 16)
+        return kh, _round_up(kh + k, 32)  # whole 32-byte K-blocks (see pack)
 
     @staticmethod
     def geometry_cs(k: int) -> tuple[int, int]:
@@ -576,8 +576,8 @@ class TrioSession:
         """Pack one cross-term operand in the reusable layout (see Packed);
         `zero`: the next GEMM's C, cleared by the same launch when that GEMM
         accumulates atomically; `geom`: (kh, kp) other than Packed.geometry."""
-        if role == 3:
-            kh, kp = k, _round_up(k, 16)
+        if role == 3:  # (kp a whole number of 32-byte K-blocks: a TMA box reaching past the end of a row
+            kh, kp = k, _round_up(k, 32)  # is zero-filled on a slow path — conv1's GEMM 123 -> 157 us)
         else:
             kh, kp = geom if geom is not None else Packed.geometry(k)
         buf = torch.empty(3 * 8 * rows * kp, dtype=torch.uint8, device=_dev())
@@ -738,7 +738,7 @@ class TrioSession:
             return z
         if CS_PACKS:
             return self._cross_gemm_cs(a_src, a_op, b_src, b_op, M, N, Kd, c_col)
-        kp = _round_up(2 * Kd, 16)
+        kp = _round_up(2 * Kd, 32)  # whole 32-byte K-blocks (see pack)
         A = torch.empty(3 * 8 * M * kp, dtype=torch.uint8, device=_dev())
         st = _stream()
         if self._wcache is not None:  # frozen weights (inference): B packed once per weight version
@@ -1370,7 +1370,7 @@ def plain_conv2d(x: np.ndarray, k: np.ndarray, stride, padding) -> np.ndarray:
     dx, dk = to_device(x), to_device(k)
     K_ = c * kh * kw
     M = nb * oh * ow
-    kp = _round_up(K_, 16)
+    kp = _round_up(K_, 32)
     A = torch.empty(8 * M * kp, dtype=torch.uint8, device=_dev())
     B = torch.empty(8 * o * kp, dtype=torch.uint8, device=_dev())
     a_op = K.conv_operand(K.GATHER_IM2COL, M, K_, nb, c, h, w, dx.stride(), kh, kw, sh, sw, ph, pw, oh, ow)
