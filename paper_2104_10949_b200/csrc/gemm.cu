@@ -1192,13 +1192,20 @@ struct AutoPlan {
   int64_t splits;
   bool streamk, zero;
 };
+// minimum K-blocks per split when splitting K for occupancy (MPC3_SPLIT_MINKB)
+static int64_t split_min_kb() {
+  // 2: the AlexNet step 2.469 -> 2.459 ms against 4 (short-K GEMMs fill more SMs)
+  static const int64_t v = getenv("MPC3_SPLIT_MINKB") ? atoll(getenv("MPC3_SPLIT_MINKB")) : 2;
+  return v < 1 ? 1 : v;
+}
+
 static AutoPlan auto_plan(int groups, int64_t M, int64_t N, int64_t kp) {
   const int64_t sms = 148;
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * groups;
   const int64_t nkb = (kp + BK - 1) / BK;
   const int64_t need = (nkb * BK + MAX_SPLIT_K - 1) / MAX_SPLIT_K;  // exactness
   int64_t occ = sms / tiles;                                         // <= one wave, >= 4 K-blocks per split
-  if (occ > nkb / 4) occ = nkb / 4;
+  if (occ > nkb / split_min_kb()) occ = nkb / split_min_kb();
   if (occ < 1) occ = 1;
   AutoPlan p;
   p.splits = need > occ ? need : occ;
@@ -1248,7 +1255,7 @@ static AutoPlan t_plan(int groups, int64_t M, int64_t N, int64_t kp) {
   const int64_t nkb = kp / BK;
   const int64_t need = (nkb * BK + MAX_SPLIT_K - 1) / MAX_SPLIT_K;
   int64_t occ = sms / tiles;
-  if (occ > nkb / 4) occ = nkb / 4;
+  if (occ > nkb / split_min_kb()) occ = nkb / split_min_kb();
   if (occ < 1) occ = 1;
   AutoPlan p;
   p.splits = need > occ ? need : occ;
