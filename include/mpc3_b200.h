@@ -200,9 +200,10 @@ int mpc3_rss_sign(const uint32_t* rk3, const uint64_t* ctr, int mode, uint64_t j
                   uint64_t elem_off, void* stream);
 
 
-/* bit_inject of XOR-shared bits (protocols.py:304-331), 2 ARITH counters. */
+/* bit_inject of XOR-shared bits (protocols.py:304-331), 2 ARITH counters;
+ * elem_off (even) = the global flat index of bits[0] (batch shard). */
 int mpc3_rss_bit_inject(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, const uint64_t* bits, uint64_t* out,
-                        uint64_t n, void* stream);
+                        uint64_t n, uint64_t elem_off, void* stream);
 
 /* Output view of a bilinear result: the logical ("full") output is a 4-d
  * C-order tensor of sizes full[4]; PRF word index = its flat index.  Only the
@@ -294,6 +295,15 @@ int mpc3_rss_avgpool_backward_mask(const uint32_t* rk3, const uint64_t* ctr, uin
                                    uint64_t mulc, const uint64_t* g, const uint64_t* mask, uint64_t j_arith,
                                    uint64_t* out, int64_t N, int64_t C, int64_t H, int64_t W, int64_t OH, int64_t OW,
                                    int kh, int kw, int sh, int sw, int ph, int pw, uint64_t elem_off, void* stream);
+
+/* Max-pool windows of a trio tensor x (3, N, C, H, W) -> out (3, N*C*OH*OW,
+ * kh*kw), (kh, kw) row-major; positions in the padding hold the public
+ * constant `pad` in component 0 (sharing.py:184-187 const placement).  The
+ * max-pool extension (absent from the reference) is then
+ * max_tree (protocols.py:356-380) over each window row: the reference's
+ * composition, bit for bit (tests/golden/make_golden_configs.py maxpool). */
+int mpc3_rss_window_gather(const uint64_t* x, uint64_t* out, int64_t N, int64_t C, int64_t H, int64_t W,
+                           int kh, int kw, int sh, int sw, int ph, int pw, uint64_t pad, void* stream);
 
 /* Plain sum-pool of one ring tensor (ring.py:259-268). */
 int mpc3_ring_sumpool(const uint64_t* x, uint64_t* out, int64_t N, int64_t C, int64_t H, int64_t W,

@@ -23,6 +23,7 @@ CONV, FC, POOL, RELU, FLAT = "Conv2d", "FullyConnected", "AvgPool", "ReLU", "Fla
 
 
 RES = "Residual"
+MAXP = "MaxPool"
 
 
 @dataclass(frozen=True)
@@ -484,6 +485,8 @@ def forward_ext(s: R.Session, layers, it, h):
             if ph or pw:
                 h = np.pad(h, ((0, 0), (0, 0), (0, 0), (ph, ph), (pw, pw)))
             h = R.avgpool_shares(s, h, L.window, L.stride)
+        elif L.kind == MAXP:
+            h = R.maxpool_shares(s, h, L.window, L.stride, L.padding)
         elif L.kind == RELU:
             h = R.relu(s, h)
         elif L.kind == FLAT:

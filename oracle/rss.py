@@ -453,6 +453,27 @@ def max_tree(s: Session, v):
     return v[..., 0]
 
 
+MAXPOOL_PAD = (1 << 64) - (1 << 60)  # public padding constant (ring encoding of -2^60)
+
+
+def maxpool_shares(s: Session, x, window, stride=None, padding=(0, 0)):
+    """Max-pool composed from reference primitives (the reference has no
+    max-pool layer): each component's (kh, kw) windows gathered
+    row-major (a local structural op; padded positions hold the public
+    constant in component 0, sharing.py:184-187), then max_tree
+    (protocols.py:356-380) over the window axis."""
+    (kh, kw), (ph, pw) = window, padding
+    sh, sw = stride or window
+    outs = []
+    for i in range(3):
+        v = x[i]
+        if ph or pw:
+            v = np.pad(v, ((0, 0), (0, 0), (ph, ph), (pw, pw)), constant_values=MAXPOOL_PAD if i == 0 else 0)
+        win = np.lib.stride_tricks.sliding_window_view(v, (kh, kw), axis=(2, 3))[:, :, ::sh, ::sw]
+        outs.append(win.reshape(win.shape[:4] + (kh * kw,)))
+    return max_tree(s, np.ascontiguousarray(np.stack(outs)))
+
+
 # ---------------------------------------------------------------------------
 # function approximations (protocols.py:387-468)
 

@@ -167,7 +167,7 @@ _SIGS = {
     "mpc3_rss_sgd_multi": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, _U64, _P]),
     "mpc3_rss_max_level": (C.c_int, [_P, _P, _U64, _U64, _U64, _P, _P, _U64, _U64, _U64, _U64, _P]),
     "mpc3_rss_chain": (C.c_int, [_P, _P, _P, C.c_int, _U64, _U64, _U64, _P, _P, _U64, _U64, _P]),
-    "mpc3_rss_bit_inject": (C.c_int, [_P, _P, _U64, _P, _P, _U64, _P]),
+    "mpc3_rss_bit_inject": (C.c_int, [_P, _P, _U64, _P, _P, _U64, _U64, _P]),
     "mpc3_rss_reshare_truncate": (C.c_int, [_P, _P, _U64, _U64, _U64, C.c_int, _P, C.POINTER(View4), _P, _U64,
                                             _P]),
     "mpc3_rss_reshare_truncate_bias": (C.c_int, [_P, _P, _U64, _U64, _U64, C.c_int, _P, C.POINTER(View4), _P, _I64,
@@ -186,6 +186,8 @@ _SIGS = {
     "mpc3_rss_col2im_reshare_truncate_layout": (C.c_int, [_P, _P, _U64, _U64, _U64, C.c_int, _P, C.c_int, _I64, _I64,
                                                           _I64, _I64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                                           C.c_int, _I64, _I64, _P, _U64, _P]),
+    "mpc3_rss_window_gather": (C.c_int, [_P, _P, _I64, _I64, _I64, _I64, C.c_int, C.c_int, C.c_int, C.c_int,
+                                         C.c_int, C.c_int, _U64, _P]),
     "mpc3_ring_sumpool": (C.c_int, [_P, _P, _I64, _I64, _I64, _I64, C.c_int, C.c_int, C.c_int, C.c_int, _P]),
     "mpc3_ring_pack": (C.c_int, [_P, _I64, C.POINTER(Operand), C.c_int, _P, _I64, _P]),
     "mpc3_ring_pack_halves": (C.c_int, [_P, _I64, C.POINTER(Operand), C.c_int, _P, _I64, _I64, _P]),

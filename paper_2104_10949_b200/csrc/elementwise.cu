@@ -584,10 +584,10 @@ template <bool F>
 __global__ void __launch_bounds__(Proto<F>::threads, Proto<F>::min_ctas) inject_kernel(const __grid_constant__ KeySched ks,
                                                          const uint64_t* __restrict__ ctr, StreamRef r0,
                                                          StreamRef r1, const uint64_t* __restrict__ bits,
-                                                         uint64_t* __restrict__ out, uint64_t n) {
+                                                         uint64_t* __restrict__ out, uint64_t n, uint64_t pb0) {
   auto tab = Proto<F>::init();
   StreamHead a0 = resolve(r0, ctr), a1 = resolve(r1, ctr);
-  GRID_LOOP(b, (n + 1) >> 1) inject_item(tab, &ks.rk[0][0], a0, a1, bits, out, n, b);
+  GRID_LOOP(b, (n + 1) >> 1) inject_item(tab, &ks.rk[0][0], a0, a1, bits, out, n, b, pb0);
 }
 
 template <bool F>
@@ -648,6 +648,34 @@ __global__ void sumpool_kernel(const uint64_t* __restrict__ x, uint64_t* __restr
     for (int u = 0; u < p.kh; ++u)
       for (int q = 0; q < p.kw; ++q) s += base[u * p.W + q];
     out[f] = s;
+  }
+}
+
+
+// Max-pool windows (nn.MaxPool extension): out[(n, c, oy, ox), (u, v)] =
+// x[n, c, oy*sh - ph + u, ox*sw - pw + v] for the three components, (u, v)
+// row-major; a window position in the zero padding holds the public
+// constant pad in component 0 and 0 in components 1, 2 (sharing.py:184-187),
+// so max_tree over the window row is the composed reference max-pool.
+__global__ void window_gather_kernel(const uint64_t* __restrict__ x, uint64_t* __restrict__ out, PoolGeom p,
+                                     int ph, int pw, uint64_t pad) {
+  griddep_launch();
+  griddep_wait();
+  const uint64_t kk = (uint64_t)p.kh * p.kw;
+  const uint64_t n = (uint64_t)p.N * p.C * p.OH * p.OW * kk;
+  const uint64_t plane_in = (uint64_t)p.N * p.C * p.H * p.W;
+  GRID_LOOP(f, 3 * n) {
+    const uint64_t comp = f / n, e = f - comp * n;
+    const uint64_t w = e / kk, uv = e - w * kk;
+    const int64_t u = (int64_t)(uv / p.kw), v = (int64_t)(uv % p.kw);
+    const int64_t ox = w % p.OW, oy = (w / p.OW) % p.OH, nc = w / ((uint64_t)p.OW * p.OH);
+    const int64_t yy = oy * p.sh - ph + u, xx = ox * p.sw - pw + v;
+    uint64_t r;
+    if (yy < 0 || yy >= p.H || xx < 0 || xx >= p.W)
+      r = comp == 0 ? pad : 0;
+    else
+      r = x[comp * plane_in + (nc * p.H + yy) * p.W + xx];
+    out[f] = r;
   }
 }
 
@@ -1018,13 +1046,14 @@ int mpc3_rss_max_tree(const uint32_t* rk3, const uint64_t* ctr, int levels, cons
 }
 
 int mpc3_rss_bit_inject(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, const uint64_t* bits, uint64_t* out,
-                        uint64_t n, void* stream) {
+                        uint64_t n, uint64_t elem_off, void* stream) {
   if (j_arith + 1 >= (1ull << 48)) return MPC3_ERR_RANGE;
+  if (elem_off & 1) return MPC3_ERR_CONFIG;
   if (n == 0) return MPC3_OK;
   KeySched ks;
   if (int e = load_keys(rk3, 3, stream, &ks)) return e;
   AES_LAUNCH(inject_kernel, (n + 1) / 2, as_stream(stream), 
-      ks, ctr, sref(ARITH_ZERO, j_arith), sref(ARITH_ZERO, j_arith + 1), bits, out, n);
+      ks, ctr, sref(ARITH_ZERO, j_arith), sref(ARITH_ZERO, j_arith + 1), bits, out, n, elem_off >> 1);
   return check_launch("rss_bit_inject");
 }
 
@@ -1172,6 +1201,19 @@ int mpc3_ring_sumpool(const uint64_t* x, uint64_t* out, int64_t N, int64_t C, in
   sumpool_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(x, out,
                                                                 pool_geom(N, C, H, W, OH, OW, kh, kw, sh, sw));
   return check_launch("ring_sumpool");
+}
+
+int mpc3_rss_window_gather(const uint64_t* x, uint64_t* out, int64_t N, int64_t C, int64_t H, int64_t W, int kh,
+                           int kw, int sh, int sw, int ph, int pw, uint64_t pad, void* stream) {
+  if (kh < 1 || kw < 1 || sh < 1 || sw < 1 || ph < 0 || pw < 0 || 2 * ph >= kh + 1 || 2 * pw >= kw + 1 ||
+      H + 2 * ph < kh || W + 2 * pw < kw)
+    return MPC3_ERR_SHAPE;
+  int64_t OH = (H + 2 * ph - kh) / sh + 1, OW = (W + 2 * pw - kw) / sw + 1;
+  uint64_t n = 3ull * N * C * OH * OW * kh * kw;
+  if (n == 0) return MPC3_OK;
+  launch_pdl(window_gather_kernel, dim3(grid_for(n, 256)), dim3(256), 0, as_stream(stream), x, out,
+             pool_geom(N, C, H, W, OH, OW, kh, kw, sh, sw), ph, pw, pad);
+  return check_launch("rss_window_gather");
 }
 
 }  // extern "C"

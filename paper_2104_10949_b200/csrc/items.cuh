@@ -140,12 +140,12 @@ HD void maxlevel_item(const T& tab, const uint32_t* rk3, const SignStreams& st, 
 
 template <class T>
 HD void inject_item(const T& tab, const uint32_t* rk3, StreamHead a0, StreamHead a1, const uint64_t* bits,
-                    uint64_t* out, uint64_t n, uint64_t b) {
+                    uint64_t* out, uint64_t n, uint64_t b, uint64_t pb0 = 0) {
   bool two = 2 * b + 1 < n;
   Trio v[2], o[2];
   v[0] = load_trio(bits, n, 2 * b);
   v[1] = two ? load_trio(bits, n, 2 * b + 1) : v[0];
-  inject_pair(tab, rk3, a0, a1, b, v, o);
+  inject_pair(tab, rk3, a0, a1, pb0 + b, v, o);  // PRF block of the pair: shard offset + local pair
   store_trio(out, n, 2 * b, o[0]);
   if (two) store_trio(out, n, 2 * b + 1, o[1]);
 }

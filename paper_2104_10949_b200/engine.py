@@ -62,6 +62,12 @@ CS_PACKS = os.environ.get("MPC3_CS_PACKS", "1") == "1"
 SIMT_MACS = int(os.environ.get("MPC3_SIMT_MACS", "0"))
 # MPC3_MAXTREE_FUSED=0: one launch per max_tree level instead of one for the whole tree
 MAXTREE_FUSED = os.environ.get("MPC3_MAXTREE_FUSED", "1") == "1"
+# the one-launch max_tree runs two rows per CTA (a latency design for the
+# softmax's (batch, classes) rows); many rows (max-pool windows) go level by
+# level through the persistent sign kernel instead
+MAXTREE_FUSED_MAX_ROWS = 8192
+# public padding constant of the max-pool extension: the ring encoding of -2^60
+MAXPOOL_PAD = (1 << 64) - (1 << 60)
 
 
 @dataclass
@@ -244,6 +250,8 @@ class TrioSession:
         if torch.cuda.is_available():
             self.rk3 = self.rk3.pin_memory()
         self.seq = {p: 0 for p in PURPOSES}
+        self.engine_mark = {p: 0 for p in PURPOSES}  # first counter no engine kernel has drawn
+        self._party_seq = {}  # per-party counters of PartyContext.take (lockstep, sharing.py:225-230)
         self.ledger = Ledger()
         self.ctr = None  # optional device per-purpose counter base (CUDA-graph replay)
         self.dp = None  # DataParallel: this session computes one batch shard
@@ -257,7 +265,9 @@ class TrioSession:
     def frozen_weights(self):
         """Context: the weight operands (GEMM B side) do not change, so their
         packed limb planes are built once and reused (inference; a weight
-        modified in place gets a new tensor version and is repacked)."""
+        modified by a torch in-place op gets a new tensor version and is
+        repacked, and sgd_launch, which writes through raw pointers, drops
+        the cache)."""
         sess = self
 
         class _Ctx:
@@ -319,7 +329,28 @@ class TrioSession:
         if j + count > (1 << 48):
             raise FreshnessError(f"stream counters for purpose {purpose:#06x} exhausted")
         self.seq[purpose] = j + count
+        self.engine_mark[purpose] = max(self.engine_mark[purpose], j + count)
         return j
+
+    def party_take(self, party: int, purpose: int) -> int:
+        """PartyContext.take for party `party` (sharing.py:225-230): the three
+        parties draw the same counter in lockstep, never one an engine kernel
+        has already used; once all three hold j, the engine's next counter
+        is past it."""
+        own = self._party_seq.setdefault(party, {})
+        j = max(own.get(purpose, 0), self.seq[purpose])
+        if j + 1 > (1 << 48):
+            raise FreshnessError(f"stream counters for purpose {purpose:#06x} exhausted")
+        own[purpose] = j + 1
+        if all(self._party_seq.get(p, {}).get(purpose, 0) >= j + 1 for p in range(3)):
+            self.seq[purpose] = max(self.seq[purpose], j + 1)
+        return j
+
+    def check_fresh(self, purpose: int, j: int) -> None:
+        """A stream a protocol kernel has already consumed may not be drawn
+        again through the per-party randomness API (sharing.py:198-204)."""
+        if j < self.engine_mark.get(purpose, 0):
+            raise FreshnessError(f"counter {j} for purpose {purpose:#06x} already consumed by the engine")
 
     def counters(self) -> dict:
         return dict(self.seq)
@@ -493,6 +524,10 @@ class TrioSession:
                     p.data.data_ptr(), g.data.data_ptr(), p.numel, jr, jq)
             K.call("mpc3_rss_sgd_multi", self.rk, self.ctr_ptr, arr, len(chunk), chunk[0][4], int(c) % (1 << 64),
                    _stream())
+        # the parameters changed through raw pointers (no torch version bump):
+        # packed weight operands cached under frozen_weights are stale now
+        if self._wcache:
+            self._wcache.clear()
 
     def mul_truncate(self, x, y, bits=None, label="mul.reshare") -> RssTensor:
         """truncate(mul(x, y)) in one launch; same counters and accounting."""
@@ -565,7 +600,7 @@ class TrioSession:
         out = empty(b.shape, b.fp)
         ja = self.take(ARITH, 2)
         K.call("mpc3_rss_bit_inject", self.rk, self.ctr_ptr, ja, b.data.data_ptr(), out.data.data_ptr(), b.numel,
-               _stream())
+               self.shard_offset(b.numel)[0], _stream())
         self.ledger.ring("mul.inject", b.numel)
         self.ledger.ring("mul.inject", b.numel)
         return out
@@ -1149,6 +1184,25 @@ class TrioSession:
         self.ledger.ring("mul.mask", out.numel)
         return out
 
+    def maxpool(self, x: RssTensor, window, stride=None, padding=(0, 0)) -> RssTensor:
+        """Max-pool extension (absent from the reference):
+        each (kh, kw) window flattened row-major (mpc3_rss_window_gather;
+        padded positions hold the public constant -2^60 in component 0) and
+        reduced by max_tree (protocols.py:356-380) — the composition of the
+        reference's own primitives, share for share."""
+        kh, kw = window
+        sh, sw = stride or window
+        ph, pw = padding
+        if x.ndim != 4 or x.shape[2] + 2 * ph < kh or x.shape[3] + 2 * pw < kw or 2 * ph > kh or 2 * pw > kw:
+            raise ShapeError("max-pool window does not fit the input")
+        x = x.contiguous()
+        nb, c, h, w = x.shape
+        oh, ow = (h + 2 * ph - kh) // sh + 1, (w + 2 * pw - kw) // sw + 1
+        win = empty((nb, c, oh, ow, kh * kw), x.fp)
+        K.call("mpc3_rss_window_gather", x.data.data_ptr(), win.data.data_ptr(), nb, c, h, w, kh, kw, sh, sw, ph, pw,
+               MAXPOOL_PAD, _stream())
+        return self.max_tree(win)
+
     def div_area(self, x: RssTensor, area: int) -> RssTensor:
         bits, mulc = self._area_params(area)
         if mulc != 1:
@@ -1171,7 +1225,7 @@ class TrioSession:
             levels.append(mm)
             mm = mm // 2 + mm % 2
         row_off, rows_total = self.shard_offset(rows)
-        if MAXTREE_FUSED and levels and len(levels) <= 16 and row_off % 2 == 0:
+        if MAXTREE_FUSED and levels and len(levels) <= 16 and row_off % 2 == 0 and rows <= MAXTREE_FUSED_MAX_ROWS:
             # every level in one launch (mpc3_rss_max_tree), the same counters
             jb, jx, ja = (np.zeros(len(levels), np.uint64) for _ in range(3))
             for i, ml in enumerate(levels):
@@ -1220,8 +1274,8 @@ class TrioSession:
         of the unfused sequence of mul_truncate calls."""
         muls = (K.CHAIN_SQ, K.CHAIN_MULX, K.CHAIN_SQT)
         nmul = sum(1 for op, _, _ in steps if op in muls)
-        if len(steps) > K.CHAIN_MAX_STEPS:
-            raise ConfigError(f"chain of {len(steps)} steps exceeds {K.CHAIN_MAX_STEPS}")
+        if len(steps) > K.CHAIN_MAX_STEPS:  # e.g. ReciprocalConfig(iterations >= 16)
+            return self._chain_unfused(x, steps)
         for op, bits, _ in steps:
             if op in muls and not 1 <= bits <= 61:
                 raise RangeError(f"truncation by {bits} bits outside [1, 61]")
@@ -1235,6 +1289,29 @@ class TrioSession:
             self.ledger.ring("mul.reshare", x.numel)
             self._charge_trunc(x.numel)
         return out
+
+    def _chain_unfused(self, x: RssTensor, steps) -> RssTensor:
+        """The chain program as separate launches (one mul_truncate per
+        multiply): the same counters, accounting and shares as _chain, for
+        programs longer than one chain launch holds."""
+        x = x.contiguous()
+        z, t = x, None
+        for op, bits, c in steps:
+            if op == K.CHAIN_ADDC:
+                z = self.add_const(z, c)
+            elif op == K.CHAIN_SETC:
+                z = self.const_share(c, x.shape)
+            elif op == K.CHAIN_SQ:
+                z = self.mul_truncate(z, z, bits)
+            elif op == K.CHAIN_SQT:
+                t = self.mul_truncate(z, z, bits)
+            elif op == K.CHAIN_MULX:
+                t = self.mul_truncate(x, t, bits)
+            elif op == K.CHAIN_NEWTON:
+                z = self.sub(self.mul_const(z, 2), t)
+            else:
+                raise ConfigError(f"unknown chain op {op}")
+        return z
 
     def division(self, x, y, cfg: ReciprocalConfig = ReciprocalConfig()):
         return self.mul_truncate(x, self.reciprocal(y, cfg))

@@ -39,6 +39,10 @@ FLATTEN = "Flatten"
 # composed from its primitives: bias = local add after the truncation,
 # residual = local add of two branches, padded avg-pool = zero pad + avg-pool)
 RESIDUAL = "Residual"
+# max-pooling (absent from the reference; the paper swaps it for avg-pooling,
+# PAPER.md:1405-1420): each window flattened row-major into max_tree
+# (protocols.py:356-380), padded positions holding a public -2^60
+MAXPOOL = "MaxPool"
 # MPC3_OVERLAP=0: weight gradients on the main stream (no side-stream overlap)
 OVERLAP = os.environ.get("MPC3_OVERLAP", "1") == "1"
 # MPC3_FUSE_RELU=0: a conv / linear layer's epilogue and the ReLU after it as two launches
@@ -83,6 +87,12 @@ def fully_connected(out_features: int, bias: bool = False) -> LayerSpec:
 def avgpool(window, stride=None, padding=0) -> LayerSpec:
     w = _pair(window)
     return LayerSpec(AVGPOOL, window=w, stride=_pair(stride) if stride is not None else w, padding=_pair(padding))
+
+
+def maxpool(window, stride=None, padding=0) -> LayerSpec:
+    """Max-pool (inference extension): max_tree over each flattened window."""
+    w = _pair(window)
+    return LayerSpec(MAXPOOL, window=w, stride=_pair(stride) if stride is not None else w, padding=_pair(padding))
 
 
 def residual(main, shortcut=()) -> LayerSpec:
@@ -145,7 +155,7 @@ class ModelGraph:
     @property
     def trainable(self) -> bool:
         """The reference's layer kinds only (backward is defined for them)."""
-        return all(s.kind != RESIDUAL and not s.bias for s in self.layers)
+        return all(s.kind not in (RESIDUAL, MAXPOOL) and not s.bias for s in self.layers)
 
 
 def _infer(layers, shape) -> list:
@@ -169,15 +179,15 @@ def _infer(layers, shape) -> list:
                 if h + 2 * ph < kh or w + 2 * pw < kw or ho < 1 or wo < 1:
                     raise ShapeError(f"Conv2d kernel {s.kernel} does not fit {shape}")
                 shape = (s.out_channels, ho, wo)
-            elif s.kind == AVGPOOL:
+            elif s.kind in (AVGPOOL, MAXPOOL):
                 if len(shape) != 3:
-                    raise ShapeError(f"AvgPool needs (C,H,W), got {shape}")
+                    raise ShapeError(f"{s.kind} needs (C,H,W), got {shape}")
                 c, h, w = shape
                 ph, pw = s.padding
                 ho = (h + 2 * ph - s.window[0]) // s.stride[0] + 1
                 wo = (w + 2 * pw - s.window[1]) // s.stride[1] + 1
                 if ho < 1 or wo < 1:
-                    raise ShapeError(f"AvgPool window {s.window} does not fit {shape}")
+                    raise ShapeError(f"{s.kind} window {s.window} does not fit {shape}")
                 shape = (c, ho, wo)
             elif s.kind == FULLY_CONNECTED:
                 if len(shape) != 1:
@@ -318,6 +328,9 @@ class TrioNet:
             elif spec.kind == AVGPOOL:
                 acts.append((h.shape,) if record else None)
                 h = S.avgpool(h, spec.window, spec.stride, spec.padding)
+            elif spec.kind == MAXPOOL:
+                acts.append((h.shape,) if record else None)
+                h = S.maxpool(h, spec.window, spec.stride, spec.padding)
             elif spec.kind == RELU:
                 h, mask = S.relu_with_mask(h)
                 acts.append((mask,) if record else None)
@@ -568,14 +581,14 @@ class GraphStep:
         S.ctr = torch.zeros(8, dtype=torch.int64, device=xs.data.device)
         self.ctr = S.ctr
         self.graph = torch.cuda.CUDAGraph()
-        ledger_on = S.ledger.enabled
-        S.ledger.enabled = False
         try:
-            with torch.cuda.graph(self.graph):
+            # the step's rounds are recorded, not charged, at capture and
+            # charged on every replay (CommStats as the eager steps')
+            with S.ledger.capture() as cap, torch.cuda.graph(self.graph):
                 self.logits = st.step(xs, ys)
         finally:
-            S.ledger.enabled = ledger_on
             S.ctr = None  # the graph keeps the buffer's address; eager calls stay absolute
+        self.charge = cap.charge
         self.delta = {p: S.seq[p] - self.seq0[p] for p in S.seq}
         S.seq = dict(self.seq0)  # nothing consumed until a replay
         self.replays = 0
@@ -603,6 +616,7 @@ class GraphStep:
         self.replays += 1
         for p, d in self.delta.items():
             S.seq[p] += d
+        S.ledger.apply(self.charge)
         return self.logits
 
 
@@ -736,12 +750,13 @@ class TPNet(TrioNet):
                         h = RssTensor(h.data[:, :, tp.slab(h.shape[1])].contiguous(), h.fp)
                         split = True
                 slab = split
-            elif spec.kind == AVGPOOL:
+            elif spec.kind in (AVGPOOL, MAXPOOL):
+                pool = S.avgpool if spec.kind == AVGPOOL else S.maxpool
                 if slab:
-                    h = S.avgpool(h, spec.window, spec.stride, spec.padding)
+                    h = pool(h, spec.window, spec.stride, spec.padding)
                 else:
                     with S.replicated():
-                        h = S.avgpool(h, spec.window, spec.stride, spec.padding)
+                        h = pool(h, spec.window, spec.stride, spec.padding)
             elif spec.kind == RELU:
                 if slab:
                     h = S.relu(h)
@@ -781,14 +796,12 @@ class InferenceGraph:
             net.forward(model, params, x, record=False)  # warm allocations + weight packs outside capture
             self.seq0 = dict(sess.seq)
             self.graph = torch.cuda.CUDAGraph()
-            on = sess.ledger.enabled
-            sess.ledger.enabled = False
             try:
-                with torch.cuda.graph(self.graph):
+                with sess.ledger.capture() as cap, torch.cuda.graph(self.graph):
                     self.logits = net.forward(model, params, x, record=False)[0]
             finally:
-                sess.ledger.enabled = on
                 sess.ctr = None
+            self.charge = cap.charge
         finally:
             self._wpacks = sess._wcache  # the graph reads these buffers: keep them alive
             self._frozen.__exit__(None, None, None)
@@ -808,6 +821,7 @@ class InferenceGraph:
         self.graph.replay()
         for p, d in self.delta.items():
             S.seq[p] += d
+        S.ledger.apply(self.charge)
         return self.logits
 
 
@@ -985,6 +999,8 @@ def infer_plain_float(model: ModelGraph, x: np.ndarray) -> np.ndarray:
             pi += 1
         elif s.kind == AVGPOOL:
             h = F.avg_pool2d(h, s.window, s.stride)
+        elif s.kind == MAXPOOL:
+            h = F.max_pool2d(h, s.window, s.stride, s.padding)
         elif s.kind == RELU:
             h = h * (h >= 0)
         elif s.kind == FLATTEN:
@@ -994,6 +1010,7 @@ def infer_plain_float(model: ModelGraph, x: np.ndarray) -> np.ndarray:
 
 __all__ = [
     "LayerSpec", "ModelGraph", "TrainConfig", "TrainResult", "TrioNet", "TrainState", "avgpool", "backward",
+    "maxpool", "residual",
     "conv2d", "flatten", "forward_private", "fully_connected", "infer_plain_float", "infer_private", "infer_trio",
     "init_params", "init_params_float", "loss_grad_output", "mean_relative_error", "relu", "sgd_step",
     "share_model", "train_private", "train_trio", "one_hot", "cross_entropy", "batch_indices", "moving_average",

@@ -17,7 +17,7 @@ from .sharing import ArithmeticShare, BinaryShare, PartyContext, assemble, split
 
 __all__ = [
     "ExpConfig", "ReciprocalConfig", "a2b", "add_const", "avgpool_shares", "bit_inject", "compare",
-    "conv2d_shares", "division", "drelu", "exp_approx", "matmul_shares", "max_tree", "msb", "mul", "mul_const",
+    "conv2d_shares", "division", "drelu", "exp_approx", "matmul_shares", "max_tree", "maxpool_shares", "msb", "mul", "mul_const",
     "reciprocal", "relu", "relu_with_mask", "softmax", "sub_from_const", "truncate", "truncation_offset",
 ]
 
@@ -38,8 +38,8 @@ def _dev_const(c, shape):
 def add_const(x: ArithmeticShare, c) -> ArithmeticShare:
     """x + public c, the constant in component 0 (held by party 0 as lo and party 2 as hi)."""
     cd = _dev_const(c, x.shape)
-    lo = x.lo + cd if x.owner == 0 else x.lo
-    hi = x.hi + cd if x.owner == 2 else x.hi
+    lo = x.dlo + cd if x.owner == 0 else x.dlo
+    hi = x.dhi + cd if x.owner == 2 else x.dhi
     return ArithmeticShare(x.owner, lo, hi, x.fp)
 
 
@@ -103,6 +103,14 @@ def conv2d_shares(ctx: PartyContext, x: ArithmeticShare, k: ArithmeticShare, str
 
 def avgpool_shares(ctx: PartyContext, x: ArithmeticShare, window, stride=None):
     return _run(ctx, "avgpool", (x,), lambda s, a: s.avgpool(a, tuple(window), tuple(stride or window)))
+
+
+def maxpool_shares(ctx: PartyContext, x: ArithmeticShare, window, stride=None, padding=(0, 0)):
+    """Max-pooling extension (the reference has none): windows flattened
+    row-major into max_tree (protocols.py:356-380); padded positions hold the
+    public constant -2^60 in component 0."""
+    return _run(ctx, "maxpool", (x,), lambda s, a: s.maxpool(a, tuple(window), tuple(stride or window),
+                                                             tuple(padding)))
 
 
 def truncate(ctx: PartyContext, x: ArithmeticShare, bits: int | None = None) -> ArithmeticShare:

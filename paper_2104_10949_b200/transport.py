@@ -127,9 +127,13 @@ class Ledger:
     def __init__(self):
         self.parties = [Transport(i) for i in range(NUM_PARTIES)]
         self.enabled = True
+        self._rec = None
 
     def round(self, label: str, sends=()) -> None:
         """One round: every party marks `label`; sends = [(src, dst, words)]."""
+        if self._rec is not None:
+            self._rec.append((label, tuple(sends)))
+            return
         if not self.enabled:
             return
         for t in self.parties:
@@ -137,6 +141,48 @@ class Ledger:
         for src, dst, words in sends:
             self.parties[src].charge_send(dst, words)
             self.parties[dst].charge_recv(src, words)
+
+    def capture(self):
+        """Context for a CUDA-graph capture: the rounds the captured calls
+        charge are recorded instead of applied; `.charge` (per-party CommStats
+        of one replay) is then applied by `apply` on every replay."""
+        led = self
+
+        class _Cap:
+            charge = None
+
+            def __enter__(self_inner):
+                led._rec = []
+                return self_inner
+
+            def __exit__(self_inner, *exc):
+                rec, led._rec = led._rec, None
+                tmp = [Transport(i) for i in range(NUM_PARTIES)]
+                for label, sends in rec:
+                    for t in tmp:
+                        t.round_mark(label)
+                    for src, dst, words in sends:
+                        tmp[src].charge_send(dst, words)
+                        tmp[dst].charge_recv(src, words)
+                self_inner.charge = [t.stats for t in tmp]
+                return False
+
+        return _Cap()
+
+    def apply(self, charge) -> None:
+        """Add one replay's per-party CommStats (from capture) to the parties."""
+        if not self.enabled or charge is None:
+            return
+        for t, d in zip(self.parties, charge):
+            st = t.stats
+            for k, v in d.bytes_sent.items():
+                st.bytes_sent[k] = st.bytes_sent.get(k, 0) + v
+            for k, v in d.bytes_received.items():
+                st.bytes_received[k] = st.bytes_received.get(k, 0) + v
+            st.messages += d.messages
+            st.messages_received += d.messages_received
+            st.rounds += d.rounds
+            st.round_labels.extend(d.round_labels)
 
     def ring(self, label: str, words: int) -> None:
         """Every party i sends `words` to i+1 (reshare / AND / open)."""

@@ -1,0 +1,231 @@
+"""Golden fixtures at the BASELINE.json configurations, from the REAL reference.
+
+Run in the build container, where /root/reference is readable:
+
+    python tests/golden/make_golden_configs.py [name ...]
+
+Each configuration writes tests/golden/cfg_<name>.npz (arrays + a JSON
+"meta" entry).  These pin the sizes the benchmark times:
+
+* alexnet_b128  — `train_private` (nn.py:679-751), AlexNet-CIFAR, batch 128,
+  1 and 2 iterations, session seed 0, TrainConfig(0.01, 128, n, seed=0), on
+  bench.py's synthetic batch (`default_rng(100)`): SHA-256 of the opened
+  weights after each, plus the cross-entropy history.
+* lenet_b64     — `infer_private` (nn.py:550) of LeNet at batch 64: every
+  party's logit shares (session seed 3, dealer `default_rng(3)`).
+* vgg16ti_b32   — `infer_private` of VGG-16 (avg-pool, Tiny-ImageNet 64x64,
+  200 classes), built from the reference's own LayerSpecs, batch 32: the
+  logit shares (session seed 5, dealer `default_rng(5)`).
+* vgg16ti_train — one `train_private` iteration of the same VGG-16 at batch 32
+  (weights digest).
+* resnet50_b1   — ResNet-50 v1.5 inference at 224x224, batch 1, COMPOSED from
+  the reference's per-party protocols (the reference graph has no residual /
+  bias / padded pool): `conv2d_shares` (protocols.py:120) then
+  a local add of the shared bias, `relu` (:340), zero-padded
+  `avgpool_shares` (:139), `matmul_shares` (:97), residual = local add.
+* maxpool       — max-pooling composed from the reference: per-party window
+  gather (a local structural op) then `max_tree` (protocols.py:356-380) over
+  the flattened (kh, kw) window; padded windows hold the public constant
+  -2^60 in component 0 (sharing.py:184-187).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+sys.path.insert(0, REF)
+sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
+
+import mpc3.protocols as P  # noqa: E402
+from mpc3 import models, nn  # noqa: E402
+from mpc3.ring import fx_encode  # noqa: E402
+from mpc3.session import distribute_input, run_in_process  # noqa: E402
+from mpc3.sharing import ArithmeticShare  # noqa: E402
+
+U64 = np.uint64
+OUT = Path(__file__).resolve().parent
+MAXPOOL_PAD = (1 << 64) - (1 << 60)  # ring encoding of -2^60
+
+
+def digest(ws) -> str:
+    return hashlib.sha256(b"".join(np.ascontiguousarray(x, "<u8").tobytes() for x in ws)).hexdigest()
+
+
+def comps(shares):
+    c = np.stack([s.lo for s in shares])
+    for p in range(3):
+        assert np.array_equal(shares[p].hi, c[(p + 1) % 3])
+    return c
+
+
+def save(name, arrays, meta):
+    np.savez_compressed(OUT / f"cfg_{name}.npz", meta=np.frombuffer(json.dumps(meta).encode(), np.uint8), **arrays)
+    print(f"wrote cfg_{name}.npz: {meta}", flush=True)
+
+
+def vgg16_ti():
+    """VGG-16 (2x2 avg-pool) for Tiny-ImageNet, from the reference's LayerSpecs."""
+    cfg = [64, 64, "P", 128, 128, "P", 256, 256, 256, "P", 512, 512, 512, "P", 512, 512, 512, "P"]
+    layers = []
+    for v in cfg:
+        layers += [nn.avgpool(2)] if v == "P" else [nn.conv2d(v, 3, padding=1), nn.relu()]
+    layers += [nn.flatten(), nn.fully_connected(512), nn.relu(), nn.fully_connected(512), nn.relu(),
+               nn.fully_connected(200)]
+    return nn.ModelGraph(layers, (3, 64, 64))
+
+
+def gen_alexnet_b128():
+    rng = np.random.default_rng(100)  # bench.py _synthetic(128, 100)
+    imgs, labels = rng.uniform(0, 1, (128, 3, 32, 32)), rng.integers(0, 10, 128)
+    meta = {"batch": 128, "session_seed": 0, "cfg_seed": 0, "lr": 0.01, "data": "default_rng(100)"}
+    for iters in (1, 2):
+        cfg = nn.TrainConfig(0.01, 128, iters, 0)
+        t0 = time.time()
+        res = run_in_process(lambda ctx: nn.train_private(ctx, models.alexnet_cifar(), cfg,
+                                                          (imgs, labels) if ctx.party == 0 else None),
+                             seed=0, timeout=60000)
+        meta[f"digest_{iters}"] = digest(res[0].weights)
+        meta[f"ce_{iters}"] = res[0].ce_history
+        meta[f"seconds_{iters}"] = time.time() - t0
+    save("alexnet_b128", {}, meta)
+
+
+def _infer_golden(name, model, batch, seed):
+    w = nn.init_params(model, seed=seed)
+    shape = (batch,) + model.input_shape
+
+    def job(ctx):
+        rin = np.random.default_rng(seed)
+        priv = nn.share_model(ctx, model.with_params(w), rin)
+        x = fx_encode(rin.uniform(0, 1, shape)) if ctx.party == 0 else None
+        xs = distribute_input(ctx, x, rin, shape=shape)
+        return nn.infer_private(ctx, priv, xs)
+
+    t0 = time.time()
+    c = comps(run_in_process(job, seed=seed, timeout=60000))
+    save(name, {"logits": c}, {"batch": batch, "seed": seed, "seconds": time.time() - t0,
+                               "digest": digest([c])})
+
+
+def gen_lenet_b64():
+    _infer_golden("lenet_b64", models.lenet(), 64, 3)
+
+
+def gen_vgg16ti_b32():
+    _infer_golden("vgg16ti_b32", vgg16_ti(), 32, 5)
+
+
+def gen_vgg16ti_train():
+    rng = np.random.default_rng(5)
+    imgs, labels = rng.uniform(0, 1, (32, 3, 64, 64)), rng.integers(0, 200, 32)
+    cfg = nn.TrainConfig(0.01, 32, 1, 5)
+    t0 = time.time()
+    res = run_in_process(lambda ctx: nn.train_private(ctx, vgg16_ti(), cfg, (imgs, labels) if ctx.party == 0 else None),
+                         seed=5, timeout=60000)
+    save("vgg16ti_train", {}, {"batch": 32, "session_seed": 5, "cfg_seed": 5, "lr": 0.01, "data": "default_rng(5)",
+                               "digest": digest(res[0].weights), "ce": res[0].ce_history,
+                               "seconds": time.time() - t0})
+
+
+def _composed_forward(ctx, layers, it, h):
+    """Per-party ResNet extension forward from reference primitives."""
+    from paper_2104_10949_b200 import nn as B
+
+    for L in layers:
+        if L.kind == B.CONV2D:
+            h = P.conv2d_shares(ctx, h, next(it), L.stride, L.padding)
+            if L.bias:
+                b = next(it)
+                h = ArithmeticShare(h.owner, h.lo + b.lo[None, :, None, None], h.hi + b.hi[None, :, None, None], h.fp)
+        elif L.kind == B.FULLY_CONNECTED:
+            w = next(it)
+            h = P.matmul_shares(ctx, h, w.map(lambda v: np.ascontiguousarray(v.T)))
+            if L.bias:
+                b = next(it)
+                h = ArithmeticShare(h.owner, h.lo + b.lo[None, :], h.hi + b.hi[None, :], h.fp)
+        elif L.kind == B.AVGPOOL:
+            ph, pw = L.padding
+            if ph or pw:
+                h = h.map(lambda v: np.pad(v, ((0, 0), (0, 0), (ph, ph), (pw, pw))))
+            h = P.avgpool_shares(ctx, h, L.window, L.stride)
+        elif L.kind == B.RELU:
+            h = P.relu(ctx, h)
+        elif L.kind == B.FLATTEN:
+            h = h.map(lambda v: v.reshape(v.shape[0], -1))
+        elif L.kind == B.RESIDUAL:
+            hm = _composed_forward(ctx, L.main, it, h) if L.main else h
+            hs = _composed_forward(ctx, L.shortcut, it, h) if L.shortcut else h
+            h = hm + hs
+        else:
+            raise ValueError(L.kind)
+    return h
+
+
+def gen_resnet50_b1():
+    from paper_2104_10949_b200 import models as BM
+    from paper_2104_10949_b200 import nn as B
+
+    model = BM.resnet50()
+    w = B.init_params(model, seed=11)
+    shape = (1, 3, 224, 224)
+
+    def job(ctx):
+        rin = np.random.default_rng(11)
+        params = [distribute_input(ctx, w[i] if ctx.party == 0 else None, rin, shape=w[i].shape)
+                  for i in range(len(w))]
+        x = fx_encode(rin.uniform(0, 1, shape)) if ctx.party == 0 else None
+        xs = distribute_input(ctx, x, rin, shape=shape)
+        return _composed_forward(ctx, model.layers, iter(params), xs)
+
+    t0 = time.time()
+    c = comps(run_in_process(job, seed=11, timeout=60000))
+    save("resnet50_b1", {"logits": c}, {"batch": 1, "seed": 11, "seconds": time.time() - t0, "digest": digest([c]),
+                                        "composed": "conv2d_shares+bias, relu, padded avgpool_shares, "
+                                                    "matmul_shares+bias, residual add (reference primitives)"})
+
+
+def maxpool_windows(v, window, stride, padding, pad_value):
+    """(N, C, H, W) -> (N, C, OH, OW, kh*kw) windows, (kh, kw) row-major."""
+    (kh, kw), (sh, sw), (ph, pw) = window, stride, padding
+    if ph or pw:
+        v = np.pad(v, ((0, 0), (0, 0), (ph, ph), (pw, pw)), constant_values=pad_value)
+    win = np.lib.stride_tricks.sliding_window_view(v, (kh, kw), axis=(2, 3))[:, :, ::sh, ::sw]
+    return np.ascontiguousarray(win.reshape(win.shape[:4] + (kh * kw,)))
+
+
+def gen_maxpool():
+    rng = np.random.default_rng(77)
+    cases = {"k3s2p1": ((2, 3, 9, 9), (3, 3), (2, 2), (1, 1)), "k2s2": ((2, 4, 8, 6), (2, 2), (2, 2), (0, 0)),
+             "k3s1": ((1, 2, 7, 7), (3, 3), (1, 1), (0, 0))}
+    arrays, meta = {}, {"pad_value": MAXPOOL_PAD, "seed": 3, "dealer": 7, "cases": {}}
+    for name, (shape, window, stride, padding) in cases.items():
+        x = fx_encode(rng.uniform(-8, 8, shape))
+
+        def job(ctx, x=x, shape=shape, window=window, stride=stride, padding=padding):
+            rin = np.random.default_rng(7)
+            xs = distribute_input(ctx, x if ctx.party == 0 else None, rin, shape=shape)
+            lo_pad = MAXPOOL_PAD if ctx.party == 0 else 0  # component 0 = party 0's lo, party 2's hi
+            hi_pad = MAXPOOL_PAD if ctx.party == 2 else 0
+            win = ArithmeticShare(ctx.party, maxpool_windows(xs.lo, window, stride, padding, lo_pad),
+                                  maxpool_windows(xs.hi, window, stride, padding, hi_pad), xs.fp)
+            return P.max_tree(ctx, win)
+
+        arrays[f"{name}_in"] = x
+        arrays[f"{name}_out"] = comps(run_in_process(job, seed=3))
+        meta["cases"][name] = {"window": window, "stride": stride, "padding": padding}
+    save("maxpool", arrays, meta)
+
+
+GEN = {"alexnet_b128": gen_alexnet_b128, "lenet_b64": gen_lenet_b64, "vgg16ti_b32": gen_vgg16ti_b32,
+       "vgg16ti_train": gen_vgg16ti_train, "resnet50_b1": gen_resnet50_b1, "maxpool": gen_maxpool}
+
+if __name__ == "__main__":
+    for n in sys.argv[1:] or list(GEN):
+        GEN[n]()

@@ -38,9 +38,10 @@ TRIO = {
 
 
 def comps(shares):
-    out = np.stack([s.lo.cpu().numpy().view(U64) for s in shares])
+    out = np.stack([s.lo for s in shares])
     for p in range(3):
-        assert np.array_equal(shares[p].hi.cpu().numpy().view(U64), out[(p + 1) % 3])
+        assert isinstance(shares[p].lo, np.ndarray) and shares[p].lo.dtype == U64  # reference share type
+        assert np.array_equal(shares[p].hi, out[(p + 1) % 3])
     return out
 
 
