@@ -10,13 +10,20 @@ backward, SGD update, all on shares) over one synthetic CIFAR-shaped batch.
 `value`: device-resident dealt batches, CUDA-event timed per step with an L2
 flush (256 MiB write) before each timed step, outside its events; max over
 ranks.  `e2e`: the same step through the public API with host inputs: the
-owner's fx-encoding + dealing on the host, pinned H2D of the shares, the
-step, and the D2H of the opened logits (nn.py:746) inside the timed region.
-Multi-GPU (N>1): each rank trains an independent replica on its own batch
-(replicas; no data-path collective yet — see DESIGN.md), "scaling": "weak".
+owner's images and labels H2D from pinned memory, device fx-encoding and
+dealing, the step, and the D2H of the opened logits (nn.py:746) inside the
+timed region.  `parity`: the first step's opened weights against the REAL
+reference's `train_private` on the same batch (SHA-256 digest pinned in
+tests/golden/cfg_alexnet_b128.npz); no value is printed on a mismatch.
+Multi-GPU (N>1): data parallelism with batch 128 per rank (weak scaling):
+batch shards with PRF words drawn at their global offsets, and an NCCL
+all-reduce of the weight-gradient cross terms before the replicated
+reshare / truncation (nn.DataParallel).
 
-`--impl reference` times the reference algorithm's CPU implementation (the
-oracle port, oracle/nnmirror.py) on the host cores on rank 0 only.
+`--impl reference` runs the reference's own CPU implementation (the
+unmodified `mpc3` package from baseline/_ref: numpy/OpenBLAS limb GEMMs,
+OpenSSL AES, three party threads) through `train_private` at batch 128 on
+rank 0 only; see refarm.py.
 """
 
 from __future__ import annotations
@@ -37,7 +44,8 @@ sys.path.insert(0, ROOT)
 METRIC = "private images/sec (ResNet-50 inf, AlexNet train) at 1/2/4/8 B200; ring-GEMM TOPS"
 UNIT = "images/s"
 BATCH = 128
-CPU_SAMPLE_BATCH = 32
+REF_STEPS_CAP = 3  # reference b128 steps take ~25-40 s each on the host: bounded sample
+SM_COUNT = 148
 
 
 def _args():
@@ -49,7 +57,7 @@ def _args():
     ap.add_argument("--batch", type=int, default=BATCH)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-resnet", action="store_true", help="skip the ResNet-50 inference side measurement")
+    ap.add_argument("--no-side", action="store_true", help="skip the LeNet / VGG / ResNet-50 side measurements")
     return ap.parse_args()
 
 
@@ -63,8 +71,9 @@ def _dist():
 def _config(args, ws):
     return {"workload": "AlexNet-CIFAR private training step (3-party RSS, Z_2^64, t=20)",
             "model": "alexnet_cifar", "global_batch": args.batch * ws, "per_gpu_batch": args.batch,
-            "input": "3x32x32", "classes": 10, "parallelism": f"dp{ws} (batch shards, NCCL all-reduce of weight-"
-                                                             f"gradient cross terms)" if ws > 1 else "single",
+            "input": "3x32x32", "classes": 10,
+            "parallelism": (f"dp{ws} (batch shards, NCCL all-reduce of weight-gradient cross terms)"
+                            if ws > 1 else "single"),
             "l2": "flushed (256 MiB write) before every timed step, outside its events"}
 
 
@@ -73,43 +82,68 @@ def _synthetic(batch, seed):
     return rng.uniform(0, 1, (batch, 3, 32, 32)), rng.integers(0, 10, batch)
 
 
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        return {}
+
+
 # ---------------------------------------------------------------------------
-# CPU: the reference algorithm (oracle port)
+# CPU: the reference's own implementation (refarm.py), or the oracle port
 
 
-def cpu_steps(batch, steps, warmup):
+def cpu_alexnet(batch: int, steps: int):
+    """(images/s, seconds per step, kind, sample) of the reference's
+    AlexNet-CIFAR train_private at `batch`, `steps` iterations in one call,
+    after one untimed warm-up iteration at batch 4."""
+    import refarm
+
+    imgs, labels = _synthetic(batch, 100)
+    mod, src = refarm.load()
+    if mod is not None:
+        refarm.alexnet_train(4, 1, imgs[:4], labels[:4])  # warm-up: imports, BLAS, code paths
+        dt = refarm.alexnet_train(batch, steps, imgs, labels)
+        return (batch * steps / dt, dt / steps, "reference",
+                f"unmodified reference mpc3 ({os.path.relpath(src, ROOT) if src.startswith(ROOT) else src}): "
+                f"run_in_process + nn.train_private(AlexNet-CIFAR, batch {batch}, {steps} iteration(s) in one call, "
+                f"incl. weight dealing and the final open, <1%), after 1 untimed warm-up iteration at batch 4")
+    # the reference is not importable: the oracle port (oracle/nnmirror.py), same schedule
     from oracle import nnmirror as N
     from oracle import rss as R
 
     layers, ish = N.alexnet_cifar()
-    imgs, labels = _synthetic(batch, 0)
+    N.TrainLoop(R.Session(1), layers, ish, 0.01, 4).step(imgs[:4], labels[:4])
     loop = N.TrainLoop(R.Session(0), layers, ish, 0.01, batch)
-    if warmup:
-        wi, wl = _synthetic(4, 1)
-        wloop = N.TrainLoop(R.Session(1), layers, ish, 0.01, 4)
-        for _ in range(warmup):
-            wloop.step(wi, wl)
     t0 = time.perf_counter()
     for _ in range(steps):
         loop.step(imgs, labels)
     dt = time.perf_counter() - t0
-    return batch * steps / dt, dt / steps
+    return (batch * steps / dt, dt / steps, "port",
+            f"oracle port of the reference (numpy/OpenBLAS float-limb restatement; the reference itself: {src}), "
+            f"AlexNet-CIFAR batch {batch}, {steps} step(s), after 1 warm-up step at batch 4")
 
 
 def run_reference(args, ws, rank):
     if rank != 0:
         return
-    steps = max(1, args.steps)
-    value, per_step = cpu_steps(CPU_SAMPLE_BATCH, steps, min(args.warmup, 1))
-    cores = os.cpu_count()
+    import refarm
+
+    steps = max(1, min(args.steps, REF_STEPS_CAP))
+    value, per_step, kind, sample = cpu_alexnet(args.batch, steps)
+    th = refarm.threads()
+    cfg = _config(args, 1)
+    cfg["l2"] = "n/a (CPU)"
+    cfg["parallelism"] = "3 party threads + OpenBLAS threads on the host"
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": steps, "warmup": args.warmup,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": steps, "warmup": 1,
+        "requested": {"steps": args.steps, "warmup": args.warmup,
+                      "note": f"steps capped at {REF_STEPS_CAP} (each is a full batch-{args.batch} reference step); "
+                              f"warm-up = 1 iteration at batch 4"},
         "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "u64 ring (int)", "data": "synthetic", "config": _config(args, ws), "impl": "reference",
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"AlexNet-CIFAR private train step at batch {CPU_SAMPLE_BATCH} per step "
-                                   f"(numpy/OpenBLAS float-limb restatement of the reference, 3 party threads "
-                                   f"for bilinear ops; warm-up at batch 4)"},
+        "dtype": "u64 ring (int)", "data": "synthetic", "config": cfg, "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": th["cores"], "kind": kind, "sample": sample,
+                         "threads": th},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -202,6 +236,215 @@ class NvmlClocks(Clocks):
                 "reasons": sorted(self.reasons), "samples": len(self.samples), "source": "NVML"}
 
 
+# -- per-launch instrumentation (outside every timed region) ------------------
+
+GEMM_CALLS = ("mpc3_ring_gemm_auto", "mpc3_ring_gemm_auto_z", "mpc3_ring_gemm_t", "mpc3_ring_gemm_t_z")
+SIGN_CALLS = ("mpc3_rss_sign", "mpc3_rss_layer_sign", "mpc3_rss_max_tree", "mpc3_rss_max_level")
+PACK_CALLS = ("mpc3_ring_pack", "mpc3_ring_pack_halves", "mpc3_ring_pack_halves_z", "mpc3_rss_window_gather")
+
+
+def _category(name: str) -> str:
+    if name in GEMM_CALLS:
+        return "gemm"
+    if name in SIGN_CALLS:
+        return "sign"
+    if name in PACK_CALLS:
+        return "pack"
+    if name.startswith("mpc3_ring_"):
+        return "local"
+    return "protocol"
+
+
+def _view_numel(view) -> int:
+    n = 1
+    for d in view._obj.full:
+        n *= int(d)
+    return n
+
+
+class Recorder:
+    """Wraps the C-ABI entry so that, while `on`, every launch is bracketed
+    by CUDA events on its launch stream (torch's current stream: the
+    instrumented pass runs with streams serialised) and its algorithmic work
+    is recorded: ring-GEMM int8 ops (72 per ring MAC x groups*M*N*2K) and
+    sign-circuit AES blocks (23 per ReLU element, 25.5 with a fused layer
+    epilogue; max_tree: 23 per pair compared).  While not `on`, it only
+    counts launches (gpu_launches)."""
+
+    def __init__(self, capi, engine):
+        self.capi, self.engine = capi, engine
+        self.orig = capi.call
+        self.on = False
+        self.count = 0
+        self.k = 0
+        self.events = []  # (name, category, e0, e1, work, shape)
+        capi.call = self.call
+        engine.K.call = self.call
+
+    def restore(self):
+        self.capi.call = self.orig
+        self.engine.K.call = self.orig
+
+    def call(self, name, *a):
+        if name != "mpc3_aes128_expand":
+            self.count += 1
+        if not self.on:
+            return self.orig(name, *a)
+        import torch
+
+        if name in ("mpc3_ring_pack", "mpc3_ring_pack_halves", "mpc3_ring_pack_halves_z") and a[3] in (0, 1, 3):
+            self.k = int(a[2]._obj.k)  # logical K of the cross-term operand (inner length 2K)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        self.orig(name, *a)
+        e1.record()
+        work, shape = self._work(name, a)
+        self.events.append((name, _category(name), e0, e1, work, shape))
+
+    def _work(self, name, a):
+        if name == "mpc3_rss_sign":
+            return 23.0 * int(a[9]), (int(a[9]),)
+        if name == "mpc3_rss_layer_sign":
+            n = _view_numel(a[7])
+            return 25.5 * n, (n,)
+        if name == "mpc3_rss_max_level":
+            n = int(a[7]) * (int(a[8]) // 2)
+            return 23.0 * n, (n,)
+        if name == "mpc3_rss_max_tree":
+            rows, m, pairs = int(a[9]), int(a[10]), 0
+            while m > 1:
+                pairs += rows * (m // 2)
+                m = m // 2 + m % 2
+            return 23.0 * pairs, (pairs,)
+        if name.startswith("mpc3_ring_gemm_t"):
+            groups, M, N, kc_half = int(a[11]), int(a[12]), int(a[13]), int(a[14])
+            rows = int(a[2]) if int(a[1]) & 1 else (int(a[7]) if a[6] else (self.k or kc_half))
+            return 72.0 * groups * M * N * 2 * rows, (groups, M, N, 2 * rows)
+        if name.startswith("mpc3_ring_gemm_auto"):
+            groups, M, N = int(a[3]), int(a[4]), int(a[5])
+            k = self.k if self.k else int(a[6]) // 2
+            return 72.0 * groups * M * N * 2 * k, (groups, M, N, 2 * k)
+        return 0.0, ()
+
+    def summary(self, step_ms: float) -> dict:
+        """Per-category kernel time of the instrumented pass and its share."""
+        cats = {}
+        for name, cat, e0, e1, work, shape in self.events:
+            ms = e0.elapsed_time(e1)
+            c = cats.setdefault(cat, {"ms": 0.0, "launches": 0, "work": 0.0})
+            c["ms"] += ms
+            c["launches"] += 1
+            c["work"] += work
+        total = sum(c["ms"] for c in cats.values())
+        for c in cats.values():
+            c["share_of_kernel_time"] = c["ms"] / total if total else None
+            c["share_of_step"] = c["ms"] / step_ms if step_ms else None
+        return {"categories": cats, "kernel_ms": total}
+
+    def per_launch(self, cat: str, top: int = 5):
+        rows = []
+        for name, c, e0, e1, work, shape in self.events:
+            if c != cat:
+                continue
+            us = e0.elapsed_time(e1) * 1e3
+            rows.append({"call": name[len("mpc3_"):], "shape": list(shape), "us": round(us, 2),
+                         "rate": round(work / (us / 1e6) / (1e12 if cat == "gemm" else 1e9), 2) if us else None})
+        rows.sort(key=lambda r: -r["us"])
+        return rows[:top]
+
+
+def lsu_aes_peak(sm_mhz: float) -> float:
+    """Hardware ceiling of T-table AES-128 on B200 (G blocks/s): each block
+    is 160 table lookups (16 per round x 10); the shared-memory pipe serves
+    one conflict-free 32-lane LDS per SM per clock (the tables are laid out
+    so lane l always hits bank l) = 32 lookups / clk / SM."""
+    return SM_COUNT * sm_mhz * 1e6 * 32 / 160 / 1e9
+
+
+def roofline_of(rec: Recorder, summ: dict, peaks: dict, sm_mhz: float, traffic: dict) -> dict:
+    """The roofline object for the dominant kernel class by share of the
+    instrumented pass's kernel time (ring GEMM vs sign circuit), the other
+    as `secondary`."""
+    cats = summ["categories"]
+    int8_peak = 2.0 * peaks.get("bf16_tflops", 2250.0 * 0.7225)  # dense int8 = 2x dense bf16 on B200
+    out = {}
+    g = cats.get("gemm")
+    if g and g["ms"]:
+        per = g["work"] / g["launches"] / (g["ms"] / g["launches"] / 1e3) / 1e12
+        out["gemm"] = {
+            "kernel": "gemm_tc_kernel (tcgen05.mma kind::i8, 8 TMEM diagonal accumulators, TMA)",
+            "bound": "tensor", "achieved": per, "peak": int8_peak, "unit": "TFLOP/s", "frac": per / int8_peak,
+            "traffic": traffic.get("gemm"), "launches": g["launches"], "kernel_ms_per_step": g["ms"],
+            "share_of_kernel_time": g["share_of_kernel_time"], "share_of_step": g["share_of_step"],
+            "algorithmic": "72 int8 ops per ring MAC x groups*M*N*2K per launch (TFLOP/s = int8 TOPS)",
+            "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (dense int8 = 2 x dense bf16 on B200)",
+            "top_launches": rec.per_launch("gemm"),
+        }
+    s = cats.get("sign")
+    if s and s["ms"]:
+        rate = s["work"] / (s["ms"] / 1e3) / 1e9
+        peak = lsu_aes_peak(sm_mhz)
+        out["sign"] = {
+            "kernel": "sign circuit (a2b + Kogge-Stone + bit_inject + ReLU mask, AES-128-CTR inline; "
+                      "mpc3_rss_sign / mpc3_rss_layer_sign / max_tree)",
+            "bound": "aes (shared-memory LSU pipe: 160 T-table lookups per AES block)", "achieved": rate,
+            "peak": peak, "unit": "G AES blocks/s", "frac": rate / peak, "traffic": traffic.get("sign"),
+            "launches": s["launches"], "kernel_ms_per_step": s["ms"],
+            "share_of_kernel_time": s["share_of_kernel_time"], "share_of_step": s["share_of_step"],
+            "algorithmic": "23 AES blocks per ReLU element (25.5 with the fused layer reshare + truncation); "
+                           "HBM traffic is 48-72 B per element (not the bound)",
+            "peak_source": f"{SM_COUNT} SMs x {sm_mhz:.0f} MHz x 32 lookups/clk / 160 lookups per block",
+            "top_launches": rec.per_launch("sign"),
+        }
+    if not out:
+        return {}
+    dom = max(out, key=lambda k: out[k]["share_of_kernel_time"] or 0)
+    r = dict(out[dom])
+    r["dominant_by"] = "largest share of the instrumented step's kernel time"
+    r["measured"] = ("per-launch CUDA events on the launch stream in one eager pass after the timed region "
+                     "(streams serialised, enqueued behind a GPU spin so the events bracket each kernel alone)")
+    r["kernel_time_by_category"] = {k: {"ms": round(v["ms"], 4), "share": round(v["share_of_kernel_time"], 4),
+                                        "launches": v["launches"]} for k, v in summ["categories"].items()}
+    others = [k for k in out if k != dom]
+    if others:
+        r["secondary"] = out[others[0]]
+    return r
+
+
+def _traffic():
+    """ncu dram__bytes_read.sum + dram__bytes_write.sum per launch from the
+    committed profiles (tools/traffic.py), keyed by kernel class."""
+    t = {}
+    for cls, fn in (("gemm", "r02_traffic_gemm.json"), ("sign", "r02_traffic_sign.json"),
+                    ("gemm", "r01_gemm_traffic.json")):
+        if cls in t:
+            continue
+        try:
+            tj = json.load(open(os.path.join(ROOT, "profiles", fn)))
+            t[cls] = tj["traffic_bytes_per_launch"]
+        except (OSError, KeyError, ValueError):
+            pass
+    return t
+
+
+def _instrumented(fn, rec, torch):
+    """One eager pass of fn with per-launch events, streams serialised."""
+    from paper_2104_10949_b200 import engine
+    from paper_2104_10949_b200 import nn as nn_mod
+
+    saved = (nn_mod.OVERLAP, engine.OVERLAP_PACK)
+    nn_mod.OVERLAP, engine.OVERLAP_PACK = False, False
+    rec.events.clear()
+    rec.on = True
+    try:
+        torch.cuda._sleep(int(2e8))  # ~0.1 s of GPU spin: the host enqueues the whole pass behind it
+        fn()
+        torch.cuda.synchronize()
+    finally:
+        rec.on = False
+        nn_mod.OVERLAP, engine.OVERLAP_PACK = saved
+
+
 def run_b200(args, ws, rank, local):
     import torch
 
@@ -220,77 +463,59 @@ def run_b200(args, ws, rank, local):
     # equal contiguous batch shard; weight-gradient cross terms are summed with
     # NCCL before the replicated reshare/truncation (nn.DataParallel)
     sess = M.TrioSession(seed=0)
+    comm = None
     if ws > 1:
         from paper_2104_10949_b200.nn import DataParallel
 
         sess.dp = DataParallel.nccl()
+        comm = {"backend": torch.distributed.get_backend(), "world_size": torch.distributed.get_world_size(),
+                "rank": rank, "collective": "all_reduce(sum, int64) of weight-gradient cross terms"}
     model = M.alexnet_cifar()
     cfg = M.TrainConfig(0.01, b * ws, args.warmup + args.steps, seed=0)  # global batch b * ws
     st = TrainState(sess, model, cfg)
+    # rank r's shard of the global batch; at N=1 exactly the fixture's batch (default_rng(100))
     imgs, labels = _synthetic(b, 100 + rank)
     xe, ye = M.fx_encode(imgs), M.fx_encode(one_hot(labels, 10))
 
     # device-resident dealt batches (dealing outside the timed region)
     batches = [st.deal_batch(xe, ye) for _ in range(args.warmup + args.steps)]
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
-    counter = {"n": 0}
-    orig_call = _capi.call
+    rec = Recorder(_capi, engine)
 
-    def counting_call(name, *a):
-        if name not in ("mpc3_aes128_expand",):
-            counter["n"] += 1
-        return orig_call(name, *a)
+    # parity: the first step (eager) from the dealt initial weights is the
+    # reference's train_private iteration 0 on the same batch
+    parity = {"status": "not checked"}
 
-    # roofline instrumentation: CUDA events around every launch of the
-    # dominant kernel (the tcgen05 ring GEMM) and of the fused sign circuit,
-    # on their launch stream (torch's current stream)
-    gemm_events, sign_events, gemm_bytes, gemm_shapes = [], [], [], []
-    instrument = {"on": False, "k": 0}
-
-    def traced_call(name, *a):
-        if instrument["on"] and name in ("mpc3_ring_pack", "mpc3_ring_pack_halves", "mpc3_ring_pack_halves_z") \
-                and a[3] in (0, 1, 3):
-            instrument["k"] = int(a[2]._obj.k)  # logical K of the cross-term operand (inner length 2K)
-        if instrument["on"] and name in ("mpc3_rss_sign", "mpc3_rss_layer_sign", "mpc3_ring_gemm_auto",
-                                         "mpc3_ring_gemm_auto_z", "mpc3_ring_gemm_t", "mpc3_ring_gemm_t_z"):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            counting_call(name, *a)
-            e1.record()
-            if name == "mpc3_rss_sign":  # 23 AES blocks per element
-                sign_events.append((e0, e1, int(a[9]), 23.0 * int(a[9])))
-            elif name == "mpc3_rss_layer_sign":  # + the fused layer epilogue's 2.5 blocks per element
-                n_el = 1
-                for d in a[7]._obj.full:
-                    n_el *= int(d)
-                sign_events.append((e0, e1, n_el, 25.5 * n_el))
-            elif name.startswith("mpc3_ring_gemm_t"):  # transposed operands: the contraction is an MN operand's rows
-                groups, M, N, kc_half = int(a[11]), int(a[12]), int(a[13]), int(a[14])
-                # contraction per half: an MN operand's source rows, else the logical K of the
-                # operand packed just before (a_mn bit 1 = component-plane A, K-major when bit 0 is 0)
-                rows = int(a[2]) if int(a[1]) & 1 else (int(a[7]) if a[6] else (instrument["k"] or kc_half))
-                gemm_events.append((e0, e1, 72 * groups * M * N * 2 * rows))
-                gemm_bytes.append(groups * ((M + N) * 8 * 2 * kc_half + M * N * 8))
-                gemm_shapes.append((name, groups, M, N, 2 * rows))
-            else:  # groups x M x N x 2K ring MACs, 72 int8 ops each (36 limb-pair MACs)
-                groups, M, N = int(a[3]), int(a[4]), int(a[5])
-                sign_k = instrument["k"] if instrument["k"] else int(a[6]) // 2
-                kp = int(a[6])
-                gemm_events.append((e0, e1, 72 * groups * M * N * 2 * sign_k))
-                gemm_bytes.append(groups * ((M + N) * 8 * kp + M * N * 8))  # packed A, B (8 limb planes) + C
-                gemm_shapes.append((name, groups, M, N, 2 * sign_k))
+    def check_parity():
+        if ws != 1 or b != BATCH:
+            parity["status"] = "not checked (no fixture for this global batch)"
             return
-        return counting_call(name, *a)
+        import hashlib
 
-    _capi.call = traced_call
-    engine.K.call = traced_call
+        try:
+            z = np.load(os.path.join(ROOT, "tests", "golden", "cfg_alexnet_b128.npz"))
+            want = json.loads(bytes(z["meta"]).decode())["digest_1"]
+        except (OSError, KeyError, ValueError):
+            parity["status"] = "not checked (fixture missing)"
+            return
+        got = hashlib.sha256(b"".join(np.ascontiguousarray(sess.reveal(p), "<u8").tobytes()
+                                      for p in st.params)).hexdigest()
+        parity.update({"status": "ok" if got == want else "MISMATCH", "digest": got[:16],
+                       "against": "SHA-256 of the opened weights after step 1 vs the reference's train_private "
+                                  "(tests/golden/cfg_alexnet_b128.npz, make_golden_configs.py)"})
 
-    for i in range(max(0, args.warmup - 1)):
+    # a CUDA-graph replay needs the previous replay's counters: eager warm-up
+    # steps first (the first one checked), then one graph capture
+    n_eager = max(1, args.warmup - 1)
+    for i in range(n_eager):
         st.step(*batches[i])
-    # capture one iteration as a CUDA graph (static input buffers)
+        if i == 0:
+            check_parity()
+    if parity["status"] == "MISMATCH":
+        raise SystemExit(f"[bench] parity check failed: {parity}")
     xs_static = engine.RssTensor(batches[0][0].data.clone())
     ys_static = engine.RssTensor(batches[0][1].data.clone())
-    counter["n"] = 0
+    rec.count = 0
     try:
         graph = st.capture(xs_static, ys_static)
     except Exception as e:  # noqa: BLE001 - e.g. a collective that refuses capture: time eagerly
@@ -302,7 +527,7 @@ def run_b200(args, ws, rank, local):
                 return st.step(xs_static, ys_static)
 
         graph = _Eager()
-    launches_per_step = counter["n"]
+    launches_per_step = rec.count
     graph.replay()  # last warm-up step, through the graph
     torch.cuda.synchronize()
     if ws > 1:
@@ -311,7 +536,7 @@ def run_b200(args, ws, rank, local):
     step_ms = []
     for i in range(args.steps):
         flush.zero_()
-        xb, yb = batches[args.warmup + i]
+        xb, yb = batches[min(n_eager + i, len(batches) - 1)]
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         xs_static.data.copy_(xb.data)
@@ -323,27 +548,6 @@ def run_b200(args, ws, rank, local):
     torch.cuda.synchronize()
     clk = clocks.stop()
     launches = launches_per_step * args.steps
-    # eager instrumented pass (outside the timed region): per-launch CUDA
-    # events around the dominant kernel on its launch stream
-    # The GPU is first held by a spin kernel long enough for the host to
-    # enqueue the whole step, so each launch's events bracket device time
-    # only (no host enqueue gaps inside them).
-    # Streams are serialised for this pass (no side-stream overlap), so each
-    # kernel's events measure it alone.
-    from paper_2104_10949_b200 import nn as nn_mod
-
-    saved = (nn_mod.OVERLAP, engine.OVERLAP_PACK)
-    nn_mod.OVERLAP, engine.OVERLAP_PACK = False, False
-    instrument["on"] = True
-    torch.cuda._sleep(int(2e8))  # ~0.1 s of GPU spin
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    st.step(*batches[-1])
-    e1.record()
-    torch.cuda.synchronize()
-    instrument["on"] = False
-    nn_mod.OVERLAP, engine.OVERLAP_PACK = saved
-    eager_ms = e0.elapsed_time(e1)
     total_ms = float(sum(step_ms))
     if ws > 1:
         t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
@@ -352,226 +556,202 @@ def run_b200(args, ws, rank, local):
         torch.distributed.barrier()
     value = b * args.steps * ws / (total_ms / 1e3)
 
-    # roofline of the dominant kernel (largest share of the step): the
-    # tcgen05 ring GEMM, tensor-bound.  Algorithmic work per launch =
-    # 72 int8 ops (36 u8 x u8 limb-pair MACs) per ring MAC x groups * M * N * 2K.
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except OSError:
-        pass
-    traffic = {}
-    try:  # one ncu capture of the same step's GEMM launches (tools/traffic.py)
-        tj = json.load(open(os.path.join(ROOT, "profiles", "r01_gemm_traffic.json")))
-        traffic = {"traffic_bytes_per_launch": tj["traffic_bytes_per_launch"],
-                   "source_note": "profiles/r01_gemm_traffic.json: ncu dram__bytes_read.sum + dram__bytes_write.sum, "
-                                  f"mean over the {tj['launches']} GEMM launches of one AlexNet step"}
-    except (OSError, KeyError, ValueError):
-        pass
-    gemm_ms = sum(a.elapsed_time(c) for a, c, _ in gemm_events)
-    gemm_ops = sum(w for _, _, w in gemm_events)
-    nl = max(1, len(gemm_events))
-    int8_peak = 2.0 * peaks.get("bf16_tflops", 2250.0 * 0.7225)  # dense int8 = 2x dense bf16 on B200
-    achieved = (gemm_ops / nl) / (gemm_ms / nl / 1e3) / 1e12 if gemm_ms else None
-    roofline = {"kernel": "gemm_tc_kernel (tcgen05.mma kind::i8, 8 TMEM diagonal accumulators, TMA SWIZZLE_32B)",
-                "bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TFLOP/s",
-                "frac": (achieved / int8_peak) if achieved else None,
-                "traffic": traffic.get("traffic_bytes_per_launch"),
-                "traffic_source": traffic.get("source_note"),
-                "operand_bytes_per_launch": sum(gemm_bytes) / nl if gemm_bytes else None,
-                "peak_source": ("2 x MEASURED_PEAKS.json bf16_tflops (dense int8 = 2x dense bf16 on B200; "
-                                "cuBLASLt int8 measured 2,924-3,063 TOPS, profiles/r01_microbench_quick.json)"),
-                "launches": len(gemm_events), "kernel_ms_per_step": gemm_ms,
-                "per_launch": [{"call": nm[len("mpc3_ring_"):], "groups": g_, "M": m_, "N": n_, "K2": k_,
-                                "us": round(a.elapsed_time(c) * 1e3, 2),
-                                "tops": round(w / (a.elapsed_time(c) / 1e3) / 1e12, 1)}
-                               for (a, c, w), (nm, g_, m_, n_, k_) in zip(gemm_events, gemm_shapes)],
-                "share_of_step": gemm_ms / max(total_ms / args.steps, 1e-9),
-                "algorithmic": "72 int8 ops per ring MAC x groups*M*N*2K per launch (TOPS; TFLOP/s column = int8 TOPS)",
-                "measured": "per-launch CUDA events on the launch stream in one eager step after the graph-timed region "
-                            "(streams serialised, enqueued behind a GPU spin: the events bracket each kernel alone)"}
-    # secondary bound: the nonlinear layers are AES-bound (23 AES-128 blocks
-    # per ReLU element); peak = the standalone AES-CTR keystream kernel's rate
-    sign_ms = sum(a.elapsed_time(c) for a, c, _, _ in sign_events)
-    sign_elems = sum(n for _, _, n, _ in sign_events)
-    sign_blocks = sum(bl for _, _, _, bl in sign_events)
-    aes_peak = _aes_peak_gblocks()
-    aes_rate = sign_blocks / (sign_ms / 1e3) / 1e9 if sign_ms else None
-    roofline["secondary"] = {"kernel": "sign circuit (a2b + Kogge-Stone + bit_inject + ReLU, AES-CTR inline; "
-                                       "with the layer epilogue fused for large outputs: mpc3_rss_layer_sign)",
-                             "bound": "aes", "achieved": aes_rate, "peak": aes_peak, "unit": "G AES blocks/s",
-                             "frac": aes_rate / aes_peak if aes_rate and aes_peak else None,
-                             "share_of_step": sign_ms / max(total_ms / args.steps, 1e-9),
-                             "hbm_gbs": 72.0 * sign_elems / (sign_ms / 1e3) / 1e9 if sign_ms else None,
-                             "peak_source": "mpc3_prf_words AES-128-CTR keystream kernel, 2^27 blocks, this run"}
+    # roofline: one eager instrumented step after the timed region
+    peaks = _peaks()
+    sm_mhz = float(clk.get("sm_mhz") or peaks.get("sm_max_mhz") or 1965.0)
+    _instrumented(lambda: st.step(*batches[-1]), rec, torch)
+    summ = rec.summary(total_ms / args.steps)
+    roofline = roofline_of(rec, summ, peaks, sm_mhz, _traffic())
+    rec.events.clear()
 
     # end-to-end through the public API with host inputs
-    e2e = None
-    if not args.no_e2e:
-        _capi.call = orig_call
-        engine.K.call = orig_call
-        # the owner's raw inputs arrive from pinned host memory every step: the
-        # float64 images (encoded on the device, ring.py:104-115) and the
-        # one-hot labels; the dealer (PCG64, bit-exact with numpy) runs on the
-        # device; the step's opened logits (nn.py:746) come back to the host.
-        # Double-buffered: step i's host->device copy (own stream) overlaps
-        # step i-1's graph; step i's opened logits are read back once its D2H
-        # event completes (two steps later at the latest).  Every step copies
-        # its own inputs in and its own result out.
-        nbuf = 2
-        pin_img = [torch.empty(imgs.shape, dtype=torch.float64).pin_memory() for _ in range(nbuf)]
-        pin_lab = [torch.empty((b, 10), dtype=torch.float64).pin_memory() for _ in range(nbuf)]
-        out_host = [torch.empty((b, 10), dtype=torch.int64).pin_memory() for _ in range(nbuf)]
-        dev_img = [torch.empty(imgs.shape, dtype=torch.float64, device=dev) for _ in range(nbuf)]
-        dev_lab = [torch.empty((b, 10), dtype=torch.float64, device=dev) for _ in range(nbuf)]
-        copy_stream = torch.cuda.Stream(device=dev)
-        done = [None] * nbuf
-        results = []
-        bad = torch.zeros(1, dtype=torch.int32, device=dev)
-        rng = st.rng
-        onehot = one_hot(labels, 10)
-
-        def e2e_step(i):
-            k = i % nbuf
-            if done[k] is not None:  # slot free: step i-2's logits are on the host
-                done[k].synchronize()
-                results.append(out_host[k].numpy().view(np.uint64).copy())
-            pin_img[k].numpy()[...] = imgs
-            pin_lab[k].numpy()[...] = onehot
-            with torch.cuda.stream(copy_stream):
-                dev_img[k].copy_(pin_img[k], non_blocking=True)
-                dev_lab[k].copy_(pin_lab[k], non_blocking=True)
-                h2d = torch.cuda.Event()
-                h2d.record(copy_stream)
-            main = torch.cuda.current_stream()
-            main.wait_event(h2d)
-            x_enc = sess.fx_encode_device(dev_img[k], bad)
-            y_enc = sess.fx_encode_device(dev_lab[k], bad)
-            xs_static.data.copy_(sess.share_device(x_enc, rng).data)
-            ys_static.data.copy_(sess.share_device(y_enc, rng).data)
-            logits = graph.replay()
-            out_host[k].copy_(engine.reconstruct_device(logits).view(b, 10), non_blocking=True)
-            done[k] = torch.cuda.Event()
-            done[k].record(main)
-
-        def drain():
-            for k in range(nbuf):
-                if done[k] is not None:
-                    done[k].synchronize()
-                    done[k] = None
-
-        for i in range(2):
-            e2e_step(i)
-        drain()
-        if ws > 1:
-            torch.distributed.barrier()
-        torch.cuda.synchronize()
-        results.clear()
-        t0 = time.perf_counter()
-        for i in range(args.steps):
-            e2e_step(i)
-        for k in range(nbuf):  # the last steps' logits
-            if done[k] is not None:
-                done[k].synchronize()
-                results.append(out_host[k].numpy().view(np.uint64).copy())
-        dt = time.perf_counter() - t0
-        assert len(results) == args.steps
-        if ws > 1:
-            t = torch.tensor([dt], device=dev, dtype=torch.float64)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            dt = float(t.item())
-        e2e = {"value": b * args.steps * ws / dt, "unit": UNIT,
-               "h2d_bytes_per_step": int(pin_img[0].numel() * 8 + pin_lab[0].numel() * 8),
-               "d2h_bytes_per_step": int(out_host[0].numel() * 8),
-               "note": "per step: host images+labels into pinned memory, H2D on a copy stream (double-buffered, "
-                       "overlapping the previous step), device fx-encode, device PCG64 dealer (bit-exact with "
-                       "sharing.py:113-118), graph step, opened logits D2H read on the host; wall clock"}
-        if int(bad.item()):
-            raise RuntimeError("input outside the encodable range")
+    e2e = None if args.no_e2e else _e2e(args, ws, dev, sess, st, graph, xs_static, ys_static, imgs, labels, b)
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        v, _ = cpu_steps(CPU_SAMPLE_BATCH, 1, 0)
-        cpu = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-               "sample": f"one AlexNet-CIFAR private train step at batch {CPU_SAMPLE_BATCH} "
-                         f"(oracle port of the reference, numpy/OpenBLAS, 3 party threads)"}
+        import refarm
+
+        v, per, kind, sample = cpu_alexnet(b, 1)
+        cpu = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": kind, "sample": sample,
+               "threads": refarm.threads()}
 
     also = {}
-    if not args.no_resnet:
-        try:
-            also["lenet_b64"] = lenet_inference(dev)
-            also["vgg16_ti_b32"] = vgg16_ti(dev)
-        except Exception as e:  # noqa: BLE001 - reported, not fatal to the headline
-            also["side_error"] = repr(e)[:300]
-        try:
-            also["resnet50_b64"] = resnet50_inference(dev, 64, 2, use_graph=True)
-            also["resnet50_b1"] = resnet50_inference(dev, 1, 5, use_graph=True)
-        except Exception as e:  # noqa: BLE001 - reported, not fatal to the headline
-            also["resnet50_error"] = repr(e)[:300]
+    if not args.no_side:
+        also = side_measurements(dev, ws, rank, rec, peaks, sm_mhz, args)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64 ring (int)", "data": "synthetic",
+            "config": _config(args, ws), "parity": parity, "clocks": clk, "gpu_launches": launches,
+            "e2e": e2e, "cpu_baseline": cpu, "comm": comm, "roofline": roofline,
+            "step_ms": [round(v, 3) for v in step_ms],
+            "also": also,
+        }
+        print(json.dumps(line), flush=True)
+    rec.restore()
+    if ws > 1:
+        torch.distributed.destroy_process_group()
 
-    if ws > 1 and not args.no_resnet:
+
+def _e2e(args, ws, dev, sess, st, graph, xs_static, ys_static, imgs, labels, b):
+    """The owner's raw inputs arrive from pinned host memory every step: the
+    float64 images (encoded on the device, ring.py:104-115) and the one-hot
+    labels; the dealer (PCG64, bit-exact with numpy) runs on the device; the
+    step's opened logits (nn.py:746) come back to the host.  Double-buffered:
+    step i's host->device copy (own stream) overlaps step i-1's graph; step
+    i's opened logits are read back once its D2H event completes (two steps
+    later at the latest).  Every step copies its own inputs in and its own
+    result out."""
+    import torch
+
+    from paper_2104_10949_b200 import engine
+    from paper_2104_10949_b200.nn import one_hot
+
+    nbuf = 2
+    pin_img = [torch.empty(imgs.shape, dtype=torch.float64).pin_memory() for _ in range(nbuf)]
+    pin_lab = [torch.empty((b, 10), dtype=torch.float64).pin_memory() for _ in range(nbuf)]
+    out_host = [torch.empty((b, 10), dtype=torch.int64).pin_memory() for _ in range(nbuf)]
+    dev_img = [torch.empty(imgs.shape, dtype=torch.float64, device=dev) for _ in range(nbuf)]
+    dev_lab = [torch.empty((b, 10), dtype=torch.float64, device=dev) for _ in range(nbuf)]
+    copy_stream = torch.cuda.Stream(device=dev)
+    done = [None] * nbuf
+    results = []
+    bad = torch.zeros(1, dtype=torch.int32, device=dev)
+    rng = st.rng
+    onehot = one_hot(labels, 10)
+
+    def e2e_step(i):
+        k = i % nbuf
+        if done[k] is not None:  # slot free: step i-2's logits are on the host
+            done[k].synchronize()
+            results.append(out_host[k].numpy().view(np.uint64).copy())
+        pin_img[k].numpy()[...] = imgs
+        pin_lab[k].numpy()[...] = onehot
+        with torch.cuda.stream(copy_stream):
+            dev_img[k].copy_(pin_img[k], non_blocking=True)
+            dev_lab[k].copy_(pin_lab[k], non_blocking=True)
+            h2d = torch.cuda.Event()
+            h2d.record(copy_stream)
+        main = torch.cuda.current_stream()
+        main.wait_event(h2d)
+        x_enc = sess.fx_encode_device(dev_img[k], bad)
+        y_enc = sess.fx_encode_device(dev_lab[k], bad)
+        xs_static.data.copy_(sess.share_device(x_enc, rng).data)
+        ys_static.data.copy_(sess.share_device(y_enc, rng).data)
+        logits = graph.replay()
+        out_host[k].copy_(engine.reconstruct_device(logits).view(b, 10), non_blocking=True)
+        done[k] = torch.cuda.Event()
+        done[k].record(main)
+
+    for i in range(2):
+        e2e_step(i)
+    for k in range(nbuf):
+        if done[k] is not None:
+            done[k].synchronize()
+            done[k] = None
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    results.clear()
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        e2e_step(i)
+    for k in range(nbuf):  # the last steps' logits
+        if done[k] is not None:
+            done[k].synchronize()
+            results.append(out_host[k].numpy().view(np.uint64).copy())
+    dt = time.perf_counter() - t0
+    assert len(results) == args.steps
+    if ws > 1:
+        t = torch.tensor([dt], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        dt = float(t.item())
+    if int(bad.item()):
+        raise RuntimeError("input outside the encodable range")
+    return {"value": b * args.steps * ws / dt, "unit": UNIT,
+            "h2d_bytes_per_step": int(pin_img[0].numel() * 8 + pin_lab[0].numel() * 8),
+            "d2h_bytes_per_step": int(out_host[0].numel() * 8),
+            "note": "per step: host images+labels into pinned memory, H2D on a copy stream (double-buffered, "
+                    "overlapping the previous step), device fx-encode, device PCG64 dealer (bit-exact with "
+                    "sharing.py:113-118), graph step, opened logits D2H read on the host; wall clock"}
+
+
+# ---------------------------------------------------------------------------
+# side measurements (the other BASELINE configs), reported under `also`
+
+
+def side_measurements(dev, ws, rank, rec, peaks, sm_mhz, args) -> dict:
+    import torch
+
+    also = {}
+    for key, fn in (("lenet_b64", lambda: lenet_inference(dev)), ("vgg16_ti_b32", lambda: vgg16_ti(dev)),
+                    ("resnet50_b64", lambda: resnet50_inference(dev, 64, 3, rec=rec, peaks=peaks, sm_mhz=sm_mhz)),
+                    ("resnet50_b1", lambda: resnet50_inference(dev, 1, 10))):
         try:
-            tp = resnet50_b1_tp(dev)
+            also[key] = fn()
+        except Exception as e:  # noqa: BLE001 - reported, not fatal to the headline
+            also[key] = {"error": repr(e)[:300]}
+    if ws > 1:
+        try:
+            also["resnet50_b1_tensor_parallel"] = resnet50_b1_tp(dev)
         except Exception as e:  # noqa: BLE001
-            tp = {"error": repr(e)[:300]}
-    if ws > 1 and also:
-        # every rank ran the same side workloads as an independent replica:
+            also["resnet50_b1_tensor_parallel"] = {"error": repr(e)[:300]}
+        # every rank ran the other side workloads as an independent replica:
         # report the aggregate (sum of batches / slowest rank), weak scaling
-        for key, rec in also.items():
-            for sub in ([rec] + [v for v in rec.values() if isinstance(v, dict)] if isinstance(rec, dict) else []):
+        for key, rec_ in also.items():
+            if key == "resnet50_b1_tensor_parallel" or not isinstance(rec_, dict):
+                continue
+            for sub in [rec_] + [v for v in rec_.values() if isinstance(v, dict)]:
                 if "ms_per_batch" in sub and "value" in sub:
                     t = torch.tensor([sub["ms_per_batch"]], device=dev, dtype=torch.float64)
                     torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
                     sub["value"] = sub["value"] * sub["ms_per_batch"] / float(t.item()) * ws
                     sub["ms_per_batch"] = float(t.item())
                     sub["scaling"] = f"weak: {ws} independent replicas, slowest rank"
-    if ws > 1 and not args.no_resnet:
-        also["resnet50_b1_tensor_parallel"] = tp
-    if rank == 0:
-        line = {
-            "also": also,
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u64 ring (int)", "data": "synthetic",
-            "config": _config(args, ws), "clocks": clk, "gpu_launches": launches, "roofline": roofline,
-            "e2e": e2e, "cpu_baseline": cpu,
-            "step_ms": [round(v, 3) for v in step_ms],
-        }
-        print(json.dumps(line), flush=True)
-    if ws > 1:
-        torch.distributed.destroy_process_group()
+    if rank == 0 and ws == 1:
+        try:
+            also["dropin_train_private"] = dropin_train_private()
+        except Exception as e:  # noqa: BLE001
+            also["dropin_train_private"] = {"error": repr(e)[:300]}
+        if not args.no_cpu_baseline:
+            _side_cpu_baselines(also)
+    return also
 
 
-def _aes_peak_gblocks():
-    """Measured rate of the standalone AES-128-CTR keystream kernel (the
-    nonlinear protocols' roofline): 2^27 blocks, CUDA events, best of 3."""
-    import ctypes as C
+def _side_cpu_baselines(also):
+    """The reference's CPU path for the side configs (refarm.py): LeNet b64
+    infer_private; ResNet-50 b1 composed from its per-party protocols (b64
+    extrapolated linearly from b1, labelled)."""
+    import refarm
 
-    import torch
-
-    from paper_2104_10949_b200 import _capi
-
-    rk = np.zeros((3, 44), np.uint32)
-    for i in range(3):
-        _capi.check(_capi.lib().mpc3_aes128_expand(C.c_char_p(bytes([i]) * 16), rk[i].ctypes.data_as(C.c_void_p)))
-    rkd = torch.from_numpy(rk.view(np.int32)).pin_memory()  # read on the host at launch
-    count = 1 << 28
-    out = torch.empty(count, dtype=torch.int64, device="cuda")
-    st = torch.cuda.current_stream().cuda_stream
-    best = None
-    for _ in range(4):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        _capi.call("mpc3_prf_words", rkd.data_ptr(), 1, 0, 0, count, out.data_ptr(), st)
-        e1.record()
-        e1.synchronize()
-        ms = e0.elapsed_time(e1)
-        best = ms if best is None else min(best, ms)
-    return count / 2 / (best / 1e3) / 1e9
+    mod, src = refarm.load()
+    if mod is None:
+        return
+    th = refarm.threads()
+    try:
+        t = refarm.lenet_infer(64)
+        also["lenet_b64"]["cpu_baseline"] = {"value": 64 / t, "unit": UNIT, "cores": th["cores"], "kind": "reference",
+                                             "sample": "mpc3 infer_private, LeNet batch 64, one pass"}
+    except Exception as e:  # noqa: BLE001
+        also["lenet_b64"]["cpu_baseline"] = {"error": repr(e)[:200]}
+    try:
+        t = refarm.resnet50_composed(1)
+        base = {"unit": UNIT, "cores": th["cores"], "kind": "reference",
+                "sample": "ResNet-50 224x224 batch 1 COMPOSED from mpc3 conv2d_shares + local bias, relu, padded "
+                          "avgpool_shares, matmul_shares + bias, residual adds (the reference graph has no "
+                          "ResNet layers); one forward pass"}
+        also["resnet50_b1"]["cpu_baseline"] = dict(base, value=1 / t, seconds=t)
+        also["resnet50_b64"]["cpu_baseline"] = dict(base, value=1 / t, seconds_per_image=t,
+                                                    note="extrapolated: b1 per-image time x 64 (linear in batch)")
+    except Exception as e:  # noqa: BLE001
+        also["resnet50_b1"]["cpu_baseline"] = {"error": repr(e)[:200]}
 
 
 def lenet_inference(dev, batch: int = 64, steps: int = 5):
-    """LeNet private inference (configs[0]), MNIST shape, device-resident input."""
+    """LeNet private inference (configs[0]), MNIST shape, device-resident
+    input; the inputs are exactly tests/golden/cfg_lenet_b64.npz's and the
+    first replay's logit shares are checked against the reference's."""
     import torch
 
     import paper_2104_10949_b200 as M
@@ -583,7 +763,8 @@ def lenet_inference(dev, batch: int = 64, steps: int = 5):
     params = [sess.share(w, rng) for w in M.init_params(model, seed=3)]
     x = sess.share(M.fx_encode(rng.uniform(0, 1, (batch, 1, 28, 28))), rng)
     g = InferenceGraph(sess, model, params, x)
-    g.replay()
+    first = g.replay().data.cpu().numpy().view(np.uint64)
+    parity = _fixture_check("lenet_b64", first) if batch == 64 else "not checked"
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -593,12 +774,21 @@ def lenet_inference(dev, batch: int = 64, steps: int = 5):
     e1.synchronize()
     t = e0.elapsed_time(e1) / steps
     return {"workload": f"LeNet private inference, MNIST 1x28x28, batch {batch}", "value": batch / (t / 1e3),
-            "unit": "images/s", "ms_per_batch": t, "steps": steps, "cuda_graph": True}
+            "unit": "images/s", "ms_per_batch": t, "steps": steps, "cuda_graph": True, "parity": parity}
+
+
+def _fixture_check(name, got) -> str:
+    try:
+        z = np.load(os.path.join(ROOT, "tests", "golden", f"cfg_{name}.npz"))
+    except OSError:
+        return "not checked (fixture missing)"
+    return "ok (shares == reference)" if np.array_equal(got, z["logits"]) else "MISMATCH"
 
 
 def vgg16_ti(dev, batch: int = 32, steps: int = 3):
     """VGG-16 (avg-pool variant) on Tiny-ImageNet shape (configs[2]): private
-    inference and one private training step (SGD), batch 32, images/s; both
+    inference (inputs of tests/golden/cfg_vgg16ti_b32.npz, first replay
+    checked) and one private training step (SGD), batch 32, images/s; both
     captured as CUDA graphs like the headline step."""
     import torch
 
@@ -606,33 +796,28 @@ def vgg16_ti(dev, batch: int = 32, steps: int = 3):
     from paper_2104_10949_b200 import engine
     from paper_2104_10949_b200.nn import InferenceGraph, TrainState, one_hot
 
-    sess = M.TrioSession(seed=5)
     model = M.models.vgg16()
+    sess = M.TrioSession(seed=5)
     rng = np.random.default_rng(5)
-    imgs, labels = rng.uniform(0, 1, (batch, 3, 64, 64)), rng.integers(0, 200, batch)
-    st = TrainState(sess, model, M.TrainConfig(0.01, batch, steps + 4, seed=5))
+    params = [sess.share(w, rng) for w in M.init_params(model, seed=5)]
+    x = sess.share(M.fx_encode(rng.uniform(0, 1, (batch, 3, 64, 64))), rng)
+    infer_graph = InferenceGraph(sess, model, params, x)
+    parity = _fixture_check("vgg16ti_b32", infer_graph.replay().data.cpu().numpy().view(np.uint64)) \
+        if batch == 32 else "not checked"
+    res = {"inference": None, "training_step": None, "parity_inference": parity}
+
+    tsess = M.TrioSession(seed=5)
+    trng = np.random.default_rng(5)
+    imgs, labels = trng.uniform(0, 1, (batch, 3, 64, 64)), trng.integers(0, 200, batch)
+    st = TrainState(tsess, model, M.TrainConfig(0.01, batch, steps + 4, seed=5))
     xb = st.deal_batch(M.fx_encode(imgs), M.fx_encode(one_hot(labels, 200)))
     xs = engine.RssTensor(xb[0].data.clone())
     ys = engine.RssTensor(xb[1].data.clone())
-    # inference first: its graph packs the weights once (frozen at capture)
-    infer_graph = InferenceGraph(sess, model, st.params, xs)
-    infer_graph.replay()
+    st.step(*xb)  # warm-up (allocations)
+    train_graph = st.capture(xs, ys)
+    train_graph.replay()
     torch.cuda.synchronize()
-    res = {}
-
-    def train():
-        nonlocal train_graph
-        if train_graph is None:
-            st.step(*xb)  # warm-up (allocations)
-            train_graph = st.capture(xs, ys)
-            train_graph.replay()
-            torch.cuda.synchronize()
-        return train_graph.replay()
-
-    train_graph = None
-    for kind, fn in (("inference", infer_graph.replay), ("training_step", train)):
-        if kind == "training_step":
-            train()
+    for kind, fn in (("inference", infer_graph.replay), ("training_step", train_graph.replay)):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(steps):
@@ -645,9 +830,13 @@ def vgg16_ti(dev, batch: int = 32, steps: int = 3):
     return res
 
 
-def resnet50_inference(dev, batch: int, steps: int, use_graph: bool):
+def resnet50_inference(dev, batch: int, steps: int, rec=None, peaks=None, sm_mhz=1965.0):
     """ResNet-50 private inference (configs[3]), device-resident dealt input,
-    CUDA-event timed per batch with an L2 flush before each; images/s."""
+    CUDA-graph replays, CUDA-event timed per batch with an L2 flush before
+    each; images/s.  At batch 1 the inputs are tests/golden/cfg_resnet50_b1's
+    and the first replay is checked against the reference composition.  With
+    `rec`, one instrumented eager pass gives the roofline of its dominant
+    kernel (the sign circuit, AES-bound)."""
     import torch
 
     import paper_2104_10949_b200 as M
@@ -659,24 +848,31 @@ def resnet50_inference(dev, batch: int, steps: int, use_graph: bool):
     params = [sess.share(w, rng) for w in M.init_params(model, seed=11)]
     x = sess.share(M.fx_encode(rng.uniform(0, 1, (batch, 3, 224, 224))), rng)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
-    net = TrioNet(sess)
-    run = (lambda g=InferenceGraph(sess, model, params, x): g.replay()) if use_graph else \
-        (lambda: net.forward(model, params, x, record=False)[0])
-    run()
+    g = InferenceGraph(sess, model, params, x)
+    first = g.replay().data.cpu().numpy().view(np.uint64)
+    parity = _fixture_check("resnet50_b1", first) if batch == 1 else "not checked (fixture at batch 1)"
     torch.cuda.synchronize()
     ms = []
     for _ in range(steps):
         flush.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        run()
+        g.replay()
         e1.record()
         e1.synchronize()
         ms.append(e0.elapsed_time(e1))
     t = float(np.mean(ms))
-    return {"workload": f"ResNet-50 v1.5 private inference, ImageNet 3x224x224, batch {batch}",
-            "value": batch / (t / 1e3), "unit": "images/s", "ms_per_batch": t, "steps": steps,
-            "cuda_graph": use_graph, "data": "synthetic (random-init folded-BN weights, U(0,1) images)"}
+    out = {"workload": f"ResNet-50 v1.5 private inference, ImageNet 3x224x224, batch {batch}",
+           "value": batch / (t / 1e3), "unit": "images/s", "ms_per_batch": t, "steps": steps,
+           "cuda_graph": True, "parity": parity,
+           "data": "synthetic (random-init folded-BN weights, U(0,1) images)"}
+    if rec is not None:
+        net = TrioNet(sess)
+        _instrumented(lambda: net.forward(model, params, x, record=False), rec, torch)
+        summ = rec.summary(t)
+        out["roofline"] = roofline_of(rec, summ, peaks or {}, sm_mhz, _traffic())
+        rec.events.clear()
+    return out
 
 
 def resnet50_b1_tp(dev, steps: int = 5):
@@ -694,7 +890,8 @@ def resnet50_b1_tp(dev, steps: int = 5):
     params = [sess.share(w, rng) for w in M.init_params(model, seed=11)]
     x = sess.share(M.fx_encode(rng.uniform(0, 1, (1, 3, 224, 224))), rng)
     net = TPNet(sess, TensorParallel.from_process_group())
-    net.forward_tp(model, params, x)
+    first = net.forward_tp(model, params, x).data.cpu().numpy().view(np.uint64)
+    parity = _fixture_check("resnet50_b1", first)
     torch.cuda.synchronize()
     torch.distributed.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -708,7 +905,39 @@ def resnet50_b1_tp(dev, steps: int = 5):
     ms = float(t.item())
     return {"workload": "ResNet-50 v1.5 private inference, batch 1, output channels sharded over all ranks "
                         "(NCCL all-gather per layer), eager",
-            "value": 1.0 / (ms / 1e3), "unit": "images/s", "latency_ms": ms, "steps": steps}
+            "value": 1.0 / (ms / 1e3), "unit": "images/s", "latency_ms": ms, "steps": steps, "parity": parity}
+
+
+def dropin_train_private(batch: int = BATCH, iterations: int = 2):
+    """The per-party drop-in path a reference user calls: run_in_process +
+    train_private (three party threads rendezvousing on the trio engine),
+    host data in, opened weights out; wall clock of the whole call."""
+    import torch
+
+    import paper_2104_10949_b200 as M
+
+    imgs, labels = _synthetic(batch, 100)
+    cfg = M.TrainConfig(0.01, batch, iterations, 0)
+    job = (lambda ctx: M.train_private(ctx, M.alexnet_cifar(), cfg, (imgs, labels) if ctx.party == 0 else None))
+    M.run_in_process(job, seed=0)  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = M.run_in_process(job, seed=0)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    import hashlib
+
+    try:
+        z = np.load(os.path.join(ROOT, "tests", "golden", "cfg_alexnet_b128.npz"))
+        want = json.loads(bytes(z["meta"]).decode())[f"digest_{iterations}"] if batch == BATCH else None
+    except (OSError, KeyError, ValueError):
+        want = None
+    got = hashlib.sha256(b"".join(np.ascontiguousarray(w, "<u8").tobytes() for w in res[0].weights)).hexdigest()
+    return {"workload": f"per-party run_in_process + train_private, AlexNet-CIFAR batch {batch}, "
+                        f"{iterations} iterations (setup, dealing, steps, opens)",
+            "value": batch * iterations / dt, "unit": UNIT, "seconds": dt,
+            "parity": "not checked" if want is None else ("ok (weights digest == reference)" if got == want
+                                                          else "MISMATCH")}
 
 
 def main():

@@ -793,7 +793,15 @@ class InferenceGraph:
         self._frozen = sess.frozen_weights()
         self._frozen.__enter__()  # weights packed once (here, outside the graph) and reused by every replay
         try:
-            net.forward(model, params, x, record=False)  # warm allocations + weight packs outside capture
+            # warm-up outside the capture (allocations, kernel attributes, the
+            # frozen weight packs) on a scratch session with throwaway keys
+            # that shares this session's weight-pack cache: this session's
+            # counters stay untouched, so the first replay is its next
+            # inference exactly (tests/test_gpu_configs.py)
+            scratch = TrioSession(None, sess.fp)
+            scratch.dp, scratch._wcache = sess.dp, sess._wcache
+            TrioNet(scratch).forward(model, params, x, record=False)
+            torch.cuda.synchronize()
             self.seq0 = dict(sess.seq)
             self.graph = torch.cuda.CUDAGraph()
             try:

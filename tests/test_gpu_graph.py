@@ -70,8 +70,9 @@ def test_inference_graph_with_packed_weights_matches_eager():
     s1, p1, x1 = setup()
     g = InferenceGraph(s1, model, p1, x1)
     got = [g.replay().data.cpu().numpy() for _ in range(3)]
-    # replay k equals eager call k (the graph was captured after one warm-up forward)
-    assert np.array_equal(got[0], ref[1]) and np.array_equal(got[1], ref[2])
+    # replay k equals eager call k (the warm-up ran on a scratch session: no counters consumed)
+    assert all(np.array_equal(a, b) for a, b in zip(got, ref))
+    assert s1.seq == s0.seq
 
     s2, p2, x2 = setup()
     net2 = TrioNet(s2)
