@@ -4,7 +4,7 @@ PKG := paper_2104_10949_b200
 CSRC := $(PKG)/csrc
 NVFLAGS := -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v
 HDRS := $(wildcard $(CSRC)/*.cuh) include/mpc3_b200.h
-OBJS := build/elementwise.o build/gemm.o build/deal.o
+OBJS := build/elementwise.o build/gemm.o build/deal.o build/layers.o
 LIB := $(PKG)/libmpc3b200.so
 HOSTLIB := $(PKG)/libmpc3hostcheck.so
 

@@ -461,6 +461,37 @@ size_t mpc3_ring_matmul_workspace(int64_t M, int64_t N, int64_t K);
 int mpc3_ring_matmul_u64(const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t M, int64_t N,
                          int64_t K, void* workspace, void* stream);
 
+/* ---- single-call layers (csrc/layers.cu; SURVEY.md §8(b) minimum list) ----
+ * Each is the composition of the calls above (limb packs, tcgen05 ring GEMM,
+ * fused reshare + truncate) behind one entry; workspace >= the matching
+ * *_workspace() bytes, caller-owned (the library keeps no buffer). */
+
+/* Plain ring conv2d, NCHW cross-correlation (ring.py:225-256 _conv2d_exact /
+ * bilinear_exact with conv2d_spec): y (N, O, OH, OW) = x (N, C, H, W) * w
+ * (O, C, kh, kw) mod 2^64; ExactnessError past C*kh*kw = 2^20 (ring.py:191). */
+size_t mpc3_ring_conv2d_workspace(int64_t N, int64_t C, int64_t H, int64_t W, int64_t O, int kh, int kw,
+                                  int sh, int sw, int ph, int pw);
+int mpc3_ring_conv2d_u64(const uint64_t* x, const uint64_t* w, uint64_t* y, int64_t N, int64_t C, int64_t H,
+                         int64_t W, int64_t O, int kh, int kw, int sh, int sw, int ph, int pw, void* workspace,
+                         void* stream);
+
+/* matmul_shares (protocols.py:97-117) of trio tensors x (3, M, K) and y
+ * (3, K, N) into out (3, M, N): the three cross-term GEMMs, the ARITH_ZERO
+ * reshare (j_arith) and the truncation by bits (j_rho, j_r). */
+size_t mpc3_rss_matmul_workspace(int64_t M, int64_t K, int64_t N);
+int mpc3_rss_matmul_reshare_trunc(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, uint64_t j_rho,
+                                  uint64_t j_r, int bits, const uint64_t* x, const uint64_t* y, uint64_t* out,
+                                  int64_t M, int64_t K, int64_t N, void* workspace, void* stream);
+
+/* conv2d_shares (protocols.py:120-136) of trio tensors x (3, N, C, H, W) and
+ * w (3, O, C, kh, kw) into out (3, N, O, OH, OW). */
+size_t mpc3_rss_conv2d_workspace(int64_t N, int64_t C, int64_t H, int64_t W, int64_t O, int kh, int kw,
+                                 int sh, int sw, int ph, int pw);
+int mpc3_rss_conv2d_reshare_trunc(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_arith, uint64_t j_rho,
+                                  uint64_t j_r, int bits, const uint64_t* x, const uint64_t* w, uint64_t* out,
+                                  int64_t N, int64_t C, int64_t H, int64_t W, int64_t O, int kh, int kw, int sh,
+                                  int sw, int ph, int pw, void* workspace, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -210,6 +210,14 @@ _SIGS = {
     "mpc3_ring_gemm_simt": (C.c_int, [_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _P]),
     "mpc3_ring_matmul_workspace": (C.c_size_t, [_I64, _I64, _I64]),
     "mpc3_ring_matmul_u64": (C.c_int, [_P, _P, _P, _I64, _I64, _I64, _P, _P]),
+    "mpc3_ring_conv2d_workspace": (C.c_size_t, [_I64, _I64, _I64, _I64, _I64] + [C.c_int] * 6),
+    "mpc3_ring_conv2d_u64": (C.c_int, [_P, _P, _P, _I64, _I64, _I64, _I64, _I64] + [C.c_int] * 6 + [_P, _P]),
+    "mpc3_rss_matmul_workspace": (C.c_size_t, [_I64, _I64, _I64]),
+    "mpc3_rss_matmul_reshare_trunc": (C.c_int, [_P, _P, _U64, _U64, _U64, C.c_int, _P, _P, _P, _I64, _I64, _I64, _P,
+                                                _P]),
+    "mpc3_rss_conv2d_workspace": (C.c_size_t, [_I64, _I64, _I64, _I64, _I64] + [C.c_int] * 6),
+    "mpc3_rss_conv2d_reshare_trunc": (C.c_int, [_P, _P, _U64, _U64, _U64, C.c_int, _P, _P, _P, _I64, _I64, _I64, _I64,
+                                                _I64] + [C.c_int] * 6 + [_P, _P]),
 }
 EXPORTED = tuple(_SIGS)
 

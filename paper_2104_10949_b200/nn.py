@@ -138,8 +138,11 @@ class ModelGraph:
     def param_shapes(self) -> list:
         return _param_shapes(self.layers, self.input_shape)
 
-    def validate(self, recip: ReciprocalConfig = ReciprocalConfig()) -> None:
-        if self.num_classes > recip.Y:
+    def validate(self, recip: ReciprocalConfig | None = ReciprocalConfig()) -> None:
+        """Shapes of the parameters; with `recip`, also the softmax domain
+        (training, nn.py:167-172).  Inference-only graphs (ResNet-50's 1000
+        classes) pass recip=None."""
+        if recip is not None and self.num_classes > recip.Y:
             raise ConfigError(f"{self.num_classes} classes exceed the reciprocal domain")
         if self.params is not None:
             want = self.param_shapes()

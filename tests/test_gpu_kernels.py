@@ -545,3 +545,56 @@ def test_device_fx_encode_matches_reference():
     assert int(bad.item()) == 0
     s.fx_encode_device(torch.tensor([float(1 << 43)], dtype=torch.float64, device="cuda"), bad)
     assert int(bad.item()) == 1
+
+
+# ---------------------------------------------------------------------------
+# single-call layers (csrc/layers.cu): one C-ABI entry per reference function
+
+
+@pytest.mark.parametrize("shape", [(2, 3, 10, 10, 4, 3, 3, 2, 2, 1, 1), (3, 16, 12, 12, 32, 3, 3, 1, 1, 1, 1),
+                                   (1, 3, 32, 32, 8, 11, 11, 4, 4, 2, 2)])
+def test_ring_conv2d_u64_single_call(shape):
+    nb, c, h, w, o, kh, kw, sh, sw, ph, pw = shape
+    rng = np.random.default_rng(sum(shape))
+    x, k = rnd(rng, (nb, c, h, w)), rnd(rng, (o, c, kh, kw))
+    oh, ow = (h + 2 * ph - kh) // sh + 1, (w + 2 * pw - kw) // sw + 1
+    ws = torch.empty(_capi.lib().mpc3_ring_conv2d_workspace(nb, c, h, w, o, kh, kw, sh, sw, ph, pw),
+                     dtype=torch.uint8, device="cuda")
+    y = torch.empty(nb * o * oh * ow, dtype=torch.int64, device="cuda")
+    _capi.call("mpc3_ring_conv2d_u64", p(dev(x)), p(dev(k)), p(y), nb, c, h, w, o, kh, kw, sh, sw, ph, pw, p(ws),
+               stream())
+    assert np.array_equal(host(y).reshape(nb, o, oh, ow), R.wrap_conv2d(x, k, (sh, sw), (ph, pw)))
+
+
+@pytest.mark.parametrize("m,k,n,bits", [(12, 32, 9, 20), (64, 300, 80, 23), (1, 5, 1, 1), (130, 1000, 70, 40)])
+def test_rss_matmul_reshare_trunc_single_call(m, k, n, bits):
+    rng = np.random.default_rng(m * k + n)
+    x = R.share(R.fx_encode(rng.uniform(-2, 2, (m, k))), rng)
+    y = R.share(R.fx_encode(rng.uniform(-2, 2, (k, n))), rng)
+    s = R.Session(3)
+    ref = R.matmul_shares(s, x, y, bits)  # counters ARITH 0, TRUNC_RHO 0, TRUNC_R 0
+    ws = torch.empty(_capi.lib().mpc3_rss_matmul_workspace(m, k, n), dtype=torch.uint8, device="cuda")
+    out = torch.empty(3 * m * n, dtype=torch.int64, device="cuda")
+    _capi.call("mpc3_rss_matmul_reshare_trunc", p(rk3(s.keys)), None, 0, 0, 0, bits, p(dev(x)), p(dev(y)), p(out), m,
+               k, n, p(ws), stream())
+    assert np.array_equal(host(out).reshape(3, m, n), ref)
+    with pytest.raises(_capi.E.RangeError):
+        _capi.call("mpc3_rss_matmul_reshare_trunc", p(rk3(s.keys)), None, 0, 0, 0, 62, p(dev(x)), p(dev(y)), p(out),
+                   m, k, n, p(ws), stream())
+
+
+@pytest.mark.parametrize("shape", [(2, 3, 10, 10, 4, 3, 3, 2, 2, 1, 1), (4, 16, 12, 12, 32, 3, 3, 1, 1, 1, 1),
+                                   (2, 3, 32, 32, 96, 11, 11, 4, 4, 9, 9)])
+def test_rss_conv2d_reshare_trunc_single_call(shape):
+    nb, c, h, w, o, kh, kw, sh, sw, ph, pw = shape
+    rng = np.random.default_rng(sum(shape) + 1)
+    x = R.share(R.fx_encode(rng.uniform(-2, 2, (nb, c, h, w))), rng)
+    k = R.share(R.fx_encode(rng.uniform(-0.3, 0.3, (o, c, kh, kw))), rng)
+    s = R.Session(5)
+    ref = R.conv2d_shares(s, x, k, (sh, sw), (ph, pw))
+    ws = torch.empty(_capi.lib().mpc3_rss_conv2d_workspace(nb, c, h, w, o, kh, kw, sh, sw, ph, pw),
+                     dtype=torch.uint8, device="cuda")
+    out = torch.empty(ref.size, dtype=torch.int64, device="cuda")
+    _capi.call("mpc3_rss_conv2d_reshare_trunc", p(rk3(s.keys)), None, 0, 0, 0, 20, p(dev(x)), p(dev(k)), p(out), nb,
+               c, h, w, o, kh, kw, sh, sw, ph, pw, p(ws), stream())
+    assert np.array_equal(host(out).reshape(ref.shape), ref)

@@ -138,3 +138,47 @@ def test_alexnet_train_step_digest():
                                 seed=5, offsets=R.TruncationRandomness(0))
     d = hashlib.sha256(b"".join(np.ascontiguousarray(x, "<u8").tobytes() for x in fixed)).hexdigest()
     assert d == META["train_alexnet_digest"]
+
+
+# ---------------------------------------------------------------------------
+# the oracle at the BASELINE configurations (tests/golden/make_golden_configs.py)
+
+
+def test_maxpool_composition_matches_reference():
+    from golden_configs import cfg
+
+    arrays, meta = cfg("maxpool")
+    for name, c in meta["cases"].items():
+        xs = R.share(arrays[f"{name}_in"], np.random.default_rng(meta["dealer"]))
+        out = R.maxpool_shares(R.Session(meta["seed"]), xs, tuple(c["window"]), tuple(c["stride"]),
+                               tuple(c["padding"]))
+        assert np.array_equal(out, arrays[f"{name}_out"]), name
+
+
+def test_lenet_b64_inference_matches_reference():
+    from golden_configs import cfg
+
+    arrays, _ = cfg("lenet_b64")
+    layers, ishape = N.lenet()
+    rin = np.random.default_rng(3)
+    P = [R.share(w, rin) for w in N.init_params(layers, ishape, 20, 3)]
+    x = R.share(R.fx_encode(rin.uniform(0, 1, (64,) + ishape)), rin)
+    assert np.array_equal(N.infer_private(R.Session(3), layers, P, x), arrays["logits"])
+
+
+@pytest.mark.slow
+def test_resnet50_b1_composed_oracle_matches_reference_composition():
+    """forward_ext at ResNet-50 224x224 batch 1 = the reference's per-party
+    protocols composed (cfg_resnet50_b1.npz); ~1 min of CPU."""
+    from golden_configs import cfg
+
+    from paper_2104_10949_b200 import models as BM
+    from paper_2104_10949_b200 import nn as B
+
+    arrays, _ = cfg("resnet50_b1")
+    model = BM.resnet50()
+    layers = tuple(N.from_spec(sp) for sp in model.layers)
+    rin = np.random.default_rng(11)
+    P = [R.share(t, rin) for t in B.init_params(model, seed=11)]
+    x = R.share(R.fx_encode(rin.uniform(0, 1, (1, 3, 224, 224))), rin)
+    assert np.array_equal(N.forward_ext(R.Session(11), layers, iter(P), x), arrays["logits"])

@@ -149,6 +149,46 @@ def protocol_rates():
     return res
 
 
+def cpu_reference(sizes, relu_n=1 << 20):
+    """The reference's CPU path beside the GPU sweep: the
+    unmodified mpc3 (baseline/_ref, refarm.py) `bilinear_exact(a, b,
+    matmul_spec(n, n, n))` on rand_u64 inputs (tests/test_ring.py:15-16), one
+    warm-up call, and its 3-party `relu` / `truncate` on fx_encode(U(-8, 8))
+    (cli.py:250-251) through run_in_process."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import refarm
+
+    mod, src = refarm.load()
+    if mod is None:
+        return {"unavailable": src}
+    from mpc3 import protocols as P
+    from mpc3.ring import bilinear_exact, fx_encode, matmul_spec
+    from mpc3.session import distribute_input, run_in_process
+
+    res = {"source": src, "threads": refarm.threads(), "gemm": []}
+    for n in sizes:
+        rng = np.random.default_rng(n)
+        a = rng.integers(0, 1 << 64, (n, n), dtype=np.uint64)
+        b = rng.integers(0, 1 << 64, (n, n), dtype=np.uint64)
+        bilinear_exact(a[:64, :64], b[:64, :64], matmul_spec(64, 64, 64))
+        t0 = time.perf_counter()
+        bilinear_exact(a, b, matmul_spec(n, n, n))
+        dt = time.perf_counter() - t0
+        res["gemm"].append({"n": n, "s": dt, "ring_gops": 2 * n ** 3 / dt / 1e9})
+        print("cpu gemm", res["gemm"][-1], flush=True)
+    x = fx_encode(np.random.default_rng(1).uniform(-8, 8, relu_n))
+    for name, op in (("relu", P.relu), ("truncate", P.truncate)):
+        def job(ctx, op=op):
+            xs = distribute_input(ctx, x if ctx.party == 0 else None, np.random.default_rng(2), shape=x.shape)
+            t0 = time.perf_counter()
+            op(ctx, xs)
+            return time.perf_counter() - t0
+        dt = max(run_in_process(job, seed=0, timeout=1e5))
+        res[name] = {"n": relu_n, "s": dt, "melem_s": relu_n / dt / 1e6}
+        print("cpu", name, res[name], flush=True)
+    return res
+
+
 def graph_us(launch, reps=20):
     launch()
     torch.cuda.synchronize()
@@ -165,6 +205,7 @@ def main():
     ap.add_argument("--out", default="gpurun_out/microbench.json")
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--gemm-t", action="store_true", help="only the transposed-operand GEMM comparison")
+    ap.add_argument("--cpu", action="store_true", help="also time the reference's CPU bilinear_exact / relu / truncate")
     args = ap.parse_args()
     if args.gemm_t:
         shapes = [(256, 3456, 128), (384, 3456, 128), (96, 363, 12800), (256, 2400, 512),
@@ -185,6 +226,12 @@ def main():
     res["int8_cublaslt"] = int8_peak()
     print("int8", res["int8_cublaslt"], flush=True)
     res["gemm"] = gemm_sweep([1024, 2048, 4096] if args.quick else [256, 512, 1024, 2048, 4096, 8192])
+    if args.cpu:  # bounded: n <= 4096 (8192 is ~1 min of dgemm on 16 cores)
+        res["cpu_reference"] = cpu_reference([256, 512, 1024, 2048] if args.quick else [256, 512, 1024, 2048, 4096])
+        for g in res["gemm"]:
+            c = next((c for c in res["cpu_reference"].get("gemm", []) if c["n"] == g["n"]), None)
+            if c:
+                g["speedup_vs_cpu_reference"] = c["s"] / (g["ms"] / 1e3)
     with open(args.out, "w") as f:
         json.dump(res, f, indent=1)
 
