@@ -461,6 +461,31 @@ size_t mpc3_ring_matmul_workspace(int64_t M, int64_t N, int64_t K);
 int mpc3_ring_matmul_u64(const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t M, int64_t N,
                          int64_t K, void* workspace, void* stream);
 
+/* The training step's loss gradient softmax(z) - y (nn.py:561-568;
+ * protocols.py:453-468: max_tree, z - max, exp_approx, row sum, reciprocal,
+ * mul + truncate) of a (rows, d) trio z against labels y, in ONE launch;
+ * every step draws its unfused launch's counters and PRF words: max_tree
+ * level counters as mpc3_rss_max_tree, the exp / reciprocal chain programs
+ * and counters as mpc3_rss_chain, the final mul_truncate's (fin_j).
+ * scratch: mpc3_rss_softmax_loss_scratch(rows, d) bytes. */
+typedef struct {
+  int levels;
+  uint64_t j_bin[16], j_xor[16], j_arith[16];
+  uint64_t exp_j[3];  /* ARITH_ZERO, TRUNC_RHO, TRUNC_R of the exp chain's first multiply */
+  const MPC3ChainStep* exp_steps;
+  int exp_count;
+  uint64_t rec_j[3];
+  const MPC3ChainStep* rec_steps;
+  int rec_count;
+  uint64_t fin_j[3];
+  int bits;           /* the final truncation (t) */
+  uint64_t row_off, rows_total;  /* batch shard (row_off even) */
+} mpc3_softmax_loss_args;
+size_t mpc3_rss_softmax_loss_scratch(uint64_t rows, uint64_t d);
+int mpc3_rss_softmax_loss(const uint32_t* rk3, const uint64_t* ctr, const mpc3_softmax_loss_args* a, const uint64_t* z,
+                          const uint64_t* y, uint64_t* scratch, uint64_t* out, uint64_t rows, uint64_t d,
+                          void* stream);
+
 /* ---- single-call layers (csrc/layers.cu; SURVEY.md §8(b) minimum list) ----
  * Each is the composition of the calls above (limb packs, tcgen05 ring GEMM,
  * fused reshare + truncate) behind one entry; workspace >= the matching

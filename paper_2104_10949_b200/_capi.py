@@ -66,6 +66,15 @@ class ChainStep(C.Structure):
     _fields_ = [("op", C.c_int), ("bits", C.c_int), ("c", C.c_uint64)]
 
 
+class SoftmaxLossArgs(C.Structure):
+    """mpc3_softmax_loss_args (include/mpc3_b200.h)."""
+    _fields_ = [("levels", C.c_int), ("j_bin", C.c_uint64 * 16), ("j_xor", C.c_uint64 * 16),
+                ("j_arith", C.c_uint64 * 16), ("exp_j", C.c_uint64 * 3), ("exp_steps", C.POINTER(ChainStep)),
+                ("exp_count", C.c_int), ("rec_j", C.c_uint64 * 3), ("rec_steps", C.POINTER(ChainStep)),
+                ("rec_count", C.c_int), ("fin_j", C.c_uint64 * 3), ("bits", C.c_int), ("row_off", C.c_uint64),
+                ("rows_total", C.c_uint64)]
+
+
 CHAIN_ADDC, CHAIN_SETC, CHAIN_SQ, CHAIN_MULX, CHAIN_NEWTON, CHAIN_SQT = range(6)
 CHAIN_MAX_STEPS = 48
 
@@ -165,6 +174,8 @@ _SIGS = {
     "mpc3_rss_layer_sign": (C.c_int, [_P, _P, _U64, _U64, _U64, C.c_int, _P, C.POINTER(View4), _P, _I64, C.c_int,
                                       C.c_int, _U64, _U64, _U64, _P, _P, _U64, _U64, _P]),
     "mpc3_rss_sgd_multi": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, _U64, _P]),
+    "mpc3_rss_softmax_loss_scratch": (C.c_size_t, [_U64, _U64]),
+    "mpc3_rss_softmax_loss": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _U64, _U64, _P]),
     "mpc3_rss_max_level": (C.c_int, [_P, _P, _U64, _U64, _U64, _P, _P, _U64, _U64, _U64, _U64, _P]),
     "mpc3_rss_chain": (C.c_int, [_P, _P, _P, C.c_int, _U64, _U64, _U64, _P, _P, _U64, _U64, _P]),
     "mpc3_rss_bit_inject": (C.c_int, [_P, _P, _U64, _P, _P, _U64, _U64, _P]),

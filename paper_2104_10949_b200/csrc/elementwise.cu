@@ -543,6 +543,202 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
   }
 }
 
+// The training step's loss gradient softmax(z) - y (nn.py:561-568 via
+// protocols.py:453-468) in ONE launch.  Rows are independent, so each CTA
+// takes R rows (R even: every per-op tensor range then starts on an AES-block
+// boundary) through the whole chain, with __syncthreads between the steps
+// and the intermediate tensors in global scratch (this CTA's rows only):
+//   max_tree over the row (levels as maxtree_kernel), x = z - max,
+//   e = exp_approx(x) (chain program, two-phase as chain_kernel),
+//   s = sum_j e, r = reciprocal(s) (chain program), out = truncate(e * r) - y.
+// Every step uses the counters and PRF word indices of its unfused launch
+// (each op's own flat tensor index at the batch shard's global offset), so
+// the shares are those of the separate max_tree / chain / mul_truncate calls.
+struct LossArgs {
+  int levels;
+  uint64_t jbin[MT_MAX_LEVELS], jxor[MT_MAX_LEVELS], ja[MT_MAX_LEVELS];
+  uint64_t ej[3], rj[3], fj[3];  // exp / reciprocal / final mul: ARITH, TRUNC_RHO, TRUNC_R
+  int bits;                       // final truncation (t)
+  uint64_t rows_total, row_off;   // batch shard (row_off even)
+  ChainProgram ep, rp;
+};
+constexpr int LOSS_SLOT_BYTES = 64 * 1024;
+
+// one chain program over pairs [lo, hi) of an n-element trio tensor x -> out
+DEV void chain_pairs(const SmemTables& tab, const uint32_t* rk, const uint64_t* ctr, const ChainProgram& prog,
+                     uint64_t ja, uint64_t jrho, uint64_t jr, const uint64_t* x, uint64_t* out, uint64_t n,
+                     uint64_t pb0, uint64_t lo, uint64_t hi, Word2* slots) {
+  int P = 64;
+  while (P > 1 && P * prog.nmul * CH_SLOT_WORDS * (int)sizeof(Word2) > LOSS_SLOT_BYTES) P >>= 1;
+  for (uint64_t c0 = lo; c0 < hi; c0 += P) {
+    const int Pc = (int)(hi - c0 < (uint64_t)P ? hi - c0 : (uint64_t)P);
+    for (int q = threadIdx.x; q < prog.nmul * Pc; q += blockDim.x) {
+      const int k = q / Pc, p = q % Pc;
+      const uint64_t blk = pb0 + c0 + p;
+      Word2* dst = slots + ((size_t)k * Pc + p) * CH_SLOT_WORDS;
+      Word2 w[3];
+      prf_block3(tab, rk, resolve(sref(ARITH_ZERO, ja + k), ctr), blk, w);
+      dst[0] = w[0];
+      dst[1] = w[1];
+      dst[2] = w[2];
+      trunc_words(tab, rk, resolve(sref(TRUNC_RHO, jrho + k), ctr), resolve(sref(TRUNC_R, jr + k), ctr), blk, dst[3],
+                  dst[4]);
+    }
+    __syncthreads();
+    const int p = threadIdx.x;
+    if (p < Pc) {
+      const uint64_t b = c0 + p;
+      const bool two = 2 * b + 1 < n;
+      Trio xv[2], z[2], t[2];
+      xv[0] = load_trio(x, n, 2 * b);
+      xv[1] = two ? load_trio(x, n, 2 * b + 1) : xv[0];
+      z[0] = xv[0];
+      z[1] = xv[1];
+      t[0] = t[1] = z[0];
+      int k = 0;
+      for (int i = 0; i < prog.nsteps; ++i) {
+        const MPC3ChainStep st = prog.s[i];
+        if (st.op == MPC3_CHAIN_ADDC) {
+          z[0].c[0] += st.c;
+          z[1].c[0] += st.c;
+        } else if (st.op == MPC3_CHAIN_SETC) {
+          for (int e = 0; e < 2; ++e) z[e] = Trio{{st.c, 0, 0}};
+        } else if (st.op == MPC3_CHAIN_NEWTON) {
+          for (int e = 0; e < 2; ++e)
+            for (int c = 0; c < 3; ++c) z[e].c[c] = 2 * z[e].c[c] - t[e].c[c];
+        } else {
+          const Word2* sl = slots + ((size_t)k * Pc + p) * CH_SLOT_WORDS;
+          KeyWords f0, f1;
+          for (int c = 0; c < 3; ++c) {
+            f0.k[c] = sl[c].w0;
+            f1.k[c] = sl[c].w1;
+          }
+          const Word2 rho = sl[3], r = sl[4];
+          for (int e = 0; e < 2; ++e) {
+            Trio v = st.op == MPC3_CHAIN_MULX ? trio_mul(xv[e], t[e], e ? f1 : f0) : trio_mul(z[e], z[e], e ? f1 : f0);
+            v = trio_truncate(v, e ? rho.w1 : rho.w0, e ? r.w1 : r.w0, st.bits);
+            if (st.op == MPC3_CHAIN_SQ)
+              z[e] = v;
+            else
+              t[e] = v;
+          }
+          ++k;
+        }
+      }
+      store_trio(out, n, 2 * b, z[0]);
+      if (two) store_trio(out, n, 2 * b + 1, z[1]);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) softmax_loss_kernel(
+    const __grid_constant__ KeySched ks, const uint64_t* __restrict__ ctr, const __grid_constant__ LossArgs la,
+    const uint64_t* __restrict__ z, const uint64_t* __restrict__ y, uint64_t* scratch, uint64_t* __restrict__ out,
+    uint64_t rows, uint64_t d, int R) {
+  SignStreams& st = *reinterpret_cast<SignStreams*>(reinterpret_cast<AesSmem*>(mpc3_dsm)->extra);
+  auto tab = Proto<false>::init();
+  Word2* slots = reinterpret_cast<Word2*>(mpc3_dsm + sizeof(AesSmem));
+  const uint32_t* rk = &ks.rk[0][0];
+  const uint64_t r0 = (uint64_t)blockIdx.x * R;
+  const uint64_t rn = rows - r0 < (uint64_t)R ? rows - r0 : (uint64_t)R;
+  const uint64_t half = rows * ((d + 1) / 2) * 3;
+  uint64_t* s0 = scratch;          // max_tree ping-pong
+  uint64_t* s1 = s0 + half;
+  uint64_t* mx = s1 + half;        // (rows) max
+  uint64_t* X = mx + 3 * rows;     // (rows, d) z - max, then e
+  uint64_t* E = X + 3 * rows * d;
+  uint64_t* T = E + 3 * rows * d;  // (rows) sum, then reciprocal
+  uint64_t* RR = T + 3 * rows;
+  const uint64_t n = rows * d;
+
+  // 1. max_tree (protocols.py:356-380): level by level, as maxtree_kernel
+  const uint64_t* in = z;
+  uint64_t m = d;
+  for (int l = 0; l < la.levels; ++l) {
+    const uint64_t k = m / 2, mo = k + (m & 1);
+    uint64_t* o = l == la.levels - 1 ? mx : ((l & 1) ? s1 : s0);
+    if (threadIdx.x == 0) {
+      const SignArgs a = {la.jbin[l], la.jxor[l], la.ja[l], 0, 0, 0};
+      sign_streams(st, a, ctr, false);
+    }
+    __syncthreads();
+    const uint64_t nl = rows * k, n_total = la.rows_total * k, elem_off = la.row_off * k;
+    const bool straddle = (n_total & 1) != 0;
+    const int L = straddle ? 3 : 2, used = sign_slots(straddle);
+    const uint64_t p0 = r0 * k / 2, P = (rn * k + 1) / 2;
+    const MaxGeom g = {rows, m, k};
+    for (uint64_t c = 0; c < P; c += MT_PMAX) {
+      const int Pc = (int)(P - c < (uint64_t)MT_PMAX ? P - c : (uint64_t)MT_PMAX);
+      for (int q = threadIdx.x; q < used * Pc; q += blockDim.x) {
+        const int sidx = q / Pc, p = q % Pc;
+        sign_slot_fill(tab, rk, st, sidx, (elem_off >> 1) + p0 + c + p, n_total, L, slots + ((size_t)sidx * Pc + p) * 3);
+      }
+      __syncthreads();
+      if (threadIdx.x < Pc) {
+        Replay rp;
+        rp.w = slots;
+        rp.P = Pc;
+        rp.p = threadIdx.x;
+        rp.slot = 0;
+        maxlevel_item(rp, rk, st, in, o, g, nl, n_total, elem_off, p0 + c + threadIdx.x);
+      }
+      __syncthreads();
+    }
+    if (m & 1)
+      for (uint64_t r = threadIdx.x; r < rn; r += blockDim.x)
+        store_trio(o, rows * mo, (r0 + r) * mo + k, load_trio(in, rows * m, (r0 + r) * m + m - 1));
+    __syncthreads();
+    in = o;
+    m = mo;
+  }
+  // 2. x = z - max (a local op)
+  for (uint64_t i = threadIdx.x; i < rn * d; i += blockDim.x) {
+    const uint64_t f = r0 * d + i, row = f / d;
+    const Trio a = load_trio(z, n, f), b = load_trio(mx, rows, row);
+    Trio v;
+    for (int c = 0; c < 3; ++c) v.c[c] = a.c[c] - b.c[c];
+    store_trio(X, n, f, v);
+  }
+  __syncthreads();
+  // 3. e = exp_approx(x) over this CTA's pairs of the (rows, d) tensor
+  const uint64_t plo = r0 * d / 2, phi = ((r0 + rn) * d + 1) / 2;
+  chain_pairs(tab, rk, ctr, la.ep, la.ej[0], la.ej[1], la.ej[2], X, E, n, la.row_off * d / 2, plo, phi, slots);
+  // 4. s = sum_j e (a local op)
+  for (uint64_t r = threadIdx.x; r < rn; r += blockDim.x) {
+    Trio acc{{0, 0, 0}};
+    for (uint64_t j = 0; j < d; ++j) {
+      const Trio v = load_trio(E, n, (r0 + r) * d + j);
+      for (int c = 0; c < 3; ++c) acc.c[c] += v.c[c];
+    }
+    store_trio(T, rows, r0 + r, acc);
+  }
+  __syncthreads();
+  // 5. 1/s (reciprocal's Newton chain) over this CTA's rows
+  chain_pairs(tab, rk, ctr, la.rp, la.rj[0], la.rj[1], la.rj[2], T, RR, rows, la.row_off / 2, r0 / 2,
+              (r0 + rn + 1) / 2, slots);
+  // 6. out = truncate(e * (1/s)) - y (mul_truncate, then the loss gradient's local sub)
+  const StreamHead ha = resolve(sref(ARITH_ZERO, la.fj[0]), ctr), hrho = resolve(sref(TRUNC_RHO, la.fj[1]), ctr),
+                   hr = resolve(sref(TRUNC_R, la.fj[2]), ctr);
+  for (uint64_t b = plo + threadIdx.x; b < phi; b += blockDim.x) {
+    const uint64_t blk = la.row_off * d / 2 + b;
+    Word2 w[3], rho, r;
+    prf_block3(tab, rk, ha, blk, w);
+    trunc_words(tab, rk, hrho, hr, blk, rho, r);
+    for (int e = 0; e < 2; ++e) {
+      const uint64_t f = 2 * b + e;
+      if (f >= n || f >= (r0 + rn) * d) break;
+      KeyWords kw;
+      for (int c = 0; c < 3; ++c) kw.k[c] = e ? w[c].w1 : w[c].w0;
+      Trio v = trio_mul(load_trio(E, n, f), load_trio(RR, rows, f / d), kw);
+      v = trio_truncate(v, e ? rho.w1 : rho.w0, e ? r.w1 : r.w0, la.bits);
+      const Trio yy = load_trio(y, n, f);
+      for (int c = 0; c < 3; ++c) v.c[c] -= yy.c[c];
+      store_trio(out, n, f, v);
+    }
+  }
+}
+
 // SGD on every parameter in one launch (nn.py:539-543, the reference's
 // W <- W - truncate(c * grad) per parameter): tensor i's elements use its own
 // TRUNC_RHO / TRUNC_R counters; the pair space of all tensors is one
@@ -1214,6 +1410,68 @@ int mpc3_rss_window_gather(const uint64_t* x, uint64_t* out, int64_t N, int64_t 
   launch_pdl(window_gather_kernel, dim3(grid_for(n, 256)), dim3(256), 0, as_stream(stream), x, out,
              pool_geom(N, C, H, W, OH, OW, kh, kw, sh, sw), ph, pw, pad);
   return check_launch("rss_window_gather");
+}
+
+size_t mpc3_rss_softmax_loss_scratch(uint64_t rows, uint64_t d) {
+  return (size_t)(2 * rows * ((d + 1) / 2) * 3 + 3 * rows + 2 * 3 * rows * d + 2 * 3 * rows) * sizeof(uint64_t);
+}
+
+int mpc3_rss_softmax_loss(const uint32_t* rk3, const uint64_t* ctr, const mpc3_softmax_loss_args* a, const uint64_t* z,
+                          const uint64_t* y, uint64_t* scratch, uint64_t* out, uint64_t rows, uint64_t d,
+                          void* stream) {
+  if (!a || !z || !y || !scratch || !out) return MPC3_ERR_CONFIG;
+  int lv = 0;
+  for (uint64_t mm = d; mm > 1; mm = mm / 2 + mm % 2) ++lv;
+  if (d < 2 || a->levels != lv || lv > MT_MAX_LEVELS) return MPC3_ERR_SHAPE;
+  if (a->row_off + rows > a->rows_total || (a->row_off & 1)) return MPC3_ERR_SHAPE;
+  if (a->bits < 1 || a->bits > 61) return MPC3_ERR_RANGE;
+  if (rows == 0) return MPC3_OK;
+  LossArgs la;
+  la.levels = lv;
+  for (int l = 0; l < lv; ++l) {
+    if (a->j_bin[l] >= (1ull << 48) || a->j_xor[l] + 6 >= (1ull << 48) || a->j_arith[l] + 2 >= (1ull << 48))
+      return MPC3_ERR_RANGE;
+    la.jbin[l] = a->j_bin[l];
+    la.jxor[l] = a->j_xor[l];
+    la.ja[l] = a->j_arith[l];
+  }
+  const MPC3ChainStep* progs[2] = {a->exp_steps, a->rec_steps};
+  const int counts[2] = {a->exp_count, a->rec_count};
+  ChainProgram* dst[2] = {&la.ep, &la.rp};
+  for (int q = 0; q < 2; ++q) {
+    if (counts[q] < 0 || counts[q] > MPC3_CHAIN_MAX_STEPS || (counts[q] && !progs[q])) return MPC3_ERR_CONFIG;
+    dst[q]->nsteps = counts[q];
+    dst[q]->nmul = 0;
+    for (int i = 0; i < counts[q]; ++i) {
+      dst[q]->s[i] = progs[q][i];
+      const int op = progs[q][i].op;
+      if (op < MPC3_CHAIN_ADDC || op > MPC3_CHAIN_SQT) return MPC3_ERR_CONFIG;
+      if (op == MPC3_CHAIN_SQ || op == MPC3_CHAIN_MULX || op == MPC3_CHAIN_SQT) {
+        if (progs[q][i].bits < 1 || progs[q][i].bits > 61) return MPC3_ERR_RANGE;
+        ++dst[q]->nmul;
+      }
+    }
+  }
+  for (int i = 0; i < 3; ++i) {
+    la.ej[i] = a->exp_j[i];
+    la.rj[i] = a->rec_j[i];
+    la.fj[i] = a->fin_j[i];
+    if (la.ej[i] + la.ep.nmul >= (1ull << 48) || la.rj[i] + la.rp.nmul >= (1ull << 48) || la.fj[i] >= (1ull << 48))
+      return MPC3_ERR_RANGE;
+  }
+  la.bits = a->bits;
+  la.rows_total = a->rows_total;
+  la.row_off = a->row_off;
+  KeySched ks;
+  if (int e = load_keys(rk3, 3, stream, &ks)) return e;
+  const int R = 2;
+  const int smem = kAesSmemBytes + (MT_PMAX * sign_slots(true) * SW_SLOT_BYTES > LOSS_SLOT_BYTES
+                                        ? MT_PMAX * sign_slots(true) * SW_SLOT_BYTES
+                                        : LOSS_SLOT_BYTES);
+  if (!aes_attr((const void*)softmax_loss_kernel, smem)) return check_launch("softmax_loss smem attribute");
+  launch_pdl(softmax_loss_kernel, dim3((unsigned)((rows + R - 1) / R)), dim3(kThreads), smem, as_stream(stream), ks,
+             ctr, la, z, y, scratch, out, rows, d, R);
+  return check_launch("rss_softmax_loss");
 }
 
 }  // extern "C"

@@ -62,6 +62,8 @@ CS_PACKS = os.environ.get("MPC3_CS_PACKS", "1") == "1"
 SIMT_MACS = int(os.environ.get("MPC3_SIMT_MACS", "0"))
 # MPC3_MAXTREE_FUSED=0: one launch per max_tree level instead of one for the whole tree
 MAXTREE_FUSED = os.environ.get("MPC3_MAXTREE_FUSED", "1") == "1"
+# MPC3_LOSS_FUSED=0: the loss gradient softmax(z) - y as its separate launches
+LOSS_FUSED = os.environ.get("MPC3_LOSS_FUSED", "1") == "1"
 # the one-launch max_tree runs two rows per CTA (a latency design for the
 # softmax's (batch, classes) rows); many rows (max-pool windows) go level by
 # level through the persistent sign kernel instead
@@ -1315,6 +1317,60 @@ class TrioSession:
 
     def division(self, x, y, cfg: ReciprocalConfig = ReciprocalConfig()):
         return self.mul_truncate(x, self.reciprocal(y, cfg))
+
+    def softmax_loss(self, z: RssTensor, y: RssTensor, cfg: ReciprocalConfig = ReciprocalConfig(),
+                     exp_cfg: ExpConfig = ExpConfig()) -> RssTensor:
+        """softmax(z) - y (the loss gradient, nn.py:561-568) in ONE launch
+        (mpc3_rss_softmax_loss): the counters, PRF words, shares and
+        accounting of softmax() followed by sub()."""
+        rows_shape, d = z.shape[:-1], z.shape[-1]
+        rows = int(np.prod(rows_shape, dtype=np.int64)) if rows_shape else 1
+        if d > cfg.Y:
+            raise ConfigError(f"class count {d} exceeds reciprocal domain Y={cfg.Y}")
+        if y.shape != z.shape:
+            raise ShapeError(f"logit/label shapes {z.shape} vs {y.shape}")
+        levels, mm = [], d
+        while mm > 1:
+            levels.append(mm)
+            mm = mm // 2 + mm % 2
+        s = exp_cfg.squarings
+        if self.fp.t + 2 * s > 61:
+            raise ConfigError(f"m={exp_cfg.m} too large for t={self.fp.t}")
+        exp_steps = [(K.CHAIN_ADDC, 0, int(fx_encode(float(exp_cfg.m), self.fp)))]
+        exp_steps += [(K.CHAIN_SQ, self.fp.t + 2 * s if i == 0 else self.fp.t, 0) for i in range(s)]
+        rec_steps = [(K.CHAIN_SETC, 0, int(fx_encode(1.0 / cfg.Y, self.fp)))]
+        for _ in range(cfg.iterations):
+            rec_steps += [(K.CHAIN_SQT, self.fp.t, 0), (K.CHAIN_MULX, self.fp.t, 0), (K.CHAIN_NEWTON, 0, 0)]
+        row_off, rows_total = self.shard_offset(rows)
+        if not levels or len(levels) > 16 or len(exp_steps) > K.CHAIN_MAX_STEPS or \
+                len(rec_steps) > K.CHAIN_MAX_STEPS or row_off % 2:
+            return self.sub(self.softmax(z, cfg), y)
+        z, y = z.contiguous(), y.contiguous()
+        a = K.SoftmaxLossArgs()
+        a.levels = len(levels)
+        for i, ml in enumerate(levels):  # max_tree (protocols.py:356-380)
+            a.j_bin[i], a.j_xor[i], a.j_arith[i] = self.take(BIN), self.take(XOR, 7), self.take(ARITH, 3)
+            self._charge_sign(rows * (ml // 2), K.MODE_RELU)
+        prog_e, ne = K.chain_program(exp_steps)
+        prog_r, nr = K.chain_program(rec_steps)
+        for j, prog, n, steps, cnt in ((a.exp_j, prog_e, ne, exp_steps, rows * d), (a.rec_j, prog_r, nr, rec_steps, rows)):
+            nmul = sum(1 for op, _, _ in steps if op in (K.CHAIN_SQ, K.CHAIN_MULX, K.CHAIN_SQT))
+            j[0], j[1], j[2] = self.take(ARITH, nmul), self.take(TR_RHO, nmul), self.take(TR_R, nmul)
+            for _ in range(nmul):
+                self.ledger.ring("mul.reshare", cnt)
+                self._charge_trunc(cnt)
+        a.exp_steps, a.exp_count = C.cast(prog_e, C.POINTER(K.ChainStep)), ne
+        a.rec_steps, a.rec_count = C.cast(prog_r, C.POINTER(K.ChainStep)), nr
+        a.fin_j[0], a.fin_j[1], a.fin_j[2] = self.take(ARITH), self.take(TR_RHO), self.take(TR_R)
+        self.ledger.ring("mul.reshare", rows * d)
+        self._charge_trunc(rows * d)
+        a.bits = self.fp.t
+        a.row_off, a.rows_total = row_off, rows_total
+        scratch = torch.empty(K.lib().mpc3_rss_softmax_loss_scratch(rows, d) // 8, dtype=torch.int64, device=_dev())
+        out = empty(z.shape, z.fp)
+        K.call("mpc3_rss_softmax_loss", self.rk, self.ctr_ptr, C.byref(a), z.data.data_ptr(), y.data.data_ptr(),
+               scratch.data_ptr(), out.data.data_ptr(), rows, d, _stream())
+        return out
 
     def softmax(self, z: RssTensor, cfg: ReciprocalConfig = ReciprocalConfig()) -> RssTensor:
         d = z.shape[-1]

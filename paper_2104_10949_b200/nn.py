@@ -26,7 +26,7 @@ import torch
 
 from . import engine as E
 from .engine import ReciprocalConfig, RssTensor, TrioSession
-from .errors import ConfigError, ProtocolError, ShapeError
+from .errors import ConfigError, ProtocolError, RangeError, ShapeError
 from .ring import DEFAULT_FP, FixedPointConfig, fx_decode, fx_encode
 from .sharing import ArithmeticShare, PartyContext, assemble, split_trio
 
@@ -469,6 +469,8 @@ class TrioNet:
         """softmax(logits) - y (nn.py:561-568)."""
         if logits.shape[-1] != y.shape[-1]:
             raise ShapeError(f"logit/label length mismatch {logits.shape} vs {y.shape}")
+        if E.LOSS_FUSED and logits.shape == y.shape:  # one launch (mpc3_rss_softmax_loss), same shares
+            return self.s.softmax_loss(logits, y)
         return self.s.sub(self.s.softmax(logits), y)
 
 
@@ -540,8 +542,16 @@ class TrainState:
         self.sess, self.model, self.cfg, self.owner = sess, model, cfg, owner
         self.net = TrioNet(sess)
         self.rng = np.random.default_rng(cfg.seed)
-        plain = init_params(model, sess.fp, cfg.seed) if params is None else params
-        self.params = [sess.share(w, self.rng, owner=owner) for w in plain]
+        # encoded (ring.py:104-115) and dealt on the device: the PCG64 draws
+        # numpy's Generator would make (sharing.py:113-118), the host
+        # Generator advanced past them; init_params = fx_encode of these
+        # floats (nn.py:190-202), |w| <= 1 so always in range
+        if params is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+            plain = [sess.fx_encode_device(torch.from_numpy(w).to(dev)) for w in init_params_float(model, cfg.seed)]
+        else:
+            plain = [E.to_device(w) for w in params]
+        self.params = [sess.share_device(w, self.rng, owner=owner) for w in plain]
         self.bbits = batch_bits(cfg.batch_size)
         self.inv_b = int(fx_encode(1.0 / cfg.batch_size, sess.fp)) if self.bbits == 0 else 0
 
@@ -837,18 +847,43 @@ class InferenceGraph:
 
 
 def train_trio(sess: TrioSession, model: ModelGraph, cfg: TrainConfig, images: np.ndarray, labels: np.ndarray,
-               owner: int = 0) -> TrainResult:
-    """train_private with all three parties in one thread (nn.py:679-751)."""
+               owner: int = 0, graph: bool = True) -> TrainResult:
+    """train_private with all three parties in one thread (nn.py:679-751).
+
+    The owner's batches go to the device as float64 and are fx-encoded and
+    dealt there (mpc3_fx_encode; the PCG64 dealer reproduces numpy's draws,
+    sharing.py:113-118), and from the second iteration on the step replays a
+    CUDA graph when at least two iterations remain (GraphStep: the same
+    counters, shares and CommStats as the eager step)."""
     st = TrainState(sess, model, cfg, owner)
     n = len(images)
     if n < 1:
         raise ConfigError("empty training set")
     d = model.num_classes
     ce = []
+    dev = torch.device("cuda", torch.cuda.current_device())
+    bad = torch.zeros(1, dtype=torch.int32, device=dev)  # (range checked on the host per batch)
+    images = np.asarray(images, dtype=np.float64)
+    lim = float(1 << (63 - sess.fp.t))
+    step_graph, xs_static, ys_static = None, None, None
     for it in range(cfg.iterations):
         idx = batch_indices(it, cfg.batch_size, n)
-        xs, ys = st.deal_batch(fx_encode(images[idx], sess.fp), fx_encode(one_hot(labels[idx], d), sess.fp))
-        logits = st.step(xs, ys)
+        batch = np.ascontiguousarray(images[idx])
+        if not np.isfinite(batch).all() or np.abs(batch).max(initial=0.0) >= lim:  # fx_encode's check, ring.py:107-115
+            raise RangeError(f"|x| must be < 2^{63 - sess.fp.t}")
+        xb = torch.from_numpy(batch).to(dev, non_blocking=True)
+        yb = torch.from_numpy(one_hot(labels[idx], d)).to(dev, non_blocking=True)
+        xs = sess.share_device(sess.fx_encode_device(xb, bad), st.rng, owner=owner)
+        ys = sess.share_device(sess.fx_encode_device(yb, bad), st.rng, owner=owner)
+        if graph and step_graph is None and it >= 1 and cfg.iterations - it >= 2:
+            xs_static, ys_static = RssTensor(xs.data.clone()), RssTensor(ys.data.clone())
+            step_graph = st.capture(xs_static, ys_static)
+        if step_graph is not None:
+            xs_static.data.copy_(xs.data)
+            ys_static.data.copy_(ys.data)
+            logits = step_graph.replay()
+        else:
+            logits = st.step(xs, ys)
         ce.append(cross_entropy(fx_decode(sess.reveal(logits), sess.fp), labels[idx]))
     weights = [sess.reveal(p) for p in st.params]
     return TrainResult(weights=weights, ce_history=ce)

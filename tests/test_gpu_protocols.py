@@ -222,3 +222,33 @@ def test_dgrad_formulations_share_for_share(nb, o, oh, ow, c, kh, kw, ph):
         outs.append((y.data.cpu().numpy().view(np.uint64), dict(s.seq)))
     assert np.array_equal(outs[0][0], outs[1][0])
     assert outs[0][1] == outs[1][1]
+
+
+@pytest.mark.parametrize("rows,d,shard", [(128, 10, None), (7, 10, None), (32, 200, None), (3, 2, None),
+                                          (5, 3, None), (64, 37, (2, 4)), (1, 10, None)])
+def test_fused_softmax_loss_equals_separate_launches_and_oracle(rows, d, shard):
+    """mpc3_rss_softmax_loss (max_tree, exp, row sum, reciprocal, mul +
+    truncate and the label sub in ONE launch) = softmax() then sub(): every
+    share, the counters consumed and the CommStats; and = the oracle's
+    softmax(z) - y (protocols.py:453-468)."""
+    from paper_2104_10949_b200.nn import DataParallel
+
+    rng = np.random.default_rng(rows * 1000 + d)
+    z = R.share(R.fx_encode(rng.uniform(-6, 6, (rows, d))), rng)
+    y = R.share(R.fx_encode(np.eye(d)[rng.integers(0, d, rows)]), rng)
+    outs = []
+    for fused in (True, False):
+        s = TrioSession(12)
+        if shard is not None:
+            s.dp = DataParallel(shard[0], shard[1], None)
+        base = [t.stats.copy() for t in s.ledger.parties]
+        zs, ys = s.from_components(z), s.from_components(y)
+        g = s.softmax_loss(zs, ys) if fused else s.sub(s.softmax(zs), ys)
+        acct = [t.stats.since(b) for t, b in zip(s.ledger.parties, base)]
+        outs.append((g.data.cpu().numpy().view(U64), dict(s.seq), [(a.round_labels, a.payload_bytes_sent())
+                                                                   for a in acct]))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert outs[0][1] == outs[1][1]
+    assert outs[0][2] == outs[1][2]
+    if shard is None:
+        assert np.array_equal(outs[0][0], R.softmax(R.Session(12), z) - y)
