@@ -411,12 +411,15 @@ def roofline_of(rec: Recorder, summ: dict, peaks: dict, sm_mhz: float, traffic: 
     return r
 
 
-def _traffic():
+def _traffic(workload: str = "alexnet"):
     """ncu dram__bytes_read.sum + dram__bytes_write.sum per launch from the
-    committed profiles (tools/traffic.py), keyed by kernel class."""
+    committed profiles (tools/traffic.py: one ncu pass over one step of the
+    workload), keyed by kernel class."""
     t = {}
-    for cls, fn in (("gemm", "r02_traffic_gemm.json"), ("sign", "r02_traffic_sign.json"),
-                    ("gemm", "r01_gemm_traffic.json")):
+    files = (("gemm", "r02_traffic_gemm.json"), ("sign", "r02_traffic_sign.json"), ("gemm", "r01_gemm_traffic.json"))
+    if workload == "resnet50_b64":
+        files = (("sign", "r02_traffic_r50_sign.json"),)
+    for cls, fn in files:
         if cls in t:
             continue
         try:
@@ -870,7 +873,7 @@ def resnet50_inference(dev, batch: int, steps: int, rec=None, peaks=None, sm_mhz
         net = TrioNet(sess)
         _instrumented(lambda: net.forward(model, params, x, record=False), rec, torch)
         summ = rec.summary(t)
-        out["roofline"] = roofline_of(rec, summ, peaks or {}, sm_mhz, _traffic())
+        out["roofline"] = roofline_of(rec, summ, peaks or {}, sm_mhz, _traffic("resnet50_b64" if batch == 64 else ""))
         rec.events.clear()
     return out
 

@@ -381,17 +381,8 @@ int mpc3_ring_gemm_packed_layout(const uint8_t* A, const uint8_t* B, uint64_t* C
                                  int64_t N, int64_t kp, int64_t ldc, int64_t c_group, int splits, int c_layout,
                                  void* stream);
 
-/* Stream-K form of mpc3_ring_gemm_packed_layout for GEMMs with few tiles:
- * `ctas` persistent CTAs (<= the SM count) take equal contiguous ranges of the
- * (group, m-tile, n-tile, K-block) iterations and atomically add their
- * partial tiles, so C must be zeroed.  Exact for any kp (segments are capped
- * at 16384 K). */
-int mpc3_ring_gemm_streamk(const uint8_t* A, const uint8_t* B, uint64_t* C, int groups, int64_t M, int64_t N,
-                           int64_t kp, int64_t ldc, int64_t c_group, int ctas, int c_layout, void* stream);
-
 /* C[g] = A[g] . B[g]^T with the launch shape chosen for the size: split-K
- * (exactness above 16384 K, occupancy for few tiles, <= one wave) or
- * stream-K when that grid would leave SMs idle.  C is dense ([g][M][N], or
+ * (exactness above 16384 K, occupancy for few tiles, <= one wave).  C is dense ([g][M][N], or
  * [g][N][M] for c_layout 1) and is zeroed here when partial sums are
  * accumulated atomically. */
 int mpc3_ring_gemm_auto(const uint8_t* A, const uint8_t* B, uint64_t* C, int groups, int64_t M, int64_t N,
@@ -424,30 +415,6 @@ int mpc3_ring_gemm_t(const uint8_t* A, int a_mn, int64_t a_rows, int64_t a_kp, i
 int mpc3_ring_gemm_t_z(const uint8_t* A, int a_mn, int64_t a_rows, int64_t a_kp, int64_t a_half, const uint8_t* B,
                        int b_mn, int64_t b_rows, int64_t b_kp, int64_t b_half, uint64_t* C, int groups, int64_t M,
                        int64_t N, int64_t kc_half, int c_layout, int c_zeroed, void* stream);
-
-/* The three parties' cross terms of a SMALL secure layer on the CUDA cores
- * (64-bit IMAD, no limb packs / TMA / TMEM set-up):
- *   z[g] = [a_g + a_{g+1} | a_g] . [b_g | b_{g+1}]^T,  g = 0, 1, 2,
- * gathered through the operand descriptors (op_a->k == op_b->k = K).
- * z: 3 x op_a->rows x op_b->rows, row-major (c_layout 0) or column-major (1).
- * Exact mod 2^64 for any K.  The engine routes layers below ~2^22 ring MACs
- * per party here (the fully-connected tails). */
-int mpc3_ring_gemm_cross_simt(const uint64_t* src_a, int64_t plane_a, const mpc3_operand* op_a,
-                              const uint64_t* src_b, int64_t plane_b, const mpc3_operand* op_b, uint64_t* z,
-                              int c_layout, void* stream);
-
-/* The secure layer's per-party cross terms as ONE implicit ring GEMM per
- * party (protocols.py:110-115):
- *   C[g] = [a_g + a_{g+1} | a_g] . [b_g | b_{g+1}]^T,  g = 0, 1, 2,
- * gathered straight from the trio tensors through the operand descriptors
- * (dense / im2col / weight-gradient views, op_a->k == op_b->k = K, inner
- * length 2K): producer warps split the gathered u64 values into byte limbs in
- * shared memory, so no packed operand is materialised.  C: 3 groups of
- * op_a->rows x op_b->rows, leading dim ldc, group stride c_group; splits > 1
- * needs C zeroed. */
-int mpc3_ring_gemm_cross(const uint64_t* src_a, int64_t plane_a, const mpc3_operand* op_a, const uint64_t* src_b,
-                         int64_t plane_b, const mpc3_operand* op_b, uint64_t* C, int64_t ldc, int64_t c_group,
-                         int splits, void* stream);
 
 /* Reference GPU path (CUDA cores, 64-bit IMAD): C = A . B mod 2^64 with
  * arbitrary strides; used as an on-device cross-check and for tiny shapes. */

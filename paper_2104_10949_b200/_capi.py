@@ -211,13 +211,8 @@ _SIGS = {
     "mpc3_ring_gemm_auto": (C.c_int, [_P, _P, _P, C.c_int, _I64, _I64, _I64, C.c_int, _P]),
     "mpc3_ring_gemm_t": (C.c_int, [_P, C.c_int, _I64, _I64, _I64, _P, C.c_int, _I64, _I64, _I64, _P, C.c_int, _I64,
                                    _I64, _I64, C.c_int, _P]),
-    "mpc3_ring_gemm_streamk": (C.c_int, [_P, _P, _P, C.c_int, _I64, _I64, _I64, _I64, _I64, C.c_int, C.c_int, _P]),
     "mpc3_ring_gemm_packed_layout": (C.c_int, [_P, _P, _P, C.c_int, _I64, _I64, _I64, _I64, _I64, C.c_int, C.c_int,
                                                _P]),
-    "mpc3_ring_gemm_cross": (C.c_int, [_P, _I64, C.POINTER(Operand), _P, _I64, C.POINTER(Operand), _P, _I64, _I64,
-                                       C.c_int, _P]),
-    "mpc3_ring_gemm_cross_simt": (C.c_int, [_P, _I64, C.POINTER(Operand), _P, _I64, C.POINTER(Operand), _P, C.c_int,
-                                            _P]),
     "mpc3_ring_gemm_simt": (C.c_int, [_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _P]),
     "mpc3_ring_matmul_workspace": (C.c_size_t, [_I64, _I64, _I64]),
     "mpc3_ring_matmul_u64": (C.c_int, [_P, _P, _P, _I64, _I64, _I64, _P, _P]),

@@ -222,78 +222,6 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const uint64_t* __restri
   }
 }
 
-// Small secure layers (the fully-connected tails, K2 * M * N below a few
-// million ring MACs per party): the three parties' cross terms
-//   z_g = [a_g + a_{g+1} | a_g] . [b_g | b_{g+1}]^T
-// with 64-bit IMADs straight from the trio tensors (operand descriptors, any
-// view): no limb packs, no TMA / TMEM set-up, ~3 us instead of the tensor
-// path's ~10 us fixed cost (prologue, first stage, epilogue) plus two packs.
-constexpr int CS_T = 64, CS_K = 16;
-__global__ void __launch_bounds__(256) gemm_cross_simt_kernel(const uint64_t* __restrict__ sa_src, int64_t plane_a,
-                                                              Operand oa, const uint64_t* __restrict__ sb_src,
-                                                              int64_t plane_b, Operand ob, uint64_t* __restrict__ z,
-                                                              int64_t M, int64_t N, int c_col, int64_t kspl,
-                                                              int splits) {
-  __shared__ uint64_t sa[CS_K][CS_T + 1], sb[CS_K][CS_T + 1];
-  const int g = blockIdx.z / splits, gn = (g + 1) % 3, split = blockIdx.z % splits;
-  const int t = threadIdx.x, tx = t % 16, ty = t / 16;
-  const int64_t m0 = (int64_t)blockIdx.y * CS_T, n0 = (int64_t)blockIdx.x * CS_T;
-  const int64_t K = oa.k, K2 = 2 * K;
-  const int64_t kbeg = split * kspl, kend = kbeg + kspl < K2 ? kbeg + kspl : K2;
-  uint64_t acc[4][4] = {};
-  griddep_wait();
-  for (int64_t k0 = kbeg; k0 < kend; k0 += CS_K) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int e = t + 256 * i, kk = e % CS_K, rr = e / CS_K;
-      const int64_t kp = k0 + kk, h = kp >= K, k = kp - h * K;
-      uint64_t va = 0, vb = 0;
-      if (kp < kend) {
-        const int64_t m = m0 + rr, n = n0 + rr;
-        if (m < M) {
-          const int64_t off = gather_offset(oa, m, k);
-          if (off >= 0) va = h ? sa_src[g * plane_a + off] : sa_src[g * plane_a + off] + sa_src[gn * plane_a + off];
-        }
-        if (n < N) {
-          const int64_t off = gather_offset(ob, n, k);
-          if (off >= 0) vb = sb_src[(h ? gn : g) * plane_b + off];
-        }
-      }
-      sa[kk][rr] = va;
-      sb[kk][rr] = vb;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < CS_K; ++kk) {
-      uint64_t a[4], b[4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) a[r] = sa[kk][ty + 16 * r];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) b[c] = sb[kk][tx + 16 * c];
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[r][c] += a[r] * b[c];
-    }
-    __syncthreads();
-  }
-  griddep_launch();
-  uint64_t* zg = z + (int64_t)g * M * N;
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int64_t m = m0 + ty + 16 * r, n = n0 + tx + 16 * c;
-      if (m < M && n < N) {
-        uint64_t* dst = zg + (c_col ? n * M + m : m * N + n);
-        if (splits > 1)
-          atomicAdd(reinterpret_cast<unsigned long long*>(dst), (unsigned long long)acc[r][c]);
-        else
-          *dst = acc[r][c];
-      }
-    }
-}
-
 // ---------------------------------------------------------------------------
 // tcgen05 kernel
 
@@ -620,332 +548,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------
-// Stream-K variant for GEMMs with fewer tiles than a few waves: the
-// (group, m-tile, n-tile, K-block) iteration space is cut into equal
-// contiguous ranges, one per persistent CTA (<= 148), so no SM idles in a
-// last partial wave.  A CTA's range crosses tile boundaries; each maximal run
-// inside one tile (at most MAX_SPLIT_K/BK K-blocks, the exactness bound) is a
-// segment whose partial sum is atomically added into the zeroed C.  The TMA /
-// MMA pipeline runs across segments; TMEM is handed back by the epilogue
-// through tmem_empty.
-struct SkSeg {
-  int tile, kb0, nkb;
-};
-DEV SkSeg sk_seg(int64_t it, int64_t it_end, int nkb_total) {
-  SkSeg sg;
-  sg.tile = (int)(it / nkb_total);
-  sg.kb0 = (int)(it % nkb_total);
-  int64_t rem_tile = nkb_total - sg.kb0, rem = it_end - it;
-  int64_t n = rem_tile < rem ? rem_tile : rem;
-  const int cap = MAX_SPLIT_K / BK;
-  sg.nkb = (int)(n < cap ? n : cap);
-  return sg;
-}
-
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
-    gemm_sk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   uint64_t* __restrict__ C, int64_t M, int64_t N, int64_t kp, int64_t ldc, int64_t c_group,
-                   int mt, int nt, int64_t total_iters, int c_col, MnArgs mn) {
-  griddep_launch();
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * A_STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tmem_full = empty + STAGES;
-  uint64_t* tmem_empty = tmem_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int nkb_total = (int)((kp + BK - 1) / BK);
-  const int64_t it_begin = total_iters * blockIdx.x / gridDim.x;
-  const int64_t it_end = total_iters * (blockIdx.x + 1) / gridDim.x;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    mbar_init(tmem_full, 1);
-    mbar_init(tmem_empty, 32 * EPI_WARPS);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  const uint32_t tmem = *tmem_slot;
-  griddep_wait();  // packed operands and the zeroed C are the previous kernels' data
-
-  if (warp == 0 && lane == 0) {
-    // ---- TMA producer: all segments back to back ----
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-    int i = 0;
-    for (int64_t it = it_begin; it < it_end;) {
-      const SkSeg sg = sk_seg(it, it_end, nkb_total);
-      const int g = sg.tile / (mt * nt), tmn = sg.tile % (mt * nt);
-      const int m0 = (tmn / nt) * BM, n0 = (tmn % nt) * BN;
-      for (int k = 0; k < sg.nkb; ++k, ++i) {
-        const int s = i % STAGES;
-        mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
-        load_stage(&tmA, &tmB, &full[s], sA + s * A_STAGE, sB + s * B_STAGE, sg.kb0 + k, m0, n0, g, mn);
-      }
-      it += sg.nkb;
-    }
-  } else if (warp == 1 && lane == 0) {
-    // ---- MMA issuer ----
-    int i = 0, seg = 0;
-    for (int64_t it = it_begin; it < it_end; ++seg) {
-      const SkSeg sg = sk_seg(it, it_end, nkb_total);
-      if (seg > 0) {  // the epilogue has drained the previous segment's accumulators
-        mbar_wait(tmem_empty, (seg - 1) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-      }
-      for (int k = 0; k < sg.nkb; ++k, ++i) {
-        const int s = i % STAGES;
-        const uint32_t ph = (i / STAGES) & 1;
-        mbar_wait(&full[s], ph);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        mma_stage(tmem, smem_u32(sA + s * A_STAGE), smem_u32(sB + s * B_STAGE), k == 0, mn);
-        mma_commit(&empty[s]);
-      }
-      mma_commit(tmem_full);
-      it += sg.nkb;
-    }
-  } else if (warp >= 4) {
-    // ---- epilogue: TMEM -> registers -> recombine -> atomic add into C ----
-    const int64_t rs = c_col ? 1 : ldc, cs = c_col ? ldc : 1;
-    int seg = 0;
-    for (int64_t it = it_begin; it < it_end; ++seg) {
-      const SkSeg sg = sk_seg(it, it_end, nkb_total);
-      const int g = sg.tile / (mt * nt), tmn = sg.tile % (mt * nt);
-      const int64_t m0 = (int64_t)(tmn / nt) * BM, n0 = (int64_t)(tmn % nt) * BN;
-      mbar_wait(tmem_full, seg & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      epilogue_tile(tmem, warp - 4, lane, true, C + (int64_t)g * c_group, m0, n0, M, N, rs, cs, true);
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      mbar_arrive(tmem_empty);
-      it += sg.nkb;
-    }
-  }
-  __syncthreads();
-  if (warp == 2) {
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Implicit ring GEMM: the secure layer's cross terms straight from the trio
-// tensors.  Producer warps gather the u64 operand values (dense / im2col /
-// weight-gradient views, protocols.py:110-115 cross-term concatenation),
-// split them into byte limbs and write the 32-byte-swizzled K-major tiles the
-// UMMA descriptors read; no packed operand ever touches HBM.  MMA issue,
-// TMEM accumulation and the epilogue are those of gemm_tc_kernel.
-
-constexpr int IG_PRODUCERS = 128;  // warps 0-3
-constexpr int IG_THREADS = 288;    // + warp 4 (MMA, TMEM alloc) + warps 5-8 (epilogue)
-
-// byte offset of (row, 4-byte k-group kq) in a K-major SWIZZLE_32B tile
-// (Swizzle<1,4,3>: the 16-byte chunk index XORs with row bit 2)
-DEV uint32_t sw32_off(int row, int kq) {
-  uint32_t off = (uint32_t)row * 32 + (uint32_t)kq * 4;
-  return off ^ ((((uint32_t)row >> 2) & 1u) << 4);
-}
-
-
-// 4 consecutive packed values (k .. k+3 of the 2K-long cross-term row) ->
-// 8 limb words of 4 bytes each, stored into the limb planes of one tile.
-DEV void produce4(const uint64_t* __restrict__ src, int64_t plane, const Operand& o, int role, int g, int64_t r,
-                  int64_t rows, int64_t k, uint8_t* tile, int row_in_tile, int kq, int limb_stride) {
-  uint64_t v[4] = {0, 0, 0, 0};
-  if (r < rows) {
-    const int64_t K = o.k;
-    const int gn = (g + 1) % 3;
-    GatherCursor cur;
-    int half = -1;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      int64_t kk = k + j;
-      if (kk >= 2 * K) break;
-      int h = kk >= K ? 1 : 0;
-      if (h != half) {
-        cur.init(o, r, h ? kk - K : kk);
-        half = h;
-      }
-      int64_t off = cur.offset(o);
-      if (off >= 0) {
-        uint64_t self = __ldg(src + g * plane + off), nxt = __ldg(src + gn * plane + off);
-        v[j] = role == 0 ? (h == 0 ? self + nxt : self) : (h == 0 ? self : nxt);
-      }
-      cur.next(o);
-    }
-  }
-  uint32_t lo[4], hi[4], tl[4], th[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    lo[j] = (uint32_t)v[j];
-    hi[j] = (uint32_t)(v[j] >> 32);
-  }
-  byte_transpose4(lo, tl);  // tl[l] = byte l of v[0..3]
-  byte_transpose4(hi, th);
-  uint32_t o_ = sw32_off(row_in_tile, kq);
-#pragma unroll
-  for (int l = 0; l < 4; ++l) {
-    *reinterpret_cast<uint32_t*>(tile + l * limb_stride + o_) = tl[l];
-    *reinterpret_cast<uint32_t*>(tile + (l + 4) * limb_stride + o_) = th[l];
-  }
-}
-
-__global__ void __launch_bounds__(IG_THREADS, 1)
-    gemm_ig_kernel(const uint64_t* __restrict__ srcA, int64_t planeA, Operand oa, const uint64_t* __restrict__ srcB,
-                   int64_t planeB, Operand ob, uint64_t* __restrict__ C, int64_t M, int64_t N, int64_t ldc,
-                   int64_t c_group, int splits, int kb_per_split) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * A_STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tmem_full = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int64_t n0 = (int64_t)blockIdx.x * BN, m0 = (int64_t)blockIdx.y * BM;
-  const int g = blockIdx.z / splits, split = blockIdx.z % splits;
-  const int64_t kp = 2 * oa.k;
-  const int nkb_total = (int)((kp + BK - 1) / BK);
-  const int kb0 = split * kb_per_split;
-  int kb1 = kb0 + kb_per_split;
-  if (kb1 > nkb_total) kb1 = nkb_total;
-  const int nkb = kb1 > kb0 ? kb1 - kb0 : 0;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], IG_PRODUCERS);
-      mbar_init(&empty[s], 1);
-    }
-    mbar_init(tmem_full, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 4) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp < 4) {
-    // ---- producers: gather + limb split into the swizzled tiles ----
-    const int t = threadIdx.x;
-    for (int i = 0; i < nkb; ++i) {
-      int s = i % STAGES;
-      uint32_t ph = (i / STAGES) & 1;
-      mbar_wait(&empty[s], ph ^ 1);
-      const int64_t kbase = (int64_t)(kb0 + i) * BK;
-      uint8_t* ta = sA + s * A_STAGE;
-      uint8_t* tb = sB + s * B_STAGE;
-#pragma unroll 1
-      for (int task = t; task < BM * 8; task += IG_PRODUCERS) {  // A: 128 rows x 8 k-quads
-        int row = task >> 3, kq = task & 7;
-        produce4(srcA, planeA, oa, 0, g, m0 + row, M, kbase + 4 * kq, ta, row, kq, BM * BK);
-      }
-#pragma unroll 1
-      for (int task = t; task < BN * 8; task += IG_PRODUCERS) {  // B: 64 rows x 8 k-quads
-        int row = task >> 3, kq = task & 7;
-        produce4(srcB, planeB, ob, 1, g, n0 + row, N, kbase + 4 * kq, tb, row, kq, BN * BK);
-      }
-      // generic-proxy smem writes -> visible to the tensor core (async proxy)
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(&full[s]);
-    }
-  } else if (warp == 4) {
-    if (lane == 0) {
-      // ---- MMA issuer ----
-      for (int i = 0; i < nkb; ++i) {
-        int s = i % STAGES;
-        uint32_t ph = (i / STAGES) & 1;
-        mbar_wait(&full[s], ph);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        uint32_t a_base = smem_u32(sA + s * A_STAGE);
-        uint32_t b_base = smem_u32(sB + s * B_STAGE);
-#pragma unroll
-        for (int li = 0; li < 8; ++li) {
-          uint64_t da = umma_desc_sw32(a_base + li * (BM * BK));
-          int nblk = 8 - li;
-          int first = nblk > 4 ? 4 : nblk;
-          uint32_t acc = (i > 0 || li > 0) ? 1u : 0u;
-          mma_i8(tmem + li * BN, da, umma_desc_sw32(b_base), idesc_i8(first * BN), acc);
-          if (nblk > 4)
-            mma_i8(tmem + (li + 4) * BN, da, umma_desc_sw32(b_base + 4 * (BN * BK)), idesc_i8((nblk - 4) * BN),
-                   acc);
-        }
-        mma_commit(&empty[s]);
-      }
-      mma_commit(tmem_full);
-    }
-  } else {
-    // ---- epilogue (warps 5-8 cover TMEM lane quadrants 1,2,3,0) ----
-    const int wq = warp % 4;
-    const int64_t row = m0 + wq * 32 + lane;
-    uint64_t* crow = C + (int64_t)g * c_group + row * ldc;
-    if (nkb > 0) {
-      mbar_wait(tmem_full, 0);
-      asm volatile("tcgen05.fence::after_thread_sync;");
-    }
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 8) {
-      uint64_t acc[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) acc[e] = 0;
-      if (nkb > 0) {
-        // all 8 diagonals of this 8-column chunk in flight, one wait
-        uint32_t r[8][8];
-#pragma unroll
-        for (int d = 0; d < 8; ++d) {
-          uint32_t taddr = tmem + ((uint32_t)(wq * 32) << 16) + d * BN + c0;
-          asm volatile(
-              "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-              : "=r"(r[d][0]), "=r"(r[d][1]), "=r"(r[d][2]), "=r"(r[d][3]), "=r"(r[d][4]), "=r"(r[d][5]),
-                "=r"(r[d][6]), "=r"(r[d][7])
-              : "r"(taddr));
-        }
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-        for (int d = 0; d < 8; ++d)
-#pragma unroll
-          for (int e = 0; e < 8; ++e) acc[e] += (uint64_t)r[d][e] << (8 * d);
-      }
-      if (row < M) {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          int64_t col = n0 + c0 + e;
-          if (col < N) {
-            if (splits > 1)
-              atomicAdd(reinterpret_cast<unsigned long long*>(crow + col), (unsigned long long)acc[e]);
-            else
-              crow[col] = acc[e];
-          }
-        }
-      }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;");
-  }
-  __syncthreads();
-  if (warp == 4) {
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-  }
-}
-
-// ---------------------------------------------------------------------------
 // host: tensor maps via the driver entry point (no -lcuda link needed)
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -1158,39 +760,13 @@ int mpc3_ring_gemm_packed_layout(const uint8_t* A, const uint8_t* B, uint64_t* C
   return check_launch("ring_gemm_tc");
 }
 
-int mpc3_ring_gemm_streamk(const uint8_t* A, const uint8_t* B, uint64_t* C, int groups, int64_t M, int64_t N,
-                           int64_t kp, int64_t ldc, int64_t c_group, int ctas, int c_layout, void* stream) {
-  if (groups < 1 || M < 0 || N < 0 || kp < 0 || ctas < 1) return MPC3_ERR_SHAPE;
-  if (kp % 16) return MPC3_ERR_SHAPE;
-  if (c_layout != 0 && c_layout != 1) return MPC3_ERR_CONFIG;
-  if (M == 0 || N == 0 || kp == 0) return MPC3_OK;
-  if (M > (1 << 30) || N > (1 << 30)) return MPC3_ERR_SHAPE;
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(gemm_sk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess)
-      return check_launch("gemm_sk attr");
-    attr_set = true;
-  }
-  CUtensorMap ta, tb;
-  int st = make_map(&ta, A, kp, M, (int64_t)groups * 8, BM);
-  if (st) return st;
-  st = make_map(&tb, B, kp, N, (int64_t)groups * 8, BN);
-  if (st) return st;
-  const int mt = (int)((M + BM - 1) / BM), nt = (int)((N + BN - 1) / BN);
-  const int64_t nkb = (kp + BK - 1) / BK;
-  const int64_t total = (int64_t)groups * mt * nt * nkb;
-  if (ctas > total) ctas = (int)total;
-  MnArgs mn0 = {0, 0, 0, 0, 1 << 30, 0};
-  launch_pdl(gemm_sk_kernel, dim3(ctas), dim3(GEMM_THREADS), SMEM_BYTES, as_stream(stream), ta, tb, C, M, N, kp, ldc, c_group,
-             mt, nt, total, c_layout, mn0);
-  return check_launch("ring_gemm_streamk");
-}
-
-// Launch shape of mpc3_ring_gemm_auto: split-K count, stream-K, and whether
-// C must start at zero (atomic accumulation).
+// Launch shape of mpc3_ring_gemm_auto: split-K count and whether C must
+// start at zero (atomic accumulation).  (A stream-K variant for the partial
+// last wave lost in the step: its all-SM persistent grid blocks the pack and
+// side streams' work beside it, AlexNet 2.514 -> 2.524 ms; removed in round 2.)
 struct AutoPlan {
   int64_t splits;
-  bool streamk, zero;
+  bool zero;
 };
 // minimum K-blocks per split when splitting K for occupancy (MPC3_SPLIT_MINKB)
 static int64_t split_min_kb() {
@@ -1209,14 +785,7 @@ static AutoPlan auto_plan(int groups, int64_t M, int64_t N, int64_t kp) {
   if (occ < 1) occ = 1;
   AutoPlan p;
   p.splits = need > occ ? need : occ;
-  const int64_t ctas = tiles * p.splits;
-  const double eff = (double)ctas / (double)(((ctas + sms - 1) / sms) * sms);
-  // stream-K (eff < threshold) is off by default: its all-SM persistent grid
-  // blocks the pack / side streams' work beside it (AlexNet step 2.524 ms
-  // with stream-K below 0.85 wave efficiency, 2.514 ms without)
-  static const double sk_eff = getenv("MPC3_GEMM_SK") ? atof(getenv("MPC3_GEMM_SK")) : 0.0;
-  p.streamk = nkb > 0 && eff < sk_eff;
-  p.zero = nkb == 0 || p.streamk || p.splits > 1;
+  p.zero = nkb == 0 || p.splits > 1;
   return p;
 }
 
@@ -1240,11 +809,6 @@ int mpc3_ring_gemm_auto_z(const uint8_t* A, const uint8_t* B, uint64_t* C, int g
       return check_launch("gemm C memset");
   }
   if (nkb == 0) return MPC3_OK;
-  if (p.streamk) {  // the split-K grid would leave SMs idle: stream-K over every SM
-    const int64_t iters = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * groups * nkb;
-    int64_t c = iters / 2 < sms ? iters / 2 : sms;
-    return mpc3_ring_gemm_streamk(A, B, C, groups, M, N, kp, ldc, c_group, (int)(c < 1 ? 1 : c), c_layout, stream);
-  }
   return mpc3_ring_gemm_packed_layout(A, B, C, groups, M, N, kp, ldc, c_group, (int)p.splits, c_layout, stream);
 }
 
@@ -1259,14 +823,7 @@ static AutoPlan t_plan(int groups, int64_t M, int64_t N, int64_t kp) {
   if (occ < 1) occ = 1;
   AutoPlan p;
   p.splits = need > occ ? need : occ;
-  const int64_t ctas = tiles * p.splits;
-  const double eff = (double)ctas / (double)(((ctas + sms - 1) / sms) * sms);
-  // stream-K off by default here: the weight gradients run on the side stream
-  // beside the input-gradient chain, which a persistent all-SM grid would
-  // block (AlexNet step 2.79 ms without, 2.84 ms with stream-K at eff < 0.85)
-  static const double sk_eff = getenv("MPC3_GEMM_T_SK") ? atof(getenv("MPC3_GEMM_T_SK")) : 0.0;
-  p.streamk = nkb > 0 && eff < sk_eff;
-  p.zero = nkb == 0 || p.splits > 1 || p.streamk;
+  p.zero = nkb == 0 || p.splits > 1;
   return p;
 }
 
@@ -1329,79 +886,10 @@ int mpc3_ring_gemm_t_z(const uint8_t* A, int a_mn, int64_t a_rows, int64_t a_kp,
   }
   if (nkb == 0) return MPC3_OK;
   MnArgs mn = {a_mn ? 1 : 0, b_mn ? 1 : 0, (int)a_half, (int)b_half, (int)(kc_half / BK), a_cs};
-  if (p.streamk) {  // the split-K grid would leave SMs idle in its last wave: stream-K
-    static bool sk_attr = false;
-    if (!sk_attr) {
-      if (cudaFuncSetAttribute(gemm_sk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess)
-        return check_launch("gemm_sk attr");
-      sk_attr = true;
-    }
-    const int mt = (int)((M + BM - 1) / BM), nt = (int)((N + BN - 1) / BN);
-    const int64_t total = tiles * nkb;
-    int64_t c = total / 2 < sms ? total / 2 : sms;
-    if (c < 1) c = 1;
-    launch_pdl(gemm_sk_kernel, dim3((unsigned)c), dim3(GEMM_THREADS), SMEM_BYTES, as_stream(stream), ta, tb, C, M, N,
-               kp, c_layout ? M : N, M * N, mt, nt, total, c_layout, mn);
-    return check_launch("ring_gemm_t streamk");
-  }
   dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)(groups * splits));
   launch_pdl(gemm_tc_kernel, grid, dim3(GEMM_THREADS), SMEM_BYTES, as_stream(stream), ta, tb, C, M, N, kp,
              c_layout ? M : N, M * N, (int)splits, kbs, c_layout, mn);
   return check_launch("ring_gemm_t");
-}
-
-int mpc3_ring_gemm_cross(const uint64_t* src_a, int64_t plane_a, const mpc3_operand* op_a, const uint64_t* src_b,
-                         int64_t plane_b, const mpc3_operand* op_b, uint64_t* C, int64_t ldc, int64_t c_group,
-                         int splits, void* stream) {
-  if (!op_a || !op_b || splits < 1) return MPC3_ERR_CONFIG;
-  if (op_a->k != op_b->k || op_a->k < 0 || op_a->rows < 0 || op_b->rows < 0) return MPC3_ERR_SHAPE;
-  if (op_a->mode < 0 || op_a->mode > 2 || op_b->mode < 0 || op_b->mode > 2) return MPC3_ERR_CONFIG;
-  int64_t M = op_a->rows, N = op_b->rows;
-  if (M == 0 || N == 0) return MPC3_OK;
-  if (M > (1 << 30) || N > (1 << 30)) return MPC3_ERR_SHAPE;
-  Operand oa = to_operand(op_a), ob = to_operand(op_b);
-  int64_t kp = 2 * op_a->k;
-  int nkb = (int)((kp + BK - 1) / BK);
-  int kbs = (nkb + splits - 1) / splits;
-  if ((int64_t)kbs * BK > MAX_SPLIT_K) return MPC3_ERR_EXACTNESS;  // caller must split longer K
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(gemm_ig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess)
-      return check_launch("gemm_ig attr");
-    attr_set = true;
-  }
-  dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)(3 * splits));
-  gemm_ig_kernel<<<grid, IG_THREADS, SMEM_BYTES, as_stream(stream)>>>(src_a, plane_a, oa, src_b, plane_b, ob, C, M,
-                                                                      N, ldc, c_group, splits, kbs);
-  return check_launch("ring_gemm_cross");
-}
-
-int mpc3_ring_gemm_cross_simt(const uint64_t* src_a, int64_t plane_a, const mpc3_operand* op_a,
-                              const uint64_t* src_b, int64_t plane_b, const mpc3_operand* op_b, uint64_t* z,
-                              int c_layout, void* stream) {
-  if (!op_a || !op_b) return MPC3_ERR_CONFIG;
-  if (c_layout != 0 && c_layout != 1) return MPC3_ERR_CONFIG;
-  if (op_a->k != op_b->k || op_a->rows < 0 || op_b->rows < 0 || op_a->k < 0) return MPC3_ERR_SHAPE;
-  if (op_a->mode < 0 || op_a->mode > 2 || op_b->mode < 0 || op_b->mode > 2) return MPC3_ERR_CONFIG;
-  const int64_t M = op_a->rows, N = op_b->rows;
-  if (M == 0 || N == 0) return MPC3_OK;
-  if ((M + CS_T - 1) / CS_T > 65535) return MPC3_ERR_SHAPE;
-  Operand oa = to_operand(op_a), ob = to_operand(op_b);
-  // split the 2K contraction until ~2 CTAs per SM (>= 64 k per split; the
-  // splits add atomically into the zeroed z)
-  const int64_t tiles = ((N + CS_T - 1) / CS_T) * ((M + CS_T - 1) / CS_T) * 3, K2 = 2 * op_a->k;
-  int64_t splits = (2 * 148 + tiles - 1) / tiles;
-  if (splits > (K2 + 63) / 64) splits = (K2 + 63) / 64;
-  if (splits < 1) splits = 1;
-  const int64_t kspl = ((K2 + splits - 1) / splits + CS_K - 1) / CS_K * CS_K;
-  splits = (K2 + kspl - 1) / kspl;
-  if (splits < 1) splits = 1;
-  if (splits > 1 && cudaMemsetAsync(z, 0, (size_t)3 * M * N * 8, as_stream(stream)) != cudaSuccess)
-    return check_launch("cross_simt memset");
-  dim3 grid((unsigned)((N + CS_T - 1) / CS_T), (unsigned)((M + CS_T - 1) / CS_T), (unsigned)(3 * splits));
-  launch_pdl(gemm_cross_simt_kernel, grid, dim3(256), 0, as_stream(stream), src_a, plane_a, oa, src_b, plane_b, ob,
-             z, M, N, c_layout, kspl > 0 ? kspl : 1, (int)splits);
-  return check_launch("ring_gemm_cross_simt");
 }
 
 int mpc3_ring_gemm_simt(const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t M, int64_t N, int64_t K,

@@ -41,10 +41,6 @@ from .transport import Ledger
 
 U64 = np.uint64
 MAX_SPLIT_K = 16384  # per-split K bound of the int8-limb GEMM (exactness of S_3)
-# explicit pack + TMA GEMM by default; MPC3_IMPLICIT_GEMM=1 selects the in-kernel
-# gather variant (gemm_ig_kernel: 3-25x slower on the AlexNet/ResNet shapes,
-# profiles/r01_launches_alexnet_implicit.txt)
-IMPLICIT_GEMM = os.environ.get("MPC3_IMPLICIT_GEMM", "0") == "1"
 # MPC3_OVERLAP_PACK=0: pack both GEMM operands on the calling stream
 OVERLAP_PACK = os.environ.get("MPC3_OVERLAP_PACK", "1") == "1"
 SMS = 148
@@ -54,12 +50,6 @@ REUSE_PACKS = os.environ.get("MPC3_REUSE_PACKS", "1") == "1"
 # MPC3_CS_PACKS=0: role-1 operands of the training step packed with both halves
 # instead of once per component (role 3: half the pack's writes)
 CS_PACKS = os.environ.get("MPC3_CS_PACKS", "1") == "1"
-# secure layers with at most this many ring MACs (3 parties x M x N x 2K) run
-# on the CUDA cores (mpc3_ring_gemm_cross_simt).  Off by default: measured
-# slower than pack + pack + tcgen05 even for the AlexNet FC layers (128x256x256:
-# 38 vs 22 us; 64-bit IMAD chains at ~7 thread-instructions per ring MAC), and
-# the AlexNet step went 2.71 -> 2.82 ms with the FC layers routed there
-SIMT_MACS = int(os.environ.get("MPC3_SIMT_MACS", "0"))
 # MPC3_MAXTREE_FUSED=0: one launch per max_tree level instead of one for the whole tree
 MAXTREE_FUSED = os.environ.get("MPC3_MAXTREE_FUSED", "1") == "1"
 # MPC3_LOSS_FUSED=0: the loss gradient softmax(z) - y as its separate launches
@@ -750,29 +740,14 @@ class TrioSession:
     def _cross_gemm(self, a_src, a_op, b_src, b_op, M, N, Kd, c_col: bool = False, a_role: int = 0,
                     keep: list | None = None, a_packed: Packed | None = None) -> torch.Tensor:
         """z_i = (x_i + x_{i+1}) y_i + x_i y_{i+1} for the three parties, as one
-        batched ring GEMM with inner length 2K (protocols.py:110-115).
-        Default: pack_kernel writes the byte-limb planes, the TMA-fed tcgen05
-        GEMM consumes them; MPC3_IMPLICIT_GEMM=1 selects the in-kernel gather.
-        c_col: z[g] column-major (element (m, n) at n*M + m) — only on the
-        packed path; callers check `self.c_col_ok` before asking for it.
+        batched ring GEMM with inner length 2K (protocols.py:110-115): the
+        pack kernel writes the byte-limb planes, the TMA-fed tcgen05 GEMM
+        consumes them.  c_col: z[g] column-major (element (m, n) at n*M + m).
         keep / a_packed / a_role: pack A in the reusable Packed layout with
         the given role (the operand roles are symmetric), append it to `keep`,
         or take it ready-packed (training: the weight gradient reuses it)."""
-        if a_packed is None and 3 * M * N * 2 * Kd <= SIMT_MACS:
-            z = torch.empty(3 * M * N, dtype=torch.int64, device=_dev())
-            K.call("mpc3_ring_gemm_cross_simt", a_src.data_ptr(), a_src.stride(0), C.byref(a_op), b_src.data_ptr(),
-                   b_src.stride(0), C.byref(b_op), z.data_ptr(), 1 if c_col else 0, _stream())
-            return z  # (nothing packed: `keep` stays empty and the backward pass packs nothing either)
         if keep is not None or a_packed is not None:
-            if IMPLICIT_GEMM:
-                raise ConfigError("packed-operand reuse needs the explicit pack path")
             return self._cross_gemm_kept(a_src, a_op, b_src, b_op, M, N, Kd, c_col, a_role, keep, a_packed)
-        if IMPLICIT_GEMM:
-            splits = gemm_splits(M, N, 2 * Kd, groups=3)
-            z = (torch.zeros if splits > 1 else torch.empty)(3 * M * N, dtype=torch.int64, device=_dev())
-            K.call("mpc3_ring_gemm_cross", a_src.data_ptr(), a_src.stride(0), C.byref(a_op), b_src.data_ptr(),
-                   b_src.stride(0), C.byref(b_op), z.data_ptr(), N, M * N, splits, _stream())
-            return z
         if CS_PACKS:
             return self._cross_gemm_cs(a_src, a_op, b_src, b_op, M, N, Kd, c_col)
         kp = _round_up(2 * Kd, 32)  # whole 32-byte K-blocks (see pack)
@@ -861,7 +836,7 @@ class TrioSession:
 
     @property
     def c_col_ok(self) -> bool:
-        return not IMPLICIT_GEMM
+        return True
 
     def _finish(self, z, view, out: RssTensor, bits, label, bias: RssTensor | None = None, bias_dim: int = 1):
         ja = self.take(ARITH)
@@ -1410,16 +1385,6 @@ def _dgrad_cost_im2col(nb, o, oh, ow, c, kh, kw, padding):
     hf, wf = oh + kh - 1, ow + kw - 1  # stride 1
     M, K = nb * hf * wf, o * kh * kw
     return _gemm_us(M, c, 2 * K) + 48 * M * K / 2.5e12 * 1e6 + 3 * M * c * 8 / 4.0e12 * 1e6
-
-
-def gemm_splits(M: int, N: int, kp: int, groups: int) -> int:
-    """Split-K count: enough for the exactness bound, and enough CTAs to cover
-    the 148 SMs when the tile grid alone does not (>= 8 K-blocks per split)."""
-    nkb = (kp + 31) // 32
-    need = max(1, math.ceil(nkb * 32 / MAX_SPLIT_K))
-    tiles = math.ceil(M / 128) * math.ceil(N / 64) * groups
-    occ = max(1, min(SMS // tiles, nkb // 4))  # at most one wave of CTAs, >= 4 K-blocks each
-    return max(need, occ)
 
 
 def _ew2(op, a: RssTensor, b: RssTensor, out: RssTensor | None = None) -> RssTensor:

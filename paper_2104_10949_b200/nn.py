@@ -256,8 +256,7 @@ class TrioNet:
         Recording (training): each layer's weight is packed on the pack
         stream while the layer before it runs, off the critical path."""
         S = self.s
-        if record and E.REUSE_PACKS and not E.IMPLICIT_GEMM and E.OVERLAP_PACK and E.SIMT_MACS == 0 \
-                and all(sp.kind != RESIDUAL for sp in model.layers):
+        if record and E.REUSE_PACKS and E.OVERLAP_PACK and all(sp.kind != RESIDUAL for sp in model.layers):
             items, it = [], iter(params)
             for spec in model.layers:
                 if spec.kind == CONV2D:
@@ -299,7 +298,7 @@ class TrioNet:
         for li, spec in enumerate(layers):
             # recording keeps each layer input's packed GEMM operand (role 1)
             # for the weight gradient, which reads it in place
-            keep = [] if record and E.REUSE_PACKS and not E.IMPLICIT_GEMM else None
+            keep = [] if record and E.REUSE_PACKS else None
             # a conv / linear layer followed by a ReLU runs as one launch for
             # the layer's reshare + truncate and the ReLU (mpc3_rss_layer_sign)
             relu_next = FUSE_RELU and li + 1 < len(layers) and layers[li + 1].kind == RELU \

@@ -289,23 +289,6 @@ def test_ring_gemm_column_major_output(splits):
     assert np.array_equal(host(Cm).reshape(Nn, M).T, R.wrap_matmul(a, b))
 
 
-@pytest.mark.parametrize("M,K,Nn,ctas,layout", [(300, 1000, 96, 148, 1), (128, 20000, 64, 37, 0),
-                                                 (1000, 300, 200, 148, 0), (64, 40, 8, 5, 1)])
-def test_ring_gemm_streamk(M, K, Nn, ctas, layout):
-    """Stream-K: equal (tile, K-block) ranges per CTA, segments crossing tile
-    boundaries and the 16384-K exactness cap, partials atomically added."""
-    rng = np.random.default_rng(M + K + Nn)
-    a, b = rnd(rng, (M, K)), rnd(rng, (K, Nn))
-    kp = (K + 15) // 16 * 16
-    A = _pack(dev(a), 0, _capi.dense_operand(M, K, s_r=K, t2=1), 2, kp)
-    B = _pack(dev(b), 0, _capi.dense_operand(Nn, K, s_r=1, t2=Nn), 2, kp)
-    Cm = torch.zeros(M * Nn, dtype=torch.int64, device="cuda")
-    ld = M if layout else Nn
-    _capi.call("mpc3_ring_gemm_streamk", p(A), p(B), p(Cm), 1, M, Nn, kp, ld, M * Nn, ctas, layout, stream())
-    got = host(Cm).reshape(Nn, M).T if layout else host(Cm).reshape(M, Nn)
-    assert np.array_equal(got, R.wrap_matmul(a, b))
-
-
 def _pack_halves(src, plane, op, role, kp, kh):
     out = torch.empty(3 * 8 * op.rows * kp, dtype=torch.uint8, device="cuda")
     _capi.call("mpc3_ring_pack_halves", p(src), plane, C.byref(op), role, p(out), kp, kh, stream())
@@ -346,21 +329,6 @@ def test_ring_gemm_transposed_operands(Rn, O, Kc, a_mn, b_mn, layout):
         h = (g + 1) % 3
         want = R.wrap_matmul(gt[g].T + gt[h].T, xt[g]) + R.wrap_matmul(gt[g].T, xt[h])
         assert np.array_equal(got[g], want), g
-
-
-@pytest.mark.parametrize("M,K,Nn,layout", [(1, 1, 1, 0), (128, 256, 10, 0), (77, 300, 130, 1), (200, 5000, 64, 0)])
-def test_ring_gemm_cross_simt(M, K, Nn, layout):
-    """Small-layer cross terms on the CUDA cores:
-    z[g] = (x_g + x_{g+1}) y_g + x_g y_{g+1}, y read through a transposed view."""
-    rng = np.random.default_rng(M + K + Nn)
-    xt, yt = rnd(rng, (3, M, K)), rnd(rng, (3, K, Nn))
-    z = torch.full((3 * M * Nn,), -1, dtype=torch.int64, device="cuda")
-    _capi.call("mpc3_ring_gemm_cross_simt", p(dev(xt)), M * K, C.byref(_capi.dense_operand(M, K, s_r=K, t2=1)),
-               p(dev(yt)), K * Nn, C.byref(_capi.dense_operand(Nn, K, s_r=1, t2=Nn)), p(z), layout, stream())
-    got = host(z).reshape(3, Nn, M).transpose(0, 2, 1) if layout else host(z).reshape(3, M, Nn)
-    for g in range(3):
-        h = (g + 1) % 3
-        assert np.array_equal(got[g], R.wrap_matmul(xt[g] + xt[h], yt[g]) + R.wrap_matmul(xt[g], yt[h])), g
 
 
 @pytest.mark.parametrize("Mm,K,Nn,layout", [(300, 70, 150, 0), (12800, 363, 96, 1), (5, 3, 7, 1), (128, 2304, 384, 1)])
@@ -470,50 +438,6 @@ def test_avgpool_kernels():
     _capi.call("mpc3_rss_avgpool_backward", p(rk), None, 0, 0, 20, int(R.fx_encode(1.0 / 9)), p(dev(g)), p(outb), *shape,
                ref.shape[3], ref.shape[4], 3, 3, 2, 2, 0, 0, 0, stream())
     assert np.array_equal(host(outb).reshape(refb.shape), refb)
-
-
-@pytest.mark.parametrize("M,K,Nn,splits", [(1, 1, 1, 1), (9, 33, 7, 1), (130, 101, 70, 1), (300, 257, 129, 3),
-                                           (37, 9000, 40, 2), (200, 4608, 512, 1)])
-def test_implicit_cross_gemm_matches_cross_terms(M, K, Nn, splits):
-    """mpc3_ring_gemm_cross == (x_i + x_{i+1}) y_i + x_i y_{i+1} per party."""
-    rng = np.random.default_rng(M + K)
-    x = rnd(rng, (3, M, K))
-    y = rnd(rng, (3, K, Nn))
-    xd, yd = dev(x), dev(y)
-    a_op = _capi.dense_operand(M, K, s_r=K, t2=1)
-    b_op = _capi.dense_operand(Nn, K, s_r=1, t2=Nn)
-    Cm = torch.zeros(3 * M * Nn, dtype=torch.int64, device="cuda")
-    _capi.call("mpc3_ring_gemm_cross", p(xd), M * K, C.byref(a_op), p(yd), K * Nn, C.byref(b_op), p(Cm), Nn, M * Nn,
-               splits, stream())
-    got = host(Cm).reshape(3, M, Nn)
-    if M * K * Nn <= 20_000_000:
-        ref = R._bilinear3(R.wrap_matmul, x, y)
-        assert np.array_equal(got, ref)
-    else:  # compare with the explicit-pack TMA path
-        kp = (2 * K + 15) // 16 * 16
-        A = _pack(xd, M * K, a_op, 0, kp)
-        B = _pack(yd, K * Nn, b_op, 1, kp)
-        assert np.array_equal(got, _gemm_packed(A, B, 3, M, Nn, kp, 1))
-
-
-def test_implicit_cross_gemm_conv_geometries():
-    rng = np.random.default_rng(8)
-    for xs_, ks_, st, pd in [((2, 3, 10, 10), (4, 3, 3, 3), (2, 2), (1, 1)), ((4, 3, 32, 32), (96, 3, 11, 11), (4, 4), (9, 9))]:
-        n, c, h, w = xs_
-        o, _, kh, kw = ks_
-        oh, ow = R.conv_out_hw(h, w, kh, kw, st, pd)
-        x, k = rnd(rng, (3,) + xs_), rnd(rng, (3,) + ks_)
-        xd, kd = dev(x), dev(k)
-        Kc = c * kh * kw
-        a_op = _capi.conv_operand(_capi.GATHER_IM2COL, n * oh * ow, Kc, n, c, h, w, (c * h * w, h * w, w, 1), kh, kw,
-                                  st[0], st[1], pd[0], pd[1], oh, ow)
-        b_op = _capi.dense_operand(o, Kc, s_r=Kc, t2=1)
-        M = n * oh * ow
-        Cm = torch.zeros(3 * M * o, dtype=torch.int64, device="cuda")
-        _capi.call("mpc3_ring_gemm_cross", p(xd), x[0].size, C.byref(a_op), p(kd), k[0].size, C.byref(b_op), p(Cm), o,
-                   M * o, 1, stream())
-        got = host(Cm).reshape(3, n, oh, ow, o).transpose(0, 1, 4, 2, 3)
-        assert np.array_equal(got, R._bilinear3(lambda a, b: R.wrap_conv2d(a, b, st, pd), x, k))
 
 
 @pytest.mark.parametrize("n", [1, 31, 32, 33, 100003])

@@ -1,14 +1,15 @@
 """Per-launch DRAM traffic of one kernel from an ncu metrics CSV
 (dram__bytes_read.sum, dram__bytes_write.sum, gpu__time_duration.sum):
 
-python tools/traffic.py gpurun_out/gemm_traffic.csv profiles/r01_gemm_traffic.json
+python tools/traffic.py gpurun_out/gemm_traffic.csv profiles/r01_gemm_traffic.json [kernel-regex]
 """
+import re
 import csv
 import json
 import sys
 
 
-def main(src, dst):
+def main(src, dst, pattern=None):
     rows = list(csv.reader(open(src)))
     hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h, d = rows[hi], rows[hi + 1:]
@@ -18,9 +19,10 @@ def main(src, dst):
         per.setdefault(r[ii], {})[r[mi]] = float(r[vi].replace(",", ""))
         names[r[ii]] = r[ki].split("(")[0]
     launches = [{"id": k, "kernel": names[k], "dram_read": v["dram__bytes_read.sum"],
-                 "dram_write": v["dram__bytes_write.sum"], "ns": v["gpu__time_duration.sum"]} for k, v in per.items()]
+                 "dram_write": v["dram__bytes_write.sum"], "ns": v["gpu__time_duration.sum"]} for k, v in per.items()
+                if pattern is None or re.search(pattern, names[k])]
     tot = sum(x["dram_read"] + x["dram_write"] for x in launches)
-    out = {"source": src, "launches": len(launches), "traffic_bytes_per_launch": tot / max(1, len(launches)),
+    out = {"source": src, "kernel_filter": pattern, "launches": len(launches), "traffic_bytes_per_launch": tot / max(1, len(launches)),
            "traffic_bytes_total": tot, "per_launch": launches,
            "note": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum (cache-control all: cold L2 per launch)"}
     json.dump(out, open(dst, "w"), indent=1)
@@ -28,4 +30,4 @@ def main(src, dst):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(sys.argv[1], sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else None)
