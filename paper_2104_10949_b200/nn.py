@@ -52,6 +52,10 @@ FUSE_RELU = os.environ.get("MPC3_FUSE_RELU", "1") == "1"
 # (two more keystream slots, smaller chunks) does not (AlexNet step: fused
 # everywhere 2.559 ms, from 100 K elements 2.530 ms, never 2.541 ms)
 FUSE_RELU_MIN = int(os.environ.get("MPC3_FUSE_RELU_MIN", "100000"))  # output elements
+# train_trio replays a CUDA graph once this many iterations remain (the
+# capture's host cost pays off after ~80 AlexNet steps: eager 4.4 ms vs
+# replay 2.5 ms per step, capture ~170 ms)
+GRAPH_MIN_STEPS = 96
 
 
 def _pair(v) -> tuple:
@@ -852,8 +856,9 @@ def train_trio(sess: TrioSession, model: ModelGraph, cfg: TrainConfig, images: n
     The owner's batches go to the device as float64 and are fx-encoded and
     dealt there (mpc3_fx_encode; the PCG64 dealer reproduces numpy's draws,
     sharing.py:113-118), and from the second iteration on the step replays a
-    CUDA graph when at least two iterations remain (GraphStep: the same
-    counters, shares and CommStats as the eager step)."""
+    CUDA graph when at least GRAPH_MIN_STEPS iterations remain (GraphStep:
+    the same counters, shares and CommStats as the eager step; a capture
+    costs ~170 ms of host time against ~2 ms saved per replayed step)."""
     st = TrainState(sess, model, cfg, owner)
     n = len(images)
     if n < 1:
@@ -874,7 +879,7 @@ def train_trio(sess: TrioSession, model: ModelGraph, cfg: TrainConfig, images: n
         yb = torch.from_numpy(one_hot(labels[idx], d)).to(dev, non_blocking=True)
         xs = sess.share_device(sess.fx_encode_device(xb, bad), st.rng, owner=owner)
         ys = sess.share_device(sess.fx_encode_device(yb, bad), st.rng, owner=owner)
-        if graph and step_graph is None and it >= 1 and cfg.iterations - it >= 2:
+        if graph and step_graph is None and it >= 1 and cfg.iterations - it >= GRAPH_MIN_STEPS:
             xs_static, ys_static = RssTensor(xs.data.clone()), RssTensor(ys.data.clone())
             step_graph = st.capture(xs_static, ys_static)
         if step_graph is not None:

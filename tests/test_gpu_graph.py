@@ -87,3 +87,26 @@ def test_inference_graph_with_packed_weights_matches_eager():
     b3 = net3.forward(model, p3, x3, record=False)[0].data.clone()
     torch.cuda.synchronize()
     assert torch.equal(a, a3) and torch.equal(b, b3)
+
+
+def test_train_trio_graph_replays_equal_eager_run(monkeypatch):
+    """train_trio (the drop-in train_private's body) switching to CUDA-graph
+    replays mid-run gives the eager run's weights, losses and CommStats."""
+    import paper_2104_10949_b200 as M
+    from paper_2104_10949_b200 import nn
+    from paper_2104_10949_b200.engine import TrioSession
+
+    rng = np.random.default_rng(3)
+    imgs, labels = rng.uniform(0, 1, (24, 1, 28, 28)), rng.integers(0, 10, 24)
+    cfg = M.TrainConfig(0.05, 8, 5, seed=2)
+    runs = []
+    for min_steps in (2, 10 ** 9):
+        monkeypatch.setattr(nn, "GRAPH_MIN_STEPS", min_steps)
+        s = TrioSession(4)
+        res = nn.train_trio(s, M.lenet(), cfg, imgs, labels)
+        runs.append((res, [t.stats.as_dict() for t in s.ledger.parties], dict(s.seq)))
+    (a, sa, qa), (b, sb, qb) = runs
+    for wa, wb in zip(a.weights, b.weights):
+        assert np.array_equal(wa, wb)
+    assert a.ce_history == b.ce_history
+    assert sa == sb and qa == qb
