@@ -451,11 +451,18 @@ def _instrumented(fn, rec, torch):
 def run_b200(args, ws, rank, local):
     import torch
 
+    # one GPU per rank; more ranks than devices (a functional multi-rank run
+    # on a one-GPU box, MPC3_DIST_BACKEND=gloo) share them round-robin
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if ws > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("MPC3_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     import paper_2104_10949_b200 as M
     from paper_2104_10949_b200 import _capi, engine
     from paper_2104_10949_b200.nn import TrainState, one_hot
@@ -472,7 +479,8 @@ def run_b200(args, ws, rank, local):
 
         sess.dp = DataParallel.nccl()
         comm = {"backend": torch.distributed.get_backend(), "world_size": torch.distributed.get_world_size(),
-                "rank": rank, "collective": "all_reduce(sum, int64) of weight-gradient cross terms"}
+                "devices": torch.cuda.device_count(),
+                "collective": "all_reduce(sum, int64) of weight-gradient cross terms"}
     model = M.alexnet_cifar()
     cfg = M.TrainConfig(0.01, b * ws, args.warmup + args.steps, seed=0)  # global batch b * ws
     st = TrainState(sess, model, cfg)
@@ -490,22 +498,25 @@ def run_b200(args, ws, rank, local):
     parity = {"status": "not checked"}
 
     def check_parity():
-        if ws != 1 or b != BATCH:
-            parity["status"] = "not checked (no fixture for this global batch)"
+        # N = 1: the reference's train_private on this batch; N > 1: on the
+        # concatenation of the ranks' batches (global batch 128 N)
+        if b != BATCH:
+            parity["status"] = "not checked (no fixture for this batch)"
             return
         import hashlib
 
+        fixture, key = ("cfg_alexnet_b128.npz", "digest_1") if ws == 1 else ("cfg_alexnet_dp.npz", f"digest_dp{ws}")
         try:
-            z = np.load(os.path.join(ROOT, "tests", "golden", "cfg_alexnet_b128.npz"))
-            want = json.loads(bytes(z["meta"]).decode())["digest_1"]
+            z = np.load(os.path.join(ROOT, "tests", "golden", fixture))
+            want = json.loads(bytes(z["meta"]).decode())[key]
         except (OSError, KeyError, ValueError):
-            parity["status"] = "not checked (fixture missing)"
+            parity["status"] = f"not checked (no fixture for global batch {b * ws})"
             return
         got = hashlib.sha256(b"".join(np.ascontiguousarray(sess.reveal(p), "<u8").tobytes()
                                       for p in st.params)).hexdigest()
         parity.update({"status": "ok" if got == want else "MISMATCH", "digest": got[:16],
-                       "against": "SHA-256 of the opened weights after step 1 vs the reference's train_private "
-                                  "(tests/golden/cfg_alexnet_b128.npz, make_golden_configs.py)"})
+                       "against": f"SHA-256 of the opened weights after step 1 vs the reference's train_private at "
+                                  f"global batch {b * ws} (tests/golden/{fixture}, make_golden_configs.py)"})
 
     # a CUDA-graph replay needs the previous replay's counters: eager warm-up
     # steps first (the first one checked), then one graph capture

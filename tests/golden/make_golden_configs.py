@@ -23,6 +23,8 @@ Each configuration writes tests/golden/cfg_<name>.npz (arrays + a JSON
   bias / padded pool): `conv2d_shares` (protocols.py:120) then
   a local add of the shared bias, `relu` (:340), zero-padded
   `avgpool_shares` (:139), `matmul_shares` (:97), residual = local add.
+* alexnet_dp    — the same step at global batch 128 x N (N = 2, 4, 8): the
+  data-parallel bench's pinned digest.
 * maxpool       — max-pooling composed from the reference: per-party window
   gather (a local structural op) then `max_tree` (protocols.py:356-380) over
   the flattened (kh, kw) window; padded windows hold the public constant
@@ -95,6 +97,30 @@ def gen_alexnet_b128():
         meta[f"ce_{iters}"] = res[0].ce_history
         meta[f"seconds_{iters}"] = time.time() - t0
     save("alexnet_b128", {}, meta)
+
+
+def gen_alexnet_dp():
+    """The data-parallel bench (N ranks x batch 128, rank r's shard =
+    default_rng(100 + r)) is the reference's train_private on the
+    concatenated global batch: digest of the weights after one iteration for
+    N = 2, 4, 8 (opened outputs do not depend on how the owner's shares were
+    drawn, only on the PRF streams, nn.py:295-301)."""
+    meta = {"per_rank_batch": 128, "session_seed": 0, "cfg_seed": 0, "lr": 0.01}
+    for ranks in (2, 4, 8):
+        parts = [np.random.default_rng(100 + r) for r in range(ranks)]
+        data = [(g.uniform(0, 1, (128, 3, 32, 32)), g.integers(0, 10, 128)) for g in parts]
+        imgs = np.concatenate([d[0] for d in data])
+        labels = np.concatenate([d[1] for d in data])
+        cfg = nn.TrainConfig(0.01, 128 * ranks, 1, 0)
+        t0 = time.time()
+        res = run_in_process(lambda ctx: nn.train_private(ctx, models.alexnet_cifar(), cfg,
+                                                          (imgs, labels) if ctx.party == 0 else None),
+                             seed=0, timeout=60000)
+        meta[f"digest_dp{ranks}"] = digest(res[0].weights)
+        meta[f"ce_dp{ranks}"] = res[0].ce_history
+        meta[f"seconds_dp{ranks}"] = time.time() - t0
+        print(ranks, meta[f"digest_dp{ranks}"], flush=True)
+    save("alexnet_dp", {}, meta)
 
 
 def _infer_golden(name, model, batch, seed):
@@ -223,7 +249,7 @@ def gen_maxpool():
     save("maxpool", arrays, meta)
 
 
-GEN = {"alexnet_b128": gen_alexnet_b128, "lenet_b64": gen_lenet_b64, "vgg16ti_b32": gen_vgg16ti_b32,
+GEN = {"alexnet_b128": gen_alexnet_b128, "alexnet_dp": gen_alexnet_dp, "lenet_b64": gen_lenet_b64, "vgg16ti_b32": gen_vgg16ti_b32,
        "vgg16ti_train": gen_vgg16ti_train, "resnet50_b1": gen_resnet50_b1, "maxpool": gen_maxpool}
 
 if __name__ == "__main__":
