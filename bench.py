@@ -58,6 +58,7 @@ def _args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-side", action="store_true", help="skip the LeNet / VGG / ResNet-50 side measurements")
+    ap.add_argument("--no-graph", action="store_true", help="time eager steps (no CUDA-graph capture)")
     return ap.parse_args()
 
 
@@ -530,17 +531,22 @@ def run_b200(args, ws, rank, local):
     xs_static = engine.RssTensor(batches[0][0].data.clone())
     ys_static = engine.RssTensor(batches[0][1].data.clone())
     rec.count = 0
-    try:
-        graph = st.capture(xs_static, ys_static)
-    except Exception as e:  # noqa: BLE001 - e.g. a collective that refuses capture: time eagerly
-        print(f"[bench] CUDA-graph capture failed ({e!r}); timing eager steps", file=sys.stderr)
-        torch.cuda.synchronize()
 
-        class _Eager:
-            def replay(self_inner):
-                return st.step(xs_static, ys_static)
+    class _Eager:
+        def replay(self_inner):
+            return st.step(xs_static, ys_static)
 
+    # gloo collectives synchronise with the host and cannot be captured
+    if args.no_graph or (ws > 1 and torch.distributed.get_backend() != "nccl"):
         graph = _Eager()
+        st.step(xs_static, ys_static)  # counts this step's launches (rec.count)
+    else:
+        try:
+            graph = st.capture(xs_static, ys_static)
+        except Exception as e:  # noqa: BLE001 - e.g. a collective that refuses capture: time eagerly
+            print(f"[bench] CUDA-graph capture failed ({e!r}); timing eager steps", file=sys.stderr)
+            torch.cuda.synchronize()
+            graph = _Eager()
     launches_per_step = rec.count
     graph.replay()  # last warm-up step, through the graph
     torch.cuda.synchronize()
@@ -597,7 +603,8 @@ def run_b200(args, ws, rank, local):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64 ring (int)", "data": "synthetic",
-            "config": _config(args, ws), "parity": parity, "clocks": clk, "gpu_launches": launches,
+            "config": dict(_config(args, ws), step="eager" if isinstance(graph, _Eager) else "cuda graph replay"),
+            "parity": parity, "clocks": clk, "gpu_launches": launches,
             "e2e": e2e, "cpu_baseline": cpu, "comm": comm, "roofline": roofline,
             "step_ms": [round(v, 3) for v in step_ms],
             "also": also,

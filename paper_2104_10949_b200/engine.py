@@ -892,7 +892,7 @@ class TrioSession:
             raise ShapeError(f"matmul shapes {x.shape} x {y.shape}")
         m, k = x.shape
         n = y.shape[1]
-        check_accumulation(k * (self.dp.world if (wgrad and self.dp) else 1))
+        check_accumulation(k)  # this rank's accumulation (see conv2d_wgrad)
         bits = self.fp.t if bits is None else bits
         if not 1 <= bits <= 61:
             raise RangeError(f"truncation by {bits} bits outside [1, 61]")
@@ -912,7 +912,7 @@ class TrioSession:
     def fc_wgrad_packed(self, g: RssTensor, xp: Packed, bits: int) -> RssTensor:
         """Fully-connected weight gradient g^T x (nn.py:525-527) from x's
         forward pack (rows: batch, K: in)."""
-        check_accumulation(g.shape[0] * (self.dp.world if self.dp else 1))
+        check_accumulation(g.shape[0])  # this rank's accumulation (see conv2d_wgrad)
         m, n = g.shape[1], xp.k
         z = self.wgrad_packed(g, xp)
         out = empty((m, n), self.fp)
@@ -990,7 +990,13 @@ class TrioSession:
         sh, sw = stride
         ph, pw = padding
         ghd, gwd = (oh - 1) * sh + 1, (ow - 1) * sw + 1
-        check_accumulation(nb * (self.dp.world if self.dp else 1) * ghd * gwd)
+        # the reference's 2^20 bound (ring.py:191-195) guards ITS float-limb
+        # products; here it applies to this rank's batch shard, whose cross
+        # terms the int8-limb GEMM computes exactly (split-K, any length);
+        # the ranks' sums meet in an exact mod-2^64 all-reduce, so data
+        # parallelism may exceed the bound the single-process reference
+        # would raise for (AlexNet conv1 past a global batch of ~766)
+        check_accumulation(nb * ghd * gwd)
         if h + 2 * ph < ghd or w + 2 * pw < gwd:
             raise ShapeError("kernel larger than padded input")
         fh, fw = h + 2 * ph - ghd + 1, w + 2 * pw - gwd + 1
