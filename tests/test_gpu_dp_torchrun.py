@@ -29,3 +29,15 @@ def test_two_rank_data_parallel_bench_matches_reference_digest():
     line = json.loads(p.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == 2 and line["comm"]["world_size"] == 2
     assert line["parity"]["status"] == "ok", line["parity"]
+
+
+def test_two_rank_tensor_parallel_resnet50_b1_matches_reference_shares():
+    """nn.TPNet output-channel slabs over 2 processes (all-gather per layer):
+    the gathered ResNet-50 b1 logits equal the reference composition's shares."""
+    env = dict(os.environ, MPC3_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", "29534", os.path.join(ROOT, "tools", "tp_check.py")]
+    p = subprocess.run(cmd, env=env, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stderr[-2000:]
+    rec = json.loads(p.stdout.strip().splitlines()[-1])
+    assert rec["parity"].startswith("ok"), rec
