@@ -871,7 +871,7 @@ def resnet50_inference(dev, batch: int, steps: int, rec=None, peaks=None, sm_mhz
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     g = InferenceGraph(sess, model, params, x)
     first = g.replay().data.cpu().numpy().view(np.uint64)
-    parity = _fixture_check("resnet50_b1", first) if batch == 1 else "not checked (fixture at batch 1)"
+    parity = _fixture_check(f"resnet50_b{batch}", first) if batch in (1, 64) else "not checked (no fixture)"
     torch.cuda.synchronize()
     ms = []
     for _ in range(steps):

@@ -27,6 +27,8 @@ Each configuration writes tests/golden/cfg_<name>.npz (arrays + a JSON
   data-parallel bench's pinned digest (N = 8 is beyond the reference: its
   conv1 weight gradient would accumulate 1,401,856 > 2^20 terms and raise
   ExactnessError, ring.py:191-195).
+* resnet50_b64  — the same composition at batch 64 (the ResNet headline's
+  batch; ~1 h of CPU here).
 * maxpool       — max-pooling composed from the reference: per-party window
   gather (a local structural op) then `max_tree` (protocols.py:356-380) over
   the flattened (kh, kw) window; padded windows hold the public constant
@@ -196,13 +198,13 @@ def _composed_forward(ctx, layers, it, h):
     return h
 
 
-def gen_resnet50_b1():
+def gen_resnet50_b1(batch: int = 1, name: str = "resnet50_b1"):
     from paper_2104_10949_b200 import models as BM
     from paper_2104_10949_b200 import nn as B
 
     model = BM.resnet50()
     w = B.init_params(model, seed=11)
-    shape = (1, 3, 224, 224)
+    shape = (batch, 3, 224, 224)
 
     def job(ctx):
         rin = np.random.default_rng(11)
@@ -214,9 +216,14 @@ def gen_resnet50_b1():
 
     t0 = time.time()
     c = comps(run_in_process(job, seed=11, timeout=60000))
-    save("resnet50_b1", {"logits": c}, {"batch": 1, "seed": 11, "seconds": time.time() - t0, "digest": digest([c]),
+    save(name, {"logits": c}, {"batch": batch, "seed": 11, "seconds": time.time() - t0, "digest": digest([c]),
                                         "composed": "conv2d_shares+bias, relu, padded avgpool_shares, "
                                                     "matmul_shares+bias, residual add (reference primitives)"})
+
+
+def gen_resnet50_b64():
+    """The ResNet-50 headline batch (bench.py resnet50_inference(64)): ~1 h of CPU."""
+    gen_resnet50_b1(64, "resnet50_b64")
 
 
 def maxpool_windows(v, window, stride, padding, pad_value):
@@ -252,7 +259,8 @@ def gen_maxpool():
 
 
 GEN = {"alexnet_b128": gen_alexnet_b128, "alexnet_dp": gen_alexnet_dp, "lenet_b64": gen_lenet_b64, "vgg16ti_b32": gen_vgg16ti_b32,
-       "vgg16ti_train": gen_vgg16ti_train, "resnet50_b1": gen_resnet50_b1, "maxpool": gen_maxpool}
+       "vgg16ti_train": gen_vgg16ti_train, "resnet50_b1": gen_resnet50_b1, "resnet50_b64": gen_resnet50_b64,
+       "maxpool": gen_maxpool}
 
 if __name__ == "__main__":
     for n in sys.argv[1:] or list(GEN):

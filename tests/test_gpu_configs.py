@@ -100,6 +100,7 @@ def _deal_inference(model, batch, seed):
     ("lenet_b64", M.lenet, 64, 3),
     ("vgg16ti_b32", M.vgg16, 32, 5),
     ("resnet50_b1", M.resnet50, 1, 11),
+    ("resnet50_b64", M.resnet50, 64, 11),
 ])
 def test_inference_configs_match_reference_shares(name, builder, batch, seed, graph):
     arrays, _ = need(name)
@@ -135,6 +136,22 @@ def test_vgg16ti_b32_training_step_matches_reference_digest():
     imgs, labels = vgg16ti_train_data()
     res = nn.train_trio(TrioSession(5), M.vgg16(), M.TrainConfig(0.01, 32, 1, seed=5), imgs, labels)
     assert digest(res.weights) == meta["digest"]
+
+
+def test_vgg16ti_b32_graph_step_matches_reference_digest():
+    """The CUDA-graph training step bench.py times for VGG-16-TI, captured on
+    fresh state and replayed once: the reference's weights."""
+    _, meta = need("vgg16ti_train")
+    imgs, labels = vgg16ti_train_data()
+    s = TrioSession(5)
+    st = nn.TrainState(s, M.vgg16(), M.TrainConfig(0.01, 32, 1, seed=5))
+    xs, ys = st.deal_batch(M.fx_encode(imgs), M.fx_encode(nn.one_hot(labels, 200)))
+    g = st.capture(E.RssTensor(xs.data.clone()), E.RssTensor(ys.data.clone()))
+    g.xs.data.copy_(xs.data)
+    g.ys.data.copy_(ys.data)
+    g.replay()
+    torch.cuda.synchronize()
+    assert digest([s.reveal(p) for p in st.params]) == meta["digest"]
 
 
 # ---------------------------------------------------------------------------
