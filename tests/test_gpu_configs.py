@@ -75,6 +75,21 @@ def test_alexnet_b128_graph_replays_match_reference_digest():
         assert digest([s.reveal(p) for p in st.params]) == meta[f"digest_{it}"], f"replay {it}"
 
 
+def test_alexnet_b128_eager_then_graph_matches_reference_digest():
+    """bench.py's sequence: an eager step, then a CUDA graph captured after
+    it and replayed on the next batch."""
+    _, meta = need("alexnet_b128")
+    s, st, batches = _alexnet_state()
+    st.step(*batches[0])
+    assert digest([s.reveal(p) for p in st.params]) == meta["digest_1"]
+    xs = E.RssTensor(batches[1][0].data.clone())
+    ys = E.RssTensor(batches[1][1].data.clone())
+    g = st.capture(xs, ys)
+    g.replay()
+    torch.cuda.synchronize()
+    assert digest([s.reveal(p) for p in st.params]) == meta["digest_2"]
+
+
 def test_alexnet_b128_train_trio_matches_reference():
     _, meta = need("alexnet_b128")
     imgs, labels = alexnet_b128_data()
