@@ -800,7 +800,6 @@ int mpc3_ring_gemm_auto_z(const uint8_t* A, const uint8_t* B, uint64_t* C, int g
   if (kp % 16) return MPC3_ERR_SHAPE;
   if (c_layout != 0 && c_layout != 1) return MPC3_ERR_CONFIG;
   if (M == 0 || N == 0) return MPC3_OK;
-  const int64_t sms = 148;
   const int64_t ldc = c_layout ? M : N, c_group = M * N;
   const AutoPlan p = auto_plan(groups, M, N, kp);
   const int64_t nkb = (kp + BK - 1) / BK;
@@ -873,8 +872,6 @@ int mpc3_ring_gemm_t_z(const uint8_t* A, int a_mn, int64_t a_rows, int64_t a_kp,
   st = b_mn ? make_map_mn(&tb, B, b_kp, b_rows, (int64_t)groups * 8, BN, CU_TENSOR_MAP_SWIZZLE_64B)
             : make_map(&tb, B, kp, N, (int64_t)groups * 8, BN);
   if (st) return st;
-  const int64_t sms = 148;
-  const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * groups;
   const int64_t nkb = kp / BK;
   const AutoPlan p = t_plan(groups, M, N, kp);
   const int64_t splits = p.splits;
