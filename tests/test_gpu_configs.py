@@ -270,3 +270,16 @@ def test_conv1_layer_sign_b128_vs_oracle(bias):
     assert out.numel == 1_228_800
     assert np.array_equal(host(out), ro)
     assert np.array_equal(host(mask), rm)
+
+
+def test_maxpool_large_level_by_level_vs_oracle():
+    """A ResNet-stem-sized max-pool (3x3 / s2 / p1 over 4 x 16 x 56 x 56: 50 K
+    window rows, above the one-launch max_tree's row limit, so each level runs
+    through the sign kernels) against the oracle's composition."""
+    rng = np.random.default_rng(31)
+    x = R.share(R.fx_encode(rng.uniform(-4, 4, (4, 16, 56, 56))), rng)
+    ref = R.maxpool_shares(R.Session(13), x, (3, 3), (2, 2), (1, 1))
+    s = TrioSession(13)
+    out = s.maxpool(s.from_components(x), (3, 3), (2, 2), (1, 1))
+    assert out.shape == (4, 16, 28, 28)
+    assert np.array_equal(host(out), ref)
