@@ -693,6 +693,8 @@ def _e2e(args, ws, dev, sess, st, graph, xs_static, ys_static, imgs, labels, b):
     return {"value": b * args.steps * ws / dt, "unit": UNIT,
             "h2d_bytes_per_step": int(pin_img[0].numel() * 8 + pin_lab[0].numel() * 8),
             "d2h_bytes_per_step": int(out_host[0].numel() * 8),
+            "api": "the trio engine API (INTEGRATION.md §2: TrainState + GraphStep) with host-resident inputs; "
+                   "the per-party drop-in run_in_process + train_private call is also.dropin_train_private",
             "note": "per step: host images+labels into pinned memory, H2D on a copy stream (double-buffered, "
                     "overlapping the previous step), device fx-encode, device PCG64 dealer (bit-exact with "
                     "sharing.py:113-118), graph step, opened logits D2H read on the host; wall clock"}
