@@ -51,6 +51,18 @@ def prf_words(key: bytes, purpose: int, index: int, count: int) -> np.ndarray:
     return np.frombuffer(raw, dtype="<u8").astype(U64)
 
 
+def prf_words_at(key: bytes, purpose: int, index: int, word_off: int, count: int) -> np.ndarray:
+    """Words [word_off, word_off + count) of the prf_words stream without
+    generating the prefix: CTR mode started at block word_off // 2 (the
+    counter runs over the big-endian low 64 bits of the block, prf.py:40-49)."""
+    b0 = word_off // 2
+    block0 = purpose.to_bytes(2, "little") + index.to_bytes(6, "little") + b0.to_bytes(8, "big")
+    enc = Cipher(algorithms.AES(key), modes.CTR(block0)).encryptor()
+    skip = word_off - 2 * b0
+    raw = enc.update(bytes(8 * (int(count) + skip)))
+    return np.frombuffer(raw, dtype="<u8").astype(U64)[skip:]
+
+
 def session_id(seed: int) -> bytes:
     """session.py:29-32."""
     return hashlib.sha256(f"mpc3-session|{seed}".encode()).digest()[:16]

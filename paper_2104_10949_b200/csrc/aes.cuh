@@ -72,9 +72,13 @@ HD void aes128_expand(const uint8_t key[16], uint32_t rk[44]) {
   }
 }
 
-// Columns 0-1 of every counter block of stream (purpose, index).
+// Columns 0-1 of every counter block of stream (purpose, index).  pc: the
+// shared-memory address of the stream's round-1/2 constants under the three
+// session keys (HeadConst[3], see aes128_ctr), 0 when the launch did not
+// precompute them (then every block runs all ten rounds).
 struct StreamHead {
   uint32_t s0, s1;
+  uint32_t pc;
 };
 HD StreamHead stream_head(uint32_t purpose, uint64_t index) {
   uint8_t b[8];
@@ -84,6 +88,7 @@ HD StreamHead stream_head(uint32_t purpose, uint64_t index) {
   StreamHead h;
   h.s0 = ((uint32_t)b[0] << 24) | ((uint32_t)b[1] << 16) | ((uint32_t)b[2] << 8) | b[3];
   h.s1 = ((uint32_t)b[4] << 24) | ((uint32_t)b[5] << 16) | ((uint32_t)b[6] << 8) | b[7];
+  h.pc = 0;
   return h;
 }
 
@@ -207,6 +212,7 @@ __constant__ Te0Table c_te0 = make_te0();
 struct SmemTables {
   uint32_t hl;  // (shared window base & 0xff000000) | 4 * lane
   static constexpr bool kFour = false;
+  static constexpr int kTops = 1;  // counter top-byte values with cached round-2 constants
 };
 // Four-table variant (128 KiB): a second 64 KiB region holds Te2 / Te3 with
 // the same entry layout, so Te2[x] and Te3[x] are the same PRMT address plus
@@ -216,18 +222,35 @@ struct SmemTables {
 struct SmemTables4 {
   uint32_t hl;
   static constexpr bool kFour = true;
+  static constexpr int kTops = 4;
 };
 
+// Counter-mode constants of one (stream, key, counter top byte v).  The
+// counter blocks of a stream differ only in column 3 (the low word of the
+// big-endian counter, below 2^32), so after AddRoundKey columns 0-2 are fixed
+// and each column of round 1 has three fixed table terms (c[0..2], with the
+// round key) and one that depends on a counter byte; for blocks whose top
+// byte is v, round 1's column 3 is fixed too (c[3]), and so is one table term
+// of every column of round 2 (d[j], with the round key).  Rounds 1-2 then
+// take 3 + 12 lookups instead of 32 (160 -> 143 per block).  Slots are laid
+// out [head][v][key]; a head's pc points at its (v = 0, key 0) constant.
+struct __align__(16) HeadConst {
+  uint32_t c[4], d[4];
+};
+constexpr int kHeadSlots = 16;
+constexpr int kMaxTops = 4;
+
+// (The session keys travel in the kernel parameters, not here.)
 struct __align__(16) AesSmem {
   uint32_t te[256 * 64];
-  uint32_t rk[3][44];
-  uint64_t extra[16];  // per-kernel uniform data (stream heads)
+  uint64_t extra[24];                // per-kernel uniform data (stream heads)
+  HeadConst hc[kHeadSlots * 1 * 3];  // per-launch counter-mode constants (aes128_ctr), SmemTables::kTops = 1
 };
 constexpr int kAesSmemBytes = (int)sizeof(AesSmem);
 struct __align__(16) AesSmem4 {
   uint32_t te[2][256 * 64];
-  uint32_t rk[3][44];
-  uint64_t extra[16];
+  uint64_t extra[24];
+  HeadConst hc[kHeadSlots * kMaxTops * 3];
 };
 constexpr int kAesSmem4Bytes = (int)sizeof(AesSmem4);
 constexpr uint32_t kAesTableOff = 1024;
@@ -351,6 +374,117 @@ DEV void aes128_multi(const TT& tab, const uint32_t* const rks[NB], uint32_t s[N
   }
 }
 
+// Table term k of a column (Te_k indexed by byte 3 - k of x), both layouts.
+#define MPC3_TE0(x) lds_te0(MPC3_I3(x))
+#define MPC3_TE1(x) lds_te1(MPC3_I2(x))
+#define MPC3_TE2(x) (FOUR ? lds_te2(MPC3_I1(x)) : __byte_perm(lds_te0(MPC3_I1(x)), 0, 0x1032))
+#define MPC3_TE3(x) (FOUR ? lds_te3(MPC3_I0(x)) : __byte_perm(lds_te1(MPC3_I0(x)), 0, 0x1032))
+
+// Round-1/2 constants of stream columns (s0, s1) under the expanded key rk
+// (counter word 2 = 0, top byte of word 3 = v; see HeadConst).
+template <class TT>
+DEV void head_const(const TT& tab, const uint32_t* rk, uint32_t s0, uint32_t s1, uint32_t v, HeadConst& o) {
+  constexpr bool FOUR = TT::kFour;
+  const uint32_t hl = tab.hl;
+  const uint32_t x0 = s0 ^ rk[0], x1 = s1 ^ rk[1], x2 = rk[2], x3 = rk[3] ^ (v << 24);
+  o.c[0] = MPC3_TE0(x0) ^ MPC3_TE1(x1) ^ MPC3_TE2(x2) ^ rk[4];
+  o.c[1] = MPC3_TE0(x1) ^ MPC3_TE1(x2) ^ MPC3_TE3(x0) ^ rk[5];
+  o.c[2] = MPC3_TE0(x2) ^ MPC3_TE2(x0) ^ MPC3_TE3(x1) ^ rk[6];
+  const uint32_t c3 = MPC3_TE0(x3) ^ MPC3_TE1(x0) ^ MPC3_TE2(x1) ^ MPC3_TE3(x2) ^ rk[7];
+  o.c[3] = c3;
+  o.d[0] = MPC3_TE3(c3) ^ rk[8];
+  o.d[1] = MPC3_TE2(c3) ^ rk[9];
+  o.d[2] = MPC3_TE1(c3) ^ rk[10];
+  o.d[3] = MPC3_TE0(c3) ^ rk[11];
+}
+
+DEV uint4 lds_v4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+
+// NB blocks of one counter value blk, block i of stream columns (s01[i][0],
+// s01[i][1]) under key schedule rks[i] whose counter-mode constants (v = 0)
+// sit at shared address pcs[i] (0: none).  Output: the ciphertext columns.
+// Blocks whose counter top byte has constants (below kTops << 24) start at
+// round 3 (rounds 1-2 from the constants, 15 lookups), other blocks below
+// 2^32 at round 2 (round 1: 5 lookups); otherwise all rounds run.
+template <int NB, class TT>
+DEV void aes128_ctr(const TT& tab, const uint32_t* const rks[NB], const uint32_t pcs[NB], const uint32_t s01[NB][2],
+                    uint64_t blk, uint32_t s[NB][4]) {
+  constexpr bool FOUR = TT::kFour;
+  const uint32_t hl = tab.hl;
+  bool cached = (blk >> 32) == 0;
+#pragma unroll
+  for (int i = 0; i < NB; ++i) cached = cached && pcs[i] != 0;
+  int r0 = 1;
+  if (cached) {
+    const uint32_t lo = (uint32_t)blk, v = lo >> 24;
+    const bool top0 = v < (uint32_t)TT::kTops;
+    const uint32_t voff = top0 ? v * 96u : 0u;  // [v][key] stride: 3 keys x 32 bytes
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      const uint4 c = lds_v4(pcs[i] + voff);
+      const uint32_t x3 = lo ^ rks[i][3];
+      s[i][0] = c.x ^ MPC3_TE3(x3);
+      s[i][1] = c.y ^ MPC3_TE2(x3);
+      s[i][2] = c.z ^ MPC3_TE1(x3);
+      s[i][3] = top0 ? c.w : c.w ^ MPC3_TE0(rks[i][3]) ^ MPC3_TE0(x3);
+    }
+    if (top0) {
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        const uint4 d = lds_v4(pcs[i] + voff + 16);
+        const uint32_t t0 = s[i][0], t1 = s[i][1], t2 = s[i][2];
+        s[i][0] = MPC3_TE0(t0) ^ MPC3_TE1(t1) ^ MPC3_TE2(t2) ^ d.x;
+        s[i][1] = MPC3_TE0(t1) ^ MPC3_TE1(t2) ^ MPC3_TE3(t0) ^ d.y;
+        s[i][2] = MPC3_TE0(t2) ^ MPC3_TE2(t0) ^ MPC3_TE3(t1) ^ d.z;
+        s[i][3] = MPC3_TE1(t0) ^ MPC3_TE2(t1) ^ MPC3_TE3(t2) ^ d.w;
+      }
+      r0 = 3;
+    } else {
+      r0 = 2;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      s[i][0] = s01[i][0] ^ rks[i][0];
+      s[i][1] = s01[i][1] ^ rks[i][1];
+      s[i][2] = (uint32_t)(blk >> 32) ^ rks[i][2];
+      s[i][3] = (uint32_t)blk ^ rks[i][3];
+    }
+  }
+#pragma unroll 1
+  for (int r = r0; r < 10; ++r) {
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      const uint4 k = *reinterpret_cast<const uint4*>(rks[i] + 4 * r);
+      uint32_t t0 = MPC3_COL(s[i][0], s[i][1], s[i][2], s[i][3], k.x);
+      uint32_t t1 = MPC3_COL(s[i][1], s[i][2], s[i][3], s[i][0], k.y);
+      uint32_t t2 = MPC3_COL(s[i][2], s[i][3], s[i][0], s[i][1], k.z);
+      uint32_t t3 = MPC3_COL(s[i][3], s[i][0], s[i][1], s[i][2], k.w);
+      s[i][0] = t0;
+      s[i][1] = t1;
+      s[i][2] = t2;
+      s[i][3] = t3;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NB; ++i) {
+    const uint4 k = *reinterpret_cast<const uint4*>(rks[i] + 40);
+    uint32_t a = s[i][0], b = s[i][1], c = s[i][2], d = s[i][3];
+    s[i][0] = MPC3_FIN(a, b, c, d, k.x);
+    s[i][1] = MPC3_FIN(b, c, d, a, k.y);
+    s[i][2] = MPC3_FIN(c, d, a, b, k.z);
+    s[i][3] = MPC3_FIN(d, a, b, c, k.w);
+  }
+}
+#undef MPC3_TE0
+#undef MPC3_TE1
+#undef MPC3_TE2
+#undef MPC3_TE3
+
 // Three blocks with the same counter under k_0, k_1, k_2: every zero share
 // needs all three keys' words at one position (sharing.py:233-250).
 template <class TT>
@@ -371,7 +505,7 @@ DEV void aes128_block3(const TT& tab, const uint32_t* rk3, uint32_t s[3][4]) {
 // Programmatic dependent launch: the table expansion only reads the constant
 // bank and the session keys, so it runs before griddep_wait() and overlaps
 // the previous kernel's tail; every protocol kernel goes through here.
-__device__ inline SmemTables aes_smem_init(AesSmem& sm, const uint32_t* __restrict__ rk_dev, int nkeys) {
+__device__ inline SmemTables aes_smem_init(AesSmem& sm) {
   griddep_launch();
   uint4* dst = reinterpret_cast<uint4*>(sm.te);
   for (int i = threadIdx.x; i < 256 * 16; i += blockDim.x) {
@@ -379,7 +513,6 @@ __device__ inline SmemTables aes_smem_init(AesSmem& sm, const uint32_t* __restri
     if (i & 8) v = __funnelshift_r(v, v, 8);  // words 32-63 of the entry: Te1
     dst[i] = make_uint4(v, v, v, v);
   }
-  for (int i = threadIdx.x; i < nkeys * 44; i += blockDim.x) (&sm.rk[0][0])[i] = rk_dev[i];
   const uint32_t base = (uint32_t)__cvta_generic_to_shared(mpc3_dsm);
   if ((base & 0x00ffffffu) != kAesTableOff) __trap();  // the LDS immediates assume this layout
   __syncthreads();
@@ -390,7 +523,7 @@ __device__ inline SmemTables aes_smem_init(AesSmem& sm, const uint32_t* __restri
 }
 
 // Four-table expansion (Te0/Te1 in region 0, Te2/Te3 = ror16 of them in region 1).
-__device__ inline SmemTables4 aes_smem_init4(AesSmem4& sm, const uint32_t* __restrict__ rk_dev, int nkeys) {
+__device__ inline SmemTables4 aes_smem_init4(AesSmem4& sm) {
   griddep_launch();
   uint4* dst = reinterpret_cast<uint4*>(&sm.te[0][0]);
   for (int i = threadIdx.x; i < 2 * 256 * 16; i += blockDim.x) {
@@ -400,7 +533,6 @@ __device__ inline SmemTables4 aes_smem_init4(AesSmem4& sm, const uint32_t* __res
     v = __funnelshift_r(v, v, rot);
     dst[i] = make_uint4(v, v, v, v);
   }
-  for (int i = threadIdx.x; i < nkeys * 44; i += blockDim.x) (&sm.rk[0][0])[i] = rk_dev[i];
   const uint32_t base = (uint32_t)__cvta_generic_to_shared(mpc3_dsm);
   if ((base & 0x00ffffffu) != kAesTableOff) __trap();
   __syncthreads();
@@ -408,6 +540,28 @@ __device__ inline SmemTables4 aes_smem_init4(AesSmem4& sm, const uint32_t* __res
   SmemTables4 t;
   t.hl = (base & 0xff000000u) | ((threadIdx.x & 31) * 4);
   return t;
+}
+
+// Counter-mode constants of NH stream heads (aes128_ctr): every thread of the
+// CTA calls this after the tables are built; thread t < 3 kTops NH computes
+// (head, v, key) = (t / 3 kTops, t / 3 % kTops, t % 3), and after the barrier
+// each head's pc points at its (v = 0, key 0) slot.
+// `on` (uniform over the grid) = false skips it (pc stays 0): tiny launches
+// whose threads run a block or two are better off without the barrier.
+template <class TT, class... H>
+DEV void cache_heads(const TT& tab, const uint32_t* rk3, HeadConst* slots, bool on, H&... h) {
+  constexpr int KT = TT::kTops;
+  static_assert(sizeof...(H) <= kHeadSlots, "head slots");
+#if defined(MPC3_NO_HEAD_CACHE)
+  on = false;
+#endif
+  if (!on) return;
+  const int t = threadIdx.x, v = t / 3 % KT, k = t % 3;
+  int i = 0;
+  (((t / (3 * KT) == i ? head_const(tab, rk3 + 44 * k, h.s0, h.s1, (uint32_t)v, slots[t]) : void()), ++i), ...);
+  __syncthreads();
+  i = 0;
+  (((h.pc = (uint32_t)__cvta_generic_to_shared(&slots[i * KT * 3])), ++i), ...);
 }
 
 #define MPC3_AES_SMEM() AesSmem& sm = *reinterpret_cast<AesSmem*>(mpc3_dsm)

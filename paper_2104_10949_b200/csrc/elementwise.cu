@@ -46,13 +46,15 @@ template <>
 struct Proto<true> {
   using TT = SmemTables4;
   static constexpr int threads = kProto4Threads, min_ctas = 1;
-  DEV static TT init() { return aes_smem_init4(*reinterpret_cast<AesSmem4*>(mpc3_dsm), nullptr, 0); }
+  DEV static TT init() { return aes_smem_init4(*reinterpret_cast<AesSmem4*>(mpc3_dsm)); }
+  DEV static HeadConst* slots() { return reinterpret_cast<AesSmem4*>(mpc3_dsm)->hc; }
 };
 template <>
 struct Proto<false> {
   using TT = SmemTables;
   static constexpr int threads = kProto2Threads, min_ctas = 3;  // 3 x 64 KiB tables per SM
-  DEV static TT init() { return aes_smem_init(*reinterpret_cast<AesSmem*>(mpc3_dsm), nullptr, 0); }
+  DEV static TT init() { return aes_smem_init(*reinterpret_cast<AesSmem*>(mpc3_dsm)); }
+  DEV static HeadConst* slots() { return reinterpret_cast<AesSmem*>(mpc3_dsm)->hc; }
 };
 bool pdl_enabled() {
   static const bool on = [] {
@@ -147,6 +149,19 @@ HD StreamRef sref(uint32_t purpose, uint64_t j) {
   return r;
 }
 
+// Counter-mode constants in the two-phase sign kernels (sign2, max_tree,
+// softmax) and in grid-stride protocol kernels whose threads get at least
+// MPC3_HEAD_CACHE_MIN pairs.
+#ifndef MPC3_HEAD_CACHE_TWO_PHASE
+#define MPC3_HEAD_CACHE_TWO_PHASE 1
+#endif
+#ifndef MPC3_HEAD_CACHE_MIN
+#define MPC3_HEAD_CACHE_MIN 0
+#endif
+DEV bool cache_worth(uint64_t pairs) {
+  return pairs >= (uint64_t)MPC3_HEAD_CACHE_MIN * gridDim.x * blockDim.x;
+}
+
 #define GRID_LOOP(var, count) \
   for (uint64_t var = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; var < (count); \
        var += (uint64_t)gridDim.x * blockDim.x)
@@ -158,9 +173,11 @@ __global__ void __launch_bounds__(kSignThreads, 1) prf_words_kernel(const __grid
                                                                    StreamHead h, uint64_t word_off,
                                                                    uint64_t count, uint64_t* __restrict__ out) {
   MPC3_AES_SMEM4();
-  SmemTables4 tab = aes_smem_init4(sm, nullptr, 0);
+  SmemTables4 tab = aes_smem_init4(sm);
+  StreamHead hc = h;
+  cache_heads(tab, &ks.rk[0][0], sm.hc, true, hc);  // (keys 1-2 of ks are zero here: their slots go unused)
   uint64_t nblk = ((word_off + count - 1) >> 1) - (word_off >> 1) + 1;
-  GRID_LOOP(t, nblk) prf_words_item(tab, ks.rk[0], h, word_off, count, out, t);
+  GRID_LOOP(t, nblk) prf_words_item(tab, &ks.rk[0][0], hc, word_off, count, out, t);
 }
 
 template <bool F>
@@ -169,6 +186,7 @@ __global__ void __launch_bounds__(Proto<F>::threads, Proto<F>::min_ctas) zero_sh
                                                              int xor_mode, uint64_t n, uint64_t* __restrict__ out) {
   StreamHead h = resolve(rh, ctr);
   auto tab = Proto<F>::init();
+  cache_heads(tab, &ks.rk[0][0], Proto<F>::slots(), cache_worth((n + 1) >> 1), h);
   GRID_LOOP(b, (n + 1) >> 1) zero_share_item(tab, &ks.rk[0][0], h, xor_mode, n, out, b);
 }
 
@@ -229,6 +247,7 @@ __global__ void __launch_bounds__(Proto<F>::threads, Proto<F>::min_ctas) arith_k
                                                         uint64_t* __restrict__ out, uint64_t n, uint64_t pb0) {
   auto tab = Proto<F>::init();
   StreamHead ha = resolve(ra, ctr), hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
+  cache_heads(tab, &ks.rk[0][0], Proto<F>::slots(), cache_worth((n + 1) >> 1), ha, hrho, hr);
   GRID_LOOP(b, (n + 1) >> 1) arith_item(tab, &ks.rk[0][0], kind, ha, hrho, hr, bits, x, y, out, n, b, pb0);
 }
 
@@ -236,6 +255,28 @@ struct SignArgs {
   uint64_t jbin, jxor, ja;
   uint64_t jra, jrho, jr;  // fused layer + ReLU: the layer's ARITH_ZERO / TRUNC_RHO / TRUNC_R counters
 };
+
+// Counter-mode constants of a launch's SignStreams (all threads, after the
+// tables are built; heads in declaration order -> slots; two barriers).
+template <class TT>
+DEV void cache_sign_streams(const TT& tab, const uint32_t* rk3, SignStreams& st, HeadConst* slots, bool rs,
+                            bool two_phase = false) {
+  static_assert(sizeof(SignStreams) == 14 * sizeof(StreamHead), "SignStreams is an array of heads");
+#if defined(MPC3_NO_HEAD_CACHE)
+  return;
+#endif
+  if (two_phase && !MPC3_HEAD_CACHE_TWO_PHASE) return;
+  constexpr int KT = TT::kTops;
+  StreamHead* hs = reinterpret_cast<StreamHead*>(&st);
+  const int nh = rs ? 14 : 11;
+  for (int t = threadIdx.x; t < 3 * KT * nh; t += blockDim.x) {
+    const StreamHead h = hs[t / (3 * KT)];
+    head_const(tab, rk3 + 44 * (t % 3), h.s0, h.s1, (uint32_t)(t / 3 % KT), slots[t]);
+  }
+  __syncthreads();
+  if (threadIdx.x < nh) hs[threadIdx.x].pc = (uint32_t)__cvta_generic_to_shared(&slots[threadIdx.x * KT * 3]);
+  __syncthreads();
+}
 
 // the stream heads a sign launch needs, resolved by one thread into shared memory
 DEV void sign_streams(SignStreams& st, const SignArgs& args, const uint64_t* ctr, bool rs) {
@@ -265,7 +306,8 @@ __global__ void __launch_bounds__(kSignThreads, 1) sign_kernel(const __grid_cons
   static_assert(sizeof(SignStreams) <= sizeof(sm.extra), "stream heads fit the AesSmem extra area");
   SignStreams& st = *reinterpret_cast<SignStreams*>(sm.extra);  // uniform stream heads, indexed by level
   if (threadIdx.x == 0) sign_streams(st, args, ctr, RS);
-  SmemTables4 tab = aes_smem_init4(sm, nullptr, 0);  // includes the barrier
+  SmemTables4 tab = aes_smem_init4(sm);  // includes the barrier
+  cache_sign_streams(tab, &ks.rk[0][0], st, sm.hc, RS);
   if constexpr (RS) {
     GRID_LOOP(b, (n + 1) >> 1) {
       Word2 w3[3], rho, r;
@@ -299,7 +341,7 @@ template <class TT>
 DEV void sign_slot_fill(const TT& tab, const uint32_t* rk, const SignStreams& st, int s, uint64_t blk,
                         uint64_t n_total, int L, Word2* dst) {
   if (s == 0) {
-    dst[0] = prf_block(tab, rk, st.bin, blk);
+    dst[0] = prf_block_k(tab, rk, 0, st.bin, blk);
     return;
   }
   StreamHead h;
@@ -338,6 +380,7 @@ __global__ void __launch_bounds__(F ? kSignThreads : kThreads, F ? 1 : 2)
                                                       : reinterpret_cast<AesSmem*>(mpc3_dsm)->extra);
   if (threadIdx.x == 0) sign_streams(st, args, ctr, KIND == S2_RS);
   auto tab = Proto<F>::init();  // (its __syncthreads publishes st)
+  cache_sign_streams(tab, &ks.rk[0][0], st, Proto<F>::slots(), KIND == S2_RS, true);
   Word2* pre = reinterpret_cast<Word2*>(mpc3_dsm + (F ? sizeof(AesSmem4) : sizeof(AesSmem)));
   Word2* slots = pre + (size_t)PRE * P * 3;
   const bool straddle = (n_total & 1) != 0;
@@ -355,8 +398,8 @@ __global__ void __launch_bounds__(F ? kSignThreads : kThreads, F ? 1 : 2)
         if (sa == 0) {
           prf_block3(tab, &ks.rk[0][0], st.ra, blk, dst);
         } else {
-          dst[0] = prf_block(tab, &ks.rk[0][0] + 2 * 44, st.rrho, blk);  // protocols.py:166-216
-          dst[1] = prf_block(tab, &ks.rk[0][0] + 1 * 44, st.rr, blk);
+          dst[0] = prf_block_k(tab, &ks.rk[0][0], 2, st.rrho, blk);  // protocols.py:166-216
+          dst[1] = prf_block_k(tab, &ks.rk[0][0], 1, st.rr, blk);
         }
         continue;
       }
@@ -426,6 +469,7 @@ __global__ void __launch_bounds__(kThreads, 1) maxtree_kernel(const __grid_const
       sign_streams(st, a, ctr, false);
     }
     __syncthreads();
+    cache_sign_streams(tab, &ks.rk[0][0], st, reinterpret_cast<AesSmem*>(mpc3_dsm)->hc, false, true);
     const uint64_t n = rows * k, n_total = ta.rows_total * k, elem_off = ta.row_off * k;
     const bool straddle = (n_total & 1) != 0;
     const int L = straddle ? 3 : 2, used = sign_slots(straddle);
@@ -477,7 +521,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
                                                            const uint64_t* __restrict__ x, uint64_t* __restrict__ out,
                                                            uint64_t n, uint64_t pb0, int P) {
   MPC3_AES_SMEM();
-  SmemTables tab = aes_smem_init(sm, nullptr, 0);
+  SmemTables tab = aes_smem_init(sm);
   Word2* slots = reinterpret_cast<Word2*>(mpc3_dsm + sizeof(AesSmem));
   const uint64_t npairs = (n + 1) >> 1;
   const uint32_t* rk = &ks.rk[0][0];
@@ -663,6 +707,7 @@ __global__ void __launch_bounds__(kThreads, 1) softmax_loss_kernel(
       sign_streams(st, a, ctr, false);
     }
     __syncthreads();
+    cache_sign_streams(tab, &ks.rk[0][0], st, reinterpret_cast<AesSmem*>(mpc3_dsm)->hc, false, true);
     const uint64_t nl = rows * k, n_total = la.rows_total * k, elem_off = la.row_off * k;
     const bool straddle = (n_total & 1) != 0;
     const int L = straddle ? 3 : 2, used = sign_slots(straddle);
@@ -783,6 +828,7 @@ __global__ void __launch_bounds__(Proto<F>::threads, Proto<F>::min_ctas) inject_
                                                          uint64_t* __restrict__ out, uint64_t n, uint64_t pb0) {
   auto tab = Proto<F>::init();
   StreamHead a0 = resolve(r0, ctr), a1 = resolve(r1, ctr);
+  cache_heads(tab, &ks.rk[0][0], Proto<F>::slots(), cache_worth((n + 1) >> 1), a0, a1);
   GRID_LOOP(b, (n + 1) >> 1) inject_item(tab, &ks.rk[0][0], a0, a1, bits, out, n, b, pb0);
 }
 
@@ -795,6 +841,7 @@ __global__ void __launch_bounds__(Proto<F>::threads, Proto<F>::min_ctas) reshare
                                                                 uint64_t pb0) {
   auto tab = Proto<F>::init();
   StreamHead ha = resolve(ra, ctr), hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
+  cache_heads(tab, &ks.rk[0][0], Proto<F>::slots(), cache_worth((n + 1) >> 1), ha, hrho, hr);
   if (n < (1ull << 32))
     GRID_LOOP(b, (n + 1) >> 1) reshare_trunc_item<typename Proto<F>::TT, uint32_t>(tab, &ks.rk[0][0], ha, hrho, hr, bits, z, v, out,
                                                                          n, b, pb0);
@@ -811,7 +858,8 @@ __global__ void __launch_bounds__(Proto<F>::threads, Proto<F>::min_ctas) pool_ke
                                                        uint64_t pb0, const uint64_t* __restrict__ mask,
                                                        StreamRef ra) {
   auto tab = Proto<F>::init();
-  StreamHead hrho = resolve(rrho, ctr), hr = resolve(rr, ctr), ha = mask ? resolve(ra, ctr) : StreamHead{0, 0};
+  StreamHead hrho = resolve(rrho, ctr), hr = resolve(rr, ctr), ha = mask ? resolve(ra, ctr) : StreamHead{0, 0, 0};
+  cache_heads(tab, &ks.rk[0][0], Proto<F>::slots(), cache_worth((n + 1) >> 1), hrho, hr, ha);
   if (2 * n < (1ull << 32) && (uint64_t)p.N * p.C * p.H * p.W < (1ull << 32))
     GRID_LOOP(b, (n + 1) >> 1) pool_item<typename Proto<F>::TT, uint32_t>(tab, &ks.rk[0][0], backward != 0, hrho, hr, bits, mulc, x,
                                                                 out, p, b, pb0, mask, ha);
@@ -828,6 +876,7 @@ __global__ void __launch_bounds__(Proto<F>::threads, Proto<F>::min_ctas) col2im_
                                                          uint64_t* __restrict__ out, uint64_t n, uint64_t pb0) {
   auto tab = Proto<F>::init();
   StreamHead ha = resolve(ra, ctr), hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
+  cache_heads(tab, &ks.rk[0][0], Proto<F>::slots(), cache_worth((n + 1) >> 1), ha, hrho, hr);
   if (2 * n < (1ull << 32))
     GRID_LOOP(b, (n + 1) >> 1) col2im_item<typename Proto<F>::TT, uint32_t>(tab, &ks.rk[0][0], ha, hrho, hr, bits, z, g, out, b,
                                                                   pb0);
@@ -1059,8 +1108,12 @@ int mpc3_rss_chain(const uint32_t* rk3, const uint64_t* ctr, const MPC3ChainStep
 constexpr bool kSign2Four = MPC3_SIGN2_FOUR;
 static int sign2_pmax(bool straddle, bool rs) {
   if (rs) return straddle ? 32 : 48;  // two more slots per pair (the layer's reshare / truncation words)
-  return (straddle ? 32 : 64) * (kSign2Four ? 2 : 1);
+  // 60, not 64: two two-table CTAs (AES tables + counter-mode constants + 16
+  // slots x 48 B per pair) must fit one SM's 228 KiB
+  return (straddle ? 32 : 60) * (kSign2Four ? 2 : 1);
 }
+static_assert(kSign2Four || 2 * (kAesSmemBytes + 60 * 16 * 3 * (int)sizeof(Word2) + 1024) <= 228 * 1024,
+              "two sign2 CTAs per SM");
 static int sign2_chunk(uint64_t pairs, bool straddle, bool rs = false) {
   const uint64_t pmax = sign2_pmax(straddle, rs), slots = (kSign2Four ? 1 : 2) * 148;
   const uint64_t waves = (pairs + slots * pmax - 1) / (slots * pmax);

@@ -26,7 +26,7 @@ template <class T>
 HD void prf_words_item(const T& tab, const uint32_t* rk, StreamHead h, uint64_t word_off, uint64_t count,
                        uint64_t* out, uint64_t t) {
   uint64_t blk = (word_off >> 1) + t;
-  Word2 w = prf_block(tab, rk, h, blk);
+  Word2 w = prf_block_k(tab, rk, 0, h, blk);
   uint64_t w0 = 2 * blk;
   if (w0 >= word_off && w0 < word_off + count) out[w0 - word_off] = w.w0;
   if (w0 + 1 >= word_off && w0 + 1 < word_off + count) out[w0 + 1 - word_off] = w.w1;

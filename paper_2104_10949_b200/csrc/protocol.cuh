@@ -110,14 +110,10 @@ template <class TT>
 HD void prf_block3_dev(const TT& tab, const uint32_t* rk3, StreamHead h, uint64_t blk, Word2 w[3]) {
 #if defined(__CUDA_ARCH__)
   uint32_t s[3][4];
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    s[i][0] = h.s0;
-    s[i][1] = h.s1;
-    s[i][2] = (uint32_t)(blk >> 32);
-    s[i][3] = (uint32_t)blk;
-  }
-  aes128_block3(tab, rk3, s);
+  const uint32_t* rks[3] = {rk3, rk3 + 44, rk3 + 88};
+  const uint32_t pcs[3] = {h.pc, h.pc ? h.pc + 32 : 0u, h.pc ? h.pc + 64 : 0u};
+  const uint32_t s01[3][2] = {{h.s0, h.s1}, {h.s0, h.s1}, {h.s0, h.s1}};
+  aes128_ctr<3>(tab, rks, pcs, s01, blk, s);
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     w[i].w0 = (uint64_t)bswap32(s[i][0]) | ((uint64_t)bswap32(s[i][1]) << 32);
@@ -133,6 +129,34 @@ HD void prf_block3(const SmemTables4& tab, const uint32_t* rk3, StreamHead h, ui
 }
 #endif
 
+// Block blk of one stream under session key k (k_0, k_1, k_2).
+template <class T>
+HD Word2 prf_block_k(const T& tab, const uint32_t* rk3, int k, StreamHead h, uint64_t blk) {
+  return prf_block(tab, rk3 + 44 * k, h, blk);
+}
+#if defined(__CUDACC__)
+template <class TT>
+HD Word2 prf_block_k_dev(const TT& tab, const uint32_t* rk3, int k, StreamHead h, uint64_t blk) {
+  Word2 w;
+#if defined(__CUDA_ARCH__)
+  uint32_t s[1][4];
+  const uint32_t* rks[1] = {rk3 + 44 * k};
+  const uint32_t pcs[1] = {h.pc ? h.pc + 32 * k : 0u};
+  const uint32_t s01[1][2] = {{h.s0, h.s1}};
+  aes128_ctr<1>(tab, rks, pcs, s01, blk, s);
+  w.w0 = (uint64_t)bswap32(s[0][0]) | ((uint64_t)bswap32(s[0][1]) << 32);
+  w.w1 = (uint64_t)bswap32(s[0][2]) | ((uint64_t)bswap32(s[0][3]) << 32);
+#endif
+  return w;
+}
+HD Word2 prf_block_k(const SmemTables& tab, const uint32_t* rk3, int k, StreamHead h, uint64_t blk) {
+  return prf_block_k_dev(tab, rk3, k, h, blk);
+}
+HD Word2 prf_block_k(const SmemTables4& tab, const uint32_t* rk3, int k, StreamHead h, uint64_t blk) {
+  return prf_block_k_dev(tab, rk3, k, h, blk);
+}
+#endif
+
 #if defined(__CUDACC__)
 // Keystream replay: a circuit templated on the table type runs unchanged on
 // words an earlier phase computed into shared memory, one slot per AES call
@@ -143,6 +167,9 @@ struct Replay {
   mutable int slot;
 };
 DEV Word2 prf_block(const Replay& t, const uint32_t*, StreamHead, uint64_t) {
+  return t.w[((size_t)t.slot++ * t.P + t.p) * 3];
+}
+DEV Word2 prf_block_k(const Replay& t, const uint32_t*, int, StreamHead, uint64_t) {
   return t.w[((size_t)t.slot++ * t.P + t.p) * 3];
 }
 DEV void prf_block3(const Replay& t, const uint32_t*, StreamHead, uint64_t, Word2 w[3]) {
@@ -167,10 +194,11 @@ template <class TT>
 HD void trunc_words_dev(const TT& tab, const uint32_t* rk3, StreamHead hrho, StreamHead hr, uint64_t blk,
                         Word2& rho, Word2& r) {
 #if defined(__CUDA_ARCH__)
-  uint32_t s[2][4] = {{hrho.s0, hrho.s1, (uint32_t)(blk >> 32), (uint32_t)blk},
-                      {hr.s0, hr.s1, (uint32_t)(blk >> 32), (uint32_t)blk}};
+  uint32_t s[2][4];
+  const uint32_t s01[2][2] = {{hrho.s0, hrho.s1}, {hr.s0, hr.s1}};
   const uint32_t* rks[2] = {rk3 + 2 * 44, rk3 + 1 * 44};
-  aes128_multi<2>(tab, rks, s);
+  const uint32_t pcs[2] = {hrho.pc ? hrho.pc + 64 : 0u, hr.pc ? hr.pc + 32 : 0u};
+  aes128_ctr<2>(tab, rks, pcs, s01, blk, s);
   rho.w0 = (uint64_t)bswap32(s[0][0]) | ((uint64_t)bswap32(s[0][1]) << 32);
   rho.w1 = (uint64_t)bswap32(s[0][2]) | ((uint64_t)bswap32(s[0][3]) << 32);
   r.w0 = (uint64_t)bswap32(s[1][0]) | ((uint64_t)bswap32(s[1][1]) << 32);
@@ -201,14 +229,12 @@ template <class TT>
 HD void reshare_trunc_words_dev(const TT& tab, const uint32_t* rk3, StreamHead ha, StreamHead hrho, StreamHead hr,
                                 uint64_t blk, Word2 w[3], Word2& rho, Word2& r) {
 #if defined(__CUDA_ARCH__)
-  const uint32_t hi = (uint32_t)(blk >> 32), lo = (uint32_t)blk;
-  uint32_t s[5][4] = {{ha.s0, ha.s1, hi, lo},
-                      {ha.s0, ha.s1, hi, lo},
-                      {ha.s0, ha.s1, hi, lo},
-                      {hrho.s0, hrho.s1, hi, lo},
-                      {hr.s0, hr.s1, hi, lo}};
+  uint32_t s[5][4];
+  const uint32_t s01[5][2] = {{ha.s0, ha.s1}, {ha.s0, ha.s1}, {ha.s0, ha.s1}, {hrho.s0, hrho.s1}, {hr.s0, hr.s1}};
   const uint32_t* rks[5] = {rk3, rk3 + 44, rk3 + 2 * 44, rk3 + 2 * 44, rk3 + 1 * 44};
-  aes128_multi<5>(tab, rks, s);
+  const uint32_t pcs[5] = {ha.pc, ha.pc ? ha.pc + 32 : 0u, ha.pc ? ha.pc + 64 : 0u, hrho.pc ? hrho.pc + 64 : 0u,
+                           hr.pc ? hr.pc + 32 : 0u};
+  aes128_ctr<5>(tab, rks, pcs, s01, blk, s);
   Word2 o[5];
 #pragma unroll
   for (int i = 0; i < 5; ++i) {
@@ -358,7 +384,7 @@ template <class T, class Ld>
 HD void sign_circuit_pair(const T& tab, const uint32_t* rk3, const SignStreams& st, uint64_t n_total,
                           uint64_t blk, int mode, const Ld& ld, Trio out[2], Trio mask[2]) {
   // a2b input sharing (protocols.py:278-295): w = ((c0+c1)^r, r, 0), x2 = (0,0,c2)
-  const Word2 rb = prf_block(tab, rk3 + 0 * 44, st.bin, blk);
+  const Word2 rb = prf_block_k(tab, rk3, 0, st.bin, blk);
   Trio p[2], g[2];
   const uint64_t pw = n_total + 2 * blk;  // stream word of element 0's p-half
 #if defined(__CUDA_ARCH__)

@@ -72,6 +72,22 @@ def test_prf_words(purpose, index, off, count):
     assert np.array_equal(host(out), ref)
 
 
+# counter-mode constants (aes.cuh aes128_ctr): blocks below 4 x 2^24 start
+# at round 3 (per-top-byte constants), other blocks below 2^32 at round 2,
+# the rest run all rounds; these offsets straddle every boundary (words
+# 2^25, 2^27 and 2^33)
+@pytest.mark.parametrize("purpose,index,off,count", [(1, 3, (1 << 25) - 37, 80), (4, 1, (1 << 27) - 37, 80),
+                                                     (2, 9, (1 << 33) - 37, 80),
+                                                     (5, 77, (1 << 40) + 1, 33), (3, 0, (1 << 24) + 5, 4099)])
+def test_prf_words_far_offsets(purpose, index, off, count):
+    keys = R.party_keys(4)
+    rk = rk3(keys)
+    out = torch.zeros(count, dtype=torch.int64, device="cuda")
+    _capi.call("mpc3_prf_words", C.c_void_p(rk.data_ptr() + 44 * 8), purpose, index, off, count, p(out), stream())
+    ref = R.prf_words_at(keys[2], purpose, index, off, count)
+    assert np.array_equal(host(out), ref)
+
+
 def test_prf_range_errors():
     rk = rk3(R.party_keys(0))
     out = torch.zeros(4, dtype=torch.int64, device="cuda")

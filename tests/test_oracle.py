@@ -43,6 +43,15 @@ def test_prf_prefix_and_range():
         R.prf_words(k, 1, 1 << 48, 1)
 
 
+def test_prf_words_at_offset():
+    """prf_words_at (started mid-stream, for the far-offset GPU tests) equals
+    the stream prefix it skips, for even and odd offsets."""
+    k = R.party_keys(1)[2]
+    full = R.prf_words(k, 3, 11, 600)
+    for off, cnt in [(0, 5), (1, 9), (256, 300), (511, 89)]:
+        assert np.array_equal(R.prf_words_at(k, 3, 11, off, cnt), full[off:off + cnt])
+
+
 def test_bilinear_engine():
     assert np.array_equal(R.ring_matmul(G["mm_a"], G["mm_b"]), G["mm_out"])
     assert np.array_equal(R.wrap_matmul(G["mm_a"], G["mm_b"]), G["mm_out"])

@@ -205,6 +205,7 @@ def main():
     ap.add_argument("--out", default="gpurun_out/microbench.json")
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--gemm-t", action="store_true", help="only the transposed-operand GEMM comparison")
+    ap.add_argument("--aes", action="store_true", help="only the AES keystream and protocol-kernel rates")
     ap.add_argument("--cpu", action="store_true", help="also time the reference's CPU bilinear_exact / relu / truncate")
     args = ap.parse_args()
     if args.gemm_t:
@@ -223,6 +224,10 @@ def main():
     print("aes", res["aes"], flush=True)
     res["protocols"] = protocol_rates()
     print("protocols", res["protocols"], flush=True)
+    if args.aes:
+        with open(args.out, "w") as f:
+            json.dump(res, f, indent=1)
+        return
     res["int8_cublaslt"] = int8_peak()
     print("int8", res["int8_cublaslt"], flush=True)
     res["gemm"] = gemm_sweep([1024, 2048, 4096] if args.quick else [256, 512, 1024, 2048, 4096, 8192])
