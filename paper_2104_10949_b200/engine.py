@@ -50,6 +50,9 @@ REUSE_PACKS = os.environ.get("MPC3_REUSE_PACKS", "1") == "1"
 # MPC3_CS_PACKS=0: role-1 operands of the training step packed with both halves
 # instead of once per component (role 3: half the pack's writes)
 CS_PACKS = os.environ.get("MPC3_CS_PACKS", "1") == "1"
+# MPC3_T_PACKS=0: role-3 operands packed K-major (rows = the GEMM's rows)
+# instead of transposed (rows = the contraction), see Packed.t
+T_PACKS = os.environ.get("MPC3_T_PACKS", "1") == "1"
 # MPC3_MAXTREE_FUSED=0: one launch per max_tree level instead of one for the whole tree
 MAXTREE_FUSED = os.environ.get("MPC3_MAXTREE_FUSED", "1") == "1"
 # MPC3_LOSS_FUSED=0: the loss gradient softmax(z) - y as its separate launches
@@ -69,13 +72,20 @@ class Packed:
     at the 16-aligned column kh, role 0 ([x_i + x_{i+1} | x_i]) or 1
     ([x_i | x_{i+1}]); or role 3, a role-1 operand stored once per component
     (plane i = x_i, K columns, kh = k unused) whose halves the GEMM reads from
-    planes i and i + 1.  A weight gradient reads two of these transposed."""
+    planes i and i + 1.  A weight gradient reads two of these transposed.
+    t: a role-3 operand packed transposed — buffer rows are the contraction
+    index, columns the GEMM's rows (rows / k / kp describe the buffer).  The
+    GEMM then reads its A tiles MN-major: 128-byte TMA rows and SWIZZLE_128B
+    instead of 32-byte K-major rows (the forward and input-gradient GEMMs
+    +12-17 %, profiles/README.md), and a weight gradient reads the forward
+    pack K-major."""
     buf: torch.Tensor
     rows: int
     k: int
     kh: int
     kp: int
     role: int
+    t: bool = False
 
     @staticmethod
     def geometry(k: int) -> tuple[int, int]:
@@ -598,6 +608,25 @@ class TrioSession:
         return out
 
     # -- bilinear layers (protocols.py:97-136, nn.py:435-484) --
+    def pack_t(self, src: torch.Tensor, op, rows: int, k: int, zero: torch.Tensor | None = None) -> Packed | None:
+        """Role-3 pack of a (rows x k) operand transposed (Packed.t): the
+        buffer holds k rows of `rows` columns; None when the operand has no
+        transposed gather (dilated im2col, multi-digit dense views)."""
+        if not T_PACKS:
+            return None
+        t = K.Operand()
+        C.memmove(C.byref(t), C.byref(op), C.sizeof(K.Operand))
+        if op.mode == K.GATHER_IM2COL and op.dh <= 1 and op.dw <= 1:
+            t.mode = K.GATHER_WGRAD  # rows (c, u, v), columns (n, y, x): the same gather offsets
+        elif op.mode == K.GATHER_DENSE and op.K1 == 1 and op.K2 == op.k and op.t0 == 0 and op.t1 == 0:
+            t = K.dense_operand(op.k, op.rows, s_r=op.t2, t2=op.s_r, off=op.off)
+        else:
+            return None
+        t.rows, t.k = op.k, op.rows
+        pk = self.pack(src, t, k, rows, 3, zero=zero)
+        pk.t = True
+        return pk
+
     def pack(self, src: torch.Tensor, op, rows: int, k: int, role: int, zero: torch.Tensor | None = None,
              geom: tuple[int, int] | None = None) -> Packed:
         """Pack one cross-term operand in the reusable layout (see Packed);
@@ -678,14 +707,15 @@ class TrioSession:
             A = a_packed
         else:  # the A pack clears C when the GEMM accumulates atomically
             zeroed = self._needs_zero(cs, M, N, kp)
-            A = self.pack(a_src, a_op, M, Kd, 3 if cs else a_role, zero=z if zeroed else None)
+            A = self.pack_t(a_src, a_op, M, Kd, zero=z if zeroed else None) if cs else None
+            if A is None:
+                A = self.pack(a_src, a_op, M, Kd, 3 if cs else a_role, zero=z if zeroed else None)
         if ps is not None and ps != main:
             ev2 = torch.cuda.Event()
             ev2.record(ps)
             main.wait_event(ev2)
         if cs:  # A's halves from component planes g, g + 1; B role 0 with halves at kh = kc_half
-            K.call("mpc3_ring_gemm_t_z", A.buf.data_ptr(), 2, M, A.kp, 0, B.data_ptr(), 0, N, kp, 0, z.data_ptr(), 3,
-                   M, N, kh, 1 if c_col else 0, 1 if zeroed else 0, st)
+            self._gemm_cs(A, M, B, N, kp, z, kh, c_col, zeroed, st)
         else:
             K.call("mpc3_ring_gemm_auto_z", A.buf.data_ptr(), B.data_ptr(), z.data_ptr(), 3, M, N, kp,
                    1 if c_col else 0, 1 if zeroed else 0, st)
@@ -707,6 +737,11 @@ class TrioSession:
         z = torch.empty(3 * rows * wp.k, dtype=torch.int64, device=_dev())
         zeroed = self._needs_zero(True, rows, wp.k, 2 * kc)
         if CS_PACKS:  # g once per component (role 3): the GEMM reads half h from plane g + h
+            A = self.pack_t(g_src, g_op, rows, o, zero=z if zeroed else None)
+            if A is not None:  # transposed: A read MN-major too
+                K.call("mpc3_ring_gemm_t_z", A.buf.data_ptr(), 3, A.rows, A.kp, 0, wp.buf.data_ptr(), 1, wp.rows,
+                       wp.kp, wp.kh, z.data_ptr(), 3, rows, wp.k, kc, 1 if c_col else 0, 1 if zeroed else 0, st)
+                return z
             A = self.pack(g_src, g_op, rows, o, 3, zero=z if zeroed else None)
             K.call("mpc3_ring_gemm_t_z", A.buf.data_ptr(), 2, rows, A.kp, 0, wp.buf.data_ptr(), 1, wp.rows, wp.kp,
                    wp.kh, z.data_ptr(), 3, rows, wp.k, kc, 1 if c_col else 0, 1 if zeroed else 0, st)
@@ -724,14 +759,20 @@ class TrioSession:
         pack of g and the forward pass's role-1 pack of x, both read
         transposed.  z is [3][O][xp.k] row-major."""
         op, rows, o = self.grad_operand(g)
-        if xp.role not in (1, 3) or xp.rows != rows:
+        if xp.role not in (1, 3) or (xp.k if xp.t else xp.rows) != rows:
             raise ShapeError("weight-gradient packs do not match")
         # computed as x^T g (A = x, B = g) into the column-major layout, which
         # is the same memory and keeps the epilogue's stores coalesced
-        M, N, kc = xp.k, o, _round_up(rows, 32)
+        M, N, kc = (xp.rows if xp.t else xp.k), o, _round_up(rows, 32)
         z = torch.empty(3 * M * N, dtype=torch.int64, device=_dev())
         zeroed = self._needs_zero(True, M, N, 2 * kc)
         gp = self.pack(g.data, op, rows, o, 0, zero=z if zeroed else None)
+        if xp.t:  # x packed transposed in the forward pass: its rows are this GEMM's rows, read K-major
+            if xp.kp < kc:
+                raise ShapeError("transposed pack narrower than the contraction")
+            K.call("mpc3_ring_gemm_t_z", xp.buf.data_ptr(), 2, M, xp.kp, 0, gp.buf.data_ptr(), 1, gp.rows, gp.kp,
+                   gp.kh, z.data_ptr(), 3, M, N, kc, 1, 1 if zeroed else 0, _stream())
+            return z
         K.call("mpc3_ring_gemm_t_z", xp.buf.data_ptr(), 3 if xp.role == 3 else 1, xp.rows, xp.kp,
                0 if xp.role == 3 else xp.kh, gp.buf.data_ptr(), 1, gp.rows, gp.kp, gp.kh, z.data_ptr(), 3, M, N, kc, 1,
                1 if zeroed else 0, _stream())
@@ -819,14 +860,27 @@ class TrioSession:
                 self._wcache[key] = B
         z = torch.empty(3 * M * N, dtype=torch.int64, device=_dev())
         zeroed = self._needs_zero(True, M, N, kpb)
-        A = self.pack(a_src, a_op, M, Kd, 3, zero=z if zeroed else None)
+        A = self.pack_t(a_src, a_op, M, Kd, zero=z if zeroed else None)
+        if A is None:
+            A = self.pack(a_src, a_op, M, Kd, 3, zero=z if zeroed else None)
         if ps is not None:
             ev2 = torch.cuda.Event()
             ev2.record(ps)
             main.wait_event(ev2)
-        K.call("mpc3_ring_gemm_t_z", A.buf.data_ptr(), 2, M, A.kp, 0, B.data_ptr(), 0, N, kpb, 0, z.data_ptr(), 3, M, N,
-               kc, 1 if c_col else 0, 1 if zeroed else 0, st)
+        self._gemm_cs(A, M, B, N, kpb, z, kc, c_col, zeroed, st)
         return z
+
+    @staticmethod
+    def _gemm_cs(A: Packed, M: int, B: torch.Tensor, N: int, kpb: int, z, kc: int, c_col, zeroed, st) -> None:
+        """The ring GEMM of a role-3 A (halves from component planes g, g + 1;
+        read MN-major when packed transposed) and a role-0 B whose halves
+        start at kc = kc_half."""
+        if A.t:
+            K.call("mpc3_ring_gemm_t_z", A.buf.data_ptr(), 3, A.rows, A.kp, 0, B.data_ptr(), 0, N, kpb, 0,
+                   z.data_ptr(), 3, M, N, kc, 1 if c_col else 0, 1 if zeroed else 0, st)
+        else:
+            K.call("mpc3_ring_gemm_t_z", A.buf.data_ptr(), 2, M, A.kp, 0, B.data_ptr(), 0, N, kpb, 0, z.data_ptr(), 3,
+                   M, N, kc, 1 if c_col else 0, 1 if zeroed else 0, st)
 
     @staticmethod
     def _pack_a_zero(a_src, a_op, A, kp, Kd, z, zeroed, st):
@@ -913,7 +967,7 @@ class TrioSession:
         """Fully-connected weight gradient g^T x (nn.py:525-527) from x's
         forward pack (rows: batch, K: in)."""
         check_accumulation(g.shape[0])  # this rank's accumulation (see conv2d_wgrad)
-        m, n = g.shape[1], xp.k
+        m, n = g.shape[1], (xp.rows if xp.t else xp.k)
         z = self.wgrad_packed(g, xp)
         out = empty((m, n), self.fp)
         self._reduce_cross_terms(z)
@@ -1007,7 +1061,7 @@ class TrioSession:
         col = self.c_col_ok
         M = c * kh * kw
         if x_packed is not None:  # z[o][(c, u, v)]: the column-major layout below
-            if (x_packed.rows, x_packed.k) != (nb * oh * ow, M):
+            if ((x_packed.k, x_packed.rows) if x_packed.t else (x_packed.rows, x_packed.k)) != (nb * oh * ow, M):
                 raise ShapeError("weight-gradient packs do not match the layer")
             z, col = self.wgrad_packed(g, x_packed), True
         else:
