@@ -407,6 +407,9 @@ int mpc3_ring_gemm_auto_z(const uint8_t* A, const uint8_t* B, uint64_t* C, int g
  *   half h of group g is read from component plane (g + h) % 3, at no column
  *   offset (a_half unused; K-major: a_kp = the component pack's kp, the
  *   contraction per half kc_half); groups must be 3.
+ * a_mn = 5 (bit 2 with MN): A is a plain transposed pack (rows = the
+ *   contraction) whose second half is source ROWS [a_half, a_half +
+ *   kc_half), a_half >= kc_half, a_rows <= a_half + kc_half (the rest zero).
  * C dense [g][M][N] (c_layout 0) or [g][N][M] (1); zeroed here when the
  * split-K partials add atomically. */
 int mpc3_ring_gemm_t(const uint8_t* A, int a_mn, int64_t a_rows, int64_t a_kp, int64_t a_half, const uint8_t* B,
@@ -423,7 +426,9 @@ int mpc3_ring_gemm_simt(const uint64_t* A, const uint64_t* B, uint64_t* C, int64
 
 /* Convenience: plain ring matmul C (M,N) = A (M,K) . B (K,N), row-major,
  * exactly `bilinear_exact(a, b, matmul_spec(m,k,n))` (ring.py:183-222) minus
- * its 2^20 limit.  workspace >= mpc3_ring_matmul_workspace(M,N,K) bytes. */
+ * its 2^20 limit.  workspace >= mpc3_ring_matmul_workspace(M,N,K) bytes
+ * (A packed transposed and read MN-major, B K-major: mpc3_ring_gemm_t with
+ * a_mn = 5). */
 size_t mpc3_ring_matmul_workspace(int64_t M, int64_t N, int64_t K);
 int mpc3_ring_matmul_u64(const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t M, int64_t N,
                          int64_t K, void* workspace, void* stream);

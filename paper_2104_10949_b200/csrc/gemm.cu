@@ -306,9 +306,10 @@ DEV void mma_commit(uint64_t* bar) {
 // LBO 2 KiB).
 struct MnArgs {
   int a_mn, b_mn;
-  int a_half, b_half;  // source column of half 1
+  int a_half, b_half;  // source column of half 1 (a_rh: A's source row of half 1)
   int nkb_half;        // contraction K-blocks per half
   int a_cs;            // A's halves are component planes g and g + 1 (role-3 pack of a role-1 operand)
+  int a_rh;            // MN-read A whose second half is further source rows (a plain transposed pack)
 };
 
 DEV uint64_t umma_desc_mn(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
@@ -348,7 +349,10 @@ DEV void load_stage(const CUtensorMap* tmA, const CUtensorMap* tmB, uint64_t* ba
     else
       tma_load_3d(tmA, bar, sa, r, m0, ap);
   } else if (mn.a_mn) {
-    tma_load_3d(tmA, bar, sa, h * mn.a_half + m0, r, g * 8);
+    if (mn.a_rh)
+      tma_load_3d(tmA, bar, sa, m0, r + h * mn.a_half, g * 8);
+    else
+      tma_load_3d(tmA, bar, sa, h * mn.a_half + m0, r, g * 8);
   } else {
     tma_load_3d(tmA, bar, sa, kc, m0, g * 8);
   }
@@ -754,7 +758,7 @@ int mpc3_ring_gemm_packed_layout(const uint8_t* A, const uint8_t* B, uint64_t* C
   st = make_map(&tb, B, kp, N, (int64_t)groups * 8, BN);
   if (st) return st;
   dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)(groups * splits));
-  MnArgs mn0 = {0, 0, 0, 0, 1 << 30, 0};
+  MnArgs mn0 = {0, 0, 0, 0, 1 << 30, 0, 0};
   launch_pdl(gemm_tc_kernel, grid, dim3(GEMM_THREADS), SMEM_BYTES, as_stream(stream), ta, tb, C, M, N, kp, ldc, c_group, splits,
              kbs, c_layout, mn0);
   return check_launch("ring_gemm_tc");
@@ -844,9 +848,11 @@ int mpc3_ring_gemm_t_z(const uint8_t* A, int a_mn, int64_t a_rows, int64_t a_kp,
                        int64_t N, int64_t kc_half, int c_layout, int c_zeroed, void* stream) {
   if (groups < 1 || M < 0 || N < 0 || kc_half < 0 || (kc_half % BK)) return MPC3_ERR_SHAPE;
   if (c_layout != 0 && c_layout != 1) return MPC3_ERR_CONFIG;
-  if (a_mn < 0 || a_mn > 3 || b_mn < 0 || b_mn > 1) return MPC3_ERR_CONFIG;
-  const int a_cs = a_mn >> 1;  // bit 1: component-plane halves (role-3 pack)
+  if (a_mn < 0 || a_mn > 5 || a_mn == 4 || b_mn < 0 || b_mn > 1) return MPC3_ERR_CONFIG;
+  const int a_cs = (a_mn >> 1) & 1;  // bit 1: component-plane halves (role-3 pack)
+  const int a_rh = a_mn >> 2;        // bit 2 (with bit 0): half 1 is source rows [a_half, a_half + kc_half)
   a_mn &= 1;
+  if (a_rh && (a_cs || a_half < kc_half)) return MPC3_ERR_CONFIG;
   if (a_cs && (groups != 3 || a_kp % 16)) return MPC3_ERR_CONFIG;
   if (M == 0 || N == 0) return MPC3_OK;
   if (M > (1 << 30) || N > (1 << 30) || a_half > (1 << 30) || b_half > (1 << 30)) return MPC3_ERR_SHAPE;
@@ -856,7 +862,7 @@ int mpc3_ring_gemm_t_z(const uint8_t* A, int a_mn, int64_t a_rows, int64_t a_kp,
     return MPC3_ERR_SHAPE;
   // an MN operand's half offset is a TMA box start along the 16-byte-granular
   // inner dimension (pack with mpc3_ring_pack_halves, kh % 16 == 0)
-  if ((a_mn && (a_kp % 16 || a_rows > kc_half || (!a_cs && a_half % 16))) ||
+  if ((a_mn && (a_kp % 16 || a_rows > (a_rh ? a_half : 0) + kc_half || (!a_cs && !a_rh && a_half % 16))) ||
       (b_mn && (b_kp % 16 || b_rows > kc_half || b_half % 16)))
     return MPC3_ERR_SHAPE;
   static bool attr_set = false;
@@ -882,7 +888,7 @@ int mpc3_ring_gemm_t_z(const uint8_t* A, int a_mn, int64_t a_rows, int64_t a_kp,
       return check_launch("gemm C memset");
   }
   if (nkb == 0) return MPC3_OK;
-  MnArgs mn = {a_mn ? 1 : 0, b_mn ? 1 : 0, (int)a_half, (int)b_half, (int)(kc_half / BK), a_cs};
+  MnArgs mn = {a_mn ? 1 : 0, b_mn ? 1 : 0, (int)a_half, (int)b_half, (int)(kc_half / BK), a_cs, a_rh};
   dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)(groups * splits));
   launch_pdl(gemm_tc_kernel, grid, dim3(GEMM_THREADS), SMEM_BYTES, as_stream(stream), ta, tb, C, M, N, kp,
              c_layout ? M : N, M * N, (int)splits, kbs, c_layout, mn);
@@ -898,34 +904,43 @@ int mpc3_ring_gemm_simt(const uint64_t* A, const uint64_t* B, uint64_t* C, int64
   return check_launch("ring_gemm_simt");
 }
 
+// A transposed (rows = the contraction, read MN-major: 128-byte TMA rows),
+// B K-major; the contraction as two halves of kc = roundup(K / 2, 32) rows.
+static int64_t matmul_kc(int64_t K) { return ((K + 1) / 2 + 31) / 32 * 32; }
+static int64_t matmul_mp(int64_t M) { return (M + 31) / 32 * 32; }
+
 size_t mpc3_ring_matmul_workspace(int64_t M, int64_t N, int64_t K) {
-  int64_t kp = (K + 31) / 32 * 32;  // whole 32-byte K-blocks (partial TMA boxes are slow)
-  return (size_t)(8 * M * kp + 8 * N * kp);
+  if (M < 0 || N < 0 || K < 0) return 0;
+  return (size_t)(8 * K * matmul_mp(M) + 8 * N * 2 * matmul_kc(K));
 }
 
 int mpc3_ring_matmul_u64(const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t M, int64_t N, int64_t K,
                          void* workspace, void* stream) {
   if (M < 0 || N < 0 || K < 0) return MPC3_ERR_SHAPE;
   if (M == 0 || N == 0) return MPC3_OK;
-  int64_t kp = (K + 31) / 32 * 32;
+  if (K == 0) return cudaMemsetAsync(C, 0, (size_t)M * N * 8, as_stream(stream)) == cudaSuccess
+                         ? MPC3_OK
+                         : check_launch("matmul zero");
+  const int64_t kc = matmul_kc(K), mp = matmul_mp(M);
   uint8_t* pa = reinterpret_cast<uint8_t*>(workspace);
-  uint8_t* pb = pa + 8 * M * kp;
-  mpc3_operand oa;
+  uint8_t* pb = pa + 8 * K * mp;
+  mpc3_operand oa;  // A^T: row k = column k of A
   memset(&oa, 0, sizeof(oa));
   oa.mode = MPC3_GATHER_DENSE;
-  oa.rows = M;
-  oa.k = K;
-  oa.s_r = K;
-  oa.t2 = 1;
-  mpc3_operand ob = oa;
+  oa.rows = K;
+  oa.k = M;
+  oa.s_r = 1;
+  oa.t2 = K;
+  mpc3_operand ob = oa;  // B^T: row n = column n of B, K-major
   ob.rows = N;
+  ob.k = K;
   ob.s_r = 1;
   ob.t2 = N;
-  int st = mpc3_ring_pack(A, 0, &oa, 2, pa, kp, stream);
+  int st = mpc3_ring_pack(A, 0, &oa, 2, pa, mp, stream);
   if (st) return st;
-  st = mpc3_ring_pack(B, 0, &ob, 2, pb, kp, stream);
+  st = mpc3_ring_pack(B, 0, &ob, 2, pb, 2 * kc, stream);
   if (st) return st;
-  return mpc3_ring_gemm_auto(pa, pb, C, 1, M, N, kp, 0, stream);
+  return mpc3_ring_gemm_t(pa, 5, K, mp, kc, pb, 0, N, 2 * kc, 0, C, 1, M, N, kc, 0, stream);
 }
 
 }  // extern "C"

@@ -407,14 +407,38 @@ def test_pack_halves_z_clears_the_next_gemm_output():
     assert int(torch.count_nonzero(z)) == 0
 
 
-def test_ring_matmul_u64_convenience():
-    rng = np.random.default_rng(3)
-    M, K, Nn = 77, 20000, 33
+@pytest.mark.parametrize("M,K,Nn", [(77, 20000, 33), (1, 1, 1), (9, 33, 7), (130, 100, 70), (300, 257, 129),
+                                    (200, 4608, 512), (64, 63, 65)])
+def test_ring_matmul_u64_convenience(M, K, Nn):
+    """The single-call ring matmul (A packed transposed and read MN-major
+    with its halves along the source rows, a_mn = 5) vs the oracle."""
+    rng = np.random.default_rng(3 + M + K)
     a, b = rnd(rng, (M, K)), rnd(rng, (K, Nn))
     ws = torch.empty(_capi.lib().mpc3_ring_matmul_workspace(M, Nn, K), dtype=torch.uint8, device="cuda")
     out = torch.empty(M * Nn, dtype=torch.int64, device="cuda")
     _capi.call("mpc3_ring_matmul_u64", p(dev(a)), p(dev(b)), p(out), M, Nn, K, p(ws), stream())
     assert np.array_equal(host(out).reshape(M, Nn), R.wrap_matmul(a, b))
+
+
+def test_ring_matmul_u64_all_ones_exactness_edge():
+    """All-0xFF limbs through the single-call path at and past the per-split
+    exactness edge (K = 16384 and 3 x 16384 + 48: exactness splits)."""
+    for K in (16384, 3 * 16384 + 48):
+        a = np.full((128, K), (1 << 64) - 1, U64)
+        b = np.full((K, 64), (1 << 64) - 1, U64)
+        ws = torch.empty(_capi.lib().mpc3_ring_matmul_workspace(128, 64, K), dtype=torch.uint8, device="cuda")
+        out = torch.empty(128 * 64, dtype=torch.int64, device="cuda")
+        _capi.call("mpc3_ring_matmul_u64", p(dev(a)), p(dev(b)), p(out), 128, 64, K, p(ws), stream())
+        assert np.all(host(out) == U64(K))
+
+
+def test_ring_gemm_t_row_halves_config_errors():
+    z = torch.zeros(64, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(8 * 64 * 64, dtype=torch.uint8, device="cuda")
+    with pytest.raises(_capi.E.ConfigError):  # row halves need a_half >= kc_half
+        _capi.call("mpc3_ring_gemm_t", p(buf), 5, 32, 64, 16, p(buf), 0, 8, 64, 0, p(z), 1, 8, 8, 32, 0, stream())
+    with pytest.raises(_capi.E.ConfigError):  # not with component-plane halves
+        _capi.call("mpc3_ring_gemm_t", p(buf), 7, 32, 64, 32, p(buf), 0, 8, 64, 0, p(z), 3, 8, 8, 32, 0, stream())
 
 
 def test_secure_matmul_cross_terms_reshare_truncate():

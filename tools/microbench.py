@@ -57,22 +57,32 @@ def rk3():
 
 
 def gemm_sweep(sizes):
+    """M = N = K = n ring GEMMs (72 int8 ops per ring MAC) on random packed
+    operands in the layout the engine's forward GEMMs use (A read MN-major
+    from a transposed pack, B K-major: mpc3_ring_gemm_t with a_mn = 1, the
+    contraction as two halves of n/2 source rows each), and for reference
+    the all-K-major form (mpc3_ring_gemm_auto)."""
     out = []
     for n in sizes:
-        kp = (n + 15) // 16 * 16
-        A = torch.randint(0, 256, (8 * n * kp,), dtype=torch.uint8, device="cuda")
-        B = torch.randint(0, 256, (8 * n * kp,), dtype=torch.uint8, device="cuda")
+        kc = n // 2
+        At = torch.randint(0, 256, (8 * kc * 2 * n,), dtype=torch.uint8, device="cuda")  # [8][n/2][2n]
+        B = torch.randint(0, 256, (8 * n * n,), dtype=torch.uint8, device="cuda")         # [8][n][n]
         Cm = torch.empty(n * n, dtype=torch.int64, device="cuda")
 
         def run():
-            _capi.call("mpc3_ring_gemm_auto", p(A), p(B), p(Cm), 1, n, n, kp, 0, st())
+            _capi.call("mpc3_ring_gemm_t", p(At), 1, kc, 2 * n, n, p(B), 0, n, n, 0, p(Cm), 1, n, n, kc, 0, st())
+
+        def run_k():
+            _capi.call("mpc3_ring_gemm_auto", p(At), p(B), p(Cm), 1, n, n, n, 0, st())
 
         med, best = timeit(run, iters=5 if n >= 4096 else 10)
+        med_k, _ = timeit(run_k, iters=5 if n >= 4096 else 10)
         ring_macs = n ** 3
         out.append({"n": n, "ms": med * 1e3, "ring_tops": 2 * ring_macs / med / 1e12,
-                    "int8_tops": 72 * ring_macs / med / 1e12, "best_ms": best * 1e3})
+                    "int8_tops": 72 * ring_macs / med / 1e12, "best_ms": best * 1e3,
+                    "kmajor_ms": med_k * 1e3, "kmajor_int8_tops": 72 * ring_macs / med_k / 1e12})
         print("gemm", out[-1], flush=True)
-        del A, B, Cm
+        del At, B, Cm
     return out
 
 

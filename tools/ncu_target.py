@@ -1,6 +1,7 @@
 """Launch one kernel a few times for an `ncu --set full` capture.
 
 python tools/ncu_target.py gemm 4096      # mpc3_ring_gemm_packed, M=N=K=n (packed limb planes)
+python tools/ncu_target.py gemm_mn 4096   # the same product with A read MN-major (the engine's forward layout)
 python tools/ncu_target.py sign 16777216  # fused sign/ReLU circuit on n elements
 python tools/ncu_target.py pack 4096      # dense cross-term pack, 3 parties, M=K=n
 python tools/ncu_target.py wgrad 128      # transposed-operand GEMM, AlexNet conv5 weight gradient (R=n)
@@ -24,6 +25,13 @@ def main(kind, n, reps=3):
         Cm = torch.empty(n * n, dtype=torch.int64, device="cuda")
         for _ in range(reps):
             _capi.call("mpc3_ring_gemm_packed", p(A), p(B), p(Cm), 1, n, n, kp, n, 0, 1, st())
+    elif kind == "gemm_mn":  # the engine's forward layout: A read MN-major from a transposed pack
+        kc = n // 2
+        At = torch.randint(0, 256, (8 * kc * 2 * n,), dtype=torch.uint8, device="cuda")
+        B = torch.randint(0, 256, (8 * n * n,), dtype=torch.uint8, device="cuda")
+        Cm = torch.empty(n * n, dtype=torch.int64, device="cuda")
+        for _ in range(reps):
+            _capi.call("mpc3_ring_gemm_t", p(At), 1, kc, 2 * n, n, p(B), 0, n, n, 0, p(Cm), 1, n, n, kc, 0, st())
     elif kind == "sign":
         rk = rk3()
         x = torch.randint(-(1 << 40), 1 << 40, (3 * n,), dtype=torch.int64, device="cuda")
