@@ -237,7 +237,8 @@ struct SmemTables4 {
 struct __align__(16) HeadConst {
   uint32_t c[4], d[4];
 };
-constexpr int kHeadSlots = 16;
+constexpr int kHeadSlots = 16;   // two-table kernels (up to three CTAs per SM)
+constexpr int kHeadSlots4 = 40;  // four-table kernels (one CTA per SM): the SGD launch's per-tensor heads
 constexpr int kMaxTops = 4;
 
 // (The session keys travel in the kernel parameters, not here.)
@@ -249,8 +250,8 @@ struct __align__(16) AesSmem {
 constexpr int kAesSmemBytes = (int)sizeof(AesSmem);
 struct __align__(16) AesSmem4 {
   uint32_t te[2][256 * 64];
-  uint64_t extra[24];
-  HeadConst hc[kHeadSlots * kMaxTops * 3];
+  uint64_t extra[64];
+  HeadConst hc[kHeadSlots4 * kMaxTops * 3];
 };
 constexpr int kAesSmem4Bytes = (int)sizeof(AesSmem4);
 constexpr uint32_t kAesTableOff = 1024;
@@ -546,16 +547,15 @@ __device__ inline SmemTables4 aes_smem_init4(AesSmem4& sm) {
 // CTA calls this after the tables are built; thread t < 3 kTops NH computes
 // (head, v, key) = (t / 3 kTops, t / 3 % kTops, t % 3), and after the barrier
 // each head's pc points at its (v = 0, key 0) slot.
-// `on` (uniform over the grid) = false skips it (pc stays 0): tiny launches
-// whose threads run a block or two are better off without the barrier.
+// (Building with -DMPC3_NO_HEAD_CACHE leaves every pc 0: the A/B baseline,
+// profiles/r02_variants_aes_ctr_cache.txt.)
 template <class TT, class... H>
-DEV void cache_heads(const TT& tab, const uint32_t* rk3, HeadConst* slots, bool on, H&... h) {
+DEV void cache_heads(const TT& tab, const uint32_t* rk3, HeadConst* slots, H&... h) {
   constexpr int KT = TT::kTops;
   static_assert(sizeof...(H) <= kHeadSlots, "head slots");
 #if defined(MPC3_NO_HEAD_CACHE)
-  on = false;
+  return;
 #endif
-  if (!on) return;
   const int t = threadIdx.x, v = t / 3 % KT, k = t % 3;
   int i = 0;
   (((t / (3 * KT) == i ? head_const(tab, rk3 + 44 * k, h.s0, h.s1, (uint32_t)v, slots[t]) : void()), ++i), ...);

@@ -149,19 +149,6 @@ HD StreamRef sref(uint32_t purpose, uint64_t j) {
   return r;
 }
 
-// Counter-mode constants in the two-phase sign kernels (sign2, max_tree,
-// softmax) and in grid-stride protocol kernels whose threads get at least
-// MPC3_HEAD_CACHE_MIN pairs.
-#ifndef MPC3_HEAD_CACHE_TWO_PHASE
-#define MPC3_HEAD_CACHE_TWO_PHASE 1
-#endif
-#ifndef MPC3_HEAD_CACHE_MIN
-#define MPC3_HEAD_CACHE_MIN 0
-#endif
-DEV bool cache_worth(uint64_t pairs) {
-  return pairs >= (uint64_t)MPC3_HEAD_CACHE_MIN * gridDim.x * blockDim.x;
-}
-
 #define GRID_LOOP(var, count) \
   for (uint64_t var = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; var < (count); \
        var += (uint64_t)gridDim.x * blockDim.x)
@@ -175,7 +162,7 @@ __global__ void __launch_bounds__(kSignThreads, 1) prf_words_kernel(const __grid
   MPC3_AES_SMEM4();
   SmemTables4 tab = aes_smem_init4(sm);
   StreamHead hc = h;
-  cache_heads(tab, &ks.rk[0][0], sm.hc, true, hc);  // (keys 1-2 of ks are zero here: their slots go unused)
+  cache_heads(tab, &ks.rk[0][0], sm.hc, hc);  // (keys 1-2 of ks are zero here: their slots go unused)
   uint64_t nblk = ((word_off + count - 1) >> 1) - (word_off >> 1) + 1;
   GRID_LOOP(t, nblk) prf_words_item(tab, &ks.rk[0][0], hc, word_off, count, out, t);
 }
@@ -186,7 +173,7 @@ __global__ void __launch_bounds__(Proto<F>::threads, Proto<F>::min_ctas) zero_sh
                                                              int xor_mode, uint64_t n, uint64_t* __restrict__ out) {
   StreamHead h = resolve(rh, ctr);
   auto tab = Proto<F>::init();
-  cache_heads(tab, &ks.rk[0][0], Proto<F>::slots(), cache_worth((n + 1) >> 1), h);
+  cache_heads(tab, &ks.rk[0][0], Proto<F>::slots(), h);
   GRID_LOOP(b, (n + 1) >> 1) zero_share_item(tab, &ks.rk[0][0], h, xor_mode, n, out, b);
 }
 
@@ -247,7 +234,7 @@ __global__ void __launch_bounds__(Proto<F>::threads, Proto<F>::min_ctas) arith_k
                                                         uint64_t* __restrict__ out, uint64_t n, uint64_t pb0) {
   auto tab = Proto<F>::init();
   StreamHead ha = resolve(ra, ctr), hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
-  cache_heads(tab, &ks.rk[0][0], Proto<F>::slots(), cache_worth((n + 1) >> 1), ha, hrho, hr);
+  cache_heads(tab, &ks.rk[0][0], Proto<F>::slots(), ha, hrho, hr);
   GRID_LOOP(b, (n + 1) >> 1) arith_item(tab, &ks.rk[0][0], kind, ha, hrho, hr, bits, x, y, out, n, b, pb0);
 }
 
@@ -259,13 +246,11 @@ struct SignArgs {
 // Counter-mode constants of a launch's SignStreams (all threads, after the
 // tables are built; heads in declaration order -> slots; two barriers).
 template <class TT>
-DEV void cache_sign_streams(const TT& tab, const uint32_t* rk3, SignStreams& st, HeadConst* slots, bool rs,
-                            bool two_phase = false) {
+DEV void cache_sign_streams(const TT& tab, const uint32_t* rk3, SignStreams& st, HeadConst* slots, bool rs) {
   static_assert(sizeof(SignStreams) == 14 * sizeof(StreamHead), "SignStreams is an array of heads");
 #if defined(MPC3_NO_HEAD_CACHE)
   return;
 #endif
-  if (two_phase && !MPC3_HEAD_CACHE_TWO_PHASE) return;
   constexpr int KT = TT::kTops;
   StreamHead* hs = reinterpret_cast<StreamHead*>(&st);
   const int nh = rs ? 14 : 11;
@@ -380,7 +365,7 @@ __global__ void __launch_bounds__(F ? kSignThreads : kThreads, F ? 1 : 2)
                                                       : reinterpret_cast<AesSmem*>(mpc3_dsm)->extra);
   if (threadIdx.x == 0) sign_streams(st, args, ctr, KIND == S2_RS);
   auto tab = Proto<F>::init();  // (its __syncthreads publishes st)
-  cache_sign_streams(tab, &ks.rk[0][0], st, Proto<F>::slots(), KIND == S2_RS, true);
+  cache_sign_streams(tab, &ks.rk[0][0], st, Proto<F>::slots(), KIND == S2_RS);
   Word2* pre = reinterpret_cast<Word2*>(mpc3_dsm + (F ? sizeof(AesSmem4) : sizeof(AesSmem)));
   Word2* slots = pre + (size_t)PRE * P * 3;
   const bool straddle = (n_total & 1) != 0;
@@ -469,7 +454,7 @@ __global__ void __launch_bounds__(kThreads, 1) maxtree_kernel(const __grid_const
       sign_streams(st, a, ctr, false);
     }
     __syncthreads();
-    cache_sign_streams(tab, &ks.rk[0][0], st, reinterpret_cast<AesSmem*>(mpc3_dsm)->hc, false, true);
+    cache_sign_streams(tab, &ks.rk[0][0], st, reinterpret_cast<AesSmem*>(mpc3_dsm)->hc, false);
     const uint64_t n = rows * k, n_total = ta.rows_total * k, elem_off = ta.row_off * k;
     const bool straddle = (n_total & 1) != 0;
     const int L = straddle ? 3 : 2, used = sign_slots(straddle);
@@ -707,7 +692,7 @@ __global__ void __launch_bounds__(kThreads, 1) softmax_loss_kernel(
       sign_streams(st, a, ctr, false);
     }
     __syncthreads();
-    cache_sign_streams(tab, &ks.rk[0][0], st, reinterpret_cast<AesSmem*>(mpc3_dsm)->hc, false, true);
+    cache_sign_streams(tab, &ks.rk[0][0], st, reinterpret_cast<AesSmem*>(mpc3_dsm)->hc, false);
     const uint64_t nl = rows * k, n_total = la.rows_total * k, elem_off = la.row_off * k;
     const bool straddle = (n_total & 1) != 0;
     const int L = straddle ? 3 : 2, used = sign_slots(straddle);
@@ -828,7 +813,7 @@ __global__ void __launch_bounds__(Proto<F>::threads, Proto<F>::min_ctas) inject_
                                                          uint64_t* __restrict__ out, uint64_t n, uint64_t pb0) {
   auto tab = Proto<F>::init();
   StreamHead a0 = resolve(r0, ctr), a1 = resolve(r1, ctr);
-  cache_heads(tab, &ks.rk[0][0], Proto<F>::slots(), cache_worth((n + 1) >> 1), a0, a1);
+  cache_heads(tab, &ks.rk[0][0], Proto<F>::slots(), a0, a1);
   GRID_LOOP(b, (n + 1) >> 1) inject_item(tab, &ks.rk[0][0], a0, a1, bits, out, n, b, pb0);
 }
 
@@ -841,7 +826,7 @@ __global__ void __launch_bounds__(Proto<F>::threads, Proto<F>::min_ctas) reshare
                                                                 uint64_t pb0) {
   auto tab = Proto<F>::init();
   StreamHead ha = resolve(ra, ctr), hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
-  cache_heads(tab, &ks.rk[0][0], Proto<F>::slots(), cache_worth((n + 1) >> 1), ha, hrho, hr);
+  cache_heads(tab, &ks.rk[0][0], Proto<F>::slots(), ha, hrho, hr);
   if (n < (1ull << 32))
     GRID_LOOP(b, (n + 1) >> 1) reshare_trunc_item<typename Proto<F>::TT, uint32_t>(tab, &ks.rk[0][0], ha, hrho, hr, bits, z, v, out,
                                                                          n, b, pb0);
@@ -859,7 +844,7 @@ __global__ void __launch_bounds__(Proto<F>::threads, Proto<F>::min_ctas) pool_ke
                                                        StreamRef ra) {
   auto tab = Proto<F>::init();
   StreamHead hrho = resolve(rrho, ctr), hr = resolve(rr, ctr), ha = mask ? resolve(ra, ctr) : StreamHead{0, 0, 0};
-  cache_heads(tab, &ks.rk[0][0], Proto<F>::slots(), cache_worth((n + 1) >> 1), hrho, hr, ha);
+  cache_heads(tab, &ks.rk[0][0], Proto<F>::slots(), hrho, hr, ha);
   if (2 * n < (1ull << 32) && (uint64_t)p.N * p.C * p.H * p.W < (1ull << 32))
     GRID_LOOP(b, (n + 1) >> 1) pool_item<typename Proto<F>::TT, uint32_t>(tab, &ks.rk[0][0], backward != 0, hrho, hr, bits, mulc, x,
                                                                 out, p, b, pb0, mask, ha);
@@ -876,7 +861,7 @@ __global__ void __launch_bounds__(Proto<F>::threads, Proto<F>::min_ctas) col2im_
                                                          uint64_t* __restrict__ out, uint64_t n, uint64_t pb0) {
   auto tab = Proto<F>::init();
   StreamHead ha = resolve(ra, ctr), hrho = resolve(rrho, ctr), hr = resolve(rr, ctr);
-  cache_heads(tab, &ks.rk[0][0], Proto<F>::slots(), cache_worth((n + 1) >> 1), ha, hrho, hr);
+  cache_heads(tab, &ks.rk[0][0], Proto<F>::slots(), ha, hrho, hr);
   if (2 * n < (1ull << 32))
     GRID_LOOP(b, (n + 1) >> 1) col2im_item<typename Proto<F>::TT, uint32_t>(tab, &ks.rk[0][0], ha, hrho, hr, bits, z, g, out, b,
                                                                   pb0);

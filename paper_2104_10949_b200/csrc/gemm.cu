@@ -708,8 +708,6 @@ int mpc3_ring_pack_halves_z(const uint64_t* src, int64_t src_plane, const mpc3_o
       a.sH = (int32_t)o.sH;
       a.sW = (int32_t)o.sW;
       r_fast = o.mode == MPC3_GATHER_IM2COL && o.sw <= 2;  // strided windows: walk the kernel row (contiguous input x)
-      static const char* force = getenv("MPC3_PACK_RFAST");
-      if (force) r_fast = force[0] == '1';
     }
     dim3 grid((unsigned)((kp + PT_K - 1) / PT_K), (unsigned)row_tiles, (unsigned)groups);
     void (*k)(const uint64_t*, int64_t, Operand, PackTileArgs, uint8_t*) =
@@ -772,12 +770,9 @@ struct AutoPlan {
   int64_t splits;
   bool zero;
 };
-// minimum K-blocks per split when splitting K for occupancy (MPC3_SPLIT_MINKB)
-static int64_t split_min_kb() {
-  // 2: the AlexNet step 2.469 -> 2.459 ms against 4 (short-K GEMMs fill more SMs)
-  static const int64_t v = getenv("MPC3_SPLIT_MINKB") ? atoll(getenv("MPC3_SPLIT_MINKB")) : 2;
-  return v < 1 ? 1 : v;
-}
+// minimum K-blocks per split when splitting K for occupancy
+// (2: the AlexNet step 2.469 -> 2.459 ms against 4: short-K GEMMs fill more SMs)
+static int64_t split_min_kb() { return 2; }
 
 static AutoPlan auto_plan(int groups, int64_t M, int64_t N, int64_t kp) {
   const int64_t sms = 148;

@@ -3,6 +3,7 @@
 python tools/ncu_target.py gemm 4096      # mpc3_ring_gemm_packed, M=N=K=n (packed limb planes)
 python tools/ncu_target.py gemm_mn 4096   # the same product with A read MN-major (the engine's forward layout)
 python tools/ncu_target.py sign 16777216  # fused sign/ReLU circuit on n elements
+python tools/ncu_target.py reshare 884736 # reshare + truncate of n cross terms (an AlexNet wgrad epilogue)
 python tools/ncu_target.py pack 4096      # dense cross-term pack, 3 parties, M=K=n
 python tools/ncu_target.py wgrad 128      # transposed-operand GEMM, AlexNet conv5 weight gradient (R=n)
 """
@@ -32,6 +33,13 @@ def main(kind, n, reps=3):
         Cm = torch.empty(n * n, dtype=torch.int64, device="cuda")
         for _ in range(reps):
             _capi.call("mpc3_ring_gemm_t", p(At), 1, kc, 2 * n, n, p(B), 0, n, n, 0, p(Cm), 1, n, n, kc, 0, st())
+    elif kind == "reshare":  # reshare + truncate of n cross terms (a layer epilogue), row-major view
+        rk = rk3()
+        z = torch.randint(-(1 << 62), 1 << 62, (3 * n,), dtype=torch.int64, device="cuda")
+        out = torch.empty_like(z)
+        v = _capi.make_view((1, 1, n // 256, 256))
+        for _ in range(reps):
+            _capi.call("mpc3_rss_reshare_truncate", p(rk), None, 0, 0, 0, 20, p(z), C.byref(v), p(out), 0, st())
     elif kind == "sign":
         rk = rk3()
         x = torch.randint(-(1 << 40), 1 << 40, (3 * n,), dtype=torch.int64, device="cuda")
