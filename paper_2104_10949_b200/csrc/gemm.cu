@@ -228,7 +228,10 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const uint64_t* __restri
 constexpr int BM = 128;            // rows per CTA (TMEM lanes)
 constexpr int BN = 64;             // output columns per CTA (per limb block)
 constexpr int BK = 32;             // K bytes per stage (one kind::i8 MMA K)
-constexpr int STAGES = 4;
+#ifndef MPC3_GEMM_STAGES
+#define MPC3_GEMM_STAGES 4
+#endif
+constexpr int STAGES = MPC3_GEMM_STAGES;
 constexpr int A_STAGE = 8 * BM * BK;  // 32 KiB
 constexpr int B_STAGE = 8 * BN * BK;  // 16 KiB
 constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) + 1024 /*align*/ + 256 /*barriers*/;
