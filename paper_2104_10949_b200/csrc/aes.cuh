@@ -405,27 +405,29 @@ DEV uint4 lds_v4(uint32_t addr) {
   return v;
 }
 
-// NB blocks of one counter value blk, block i of stream columns (s01[i][0],
+// NB blocks, block i at counter blks[i] of stream columns (s01[i][0],
 // s01[i][1]) under key schedule rks[i] whose counter-mode constants (v = 0)
 // sit at shared address pcs[i] (0: none).  Output: the ciphertext columns.
 // Blocks whose counter top byte has constants (below kTops << 24) start at
 // round 3 (rounds 1-2 from the constants, 15 lookups), other blocks below
 // 2^32 at round 2 (round 1: 5 lookups); otherwise all rounds run.
 template <int NB, class TT>
-DEV void aes128_ctr(const TT& tab, const uint32_t* const rks[NB], const uint32_t pcs[NB], const uint32_t s01[NB][2],
-                    uint64_t blk, uint32_t s[NB][4]) {
+DEV void aes128_ctr_n(const TT& tab, const uint32_t* const rks[NB], const uint32_t pcs[NB],
+                      const uint32_t s01[NB][2], const uint64_t blks[NB], uint32_t s[NB][4]) {
   constexpr bool FOUR = TT::kFour;
   const uint32_t hl = tab.hl;
-  bool cached = (blk >> 32) == 0;
+  bool cached = true, top0 = true;
 #pragma unroll
-  for (int i = 0; i < NB; ++i) cached = cached && pcs[i] != 0;
+  for (int i = 0; i < NB; ++i) {
+    cached = cached && pcs[i] != 0 && (blks[i] >> 32) == 0;
+    top0 = top0 && ((uint32_t)blks[i] >> 24) < (uint32_t)TT::kTops;
+  }
   int r0 = 1;
   if (cached) {
-    const uint32_t lo = (uint32_t)blk, v = lo >> 24;
-    const bool top0 = v < (uint32_t)TT::kTops;
-    const uint32_t voff = top0 ? v * 96u : 0u;  // [v][key] stride: 3 keys x 32 bytes
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
+      const uint32_t lo = (uint32_t)blks[i];
+      const uint32_t voff = top0 ? (lo >> 24) * 96u : 0u;  // [v][key] stride: 3 keys x 32 bytes
       const uint4 c = lds_v4(pcs[i] + voff);
       const uint32_t x3 = lo ^ rks[i][3];
       s[i][0] = c.x ^ MPC3_TE3(x3);
@@ -436,7 +438,7 @@ DEV void aes128_ctr(const TT& tab, const uint32_t* const rks[NB], const uint32_t
     if (top0) {
 #pragma unroll
       for (int i = 0; i < NB; ++i) {
-        const uint4 d = lds_v4(pcs[i] + voff + 16);
+        const uint4 d = lds_v4(pcs[i] + ((uint32_t)blks[i] >> 24) * 96u + 16);
         const uint32_t t0 = s[i][0], t1 = s[i][1], t2 = s[i][2];
         s[i][0] = MPC3_TE0(t0) ^ MPC3_TE1(t1) ^ MPC3_TE2(t2) ^ d.x;
         s[i][1] = MPC3_TE0(t1) ^ MPC3_TE1(t2) ^ MPC3_TE3(t0) ^ d.y;
@@ -452,8 +454,8 @@ DEV void aes128_ctr(const TT& tab, const uint32_t* const rks[NB], const uint32_t
     for (int i = 0; i < NB; ++i) {
       s[i][0] = s01[i][0] ^ rks[i][0];
       s[i][1] = s01[i][1] ^ rks[i][1];
-      s[i][2] = (uint32_t)(blk >> 32) ^ rks[i][2];
-      s[i][3] = (uint32_t)blk ^ rks[i][3];
+      s[i][2] = (uint32_t)(blks[i] >> 32) ^ rks[i][2];
+      s[i][3] = (uint32_t)blks[i] ^ rks[i][3];
     }
   }
 #pragma unroll 1
@@ -480,6 +482,15 @@ DEV void aes128_ctr(const TT& tab, const uint32_t* const rks[NB], const uint32_t
     s[i][2] = MPC3_FIN(c, d, a, b, k.z);
     s[i][3] = MPC3_FIN(d, a, b, c, k.w);
   }
+}
+// All NB blocks at one counter value.
+template <int NB, class TT>
+DEV void aes128_ctr(const TT& tab, const uint32_t* const rks[NB], const uint32_t pcs[NB], const uint32_t s01[NB][2],
+                    uint64_t blk, uint32_t s[NB][4]) {
+  uint64_t blks[NB];
+#pragma unroll
+  for (int i = 0; i < NB; ++i) blks[i] = blk;
+  aes128_ctr_n<NB>(tab, rks, pcs, s01, blks, s);
 }
 #undef MPC3_TE0
 #undef MPC3_TE1

@@ -129,6 +129,44 @@ HD void prf_block3(const SmemTables4& tab, const uint32_t* rk3, StreamHead h, ui
 }
 #endif
 
+// Blocks ba and bb of one stream under the three session keys (on the device
+// six interleaved AES chains: the Kogge-Stone level's g- and p-halves).
+template <class T>
+HD void prf_block3x2(const T& tab, const uint32_t* rk3, StreamHead h, uint64_t ba, uint64_t bb, Word2 wa[3],
+                     Word2 wb[3]) {
+  prf_block3(tab, rk3, h, ba, wa);
+  prf_block3(tab, rk3, h, bb, wb);
+}
+#if defined(__CUDACC__)
+template <class TT>
+HD void prf_block3x2_dev(const TT& tab, const uint32_t* rk3, StreamHead h, uint64_t ba, uint64_t bb, Word2 wa[3],
+                         Word2 wb[3]) {
+#if defined(__CUDA_ARCH__)
+  uint32_t s[6][4];
+  const uint32_t* rks[6] = {rk3, rk3 + 44, rk3 + 88, rk3, rk3 + 44, rk3 + 88};
+  const uint32_t p1 = h.pc ? h.pc + 32 : 0u, p2 = h.pc ? h.pc + 64 : 0u;
+  const uint32_t pcs[6] = {h.pc, p1, p2, h.pc, p1, p2};
+  const uint32_t s01[6][2] = {{h.s0, h.s1}, {h.s0, h.s1}, {h.s0, h.s1}, {h.s0, h.s1}, {h.s0, h.s1}, {h.s0, h.s1}};
+  const uint64_t blks[6] = {ba, ba, ba, bb, bb, bb};
+  aes128_ctr_n<6>(tab, rks, pcs, s01, blks, s);
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    Word2& w = i < 3 ? wa[i] : wb[i - 3];
+    w.w0 = (uint64_t)bswap32(s[i][0]) | ((uint64_t)bswap32(s[i][1]) << 32);
+    w.w1 = (uint64_t)bswap32(s[i][2]) | ((uint64_t)bswap32(s[i][3]) << 32);
+  }
+#endif
+}
+HD void prf_block3x2(const SmemTables& tab, const uint32_t* rk3, StreamHead h, uint64_t ba, uint64_t bb, Word2 wa[3],
+                     Word2 wb[3]) {
+  prf_block3x2_dev(tab, rk3, h, ba, bb, wa, wb);
+}
+HD void prf_block3x2(const SmemTables4& tab, const uint32_t* rk3, StreamHead h, uint64_t ba, uint64_t bb,
+                     Word2 wa[3], Word2 wb[3]) {
+  prf_block3x2_dev(tab, rk3, h, ba, bb, wa, wb);
+}
+#endif
+
 // Block blk of one stream under session key k (k_0, k_1, k_2).
 template <class T>
 HD Word2 prf_block_k(const T& tab, const uint32_t* rk3, int k, StreamHead h, uint64_t blk) {
@@ -363,6 +401,22 @@ HD void fold_sel(Trio z[2], const Word2 w[3], int sel, bool xor_mode) {
   }
 }
 
+// Kogge-Stone level shape of sign_circuit_pair per keystream source: the
+// two-phase kernel's replayed words run each level's g- and p-halves
+// together (fewer, longer steps: its circuit phase 37.6 -> 33.4 us at 50 K
+// elements); the persistent kernel, at its register cap, keeps one AND
+// half live at a time (the merged form spills there).
+template <class T>
+struct MergedLevels {
+  static constexpr bool value = false;
+};
+#if defined(__CUDACC__)
+template <>
+struct MergedLevels<Replay> {
+  static constexpr bool value = true;
+};
+#endif
+
 // The fused sign circuit for the element pair (2*blk, 2*blk+1) of a tensor of
 // n_total elements (n_total sets where the Kogge-Stone p-half lives, word
 // n_total + e, protocols.py:247-259).  x is read through `ld` (local element
@@ -386,16 +440,11 @@ HD void sign_circuit_pair(const T& tab, const uint32_t* rk3, const SignStreams& 
   // a2b input sharing (protocols.py:278-295): w = ((c0+c1)^r, r, 0), x2 = (0,0,c2)
   const Word2 rb = prf_block_k(tab, rk3, 0, st.bin, blk);
   Trio p[2], g[2];
-  const uint64_t pw = n_total + 2 * blk;  // stream word of element 0's p-half
-#if defined(__CUDA_ARCH__)
-#pragma unroll 1
-#endif
-  for (int job = 0; job < 12; ++job) {
-    const int lvl = (job + 1) >> 1;  // 0, 1, 1, 2, 2, ..., 6
-    const int d = lvl > 0 ? 1 << (lvl - 1) : 0;
-    const bool phalf = job > 0 && (job & 1) == 0;
-    Trio t[2];
-    if (job == 0) {
+  if constexpr (MergedLevels<T>::value) {
+    const uint64_t pw = n_total + 2 * blk;  // stream word of element 0's p-half
+    const bool straddle = (pw & 1) != 0;
+    {  // level 0: g = a AND b
+      Trio t[2];
       for (int e = 0; e < 2; ++e) {
         Trio x = ld(e);
         uint64_t r = e ? rb.w1 : rb.w0;
@@ -404,28 +453,83 @@ HD void sign_circuit_pair(const T& tab, const uint32_t* rk3, const SignStreams& 
         p[e] = trio_xor(a, b);
         t[e] = and_local(a, b);
       }
-    } else {
-      for (int e = 0; e < 2; ++e) t[e] = and_local(p[e], trio_shl(phalf ? p[e] : g[e], d));
-    }
-    const StreamHead h = st.x[lvl];
-    const bool straddle = phalf && (pw & 1);
-    const uint64_t b0 = phalf ? (pw >> 1) : blk;
-#if defined(__CUDA_ARCH__)
-#pragma unroll 1
-#endif
-    for (int sub = 0; sub < (straddle ? 2 : 1); ++sub) {
       Word2 w[3];
-      prf_block3(tab, rk3, h, b0 + sub, w);
-      fold_sel(t, w, straddle ? 1 + sub : 0, true);
+      prf_block3(tab, rk3, st.x[0], blk, w);
+      fold_sel(t, w, 0, true);
+      for (int e = 0; e < 2; ++e) g[e] = relabel(t[e]);
     }
-    for (int e = 0; e < 2; ++e) {
-      Trio r = relabel(t[e]);
-      if (job == 0)
-        g[e] = r;
-      else if (phalf)
-        p[e] = r;
-      else
-        g[e] = trio_xor(g[e], r);
+    // levels 1-6: the g-half (p AND g << d) and the p-half (p AND p << d) of a
+    // level both read the level's input p, so their keystream (words 2 blk of
+    // the level's XOR stream, and words n_total + 2 blk) is one six-chain AES
+    // call; level 6's p-half is dead (p is not read after the loop)
+  #if defined(__CUDA_ARCH__)
+  #pragma unroll 1
+  #endif
+    for (int lvl = 1; lvl <= 6; ++lvl) {
+      const int d = 1 << (lvl - 1);
+      const StreamHead h = st.x[lvl];
+      Trio tg[2], tp[2];
+      for (int e = 0; e < 2; ++e) tg[e] = and_local(p[e], trio_shl(g[e], d));
+      if (lvl < 6) {
+        for (int e = 0; e < 2; ++e) tp[e] = and_local(p[e], trio_shl(p[e], d));
+        Word2 wg[3], wp[3];
+        prf_block3x2(tab, rk3, h, blk, pw >> 1, wg, wp);
+        fold_sel(tg, wg, 0, true);
+        fold_sel(tp, wp, straddle ? 1 : 0, true);
+        if (straddle) {  // the pair's p-half straddles two blocks (odd n_total)
+          prf_block3(tab, rk3, h, (pw >> 1) + 1, wp);
+          fold_sel(tp, wp, 2, true);
+        }
+        for (int e = 0; e < 2; ++e) p[e] = relabel(tp[e]);
+      } else {
+        Word2 wg[3];
+        prf_block3(tab, rk3, h, blk, wg);
+        fold_sel(tg, wg, 0, true);
+      }
+      for (int e = 0; e < 2; ++e) g[e] = trio_xor(g[e], relabel(tg[e]));
+    }
+  } else {
+    const uint64_t pw = n_total + 2 * blk;  // stream word of element 0's p-half
+  #if defined(__CUDA_ARCH__)
+  #pragma unroll 1
+  #endif
+    for (int job = 0; job < 12; ++job) {
+      const int lvl = (job + 1) >> 1;  // 0, 1, 1, 2, 2, ..., 6
+      const int d = lvl > 0 ? 1 << (lvl - 1) : 0;
+      const bool phalf = job > 0 && (job & 1) == 0;
+      Trio t[2];
+      if (job == 0) {
+        for (int e = 0; e < 2; ++e) {
+          Trio x = ld(e);
+          uint64_t r = e ? rb.w1 : rb.w0;
+          Trio a = {{(x.c[0] + x.c[1]) ^ r, r, 0}};
+          Trio b = {{0, 0, x.c[2]}};
+          p[e] = trio_xor(a, b);
+          t[e] = and_local(a, b);
+        }
+      } else {
+        for (int e = 0; e < 2; ++e) t[e] = and_local(p[e], trio_shl(phalf ? p[e] : g[e], d));
+      }
+      const StreamHead h = st.x[lvl];
+      const bool straddle = phalf && (pw & 1);
+      const uint64_t b0 = phalf ? (pw >> 1) : blk;
+  #if defined(__CUDA_ARCH__)
+  #pragma unroll 1
+  #endif
+      for (int sub = 0; sub < (straddle ? 2 : 1); ++sub) {
+        Word2 w[3];
+        prf_block3(tab, rk3, h, b0 + sub, w);
+        fold_sel(t, w, straddle ? 1 + sub : 0, true);
+      }
+      for (int e = 0; e < 2; ++e) {
+        Trio r = relabel(t[e]);
+        if (job == 0)
+          g[e] = r;
+        else if (phalf)
+          p[e] = r;
+        else
+          g[e] = trio_xor(g[e], r);
+      }
     }
   }
   Trio s[2];
