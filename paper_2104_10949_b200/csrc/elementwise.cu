@@ -785,23 +785,55 @@ __global__ void __launch_bounds__(Proto<F>::threads, Proto<F>::min_ctas) sgd_ker
                                                       uint64_t c) {
   auto tab = Proto<F>::init();
   const uint64_t total = tb.pair0[tb.nt];
+  // the first kHeadSlots4 / 2 tensors' (rho, r) heads with counter-mode
+  // constants in shared memory (four-table launches: one CTA per SM); the
+  // rest resolved per pair
+  constexpr int KT = Proto<F>::TT::kTops;
+  const int nc = F ? imin32(tb.nt, kHeadSlots4 / 2) : 0;
+  StreamHead* hs = reinterpret_cast<StreamHead*>(reinterpret_cast<AesSmem4*>(mpc3_dsm)->extra);
+  static_assert(sizeof(StreamHead) * kHeadSlots4 <= sizeof(AesSmem4::extra), "SGD heads fit the extra area");
+  if (nc) {
+    HeadConst* slots = Proto<F>::slots();
+    if (threadIdx.x < 2 * nc) {
+      const MPC3SgdTensor& T = tb.t[threadIdx.x >> 1];
+      hs[threadIdx.x] = (threadIdx.x & 1) ? resolve(sref(TRUNC_R, T.j_r), ctr) : resolve(sref(TRUNC_RHO, T.j_rho), ctr);
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < 2 * nc * KT * 3; t += blockDim.x) {
+      const StreamHead h = hs[t / (3 * KT)];
+      head_const(tab, &ks.rk[0][0] + 44 * (t % 3), h.s0, h.s1, (uint32_t)(t / 3 % KT), slots[t]);
+    }
+    __syncthreads();
+    if (threadIdx.x < 2 * nc) hs[threadIdx.x].pc = (uint32_t)__cvta_generic_to_shared(&slots[threadIdx.x * KT * 3]);
+    __syncthreads();
+  }
   GRID_LOOP(q, total) {
     int i = 0;
     while (q >= tb.pair0[i + 1]) ++i;  // few tensors: linear scan
     const MPC3SgdTensor& T = tb.t[i];
     const uint64_t b = q - tb.pair0[i], n = T.n;
+    // the pair's gradient and parameter loads are issued before its AES
+    // blocks, whose latency then covers them (ncu: long-scoreboard stalls
+    // were a quarter of the warp samples with the loads after)
+    Trio g[2], w[2];
+    const bool two = 2 * b + 1 < n;
+    g[0] = load_trio(T.grad, n, 2 * b);
+    w[0] = load_trio(T.param, n, 2 * b);
+    if (two) {
+      g[1] = load_trio(T.grad, n, 2 * b + 1);
+      w[1] = load_trio(T.param, n, 2 * b + 1);
+    }
     Word2 rho, r;
-    trunc_words(tab, &ks.rk[0][0], resolve(sref(TRUNC_RHO, T.j_rho), ctr), resolve(sref(TRUNC_R, T.j_r), ctr), b, rho,
-                r);
-    for (int e = 0; e < 2; ++e) {
-      const uint64_t f = 2 * b + e;
-      if (f >= n) break;
-      Trio g = load_trio(T.grad, n, f);
-      for (int k = 0; k < 3; ++k) g.c[k] *= c;
-      const Trio v = trio_truncate(g, e ? rho.w1 : rho.w0, e ? r.w1 : r.w0, bits);
-      Trio w = load_trio(T.param, n, f);
-      for (int k = 0; k < 3; ++k) w.c[k] -= v.c[k];
-      store_trio(T.param, n, f, w);
+    if (i < nc)
+      trunc_words(tab, &ks.rk[0][0], hs[2 * i], hs[2 * i + 1], b, rho, r);
+    else
+      trunc_words(tab, &ks.rk[0][0], resolve(sref(TRUNC_RHO, T.j_rho), ctr), resolve(sref(TRUNC_R, T.j_r), ctr), b,
+                  rho, r);
+    for (int e = 0; e < (two ? 2 : 1); ++e) {
+      for (int k = 0; k < 3; ++k) g[e].c[k] *= c;
+      const Trio v = trio_truncate(g[e], e ? rho.w1 : rho.w0, e ? r.w1 : r.w0, bits);
+      for (int k = 0; k < 3; ++k) w[e].c[k] -= v.c[k];
+      store_trio(T.param, n, 2 * b + e, w[e]);
     }
   }
 }

@@ -259,6 +259,11 @@ HD void reshare_trunc_item(const T& tab, const uint32_t* rk3, StreamHead ha, Str
     ooff[e] = i0 * v.os[0] + i1 * v.os[1] + i2 * v.os[2] + i3 * v.os[3];
   }
   if (!ok[0] && !ok[1]) return;
+  // the cross terms are loaded before the pair's AES blocks (their latency
+  // hides the loads)
+  Trio zt[2];
+  for (int e = 0; e < 2; ++e)
+    if (ok[e]) zt[e] = load_trio(z + zoff[e], v.zp, 0);
   KeyWords f0, f1;
   Word2 rho = {0, 0}, r = {0, 0};
   if (bits) {
@@ -274,8 +279,7 @@ HD void reshare_trunc_item(const T& tab, const uint32_t* rk3, StreamHead ha, Str
   }
   for (int e = 0; e < 2; ++e) {
     if (!ok[e]) continue;
-    Trio t = load_trio(z + zoff[e], v.zp, 0);
-    t = trio_reshare(t, e ? f1 : f0);
+    Trio t = trio_reshare(zt[e], e ? f1 : f0);
     if (bits) t = trio_truncate(t, e ? rho.w1 : rho.w0, e ? r.w1 : r.w0, bits);
     if (v.bias) {  // local add of the bias shares (component-wise), as a separate add would
       for (int k = 0; k < 3; ++k) t.c[k] += v.bias[k * v.bias_plane + bidx[e]];

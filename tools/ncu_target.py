@@ -4,6 +4,7 @@ python tools/ncu_target.py gemm 4096      # mpc3_ring_gemm_packed, M=N=K=n (pack
 python tools/ncu_target.py gemm_mn 4096   # the same product with A read MN-major (the engine's forward layout)
 python tools/ncu_target.py sign 16777216  # fused sign/ReLU circuit on n elements
 python tools/ncu_target.py reshare 884736 # reshare + truncate of n cross terms (an AlexNet wgrad epilogue)
+python tools/ncu_target.py sgd 0          # the AlexNet step's SGD over all parameters (one launch)
 python tools/ncu_target.py pack 4096      # dense cross-term pack, 3 parties, M=K=n
 python tools/ncu_target.py wgrad 128      # transposed-operand GEMM, AlexNet conv5 weight gradient (R=n)
 """
@@ -40,6 +41,14 @@ def main(kind, n, reps=3):
         v = _capi.make_view((1, 1, n // 256, 256))
         for _ in range(reps):
             _capi.call("mpc3_rss_reshare_truncate", p(rk), None, 0, 0, 0, 20, p(z), C.byref(v), p(out), 0, st())
+    elif kind == "sgd":  # the AlexNet-CIFAR step's one-launch SGD over every parameter (n unused)
+        import paper_2104_10949_b200 as M
+        sess = M.TrioSession(seed=0)
+        params = [sess.share(w, __import__("numpy").random.default_rng(1)) for w in
+                  M.init_params(M.alexnet_cifar(), seed=0)]
+        grads = [M.engine.RssTensor(p.data.clone()) for p in params]
+        for _ in range(reps):
+            sess.sgd_inplace(params, grads, 3)
     elif kind == "sign":
         rk = rk3()
         x = torch.randint(-(1 << 40), 1 << 40, (3 * n,), dtype=torch.int64, device="cuda")
