@@ -407,6 +407,10 @@ int mpc3_ring_gemm_auto_z(const uint8_t* A, const uint8_t* B, uint64_t* C, int g
  *   half h of group g is read from component plane (g + h) % 3, at no column
  *   offset (a_half unused; K-major: a_kp = the component pack's kp, the
  *   contraction per half kc_half); groups must be 3.
+ * b_mn = 2: B is a role-3 pack (component planes) read K-major, half h of
+ *   group g from component plane (g + h) % 3 at no column offset (b_rows = N,
+ *   b_kp >= kc_half, groups 3) — the weight gradient g^T x with x's
+ *   transposed forward pack as B.
  * a_mn = 5 (bit 2 with MN): A is a plain transposed pack (rows = the
  *   contraction) whose second half is source ROWS [a_half, a_half +
  *   kc_half), a_half >= kc_half, a_rows <= a_half + kc_half (the rest zero).

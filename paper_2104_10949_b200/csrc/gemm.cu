@@ -313,6 +313,7 @@ struct MnArgs {
   int nkb_half;        // contraction K-blocks per half
   int a_cs;            // A's halves are component planes g and g + 1 (role-3 pack of a role-1 operand)
   int a_rh;            // MN-read A whose second half is further source rows (a plain transposed pack)
+  int b_cs;            // K-major B whose halves are component planes g and g + 1 (role-3 pack)
 };
 
 DEV uint64_t umma_desc_mn(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
@@ -361,6 +362,8 @@ DEV void load_stage(const CUtensorMap* tmA, const CUtensorMap* tmB, uint64_t* ba
   }
   if (mn.b_mn)
     tma_load_3d(tmB, bar, sb, h * mn.b_half + n0, r, g * 8);
+  else if (mn.b_cs)
+    tma_load_3d(tmB, bar, sb, r, n0, ((g + h) % 3) * 8);
   else
     tma_load_3d(tmB, bar, sb, kc, n0, g * 8);
 }
@@ -759,7 +762,7 @@ int mpc3_ring_gemm_packed_layout(const uint8_t* A, const uint8_t* B, uint64_t* C
   st = make_map(&tb, B, kp, N, (int64_t)groups * 8, BN);
   if (st) return st;
   dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)(groups * splits));
-  MnArgs mn0 = {0, 0, 0, 0, 1 << 30, 0, 0};
+  MnArgs mn0 = {0, 0, 0, 0, 1 << 30, 0, 0, 0};
   launch_pdl(gemm_tc_kernel, grid, dim3(GEMM_THREADS), SMEM_BYTES, as_stream(stream), ta, tb, C, M, N, kp, ldc, c_group, splits,
              kbs, c_layout, mn0);
   return check_launch("ring_gemm_tc");
@@ -846,7 +849,10 @@ int mpc3_ring_gemm_t_z(const uint8_t* A, int a_mn, int64_t a_rows, int64_t a_kp,
                        int64_t N, int64_t kc_half, int c_layout, int c_zeroed, void* stream) {
   if (groups < 1 || M < 0 || N < 0 || kc_half < 0 || (kc_half % BK)) return MPC3_ERR_SHAPE;
   if (c_layout != 0 && c_layout != 1) return MPC3_ERR_CONFIG;
-  if (a_mn < 0 || a_mn > 5 || a_mn == 4 || b_mn < 0 || b_mn > 1) return MPC3_ERR_CONFIG;
+  if (a_mn < 0 || a_mn > 5 || a_mn == 4 || b_mn < 0 || b_mn > 2) return MPC3_ERR_CONFIG;
+  const int b_cs = b_mn >> 1;  // 2: B is a role-3 pack read K-major, half h from component plane g + h
+  b_mn &= 1;
+  if (b_cs && (groups != 3 || b_kp % 16)) return MPC3_ERR_CONFIG;
   const int a_cs = (a_mn >> 1) & 1;  // bit 1: component-plane halves (role-3 pack)
   const int a_rh = a_mn >> 2;        // bit 2 (with bit 0): half 1 is source rows [a_half, a_half + kc_half)
   a_mn &= 1;
@@ -856,7 +862,7 @@ int mpc3_ring_gemm_t_z(const uint8_t* A, int a_mn, int64_t a_rows, int64_t a_kp,
   if (M > (1 << 30) || N > (1 << 30) || a_half > (1 << 30) || b_half > (1 << 30)) return MPC3_ERR_SHAPE;
   const int64_t kp = 2 * kc_half;
   if ((!a_mn && !a_cs && (a_kp != kp || a_rows != M)) || (!a_mn && a_cs && a_rows != M) ||
-      (!b_mn && (b_kp != kp || b_rows != N)))
+      (!b_mn && !b_cs && (b_kp != kp || b_rows != N)) || (b_cs && (b_rows != N || b_kp < kc_half)))
     return MPC3_ERR_SHAPE;
   // an MN operand's half offset is a TMA box start along the 16-byte-granular
   // inner dimension (pack with mpc3_ring_pack_halves, kh % 16 == 0)
@@ -874,7 +880,7 @@ int mpc3_ring_gemm_t_z(const uint8_t* A, int a_mn, int64_t a_rows, int64_t a_kp,
                 : make_map(&ta, A, a_cs ? a_kp : kp, M, (int64_t)groups * 8, BM);
   if (st) return st;
   st = b_mn ? make_map_mn(&tb, B, b_kp, b_rows, (int64_t)groups * 8, BN, CU_TENSOR_MAP_SWIZZLE_64B)
-            : make_map(&tb, B, kp, N, (int64_t)groups * 8, BN);
+            : make_map(&tb, B, b_cs ? b_kp : kp, N, (int64_t)groups * 8, BN);
   if (st) return st;
   const int64_t nkb = kp / BK;
   const AutoPlan p = t_plan(groups, M, N, kp);
@@ -886,7 +892,7 @@ int mpc3_ring_gemm_t_z(const uint8_t* A, int a_mn, int64_t a_rows, int64_t a_kp,
       return check_launch("gemm C memset");
   }
   if (nkb == 0) return MPC3_OK;
-  MnArgs mn = {a_mn ? 1 : 0, b_mn ? 1 : 0, (int)a_half, (int)b_half, (int)(kc_half / BK), a_cs, a_rh};
+  MnArgs mn = {a_mn ? 1 : 0, b_mn ? 1 : 0, (int)a_half, (int)b_half, (int)(kc_half / BK), a_cs, a_rh, b_cs};
   dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)(groups * splits));
   launch_pdl(gemm_tc_kernel, grid, dim3(GEMM_THREADS), SMEM_BYTES, as_stream(stream), ta, tb, C, M, N, kp,
              c_layout ? M : N, M * N, (int)splits, kbs, c_layout, mn);

@@ -53,6 +53,9 @@ CS_PACKS = os.environ.get("MPC3_CS_PACKS", "1") == "1"
 # MPC3_T_PACKS=0: role-3 operands packed K-major (rows = the GEMM's rows)
 # instead of transposed (rows = the contraction), see Packed.t
 T_PACKS = os.environ.get("MPC3_T_PACKS", "1") == "1"
+# weight gradients from a transposed x pack with at least this contraction
+# per half run as g^T x (x as B, see wgrad_packed)
+WGRAD_SWAP_MIN_KC = 4096
 # MPC3_MAXTREE_FUSED=0: one launch per max_tree level instead of one for the whole tree
 MAXTREE_FUSED = os.environ.get("MPC3_MAXTREE_FUSED", "1") == "1"
 # MPC3_LOSS_FUSED=0: the loss gradient softmax(z) - y as its separate launches
@@ -765,11 +768,23 @@ class TrioSession:
         # is the same memory and keeps the epilogue's stores coalesced
         M, N, kc = (xp.rows if xp.t else xp.k), o, _round_up(rows, 32)
         z = torch.empty(3 * M * N, dtype=torch.int64, device=_dev())
+        if xp.t and xp.kp < kc:
+            raise ShapeError("transposed pack narrower than the contraction")
+        if xp.t and kc >= WGRAD_SWAP_MIN_KC:
+            # x packed transposed in the forward pass (its rows are (c, u, v)),
+            # long contraction: computed as g^T x with g's pack as the MN-read A
+            # and x's pack as a component-plane K-major B (b_mn = 2), row-major
+            # [O][(c, u, v)] — the same memory as the column-major x^T g below
+            # (AlexNet conv1, kc = 12,800: 99 -> 86 us; the short-contraction
+            # weight gradients of conv2-5 are 20-35 % slower this way)
+            zeroed = self._needs_zero(True, N, M, 2 * kc)
+            gp = self.pack(g.data, op, rows, o, 0, zero=z if zeroed else None)
+            K.call("mpc3_ring_gemm_t_z", gp.buf.data_ptr(), 1, gp.rows, gp.kp, gp.kh, xp.buf.data_ptr(), 2, M, xp.kp,
+                   0, z.data_ptr(), 3, N, M, kc, 0, 1 if zeroed else 0, _stream())
+            return z
         zeroed = self._needs_zero(True, M, N, 2 * kc)
         gp = self.pack(g.data, op, rows, o, 0, zero=z if zeroed else None)
-        if xp.t:  # x packed transposed in the forward pass: its rows are this GEMM's rows, read K-major
-            if xp.kp < kc:
-                raise ShapeError("transposed pack narrower than the contraction")
+        if xp.t:  # the transposed x pack's rows are this GEMM's rows: read K-major
             K.call("mpc3_ring_gemm_t_z", xp.buf.data_ptr(), 2, M, xp.kp, 0, gp.buf.data_ptr(), 1, gp.rows, gp.kp,
                    gp.kh, z.data_ptr(), 3, M, N, kc, 1, 1 if zeroed else 0, _stream())
             return z
