@@ -5,6 +5,7 @@ python tools/ncu_target.py gemm_mn 4096   # the same product with A read MN-majo
 python tools/ncu_target.py sign 16777216  # fused sign/ReLU circuit on n elements
 python tools/ncu_target.py reshare 884736 # reshare + truncate of n cross terms (an AlexNet wgrad epilogue)
 python tools/ncu_target.py sgd 0          # the AlexNet step's SGD over all parameters (one launch)
+python tools/ncu_target.py poolbwd 128    # AlexNet conv1's avg-pool backward + ReLU mask at batch n
 python tools/ncu_target.py pack 4096      # dense cross-term pack, 3 parties, M=K=n
 python tools/ncu_target.py wgrad 128      # transposed-operand GEMM, AlexNet conv5 weight gradient (R=n)
 """
@@ -49,6 +50,15 @@ def main(kind, n, reps=3):
         grads = [M.engine.RssTensor(p.data.clone()) for p in params]
         for _ in range(reps):
             sess.sgd_inplace(params, grads, 3)
+    elif kind == "poolbwd":  # AlexNet conv1's avg-pool backward + ReLU mask (batch n), one launch
+        rk = rk3()
+        N, Cc, H, W, OH, OW = n, 96, 10, 10, 4, 4
+        g = torch.randint(-(1 << 40), 1 << 40, (3 * N * Cc * OH * OW,), dtype=torch.int64, device="cuda")
+        m = torch.randint(0, 2, (3 * N * Cc * H * W,), dtype=torch.int64, device="cuda")
+        out = torch.empty_like(m)
+        for _ in range(reps):
+            _capi.call("mpc3_rss_avgpool_backward_mask", p(rk), None, 0, 0, 20, 7282, p(g), p(m), 0, p(out), N, Cc, H, W,
+                       OH, OW, 3, 3, 2, 2, 0, 0, 0, st())
     elif kind == "sign":
         rk = rk3()
         x = torch.randint(-(1 << 40), 1 << 40, (3 * n,), dtype=torch.int64, device="cuda")
