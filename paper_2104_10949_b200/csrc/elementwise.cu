@@ -792,7 +792,7 @@ __global__ void __launch_bounds__(Proto<F>::threads, Proto<F>::min_ctas) sgd_ker
   const int nc = F ? imin32(tb.nt, kHeadSlots4 / 2) : 0;
   StreamHead* hs = reinterpret_cast<StreamHead*>(reinterpret_cast<AesSmem4*>(mpc3_dsm)->extra);
   static_assert(sizeof(StreamHead) * kHeadSlots4 <= sizeof(AesSmem4::extra), "SGD heads fit the extra area");
-  if (nc) {
+  if constexpr (F) {
     HeadConst* slots = Proto<F>::slots();
     if (threadIdx.x < 2 * nc) {
       const MPC3SgdTensor& T = tb.t[threadIdx.x >> 1];
@@ -1149,6 +1149,12 @@ static int sign2_smem_max(bool rs = false) {  // the largest chunk a launch uses
 
 // The sign circuit over n elements (x, or a fused layer's cross terms rin):
 // whole rounds of the persistent single-phase kernel, the rest two-phase.
+#ifndef MPC3_SIGN_ROUND_PCT
+#define MPC3_SIGN_ROUND_PCT 72
+#endif
+#ifndef MPC3_SIGN_ROUND_RS_PCT
+#define MPC3_SIGN_ROUND_RS_PCT 55
+#endif
 static int sign_launch(const KeySched& ks, const uint64_t* ctr, const SignArgs& a, int mode, const uint64_t* x,
                        const RsIn* rin, uint64_t* out, uint64_t* mask, uint64_t n, uint64_t n_total,
                        uint64_t elem_off, void* stream) {
@@ -1162,13 +1168,15 @@ static int sign_launch(const KeySched& ks, const uint64_t* ctr, const SignArgs& 
   const uint64_t persist = 148ull * kSignThreads;
   uint64_t main_pairs = 0;
   if (!g_sign_fused) {
-    // whole rounds of the persistent grid (one pair per thread per round; a
-    // lone pair's 46 dependent AES blocks take ~55 us, so tensors below one
-    // round go to the two-phase kernel entirely); a remainder above half a
-    // round costs more in the two-phase kernel than one more pair for part of
-    // the persistent threads
+    // whole rounds of the persistent grid (one pair per thread per round,
+    // ~50 us a round full or not), the remainder in the two-phase kernel
+    // (~8 us + 57 us x the fraction of a round; 85 us with the fused layer
+    // epilogue) — unless the remainder is large enough that one more
+    // persistent round is cheaper (tools/dbg/sign_sizes.py), also for
+    // tensors below one round
     main_pairs = pairs / persist * persist;
-    if (main_pairs && (pairs - main_pairs) * 2 > persist) main_pairs = pairs;
+    const uint64_t rem = pairs - main_pairs;
+    if (rem * 100 >= persist * (rs ? MPC3_SIGN_ROUND_RS_PCT : MPC3_SIGN_ROUND_PCT)) main_pairs = pairs;
   }
   if (g_sign_fused) main_pairs = pairs;
   if (main_pairs) {
