@@ -248,6 +248,16 @@ int mpc3_rss_layer_sign(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_ra,
                         int bits, const uint64_t* z, const mpc3_view4* view, const uint64_t* bias, int64_t bias_plane,
                         int bias_dim, int mode, uint64_t j_bin, uint64_t j_xor, uint64_t j_arith, uint64_t* out,
                         uint64_t* mask, uint64_t elem_off, uint64_t n_total, void* stream);
+/* Same with a residual block's shortcut added after the bias (the local add
+ * of the inference extension's residual layer before its ReLU): element f of
+ * the view gets res[k * res_plane + f] in component k (res_plane >= n).  The
+ * caller takes the counters in the unfused order (the layer's reshare and
+ * truncation before the shortcut branch, the ReLU's after). */
+int mpc3_rss_layer_sign_residual(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_ra, uint64_t j_rho,
+                                 uint64_t j_r, int bits, const uint64_t* z, const mpc3_view4* view,
+                                 const uint64_t* bias, int64_t bias_plane, int bias_dim, const uint64_t* res,
+                                 int64_t res_plane, int mode, uint64_t j_bin, uint64_t j_xor, uint64_t j_arith,
+                                 uint64_t* out, uint64_t* mask, uint64_t elem_off, uint64_t n_total, void* stream);
 
 /* Input gradient epilogue (nn.py:460-484): z holds per-party cross terms
  * cols[(n,y,x), (c,a,b)] = sum_o g[n,o,y,x] k[o,c,a,b] (a GEMM with inner

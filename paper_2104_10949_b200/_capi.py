@@ -173,6 +173,8 @@ _SIGS = {
     "mpc3_rss_max_tree": (C.c_int, [_P, _P, C.c_int, _P, _P, _P, _P, _P, _P, _U64, _U64, _U64, _U64, _P]),
     "mpc3_rss_layer_sign": (C.c_int, [_P, _P, _U64, _U64, _U64, C.c_int, _P, C.POINTER(View4), _P, _I64, C.c_int,
                                       C.c_int, _U64, _U64, _U64, _P, _P, _U64, _U64, _P]),
+    "mpc3_rss_layer_sign_residual": (C.c_int, [_P, _P, _U64, _U64, _U64, C.c_int, _P, C.POINTER(View4), _P, _I64,
+                                               C.c_int, _P, _I64, C.c_int, _U64, _U64, _U64, _P, _P, _U64, _U64, _P]),
     "mpc3_rss_sgd_multi": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, _U64, _P]),
     "mpc3_rss_softmax_loss_scratch": (C.c_size_t, [_U64, _U64]),
     "mpc3_rss_softmax_loss": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _U64, _U64, _P]),

@@ -1228,7 +1228,17 @@ int mpc3_rss_layer_sign(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_ra,
                         int bits, const uint64_t* z, const mpc3_view4* view, const uint64_t* bias, int64_t bias_plane,
                         int bias_dim, int mode, uint64_t j_bin, uint64_t j_xor, uint64_t j_arith, uint64_t* out,
                         uint64_t* mask, uint64_t elem_off, uint64_t n_total, void* stream) {
+  return mpc3_rss_layer_sign_residual(rk3, ctr, j_ra, j_rho, j_r, bits, z, view, bias, bias_plane, bias_dim, nullptr, 0,
+                                      mode, j_bin, j_xor, j_arith, out, mask, elem_off, n_total, stream);
+}
+
+int mpc3_rss_layer_sign_residual(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_ra, uint64_t j_rho,
+                                 uint64_t j_r, int bits, const uint64_t* z, const mpc3_view4* view,
+                                 const uint64_t* bias, int64_t bias_plane, int bias_dim, const uint64_t* res,
+                                 int64_t res_plane, int mode, uint64_t j_bin, uint64_t j_xor, uint64_t j_arith,
+                                 uint64_t* out, uint64_t* mask, uint64_t elem_off, uint64_t n_total, void* stream) {
   if (mode < MODE_A2B || mode > MODE_RELU) return MPC3_ERR_CONFIG;
+  if (res && res_plane < 0) return MPC3_ERR_CONFIG;
   if (bits < 1 || bits > 61) return MPC3_ERR_RANGE;
   if (bias && (bias_dim < 0 || bias_dim > 3 || bias_plane < 0)) return MPC3_ERR_CONFIG;
   if (!view || !z || (elem_off & 1)) return MPC3_ERR_CONFIG;
@@ -1252,6 +1262,9 @@ int mpc3_rss_layer_sign(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_ra,
   ri.v.bias_plane = bias_plane;
   ri.v.bias_dim = bias_dim;
   ri.small = n < (1ull << 32) ? 1 : 0;
+  ri.res = res;
+  ri.res_plane = (uint64_t)res_plane;
+  if (res && (uint64_t)res_plane < n) return MPC3_ERR_SHAPE;
   if (elem_off + n > n_total) return MPC3_ERR_SHAPE;
   if (j_bin >= (1ull << 48) || j_xor + 6 >= (1ull << 48) || j_arith + 2 >= (1ull << 48) || j_ra >= (1ull << 48) ||
       j_rho >= (1ull << 48) || j_r >= (1ull << 48))

@@ -168,6 +168,8 @@ struct RsIn {
   int bits;
   uint64_t f0;  // flat index (in v) of the launch's element 0
   int small;    // the view's element count fits 32 bits
+  const uint64_t* res;  // optional residual trio added after the bias (element f at res[k * res_plane + f])
+  uint64_t res_plane;
 };
 template <class I>
 HD void view_index(const View4& v, uint64_t f, int64_t& i0, int64_t& i1, int64_t& i2, int64_t& i3) {
@@ -196,6 +198,8 @@ HD Trio reshare_input(const RsIn& in, uint64_t f, const uint64_t kw[3], uint64_t
     const int64_t bi = v.bias_dim == 0 ? i0 : v.bias_dim == 1 ? i1 : v.bias_dim == 2 ? i2 : i3;
     for (int k = 0; k < 3; ++k) t.c[k] += v.bias[k * v.bias_plane + bi];
   }
+  if (in.res)  // a residual block's shortcut, a local add before its ReLU
+    for (int k = 0; k < 3; ++k) t.c[k] += in.res[k * in.res_plane + f];
   return t;
 }
 

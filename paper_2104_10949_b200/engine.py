@@ -931,21 +931,43 @@ class TrioSession:
         """_finish followed by relu_with_mask in ONE launch (mpc3_rss_layer_sign):
         the same counters in the same order, the same shares and accounting;
         the pre-activation tensor is never materialised.  -> (relu, mask)."""
+        return self.relu_epilogue_end(self.relu_epilogue_begin(z, view, shape, bits, label, bias, bias_dim))
+
+    def relu_epilogue_begin(self, z, view, shape, bits, label, bias: RssTensor | None = None, bias_dim: int = 1):
+        """First half of _finish_relu: the layer epilogue's counters (reshare,
+        truncation) and accounting, taken here in program order; the launch
+        waits for relu_epilogue_end, so a residual block's shortcut branch
+        can run (and take its own counters) in between."""
+        if bias is not None and (bias.ndim != 1 or bias.data.stride(1) != 1):
+            raise ShapeError("bias must be a 1-d shared vector with unit stride")
         ja = self.take(ARITH)
         jr, jq = self.take(TR_RHO), self.take(TR_R)
+        full = int(np.prod(view.full))
+        self.ledger.ring(label, full)
+        self._charge_trunc(full)
+        return {"z": z, "view": view, "shape": shape, "bits": bits, "bias": bias, "bias_dim": bias_dim,
+                "ja": ja, "jr": jr, "jq": jq, "full": full}
+
+    def relu_epilogue_end(self, pend: dict, residual: RssTensor | None = None):
+        """Second half: the ReLU's counters, then ONE launch of the layer's
+        reshare + truncate (+ bias) (+ the residual shortcut, a local add) and
+        the ReLU (mpc3_rss_layer_sign_residual).  -> (relu, mask)."""
         jb = self.take(BIN)
         jx = self.take(XOR, 7)
         jm = self.take(ARITH, 3)
-        full = int(np.prod(view.full))
+        full, shape, bias, view = pend["full"], pend["shape"], pend["bias"], pend["view"]
         off, n_total = self.shard_offset(full)
         out, mask = empty(shape, self.fp), empty(shape, self.fp)
-        if bias is not None and (bias.ndim != 1 or bias.data.stride(1) != 1):
-            raise ShapeError("bias must be a 1-d shared vector with unit stride")
-        K.call("mpc3_rss_layer_sign", self.rk, self.ctr_ptr, ja, jr, jq, bits, z.data_ptr(), C.byref(view),
-               None if bias is None else bias.data.data_ptr(), 0 if bias is None else bias.data.stride(0), bias_dim,
-               K.MODE_RELU, jb, jx, jm, out.data.data_ptr(), mask.data.data_ptr(), off, n_total, _stream())
-        self.ledger.ring(label, full)
-        self._charge_trunc(full)
+        res = None
+        if residual is not None:
+            if tuple(residual.shape) != tuple(shape):
+                raise ShapeError(f"residual {tuple(residual.shape)} does not match the layer output {tuple(shape)}")
+            res = residual.data.contiguous()
+        K.call("mpc3_rss_layer_sign_residual", self.rk, self.ctr_ptr, pend["ja"], pend["jr"], pend["jq"],
+               pend["bits"], pend["z"].data_ptr(), C.byref(view), None if bias is None else bias.data.data_ptr(),
+               0 if bias is None else bias.data.stride(0), pend["bias_dim"], None if res is None else res.data_ptr(),
+               0 if res is None else res.stride(0), K.MODE_RELU, jb, jx, jm, out.data.data_ptr(),
+               mask.data.data_ptr(), off, n_total, _stream())
         self._charge_sign(full, K.MODE_RELU)
         return out, mask
 
@@ -1042,6 +1064,8 @@ class TrioSession:
         # z[(n, y, x), o]: column-major keeps each (n, o) plane's (y, x) run contiguous
         zs = (oh * ow, M, ow, 1) if col else (oh * ow * o, 1, ow * o, o)
         view = K.make_view((nb, o, oh, ow), z_stride=zs)
+        if relu == "defer":  # the epilogue's counters now, the fused launch later (relu_epilogue_end)
+            return self.relu_epilogue_begin(z, view, (nb, o, oh, ow), bits, "mul.reshare", bias=bias, bias_dim=1)
         if relu:  # fused with the ReLU after it: -> (relu, mask)
             return self._finish_relu(z, view, (nb, o, oh, ow), bits, "mul.reshare", bias=bias, bias_dim=1)
         return self._finish(z, view, out, bits, "mul.reshare", bias=bias, bias_dim=1)

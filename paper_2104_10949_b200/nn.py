@@ -52,6 +52,9 @@ FUSE_RELU = os.environ.get("MPC3_FUSE_RELU", "1") == "1"
 # (two more keystream slots, smaller chunks) does not (AlexNet step: fused
 # everywhere 2.559 ms, from 100 K elements 2.530 ms, never 2.541 ms)
 FUSE_RELU_MIN = int(os.environ.get("MPC3_FUSE_RELU_MIN", "100000"))  # output elements
+# MPC3_FUSE_RESIDUAL=0: a residual block's last conv, shortcut add and ReLU as three launches
+FUSE_RESIDUAL = os.environ.get("MPC3_FUSE_RESIDUAL", "1") == "1"
+FUSE_RESIDUAL_MAX = 4 << 20  # block input elements
 # train_trio replays a CUDA graph once this many iterations remain (the
 # capture's host cost pays off after ~80 AlexNet steps: eager 4.4 ms vs
 # replay 2.5 ms per step, capture ~170 ms)
@@ -345,9 +348,26 @@ class TrioNet:
                 acts.append((shp,) if record else None)
                 h = h.contiguous().reshape(shp[0], -1)
             elif spec.kind == RESIDUAL:
-                hm = self._run(spec.main, it, h, False)[0] if spec.main else h
-                hs = self._run(spec.shortcut, it, h, False)[0] if spec.shortcut else h
-                h = S.add(hm, hs)
+                last = spec.main[-1] if spec.main else None
+                if FUSE_RESIDUAL and li + 1 < len(layers) and layers[li + 1].kind == RELU and last is not None \
+                        and last.kind == CONV2D and h.numel <= FUSE_RESIDUAL_MAX:
+                    # the main branch's last conv, the shortcut add and the ReLU
+                    # after the block in one launch (mpc3_rss_layer_sign_residual);
+                    # counters in the unfused order: the conv's epilogue, then
+                    # the shortcut branch, then the ReLU.  (ResNet-50 b1 138.4 ->
+                    # 139.4 img/s; at b64 the fused epilogue in the persistent
+                    # sign kernel is slower than the separate reshare: 186.9 ->
+                    # 186.4, so large blocks stay unfused.)
+                    hm = self._run(spec.main[:-1], it, h, False)[0] if len(spec.main) > 1 else h
+                    k = next(it)
+                    pend = S.conv2d(hm, k, last.stride, last.padding, bias=next(it) if last.bias else None,
+                                    relu="defer")
+                    hs = self._run(spec.shortcut, it, h, False)[0] if spec.shortcut else h
+                    h, fused = S.relu_epilogue_end(pend, residual=hs)
+                else:
+                    hm = self._run(spec.main, it, h, False)[0] if spec.main else h
+                    hs = self._run(spec.shortcut, it, h, False)[0] if spec.shortcut else h
+                    h = S.add(hm, hs)
                 acts.append(("residual",) if record else None)
         return h, acts
 

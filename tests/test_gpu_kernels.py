@@ -159,6 +159,32 @@ def test_sign_single_phase_equals_two_phase_shards(n):
         assert np.array_equal(host(mk).reshape(3, m), host(fmask).reshape(3, n)[:, a:b])
 
 
+@pytest.mark.parametrize("shape", [(2, 64, 7, 7), (1, 256, 14, 14), (3, 5, 7, 9)])
+def test_layer_sign_residual_equals_reshare_add_sign(shape):
+    """mpc3_rss_layer_sign_residual = reshare/truncate + bias, the shortcut's
+    local add, then the ReLU, share for share (a residual block's tail)."""
+    rng = np.random.default_rng(7 + sum(shape))
+    nb, o, oh, ow = shape
+    n = nb * o * oh * ow
+    M = nb * oh * ow
+    z = dev(rnd(rng, (3, n)))
+    view = _capi.make_view(shape, z_stride=(oh * ow, M, ow, 1))
+    bv = dev(rnd(rng, (3, o)))
+    res = dev(rnd(rng, (3, n)))
+    rk = rk3(R.Session(8).keys)
+    x = torch.empty(3 * n, dtype=torch.int64, device="cuda")
+    _capi.call("mpc3_rss_reshare_truncate_bias", p(rk), None, 11, 12, 13, 20, p(z), C.byref(view), p(bv), o, 1, p(x),
+               0, stream())
+    x += res.reshape(-1)
+    out1, m1 = torch.empty_like(x), torch.empty_like(x)
+    _capi.call("mpc3_rss_sign", p(rk), None, 3, 4, 5, 6, p(x), p(out1), p(m1), n, n, 0, stream())
+    out2, m2 = torch.full_like(x, -1), torch.full_like(x, -1)
+    _capi.call("mpc3_rss_layer_sign_residual", p(rk), None, 11, 12, 13, 20, p(z), C.byref(view), p(bv), o, 1, p(res),
+               n, 3, 4, 5, 6, p(out2), p(m2), 0, n, stream())
+    assert np.array_equal(host(out2), host(out1))
+    assert np.array_equal(host(m2), host(m1))
+
+
 @pytest.mark.parametrize("shape,bias,shard", [((128, 96, 10, 10), False, None), ((128, 96, 10, 10), True, None),
                                               ((3, 5, 7, 9), True, None), ((64, 256, 1, 1), False, None),
                                               ((1, 1, 128, 257), True, None), ((40, 7, 33, 33), False, (2, 3))])
