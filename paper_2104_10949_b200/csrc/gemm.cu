@@ -713,7 +713,14 @@ int mpc3_ring_pack_halves_z(const uint64_t* src, int64_t src_plane, const mpc3_o
       a.W = (int32_t)o.w;
       a.sH = (int32_t)o.sH;
       a.sW = (int32_t)o.sW;
-      r_fast = o.mode == MPC3_GATHER_IM2COL && o.sw <= 2;  // strided windows: walk the kernel row (contiguous input x)
+      // walk the direction whose consecutive elements are closest in the
+      // source: an im2col row's columns (c, u, v) run along the kernel row
+      // (contiguous x), its rows (n, y, x) step by the stride; the transposed
+      // (WGRAD-layout) pack has them the other way round
+#ifndef MPC3_PACK_T_RFAST_SW
+#define MPC3_PACK_T_RFAST_SW 3
+#endif
+      r_fast = o.mode == MPC3_GATHER_IM2COL ? o.sw <= 2 : o.sw >= MPC3_PACK_T_RFAST_SW;
     }
     dim3 grid((unsigned)((kp + PT_K - 1) / PT_K), (unsigned)row_tiles, (unsigned)groups);
     void (*k)(const uint64_t*, int64_t, Operand, PackTileArgs, uint8_t*) =
