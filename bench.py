@@ -240,7 +240,8 @@ class NvmlClocks(Clocks):
 # -- per-launch instrumentation (outside every timed region) ------------------
 
 GEMM_CALLS = ("mpc3_ring_gemm_auto", "mpc3_ring_gemm_auto_z", "mpc3_ring_gemm_t", "mpc3_ring_gemm_t_z")
-SIGN_CALLS = ("mpc3_rss_sign", "mpc3_rss_layer_sign", "mpc3_rss_max_tree", "mpc3_rss_max_level")
+SIGN_CALLS = ("mpc3_rss_sign", "mpc3_rss_layer_sign", "mpc3_rss_layer_sign_residual", "mpc3_rss_max_tree",
+              "mpc3_rss_max_level")
 PACK_CALLS = ("mpc3_ring_pack", "mpc3_ring_pack_halves", "mpc3_ring_pack_halves_z", "mpc3_rss_window_gather")
 
 
@@ -305,7 +306,7 @@ class Recorder:
     def _work(self, name, a):
         if name == "mpc3_rss_sign":
             return 23.0 * int(a[9]), (int(a[9]),)
-        if name == "mpc3_rss_layer_sign":
+        if name in ("mpc3_rss_layer_sign", "mpc3_rss_layer_sign_residual"):
             n = _view_numel(a[7])
             return 25.5 * n, (n,)
         if name == "mpc3_rss_max_level":
@@ -553,6 +554,8 @@ def run_b200(args, ws, rank, local):
     if ws > 1:
         torch.distributed.barrier()
     clocks = Clocks(local)
+    switch = sys.getswitchinterval()
+    sys.setswitchinterval(1e-4)  # the clock sampler thread runs during the short timed region
     step_ms = []
     for i in range(args.steps):
         flush.zero_()
@@ -567,6 +570,7 @@ def run_b200(args, ws, rank, local):
         step_ms.append(e0.elapsed_time(e1))
     torch.cuda.synchronize()
     clk = clocks.stop()
+    sys.setswitchinterval(switch)
     launches = launches_per_step * args.steps
     total_ms = float(sum(step_ms))
     if ws > 1:
