@@ -714,7 +714,8 @@ def side_measurements(dev, ws, rank, rec, peaks, sm_mhz, args) -> dict:
     also = {}
     for key, fn in (("lenet_b64", lambda: lenet_inference(dev)), ("vgg16_ti_b32", lambda: vgg16_ti(dev)),
                     ("resnet50_b64", lambda: resnet50_inference(dev, 64, 3, rec=rec, peaks=peaks, sm_mhz=sm_mhz)),
-                    ("resnet50_b1", lambda: resnet50_inference(dev, 1, 10))):
+                    ("resnet50_b1", lambda: resnet50_inference(dev, 1, 10)),
+                    ("ring_gemm", lambda: ring_gemm_sweep(dev))):
         try:
             also[key] = fn()
         except Exception as e:  # noqa: BLE001 - reported, not fatal to the headline
@@ -746,6 +747,54 @@ def side_measurements(dev, ws, rank, rec, peaks, sm_mhz, args) -> dict:
     return also
 
 
+def ring_gemm_sweep(dev, sizes=(1024, 2048, 4096)) -> dict:
+    """The ring GEMM (BASELINE.json's "ring-GEMM TOPS", configs[4]) at M = N = K
+    = n on random packed limb planes in the engine's layout (A read MN-major
+    from a transposed pack, B K-major: mpc3_ring_gemm_t), L2 flushed before
+    each timed launch; 72 int8 ops per ring MAC; cuBLASLt int8
+    (torch._int_mm) at the largest n for context."""
+    import torch
+
+    from paper_2104_10949_b200 import _capi
+
+    st = torch.cuda.current_stream().cuda_stream
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def timed(fn, iters):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(iters):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1) / 1e3)
+        return float(np.median(ts))
+
+    out = {"layout": "A MN-major (transposed pack, SWIZZLE_128B), B K-major; L2 flushed per launch", "sizes": []}
+    for n in sizes:
+        kc = n // 2
+        at = torch.randint(0, 256, (8 * kc * 2 * n,), dtype=torch.uint8, device=dev)
+        b = torch.randint(0, 256, (8 * n * n,), dtype=torch.uint8, device=dev)
+        c = torch.empty(n * n, dtype=torch.int64, device=dev)
+        s = timed(lambda: _capi.call("mpc3_ring_gemm_t", at.data_ptr(), 1, kc, 2 * n, n, b.data_ptr(), 0, n, n, 0,
+                                     c.data_ptr(), 1, n, n, kc, 0, st), 5)
+        out["sizes"].append({"n": n, "ms": s * 1e3, "int8_tops": 72 * n ** 3 / s / 1e12, "ring_tops": 2 * n ** 3 / s / 1e12})
+        del at, b, c
+    n = sizes[-1]
+    try:
+        a8 = torch.randint(-128, 127, (n, n), dtype=torch.int8, device=dev)
+        b8 = torch.randint(-128, 127, (n, n), dtype=torch.int8, device=dev).t().contiguous().t()
+        s = timed(lambda: torch._int_mm(a8, b8), 5)
+        out["cublaslt_int8"] = {"n": n, "tops": 2 * n ** 3 / s / 1e12}
+    except Exception as e:  # noqa: BLE001
+        out["cublaslt_int8"] = {"error": repr(e)[:200]}
+    return out
+
+
 def _side_cpu_baselines(also):
     """The reference's CPU path for the side configs (refarm.py): LeNet b64
     infer_private; ResNet-50 b1 composed from its per-party protocols (b64
@@ -773,6 +822,23 @@ def _side_cpu_baselines(also):
                                                     note="extrapolated: b1 per-image time x 64 (linear in batch)")
     except Exception as e:  # noqa: BLE001
         also["resnet50_b1"]["cpu_baseline"] = {"error": repr(e)[:200]}
+    if isinstance(also.get("ring_gemm"), dict) and "sizes" in also["ring_gemm"]:
+        try:  # the reference's bilinear_exact (ring.py:183-222) at n = 2048 (tests/test_ring.py inputs)
+            from mpc3.ring import bilinear_exact, matmul_spec
+
+            n = 2048
+            rng = np.random.default_rng(n)
+            a = rng.integers(0, 1 << 64, (n, n), dtype=np.uint64)
+            b = rng.integers(0, 1 << 64, (n, n), dtype=np.uint64)
+            bilinear_exact(a[:64, :64], b[:64, :64], matmul_spec(64, 64, 64))
+            t0 = time.perf_counter()
+            bilinear_exact(a, b, matmul_spec(n, n, n))
+            dt = time.perf_counter() - t0
+            also["ring_gemm"]["cpu_baseline"] = {"value": 2 * n ** 3 / dt / 1e12, "unit": "ring-TOPS (2 ops per ring MAC)",
+                                                 "cores": th["cores"], "kind": "reference",
+                                                 "sample": f"mpc3.ring.bilinear_exact, M = N = K = {n}, one call"}
+        except Exception as e:  # noqa: BLE001
+            also["ring_gemm"]["cpu_baseline"] = {"error": repr(e)[:200]}
 
 
 def lenet_inference(dev, batch: int = 64, steps: int = 5):
@@ -897,7 +963,16 @@ def resnet50_inference(dev, batch: int, steps: int, rec=None, peaks=None, sm_mhz
         net = TrioNet(sess)
         _instrumented(lambda: net.forward(model, params, x, record=False), rec, torch)
         summ = rec.summary(t)
-        out["roofline"] = roofline_of(rec, summ, peaks or {}, sm_mhz, _traffic("resnet50_b64" if batch == 64 else ""))
+        rf = roofline_of(rec, summ, peaks or {}, sm_mhz, _traffic("resnet50_b64" if batch == 64 else ""))
+        # compact (the whole line must survive the driver's stdout tail): the
+        # headline's roofline carries the long-form fields
+        keep = ("kernel", "bound", "achieved", "peak", "unit", "frac", "traffic", "launches", "share_of_step",
+                "kernel_time_by_category")
+        out["roofline"] = {k: rf[k] for k in keep if k in rf}
+        out["roofline"]["top_launches"] = rf.get("top_launches", [])[:3]
+        if "secondary" in rf:
+            out["roofline"]["secondary"] = {k: rf["secondary"][k] for k in ("kernel", "achieved", "unit", "frac")
+                                            if k in rf["secondary"]}
         rec.events.clear()
     return out
 
