@@ -6,6 +6,7 @@ python tools/ncu_target.py sign 16777216  # fused sign/ReLU circuit on n element
 python tools/ncu_target.py reshare 884736 # reshare + truncate of n cross terms (an AlexNet wgrad epilogue)
 python tools/ncu_target.py sgd 0          # the AlexNet step's SGD over all parameters (one launch)
 python tools/ncu_target.py poolbwd 128    # AlexNet conv1's avg-pool backward + ReLU mask at batch n
+python tools/ncu_target.py layersign 128  # AlexNet conv1's fused reshare + truncate + ReLU at batch n
 python tools/ncu_target.py pack 4096      # dense cross-term pack, 3 parties, M=K=n
 python tools/ncu_target.py wgrad 128      # transposed-operand GEMM, AlexNet conv5 weight gradient (R=n)
 """
@@ -65,6 +66,16 @@ def main(kind, n, reps=3):
         y, m = torch.empty_like(x), torch.empty_like(x)
         for _ in range(reps):
             _capi.call("mpc3_rss_sign", p(rk), None, 3, 0, 0, 0, p(x), p(y), p(m), n, n, 0, st())
+    elif kind == "layersign":  # AlexNet conv1's fused reshare + truncate + ReLU (batch n): column-major z view
+        rk = rk3()
+        nb, o, oh, ow = n, 96, 10, 10
+        m = nb * oh * ow
+        z = torch.randint(-(1 << 62), 1 << 62, (3 * nb * o * oh * ow,), dtype=torch.int64, device="cuda")
+        y, mk = torch.empty_like(z), torch.empty_like(z)
+        v = _capi.make_view((nb, o, oh, ow), z_stride=(oh * ow, m, ow, 1))
+        for _ in range(reps):
+            _capi.call("mpc3_rss_layer_sign", p(rk), None, 1, 2, 3, 20, p(z), C.byref(v), None, 0, 1, 3, 4, 5, 6,
+                       p(y), p(mk), 0, nb * o * oh * ow, st())
     elif kind == "pack":
         x = torch.randint(-(1 << 62), 1 << 62, (3 * n * n,), dtype=torch.int64, device="cuda")
         kp = 2 * n
