@@ -646,6 +646,8 @@ def _e2e(args, ws, dev, sess, st, graph, xs_static, ys_static, imgs, labels, b):
     rng = st.rng
     onehot = one_hot(labels, 10)
 
+    held = [None] * nbuf  # slot k's dealt shares, alive until the slot comes round again
+
     def e2e_step(i):
         k = i % nbuf
         if done[k] is not None:  # slot free: step i-2's logits are on the host
@@ -653,17 +655,20 @@ def _e2e(args, ws, dev, sess, st, graph, xs_static, ys_static, imgs, labels, b):
             results.append(out_host[k].numpy().view(np.uint64).copy())
         pin_img[k].numpy()[...] = imgs
         pin_lab[k].numpy()[...] = onehot
+        main = torch.cuda.current_stream()
+        # copy in, encode and deal on the copy stream, beside the previous
+        # step's graph (the dealer's draws are host-ordered: same shares)
         with torch.cuda.stream(copy_stream):
             dev_img[k].copy_(pin_img[k], non_blocking=True)
             dev_lab[k].copy_(pin_lab[k], non_blocking=True)
-            h2d = torch.cuda.Event()
-            h2d.record(copy_stream)
-        main = torch.cuda.current_stream()
-        main.wait_event(h2d)
-        x_enc = sess.fx_encode_device(dev_img[k], bad)
-        y_enc = sess.fx_encode_device(dev_lab[k], bad)
-        xs_static.data.copy_(sess.share_device(x_enc, rng).data)
-        ys_static.data.copy_(sess.share_device(y_enc, rng).data)
+            x_enc = sess.fx_encode_device(dev_img[k], bad)
+            y_enc = sess.fx_encode_device(dev_lab[k], bad)
+            held[k] = (sess.share_device(x_enc, rng), sess.share_device(y_enc, rng))
+            dealt = torch.cuda.Event()
+            dealt.record(copy_stream)
+        main.wait_event(dealt)
+        xs_static.data.copy_(held[k][0].data)
+        ys_static.data.copy_(held[k][1].data)
         logits = graph.replay()
         out_host[k].copy_(engine.reconstruct_device(logits).view(b, 10), non_blocking=True)
         done[k] = torch.cuda.Event()
@@ -699,9 +704,9 @@ def _e2e(args, ws, dev, sess, st, graph, xs_static, ys_static, imgs, labels, b):
             "d2h_bytes_per_step": int(out_host[0].numel() * 8),
             "api": "the trio engine API (INTEGRATION.md §2: TrainState + GraphStep) with host-resident inputs; "
                    "the per-party drop-in run_in_process + train_private call is also.dropin_train_private",
-            "note": "per step: host images+labels into pinned memory, H2D on a copy stream (double-buffered, "
-                    "overlapping the previous step), device fx-encode, device PCG64 dealer (bit-exact with "
-                    "sharing.py:113-118), graph step, opened logits D2H read on the host; wall clock"}
+            "note": "per step: host images+labels into pinned memory, H2D + device fx-encode + device PCG64 dealer "
+                    "(bit-exact with sharing.py:113-118) on a copy stream (double-buffered, overlapping the "
+                    "previous step's graph), graph step, opened logits D2H read on the host; wall clock"}
 
 
 # ---------------------------------------------------------------------------
