@@ -135,6 +135,22 @@ def test_sign_modes(n):
     assert np.array_equal(host(mask).reshape(3, n), rm)
 
 
+# one persistent round = 148 x 384 pairs; a remainder of >= 72 % of a round
+# takes one more persistent round, below that the two-phase kernel
+# (elementwise.cu sign_launch): sizes either side of both policies' edges
+@pytest.mark.parametrize("n", [81836, 81841, 113664 + 81836, 113664 + 81843])
+def test_relu_partial_round_edges_vs_oracle(n):
+    rng = np.random.default_rng(n)
+    xs = R.share(rnd(rng, n), rng)
+    rk = rk3(R.Session(10).keys)
+    out = torch.empty(3 * n, dtype=torch.int64, device="cuda")
+    mask = torch.empty(3 * n, dtype=torch.int64, device="cuda")
+    _capi.call("mpc3_rss_sign", p(rk), None, 3, 0, 0, 0, p(dev(xs)), p(out), p(mask), n, n, 0, stream())
+    ro, rm = R.relu_with_mask(R.Session(10), xs)
+    assert np.array_equal(host(out).reshape(3, n), ro)
+    assert np.array_equal(host(mask).reshape(3, n), rm)
+
+
 @pytest.mark.parametrize("n", [600000, 600001])
 def test_sign_single_phase_equals_two_phase_shards(n):
     """Large tensors run the single-phase sign kernel, small ones the two-phase
