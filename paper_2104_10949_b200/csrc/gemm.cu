@@ -23,6 +23,7 @@
 #include <string.h>
 
 #include <mutex>
+#include <set>
 
 #include "launch.cuh"
 #include "items.cuh"
@@ -620,6 +621,21 @@ static int make_map_mn(CUtensorMap* map, const uint8_t* base, int64_t kp, int64_
   return MPC3_OK;
 }
 
+// The GEMM's dynamic shared memory (192 KiB + barriers), opted into once per
+// device (the attribute is per device: a process may drive several GPUs).
+static bool gemm_attr() {
+  static std::mutex mu;
+  static std::set<int> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count(dev)) return true;
+  if (cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess)
+    return false;
+  done.insert(dev);
+  return true;
+}
+
 static Operand to_operand(const mpc3_operand* o) {
   Operand p;
   p.mode = o->mode;
@@ -756,13 +772,7 @@ int mpc3_ring_gemm_packed_layout(const uint8_t* A, const uint8_t* B, uint64_t* C
   int nkb = (int)((kp + BK - 1) / BK);
   int kbs = (nkb + splits - 1) / splits;
   if ((int64_t)kbs * BK > MAX_SPLIT_K) return MPC3_ERR_EXACTNESS;  // caller must split longer K
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) !=
-        cudaSuccess)
-      return check_launch("gemm_tc attr");
-    attr_set = true;
-  }
+  if (!gemm_attr()) return check_launch("gemm_tc attr");
   CUtensorMap ta, tb;
   int st = make_map(&ta, A, kp, M, (int64_t)groups * 8, BM);
   if (st) return st;
@@ -876,12 +886,7 @@ int mpc3_ring_gemm_t_z(const uint8_t* A, int a_mn, int64_t a_rows, int64_t a_kp,
   if ((a_mn && (a_kp % 16 || a_rows > (a_rh ? a_half : 0) + kc_half || (!a_cs && !a_rh && a_half % 16))) ||
       (b_mn && (b_kp % 16 || b_rows > kc_half || b_half % 16)))
     return MPC3_ERR_SHAPE;
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess)
-      return check_launch("gemm_tc attr");
-    attr_set = true;
-  }
+  if (!gemm_attr()) return check_launch("gemm_tc attr");
   CUtensorMap ta, tb;
   int st = a_mn ? make_map_mn(&ta, A, a_kp, a_rows, (int64_t)groups * 8, BM, CU_TENSOR_MAP_SWIZZLE_128B)
                 : make_map(&ta, A, a_cs ? a_kp : kp, M, (int64_t)groups * 8, BM);
