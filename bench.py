@@ -280,6 +280,7 @@ class Recorder:
         self.count = 0
         self.k = 0
         self.events = []  # (name, category, e0, e1, work, shape)
+        self.ms = None  # per-event durations chosen by _instrumented (None: read the events)
         capi.call = self.call
         engine.K.call = self.call
 
@@ -331,8 +332,8 @@ class Recorder:
     def summary(self, step_ms: float) -> dict:
         """Per-category kernel time of the instrumented pass and its share."""
         cats = {}
-        for name, cat, e0, e1, work, shape in self.events:
-            ms = e0.elapsed_time(e1)
+        for i, (name, cat, e0, e1, work, shape) in enumerate(self.events):
+            ms = self.ms[i] if self.ms is not None else e0.elapsed_time(e1)
             c = cats.setdefault(cat, {"ms": 0.0, "launches": 0, "work": 0.0})
             c["ms"] += ms
             c["launches"] += 1
@@ -345,10 +346,10 @@ class Recorder:
 
     def per_launch(self, cat: str, top: int = 5):
         rows = []
-        for name, c, e0, e1, work, shape in self.events:
+        for i, (name, c, e0, e1, work, shape) in enumerate(self.events):
             if c != cat:
                 continue
-            us = e0.elapsed_time(e1) * 1e3
+            us = (self.ms[i] if self.ms is not None else e0.elapsed_time(e1)) * 1e3
             rows.append({"call": name[len("mpc3_"):], "shape": list(shape), "us": round(us, 2),
                          "rate": round(work / (us / 1e6) / (1e12 if cat == "gemm" else 1e9), 2) if us else None})
         rows.sort(key=lambda r: -r["us"])
@@ -432,22 +433,35 @@ def _traffic(workload: str = "alexnet"):
     return t
 
 
-def _instrumented(fn, rec, torch):
-    """One eager pass of fn with per-launch events, streams serialised."""
+def _instrumented(fn, rec, torch, passes: int = 2):
+    """Eager passes of fn with per-launch events, streams serialised; each
+    launch keeps its shortest time over the passes (a host stall while the
+    pass is enqueued behind the GPU spin would otherwise stretch one
+    launch's events)."""
     from paper_2104_10949_b200 import engine
     from paper_2104_10949_b200 import nn as nn_mod
 
     saved = (nn_mod.OVERLAP, engine.OVERLAP_PACK)
     nn_mod.OVERLAP, engine.OVERLAP_PACK = False, False
-    rec.events.clear()
-    rec.on = True
+    runs = []
     try:
-        torch.cuda._sleep(int(2e8))  # ~0.1 s of GPU spin: the host enqueues the whole pass behind it
-        fn()
-        torch.cuda.synchronize()
+        for _ in range(passes):
+            rec.events.clear()
+            rec.on = True
+            torch.cuda._sleep(int(2e8))  # ~0.1 s of GPU spin: the host enqueues the whole pass behind it
+            fn()
+            torch.cuda.synchronize()
+            rec.on = False
+            runs.append([(ev, ev[2].elapsed_time(ev[3])) for ev in rec.events])
     finally:
         rec.on = False
         nn_mod.OVERLAP, engine.OVERLAP_PACK = saved
+    if len(runs) > 1 and all(len(r) == len(runs[0]) for r in runs):
+        rec.events = [r[0] for r in runs[0]]
+        rec.ms = [min(r[i][1] for r in runs) for i in range(len(runs[0]))]
+    else:
+        rec.events = [r[0] for r in runs[-1]]
+        rec.ms = [r[1] for r in runs[-1]]
 
 
 def run_b200(args, ws, rank, local):
@@ -587,6 +601,7 @@ def run_b200(args, ws, rank, local):
     summ = rec.summary(total_ms / args.steps)
     roofline = roofline_of(rec, summ, peaks, sm_mhz, _traffic())
     rec.events.clear()
+    rec.ms = None
 
     # end-to-end through the public API with host inputs
     e2e = None if args.no_e2e else _e2e(args, ws, dev, sess, st, graph, xs_static, ys_static, imgs, labels, b)
@@ -979,6 +994,7 @@ def resnet50_inference(dev, batch: int, steps: int, rec=None, peaks=None, sm_mhz
             out["roofline"]["secondary"] = {k: rf["secondary"][k] for k in ("kernel", "achieved", "unit", "frac")
                                             if k in rf["secondary"]}
         rec.events.clear()
+        rec.ms = None
     return out
 
 
