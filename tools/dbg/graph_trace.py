@@ -2,7 +2,7 @@
 (torch.profiler / CUPTI activity records): per-kernel start/end on the device,
 busy time vs idle gaps between consecutive kernels, overlap.
 
-python tools/dbg/graph_trace.py [replays]
+python tools/dbg/graph_trace.py [replays] [resnet50 batch: trace its inference graph instead]
 """
 import json
 import os
@@ -18,18 +18,28 @@ from paper_2104_10949_b200 import engine  # noqa: E402
 from paper_2104_10949_b200.nn import TrainState, one_hot  # noqa: E402
 
 
-def main(reps=3):
+def main(reps=3, resnet_batch=0):
     torch.cuda.set_device(0)
-    b = 128
-    sess = M.TrioSession(seed=0)
-    st = TrainState(sess, M.alexnet_cifar(), M.TrainConfig(0.01, b, 16, seed=0))
-    imgs, labels = bench._synthetic(b, 100)
-    xb = st.deal_batch(M.fx_encode(imgs), M.fx_encode(one_hot(labels, 10)))
-    for _ in range(2):
-        st.step(*xb)
-    xs = engine.RssTensor(xb[0].data.clone())
-    ys = engine.RssTensor(xb[1].data.clone())
-    g = st.capture(xs, ys)
+    if resnet_batch:  # ResNet-50 inference graph at this batch instead
+        from paper_2104_10949_b200.nn import InferenceGraph
+
+        sess = M.TrioSession(seed=11)
+        model = M.models.resnet50()
+        rng = np.random.default_rng(11)
+        params = [sess.share(w, rng) for w in M.init_params(model, seed=11)]
+        x = sess.share(M.fx_encode(rng.uniform(0, 1, (resnet_batch, 3, 224, 224))), rng)
+        g = InferenceGraph(sess, model, params, x)
+    else:
+        b = 128
+        sess = M.TrioSession(seed=0)
+        st = TrainState(sess, M.alexnet_cifar(), M.TrainConfig(0.01, b, 16, seed=0))
+        imgs, labels = bench._synthetic(b, 100)
+        xb = st.deal_batch(M.fx_encode(imgs), M.fx_encode(one_hot(labels, 10)))
+        for _ in range(2):
+            st.step(*xb)
+        xs = engine.RssTensor(xb[0].data.clone())
+        ys = engine.RssTensor(xb[1].data.clone())
+        g = st.capture(xs, ys)
     for _ in range(2):
         g.replay()
     torch.cuda.synchronize()
