@@ -152,7 +152,14 @@ def test_large_trio_ops_match_oracle():
     assert np.array_equal(got.data.cpu().numpy().view(U64), R.conv2d_shares(o, c, k, (1, 1), (1, 1)))
 
 
-def test_tiny_model_backward_bit_exact_vs_oracle():
+@pytest.mark.parametrize("swap", [False, True])
+def test_tiny_model_backward_bit_exact_vs_oracle(swap, monkeypatch):
+    """Forward + backward of a small conv net vs the oracle; `swap` runs every
+    weight gradient as g^T x (x's transposed pack as B, b_mn = 2)."""
+    from paper_2104_10949_b200 import engine as E
+
+    if swap:
+        monkeypatch.setattr(E, "WGRAD_SWAP_MIN_KC", 0)
     layers = (N.conv(4, 3, 2, 1), N.relu(), N.pool(2), N.flat(), N.fc(5))
     ishape = (3, 8, 8)
     rng = np.random.default_rng(31)
