@@ -21,6 +21,17 @@ void set_last_error(const char* msg) {
   g_last_error[sizeof(g_last_error) - 1] = 0;
 }
 
+// Two-phase circuit phase on three lanes per pair (Lane3, items.cuh); 0
+// builds the one-thread-per-pair form for A/B.
+#ifndef MPC3_SIGN2_LANES
+#define MPC3_SIGN2_LANES 1
+#endif
+#ifndef MPC3_SIGN2_WAVES  // two-phase grids: at most this many waves of CTAs (the rest loop over chunks)
+#define MPC3_SIGN2_WAVES 8
+#endif
+#ifndef MPC3_DBG_S2PHASE  // timing builds: 1 = sign2's keystream phase only, 2 = its circuit phase only
+#define MPC3_DBG_S2PHASE 0
+#endif
 constexpr int kThreads = 256;
 constexpr int kSignThreads = 384;  // four-table AES kernels: one CTA per SM
 // The protocol kernels (everything but the sign / sign2 / chain kernels) come
@@ -374,7 +385,7 @@ __global__ void __launch_bounds__(F ? kSignThreads : kThreads, F ? 1 : 2)
   const int used = mode <= MODE_MSB ? nslots - 3 : (mode == MODE_DRELU ? nslots - 1 : nslots);
   const uint64_t npairs = (n + 1) >> 1;
   for (uint64_t c0 = (uint64_t)blockIdx.x * P; c0 < npairs; c0 += (uint64_t)gridDim.x * P) {
-    for (int q = threadIdx.x; q < (used + PRE) * P; q += blockDim.x) {
+    for (int q = threadIdx.x; q < (MPC3_DBG_S2PHASE == 2 ? 0 : (used + PRE) * P); q += blockDim.x) {
       const int sa = q / P, p = q % P;
       if (c0 + p >= npairs) continue;
       const uint64_t blk = (elem_off >> 1) + c0 + p;
@@ -392,7 +403,27 @@ __global__ void __launch_bounds__(F ? kSignThreads : kThreads, F ? 1 : 2)
       sign_slot_fill(tab, &ks.rk[0][0], st, s, blk, n_total, L, slots + ((size_t)s * P + p) * 3);
     }
     __syncthreads();
-    if (threadIdx.x < P && c0 + threadIdx.x < npairs) {
+#if MPC3_SIGN2_LANES
+    if (MPC3_DBG_S2PHASE != 1) {  // the circuit, three lanes per pair (Lane3)
+      const LaneGroup G = lane_group();
+      const int nw = blockDim.x >> 5;
+      for (int base = (threadIdx.x >> 5) * 10; base < P; base += nw * 10) {
+        const int pp = base + G.gi;
+        const bool live = G.gi < 10 && pp < P && c0 + pp < npairs;
+        const Lane3 L = {slots, P, live ? pp : 0, G.ci, G.nl, G.pl};  // pair 0 of a chunk always exists
+        if constexpr (MAXL) {
+          maxlevel_item_lane(L, x, out, mg, n, n_total, c0 + L.p, live);
+        } else if constexpr (KIND == S2_RS) {
+          const Word2* w3 = pre + (size_t)L.p * 3;
+          const Word2* tr = pre + ((size_t)P + L.p) * 3;
+          sign_item_rs_lane(L, mode, rin, w3, tr[0], tr[1], out, mask, n, n_total, c0 + L.p, plane, live);
+        } else {
+          sign_item_lane(L, mode, x, out, mask, n, n_total, c0 + L.p, plane, live);
+        }
+      }
+    }
+#else
+    if (MPC3_DBG_S2PHASE != 1 && threadIdx.x < P && c0 + threadIdx.x < npairs) {
       Replay rp;
       rp.w = slots;
       rp.P = P;
@@ -409,6 +440,7 @@ __global__ void __launch_bounds__(F ? kSignThreads : kThreads, F ? 1 : 2)
         sign_item(rp, &ks.rk[0][0], st, mode, x, out, mask, n, n_total, elem_off, c0 + threadIdx.x, plane);
       }
     }
+#endif
     __syncthreads();
   }
   if constexpr (MAXL) {  // odd m: the last column passes through to the last output column
@@ -468,6 +500,18 @@ __global__ void __launch_bounds__(kThreads, 1) maxtree_kernel(const __grid_const
                        slots + ((size_t)s * Pc + p) * 3);
       }
       __syncthreads();
+#if MPC3_SIGN2_LANES
+      {
+        const LaneGroup G = lane_group();
+        const int nw = blockDim.x >> 5;
+        for (int base = (threadIdx.x >> 5) * 10; base < Pc; base += nw * 10) {
+          const int pp = base + G.gi;
+          const bool live = G.gi < 10 && pp < Pc;
+          const Lane3 L = {slots, Pc, live ? pp : 0, G.ci, G.nl, G.pl};
+          maxlevel_item_lane(L, in, o, g, n, n_total, p0 + c + L.p, live);
+        }
+      }
+#else
       if (threadIdx.x < Pc) {
         Replay rp;
         rp.w = slots;
@@ -476,6 +520,7 @@ __global__ void __launch_bounds__(kThreads, 1) maxtree_kernel(const __grid_const
         rp.slot = 0;
         maxlevel_item(rp, &ks.rk[0][0], st, in, o, g, n, n_total, elem_off, p0 + c + threadIdx.x);
       }
+#endif
       __syncthreads();
     }
     if (m & 1)  // odd m: the last column passes through to the last output column
@@ -705,6 +750,18 @@ __global__ void __launch_bounds__(kThreads, 1) softmax_loss_kernel(
         sign_slot_fill(tab, rk, st, sidx, (elem_off >> 1) + p0 + c + p, n_total, L, slots + ((size_t)sidx * Pc + p) * 3);
       }
       __syncthreads();
+#if MPC3_SIGN2_LANES
+      {
+        const LaneGroup G = lane_group();
+        const int nw = blockDim.x >> 5;
+        for (int base = (threadIdx.x >> 5) * 10; base < Pc; base += nw * 10) {
+          const int pp = base + G.gi;
+          const bool live = G.gi < 10 && pp < Pc;
+          const Lane3 L = {slots, Pc, live ? pp : 0, G.ci, G.nl, G.pl};
+          maxlevel_item_lane(L, in, o, g, nl, n_total, p0 + c + L.p, live);
+        }
+      }
+#else
       if (threadIdx.x < Pc) {
         Replay rp;
         rp.w = slots;
@@ -713,6 +770,7 @@ __global__ void __launch_bounds__(kThreads, 1) softmax_loss_kernel(
         rp.slot = 0;
         maxlevel_item(rp, rk, st, in, o, g, nl, n_total, elem_off, p0 + c + threadIdx.x);
       }
+#endif
       __syncthreads();
     }
     if (m & 1)
@@ -1199,7 +1257,7 @@ static int sign_launch(const KeySched& ks, const uint64_t* ctr, const SignArgs& 
                    : (kSign2Four ? sign2_kernel<S2_SIGN, true> : sign2_kernel<S2_SIGN, false>);
     if (!aes_attr((const void*)kern, sign2_smem_max(rs))) return check_launch("sign2 smem attribute");
     uint64_t chunks = ((nr + 1) / 2 + P - 1) / P;
-    unsigned grid = (unsigned)(chunks < 148 * 2 * 8 ? chunks : 148 * 2 * 8);
+    unsigned grid = (unsigned)(chunks < 148 * 2 * MPC3_SIGN2_WAVES ? chunks : 148 * 2 * MPC3_SIGN2_WAVES);
     ri.f0 += e0;
     launch_pdl(kern, dim3(grid), dim3(kSign2Four ? kSignThreads : kThreads), smem, as_stream(stream), ks, ctr, a, mode,
                rs ? x : x + e0, out + e0, mask ? mask + e0 : mask, nr, n_total, elem_off + e0, P, n,
@@ -1294,7 +1352,7 @@ int mpc3_rss_max_level(const uint32_t* rk3, const uint64_t* ctr, uint64_t j_bin,
   auto kern = kSign2Four ? sign2_kernel<S2_MAXL, true> : sign2_kernel<S2_MAXL, false>;
   if (!aes_attr((const void*)kern, sign2_smem_max())) return check_launch("max_level smem attribute");
   uint64_t chunks = ((n + 1) / 2 + P - 1) / P;
-  unsigned grid = (unsigned)(chunks < 148 * 2 * 8 ? chunks : 148 * 2 * 8);
+  unsigned grid = (unsigned)(chunks < 148 * 2 * MPC3_SIGN2_WAVES ? chunks : 148 * 2 * MPC3_SIGN2_WAVES);
   launch_pdl(kern, dim3(grid), dim3(kSign2Four ? kSignThreads : kThreads), smem, as_stream(stream), ks, ctr, a,
              (int)MODE_RELU, v, out, (uint64_t*)nullptr, n, n_total, elem_off, P, (uint64_t)0, MaxGeom{rows, m, k},
              RsIn{});

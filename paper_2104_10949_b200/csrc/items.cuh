@@ -488,4 +488,90 @@ HD void pack_item(const uint64_t* src, int64_t plane, const Operand& o, int role
   for (int l = 0; l < 8; ++l) *reinterpret_cast<uint64_t*>(base + (int64_t)l * o.rows * kp) = w[l];
 }
 
+#if defined(__CUDACC__)
+// Lane3 forms of sign_item / sign_item_rs / maxlevel_item for the two-phase
+// kernels' circuit phase: every lane of a group builds the pair's input
+// trios, lane i stores component i; `live` false (padding lanes, pairs past
+// the chunk) runs the circuit (the shuffles need every lane) without stores.
+DEV void store_lane(uint64_t* p, uint64_t plane, uint64_t e, int i, uint64_t v) { p[i * plane + e] = v; }
+
+DEV void sign_item_lane(const Lane3& L, int mode, const uint64_t* x, uint64_t* out, uint64_t* mask, uint64_t n,
+                        uint64_t n_total, uint64_t b, uint64_t plane, bool live) {
+  const uint64_t pl = plane ? plane : n;
+  const bool two = 2 * b + 1 < n;
+  Trio xin[2];
+  xin[0] = load_trio(x, pl, 2 * b);
+  xin[1] = two ? load_trio(x, pl, 2 * b + 1) : xin[0];
+  uint64_t o[2], m[2];
+  sign_circuit_lane(L, n_total, mode, xin, o, m);
+  if (!live) return;
+  store_lane(out, pl, 2 * b, L.i, o[0]);
+  if (two) store_lane(out, pl, 2 * b + 1, L.i, o[1]);
+  if (mode == MODE_RELU && mask) {
+    store_lane(mask, pl, 2 * b, L.i, m[0]);
+    if (two) store_lane(mask, pl, 2 * b + 1, L.i, m[1]);
+  }
+}
+
+DEV void sign_item_rs_lane(const Lane3& L, int mode, const RsIn& in, const Word2 w3[3], Word2 rho, Word2 r,
+                           uint64_t* out, uint64_t* mask, uint64_t n, uint64_t n_total, uint64_t b, uint64_t plane,
+                           bool live) {
+  const bool two = 2 * b + 1 < n;
+  const uint64_t pl = plane ? plane : n;
+  Trio xin[2];
+  {
+    const uint64_t k0[3] = {w3[0].w0, w3[1].w0, w3[2].w0}, k1[3] = {w3[0].w1, w3[1].w1, w3[2].w1};
+    xin[0] = reshare_input(in, in.f0 + 2 * b, k0, rho.w0, r.w0);
+    xin[1] = two ? reshare_input(in, in.f0 + 2 * b + 1, k1, rho.w1, r.w1) : xin[0];
+  }
+  uint64_t o[2], m[2];
+  sign_circuit_lane(L, n_total, mode, xin, o, m);
+  if (!live) return;
+  store_lane(out, pl, 2 * b, L.i, o[0]);
+  if (two) store_lane(out, pl, 2 * b + 1, L.i, o[1]);
+  if (mode == MODE_RELU && mask) {
+    store_lane(mask, pl, 2 * b, L.i, m[0]);
+    if (two) store_lane(mask, pl, 2 * b + 1, L.i, m[1]);
+  }
+}
+
+DEV void maxlevel_item_lane(const Lane3& L, const uint64_t* v, uint64_t* out, const MaxGeom& g, uint64_t n,
+                            uint64_t n_total, uint64_t b, bool live) {
+  const bool two = 2 * b + 1 < n;
+  const uint64_t pv = g.rows * g.m, mo = g.k + (g.m & 1), po = g.rows * mo;
+  Trio d[2];
+  uint64_t c[2];  // component i of the odd column (the max = it + relu(difference))
+  for (int e = 0; e < 2; ++e) {
+    const uint64_t f = (e && two) ? 2 * b + 1 : 2 * b, row = f / g.k, j = f - row * g.k;
+    const Trio a = load_trio(v, pv, row * g.m + 2 * j), cc = load_trio(v, pv, row * g.m + 2 * j + 1);
+    for (int k = 0; k < 3; ++k) d[e].c[k] = a.c[k] - cc.c[k];
+    c[e] = comp(cc, L.i);
+  }
+  uint64_t o[2], mk[2];
+  sign_circuit_lane(L, n_total, MODE_RELU, d, o, mk);
+  if (!live) return;
+  for (int e = 0; e < (two ? 2 : 1); ++e) {
+    const uint64_t f = 2 * b + e, row = f / g.k, j = f - row * g.k;
+    store_lane(out, po, row * mo + j, L.i, c[e] + o[e]);
+  }
+}
+
+// The group geometry of a lane in a CTA of whole warps: 10 groups of three
+// lanes per warp (lanes 30 and 31 pad); group q of warp w handles the
+// chunk's pairs w * 10 + q, + 10 * warps, ...
+struct LaneGroup {
+  int gi, ci, nl, pl;
+};
+DEV LaneGroup lane_group() {
+  const int lane = threadIdx.x & 31;
+  LaneGroup G;
+  G.gi = lane < 30 ? lane / 3 : 10;
+  G.ci = lane < 30 ? lane % 3 : lane - 30;
+  const int base = lane - G.ci;
+  G.nl = (base + (G.ci == 2 ? 0 : G.ci + 1)) & 31;
+  G.pl = (base + (G.ci == 0 ? 2 : G.ci - 1)) & 31;
+  return G;
+}
+#endif
+
 }  // namespace mpc3

@@ -616,4 +616,155 @@ HD void inject_pair(const T& tab, const uint32_t* rk3, StreamHead a0, StreamHead
   }
 }
 
+#if defined(__CUDACC__)
+// The two-phase kernels' circuit as a 3-lane SIMT program.  With the
+// keystream replayed from shared memory, a pair's circuit is a chain of
+// dependent integer steps; one thread per pair leaves 2 of 8 warps busy and
+// the phase latency-bound.  Here lane i of a group of three holds component
+// i of the pair's two elements: the AND / multiplication cross terms read
+// component i+1 from the next lane and the relabel (z_i -> party i+1) takes
+// component i-1 from the previous one (warp shuffles), the zero-share words
+// are read straight from the slot (lane i folds F(k_i) and F(k_{i-1})), so
+// the same circuit runs on three times the lanes with the same slot order
+// and results bit-for-bit.
+struct Lane3 {
+  const Word2* w;  // keystream slots (pair p's slot s at w[(s * P + p) * 3 + key])
+  int P, p;
+  int i, nl, pl;  // component; lanes holding components i+1 and i-1
+};
+DEV uint64_t lane_nxt(const Lane3& L, uint64_t v) { return __shfl_sync(0xffffffffu, v, L.nl); }
+DEV uint64_t lane_prv(const Lane3& L, uint64_t v) { return __shfl_sync(0xffffffffu, v, L.pl); }
+DEV uint64_t comp(const Trio& t, int i) { return i == 0 ? t.c[0] : (i == 1 ? t.c[1] : t.c[2]); }
+// (F(k_i), F(k_{i-1})) of slot s
+DEV void lane_words(const Lane3& L, int s, Word2& wi, Word2& wp) {
+  const Word2* b = L.w + ((size_t)s * L.P + L.p) * 3;
+  wi = b[L.i];
+  wp = b[L.i == 0 ? 2 : L.i - 1];
+}
+// z_i of a local AND / product: x_i y_i + x_{i+1} y_i + x_i y_{i+1}
+DEV uint64_t lane_and(uint64_t a, uint64_t an, uint64_t b, uint64_t bn) { return (a & b) ^ (an & b) ^ (a & bn); }
+DEV uint64_t lane_mul(uint64_t a, uint64_t an, uint64_t b, uint64_t bn) { return a * b + an * b + a * bn; }
+
+// sign_circuit_pair on Lane3: x[2] the pair's input trios (every lane holds
+// both full trios); out / mask: component i of the results.
+DEV void sign_circuit_lane(const Lane3& L, uint64_t n_total, int mode, const Trio x[2], uint64_t out[2],
+                           uint64_t mask[2]) {
+  const int i = L.i;
+  const bool straddle = (n_total & 1) != 0;
+  const Word2 rb = L.w[(size_t)L.p * 3];  // slot 0: BIN (k_0)
+  uint64_t p[2], g[2];
+  {  // level 0: g = a AND b with a = ((x0+x1)^r, r, 0), b = (0, 0, x2)
+    uint64_t t[2];
+    const int n = i == 2 ? 0 : i + 1;
+    for (int e = 0; e < 2; ++e) {
+      const uint64_t r = e ? rb.w1 : rb.w0;
+      const uint64_t a0 = (x[e].c[0] + x[e].c[1]) ^ r;
+      const uint64_t ai = i == 0 ? a0 : (i == 1 ? r : 0), an = n == 0 ? a0 : (n == 1 ? r : 0);
+      const uint64_t bi = i == 2 ? x[e].c[2] : 0, bn = n == 2 ? x[e].c[2] : 0;
+      p[e] = ai ^ bi;
+      t[e] = lane_and(ai, an, bi, bn);
+    }
+    Word2 wi, wp;
+    lane_words(L, 1, wi, wp);
+    t[0] ^= wi.w0 ^ wp.w0;
+    t[1] ^= wi.w1 ^ wp.w1;
+    for (int e = 0; e < 2; ++e) g[e] = lane_prv(L, t[e]);
+  }
+  int slot = 2;
+#pragma unroll 1
+  for (int lvl = 1; lvl <= 6; ++lvl) {
+    const int d = 1 << (lvl - 1);
+    uint64_t pn[2], tg[2];
+    for (int e = 0; e < 2; ++e) {
+      pn[e] = lane_nxt(L, p[e]);
+      const uint64_t gn = lane_nxt(L, g[e]);
+      tg[e] = lane_and(p[e], pn[e], g[e] << d, gn << d);
+    }
+    Word2 wi, wp;
+    lane_words(L, slot++, wi, wp);
+    tg[0] ^= wi.w0 ^ wp.w0;
+    tg[1] ^= wi.w1 ^ wp.w1;
+    if (lvl < 6) {  // level 6's p-half is dead
+      uint64_t tp[2];
+      for (int e = 0; e < 2; ++e) tp[e] = lane_and(p[e], pn[e], p[e] << d, pn[e] << d);
+      lane_words(L, slot++, wi, wp);
+      if (!straddle) {
+        tp[0] ^= wi.w0 ^ wp.w0;
+        tp[1] ^= wi.w1 ^ wp.w1;
+      } else {  // element 0 <- word 2b+1 of this block, element 1 <- word 2b of the next
+        tp[0] ^= wi.w1 ^ wp.w1;
+        lane_words(L, slot++, wi, wp);
+        tp[1] ^= wi.w0 ^ wp.w0;
+      }
+      for (int e = 0; e < 2; ++e) p[e] = lane_prv(L, tp[e]);
+    }
+    for (int e = 0; e < 2; ++e) g[e] ^= lane_prv(L, tg[e]);
+  }
+  uint64_t s[2], bit[2];
+  for (int e = 0; e < 2; ++e) {  // sum = p_leaf ^ (g << 1), p_leaf = ((x0+x1)^r, r, x2)
+    const uint64_t r = e ? rb.w1 : rb.w0;
+    const uint64_t pl = i == 0 ? (x[e].c[0] + x[e].c[1]) ^ r : (i == 1 ? r : x[e].c[2]);
+    s[e] = pl ^ (g[e] << 1);
+    bit[e] = s[e] >> 63;
+  }
+  if (mode == MODE_A2B) {
+    out[0] = s[0];
+    out[1] = s[1];
+    return;
+  }
+  if (mode == MODE_MSB) {
+    out[0] = bit[0];
+    out[1] = bit[1];
+    return;
+  }
+  // bit_inject and the ReLU mask (the ARITH slots after level 6's g-half)
+  const int sa = slot;
+  uint64_t bn[2], u[2], m[2];
+  for (int e = 0; e < 2; ++e) bn[e] = lane_nxt(L, bit[e]);
+  {  // u = s0 + s1 - 2 mul(s0, s1): t0 = (s0, 0, 0), t1 = (0, s1, 0)
+    uint64_t z[2];
+    for (int e = 0; e < 2; ++e) {
+      const uint64_t t0i = i == 0 ? bit[e] : 0, t1i = i == 1 ? bit[e] : 0;
+      const uint64_t t0n = i == 2 ? bn[e] : 0, t1n = i == 0 ? bn[e] : 0;
+      z[e] = lane_mul(t0i, t0n, t1i, t1n);
+    }
+    Word2 wi, wp;
+    lane_words(L, sa, wi, wp);
+    z[0] += wi.w0 - wp.w0;
+    z[1] += wi.w1 - wp.w1;
+    for (int e = 0; e < 2; ++e) u[e] = (i < 2 ? bit[e] : 0) - 2 * lane_prv(L, z[e]);
+  }
+  {  // v = u + s2 - 2 mul(u, s2): t2 = (0, 0, s2); drelu = 1 - v
+    uint64_t z[2];
+    for (int e = 0; e < 2; ++e) {
+      const uint64_t t2i = i == 2 ? bit[e] : 0, t2n = i == 1 ? bn[e] : 0;
+      z[e] = lane_mul(u[e], lane_nxt(L, u[e]), t2i, t2n);
+    }
+    Word2 wi, wp;
+    lane_words(L, sa + 1, wi, wp);
+    z[0] += wi.w0 - wp.w0;
+    z[1] += wi.w1 - wp.w1;
+    for (int e = 0; e < 2; ++e)
+      m[e] = (i == 0 ? 1 : 0) - (u[e] + (i == 2 ? bit[e] : 0) - 2 * lane_prv(L, z[e]));
+  }
+  if (mode == MODE_DRELU) {
+    out[0] = m[0];
+    out[1] = m[1];
+    return;
+  }
+  {  // relu = mul(x, drelu)
+    const int n = i == 2 ? 0 : i + 1;
+    uint64_t z[2];
+    for (int e = 0; e < 2; ++e) z[e] = lane_mul(comp(x[e], i), comp(x[e], n), m[e], lane_nxt(L, m[e]));
+    Word2 wi, wp;
+    lane_words(L, sa + 2, wi, wp);
+    z[0] += wi.w0 - wp.w0;
+    z[1] += wi.w1 - wp.w1;
+    for (int e = 0; e < 2; ++e) out[e] = lane_prv(L, z[e]);
+  }
+  mask[0] = m[0];
+  mask[1] = m[1];
+}
+#endif
+
 }  // namespace mpc3
