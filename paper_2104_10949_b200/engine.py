@@ -104,11 +104,19 @@ class Packed:
 
 
 def _stream() -> int:
-    return torch.cuda.current_stream().cuda_stream
+    # the raw C getters: torch.cuda.current_stream() resolves its device index
+    # through Python helpers, ~8 us per call on the eager step's ~130 launches
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
 
 
 def _dev():
-    return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cuda", torch._C._cuda_getDevice())
+
+
+def _cur():
+    """torch.cuda.current_stream() with the device index given (skips the
+    Python device-index resolution)."""
+    return torch.cuda.current_stream(torch._C._cuda_getDevice())
 
 
 def to_device(a: np.ndarray) -> torch.Tensor:
@@ -150,7 +158,7 @@ class RssTensor:
 
     @property
     def numel(self) -> int:
-        return int(np.prod(self.shape, dtype=np.int64)) if self.shape else 1
+        return self.data.numel() // 3
 
     def contiguous(self) -> "RssTensor":
         return self if self.data.is_contiguous() else RssTensor(self.data.contiguous(), self.fp)
@@ -657,7 +665,7 @@ class TrioSession:
         """Pack weight operands (role 0) ahead of the layers that use them, on
         the pack stream: items = [(src, op, rows, k)].  _cross_gemm_kept takes
         a matching prepacked B instead of packing it on the critical path."""
-        main = torch.cuda.current_stream()
+        main = _cur()
         ps = self.pack_stream()
         ev = torch.cuda.Event()
         ev.record(main)
@@ -682,7 +690,7 @@ class TrioSession:
         cs = CS_PACKS and a_role == 1 and a_packed is None
         kh, kp = Packed.geometry_cs(Kd) if cs else Packed.geometry(Kd)
         st = _stream()
-        main = torch.cuda.current_stream()
+        main = _cur()
         pre = self._prepacked.pop(self._pack_key(b_src, b_op, 1 - a_role), None) if self._prepacked else None
         if pre is not None:
             pre, done = pre
@@ -827,7 +835,7 @@ class TrioSession:
         z = torch.empty(3 * M * N, dtype=torch.int64, device=_dev())
         zeroed = self._needs_zero(False, M, N, kp)
         # the two operand packs are independent: B on the pack stream, A here
-        main = torch.cuda.current_stream()
+        main = _cur()
         ps = self.pack_stream() if OVERLAP_PACK else None
         if ps is not None and ps != main:
             ev = torch.cuda.Event()
@@ -852,7 +860,7 @@ class TrioSession:
         32-aligned kc_half (cached under frozen_weights)."""
         kc, kpb = Packed.geometry_cs(Kd)
         st = _stream()
-        main = torch.cuda.current_stream()
+        main = _cur()
         ps = None
         B = None
         key = None
@@ -912,7 +920,7 @@ class TrioSession:
         jr = jq = 0
         if bits:
             jr, jq = self.take(TR_RHO), self.take(TR_R)
-        full = int(np.prod(view.full))
+        full = math.prod(view.full)
         if bias is None:
             K.call("mpc3_rss_reshare_truncate", self.rk, self.ctr_ptr, ja, jr, jq, bits, z.data_ptr(), C.byref(view),
                    out.data.data_ptr(), self.shard_offset(full)[0], _stream())
@@ -942,7 +950,7 @@ class TrioSession:
             raise ShapeError("bias must be a 1-d shared vector with unit stride")
         ja = self.take(ARITH)
         jr, jq = self.take(TR_RHO), self.take(TR_R)
-        full = int(np.prod(view.full))
+        full = math.prod(view.full)
         self.ledger.ring(label, full)
         self._charge_trunc(full)
         return {"z": z, "view": view, "shape": shape, "bits": bits, "bias": bias, "bias_dim": bias_dim,

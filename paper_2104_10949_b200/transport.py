@@ -185,5 +185,20 @@ class Ledger:
             st.round_labels.extend(d.round_labels)
 
     def ring(self, label: str, words: int) -> None:
-        """Every party i sends `words` to i+1 (reshare / AND / open)."""
-        self.round(label, [(i, (i + 1) % 3, words) for i in range(3)])
+        """Every party i sends `words` to i+1 (reshare / AND / open).  The same
+        charges as round(label, [(i, i+1, words)]) without the per-send
+        topology checks (a ring's sends are valid by construction): this runs
+        once per protocol call on the eager path."""
+        if self._rec is not None or not self.enabled:
+            self.round(label, [(i, (i + 1) % 3, words) for i in range(3)])
+            return
+        nbytes = FRAME_HEADER_BYTES + 8 * int(words)
+        for i, t in enumerate(self.parties):
+            st = t.stats
+            st.rounds += 1
+            st.round_labels.append(label)
+            j, k = (i + 1) % 3, (i + 2) % 3
+            st.bytes_sent[j] = st.bytes_sent.get(j, 0) + nbytes
+            st.messages += 1
+            st.bytes_received[k] = st.bytes_received.get(k, 0) + nbytes
+            st.messages_received += 1
