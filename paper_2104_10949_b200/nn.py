@@ -56,9 +56,9 @@ FUSE_RELU_MIN = int(os.environ.get("MPC3_FUSE_RELU_MIN", "100000"))  # output el
 FUSE_RESIDUAL = os.environ.get("MPC3_FUSE_RESIDUAL", "1") == "1"
 FUSE_RESIDUAL_MAX = 4 << 20  # block input elements
 # train_trio replays a CUDA graph once this many iterations remain (the
-# capture's host cost pays off after ~80 AlexNet steps: eager 4.4 ms vs
-# replay 2.5 ms per step, capture ~170 ms)
-GRAPH_MIN_STEPS = 96
+# capture's host cost pays off after ~110 AlexNet steps: eager 3.9 ms
+# (host-bound) vs replay 2.36 ms per step, capture ~170 ms)
+GRAPH_MIN_STEPS = 112
 
 
 def _pair(v) -> tuple:
