@@ -915,14 +915,19 @@ class TrioSession:
     def c_col_ok(self) -> bool:
         return True
 
-    def _finish(self, z, view, out: RssTensor, bits, label, bias: RssTensor | None = None, bias_dim: int = 1):
+    def _finish(self, z, view, out: RssTensor, bits, label, bias: RssTensor | None = None, bias_dim: int = 1,
+                z_off: int = 0):
+        """Reshare + truncate (+ bias) of the cross terms z through `view`;
+        z_off (elements, may be negative): added to z's address, for a z that
+        holds only the view's crop while the view indexes the full tensor."""
         ja = self.take(ARITH)
         jr = jq = 0
         if bits:
             jr, jq = self.take(TR_RHO), self.take(TR_R)
         full = math.prod(view.full)
         if bias is None:
-            K.call("mpc3_rss_reshare_truncate", self.rk, self.ctr_ptr, ja, jr, jq, bits, z.data_ptr(), C.byref(view),
+            K.call("mpc3_rss_reshare_truncate", self.rk, self.ctr_ptr, ja, jr, jq, bits,
+                   (z.data_ptr() + 8 * z_off) % (1 << 64), C.byref(view),
                    out.data.data_ptr(), self.shard_offset(full)[0], _stream())
         else:  # the shared bias added in the same pass (a local add, nn.py bias extension)
             if bias.ndim != 1 or bias.data.stride(1) != 1:
@@ -1138,18 +1143,18 @@ class TrioSession:
                      w_packed: Packed | None = None) -> RssTensor:
         """Input gradient (nn.py:460-484).  Two bit-identical formulations
         (same ring values, same PRF words at the reference's flat indices of
-        the full (N, C, hf, wf) correlation); the cheaper one for the shape:
-        the transposed convolution (GEMM with inner length O + col2im) when O
-        is large relative to the spatial size, the reference's correlation of
-        the padded gradient with the flipped kernel (GEMM with inner length
-        O*kh*kw, no col2im) for stride 1 when O is small — e.g. VGG's 64-channel
+        the full (N, C, hf, wf) correlation); the faster one for the shape
+        (_dgrad_use_im2col): the transposed convolution (GEMM with inner
+        length O + col2im) for small maps, the reference's correlation of the
+        padded gradient with the flipped kernel, cropped to the rows the layer
+        keeps (GEMM with inner length O*kh*kw + reshare, no col2im), for
+        stride 1 on maps large enough to fill the GPU — e.g. VGG's 64 x 64
         layers, where the first would be a K=64 GEMM writing kh*kw times the
         input gradient."""
         nb, o, oh, ow = g.shape
         o2, c, kh, kw = k.shape
-        if stride == (1, 1) or tuple(stride) == (1, 1):
-            if _dgrad_cost_im2col(nb, o, oh, ow, c, kh, kw, padding) < _dgrad_cost_col2im(nb, o, oh, ow, c, kh, kw):
-                return self.conv2d_dgrad_im2col(g, k, stride, padding, in_shape, bits)
+        if tuple(stride) == (1, 1) and _dgrad_use_im2col(nb, oh, ow, kh, kw, padding):
+            return self.conv2d_dgrad_im2col(g, k, stride, padding, in_shape, bits)
         return self.conv2d_dgrad_col2im(g, k, stride, padding, in_shape, bits, w_packed=w_packed)
 
     def conv2d_dgrad_col2im(self, g: RssTensor, k: RssTensor, stride, padding, in_shape, bits,
@@ -1192,7 +1197,9 @@ class TrioSession:
 
     def conv2d_dgrad_im2col(self, g: RssTensor, k: RssTensor, stride, padding, in_shape, bits) -> RssTensor:
         """Input gradient by explicit im2col of the dilated, padded gradient
-        (the reference's formulation, kept as a cross-check path)."""
+        (the reference's formulation, nn.py:460-484), computing only the
+        window of the full correlation the layer keeps when the padding
+        allows."""
         nb, o, oh, ow = g.shape
         o2, c, kh, kw = k.shape
         sh, sw = stride
@@ -1201,13 +1208,30 @@ class TrioSession:
         check_accumulation(o * kh * kw)
         hf, wf = (oh - 1) * sh + kh, (ow - 1) * sw + kw
         gs, ks = g.data.stride(), k.data.stride()
-        a_op = K.conv_operand(K.GATHER_IM2COL, nb * hf * wf, o * kh * kw, nb, o, oh, ow, gs[1:], kh, kw, 1, 1,
-                              kh - 1, kw - 1, hf, wf, dh=sh, dw=sw)
         b_op = K.dense_operand(c, o * kh * kw, s_r=ks[2], off=(kh - 1) * ks[3] + (kw - 1) * ks[4], t0=ks[1],
                                t1=-ks[3], t2=-ks[4], K1=kh, K2=kw)
-        z = self._cross_gemm(g.data, a_op, k.data, b_op, nb * hf * wf, c, o * kh * kw)
         out = (empty if h + ph <= hf and w + pw <= wf else zeros)((nb, c, h, w), g.fp)
-        crop = (nb, c, max(0, min(h, hf - ph)), max(0, min(w, wf - pw)))
+        ch, cw = max(0, min(h, hf - ph)), max(0, min(w, wf - pw))
+        crop = (nb, c, ch, cw)
+        qh, qw = kh - 1 - ph, kw - 1 - pw
+        if qh >= 0 and qw >= 0 and ch and cw:
+            # only the rows the layer keeps: the (ch, cw) window of the full
+            # correlation at (ph, pw) is the correlation of g padded by
+            # (kh-1-ph, kw-1-pw); z holds that window (column-major when the
+            # GEMM can) and the view still indexes the full (N, C, hf, wf)
+            # output, so the PRF words stay at the reference's flat indices
+            M = nb * ch * cw
+            a_op = K.conv_operand(K.GATHER_IM2COL, M, o * kh * kw, nb, o, oh, ow, gs[1:], kh, kw, 1, 1, qh, qw,
+                                  ch, cw, dh=sh, dw=sw)
+            col = self.c_col_ok
+            z = self._cross_gemm(g.data, a_op, k.data, b_op, M, c, o * kh * kw, c_col=col)
+            zs = (ch * cw, M, cw, 1) if col else (ch * cw * c, 1, cw * c, c)
+            view = K.make_view((nb, c, hf, wf), crop=crop, origin=(0, 0, ph, pw), z_stride=zs,
+                               out_stride=(c * h * w, h * w, w, 1), out_plane=nb * c * h * w, z_plane=M * c)
+            return self._finish(z, view, out, bits, "mul.reshare", z_off=-(ph * zs[2] + pw * zs[3]))
+        a_op = K.conv_operand(K.GATHER_IM2COL, nb * hf * wf, o * kh * kw, nb, o, oh, ow, gs[1:], kh, kw, 1, 1,
+                              kh - 1, kw - 1, hf, wf, dh=sh, dw=sw)
+        z = self._cross_gemm(g.data, a_op, k.data, b_op, nb * hf * wf, c, o * kh * kw)
         view = K.make_view((nb, c, hf, wf), crop=crop, origin=(0, 0, ph, pw), z_stride=(hf * wf * c, 1, wf * c, c),
                            out_stride=(c * h * w, h * w, w, 1), out_plane=nb * c * h * w, z_plane=nb * hf * wf * c)
         return self._finish(z, view, out, bits, "mul.reshare")
@@ -1471,27 +1495,24 @@ class TrioSession:
 # kernel helpers
 
 
-def _gemm_us(M, N, K2):
-    """Rough ring-GEMM time (us): 72 int8 ops per ring MAC for 3 parties at
-    ~3 POPS, 64-column tiles, ~8 K-blocks of prologue / epilogue per tile."""
-    nkb = max(1, (K2 + 31) // 32)
-    ncol = math.ceil(N / 64) * 64
-    return 3 * M * ncol * K2 * 72 / 3.0e15 * 1e6 * (nkb + 8) / nkb
+# Input-gradient formulation (stride 1), measured per layer shape on B200
+# (tools/dbg/dgrad_paths.py, profiles/r02_dgrad_paths.txt): the cropped
+# correlation of the padded gradient wins once its GEMM has enough rows to
+# fill the GPU without split-K (VGG-16-TI b32 conv1_2 2.34 -> 1.69 ms,
+# conv2_2 1.47 -> 1.16, conv3_2 1.05 -> 0.96; 16 x 16 maps about even) and
+# loses below (8 x 8 maps and AlexNet-CIFAR's 1 x 1 / 2 x 2 maps, where its
+# GEMM is a long-K split); it also computes (h w) / (oh ow) times the
+# transposed convolution's MACs, so only kernels whose padding keeps the
+# map size qualify.
+DGRAD_IM2COL_MIN_ROWS = int(os.environ.get("MPC3_DGRAD_IM2COL_MIN_ROWS", "8192"))
 
 
-# Both dgrad formulations pay the same AES work (reshare + truncation of the
-# full correlation); the costs below are what differs, calibrated on B200
-# (VGG-16-TI b32 conv1_2 / conv2_2: col2im path 1.9 / 1.6 ms vs im2col path
-# 2.5 / 2.1 ms — the im2col operand pack at ~2.5 TB/s outweighs the better GEMM).
-def _dgrad_cost_col2im(nb, o, oh, ow, c, kh, kw):
-    M, N = nb * oh * ow, c * kh * kw
-    return _gemm_us(M, N, 2 * o) + 3 * M * N * 8 / 6.0e12 * 1e6 + 48 * M * o / 4.0e12 * 1e6
-
-
-def _dgrad_cost_im2col(nb, o, oh, ow, c, kh, kw, padding):
-    hf, wf = oh + kh - 1, ow + kw - 1  # stride 1
-    M, K = nb * hf * wf, o * kh * kw
-    return _gemm_us(M, c, 2 * K) + 48 * M * K / 2.5e12 * 1e6 + 3 * M * c * 8 / 4.0e12 * 1e6
+def _dgrad_use_im2col(nb, oh, ow, kh, kw, padding) -> bool:
+    ph, pw = padding
+    h, w = oh + kh - 1 - 2 * ph, ow + kw - 1 - 2 * pw
+    if kh - 1 - ph < 0 or kw - 1 - pw < 0 or h <= 0 or w <= 0:
+        return False
+    return nb * h * w >= DGRAD_IM2COL_MIN_ROWS and h * w * 4 <= oh * ow * 5
 
 
 def _ew2(op, a: RssTensor, b: RssTensor, out: RssTensor | None = None) -> RssTensor:

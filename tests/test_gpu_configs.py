@@ -146,7 +146,13 @@ def test_lenet_b64_per_party_infer_private_matches_reference():
     assert np.array_equal(got, arrays["logits"])
 
 
-def test_vgg16ti_b32_training_step_matches_reference_digest():
+@pytest.mark.parametrize("dgrad_rows", [None, 0, 1 << 62])
+def test_vgg16ti_b32_training_step_matches_reference_digest(dgrad_rows, monkeypatch):
+    """Eager train_trio at VGG-16-TI b32 = the reference's weights; with the
+    engine's input-gradient choice per layer (None), and with every stride-1
+    layer on the cropped correlation (0) or on the transposed convolution."""
+    if dgrad_rows is not None:
+        monkeypatch.setattr(E, "DGRAD_IM2COL_MIN_ROWS", dgrad_rows)
     _, meta = need("vgg16ti_train")
     imgs, labels = vgg16ti_train_data()
     res = nn.train_trio(TrioSession(5), M.vgg16(), M.TrainConfig(0.01, 32, 1, seed=5), imgs, labels)

@@ -207,7 +207,9 @@ def test_tiny_resnet_inference_bit_exact_vs_composed_oracle(batch):
 
 
 @pytest.mark.parametrize("nb,o,oh,ow,c,kh,kw,ph", [(2, 8, 5, 6, 3, 3, 3, 1), (3, 4, 4, 4, 5, 5, 5, 2),
-                                                  (1, 16, 7, 3, 8, 3, 2, 0), (4, 2, 6, 6, 2, 1, 1, 0)])
+                                                  (1, 16, 7, 3, 8, 3, 2, 0), (4, 2, 6, 6, 2, 1, 1, 0),
+                                                  (2, 4, 7, 8, 3, 3, 3, 3),  # padding > k-1: full grid
+                                                  (8, 24, 20, 20, 40, 3, 3, 1)])  # 3200 rows, 40 columns
 def test_dgrad_formulations_share_for_share(nb, o, oh, ow, c, kh, kw, ph):
     """The transposed-convolution (col2im) and padded-correlation (im2col)
     input gradients are the same ring values with the same PRF words: every
