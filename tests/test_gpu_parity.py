@@ -123,11 +123,12 @@ def test_alexnet_train_step_digest_bit_exact():
 @pytest.mark.parametrize("flags", [{"REUSE_PACKS": False}, {"OVERLAP_PACK": False}, {"nn.OVERLAP": False},
                                    {"REUSE_PACKS": False, "nn.OVERLAP": False}, {"nn.FUSE_RELU": False},
                                    {"nn.FUSE_RELU_MIN": 0}, {"MAXTREE_FUSED": False}, {"CS_PACKS": False},
-                                   {"T_PACKS": False}, {"WGRAD_SWAP_MIN_KC": 0}])
+                                   {"T_PACKS": False}, {"WGRAD_SWAP_MIN_KC": 0}, {"DGRAD_IM2COL_MIN_ROWS": 0}])
 def test_alexnet_train_step_digest_under_schedule_variants(flags, monkeypatch):
     """The engine's schedule choices (packs reused across the three GEMMs of a
     layer, weight packs one layer ahead, side-stream weight gradients, pack
-    stream, transposed packs, every weight gradient as g^T x) change no
+    stream, transposed packs, every weight gradient as g^T x, every stride-1
+    input gradient as the cropped padded-gradient correlation) change no
     share: the reference's digest under each variant."""
     from paper_2104_10949_b200 import engine as E
 

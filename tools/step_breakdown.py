@@ -3,6 +3,7 @@ serialised), grouped by C-ABI entry point: where a step's time goes.
 
 python tools/step_breakdown.py alexnet [--out gpurun_out/breakdown_alexnet.json]
 python tools/step_breakdown.py resnet50 64
+python tools/step_breakdown.py vgg16 32
 """
 import argparse
 import json
@@ -35,6 +36,16 @@ def main():
         st = TrainState(sess, M.alexnet_cifar(), M.TrainConfig(0.01, b, 8, seed=0))
         imgs, labels = bench._synthetic(b, 100)
         xb = st.deal_batch(M.fx_encode(imgs), M.fx_encode(one_hot(labels, 10)))
+        for _ in range(2):
+            st.step(*xb)
+        fn = lambda: st.step(*xb)  # noqa: E731
+    elif a.which == "vgg16":  # VGG-16-TI training step (bench.vgg16_ti's)
+        b = a.batch or 32
+        sess = M.TrioSession(seed=5)
+        trng = np.random.default_rng(5)
+        imgs, labels = trng.uniform(0, 1, (b, 3, 64, 64)), trng.integers(0, 200, b)
+        st = TrainState(sess, M.models.vgg16(), M.TrainConfig(0.01, b, 8, seed=5))
+        xb = st.deal_batch(M.fx_encode(imgs), M.fx_encode(one_hot(labels, 200)))
         for _ in range(2):
             st.step(*xb)
         fn = lambda: st.step(*xb)  # noqa: E731
