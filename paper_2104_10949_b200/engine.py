@@ -54,8 +54,16 @@ CS_PACKS = os.environ.get("MPC3_CS_PACKS", "1") == "1"
 # instead of transposed (rows = the contraction), see Packed.t
 T_PACKS = os.environ.get("MPC3_T_PACKS", "1") == "1"
 # weight gradients from a transposed x pack with at least this contraction
-# per half run as g^T x (x as B, see wgrad_packed)
-WGRAD_SWAP_MIN_KC = 4096
+# per half run as g^T x (x as B, see wgrad_packed) unless that orientation
+# fills the 128 x 64 tiles worse: its MN-major A reads are worth up to
+# WGRAD_SWAP_EDGE x the tile fill (VGG-16-TI conv1_2, O = 64: g^T x fills half
+# of each tile's rows, x^T g 90 %)
+WGRAD_SWAP_MIN_KC = int(os.environ.get("MPC3_WGRAD_SWAP_MIN_KC", "4096"))
+WGRAD_SWAP_EDGE = float(os.environ.get("MPC3_WGRAD_SWAP_EDGE", "1.15"))
+
+
+def _tile_fill(rows: int, cols: int) -> float:
+    return rows / (-(-rows // 128) * 128) * cols / (-(-cols // 64) * 64)
 # MPC3_MAXTREE_FUSED=0: one launch per max_tree level instead of one for the whole tree
 MAXTREE_FUSED = os.environ.get("MPC3_MAXTREE_FUSED", "1") == "1"
 # MPC3_LOSS_FUSED=0: the loss gradient softmax(z) - y as its separate launches
@@ -778,7 +786,7 @@ class TrioSession:
         z = torch.empty(3 * M * N, dtype=torch.int64, device=_dev())
         if xp.t and xp.kp < kc:
             raise ShapeError("transposed pack narrower than the contraction")
-        if xp.t and kc >= WGRAD_SWAP_MIN_KC:
+        if xp.t and kc >= WGRAD_SWAP_MIN_KC and _tile_fill(N, M) * WGRAD_SWAP_EDGE >= _tile_fill(M, N):
             # x packed transposed in the forward pass (its rows are (c, u, v)),
             # long contraction: computed as g^T x with g's pack as the MN-read A
             # and x's pack as a component-plane K-major B (b_mn = 2), row-major
