@@ -529,14 +529,16 @@ def run_b200(args, ws, rank, local):
         fixture, key = ("cfg_alexnet_b128.npz", "digest_1") if ws == 1 else ("cfg_alexnet_dp.npz", f"digest_dp{ws}")
         try:
             z = np.load(os.path.join(ROOT, "tests", "golden", fixture))
-            want = json.loads(bytes(z["meta"]).decode())[key]
+            fmeta = json.loads(bytes(z["meta"]).decode())
+            want = fmeta[key]
         except (OSError, KeyError, ValueError):
             parity["status"] = f"not checked (no fixture for global batch {b * ws})"
             return
         got = hashlib.sha256(b"".join(np.ascontiguousarray(sess.reveal(p), "<u8").tobytes()
                                       for p in st.params)).hexdigest()
+        source = fmeta.get(f"{key}_source", "the reference's train_private")
         parity.update({"status": "ok" if got == want else "MISMATCH", "digest": got[:16],
-                       "against": f"SHA-256 of the opened weights after step 1 vs the reference's train_private at "
+                       "against": f"SHA-256 of the opened weights after step 1 vs {source} at "
                                   f"global batch {b * ws} (tests/golden/{fixture}, make_golden_configs.py)"})
 
     # a CUDA-graph replay needs the previous replay's counters: eager warm-up

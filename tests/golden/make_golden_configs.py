@@ -258,7 +258,56 @@ def gen_maxpool():
     save("maxpool", arrays, meta)
 
 
-GEN = {"alexnet_b128": gen_alexnet_b128, "alexnet_dp": gen_alexnet_dp, "lenet_b64": gen_lenet_b64, "vgg16ti_b32": gen_vgg16ti_b32,
+def gen_alexnet_dp8():
+    """N = 8 (global batch 1024) is past the reference's 2^20 accumulation
+    bound, so its digest comes from the oracle's trio restatement of
+    train_private (oracle/nnmirror.py, exact integer arithmetic), after the
+    same restatement reproduces the reference's N = 2 digest; both are added
+    to cfg_alexnet_dp.npz (digest_dp8, digest_dp8_source)."""
+    sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
+    from oracle import nnmirror as N
+    from oracle import rss as R
+
+    z = np.load(OUT / "cfg_alexnet_dp.npz")
+    meta = json.loads(bytes(z["meta"]).decode())
+    layers, ishape = N.alexnet_cifar()
+    # past 2^20 terms the float-limb conv splits its contraction (the input
+    # channels, here the weight gradient's batch) into exact chunks whose
+    # results add mod 2^64: the exact ring value the reference would need
+    conv = R.ring_conv2d
+
+    def chunked_conv2d(x, k, stride=(1, 1), padding=(0, 0)):
+        c, kh, kw = k.shape[1:]
+        if c * kh * kw <= R.MAX_ACCUM:
+            return conv(x, k, stride, padding)
+        step = max(1, min(R.MAX_ACCUM // (kh * kw), 128))  # 128: bounded im2col memory
+        out = None
+        for c0 in range(0, c, step):
+            part = conv(x[:, c0:c0 + step], k[:, c0:c0 + step], stride, padding)
+            out = part if out is None else out + part
+        return out
+
+    R.ring_conv2d = chunked_conv2d
+    for ranks in (2, 8):
+        parts = [np.random.default_rng(100 + r) for r in range(ranks)]
+        data = [(g.uniform(0, 1, (128, 3, 32, 32)), g.integers(0, 10, 128)) for g in parts]
+        imgs = np.concatenate([d[0] for d in data])
+        labels = np.concatenate([d[1] for d in data])
+        t0 = time.time()
+        P, _ = N.train_private(R.Session(0), layers, ishape, imgs, labels, 0.01, 128 * ranks, 1, seed=0)
+        d = digest([R.open_trio(p) for p in P])
+        print(ranks, d, time.time() - t0, flush=True)
+        if ranks == 2:
+            assert d == meta["digest_dp2"], "the oracle restatement does not reproduce the reference at N = 2"
+        else:
+            meta["digest_dp8"] = d
+            meta["digest_dp8_source"] = ("oracle/nnmirror.train_private (the reference raises ExactnessError at "
+                                         "global batch 1024; the same restatement reproduces its N = 2 digest)")
+            meta["seconds_dp8_oracle"] = time.time() - t0
+    save("alexnet_dp", {}, meta)
+
+
+GEN = {"alexnet_b128": gen_alexnet_b128, "alexnet_dp": gen_alexnet_dp, "alexnet_dp8": gen_alexnet_dp8, "lenet_b64": gen_lenet_b64, "vgg16ti_b32": gen_vgg16ti_b32,
        "vgg16ti_train": gen_vgg16ti_train, "resnet50_b1": gen_resnet50_b1, "resnet50_b64": gen_resnet50_b64,
        "maxpool": gen_maxpool}
 

@@ -116,3 +116,41 @@ def test_dp_train_step_bit_exact(model_name, batch, world):
         for p, w in zip(out[r][1], w0):
             assert np.array_equal((p[0] + p[1] + p[2]).cpu().numpy().view(np.uint64), w)
         assert out[r][2] == s0.seq
+
+
+def test_dp8_alexnet_step_matches_pinned_digest():
+    """Eight virtual ranks of the data-parallel bench step (AlexNet-CIFAR, 128
+    images per rank, rank r's batch from default_rng(100 + r), as bench.py
+    under torchrun --nproc-per-node 8): the opened weights after one step
+    equal digest_dp8 of tests/golden/cfg_alexnet_dp.npz (the oracle's
+    train_private at global batch 1024, where the reference raises
+    ExactnessError; the same oracle reproduces the reference at N = 2)."""
+    import hashlib
+    import json
+    import os
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import bench
+
+    meta = json.loads(bytes(np.load(os.path.join(root, "tests", "golden", "cfg_alexnet_dp.npz"))["meta"]).decode())
+    if "digest_dp8" not in meta:
+        pytest.skip("no N = 8 digest in the fixture")
+    world = 8
+    ar = ThreadAllReduce(world)
+    out = [None] * world
+
+    def rank(r):
+        s = TrioSession(0)
+        s.dp = DataParallel(r, world, ar)
+        st = TrainState(s, M.alexnet_cifar(), M.TrainConfig(0.01, 128 * world, 1, seed=0))
+        imgs, labels = bench._synthetic(128, 100 + r)
+        st.step(*st.deal_batch(M.fx_encode(imgs), M.fx_encode(one_hot(labels, 10))))
+        torch.cuda.synchronize()
+        out[r] = [s.reveal(p) for p in st.params]
+
+    _run_threads([lambda r=r: rank(r) for r in range(world)], ar)
+    for r in range(world):
+        d = hashlib.sha256(b"".join(np.ascontiguousarray(w, "<u8").tobytes() for w in out[r])).hexdigest()
+        assert d == meta["digest_dp8"], r
