@@ -851,18 +851,28 @@ class InferenceGraph:
             self._frozen.__exit__(None, None, None)
         self.delta = {p: sess.seq[p] - self.seq0[p] for p in sess.seq}
         sess.seq = dict(self.seq0)
-        self._host = torch.zeros(8, dtype=torch.int64).pin_memory()
+        # ring of pinned counter buffers, an event guarding each against reuse
+        # (as GraphStep): replays queue back to back, no host-device sync
+        self._host = [torch.zeros(8, dtype=torch.int64).pin_memory() for _ in range(4)]
+        self._done = [None] * 4
+        self.replays = 0
 
     def replay(self) -> RssTensor:
         import torch
 
         S = self.sess
-        torch.cuda.current_stream().synchronize()  # the pinned counter buffer is reused
-        hv = self._host.numpy()
+        slot = self.replays % 4
+        if self._done[slot] is not None:
+            self._done[slot].synchronize()
+        hv = self._host[slot].numpy()
         for p in self.delta:
             hv[p] = S.seq[p] - self.seq0[p]
-        self.ctr.copy_(self._host, non_blocking=True)
+        self.ctr.copy_(self._host[slot], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._done[slot] = ev
         self.graph.replay()
+        self.replays += 1
         for p, d in self.delta.items():
             S.seq[p] += d
         S.ledger.apply(self.charge)
