@@ -817,15 +817,19 @@ class InferenceGraph:
     """Private inference of a fixed-shape batch captured as a CUDA graph.
 
     Same counter mechanism as GraphStep: each replay draws the PRF words the
-    next eager inference would.  `x` is the static input buffer."""
+    next eager inference would.  `x` is the static input buffer.  `forward`
+    (sess, model, params, x) -> logits replaces TrioNet.forward, e.g. a
+    TPNet's tensor-parallel pass whose NCCL all-gathers are captured too."""
 
-    def __init__(self, sess: TrioSession, model: ModelGraph, params: list, x: RssTensor):
+    def __init__(self, sess: TrioSession, model: ModelGraph, params: list, x: RssTensor, forward=None):
         import torch
 
+        if forward is None:
+            def forward(s, m, p, xx):
+                return TrioNet(s).forward(m, p, xx, record=False)[0]
         self.sess, self.x = sess, x
         self.seq0 = dict(sess.seq)
         self.ctr = sess.ctr = torch.zeros(8, dtype=torch.int64, device=x.data.device)
-        net = TrioNet(sess)
         self._frozen = sess.frozen_weights()
         self._frozen.__enter__()  # weights packed once (here, outside the graph) and reused by every replay
         try:
@@ -836,13 +840,13 @@ class InferenceGraph:
             # inference exactly (tests/test_gpu_configs.py)
             scratch = TrioSession(None, sess.fp)
             scratch.dp, scratch._wcache = sess.dp, sess._wcache
-            TrioNet(scratch).forward(model, params, x, record=False)
+            forward(scratch, model, params, x)
             torch.cuda.synchronize()
             self.seq0 = dict(sess.seq)
             self.graph = torch.cuda.CUDAGraph()
             try:
                 with sess.ledger.capture() as cap, torch.cuda.graph(self.graph):
-                    self.logits = net.forward(model, params, x, record=False)[0]
+                    self.logits = forward(sess, model, params, x)
             finally:
                 sess.ctr = None
             self.charge = cap.charge
