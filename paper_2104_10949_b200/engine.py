@@ -404,18 +404,22 @@ class TrioSession:
         return RssTensor(to_device(comps), self.fp)
 
     def share_device(self, x: torch.Tensor, rng: np.random.Generator, label: str = "share.input",
-                     owner: int = 0) -> RssTensor:
+                     owner: int = 0, out: RssTensor | None = None) -> RssTensor:
         """`share` for an input already on the device (int64 bit-cast ring
         values): the dealer's PCG64 draws are generated by the GPU, word for
         word the ones numpy would return, and the host Generator is advanced
-        past them (sharing.py:113-118)."""
+        past them (sharing.py:113-118).  `out`: a contiguous (3, *x.shape)
+        sharing to deal into (e.g. a captured graph's static input)."""
         st = rng.bit_generator.state
         if st.get("bit_generator") != "PCG64":
             raise ConfigError("device dealing reproduces numpy's PCG64 Generator only")
         s, inc = int(st["state"]["state"]), int(st["state"]["inc"])
         x = x.contiguous()
         n = x.numel()
-        out = empty(tuple(x.shape), self.fp)
+        if out is None:
+            out = empty(tuple(x.shape), self.fp)
+        elif out.shape != tuple(x.shape) or not out.data.is_contiguous():
+            raise ShapeError("out must be a contiguous sharing of the input's shape")
         m64 = (1 << 64) - 1
         K.call("mpc3_deal_pcg64", s >> 64, s & m64, inc >> 64, inc & m64, x.data_ptr(), out.data.data_ptr(), n,
                _stream())
