@@ -319,7 +319,8 @@ __global__ void __launch_bounds__(kSignThreads, 1) sign_kernel(const __grid_cons
 // depend on the data, so phase 1 computes them for P pairs with all 256
 // threads in parallel (one three-key block per (slot, pair) item, a warp per
 // 32 pairs of one slot) into shared memory, and phase 2 runs the circuit of
-// each pair (one thread per pair) replaying those words.  A pair's latency
+// each pair (three lanes per pair, Lane3 in protocol.cuh; one thread per pair
+// with -DMPC3_SIGN2_LANES=0) replaying those words.  A pair's latency
 // is then ~1/4 of its AES work instead of all 16 dependent AES groups, which
 // is what bounds the many small ReLU / max_tree launches of a training step;
 // at large n it is throughput-bound like sign_kernel.
@@ -456,7 +457,7 @@ __global__ void __launch_bounds__(F ? kSignThreads : kThreads, F ? 1 : 2)
 // The whole max_tree (protocols.py:356-380) in one launch.  Rows are
 // independent, so each CTA takes R rows (R even: the rows' level tensors then
 // start on AES-block boundaries) through every level, two-phase per level as
-// sign2_kernel (keystream slots, then one thread per pair runs the circuit),
+// sign2_kernel (keystream slots, then three lanes per pair run the circuit),
 // with __syncthreads between levels; the level outputs ping-pong through
 // global scratch.  Counters per level as the per-level launches.
 constexpr int MT_MAX_LEVELS = 16, MT_PMAX = 64;

@@ -619,14 +619,15 @@ HD void inject_pair(const T& tab, const uint32_t* rk3, StreamHead a0, StreamHead
 #if defined(__CUDACC__)
 // The two-phase kernels' circuit as a 3-lane SIMT program.  With the
 // keystream replayed from shared memory, a pair's circuit is a chain of
-// dependent integer steps; one thread per pair leaves 2 of 8 warps busy and
-// the phase latency-bound.  Here lane i of a group of three holds component
+// dependent integer steps; one thread per pair leaves 2 of 8 warps busy.
+// Here lane i of a group of three holds component
 // i of the pair's two elements: the AND / multiplication cross terms read
 // component i+1 from the next lane and the relabel (z_i -> party i+1) takes
 // component i-1 from the previous one (warp shuffles), the zero-share words
 // are read straight from the slot (lane i folds F(k_i) and F(k_{i-1})), so
 // the same circuit runs on three times the lanes with the same slot order
-// and results bit-for-bit.
+// and results bit-for-bit.  (Measured: no faster than one thread per pair —
+// the keystream phase bounds the kernel, profiles/r02_sign2_lanes.txt.)
 struct Lane3 {
   const Word2* w;  // keystream slots (pair p's slot s at w[(s * P + p) * 3 + key])
   int P, p;
