@@ -626,8 +626,9 @@ HD void inject_pair(const T& tab, const uint32_t* rk3, StreamHead a0, StreamHead
 // component i-1 from the previous one (warp shuffles), the zero-share words
 // are read straight from the slot (lane i folds F(k_i) and F(k_{i-1})), so
 // the same circuit runs on three times the lanes with the same slot order
-// and results bit-for-bit.  (Measured: no faster than one thread per pair —
-// the keystream phase bounds the kernel, profiles/r02_sign2_lanes.txt.)
+// and results bit-for-bit.  (Measured: barely faster than one thread per pair,
+// 32.3 vs 32.6 us at 49 K elements: the keystream phase bounds the kernel,
+// profiles/r02_sign2_lanes.txt.)
 struct Lane3 {
   const Word2* w;  // keystream slots (pair p's slot s at w[(s * P + p) * 3 + key])
   int P, p;
