@@ -707,11 +707,30 @@ DEV void chain_pairs(const SmemTables& tab, const uint32_t* rk, const uint64_t* 
   }
 }
 
+#ifdef MPC3_LOSS_TRACE
+// debug build only (tools/dbg/loss_trace.py): phase timestamps of CTA 0
+__device__ unsigned long long g_loss_trace[8];
+#define LOSS_TRACE(k)                                                                          \
+  do {                                                                                         \
+    __syncthreads();                                                                           \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                                                 \
+      unsigned long long t_;                                                                   \
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_));                                    \
+      g_loss_trace[k] = t_;                                                                    \
+    }                                                                                          \
+  } while (0)
+extern "C" int mpc3_dbg_loss_trace(unsigned long long* host8) {
+  return cudaMemcpyFromSymbol(host8, g_loss_trace, sizeof(g_loss_trace)) == cudaSuccess ? 0 : 1;
+}
+#else
+#define LOSS_TRACE(k)
+#endif
 __global__ void __launch_bounds__(kThreads, 1) softmax_loss_kernel(
     const __grid_constant__ KeySched ks, const uint64_t* __restrict__ ctr, const __grid_constant__ LossArgs la,
     const uint64_t* __restrict__ z, const uint64_t* __restrict__ y, uint64_t* scratch, uint64_t* __restrict__ out,
     uint64_t rows, uint64_t d, int R) {
   SignStreams& st = *reinterpret_cast<SignStreams*>(reinterpret_cast<AesSmem*>(mpc3_dsm)->extra);
+  LOSS_TRACE(0);
   auto tab = Proto<false>::init();
   Word2* slots = reinterpret_cast<Word2*>(mpc3_dsm + sizeof(AesSmem));
   const uint32_t* rk = &ks.rk[0][0];
@@ -727,6 +746,7 @@ __global__ void __launch_bounds__(kThreads, 1) softmax_loss_kernel(
   uint64_t* RR = T + 3 * rows;
   const uint64_t n = rows * d;
 
+  LOSS_TRACE(1);
   // 1. max_tree (protocols.py:356-380): level by level, as maxtree_kernel
   const uint64_t* in = z;
   uint64_t m = d;
@@ -781,6 +801,7 @@ __global__ void __launch_bounds__(kThreads, 1) softmax_loss_kernel(
     in = o;
     m = mo;
   }
+  LOSS_TRACE(2);
   // 2. x = z - max (a local op)
   for (uint64_t i = threadIdx.x; i < rn * d; i += blockDim.x) {
     const uint64_t f = r0 * d + i, row = f / d;
@@ -790,9 +811,11 @@ __global__ void __launch_bounds__(kThreads, 1) softmax_loss_kernel(
     store_trio(X, n, f, v);
   }
   __syncthreads();
+  LOSS_TRACE(3);
   // 3. e = exp_approx(x) over this CTA's pairs of the (rows, d) tensor
   const uint64_t plo = r0 * d / 2, phi = ((r0 + rn) * d + 1) / 2;
   chain_pairs(tab, rk, ctr, la.ep, la.ej[0], la.ej[1], la.ej[2], X, E, n, la.row_off * d / 2, plo, phi, slots);
+  LOSS_TRACE(4);
   // 4. s = sum_j e (a local op)
   for (uint64_t r = threadIdx.x; r < rn; r += blockDim.x) {
     Trio acc{{0, 0, 0}};
@@ -803,9 +826,11 @@ __global__ void __launch_bounds__(kThreads, 1) softmax_loss_kernel(
     store_trio(T, rows, r0 + r, acc);
   }
   __syncthreads();
+  LOSS_TRACE(5);
   // 5. 1/s (reciprocal's Newton chain) over this CTA's rows
   chain_pairs(tab, rk, ctr, la.rp, la.rj[0], la.rj[1], la.rj[2], T, RR, rows, la.row_off / 2, r0 / 2,
               (r0 + rn + 1) / 2, slots);
+  LOSS_TRACE(6);
   // 6. out = truncate(e * (1/s)) - y (mul_truncate, then the loss gradient's local sub)
   const StreamHead ha = resolve(sref(ARITH_ZERO, la.fj[0]), ctr), hrho = resolve(sref(TRUNC_RHO, la.fj[1]), ctr),
                    hr = resolve(sref(TRUNC_R, la.fj[2]), ctr);
@@ -826,6 +851,7 @@ __global__ void __launch_bounds__(kThreads, 1) softmax_loss_kernel(
       store_trio(out, n, f, v);
     }
   }
+  LOSS_TRACE(7);
 }
 
 // SGD on every parameter in one launch (nn.py:539-543, the reference's
