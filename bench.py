@@ -1066,16 +1066,20 @@ def resnet50_b1_tp(dev, steps: int = 5):
     tp = TensorParallel.from_process_group()
     net = TPNet(sess, tp)
     mode = "CUDA graph"
-    try:
-        g = InferenceGraph(sess, model, params, x, forward=lambda s, m, p, xx: TPNet(s, tp).forward_tp(m, p, xx))
-        run = g.replay
-    except Exception as e:  # noqa: BLE001 - a collective that refuses capture: time eager passes
-        print(f"[bench] TP graph capture failed ({e!r}); timing eager passes", file=sys.stderr)
-        torch.cuda.synchronize()
-        mode = "eager"
 
-        def run():
-            return net.forward_tp(model, params, x)
+    def run():
+        return net.forward_tp(model, params, x)
+
+    if torch.distributed.get_backend() == "nccl":  # gloo collectives synchronise with the host: no capture
+        try:
+            run = InferenceGraph(sess, model, params, x,
+                                 forward=lambda s, m, p, xx: TPNet(s, tp).forward_tp(m, p, xx)).replay
+        except Exception as e:  # noqa: BLE001 - a collective that refuses capture: time eager passes
+            print(f"[bench] TP graph capture failed ({e!r}); timing eager passes", file=sys.stderr)
+            torch.cuda.synchronize()
+            mode = "eager"
+    else:
+        mode = "eager"
     first = run().data.cpu().numpy().view(np.uint64)
     parity = _fixture_check("resnet50_b1", first)
     torch.cuda.synchronize()

@@ -640,24 +640,35 @@ struct LossArgs {
 constexpr int LOSS_SLOT_BYTES = 64 * 1024;
 
 // one chain program over pairs [lo, hi) of an n-element trio tensor x -> out
+// The chain's keystream item (mul k, pair p): the three ARITH words, then
+// TRUNC_RHO / TRUNC_R, at PRF block blk.
+DEV void chain_slot_fill(const SmemTables& tab, const uint32_t* rk, const uint64_t* ctr, uint64_t ja, uint64_t jrho,
+                         uint64_t jr, int k, uint64_t blk, Word2* dst) {
+  Word2 w[3];
+  prf_block3(tab, rk, resolve(sref(ARITH_ZERO, ja + k), ctr), blk, w);
+  dst[0] = w[0];
+  dst[1] = w[1];
+  dst[2] = w[2];
+  trunc_words(tab, rk, resolve(sref(TRUNC_RHO, jrho + k), ctr), resolve(sref(TRUNC_R, jr + k), ctr), blk, dst[3],
+              dst[4]);
+}
+
+// pre: the whole range's keystream already in shared memory ((k * (hi - lo)
+// + p) * CH_SLOT_WORDS, one chunk), else filled chunk by chunk into `slots`
 DEV void chain_pairs(const SmemTables& tab, const uint32_t* rk, const uint64_t* ctr, const ChainProgram& prog,
                      uint64_t ja, uint64_t jrho, uint64_t jr, const uint64_t* x, uint64_t* out, uint64_t n,
-                     uint64_t pb0, uint64_t lo, uint64_t hi, Word2* slots) {
+                     uint64_t pb0, uint64_t lo, uint64_t hi, Word2* slots, const Word2* pre = nullptr) {
   int P = 64;
   while (P > 1 && P * prog.nmul * CH_SLOT_WORDS * (int)sizeof(Word2) > LOSS_SLOT_BYTES) P >>= 1;
+  if (pre) {
+    P = (int)(hi - lo);
+    slots = const_cast<Word2*>(pre);
+  }
   for (uint64_t c0 = lo; c0 < hi; c0 += P) {
     const int Pc = (int)(hi - c0 < (uint64_t)P ? hi - c0 : (uint64_t)P);
-    for (int q = threadIdx.x; q < prog.nmul * Pc; q += blockDim.x) {
+    for (int q = threadIdx.x; q < (pre ? 0 : prog.nmul * Pc); q += blockDim.x) {
       const int k = q / Pc, p = q % Pc;
-      const uint64_t blk = pb0 + c0 + p;
-      Word2* dst = slots + ((size_t)k * Pc + p) * CH_SLOT_WORDS;
-      Word2 w[3];
-      prf_block3(tab, rk, resolve(sref(ARITH_ZERO, ja + k), ctr), blk, w);
-      dst[0] = w[0];
-      dst[1] = w[1];
-      dst[2] = w[2];
-      trunc_words(tab, rk, resolve(sref(TRUNC_RHO, jrho + k), ctr), resolve(sref(TRUNC_R, jr + k), ctr), blk, dst[3],
-                  dst[4]);
+      chain_slot_fill(tab, rk, ctr, ja, jrho, jr, k, pb0 + c0 + p, slots + ((size_t)k * Pc + p) * CH_SLOT_WORDS);
     }
     __syncthreads();
     const int p = threadIdx.x;
@@ -709,7 +720,7 @@ DEV void chain_pairs(const SmemTables& tab, const uint32_t* rk, const uint64_t* 
 
 #ifdef MPC3_LOSS_TRACE
 // debug build only (tools/dbg/loss_trace.py): phase timestamps of CTA 0
-__device__ unsigned long long g_loss_trace[8];
+__device__ unsigned long long g_loss_trace[16];
 #define LOSS_TRACE(k)                                                                          \
   do {                                                                                         \
     __syncthreads();                                                                           \
@@ -746,6 +757,83 @@ __global__ void __launch_bounds__(kThreads, 1) softmax_loss_kernel(
   uint64_t* RR = T + 3 * rows;
   const uint64_t n = rows * d;
 
+  // Small problems (AlexNet's 128 x 10): every phase's keystream — each
+  // max_tree level's slots, the exp and reciprocal chains', the final
+  // mul + truncate's — in ONE parallel fill up front (full AES rounds, no
+  // counter-mode constants), so the phases after it are circuits only: the
+  // per-phase fills were serial latency (profiles/r02_loss_phases.txt).
+  // Sized with R rows (every CTA takes the same decision); regions are laid
+  // out with this CTA's own pair counts.
+  const uint64_t plo = r0 * d / 2, phi = ((r0 + rn) * d + 1) / 2;
+  const uint64_t rlo = r0 / 2, rhi = (r0 + rn + 1) / 2;
+  bool prefill = MPC3_SIGN2_LANES && la.levels <= MT_MAX_LEVELS;
+  {
+    uint64_t words = 0, mm = d;
+    for (int l = 0; l < la.levels; ++l) {
+      const uint64_t kk = mm / 2;
+      words += (uint64_t)sign_slots((la.rows_total * kk) & 1) * (((uint64_t)R * kk + 1) / 2) * 3;
+      mm = kk + (mm & 1);
+    }
+    const uint64_t pe = ((uint64_t)R * d + 1) / 2 + 1, pr = (uint64_t)R / 2 + 1;
+    words += (uint64_t)(la.ep.nmul + 1) * pe * CH_SLOT_WORDS + (uint64_t)la.rp.nmul * pr * CH_SLOT_WORDS;
+    prefill = prefill && words * sizeof(Word2) + MT_MAX_LEVELS * sizeof(SignStreams) <= (uint64_t)LOSS_SLOT_BYTES;
+  }
+  Word2 *pre_l[MT_MAX_LEVELS], *pre_e = nullptr, *pre_r = nullptr, *pre_f = nullptr;
+  if (prefill) {
+    uint64_t cnt[MT_MAX_LEVELS + 3], kl[MT_MAX_LEVELS];
+    Word2* at = slots;
+    uint64_t mm = d;
+    for (int l = 0; l < la.levels; ++l) {
+      kl[l] = mm / 2;
+      const uint64_t Pl = (rn * kl[l] + 1) / 2;
+      cnt[l] = (uint64_t)sign_slots((la.rows_total * kl[l]) & 1) * Pl;
+      pre_l[l] = at;
+      at += cnt[l] * 3;
+      mm = kl[l] + (mm & 1);
+    }
+    const uint64_t Pe = phi - plo, Pr = rhi - rlo;
+    cnt[la.levels] = (uint64_t)la.ep.nmul * Pe;
+    pre_e = at;
+    at += cnt[la.levels] * CH_SLOT_WORDS;
+    cnt[la.levels + 1] = (uint64_t)la.rp.nmul * Pr;
+    pre_r = at;
+    at += cnt[la.levels + 1] * CH_SLOT_WORDS;
+    cnt[la.levels + 2] = Pe;
+    pre_f = at;
+    at += Pe * CH_SLOT_WORDS;
+    SignStreams* sts = reinterpret_cast<SignStreams*>(at);
+    if (threadIdx.x < (unsigned)la.levels) {
+      const SignArgs a = {la.jbin[threadIdx.x], la.jxor[threadIdx.x], la.ja[threadIdx.x], 0, 0, 0};
+      sign_streams(sts[threadIdx.x], a, ctr, false);
+    }
+    __syncthreads();
+    uint64_t total = 0;
+    for (int sg = 0; sg < la.levels + 3; ++sg) total += cnt[sg];
+    for (uint64_t q0 = threadIdx.x; q0 < total; q0 += blockDim.x) {
+      uint64_t q = q0;
+      int sg = 0;
+      while (q >= cnt[sg]) q -= cnt[sg++];
+      if (sg < la.levels) {  // a max_tree level's slot (s, p)
+        const uint64_t Pl = (rn * kl[sg] + 1) / 2, nt = la.rows_total * kl[sg];
+        const int sidx = (int)(q / Pl), pp = (int)(q % Pl);
+        sign_slot_fill(tab, rk, sts[sg], sidx, ((la.row_off * kl[sg]) >> 1) + r0 * kl[sg] / 2 + pp, nt,
+                       (nt & 1) ? 3 : 2, pre_l[sg] + ((size_t)sidx * Pl + pp) * 3);
+      } else if (sg == la.levels) {  // exp chain: mul k, pair p
+        const uint64_t Pe = phi - plo;
+        chain_slot_fill(tab, rk, ctr, la.ej[0], la.ej[1], la.ej[2], (int)(q / Pe),
+                        la.row_off * d / 2 + plo + q % Pe, pre_e + q * CH_SLOT_WORDS);
+      } else if (sg == la.levels + 1) {  // reciprocal chain
+        const uint64_t Pr = rhi - rlo;
+        chain_slot_fill(tab, rk, ctr, la.rj[0], la.rj[1], la.rj[2], (int)(q / Pr), la.row_off / 2 + rlo + q % Pr,
+                        pre_r + q * CH_SLOT_WORDS);
+      } else {  // the final mul + truncate of pair plo + q
+        chain_slot_fill(tab, rk, ctr, la.fj[0], la.fj[1], la.fj[2], 0, la.row_off * d / 2 + plo + q,
+                        pre_f + q * CH_SLOT_WORDS);
+      }
+    }
+    __syncthreads();
+  }
+
   LOSS_TRACE(1);
   // 1. max_tree (protocols.py:356-380): level by level, as maxtree_kernel
   const uint64_t* in = z;
@@ -753,12 +841,34 @@ __global__ void __launch_bounds__(kThreads, 1) softmax_loss_kernel(
   for (int l = 0; l < la.levels; ++l) {
     const uint64_t k = m / 2, mo = k + (m & 1);
     uint64_t* o = l == la.levels - 1 ? mx : ((l & 1) ? s1 : s0);
+    if (prefill) {  // slots filled up front: the circuit only
+      const uint64_t nl = rows * k, n_total = la.rows_total * k;
+      const int Pl = (int)((rn * k + 1) / 2);
+      const MaxGeom g = {rows, m, k};
+      const LaneGroup G = lane_group();
+      const int nw = blockDim.x >> 5;
+      for (int base = (threadIdx.x >> 5) * 10; base < Pl; base += nw * 10) {
+        const int pp = base + G.gi;
+        const bool live = G.gi < 10 && pp < Pl;
+        const Lane3 L = {pre_l[l], Pl, live ? pp : 0, G.ci, G.nl, G.pl};
+        maxlevel_item_lane(L, in, o, g, nl, n_total, r0 * k / 2 + L.p, live);
+      }
+      __syncthreads();
+      if (m & 1)
+        for (uint64_t r = threadIdx.x; r < rn; r += blockDim.x)
+          store_trio(o, rows * mo, (r0 + r) * mo + k, load_trio(in, rows * m, (r0 + r) * m + m - 1));
+      __syncthreads();
+      in = o;
+      m = mo;
+      continue;
+    }
     if (threadIdx.x == 0) {
       const SignArgs a = {la.jbin[l], la.jxor[l], la.ja[l], 0, 0, 0};
       sign_streams(st, a, ctr, false);
     }
     __syncthreads();
     cache_sign_streams(tab, &ks.rk[0][0], st, reinterpret_cast<AesSmem*>(mpc3_dsm)->hc, false);
+    if (l == 0) LOSS_TRACE(8);
     const uint64_t nl = rows * k, n_total = la.rows_total * k, elem_off = la.row_off * k;
     const bool straddle = (n_total & 1) != 0;
     const int L = straddle ? 3 : 2, used = sign_slots(straddle);
@@ -771,6 +881,7 @@ __global__ void __launch_bounds__(kThreads, 1) softmax_loss_kernel(
         sign_slot_fill(tab, rk, st, sidx, (elem_off >> 1) + p0 + c + p, n_total, L, slots + ((size_t)sidx * Pc + p) * 3);
       }
       __syncthreads();
+      if (l == 0 && c == 0) LOSS_TRACE(9);
 #if MPC3_SIGN2_LANES
       {
         const LaneGroup G = lane_group();
@@ -793,11 +904,13 @@ __global__ void __launch_bounds__(kThreads, 1) softmax_loss_kernel(
       }
 #endif
       __syncthreads();
+      if (l == 0 && c == 0) LOSS_TRACE(10);
     }
     if (m & 1)
       for (uint64_t r = threadIdx.x; r < rn; r += blockDim.x)
         store_trio(o, rows * mo, (r0 + r) * mo + k, load_trio(in, rows * m, (r0 + r) * m + m - 1));
     __syncthreads();
+    if (l == 0) LOSS_TRACE(11);
     in = o;
     m = mo;
   }
@@ -813,8 +926,7 @@ __global__ void __launch_bounds__(kThreads, 1) softmax_loss_kernel(
   __syncthreads();
   LOSS_TRACE(3);
   // 3. e = exp_approx(x) over this CTA's pairs of the (rows, d) tensor
-  const uint64_t plo = r0 * d / 2, phi = ((r0 + rn) * d + 1) / 2;
-  chain_pairs(tab, rk, ctr, la.ep, la.ej[0], la.ej[1], la.ej[2], X, E, n, la.row_off * d / 2, plo, phi, slots);
+  chain_pairs(tab, rk, ctr, la.ep, la.ej[0], la.ej[1], la.ej[2], X, E, n, la.row_off * d / 2, plo, phi, slots, pre_e);
   LOSS_TRACE(4);
   // 4. s = sum_j e (a local op)
   for (uint64_t r = threadIdx.x; r < rn; r += blockDim.x) {
@@ -828,8 +940,7 @@ __global__ void __launch_bounds__(kThreads, 1) softmax_loss_kernel(
   __syncthreads();
   LOSS_TRACE(5);
   // 5. 1/s (reciprocal's Newton chain) over this CTA's rows
-  chain_pairs(tab, rk, ctr, la.rp, la.rj[0], la.rj[1], la.rj[2], T, RR, rows, la.row_off / 2, r0 / 2,
-              (r0 + rn + 1) / 2, slots);
+  chain_pairs(tab, rk, ctr, la.rp, la.rj[0], la.rj[1], la.rj[2], T, RR, rows, la.row_off / 2, rlo, rhi, slots, pre_r);
   LOSS_TRACE(6);
   // 6. out = truncate(e * (1/s)) - y (mul_truncate, then the loss gradient's local sub)
   const StreamHead ha = resolve(sref(ARITH_ZERO, la.fj[0]), ctr), hrho = resolve(sref(TRUNC_RHO, la.fj[1]), ctr),
@@ -837,8 +948,17 @@ __global__ void __launch_bounds__(kThreads, 1) softmax_loss_kernel(
   for (uint64_t b = plo + threadIdx.x; b < phi; b += blockDim.x) {
     const uint64_t blk = la.row_off * d / 2 + b;
     Word2 w[3], rho, r;
-    prf_block3(tab, rk, ha, blk, w);
-    trunc_words(tab, rk, hrho, hr, blk, rho, r);
+    if (pre_f) {
+      const Word2* sl = pre_f + (b - plo) * CH_SLOT_WORDS;
+      w[0] = sl[0];
+      w[1] = sl[1];
+      w[2] = sl[2];
+      rho = sl[3];
+      r = sl[4];
+    } else {
+      prf_block3(tab, rk, ha, blk, w);
+      trunc_words(tab, rk, hrho, hr, blk, rho, r);
+    }
     for (int e = 0; e < 2; ++e) {
       const uint64_t f = 2 * b + e;
       if (f >= n || f >= (r0 + rn) * d) break;

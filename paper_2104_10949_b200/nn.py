@@ -622,6 +622,9 @@ class GraphStep:
             # charged on every replay (CommStats as the eager steps')
             with S.ledger.capture() as cap, torch.cuda.graph(self.graph):
                 self.logits = st.step(xs, ys)
+        except BaseException:
+            S.seq = dict(self.seq0)  # a refused capture consumes nothing (the caller may step eagerly)
+            raise
         finally:
             S.ctr = None  # the graph keeps the buffer's address; eager calls stay absolute
         self.charge = cap.charge
@@ -847,6 +850,9 @@ class InferenceGraph:
             try:
                 with sess.ledger.capture() as cap, torch.cuda.graph(self.graph):
                     self.logits = forward(sess, model, params, x)
+            except BaseException:
+                sess.seq = dict(self.seq0)  # a refused capture consumes nothing (the caller may run eagerly)
+                raise
             finally:
                 sess.ctr = None
             self.charge = cap.charge

@@ -21,11 +21,11 @@ s = TrioSession(1)
 zs, ys = s.from_components(z), s.from_components(y)
 phases = [None, "table set-up", "max_tree", "x = z - max", "exp chain", "row sum", "reciprocal",
           "mul + truncate - y"]
-acc = np.zeros(8)
+acc = np.zeros(16)
 for it in range(6):
     s.softmax_loss(zs, ys)
     torch.cuda.synchronize()
-    t = (C.c_ulonglong * 8)()
+    t = (C.c_ulonglong * 16)()
     assert _capi.lib().mpc3_dbg_loss_trace(t) == 0
     if it >= 1:
         acc += np.array(t[:], dtype=np.float64) - t[0]
@@ -33,3 +33,6 @@ acc /= 5
 for k in range(1, 8):
     print(f"{phases[k]:20s} {(acc[k] - acc[k - 1]) / 1e3:7.2f} us")
 print(f"{'total (CTA 0)':20s} {acc[7] / 1e3:7.2f} us")
+print("max_tree level 0:", ", ".join(f"{nm} {(acc[b] - acc[a]) / 1e3:.2f} us" for nm, a, b in
+                                 (("streams + head constants", 1, 8), ("keystream fill", 8, 9), ("circuit", 9, 10),
+                                  ("odd column", 10, 11))))
