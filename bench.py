@@ -1094,7 +1094,7 @@ def resnet50_b1_tp(dev, steps: int = 5):
     torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     ms = float(t.item())
     return {"workload": "ResNet-50 v1.5 private inference, batch 1, output channels sharded over all ranks "
-                        f"(NCCL all-gather per layer), {mode}",
+                        f"({torch.distributed.get_backend()} all-gather per layer), {mode}",
             "value": 1.0 / (ms / 1e3), "unit": "images/s", "latency_ms": ms, "steps": steps, "parity": parity}
 
 
