@@ -234,7 +234,8 @@ def test_dgrad_formulations_share_for_share(nb, o, oh, ow, c, kh, kw, ph):
 
 
 @pytest.mark.parametrize("rows,d,shard", [(128, 10, None), (7, 10, None), (32, 200, None), (3, 2, None),
-                                          (5, 3, None), (64, 37, (2, 4)), (1, 10, None)])
+                                          (5, 3, None), (64, 37, (2, 4)), (1, 10, None),
+                                          (64, 10, (1, 4)), (10, 10, (1, 2))])
 def test_fused_softmax_loss_equals_separate_launches_and_oracle(rows, d, shard):
     """mpc3_rss_softmax_loss (max_tree, exp, row sum, reciprocal, mul +
     truncate and the label sub in ONE launch) = softmax() then sub(): every
