@@ -644,13 +644,14 @@ constexpr int LOSS_SLOT_BYTES = 64 * 1024;
 // TRUNC_RHO / TRUNC_R, at PRF block blk.
 DEV void chain_slot_fill(const SmemTables& tab, const uint32_t* rk, const uint64_t* ctr, uint64_t ja, uint64_t jrho,
                          uint64_t jr, int k, uint64_t blk, Word2* dst) {
-  Word2 w[3];
-  prf_block3(tab, rk, resolve(sref(ARITH_ZERO, ja + k), ctr), blk, w);
+  Word2 w[3], rho, r;  // the five AES blocks interleaved in one call (one chain's latency)
+  reshare_trunc_words(tab, rk, resolve(sref(ARITH_ZERO, ja + k), ctr), resolve(sref(TRUNC_RHO, jrho + k), ctr),
+                      resolve(sref(TRUNC_R, jr + k), ctr), blk, w, rho, r);
   dst[0] = w[0];
   dst[1] = w[1];
   dst[2] = w[2];
-  trunc_words(tab, rk, resolve(sref(TRUNC_RHO, jrho + k), ctr), resolve(sref(TRUNC_R, jr + k), ctr), blk, dst[3],
-              dst[4]);
+  dst[3] = rho;
+  dst[4] = r;
 }
 
 // pre: the whole range's keystream already in shared memory ((k * (hi - lo)
@@ -809,10 +810,15 @@ __global__ void __launch_bounds__(kThreads, 1) softmax_loss_kernel(
     __syncthreads();
     uint64_t total = 0;
     for (int sg = 0; sg < la.levels + 3; ++sg) total += cnt[sg];
+    // item order: the chains' five-block items first, then the max_tree
+    // levels' slots (a partial last round then holds the cheaper items)
     for (uint64_t q0 = threadIdx.x; q0 < total; q0 += blockDim.x) {
       uint64_t q = q0;
-      int sg = 0;
-      while (q >= cnt[sg]) q -= cnt[sg++];
+      int sg = la.levels;
+      while (q >= cnt[sg]) {
+        q -= cnt[sg];
+        sg = sg == la.levels + 2 ? 0 : sg + 1;
+      }
       if (sg < la.levels) {  // a max_tree level's slot (s, p)
         const uint64_t Pl = (rn * kl[sg] + 1) / 2, nt = la.rows_total * kl[sg];
         const int sidx = (int)(q / Pl), pp = (int)(q % Pl);
