@@ -52,6 +52,9 @@ FUSE_RELU = os.environ.get("MPC3_FUSE_RELU", "1") == "1"
 # (two more keystream slots, smaller chunks) does not (AlexNet step: fused
 # everywhere 2.559 ms, from 100 K elements 2.530 ms, never 2.541 ms)
 FUSE_RELU_MIN = int(os.environ.get("MPC3_FUSE_RELU_MIN", "100000"))  # output elements
+# inference (no backward pass recorded) fuses at every size: ResNet-50 b1's
+# 25-50 K-element ReLUs 140.1 -> 141.4 img/s (profiles/README.md)
+FUSE_RELU_MIN_INFER = int(os.environ.get("MPC3_FUSE_RELU_MIN_INFER", "0"))
 # MPC3_FUSE_RESIDUAL=0: a residual block's last conv, shortcut add and ReLU as three launches
 FUSE_RESIDUAL = os.environ.get("MPC3_FUSE_RESIDUAL", "1") == "1"
 FUSE_RESIDUAL_MAX = 4 << 20  # block input elements
@@ -309,7 +312,7 @@ class TrioNet:
             # a conv / linear layer followed by a ReLU runs as one launch for
             # the layer's reshare + truncate and the ReLU (mpc3_rss_layer_sign)
             relu_next = FUSE_RELU and li + 1 < len(layers) and layers[li + 1].kind == RELU \
-                and self._out_numel(spec, h) >= FUSE_RELU_MIN
+                and self._out_numel(spec, h) >= (FUSE_RELU_MIN if record else FUSE_RELU_MIN_INFER)
             if spec.kind == RELU and fused is not None:
                 acts.append((fused,) if record else None)
                 fused = None
