@@ -280,6 +280,9 @@ class TrioSession:
         self._pack = None  # stream for the B-operand pack of a GEMM
         self._wcache = None  # packed weight operands under frozen_weights()
         self._prepacked = {}  # weight packs made ahead of their layer (prepack): key -> (Packed, event)
+        # False: the fused layer + ReLU launches skip the mask (an inference
+        # pass without a backward: TrioNet sets it per pass)
+        self.relu_masks = True
         self._replicated = 0
 
     # -- data parallelism --
@@ -976,13 +979,14 @@ class TrioSession:
     def relu_epilogue_end(self, pend: dict, residual: RssTensor | None = None):
         """Second half: the ReLU's counters, then ONE launch of the layer's
         reshare + truncate (+ bias) (+ the residual shortcut, a local add) and
-        the ReLU (mpc3_rss_layer_sign_residual).  -> (relu, mask)."""
+        the ReLU (mpc3_rss_layer_sign_residual).  -> (relu, mask); mask None
+        when relu_masks is off."""
         jb = self.take(BIN)
         jx = self.take(XOR, 7)
         jm = self.take(ARITH, 3)
         full, shape, bias, view = pend["full"], pend["shape"], pend["bias"], pend["view"]
         off, n_total = self.shard_offset(full)
-        out, mask = empty(shape, self.fp), empty(shape, self.fp)
+        out, mask = empty(shape, self.fp), (empty(shape, self.fp) if self.relu_masks else None)
         res = None
         if residual is not None:
             if tuple(residual.shape) != tuple(shape):
@@ -992,7 +996,7 @@ class TrioSession:
                pend["bits"], pend["z"].data_ptr(), C.byref(view), None if bias is None else bias.data.data_ptr(),
                0 if bias is None else bias.data.stride(0), pend["bias_dim"], None if res is None else res.data_ptr(),
                0 if res is None else res.stride(0), K.MODE_RELU, jb, jx, jm, out.data.data_ptr(),
-               mask.data.data_ptr(), off, n_total, _stream())
+               None if mask is None else mask.data.data_ptr(), off, n_total, _stream())
         self._charge_sign(full, K.MODE_RELU)
         return out, mask
 

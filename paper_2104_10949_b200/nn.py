@@ -303,6 +303,14 @@ class TrioNet:
         return 0
 
     def _run(self, layers, it, h: RssTensor, record: bool):
+        saved = self.s.relu_masks
+        self.s.relu_masks = record  # an inference pass keeps no ReLU masks
+        try:
+            return self._run_layers(layers, it, h, record)
+        finally:
+            self.s.relu_masks = saved
+
+    def _run_layers(self, layers, it, h: RssTensor, record: bool):
         S, acts = self.s, []
         fused = None  # mask of a ReLU already computed with the layer before it
         for li, spec in enumerate(layers):
@@ -324,6 +332,7 @@ class TrioNet:
                              relu=relu_next)
                 if relu_next:
                     h, fused = h
+                    fused = True if fused is None else fused  # no mask kept (inference)
                 acts.append(((x, k) + tuple(keep or ())) if record else None)
                 if self._ahead:
                     S.prepack([self._ahead.pop(0)])
@@ -334,6 +343,7 @@ class TrioNet:
                              keep=keep, x_role=1 if keep is not None else 0, relu=relu_next)
                 if relu_next:
                     h, fused = h
+                    fused = True if fused is None else fused  # no mask kept (inference)
                 acts.append(((x, w) + tuple(keep or ())) if record else None)
                 if self._ahead:
                     S.prepack([self._ahead.pop(0)])
@@ -367,6 +377,7 @@ class TrioNet:
                                     relu="defer")
                     hs = self._run(spec.shortcut, it, h, False)[0] if spec.shortcut else h
                     h, fused = S.relu_epilogue_end(pend, residual=hs)
+                    fused = True if fused is None else fused
                 else:
                     hm = self._run(spec.main, it, h, False)[0] if spec.main else h
                     hs = self._run(spec.shortcut, it, h, False)[0] if spec.shortcut else h
