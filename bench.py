@@ -69,11 +69,20 @@ def _dist():
     return ws, rank, local
 
 
+def _backend() -> str:
+    try:
+        import torch.distributed as dist
+
+        return dist.get_backend().upper() if dist.is_initialized() else "NCCL"
+    except Exception:  # noqa: BLE001 - labelling only
+        return "NCCL"
+
+
 def _config(args, ws):
     return {"workload": "AlexNet-CIFAR private training step (3-party RSS, Z_2^64, t=20)",
             "model": "alexnet_cifar", "global_batch": args.batch * ws, "per_gpu_batch": args.batch,
             "input": "3x32x32", "classes": 10,
-            "parallelism": (f"dp{ws} (batch shards, NCCL all-reduce of weight-gradient cross terms)"
+            "parallelism": (f"dp{ws} (batch shards, {_backend()} all-reduce of weight-gradient cross terms)"
                             if ws > 1 else "single"),
             "l2": "flushed (256 MiB write) before every timed step, outside its events",
             "inputs": "each step's dealt batch resident in HBM, staged into the graph's static input buffers "
